@@ -1,0 +1,48 @@
+"""The BASELINE.json configurations as plain parameter records (no method arithmetic).
+
+Grid convention: the box faces [lo, hi]^3 are the Dirichlet
+(ghost) nodes; ``n`` is the number of unknowns per axis; h = (hi-lo)/(n+1).
+"""
+from dataclasses import dataclass, field
+from typing import Optional, Tuple
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    n: int                       # unknowns per axis (R2)
+    lo: float                    # box = [lo, hi]^3 (R1, R3)
+    hi: float
+    kind: str                    # "sphere" | "ellipsoid"
+    center: Tuple[float, float, float]
+    semi: Tuple[float, float, float]   # sphere: (r, r, r)
+    lmax: int                    # spherical-harmonic degree L
+    basis: str                   # "cauchy" {Y, d*Y} | "neumann0" {Y, d^2/2*Y}  (R9)
+    dt: float                    # AP dt (cfg1, cfg4) or the PKS dt cap (cfg2, cfg3, cfg5)
+    steps: int = 0               # PKS steps (0 = not a PKS config)
+    batch: int = 0               # number of RHS in the throughput config
+    # PKS initial conditions rho0 = A_rho exp(-a_rho |x - ic_center|^2), c0 = A_c exp(-a_c |x - ic_center|^2)
+    ic_center: Tuple[float, float, float] = (0.0, 0.0, 0.0)
+    ic_rho: Tuple[float, float] = (1000.0, 100.0)
+    ic_c: Tuple[float, float] = (500.0, 50.0)
+    chi: float = 1.0             # R27: alpha = gamma_rho = gamma_c = chi = 1
+
+    @property
+    def K(self) -> int:
+        return 2 * (self.lmax + 1) ** 2
+
+
+CONFIGS = {
+    "cfg1": Config("cfg1", 16, -1.1, 1.1, "sphere", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 4, "cauchy", 1e-3,
+                   batch=51),
+    "cfg2": Config("cfg2", 32, -1.1, 1.1, "sphere", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 6, "neumann0", 1e-4,
+                   steps=10),
+    "cfg3": Config("cfg3", 64, -1.0, 1.0, "ellipsoid", (0.0, 0.0, 0.0), (0.9, 0.6, 0.5), 10, "neumann0", 2e-5,
+                   steps=100, ic_center=(0.2, 0.0, 0.0)),
+    "cfg4": Config("cfg4", 128, -1.1, 1.1, "sphere", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 16, "cauchy", 1e-5,
+                   batch=578),
+}
+
+
+def get_config(name: str) -> Config:
+    return CONFIGS[name]

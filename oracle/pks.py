@@ -1,0 +1,185 @@
+"""PKS time stepping — oracle (test infrastructure only).
+
+Transcribes, cell by cell, the hybrid finite-volume / finite-difference IMEX scheme
+ and the algorithm outline Steps 1-8, with the readings of
+SURVEY.md §8(c) R13-R20 (listed in DESIGN.md):
+
+* face gradient of c: (c_{j+1} - c_j)/h (`eqn:c-central-difference`);
+* minmod (`eqn:slope_limiter`) of (2Δ+/h, Δ0/(2h), 2Δ-/h);
+  R15: the slope of a cell is 0 along an axis unless both neighbours are in N+;
+* upwind face value: left reconstruction if ∇c > 0, else the right one (R16);
+* g = Σ_axes (χ ρ_{+½} ∇c_{+½} - χ ρ_{-½} ∇c_{-½})/h;
+* f_ρ = ρ̄ - dt g,  f_c = (1 - dt) c + dt ρ̄ on M+ (P:89-96);
+* CFL (`eqn:cfl_condition`) over faces with an endpoint in M+ (R19);
+* dt_i = min(dt_{i-1}, dt_cap, CFL, 0.5 h^2) (Step 3 P:427 + R13), BEP rebuilt iff
+  dt strictly decreases (Step 4b P:431);
+* Steps 4a-7: particular solves, reduced BEP by least squares, u_γ = E C clamped at 0
+  (R17), one combined Green's-formula solve restricted to N+ (R20);
+* mass = h^3 Σ_{M+} ρ̄ (R18).
+State: ρ̄ and c as [n][n][n] arrays holding values on N+ ∩ M0 (0 elsewhere); ghost
+nodes of N+ hold 0 (Dirichlet AP, R5).
+"""
+import numpy as np
+
+from . import ap, dpm, grid
+
+
+def minmod(*xs):
+    """minmod(x_1..x_M): min if all > 0, max if all < 0, else 0 (elementwise)."""
+    X = np.stack(np.broadcast_arrays(*[np.asarray(x, dtype=np.float64) for x in xs]))
+    return np.where((X > 0).all(axis=0), X.min(axis=0), np.where((X < 0).all(axis=0), X.max(axis=0), 0.0))
+
+
+def _pad(u):
+    n = u.shape[-1]
+    p = np.zeros((n + 2,) * 3)
+    p[1:-1, 1:-1, 1:-1] = u
+    return p
+
+
+def _shift(p, ax, s):
+    """Value at lattice index + s along axis ax (out-of-lattice -> 0 / False)."""
+    out = np.zeros_like(p)
+    src = [slice(None)] * 3
+    dst = [slice(None)] * 3
+    if s == 1:
+        src[ax] = slice(1, None)
+        dst[ax] = slice(0, -1)
+    else:
+        src[ax] = slice(0, -1)
+        dst[ax] = slice(1, None)
+    out[tuple(dst)] = p[tuple(src)]
+    return out
+
+
+def limited_slopes(rho_lat: np.ndarray, nplus_lat: np.ndarray, h: float):
+    """Per-axis minmod slopes on the (n+2)^3 lattice (R15)."""
+    sl = []
+    for ax in range(3):
+        rp, rm = _shift(rho_lat, ax, 1), _shift(rho_lat, ax, -1)
+        okp, okm = _shift(nplus_lat, ax, 1), _shift(nplus_lat, ax, -1)
+        s = minmod(2.0 * (rp - rho_lat) / h, (rp - rm) / (2.0 * h), 2.0 * (rho_lat - rm) / h)
+        sl.append(np.where(okp & okm & nplus_lat, s, 0.0))
+    return sl
+
+
+def convection(rho: np.ndarray, c: np.ndarray, ps: grid.PointSets, h: float, chi: float) -> np.ndarray:
+    """g on M+ (P:98-119), as an [n][n][n] array (0 off M+)."""
+    R = _pad(rho)
+    Cl = _pad(c)
+    npl = ps.nplus_lat
+    S = limited_slopes(R, npl, h)
+    g = np.zeros_like(R)
+    for ax in range(3):
+        Rp, Rm = _shift(R, ax, 1), _shift(R, ax, -1)
+        Sp, Sm = _shift(S[ax], ax, 1), _shift(S[ax], ax, -1)
+        Cp, Cm = _shift(Cl, ax, 1), _shift(Cl, ax, -1)
+        gE = (Cp - Cl) / h
+        gW = (Cl - Cm) / h
+        rhoE = np.where(gE > 0, R + 0.5 * h * S[ax], Rp - 0.5 * h * Sp)
+        rhoW = np.where(gW > 0, Rm + 0.5 * h * Sm, R - 0.5 * h * S[ax])
+        g += (chi * rhoE * gE - chi * rhoW * gW) / h
+    g = g[1:-1, 1:-1, 1:-1]
+    return np.where(ps.mplus, g, 0.0)
+
+
+def assemble_rhs(rho, c, g, dt):
+    """f_ρ = ρ̄ - dt g, f_c = (1 - dt) c + dt ρ̄."""
+    return rho - dt * g, (1.0 - dt) * c + dt * rho
+
+
+def cfl_dt(c: np.ndarray, ps: grid.PointSets, h: float, chi: float) -> float:
+    """min over axes of h/(6 χ max|∇c|) over faces of M+ cells (R19); inf if flat."""
+    Cl = _pad(c)
+    mp = np.zeros_like(ps.nplus_lat)
+    mp[1:-1, 1:-1, 1:-1] = ps.mplus
+    best = np.inf
+    for ax in range(3):
+        gE = np.abs(_shift(Cl, ax, 1) - Cl) / h
+        gW = np.abs(Cl - _shift(Cl, ax, -1)) / h
+        mx = max(gE[mp].max(initial=0.0), gW[mp].max(initial=0.0))
+        if mx > 0:
+            best = min(best, h / (6.0 * chi * mx))
+    return best
+
+
+class PKSOracle:
+    """Steps 1-8 for one single-domain configuration."""
+
+    def __init__(self, cfg, dt_rule: int = 0, clamp: bool = True):
+        self.cfg = cfg
+        self.g, self.ps = grid.point_sets_for(cfg)
+        self.E, self.d, self.unit, self.foot = dpm.extension_matrix(
+            self.g, self.ps, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.basis)
+        self.gin_pos = np.searchsorted(self.ps.list("gamma"), self.ps.list("gamma_in"))
+        self.dt_rule = dt_rule
+        self.clamp = clamp
+        self.dt_prev = np.inf
+        self.dt_bep = None
+        self.B = None
+        self.builds = 0
+        self.t = 0.0
+
+    def initial_state(self):
+        """R14: IC at the node on M+ \\ γ, at the foot point on γ; 0 elsewhere."""
+        cfg, g, ps = self.cfg, self.g, self.ps
+        n = g.n
+        x = g.coords()
+        X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+        c0 = np.asarray(cfg.ic_center)
+
+        def ic(A, a, XX, YY, ZZ):
+            return A * np.exp(-a * ((XX - c0[0]) ** 2 + (YY - c0[1]) ** 2 + (ZZ - c0[2]) ** 2))
+
+        rho = np.where(ps.nplus, ic(*cfg.ic_rho, X, Y, Z), 0.0)
+        c = np.where(ps.nplus, ic(*cfg.ic_c, X, Y, Z), 0.0)
+        gidx = ps.list("gamma")
+        F = self.foot
+        rho.reshape(-1)[gidx] = ic(*cfg.ic_rho, F[:, 0], F[:, 1], F[:, 2])
+        c.reshape(-1)[gidx] = ic(*cfg.ic_c, F[:, 0], F[:, 1], F[:, 2])
+        return rho, c
+
+    def build(self, dt):
+        _, self.B, _ = dpm.projection_and_bep(self.E, self.g, self.ps, dt)
+        self.dt_bep = dt
+        self.builds += 1
+
+    def step(self, rho, c):
+        cfg, g, ps, h = self.cfg, self.g, self.ps, self.g.h
+        if self.dt_rule == 0:
+            dt = min(self.dt_prev, cfg.dt, cfl_dt(c, ps, h, cfg.chi), 0.5 * h * h)   # Step 3 + R13
+        else:
+            dt = cfg.dt
+        rebuilt = False
+        if self.B is None or dt != self.dt_bep:                                     # Step 2 / 4b
+            self.build(dt)
+            rebuilt = True
+        gconv = convection(rho, c, ps, h, cfg.chi)
+        f_rho, f_c = assemble_rhs(rho, c, gconv, dt)                                # Step 4a
+        out = []
+        us = []
+        for f in (f_rho, f_c):
+            up = ap.solve(dpm.particular_rhs(f, ps, dt), h, dt)                      # G f
+            rhs = up.reshape(-1)[ps.list("gamma_in")]
+            C = dpm.lstsq(self.B, rhs)                                              # Step 5
+            u_gamma = self.E @ C
+            if self.clamp:
+                u_gamma = np.maximum(u_gamma, 0.0)                                  # R17
+            out.append(dpm.green(u_gamma, f, g, ps, dt))                            # Steps 6-7 (R20)
+            us.append(u_gamma)
+        self.dt_prev = dt
+        self.t += dt
+        return out[0], out[1], dict(dt=dt, rebuilt=rebuilt, t=self.t)
+
+    def mass(self, rho):
+        h = self.g.h
+        return h ** 3 * rho[self.ps.mplus].sum()                                    # R18
+
+    def run(self, nsteps=None):
+        rho, c = self.initial_state()
+        logs = []
+        for _ in range(nsteps if nsteps is not None else self.cfg.steps):
+            rho, c, log = self.step(rho, c)
+            log["mass"] = self.mass(rho)
+            logs.append(log)
+        return rho, c, logs

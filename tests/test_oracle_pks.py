@@ -1,0 +1,100 @@
+"""Pins for oracle/pks.py: the FV/IMEX scheme, CFL, Steps 3-7."""
+import numpy as np
+import pytest
+
+from dpm_inputs import get_config
+from dpm_inputs.rng import uniform_values
+from oracle import grid, pks
+
+
+def test_minmod_examples():
+    # SPEC S:197-199
+    assert pks.minmod(2.0, 1.5, 1.0) == 1.0
+    assert pks.minmod(-2.0, 1.0, 3.0) == 0.0
+    assert pks.minmod(-1.0, -2.0, -3.0) == -1.0
+
+
+@pytest.fixture(scope="module")
+def cfg2_sets():
+    return grid.point_sets_for(get_config("cfg2"))
+
+
+def test_slopes_linear_and_spike(cfg2_sets):
+    g, ps = cfg2_sets
+    n, h = g.n, g.h
+    x = g.coords()
+    X = np.broadcast_to(x[:, None, None], (n, n, n))
+    R = np.zeros((n + 2,) * 3)
+    R[1:-1, 1:-1, 1:-1] = np.where(ps.nplus, X, 0.0)
+    S = pks.limited_slopes(R, ps.nplus_lat, h)
+    mp = np.zeros_like(ps.nplus_lat)
+    mp[1:-1, 1:-1, 1:-1] = ps.mplus
+    interior = mp & np.roll(mp, 1, 0) & np.roll(mp, -1, 0)
+    assert np.allclose(S[0][interior], 1.0, rtol=1e-12)       # linear exactness
+    assert np.all(S[1][interior] == 0) and np.all(S[2][interior] == 0)
+    # spike -> slope 0 at the spike
+    R2 = np.zeros_like(R)
+    c = n // 2 + 1
+    R2[c, c, c] = 1.0
+    S2 = pks.limited_slopes(R2, ps.nplus_lat, h)
+    assert all(s[c, c, c] == 0 for s in S2)
+
+
+def test_convection_quadratic_exact(cfg2_sets):
+    # ρ̄ ≡ ρ0, c = x^2 -> g = 2 χ ρ0 on every M+ cell
+    g, ps = cfg2_sets
+    n = g.n
+    x = g.coords()
+    c = np.where(ps.nplus, np.broadcast_to(x[:, None, None] ** 2, (n, n, n)), 0.0)
+    rho = np.where(ps.nplus, 3.0, 0.0)
+    gconv = pks.convection(rho, c, ps, g.h, 1.0)
+    assert np.abs(gconv[ps.mplus] - 6.0).max() < 1e-9
+    # c constant -> g ≡ 0 exactly
+    assert np.all(pks.convection(rho, np.where(ps.nplus, 5.0, 0.0), ps, g.h, 1.0) == 0.0)
+
+
+def test_assemble_rhs_and_cfl(cfg2_sets):
+    # SPEC S:224-226 and S:233-235
+    fr, fc = pks.assemble_rhs(np.array(2.0), np.array(4.0), np.array(1.0), 0.5)
+    assert fr == 1.5 and fc == 3.0
+    g, ps = cfg2_sets
+    n = g.n
+    x = g.coords()
+    c = np.where(ps.nplus, np.broadcast_to(5.0 * x[:, None, None], (n, n, n)), 0.0)
+    assert abs(pks.cfl_dt(c, ps, g.h, 1.0) - g.h / 30.0) < 1e-15
+    assert pks.cfl_dt(np.where(ps.nplus, 1.0, 0.0), ps, g.h, 1.0) == np.inf
+
+
+def test_conservation_identity_and_positivity(cfg2_sets):
+    # ρ̄ = mean of the six one-sided face values; Thm 3 flux split: f_ρ >= 0 under CFL
+    g, ps = cfg2_sets
+    n, h = g.n, g.h
+    rho = np.where(ps.nplus, np.abs(uniform_values(21, (n, n, n))), 0.0)
+    c = np.where(ps.nplus, np.abs(uniform_values(22, (n, n, n))), 0.0)
+    R = np.zeros((n + 2,) * 3)
+    R[1:-1, 1:-1, 1:-1] = rho
+    S = pks.limited_slopes(R, ps.nplus_lat, h)
+    faces = sum((R + 0.5 * h * s) + (R - 0.5 * h * s) for s in S) / 6.0
+    assert np.abs(faces - R).max() < 1e-15
+    for s in S:   # limited reconstruction is non-negative
+        assert (R + 0.5 * h * s).min() >= -1e-15 and (R - 0.5 * h * s).min() >= -1e-15
+    dt = pks.cfl_dt(c, ps, h, 1.0)
+    fr, _ = pks.assemble_rhs(rho, c, pks.convection(rho, c, ps, h, 1.0), dt)
+    assert fr[ps.mplus].min() >= -1e-12
+
+
+@pytest.mark.slow
+def test_cfg2_run_survey_probe_values():
+    # SURVEY probe P11 (independent probe of readings R13-R20, cfg2, 10 steps):
+    # dt = 4.6352e-6 every step, 1 BEP build, max ρ 2.125875e3, mass drift -4.3e-15.
+    o = pks.PKSOracle(get_config("cfg2"))
+    rho0, c0 = o.initial_state()
+    m0 = o.mass(rho0)
+    rho, c, logs = o.run()
+    assert o.builds == 1
+    assert all(abs(l["dt"] / 4.6352e-6 - 1) < 1e-4 for l in logs)
+    assert abs(rho.max() / 2.125875e3 - 1) < 1e-6
+    assert abs(logs[-1]["mass"] - m0) < 1e-12 * m0
+    assert abs(m0 / 5.5683279893 - 1) < 1e-9
+    # positivity (Thm 3) up to round-off
+    assert rho.min() > -1e-9 * rho.max() and c.min() > -1e-9 * c.max()

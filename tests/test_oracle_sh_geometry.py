@@ -1,0 +1,89 @@
+"""Pins for oracle/sh.py (real SH, R8) and oracle/geometry.py (feet, d, angles; R10)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.special
+
+from dpm_inputs import get_config
+from oracle import dpm, geometry, grid, sh
+
+
+def test_y00():
+    u = np.array([[0.0, 0.0, 1.0], [1.0, 0.0, 0.0], [0.6, 0.0, 0.8]])
+    assert np.allclose(sh.real_sh(0, u)[:, 0], 1 / math.sqrt(4 * math.pi), rtol=1e-15)
+
+
+@pytest.mark.parametrize("lmax", [4, 10, 16])
+def test_orthonormality_quadrature(lmax):
+    # Gauss-Legendre in cos θ (exact to degree 2*nq-1) x uniform trapezoid in φ (exact for
+    # trigonometric degree < nphi): exact for products of degree <= 2L -> Gram = I.
+    nq = lmax + 1
+    x, w = np.polynomial.legendre.leggauss(nq)
+    nphi = 2 * lmax + 2
+    phi = 2 * np.pi * np.arange(nphi) / nphi
+    X, P = np.meshgrid(x, phi, indexing="ij")
+    W = (w[:, None] * np.full(nphi, 2 * np.pi / nphi)[None, :]).ravel()
+    s = np.sqrt(1 - X ** 2)
+    U = np.stack([(s * np.cos(P)).ravel(), (s * np.sin(P)).ravel(), X.ravel()], axis=1)
+    Y = sh.real_sh(lmax, U)
+    G = (Y * W[:, None]).T @ Y
+    assert np.abs(G - np.eye(G.shape[0])).max() < 1e-12
+
+
+def test_scipy_cross_check():
+    # SciPy's complex Y_l^m includes the Condon-Shortley phase (-1)^m (R8)
+    rng = np.random.default_rng(5)
+    v = rng.normal(size=(50, 3))
+    u = v / np.linalg.norm(v, axis=1)[:, None]
+    L = 8
+    Y = sh.real_sh(L, u)
+    theta = np.arccos(u[:, 2])
+    phi = np.arctan2(u[:, 1], u[:, 0])
+    for l in range(L + 1):
+        for m in range(-l, l + 1):
+            Z = scipy.special.sph_harm_y(l, abs(m), theta, phi)
+            if m == 0:
+                ref = Z.real
+            elif m > 0:
+                ref = math.sqrt(2) * (-1) ** m * Z.real
+            else:
+                ref = math.sqrt(2) * (-1) ** m * Z.imag
+            assert np.abs(Y[:, l * l + l + m] - ref).max() < 1e-12
+
+
+def test_sphere_closed_forms():
+    # SPEC S:76-78 examples (r = 0.5 at the origin)
+    P = np.array([[0.3, 0.0, 0.0], [0.0, 0.0, 0.6], [0.4, 0.4, 0.4]])
+    foot, d, unit = geometry.sphere_geometry(P, (0, 0, 0), 0.5)
+    assert np.allclose(foot[0], [0.5, 0, 0]) and abs(d[0] + 0.2) < 1e-15
+    assert np.allclose(foot[1], [0, 0, 0.5]) and abs(d[1] - 0.1) < 1e-15
+    assert abs(np.arccos(unit[1, 2])) < 1e-15
+    assert abs(d[2] - (0.4 * math.sqrt(3) - 0.5)) < 1e-15
+
+
+def test_ellipsoid_equals_sphere_when_round():
+    rng = np.random.default_rng(0)
+    P = rng.uniform(-1, 1, size=(20, 3))
+    f1, d1, u1 = geometry.sphere_geometry(P, (0, 0, 0), 0.7)
+    f2, d2, u2 = geometry.ellipsoid_geometry(P, (0, 0, 0), (0.7, 0.7, 0.7))
+    assert np.abs(f1 - f2).max() < 1e-14 and np.abs(d1 - d2).max() < 1e-14 and np.abs(u1 - u2).max() < 1e-14
+
+
+def test_ellipsoid_cfg3_geometry():
+    cfg = get_config("cfg3")
+    g, ps = grid.point_sets_for(cfg)
+    P = dpm.gamma_points(g, ps)
+    foot, d, unit = geometry.ellipsoid_geometry(P, cfg.center, cfg.semi)
+    s = np.asarray(cfg.semi)
+    # foot on Γ
+    assert np.abs(((foot / s) ** 2).sum(axis=1) - 1).max() < 1e-14
+    # p - foot parallel to the normal grad(Σ x^2/s^2) at the foot, |p - foot| = |d|
+    nrm = foot / s ** 2
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    assert np.abs(np.cross(P - foot, nrm)).max() < 1e-14
+    assert np.abs(P - (foot + d[:, None] * nrm)).max() < 1e-14
+    # sign(d) < 0 exactly on gamma_in (R10), |d| < 2h
+    gin = ps.gamma_in.ravel()[ps.list("gamma")]
+    assert np.array_equal(d < 0, gin)
+    assert np.abs(d).max() < 2 * g.h
