@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the B200-native DPM hot path.
+
+Metric (BASELINE.json): "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction);
+PKS time steps/sec".  The headline `value` is config 4: batched N=128 fp64 auxiliary
+solves (I/dt - Δ_h)u = q, dt = 1e-5, 578 RHS of seeded U(-1,1) values on the spherical
+shell band around r = 1 (R21), scattered into dense boxes; inputs resident in HBM.
+One "step" = one dpm_aux_solve_batch call over this rank's shard of the 578 RHS
+(sharded by RHS across ranks, no data-path collective: "scaling": "weak" in the sense
+that ranks solve disjoint shards of the fixed 578-RHS workload — see DESIGN.md).
+PKS steps/s for configs 2 and 3 are reported in the "pks" object (rank 0, N=1 only).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from dpm_inputs import get_config  # noqa: E402
+from dpm_inputs.rng import cfg4_band_values  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 37.06     # measured DMMA.8x8x4 peak on this pool's B200 (tools/microbench_fp64.cu, gpurun_out/microbench.log)
+
+
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_FILE)), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def oracle_sample_rate(cfg, nsolves, vals, band):
+    """Oracle AP solves (direct-summation DST, numpy fp64) on host cores: solves/s."""
+    from oracle import ap, dpm
+    g_h = (cfg.hi - cfg.lo) / (cfg.n + 1)
+    t0 = time.perf_counter()
+    for b in range(nsolves):
+        q = dpm.scatter(vals[b % len(vals)], band, cfg.n)
+        ap.solve(q, g_h, cfg.dt)
+    dt = time.perf_counter() - t0
+    return nsolves / dt, dt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    cfg = get_config("cfg4")
+    from oracle import grid
+    _, ps = grid.point_sets_for(cfg)
+    band = ps.list("band")
+    vals = cfg4_band_values(cfg.batch, len(band))
+    per_step = 2
+    for _ in range(args.warmup):
+        oracle_sample_rate(cfg, 1, vals, band)
+    times = []
+    for _ in range(args.steps):
+        _, t = oracle_sample_rate(cfg, per_step, vals, band)
+        times.append(t)
+    tot = sum(times)
+    value = per_step * args.steps / tot
+    line = {"impl": "reference", "metric": "fp64 auxiliary solves/sec at N=128", "value": value, "unit": "solves/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg4: N=128 box [-1.1,1.1]^3, dt=1e-5, 578 RHS U(-1,1) on the r=1 shell band",
+                       "global_batch": cfg.batch, "n": cfg.n, "parallelism": "rhs-shard"},
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": host_cores(), "kind": "oracle",
+                             "sample": f"{per_step} of the 578 cfg4 RHS per step (direct-summation DST, numpy)"},
+            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def bench_pks(api, torch, name, reps=3):
+    cfg = get_config(name)
+    ctx = api.DPM.from_config(cfg)
+    n = cfg.n
+    rho = torch.zeros((n, n, n), dtype=torch.float64, device="cuda")
+    c = torch.zeros_like(rho)
+    t0 = time.perf_counter()
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    ctx.pks_step(rho, c, 1, chi=cfg.chi, dt_cap=cfg.dt)      # builds the BEP at dt_0
+    torch.cuda.synchronize()
+    setup_ms = 1e3 * (time.perf_counter() - t0)
+    per = []
+    for _ in range(reps):
+        ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=cfg.dt)
+        torch.cuda.synchronize()
+        per.append((time.perf_counter() - t0) / cfg.steps)
+    ms = 1e3 * statistics.median(per)
+    return {"steps": cfg.steps, "ms_per_step": ms, "steps_per_s": 1e3 / ms, "setup_ms_incl_bep_build": setup_ms,
+            "rebuilds": sum(l["rebuilt"] for l in logs), "final_mass": logs[-1]["mass"], "rho_max": logs[-1]["rho_max"]}
+
+
+def main():
+    ap_ = argparse.ArgumentParser()
+    ap_.add_argument("--gpus", type=int, default=1)
+    ap_.add_argument("--steps", type=int, default=5)
+    ap_.add_argument("--warmup", type=int, default=3)
+    ap_.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap_.add_argument("--no-e2e", action="store_true")
+    ap_.add_argument("--no-cpu", action="store_true")
+    ap_.add_argument("--no-pks", action="store_true")
+    args = ap_.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_1811_03557_b200 import api
+    from paper_1811_03557_b200._lib import lib as L
+
+    cfg = get_config("cfg4")
+    n, B = cfg.n, cfg.batch
+    ctx = api.DPM.from_config(cfg, device=local)
+    band = ctx.copy_set("band")
+    per = -(-B // world)
+    b0, b1 = rank * per, min(B, (rank + 1) * per)
+    nb = max(0, b1 - b0)
+    vals = cfg4_band_values(B, len(band))[b0:b1]
+    field = n ** 3
+    q = torch.zeros((nb, field), dtype=torch.float64, device="cuda")
+    if nb:
+        q[:, torch.from_numpy(band).cuda()] = torch.from_numpy(vals).cuda()
+    q = q.view(nb, n, n, n)
+    u = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ctx.aux_solve_batch(q, u)
+    barrier()
+    peaks, peaks_kind = load_peaks()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = L.dpm_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            ctx.aux_solve_batch(q, u)
+        ev1.record(stream)
+        barrier()
+    launches = L.dpm_launch_count() - l0
+    ms_local = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+    value = B / (ms_per_step / 1e3)                      # whole-job solves/s (all ranks)
+    alg_bytes = 16 * n ** 3                              # dense fp64 box in + out per solve
+    per_launch_bytes = alg_bytes * nb                    # one dpm_aux_solve_batch call
+    achieved_gbs = per_launch_bytes / (ms_local / args.steps / 1e3) / 1e9
+    hbm_peak = peaks["hbm_gbs"]
+    flops_per_solve = 6 * n ** 3 * (n // 2) * 2          # 6 folded DST-I passes, n/2 MACs per output
+    achieved_tf = flops_per_solve * nb / (ms_local / args.steps / 1e3) / 1e12
+    clocks = clk.summary()
+
+    line = {"metric": "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction); PKS time steps/sec",
+            "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg4: N=128 box [-1.1,1.1]^3, dt=1e-5, 578 RHS U(-1,1) on the r=1 shell band "
+                                   "(R21), dense boxes in/out",
+                       "global_batch": B, "local_batch": nb, "n": n, "parallelism": f"rhs-shard x{world}",
+                       "l2": "inputs larger than L2 (%.1f GB per rank per step)" % (nb * field * 8 / 1e9)},
+            "roofline": {"bound": "hbm", "kernel": "dst_solve (X,Y,Z,Y,X passes of one dpm_aux_solve_batch)",
+                         "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
+                         "peak_kind": peaks_kind, "traffic": None, "alg_bytes_per_solve": alg_bytes,
+                         "fp64": {"achieved_tflops": achieved_tf, "peak_tflops": FP64_PEAK_TFLOPS,
+                                  "frac": achieved_tf / FP64_PEAK_TFLOPS, "flops_per_solve": flops_per_solve}},
+            "gpu_launches": int(launches), "clocks": clocks}
+
+    if not args.no_e2e and nb:
+        # e2e through the C-ABI host-buffer call: pinned host q/u, H2D + solve + D2H inside the timed region
+        qh = torch.empty((nb, n, n, n), dtype=torch.float64, pin_memory=True)
+        qh.copy_(q)
+        uh = torch.empty_like(qh, pin_memory=True)
+        ctx.aux_solve_batch_host(qh, uh)
+        barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 2))
+        for _ in range(e2e_steps):
+            ctx.aux_solve_batch_host(qh, uh)
+        barrier()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e_ms = float(el.item()) * 1e3 / e2e_steps
+        line["e2e"] = {"value": B / (e2e_ms / 1e3), "unit": "solves/s", "h2d_bytes_per_step": nb * field * 8,
+                       "d2h_bytes_per_step": nb * field * 8, "ms_per_step": e2e_ms,
+                       "path": "dpm_aux_solve_batch_host (pinned host buffers)"}
+        del qh, uh
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import grid
+        _, ps = grid.point_sets_for(cfg)
+        rate, secs = oracle_sample_rate(cfg, 3, vals[:3], ps.list("band"))
+        line["cpu_baseline"] = {"value": rate, "unit": "solves/s", "cores": host_cores(), "kind": "oracle",
+                                "sample": "3 of the 578 cfg4 RHS (direct-summation DST, numpy BLAS), %.1f s" % secs}
+
+    if rank == 0 and world == 1 and not args.no_pks:
+        del q, u
+        torch.cuda.empty_cache()
+        line["pks"] = {"cfg2": bench_pks(api, torch, "cfg2"), "cfg3": bench_pks(api, torch, "cfg3")}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,192 @@
+/*
+ * dpm.h — C ABI of the B200-native Difference Potentials Method (DPM) hot path.
+ *
+ * Paper: arXiv 1811.03557, "Efficient Numerical Algorithms Based on Difference
+ * Potentials for Chemotaxis Systems in 3D" (/root/reference/PAPER.md, cited P:<line>).
+ * Scope: SURVEY.md §8 (hot-path scope table) — batched Dirichlet modified-Helmholtz
+ * auxiliary-problem (AP) solves on the Cartesian box, restriction to the discrete grid
+ * boundary γ, the boundary projection P_γ / reduced BEP, the least-squares solve for
+ * spherical-harmonic Cauchy-data coefficients, and the PKS time step driving them.
+ *
+ * Conventions (all functions):
+ *  - fp64 everywhere; no torch or C++ types cross this boundary; nothing throws.
+ *  - Every entry point returns a dpm_status; on failure dpm_last_error(ctx) holds a
+ *    human-readable message (thread-unsafe; one ctx per host thread / stream).
+ *  - "device" pointers are CUDA device pointers on the ctx's device (e.g. torch
+ *    tensor data_ptr()); the CALLER owns every field buffer; the ctx owns its
+ *    workspaces, point-set lists and the BEP factorization.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is enqueued on
+ *    it; functions that must make a host decision synchronize it and say so.
+ *  - Grid: the cube [lo,hi]^3 has its faces on the Dirichlet ghost layer
+ *    N0\M0; n unknowns per axis; h = (hi-lo)/(n+1); node i (0-based) sits at
+ *    lo + (i+1) h.  Boxes are C-order [x][y][z] (z fastest), n^3 doubles, and a batch
+ *    is [batch][n][n][n].  "Flat index" = (i*n + j)*n + k.
+ *  - Point lists are ascending flat indices (int64) (R7).
+ */
+#ifndef DPM_H_
+#define DPM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DPM_OK = 0,
+  DPM_ERR_INVALID = 1,   /* bad argument: n<4 or n>DPM_MAX_N, lo>=hi, dt<=0, lmax<0, null ptr,
+                            domain not strictly inside the box or containing no node      */
+  DPM_ERR_OOM = 2,       /* device allocation failed                                       */
+  DPM_ERR_CUDA = 3,      /* a CUDA runtime call or kernel launch failed                    */
+  DPM_ERR_STATE = 4,     /* projection missing / built at another dt                       */
+  DPM_ERR_RANK = 5,      /* K >= |gamma_in| (under-determined BEP) or R singular     */
+  DPM_ERR_NONFINITE = 6  /* a PKS step produced a non-finite value                         */
+} dpm_status;
+
+#define DPM_MAX_N 128    /* largest n the AP-solve kernels are instantiated for            */
+
+typedef struct { int32_t n; double lo, hi; } dpm_grid;
+
+typedef enum { DPM_SPHERE = 0, DPM_ELLIPSOID = 1 } dpm_domain_kind;
+/* Ω = { x : Σ_a ((x_a - center_a)/semi_a)^2 < 1 }  (sphere: semi = (r,r,r), P:596;
+   ellipsoid: SURVEY R10).  Must lie strictly inside the box. */
+typedef struct { int32_t kind; double center[3]; double semi[3]; } dpm_domain;
+
+/* Extension-operator column sets; K = 2 (lmax+1)^2 columns,
+   column c = comp*(lmax+1)^2 + nu, nu = l^2 + l + m (real SH without Condon-Shortley
+   phase, R8).  comp 0: Y_nu(foot);  comp 1: d*Y_nu (CAUCHY) or (d^2/2)*Y_nu (NEUMANN0). */
+typedef enum { DPM_BASIS_CAUCHY = 0, DPM_BASIS_NEUMANN0 = 1 } dpm_basis;
+
+/* Point sets of Definition 1. BAND = M- ∩ dil7(gamma) = support of every
+   difference-potential right-hand side (R21). NPLUS = N+ restricted to M0. */
+typedef enum {
+  DPM_SET_MPLUS = 0, DPM_SET_GAMMA = 1, DPM_SET_GAMMA_IN = 2, DPM_SET_GAMMA_EX = 3,
+  DPM_SET_BAND = 4, DPM_SET_NPLUS = 5
+} dpm_set;
+
+typedef struct {
+  int32_t n, K, lmax, basis;
+  double h, dt;
+  int64_t n_mplus, n_gamma, n_gamma_in, n_gamma_ex, n_band, n_nplus;
+  int64_t ghosts_in_nplus;   /* ghost nodes belonging to N+ (R5; 72 at cfg1)              */
+  int32_t have_projection;   /* 1 once dpm_build_projection succeeded at the current dt    */
+  double bep_cond_est;       /* κ(R) of the column-equilibrated BEP (diag ratio estimate)  */
+} dpm_info;
+
+typedef struct dpm_ctx dpm_ctx;
+
+/* ---------------------------------------------------------------------------------
+ * Setup (P:40-60 auxiliary cube + Def. 1; P:263-299 extension data).
+ * Builds the point sets on the device (fp64 classification; ties -> M-, R6), the
+ * gamma geometry (foot point, signed distance d, SH angles; R10) and E (|gamma| x K).
+ * Synchronous (uses an internal stream and waits). *out is NULL on failure.
+ * ------------------------------------------------------------------------------- */
+dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt,
+                      int32_t basis, int32_t device, dpm_ctx** out);
+void       dpm_destroy(dpm_ctx* ctx);
+dpm_status dpm_query(const dpm_ctx* ctx, dpm_info* out);
+const char* dpm_last_error(const dpm_ctx* ctx);
+
+/* Copy a point list (ascending flat indices) to HOST memory; cap = capacity in entries;
+   DPM_ERR_INVALID if cap is too small. Synchronous. */
+dpm_status dpm_copy_set(const dpm_ctx* ctx, int32_t which, int64_t* host_idx, int64_t cap);
+
+/* Copy E (|gamma| x K, column-major) and the signed distances d (|gamma|) to HOST
+   memory (either pointer may be NULL). Synchronous. */
+dpm_status dpm_copy_extension(const dpm_ctx* ctx, double* host_E, double* host_d);
+
+/* Change dt (the operator is I/dt - Δ_h, R4). Invalidates the projection iff dt changes. */
+dpm_status dpm_set_dt(dpm_ctx* ctx, double dt);
+
+/* ---------------------------------------------------------------------------------
+ * S3 — the batched AP solve (fast Poisson solver P:166-168):
+ *   u_b = (I/dt - Δ_h)^{-1} q_b  on the n^3 interior, zero Dirichlet ghosts,
+ * by 3D DST-I, eigenvalue divide (λ_m = (4/h^2) sin^2(m pi/(2(n+1))), R26), inverse
+ * 3D DST-I.  q, u: DEVICE [batch][n][n][n]; u may equal q (in place).  batch >= 0.
+ * Asynchronous on `stream`.
+ * ------------------------------------------------------------------------------- */
+dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t batch, void* stream);
+
+/* Same operation through HOST buffers (pinned or pageable): H2D copy, solve, D2H copy,
+   chunked through ctx-owned device staging. Synchronizes `stream` before returning. */
+dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* host_u, int64_t batch,
+                                    void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * S2 / S4 building blocks (exposed for parity tests and multi-GPU column sharding).
+ * dpm_potential_rhs: q_c = χ_{M-} (I/dt - Δ_h)[v_c] for densities v (DEVICE,
+ *   |gamma| x nrhs column-major, zero-extended off gamma; Def. DP P:196-207 with R4
+ *   scaling) -> q DEVICE [nrhs][n][n][n] (fully written).
+ * dpm_trace: out[b][i] = u_b[list[i]] for which = GAMMA or GAMMA_IN.
+ * ------------------------------------------------------------------------------- */
+dpm_status dpm_potential_rhs(dpm_ctx* ctx, const double* v_gamma, double* q, int32_t nrhs, void* stream);
+dpm_status dpm_trace(dpm_ctx* ctx, const double* u, double* out, int32_t which, int64_t batch,
+                     void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * S2-S5 — boundary projection and reduced BEP (Step 2/4b P:425-431).
+ * dpm_bep_columns: for columns c in [c0, c1): u_c = AP(potential_rhs(E_c));
+ *   PgE[:, c-c0] = Tr_gamma u_c  (|gamma| x (c1-c0), col-major, DEVICE, nullable);
+ *   B[:, c-c0]  = E[gamma_in, c] - Tr_gamma_in u_c  (|gamma_in| x (c1-c0), DEVICE, nullable).
+ * dpm_bep_factor: factor B (|gamma_in| x K, DEVICE, col-major; not modified) for least
+ *   squares: column equilibration + CholeskyQR2 (Q explicit, R upper). Stored in ctx.
+ *   DPM_ERR_RANK if K >= |gamma_in| or the Cholesky breaks down.
+ * dpm_build_projection = dpm_bep_columns(0, K) + dpm_bep_factor, B kept in ctx.
+ * All asynchronous except dpm_bep_factor / dpm_build_projection (synchronize stream).
+ * ------------------------------------------------------------------------------- */
+dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, double* B, void* stream);
+dpm_status dpm_bep_factor(dpm_ctx* ctx, const double* B, void* stream);
+dpm_status dpm_build_projection(dpm_ctx* ctx, double* PgE, double* B, void* stream);
+
+/* S8 — least squares for the spectral coefficients (Step 5 P:433):
+ * coef = argmin || B coef - g ||_2 for each of nrhs right-hand sides.
+ * g: DEVICE |gamma_in| x nrhs col-major; coef: DEVICE K x nrhs; u_gamma (nullable):
+ * DEVICE |gamma| x nrhs = E coef (extension operator), not clamped.
+ * DPM_ERR_STATE if no projection at the current dt. Asynchronous. */
+dpm_status dpm_boundary_lsq(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int32_t nrhs,
+                            void* stream);
+
+/* ---------------------------------------------------------------------------------
+ * PKS time stepping (P:88-141 scheme; Steps 1-8 P:420-437; readings R13-R20).
+ * Fields rho (cell averages) and c: DEVICE [n][n][n], meaningful on N+ ∩ M0 and 0
+ * elsewhere (ghost nodes of N+ hold 0, R5).
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  double center[3];        /* Gaussian centre                                    */
+  double rho_amp, rho_rate;/* rho0 = rho_amp * exp(-rho_rate |x - center|^2)      */
+  double c_amp, c_rate;    /* c0   = c_amp   * exp(-c_rate   |x - center|^2)      */
+} dpm_pks_ic;
+
+typedef struct {
+  double chi;              /* chemotactic sensitivity (R27: 1)                   */
+  double dt_cap;           /* configured dt                                      */
+  int32_t dt_rule;         /* 0: dt_i = min(dt_{i-1}, dt_cap, CFL, h^2/2) (R13); 1: fixed dt_cap */
+  int32_t clamp;           /* 1: u_gamma = max(u_gamma, 0) (R17)                  */
+} dpm_pks_params;
+
+typedef struct {
+  double t, dt, mass, rho_max, rho_min, c_min;  /* mass = h^3 Σ_{M+} rho (R18)   */
+  int32_t rebuilt;                              /* 1 if Step 4b rebuilt the BEP  */
+  int32_t step;
+} dpm_step_log;
+
+/* Initial state (R14): IC at the node on M+\gamma, at the foot point on gamma, 0 elsewhere.
+   Resets t and the dt history. Asynchronous. */
+dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream);
+
+/* Advance nsteps steps in place. Each step: CFL (device reduction) -> dt (host decides,
+   stream synchronized once per step) -> [Step 4b rebuild when dt decreased] -> flux +
+   IMEX RHS -> 2 particular AP solves -> Tr_gamma_in -> LSQ -> u_gamma = E C,
+   clamp -> combined Green's-formula RHS (R20) -> 2 AP solves -> restrict to N+.
+   log (HOST, nullable) receives nsteps entries. DPM_ERR_NONFINITE on NaN/Inf. */
+dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, const dpm_pks_params* params,
+                        dpm_step_log* log, void* stream);
+
+/* Cumulative number of CUDA kernels this library has launched in the process (all
+   contexts).  Lets a harness count the library's launches inside a timed region. */
+int64_t dpm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPM_H_ */

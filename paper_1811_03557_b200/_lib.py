@@ -1,0 +1,94 @@
+"""ctypes declarations of libdpm.so (include/dpm.h).  Argument marshalling only.
+
+There is no fallback: if libdpm.so is missing or fails to load, importing this module
+raises (build it with ``python -m paper_1811_03557_b200.build`` or ``__graft_entry__.build()``).
+"""
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdpm.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libdpm.so not built at {LIB_PATH}; run python -m paper_1811_03557_b200.build")
+lib = C.CDLL(LIB_PATH)
+
+DPM_OK, DPM_ERR_INVALID, DPM_ERR_OOM, DPM_ERR_CUDA, DPM_ERR_STATE, DPM_ERR_RANK, DPM_ERR_NONFINITE = range(7)
+STATUS = {0: "DPM_OK", 1: "DPM_ERR_INVALID", 2: "DPM_ERR_OOM", 3: "DPM_ERR_CUDA", 4: "DPM_ERR_STATE",
+          5: "DPM_ERR_RANK", 6: "DPM_ERR_NONFINITE"}
+SPHERE, ELLIPSOID = 0, 1
+BASIS_CAUCHY, BASIS_NEUMANN0 = 0, 1
+SETS = {"mplus": 0, "gamma": 1, "gamma_in": 2, "gamma_ex": 3, "band": 4, "nplus": 5}
+MAX_N = 128
+
+
+class Grid(C.Structure):
+    _fields_ = [("n", C.c_int32), ("lo", C.c_double), ("hi", C.c_double)]
+
+
+class Domain(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("center", C.c_double * 3), ("semi", C.c_double * 3)]
+
+
+class Info(C.Structure):
+    _fields_ = [("n", C.c_int32), ("K", C.c_int32), ("lmax", C.c_int32), ("basis", C.c_int32),
+                ("h", C.c_double), ("dt", C.c_double),
+                ("n_mplus", C.c_int64), ("n_gamma", C.c_int64), ("n_gamma_in", C.c_int64),
+                ("n_gamma_ex", C.c_int64), ("n_band", C.c_int64), ("n_nplus", C.c_int64),
+                ("ghosts_in_nplus", C.c_int64), ("have_projection", C.c_int32), ("bep_cond_est", C.c_double)]
+
+
+class PksIC(C.Structure):
+    _fields_ = [("center", C.c_double * 3), ("rho_amp", C.c_double), ("rho_rate", C.c_double),
+                ("c_amp", C.c_double), ("c_rate", C.c_double)]
+
+
+class PksParams(C.Structure):
+    _fields_ = [("chi", C.c_double), ("dt_cap", C.c_double), ("dt_rule", C.c_int32), ("clamp", C.c_int32)]
+
+
+class StepLog(C.Structure):
+    _fields_ = [("t", C.c_double), ("dt", C.c_double), ("mass", C.c_double), ("rho_max", C.c_double),
+                ("rho_min", C.c_double), ("c_min", C.c_double), ("rebuilt", C.c_int32), ("step", C.c_int32)]
+
+
+P = C.c_void_p
+D = C.POINTER(C.c_double)
+_sig = {
+    "dpm_create": ([C.POINTER(Grid), C.POINTER(Domain), C.c_int32, C.c_double, C.c_int32, C.c_int32,
+                    C.POINTER(P)], C.c_int),
+    "dpm_destroy": ([P], None),
+    "dpm_query": ([P, C.POINTER(Info)], C.c_int),
+    "dpm_last_error": ([P], C.c_char_p),
+    "dpm_copy_set": ([P, C.c_int32, C.POINTER(C.c_int64), C.c_int64], C.c_int),
+    "dpm_copy_extension": ([P, D, D], C.c_int),
+    "dpm_set_dt": ([P, C.c_double], C.c_int),
+    "dpm_aux_solve_batch": ([P, P, P, C.c_int64, P], C.c_int),
+    "dpm_aux_solve_batch_host": ([P, P, P, C.c_int64, P], C.c_int),
+    "dpm_potential_rhs": ([P, P, P, C.c_int32, P], C.c_int),
+    "dpm_trace": ([P, P, P, C.c_int32, C.c_int64, P], C.c_int),
+    "dpm_bep_columns": ([P, C.c_int32, C.c_int32, P, P, P], C.c_int),
+    "dpm_bep_factor": ([P, P, P], C.c_int),
+    "dpm_build_projection": ([P, P, P, P], C.c_int),
+    "dpm_boundary_lsq": ([P, P, P, P, C.c_int32, P], C.c_int),
+    "dpm_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
+    "dpm_pks_step": ([P, P, P, C.c_int32, C.POINTER(PksParams), C.POINTER(StepLog), P], C.c_int),
+    "dpm_launch_count": ([], C.c_int64),
+}
+EXPORTED = tuple(_sig)
+for _name, (_args, _res) in _sig.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+class DPMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def check(status, ctx=None):
+    if status != DPM_OK:
+        msg = lib.dpm_last_error(ctx)
+        raise DPMError(status, msg.decode() if msg else "")

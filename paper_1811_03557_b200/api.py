@@ -1,0 +1,180 @@
+"""Thin Python binding over the C ABI (include/dpm.h): argument marshalling only.
+
+Every computation runs in libdpm.so's CUDA kernels.  torch is used for device memory
+and streams only.  Names follow the ABI: ``dpm_create`` returns a :class:`DPM` whose
+methods are the remaining ``dpm_*`` calls without the prefix.
+"""
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev_f64(t: torch.Tensor, name: str):
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+    return t
+
+
+class DPM:
+    """One dpm_ctx: grid + domain + basis + dt on one device."""
+
+    def __init__(self, n, lo, hi, kind="sphere", center=(0.0, 0.0, 0.0), semi=(1.0, 1.0, 1.0), lmax=4,
+                 dt=1e-3, basis="cauchy", device=0):
+        g = L.Grid(n, lo, hi)
+        d = L.Domain(L.SPHERE if kind == "sphere" else L.ELLIPSOID, (C.c_double * 3)(*center),
+                     (C.c_double * 3)(*semi))
+        b = L.BASIS_CAUCHY if basis == "cauchy" else L.BASIS_NEUMANN0
+        h = C.c_void_p()
+        torch.cuda.init()
+        L.check(L.lib.dpm_create(C.byref(g), C.byref(d), lmax, dt, b, device, C.byref(h)))
+        self._h = h
+        self.device = torch.device("cuda", device)
+        self.n = n
+        self.info = self.query()
+        self.K = self.info["K"]
+
+    @classmethod
+    def from_config(cls, cfg, device=0):
+        return cls(cfg.n, cfg.lo, cfg.hi, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.dt, cfg.basis, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib.dpm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _chk(self, st):
+        L.check(st, self._h)
+
+    def query(self):
+        info = L.Info()
+        self._chk(L.lib.dpm_query(self._h, C.byref(info)))
+        return {f: getattr(info, f) for f, _ in L.Info._fields_}
+
+    def copy_set(self, which: str) -> np.ndarray:
+        key = {"mplus": "n_mplus", "gamma": "n_gamma", "gamma_in": "n_gamma_in", "gamma_ex": "n_gamma_ex",
+               "band": "n_band", "nplus": "n_nplus"}[which]
+        cnt = self.query()[key]
+        out = np.empty(max(cnt, 1), dtype=np.int64)
+        self._chk(L.lib.dpm_copy_set(self._h, L.SETS[which], out.ctypes.data_as(C.POINTER(C.c_int64)), cnt))
+        return out[:cnt]
+
+    def copy_extension(self):
+        i = self.query()
+        E = np.empty((i["K"], i["n_gamma"]), dtype=np.float64)   # column-major |γ| x K
+        d = np.empty(i["n_gamma"], dtype=np.float64)
+        self._chk(L.lib.dpm_copy_extension(self._h, E.ctypes.data_as(L.D), d.ctypes.data_as(L.D)))
+        return E.T.copy(), d
+
+    def set_dt(self, dt: float):
+        self._chk(L.lib.dpm_set_dt(self._h, dt))
+
+    def aux_solve_batch(self, q: torch.Tensor, u: torch.Tensor = None, stream=None) -> torch.Tensor:
+        _dev_f64(q, "q")
+        if u is None:
+            u = torch.empty_like(q)
+        _dev_f64(u, "u")
+        batch = q.numel() // self.n ** 3
+        self._chk(L.lib.dpm_aux_solve_batch(self._h, _ptr(q), _ptr(u), batch, _stream(stream)))
+        return u
+
+    def aux_solve_batch_host(self, q_host: torch.Tensor, u_host: torch.Tensor = None, stream=None) -> torch.Tensor:
+        if q_host.is_cuda or q_host.dtype != torch.float64 or not q_host.is_contiguous():
+            raise ValueError("q_host must be a contiguous float64 CPU tensor")
+        if u_host is None:
+            u_host = torch.empty_like(q_host)
+        batch = q_host.numel() // self.n ** 3
+        self._chk(L.lib.dpm_aux_solve_batch_host(self._h, _ptr(q_host), _ptr(u_host), batch, _stream(stream)))
+        return u_host
+
+    def potential_rhs(self, v_gamma: torch.Tensor, stream=None) -> torch.Tensor:
+        """v_gamma: [nrhs, |γ|] (row r = density r) -> q [nrhs, n, n, n]."""
+        _dev_f64(v_gamma, "v_gamma")
+        nrhs = v_gamma.shape[0]
+        q = torch.empty((nrhs, self.n, self.n, self.n), dtype=torch.float64, device=self.device)
+        self._chk(L.lib.dpm_potential_rhs(self._h, _ptr(v_gamma), _ptr(q), nrhs, _stream(stream)))
+        return q
+
+    def trace(self, u: torch.Tensor, which="gamma", stream=None) -> torch.Tensor:
+        _dev_f64(u, "u")
+        batch = u.numel() // self.n ** 3
+        m = self.info["n_gamma" if which == "gamma" else "n_gamma_in"]
+        out = torch.empty((batch, m), dtype=torch.float64, device=self.device)
+        self._chk(L.lib.dpm_trace(self._h, _ptr(u), _ptr(out), L.SETS[which], batch, _stream(stream)))
+        return out
+
+    def bep_columns(self, c0: int, c1: int, stream=None):
+        """Returns (PgE [c1-c0, |γ|], B [c1-c0, |γ_in|]) — row r = column c0+r."""
+        i = self.info
+        PgE = torch.empty((c1 - c0, i["n_gamma"]), dtype=torch.float64, device=self.device)
+        B = torch.empty((c1 - c0, i["n_gamma_in"]), dtype=torch.float64, device=self.device)
+        self._chk(L.lib.dpm_bep_columns(self._h, c0, c1, _ptr(PgE), _ptr(B), _stream(stream)))
+        return PgE, B
+
+    def bep_factor(self, B: torch.Tensor, stream=None):
+        _dev_f64(B, "B")
+        self._chk(L.lib.dpm_bep_factor(self._h, _ptr(B), _stream(stream)))
+
+    def build_projection(self, want_outputs=True, stream=None):
+        i = self.info
+        PgE = B = None
+        if want_outputs:
+            PgE = torch.empty((self.K, i["n_gamma"]), dtype=torch.float64, device=self.device)
+            B = torch.empty((self.K, i["n_gamma_in"]), dtype=torch.float64, device=self.device)
+        self._chk(L.lib.dpm_build_projection(self._h, _ptr(PgE), _ptr(B), _stream(stream)))
+        return PgE, B
+
+    def boundary_lsq(self, g: torch.Tensor, want_u_gamma=True, stream=None):
+        """g: [nrhs, |γ_in|] -> (coef [nrhs, K], u_gamma [nrhs, |γ|])."""
+        _dev_f64(g, "g")
+        nrhs = g.shape[0]
+        coef = torch.empty((nrhs, self.K), dtype=torch.float64, device=self.device)
+        ug = torch.empty((nrhs, self.info["n_gamma"]), dtype=torch.float64, device=self.device) if want_u_gamma else None
+        self._chk(L.lib.dpm_boundary_lsq(self._h, _ptr(g), _ptr(coef), _ptr(ug), nrhs, _stream(stream)))
+        return coef, ug
+
+    def pks_init(self, rho: torch.Tensor, c: torch.Tensor, center, rho_amp, rho_rate, c_amp, c_rate, stream=None):
+        ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate)
+        self._chk(L.lib.dpm_pks_init(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), C.byref(ic),
+                                     _stream(stream)))
+
+    def pks_step(self, rho, c, nsteps, chi=1.0, dt_cap=1e-4, dt_rule=0, clamp=1, stream=None):
+        prm = L.PksParams(chi, dt_cap, dt_rule, clamp)
+        logs = (L.StepLog * max(nsteps, 1))()
+        self._chk(L.lib.dpm_pks_step(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), nsteps,
+                                     C.byref(prm), logs, _stream(stream)))
+        return [{f: getattr(logs[i], f) for f, _ in L.StepLog._fields_} for i in range(nsteps)]
+
+
+def dpm_create(n, lo, hi, kind, center, semi, lmax, dt, basis, device=0) -> DPM:
+    return DPM(n, lo, hi, kind, center, semi, lmax, dt, basis, device)
+
+
+def dpm_aux_solve_batch(ctx: DPM, q, u=None, stream=None):
+    return ctx.aux_solve_batch(q, u, stream)
+
+
+def dpm_build_projection(ctx: DPM, stream=None):
+    return ctx.build_projection(True, stream)
+
+
+def dpm_boundary_lsq(ctx: DPM, g, stream=None):
+    return ctx.boundary_lsq(g, True, stream)
+
+
+def dpm_pks_step(ctx: DPM, rho, c, nsteps, **kw):
+    return ctx.pks_step(rho, c, nsteps, **kw)

@@ -1,0 +1,351 @@
+// extern "C" entry points of libdpm.so (declared and documented in include/dpm.h).
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "dpm_internal.h"
+
+std::atomic<long long> g_dpm_launches{0};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+void free_ctx(dpm_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale,
+                  c->lsq_ws, c->work, c->scratch, c->red};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto* l : c->lists)
+    if (l) cudaFree(l);
+  if (c->red_host) cudaFreeHost(c->red_host);
+  dst_plan_free(c->plan);
+  if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
+  delete c;
+}
+
+dpm_status ensure_work(dpm_ctx* ctx, size_t boxes) {
+  if (ctx->work_boxes >= boxes) return DPM_OK;
+  if (ctx->work) cudaFree(ctx->work);
+  ctx->work = nullptr;
+  ctx->work_boxes = 0;
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  if (cudaMalloc(&ctx->work, boxes * field * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->err = "out of device memory for work boxes";
+    return DPM_ERR_OOM;
+  }
+  ctx->work_boxes = boxes;
+  return DPM_OK;
+}
+
+// columns processed per BEP chunk (bounded device memory: <= ~2 GB of boxes)
+int bep_chunk(const dpm_ctx* ctx) {
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n * sizeof(double);
+  return (int)std::max<size_t>(1, std::min<size_t>((size_t)ctx->K, ((size_t)2 << 30) / field));
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* dpm_last_error(const dpm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
+                      int32_t device, dpm_ctx** out) {
+  if (out) *out = nullptr;
+  g_create_err.clear();
+  if (!grid || !domain || !out) { g_create_err = "null argument"; return DPM_ERR_INVALID; }
+  if (grid->n < 4 || grid->n > DPM_MAX_N) { g_create_err = "n out of range [4, DPM_MAX_N]"; return DPM_ERR_INVALID; }
+  if (!(grid->lo < grid->hi)) { g_create_err = "lo >= hi"; return DPM_ERR_INVALID; }
+  if (!(dt > 0) || !std::isfinite(dt)) { g_create_err = "dt must be > 0"; return DPM_ERR_INVALID; }
+  if (lmax < 0 || lmax > 40) { g_create_err = "lmax out of range"; return DPM_ERR_INVALID; }
+  if (basis != DPM_BASIS_CAUCHY && basis != DPM_BASIS_NEUMANN0) { g_create_err = "bad basis"; return DPM_ERR_INVALID; }
+  if (domain->kind != DPM_SPHERE && domain->kind != DPM_ELLIPSOID) { g_create_err = "bad domain kind"; return DPM_ERR_INVALID; }
+  for (int a = 0; a < 3; ++a) {
+    const double s = domain->kind == DPM_SPHERE ? domain->semi[0] : domain->semi[a];
+    if (!(s > 0)) { g_create_err = "semi-axes must be > 0"; return DPM_ERR_INVALID; }
+    if (!(domain->center[a] - s > grid->lo && domain->center[a] + s < grid->hi)) {
+      g_create_err = "domain not strictly inside the box";
+      return DPM_ERR_INVALID;
+    }
+  }
+  if (cudaSetDevice(device) != cudaSuccess) { g_create_err = "cudaSetDevice failed"; return DPM_ERR_CUDA; }
+  dpm_ctx* ctx = new (std::nothrow) dpm_ctx();
+  if (!ctx) return DPM_ERR_OOM;
+  ctx->device = device;
+  ctx->n = grid->n;
+  ctx->lo = grid->lo;
+  ctx->hi = grid->hi;
+  ctx->h = (grid->hi - grid->lo) / (grid->n + 1);
+  ctx->dt = dt;
+  ctx->domain = *domain;
+  if (domain->kind == DPM_SPHERE) ctx->domain.semi[1] = ctx->domain.semi[2] = domain->semi[0];
+  ctx->lmax = lmax;
+  ctx->basis = basis;
+  ctx->K = 2 * (lmax + 1) * (lmax + 1);
+  dpm_status st = DPM_OK;
+  if (cudaStreamCreateWithFlags(&ctx->setup_stream, cudaStreamNonBlocking) != cudaSuccess) st = DPM_ERR_CUDA;
+  if (st == DPM_OK) st = setup_point_sets(ctx);
+  if (st == DPM_OK) st = setup_geometry(ctx);
+  if (st == DPM_OK && dst_plan_init(ctx->plan, ctx->n, ctx->h, dt) != cudaSuccess) { st = DPM_ERR_CUDA; ctx->err = "plan init"; }
+  if (st == DPM_OK && cudaMalloc(&ctx->red, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
+  if (st == DPM_OK && cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
+  if (st != DPM_OK) {
+    g_create_err = ctx->err.empty() ? "dpm_create failed" : ctx->err;
+    free_ctx(ctx);
+    return st;
+  }
+  *out = ctx;
+  return DPM_OK;
+}
+
+void dpm_destroy(dpm_ctx* ctx) { free_ctx(ctx); }
+
+dpm_status dpm_query(const dpm_ctx* ctx, dpm_info* out) {
+  if (!ctx || !out) return DPM_ERR_INVALID;
+  std::memset(out, 0, sizeof(*out));
+  out->n = ctx->n;
+  out->K = ctx->K;
+  out->lmax = ctx->lmax;
+  out->basis = ctx->basis;
+  out->h = ctx->h;
+  out->dt = ctx->dt;
+  out->n_mplus = ctx->counts[DPM_SET_MPLUS];
+  out->n_gamma = ctx->counts[DPM_SET_GAMMA];
+  out->n_gamma_in = ctx->counts[DPM_SET_GAMMA_IN];
+  out->n_gamma_ex = ctx->counts[DPM_SET_GAMMA_EX];
+  out->n_band = ctx->counts[DPM_SET_BAND];
+  out->n_nplus = ctx->counts[DPM_SET_NPLUS];
+  out->ghosts_in_nplus = ctx->ghosts_in_nplus;
+  out->have_projection = ctx->have_projection;
+  out->bep_cond_est = ctx->bep_cond;
+  return DPM_OK;
+}
+
+dpm_status dpm_copy_set(const dpm_ctx* ctx, int32_t which, int64_t* host_idx, int64_t cap) {
+  if (!ctx || !host_idx || which < 0 || which > 5) return DPM_ERR_INVALID;
+  dpm_ctx* c = const_cast<dpm_ctx*>(ctx);
+  if (cap < ctx->counts[which]) { c->err = "capacity too small"; return DPM_ERR_INVALID; }
+  cudaSetDevice(ctx->device);
+  DPM_CUDA_TRY(c, cudaMemcpy(host_idx, ctx->lists[which], ctx->counts[which] * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  return DPM_OK;
+}
+
+dpm_status dpm_copy_extension(const dpm_ctx* ctx, double* host_E, double* host_d) {
+  if (!ctx) return DPM_ERR_INVALID;
+  dpm_ctx* c = const_cast<dpm_ctx*>(ctx);
+  cudaSetDevice(ctx->device);
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA];
+  if (host_E) DPM_CUDA_TRY(c, cudaMemcpy(host_E, ctx->E, (size_t)ng * ctx->K * sizeof(double), cudaMemcpyDeviceToHost));
+  if (host_d) DPM_CUDA_TRY(c, cudaMemcpy(host_d, ctx->dist, (size_t)ng * sizeof(double), cudaMemcpyDeviceToHost));
+  return DPM_OK;
+}
+
+dpm_status dpm_set_dt(dpm_ctx* ctx, double dt) {
+  if (!ctx || !(dt > 0) || !std::isfinite(dt)) return DPM_ERR_INVALID;
+  if (dt != ctx->dt) {
+    ctx->dt = dt;
+    ctx->plan.dt = dt;
+    ctx->have_projection = 0;
+  }
+  return DPM_OK;
+}
+
+dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t batch, void* stream) {
+  if (!ctx || batch < 0 || (batch > 0 && (!q || !u))) return DPM_ERR_INVALID;
+  if (batch == 0) return DPM_OK;
+  cudaSetDevice(ctx->device);
+  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, q, u, batch, nullptr, 0, as_stream(stream)));
+  return DPM_OK;
+}
+
+dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* host_u, int64_t batch, void* stream) {
+  if (!ctx || batch < 0 || (batch > 0 && (!host_q || !host_u))) return DPM_ERR_INVALID;
+  if (batch == 0) return DPM_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  // double-buffered staging: chunk of fields per buffer
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(((size_t)256 << 20) / (field * 8))));
+  dpm_status st = ensure_work(ctx, 2 * chunk);
+  if (st != DPM_OK) return st;
+  for (int64_t b0 = 0, it = 0; b0 < batch; b0 += chunk, ++it) {
+    const int64_t nb = std::min<int64_t>(chunk, batch - b0);
+    double* buf = ctx->work + (size_t)(it & 1) * chunk * field;
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(buf, host_q + b0 * field, nb * field * 8, cudaMemcpyHostToDevice, s));
+    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, buf, buf, nb, nullptr, 0, s));
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(host_u + b0 * field, buf, nb * field * 8, cudaMemcpyDeviceToHost, s));
+  }
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return DPM_OK;
+}
+
+dpm_status dpm_potential_rhs(dpm_ctx* ctx, const double* v_gamma, double* q, int32_t nrhs, void* stream) {
+  if (!ctx || nrhs < 0 || (nrhs > 0 && (!v_gamma || !q))) return DPM_ERR_INVALID;
+  if (nrhs == 0) return DPM_OK;
+  cudaSetDevice(ctx->device);
+  DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, v_gamma, ctx->counts[DPM_SET_GAMMA], q, nrhs, as_stream(stream)));
+  return DPM_OK;
+}
+
+dpm_status dpm_trace(dpm_ctx* ctx, const double* u, double* out, int32_t which, int64_t batch, void* stream) {
+  if (!ctx || (which != DPM_SET_GAMMA && which != DPM_SET_GAMMA_IN) || batch < 0) return DPM_ERR_INVALID;
+  if (batch == 0) return DPM_OK;
+  if (!u || !out) return DPM_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  DPM_CUDA_TRY(ctx, launch_trace(ctx, u, out, which, batch, as_stream(stream)));
+  return DPM_OK;
+}
+
+dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, double* B, void* stream) {
+  if (!ctx || c0 < 0 || c1 > ctx->K || c0 > c1) return DPM_ERR_INVALID;
+  if (c0 == c1) return DPM_OK;
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  const int ch = bep_chunk(ctx);
+  dpm_status st = ensure_work(ctx, std::min(ch, c1 - c0));
+  if (st != DPM_OK) return st;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  for (int a = c0; a < c1; a += ch) {
+    const int nc = std::min(ch, c1 - a);
+    DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, nc, s));
+    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, nc, nullptr, 0, s));
+    DPM_CUDA_TRY(ctx, launch_bep_gather(ctx, ctx->work, a, nc, PgE ? PgE + (size_t)(a - c0) * ng : nullptr,
+                                        B ? B + (size_t)(a - c0) * ngin : nullptr, s));
+  }
+  return DPM_OK;
+}
+
+dpm_status dpm_bep_factor(dpm_ctx* ctx, const double* B, void* stream) {
+  if (!ctx || !B) return DPM_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  dpm_status st = lsq_factor(ctx, B, as_stream(stream));
+  if (st == DPM_OK) {
+    ctx->have_projection = 1;
+    ctx->dt_bep = ctx->dt;
+  }
+  return st;
+}
+
+dpm_status dpm_build_projection(dpm_ctx* ctx, double* PgE, double* B, void* stream) {
+  if (!ctx) return DPM_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  const int64_t ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  if (ctx->K >= ngin) { ctx->err = "K >= |gamma_in|"; return DPM_ERR_RANK; }
+  if (!ctx->B) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->B, (size_t)ngin * ctx->K * sizeof(double)));
+  dpm_status st = dpm_bep_columns(ctx, 0, ctx->K, PgE, ctx->B, stream);
+  if (st != DPM_OK) return st;
+  if (B) DPM_CUDA_TRY(ctx, cudaMemcpyAsync(B, ctx->B, (size_t)ngin * ctx->K * sizeof(double), cudaMemcpyDeviceToDevice,
+                                           as_stream(stream)));
+  return dpm_bep_factor(ctx, ctx->B, stream);
+}
+
+dpm_status dpm_boundary_lsq(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int32_t nrhs, void* stream) {
+  if (!ctx || nrhs < 1 || nrhs > 2048 || !g || !coef) return DPM_ERR_INVALID;
+  if (!ctx->have_projection || ctx->dt_bep != ctx->dt) { ctx->err = "no projection at the current dt"; return DPM_ERR_STATE; }
+  cudaSetDevice(ctx->device);
+  DPM_CUDA_TRY(ctx, lsq_apply(ctx, g, coef, u_gamma, nrhs, 0, as_stream(stream)));
+  return DPM_OK;
+}
+
+dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream) {
+  if (!ctx || !rho || !c || !ic) return DPM_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  DPM_CUDA_TRY(ctx, launch_pks_init(ctx, rho, c, ic, as_stream(stream)));
+  ctx->t = 0.0;
+  ctx->dt_prev = INFINITY;
+  ctx->pks_initialized = 1;
+  return DPM_OK;
+}
+
+static double decode_key(double slot) {
+  unsigned long long k;
+  std::memcpy(&k, &slot, 8);
+  unsigned long long x = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double v;
+  std::memcpy(&v, &x, 8);
+  return v;
+}
+
+dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, const dpm_pks_params* prm,
+                        dpm_step_log* log, void* stream) {
+  if (!ctx || !rho || !c || !prm || nsteps < 0) return DPM_ERR_INVALID;
+  if (!(prm->dt_cap > 0) || !(prm->chi > 0)) { ctx->err = "dt_cap and chi must be > 0"; return DPM_ERR_INVALID; }
+  if (!ctx->pks_initialized) { ctx->t = 0.0; ctx->dt_prev = INFINITY; ctx->pks_initialized = 1; }
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  if (!ctx->scratch || ctx->scratch_bytes < (size_t)(4 * field + 2 * ngin + 2 * ng + 2 * ctx->K) * 8) {
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    ctx->scratch_bytes = (size_t)(4 * field + 2 * ngin + 2 * ng + 2 * ctx->K) * 8;
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, ctx->scratch_bytes));
+  }
+  double* fq = ctx->scratch;              // 2 boxes: f/dt on M+
+  double* wk = fq + 2 * field;            // 2 boxes: solves
+  double* gvec = wk + 2 * field;          // |gamma_in| x 2
+  double* ug = gvec + 2 * ngin;           // |gamma| x 2
+  double* coef = ug + 2 * ng;             // K x 2
+  const double h = ctx->h;
+  for (int st = 0; st < nsteps; ++st) {
+    // Step 3: dt from the CFL condition (R19) and the dt rule (R13)
+    double dt = prm->dt_cap;
+    if (prm->dt_rule == 0) {
+      DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, ctx->red, s));
+      DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host, ctx->red, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+      double cfl = INFINITY;
+      for (int a = 0; a < 3; ++a) {
+        const double mx = ctx->red_host[a] / h;
+        if (mx > 0) cfl = std::fmin(cfl, h / (6.0 * prm->chi * mx));
+      }
+      dt = std::fmin(std::fmin(ctx->dt_prev, prm->dt_cap), std::fmin(cfl, 0.5 * h * h));
+    }
+    // Step 2 / 4b: (re)build the BEP when dt differs from the one it was built at
+    int rebuilt = 0;
+    if (!ctx->have_projection || dt != ctx->dt_bep) {
+      dpm_status r = dpm_set_dt(ctx, dt);
+      if (r != DPM_OK) return r;
+      ctx->have_projection = 0;
+      r = dpm_build_projection(ctx, nullptr, nullptr, stream);
+      if (r != DPM_OK) return r;
+      rebuilt = 1;
+    }
+    // Step 4a: flux + IMEX right-hand sides, particular solutions
+    DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s));
+    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+    // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp
+    DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
+    DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s));
+    // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
+    DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
+    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    ctx->dt_prev = dt;
+    ctx->t += dt;
+    if (ctx->red_host[12] != 0.0) { ctx->err = "non-finite value in the PKS step"; return DPM_ERR_NONFINITE; }
+    if (log) {
+      dpm_step_log& L = log[st];
+      L.t = ctx->t;
+      L.dt = dt;
+      L.mass = ctx->red_host[8] * h * h * h;
+      L.rho_max = decode_key(ctx->red_host[9]);
+      L.rho_min = -decode_key(ctx->red_host[10]);
+      L.c_min = -decode_key(ctx->red_host[11]);
+      L.rebuilt = rebuilt;
+      L.step = st;
+    }
+  }
+  return DPM_OK;
+}
+
+int64_t dpm_launch_count(void) { return (int64_t)g_dpm_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Internal declarations shared by the CUDA translation units of libdpm.so.
+// Not part of the ABI (include/dpm.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/dpm.h"
+
+// point-flag bits for the uint8 mask over the n^3 interior
+enum : uint8_t {
+  F_MPLUS = 1,   // M+
+  F_NPLUS = 2,   // N+ ∩ M0
+  F_GAMMA = 4,   // gamma
+  F_BAND = 8,    // M- ∩ dil7(gamma)
+  F_NMINUS = 16  // N- ∩ M0
+};
+
+struct DstPlan {
+  int n = 0;
+  double h = 0, dt = 0;
+  double* lam = nullptr;  // device, n eigenvalues λ_m (R26)
+};
+
+struct dpm_ctx {
+  int device = 0;
+  int n = 0;
+  double lo = 0, hi = 0, h = 0, dt = 0;
+  dpm_domain domain{};
+  int lmax = 0, basis = 0, K = 0;
+  cudaStream_t setup_stream = nullptr;
+  std::string err;
+
+  // point sets (device)
+  uint8_t* flags = nullptr;      // [n^3]
+  int32_t* gmap = nullptr;       // [n^3] gamma position or -1
+  int64_t* lists[6] = {nullptr}; // dpm_set order
+  int64_t counts[6] = {0};
+  int64_t ghosts_in_nplus = 0;
+  int32_t* gin_pos = nullptr;    // [n_gamma_in] position of gamma_in points inside gamma
+
+  // gamma geometry + extension matrix (device)
+  double* foot = nullptr;        // [n_gamma][3]
+  double* dist = nullptr;        // [n_gamma]
+  double* E = nullptr;           // [K][n_gamma] (column-major |gamma| x K)
+
+  DstPlan plan;
+
+  // BEP / LSQ (device)
+  int have_projection = 0;
+  double dt_bep = 0;
+  double* B = nullptr;           // [K][n_gin]
+  double* Q = nullptr;           // [K][n_gin]  equilibrated Q
+  double* R = nullptr;           // [K][K] col-major upper triangular
+  double* colscale = nullptr;    // [K]
+  double bep_cond = 0;
+  double* lsq_ws = nullptr;      // scratch
+
+  // workspaces
+  double* work = nullptr;        // boxes for the solver / PKS
+  size_t work_boxes = 0;
+  double* scratch = nullptr;
+  size_t scratch_bytes = 0;
+
+  // PKS state
+  double t = 0, dt_prev = 0;
+  int pks_initialized = 0;
+  double* red = nullptr;         // device reduction slots
+  double* red_host = nullptr;    // pinned
+};
+
+// process-wide launch counter (dpm_launch_count)
+#include <atomic>
+extern std::atomic<long long> g_dpm_launches;
+#define DPM_COUNT_LAUNCH(k) (g_dpm_launches.fetch_add((k), std::memory_order_relaxed))
+
+// helpers
+#define DPM_CUDA_TRY(ctx, call)                                                       \
+  do {                                                                                \
+    cudaError_t _e = (call);                                                          \
+    if (_e != cudaSuccess) {                                                          \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(_e);                \
+      return DPM_ERR_CUDA;                                                            \
+    }                                                                                 \
+  } while (0)
+
+// dst_solve.cu
+cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt);
+void dst_plan_free(DstPlan& p);
+cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_t batch, double* scratch,
+                            size_t scratch_bytes, cudaStream_t s);
+size_t dst_scratch_bytes(int n, int chunk);
+
+// setup.cu
+dpm_status setup_point_sets(dpm_ctx* ctx);
+dpm_status setup_geometry(dpm_ctx* ctx);
+
+// ops.cu
+cudaError_t launch_potential_rhs(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
+                                 cudaStream_t s);
+cudaError_t launch_trace(const dpm_ctx* ctx, const double* u, double* out, int which, int64_t batch,
+                         cudaStream_t s);
+cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int ncols, double* PgE,
+                              double* B, cudaStream_t s);
+
+// lsq.cu
+dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s);
+cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
+                      cudaStream_t s);
+
+// pks.cu
+cudaError_t launch_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, cudaStream_t s);
+cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaStream_t s);
+cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi,
+                            double* fq_rho, double* fq_c, cudaStream_t s);
+cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
+                             cudaStream_t s);
+cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
+                                  cudaStream_t s);

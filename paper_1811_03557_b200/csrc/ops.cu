@@ -1,0 +1,361 @@
+// S2 / S4 / S6 / S8-S9 element-wise and stencil kernels:
+//  * potential RHS scatter  q = χ_{M-} (I/dt - Δ_h)[v_γ]            (Def. DP; R4)
+//  * trace / BEP gather     PgE = Tr_γ u, B = E_in - Tr_γin u
+//  * PKS: CFL reduction (R19), upwind/minmod flux + IMEX RHS (R15, R16),
+//         combined Green RHS (R20), restriction to N+ with step statistics (R18).
+#include "dpm_internal.h"
+
+namespace {
+
+constexpr int TB = 256;
+
+__device__ __forceinline__ void ijk(long p, int n, int& i, int& j, int& k) {
+  i = (int)(p / ((long)n * n));
+  j = (int)((p / n) % n);
+  k = (int)(p % n);
+}
+
+__device__ __forceinline__ long flat(int n, int i, int j, int k) { return ((long)i * n + j) * n + k; }
+
+__device__ __forceinline__ bool interior(int n, int i, int j, int k) {
+  return i >= 0 && i < n && j >= 0 && j < n && k >= 0 && k < n;
+}
+
+// (I/dt - Δ_h)[v](p) for a density v given on gamma (zero elsewhere, zero ghosts)
+__device__ __forceinline__ double lop_gamma(const int32_t* __restrict__ gmap, const double* __restrict__ v, int n,
+                                            int i, int j, int k, double diag, double off) {
+  const int gp = gmap[flat(n, i, j, k)];
+  double acc = gp >= 0 ? diag * v[gp] : 0.0;
+  const int di[6] = {1, -1, 0, 0, 0, 0}, dj[6] = {0, 0, 1, -1, 0, 0}, dk[6] = {0, 0, 0, 0, 1, -1};
+  double nb = 0.0;
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const int a = i + di[s], b = j + dj[s], c = k + dk[s];
+    if (!interior(n, a, b, c)) continue;
+    const int g = gmap[flat(n, a, b, c)];
+    if (g >= 0) nb += v[g];
+  }
+  return acc - off * nb;
+}
+
+__global__ void potential_rhs_kernel(const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
+                                     int64_t nband, const double* __restrict__ v, int64_t ldv, double* q,
+                                     int nrhs, int n, double diag, double off) {
+  const size_t field = (size_t)n * n * n;
+  const long total = (long)nband * nrhs;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(t / nband);
+    const long b = t - (long)r * nband;
+    const long p = band[b];
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    q[r * field + p] = lop_gamma(gmap, v + (size_t)r * ldv, n, i, j, k, diag, off);
+  }
+}
+
+__global__ void trace_kernel(const double* __restrict__ u, const int64_t* __restrict__ list, int64_t m, double* out,
+                             int64_t batch, size_t field) {
+  const long total = (long)m * batch;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const long b = t / m, i = t - b * m;
+    out[t] = u[b * field + list[i]];
+  }
+}
+
+__global__ void bep_gather_kernel(const double* __restrict__ U, int ncols, size_t field, const int64_t* __restrict__ gamma,
+                                  int64_t ng, const int64_t* __restrict__ gin, const int32_t* __restrict__ gin_pos,
+                                  int64_t ngin, const double* __restrict__ E, int c0, double* PgE, double* B) {
+  const long tot = (long)(ng + ngin) * ncols;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(t / (ng + ngin));
+    const long r = t - (long)c * (ng + ngin);
+    const double* Uc = U + (size_t)c * field;
+    if (r < ng) {
+      if (PgE) PgE[(size_t)c * ng + r] = Uc[gamma[r]];
+    } else {
+      const long i = r - ng;
+      if (B) B[(size_t)c * ngin + i] = E[(size_t)(c0 + c) * ng + gin_pos[i]] - Uc[gin[i]];
+    }
+  }
+}
+
+// ------------------------------ PKS ------------------------------------------
+
+__device__ __forceinline__ double valat(const double* __restrict__ f, int n, int i, int j, int k) {
+  return interior(n, i, j, k) ? f[flat(n, i, j, k)] : 0.0;
+}
+
+// N+ membership of a lattice point (interior flag; a face ghost is in N+ iff its unique
+// interior neighbour is in M+, R5; anything else is not).
+__device__ __forceinline__ bool nplus_at(const uint8_t* __restrict__ flags, int n, int i, int j, int k) {
+  if (interior(n, i, j, k)) return flags[flat(n, i, j, k)] & F_NPLUS;
+  const int oi = (i < 0) || (i >= n), oj = (j < 0) || (j >= n), ok = (k < 0) || (k >= n);
+  if (oi + oj + ok != 1) return false;
+  const int a = i < 0 ? 0 : (i >= n ? n - 1 : i);
+  const int b = j < 0 ? 0 : (j >= n ? n - 1 : j);
+  const int c = k < 0 ? 0 : (k >= n ? n - 1 : k);
+  if (i < -1 || i > n || j < -1 || j > n || k < -1 || k > n) return false;
+  return flags[flat(n, a, b, c)] & F_MPLUS;
+}
+
+__device__ __forceinline__ double minmod3(double a, double b, double c) {
+  if (a > 0 && b > 0 && c > 0) return fmin(a, fmin(b, c));
+  if (a < 0 && b < 0 && c < 0) return fmax(a, fmax(b, c));
+  return 0.0;
+}
+
+// minmod slope of cell q along axis ax; 0 unless q and both neighbours are in N+ (R15).
+// Ghost cells hold 0, so their slope is 0.
+__device__ __forceinline__ double slope(const double* __restrict__ rho, const uint8_t* __restrict__ flags, int n, int i,
+                                        int j, int k, int ax, double h) {
+  if (!interior(n, i, j, k)) return 0.0;
+  if (!(flags[flat(n, i, j, k)] & F_NPLUS)) return 0.0;
+  const int di = ax == 0, dj = ax == 1, dk = ax == 2;
+  if (!nplus_at(flags, n, i + di, j + dj, k + dk) || !nplus_at(flags, n, i - di, j - dj, k - dk)) return 0.0;
+  const double r0 = rho[flat(n, i, j, k)];
+  const double rp = valat(rho, n, i + di, j + dj, k + dk), rm = valat(rho, n, i - di, j - dj, k - dk);
+  return minmod3(2.0 * (rp - r0) / h, (rp - rm) / (2.0 * h), 2.0 * (r0 - rm) / h);
+}
+
+__device__ __forceinline__ void umax_atomic(double* addr, double v) {
+  // non-negative doubles order like their bit patterns
+  atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void cfl_kernel(const double* __restrict__ c, const uint8_t* __restrict__ flags, int n, double* out3) {
+  __shared__ double red[3][TB / 32];
+  double mx[3] = {0, 0, 0};
+  const long nn = (long)n * n * n;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    if (!(flags[p] & F_MPLUS)) continue;
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    const double c0 = c[p];
+    mx[0] = fmax(mx[0], fmax(fabs(valat(c, n, i + 1, j, k) - c0), fabs(c0 - valat(c, n, i - 1, j, k))));
+    mx[1] = fmax(mx[1], fmax(fabs(valat(c, n, i, j + 1, k) - c0), fabs(c0 - valat(c, n, i, j - 1, k))));
+    mx[2] = fmax(mx[2], fmax(fabs(valat(c, n, i, j, k + 1) - c0), fabs(c0 - valat(c, n, i, j, k - 1))));
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int a = 0; a < 3; ++a) {
+    double v = mx[a];
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[a][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int q = 0; q < TB / 32; ++q) v = fmax(v, red[threadIdx.x][q]);
+    umax_atomic(out3 + threadIdx.x, v);
+  }
+}
+
+// g and the IMEX right-hand sides, written scaled for the ABI operator:
+// fq_rho = (rho - dt g)/dt, fq_c = ((1-dt) c + dt rho)/dt on M+, 0 elsewhere.
+__global__ void flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
+                                const uint8_t* __restrict__ flags, int n, double h, double dt, double chi,
+                                double* __restrict__ fq_rho, double* __restrict__ fq_c) {
+  const long nn = (long)n * n * n;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    if (!(flags[p] & F_MPLUS)) {
+      fq_rho[p] = 0.0;
+      fq_c[p] = 0.0;
+      continue;
+    }
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    const double r0 = rho[p], c0 = c[p];
+    double g = 0.0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int di = ax == 0, dj = ax == 1, dk = ax == 2;
+      const double cE = valat(c, n, i + di, j + dj, k + dk), cW = valat(c, n, i - di, j - dj, k - dk);
+      const double rE = valat(rho, n, i + di, j + dj, k + dk), rW = valat(rho, n, i - di, j - dj, k - dk);
+      const double gE = (cE - c0) / h, gW = (c0 - cW) / h;
+      const double s0 = slope(rho, flags, n, i, j, k, ax, h);
+      const double rhoE = gE > 0 ? r0 + 0.5 * h * s0 : rE - 0.5 * h * slope(rho, flags, n, i + di, j + dj, k + dk, ax, h);
+      const double rhoW = gW > 0 ? rW + 0.5 * h * slope(rho, flags, n, i - di, j - dj, k - dk, ax, h) : r0 - 0.5 * h * s0;
+      g += (chi * rhoE * gE - chi * rhoW * gW) / h;
+    }
+    fq_rho[p] = (r0 - dt * g) / dt;
+    fq_c[p] = ((1.0 - dt) * c0 + dt * r0) / dt;
+  }
+}
+
+// combined Green RHS (R20): q_r = fq_r on M+, (I/dt - Δ_h)[u_γ,r] on the band, 0 elsewhere
+__global__ void green_rhs_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap, int n,
+                                 const double* __restrict__ fq, const double* __restrict__ ug, int64_t ng, double* q,
+                                 int nrhs, double diag, double off) {
+  const long nn = (long)n * n * n;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < nn * nrhs; t += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(t / nn);
+    const long p = t - (long)r * nn;
+    const uint8_t f = flags[p];
+    double v = 0.0;
+    if (f & F_MPLUS) v = fq[t];
+    else if (f & F_BAND) {
+      int i, j, k;
+      ijk(p, n, i, j, k);
+      v = lop_gamma(gmap, ug + (size_t)r * ng, n, i, j, k, diag, off);
+    }
+    q[t] = v;
+  }
+}
+
+// restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite]
+__global__ void restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
+                                double* c, double* stats) {
+  const long nn = (long)n * n * n;
+  double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY;
+  int bad = 0;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    const uint8_t f = flags[p];
+    double a = 0.0, b = 0.0;
+    if (f & F_NPLUS) {
+      a = u[p];
+      b = u[nn + p];
+      if (!isfinite(a) || !isfinite(b)) bad = 1;
+      rmax = fmax(rmax, a);
+      rmin = fmin(rmin, a);
+      cmin = fmin(cmin, b);
+      if (f & F_MPLUS) msum += a;
+    }
+    rho[p] = a;
+    c[p] = b;
+  }
+  __shared__ double red[4][TB / 32];
+  __shared__ int sbad;
+  if (threadIdx.x == 0) sbad = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    msum += __shfl_xor_sync(0xffffffffu, msum, o);
+    rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+    cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+  }
+  if (bad) atomicOr(&sbad, 1);
+  if (lane == 0) { red[0][w] = msum; red[1][w] = rmax; red[2][w] = rmin; red[3][w] = cmin; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0, a = -INFINITY, b = INFINITY, d = INFINITY;
+    for (int q = 0; q < TB / 32; ++q) { s += red[0][q]; a = fmax(a, red[1][q]); b = fmin(b, red[2][q]); d = fmin(d, red[3][q]); }
+    atomicAdd(stats + 0, s);
+    // max via bit patterns on the ordered transform
+    auto key = [](double v) {
+      unsigned long long x = (unsigned long long)__double_as_longlong(v);
+      return (x >> 63) ? ~x : (x | 0x8000000000000000ull);
+    };
+    atomicMax((unsigned long long*)(stats + 1), key(a));
+    atomicMax((unsigned long long*)(stats + 2), key(-b));
+    atomicMax((unsigned long long*)(stats + 3), key(-d));
+    if (sbad) atomicAdd(stats + 4, 1.0);
+  }
+}
+
+__global__ void pks_init_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap,
+                                const double* __restrict__ foot, int n, double lo, double h, dpm_pks_ic ic, double* rho,
+                                double* c) {
+  const long nn = (long)n * n * n;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    const uint8_t f = flags[p];
+    double a = 0.0, b = 0.0;
+    if (f & F_NPLUS) {
+      double x, y, z;
+      const int g = gmap[p];
+      if (g >= 0) { x = foot[3 * g]; y = foot[3 * g + 1]; z = foot[3 * g + 2]; }   // R14
+      else {
+        int i, j, k;
+        ijk(p, n, i, j, k);
+        x = lo + (i + 1) * h; y = lo + (j + 1) * h; z = lo + (k + 1) * h;
+      }
+      const double r2 = (x - ic.center[0]) * (x - ic.center[0]) + (y - ic.center[1]) * (y - ic.center[1]) +
+                        (z - ic.center[2]) * (z - ic.center[2]);
+      a = ic.rho_amp * exp(-ic.rho_rate * r2);
+      b = ic.c_amp * exp(-ic.c_rate * r2);
+    }
+    rho[p] = a;
+    c[p] = b;
+  }
+}
+
+int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
+
+}  // namespace
+
+cudaError_t launch_potential_rhs(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
+                                 cudaStream_t s) {
+  const int n = ctx->n;
+  const size_t field = (size_t)n * n * n;
+  cudaError_t e = cudaMemsetAsync(q, 0, field * nrhs * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  const int64_t nb = ctx->counts[DPM_SET_BAND];
+  const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
+  DPM_COUNT_LAUNCH(1);
+  potential_rhs_kernel<<<grid_for(nb * nrhs), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, q, nrhs, n,
+                                                          diag, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trace(const dpm_ctx* ctx, const double* u, double* out, int which, int64_t batch, cudaStream_t s) {
+  const int n = ctx->n;
+  const int64_t m = ctx->counts[which];
+  if (m * batch == 0) return cudaSuccess;
+  DPM_COUNT_LAUNCH(1);
+  trace_kernel<<<grid_for(m * batch), TB, 0, s>>>(u, ctx->lists[which], m, out, batch, (size_t)n * n * n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int ncols, double* PgE, double* B,
+                              cudaStream_t s) {
+  const int n = ctx->n;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  DPM_COUNT_LAUNCH(1);
+  bep_gather_kernel<<<grid_for((ng + ngin) * ncols), TB, 0, s>>>(U, ncols, (size_t)n * n * n, ctx->lists[DPM_SET_GAMMA], ng,
+                                                                 ctx->lists[DPM_SET_GAMMA_IN], ctx->gin_pos, ngin, ctx->E,
+                                                                 c0, PgE, B);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  DPM_COUNT_LAUNCH(1);
+  pks_init_kernel<<<grid_for(nn), TB, 0, s>>>(ctx->flags, ctx->gmap, ctx->foot, ctx->n, ctx->lo, ctx->h, *ic, rho, c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  DPM_COUNT_LAUNCH(1);
+  cfl_kernel<<<grid_for(nn), TB, 0, s>>>(c, ctx->flags, ctx->n, out3);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi, double* fq_rho,
+                            double* fq_c, cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  DPM_COUNT_LAUNCH(1);
+  flux_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(rho, c, ctx->flags, ctx->n, ctx->h, dt, chi, fq_rho, fq_c);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
+                             cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
+  DPM_COUNT_LAUNCH(1);
+  green_rhs_kernel<<<grid_for(nn * nrhs), TB, 0, s>>>(ctx->flags, ctx->gmap, ctx->n, fq, u_gamma,
+                                                      ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
+                                  cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  cudaError_t e = cudaMemsetAsync(stats, 0, 5 * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  DPM_COUNT_LAUNCH(1);
+  restrict_kernel<<<grid_for(nn), TB, 0, s>>>(ctx->flags, ctx->n, u, rho, c, stats);
+  return cudaGetLastError();
+}

@@ -1,0 +1,205 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative L∞ = max|a-b|/max|b| with
+b = oracle; AP solves, P_γE, B, u_γ <= 1e-11; C <= 1e-10; PKS ρ, c <= 1e-9; dt <= 1e-12;
+point sets bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from dpm_inputs import get_config
+from dpm_inputs.rng import random_boxes, cfg1_particular_values, cfg4_band_values
+from oracle import ap, dpm, grid, pks
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1811_03557_b200 import api as A
+    assert torch.cuda.is_available()
+    return A
+
+
+def ctx_for(api, cfg, dt=None, n=None):
+    c = api.DPM.from_config(cfg)
+    if dt is not None:
+        c.set_dt(dt)
+    return c
+
+
+# ------------------------------------------------------------------ S3 AP solve
+@pytest.mark.parametrize("n", [4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 63, 64, 65, 100, 127, 128])
+def test_aux_solve_parity(api, n):
+    batch = 3 if n <= 64 else 1
+    dt = 1e-3 if n % 2 else 1e-5
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    q = random_boxes(100 + n, batch, n)
+    u = c.aux_solve_batch(torch.from_numpy(q).cuda()).cpu().numpy()
+    uo = ap.solve(q, c.info["h"], dt)
+    assert rel(u, uo) <= 1e-11, rel(u, uo)
+
+
+def test_aux_solve_inplace_chunked_and_empty(api):
+    n = 32
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, 2e-4, "cauchy")
+    # 170 RHS spans more than one L2 chunk (40 MB / 256 KB = 160 fields)
+    q = random_boxes(7, 170, n)
+    t = torch.from_numpy(q).cuda()
+    c.aux_solve_batch(t, t)                              # u aliases q
+    uo = ap.solve(q, c.info["h"], 2e-4)
+    assert rel(t.cpu().numpy(), uo) <= 1e-11
+    e = torch.empty((0, n, n, n), dtype=torch.float64, device="cuda")
+    c.aux_solve_batch(e)
+
+
+def test_aux_solve_host_path(api):
+    n = 24
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, 1e-3, "cauchy")
+    q = random_boxes(8, 5, n)
+    u = c.aux_solve_batch_host(torch.from_numpy(q).clone()).numpy()
+    assert rel(u, ap.solve(q, c.info["h"], 1e-3)) <= 1e-11
+
+
+def test_eigenfunction_on_gpu(api):
+    # closed form: q = (1/dt + λa+λb+λc) S_abc -> u = S_abc
+    n, dt = 128, 1e-5
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    h = c.info["h"]
+    lam = ap.eigenvalues(n, h)
+    j = np.arange(1, n + 1)
+    a, b, cc = 3, 77, 128
+    S = np.einsum("i,j,k->ijk", np.sin(np.pi * a * j / (n + 1)), np.sin(np.pi * b * j / (n + 1)),
+                  np.sin(np.pi * cc * j / (n + 1)))
+    q = (1 / dt + lam[a - 1] + lam[b - 1] + lam[cc - 1]) * S
+    u = c.aux_solve_batch(torch.from_numpy(q[None]).cuda()).cpu().numpy()[0]
+    assert np.abs(u - S).max() < 1e-12
+
+
+# ------------------------------------------------------------------ S1 point sets, geometry, E
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_point_sets_bit_exact(api, name):
+    cfg = get_config(name)
+    c = api.DPM.from_config(cfg)
+    g, ps = grid.point_sets_for(cfg)
+    for w in ["mplus", "gamma", "gamma_in", "gamma_ex", "band", "nplus"]:
+        assert np.array_equal(c.copy_set(w), ps.list(w)), w
+    assert c.info["ghosts_in_nplus"] == ps.ghosts_in_nplus
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_extension_matrix(api, name):
+    cfg = get_config(name)
+    c = api.DPM.from_config(cfg)
+    g, ps = grid.point_sets_for(cfg)
+    E, d, unit, foot = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.basis)
+    Eg, dg = c.copy_extension()
+    assert np.abs(dg - d).max() <= 1e-14
+    assert rel(Eg, E) <= 1e-12
+
+
+# ------------------------------------------------------------------ S2/S4 kernels
+def test_potential_rhs_and_trace(api):
+    cfg = get_config("cfg2")
+    c = api.DPM.from_config(cfg)
+    g, ps = grid.point_sets_for(cfg)
+    ng = len(ps.list("gamma"))
+    v = np.random.default_rng(9).uniform(-1, 1, size=(3, ng))
+    q = c.potential_rhs(torch.from_numpy(v).cuda()).cpu().numpy()
+    qo = np.stack([dpm.potential_rhs(v[r], g, ps, cfg.dt) for r in range(3)])
+    assert rel(q, qo) <= 1e-14
+    u = random_boxes(10, 2, cfg.n)
+    tr = c.trace(torch.from_numpy(u).cuda(), "gamma_in").cpu().numpy()
+    assert np.array_equal(tr, dpm.trace(u, ps.list("gamma_in")))
+
+
+# ------------------------------------------------------------------ cfg1: U, P_γE, B, C
+def test_cfg1_outputs(api):
+    cfg = get_config("cfg1")
+    o = dpm.cfg1_outputs(cfg)
+    c = api.DPM.from_config(cfg)
+    PgE, B = c.build_projection()
+    assert rel(PgE.cpu().numpy().T, o["PgE"]) <= 1e-11
+    assert rel(B.cpu().numpy().T, o["B"]) <= 1e-11
+    # the particular RHS (R22) placed on the CUDA path's own M+ list
+    mp = c.copy_set("mplus")
+    q = np.zeros(cfg.n ** 3)
+    q[mp] = cfg1_particular_values(len(mp))
+    up = c.aux_solve_batch(torch.from_numpy(q.reshape(1, cfg.n, cfg.n, cfg.n)).cuda())
+    assert rel(up.cpu().numpy()[0], o["U"][-1]) <= 1e-11
+    g = c.trace(up, "gamma_in")
+    coef, ug = c.boundary_lsq(g)
+    assert rel(coef.cpu().numpy()[0], o["C"]) <= 1e-10
+    assert rel(ug.cpu().numpy()[0], o["E"] @ o["C"]) <= 1e-11
+    # the 50 basis solves themselves
+    U = c.aux_solve_batch(c.potential_rhs(torch.from_numpy(o["E"].T.copy()).cuda())).cpu().numpy()
+    assert rel(U, o["U"][:-1]) <= 1e-11
+
+
+def test_state_errors(api):
+    from paper_1811_03557_b200._lib import DPMError, DPM_ERR_STATE, DPM_ERR_RANK
+    cfg = get_config("cfg1")
+    c = api.DPM.from_config(cfg)
+    g = torch.zeros((1, c.info["n_gamma_in"]), dtype=torch.float64, device="cuda")
+    with pytest.raises(DPMError) as e:
+        c.boundary_lsq(g)
+    assert e.value.status == DPM_ERR_STATE
+    big = api.DPM(cfg.n, cfg.lo, cfg.hi, cfg.kind, cfg.center, cfg.semi, 20, cfg.dt, "cauchy")   # K=882 > 528
+    with pytest.raises(DPMError) as e:
+        big.build_projection()
+    assert e.value.status == DPM_ERR_RANK
+
+
+# ------------------------------------------------------------------ PKS (cfg2, cfg3)
+def run_pks_gpu(api, cfg, dt_rule=0):
+    c = api.DPM.from_config(cfg)
+    n = cfg.n
+    rho = torch.zeros((n, n, n), dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    rho0 = rho.cpu().numpy().copy()
+    logs = c.pks_step(rho, cc, cfg.steps, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=dt_rule, clamp=1)
+    return rho0, rho.cpu().numpy(), cc.cpu().numpy(), logs
+
+
+@pytest.mark.parametrize("name,dt_rule", [("cfg2", 0), ("cfg2", 1), ("cfg3", 0)])
+def test_pks_parity(api, name, dt_rule):
+    cfg = get_config(name)
+    o = pks.PKSOracle(cfg, dt_rule=dt_rule)
+    r0o, c0o = o.initial_state()
+    rho0, rho, cc, logs = run_pks_gpu(api, cfg, dt_rule)
+    assert rel(rho0, r0o) <= 1e-14
+    ro, co, ologs = o.run()
+    assert rel(rho, ro) <= 1e-9, rel(rho, ro)
+    assert rel(cc, co) <= 1e-9, rel(cc, co)
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
+        assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
+    assert sum(l["rebuilt"] for l in logs) == o.builds
+
+
+# ------------------------------------------------------------------ cfg4 at full size (bench launch config)
+def test_cfg4_full_batch_sampled(api):
+    cfg = get_config("cfg4")
+    c = api.DPM.from_config(cfg)
+    n = cfg.n
+    band = c.copy_set("band")
+    vals = cfg4_band_values(cfg.batch, len(band))
+    q = torch.zeros((cfg.batch, n ** 3), dtype=torch.float64, device="cuda")
+    q[:, torch.from_numpy(band).cuda()] = torch.from_numpy(vals).cuda()
+    q = q.view(cfg.batch, n, n, n)
+    u = c.aux_solve_batch(q)
+    torch.cuda.synchronize()
+    g, ps = grid.point_sets_for(cfg)
+    for b in (0, 289, cfg.batch - 1):
+        qo = dpm.scatter(vals[b], ps.list("band"), n)
+        uo = ap.solve(qo, g.h, cfg.dt)
+        assert rel(u[b].cpu().numpy(), uo) <= 1e-11
+    assert torch.isfinite(u).all()
