@@ -21,6 +21,7 @@ struct DstPlan {
   int n = 0;
   double h = 0, dt = 0;
   double* lam = nullptr;  // device, n eigenvalues λ_m (R26)
+  double* atab = nullptr; // device, per-warp folded sine-matrix DMMA A fragments
 };
 
 struct dpm_ctx {

@@ -13,20 +13,25 @@
 //    odd outputs k = 2m+1 use s (plus the middle sample when n is odd), even outputs
 //    k = 2m+2 use d.  Two ceil(n/2) x ceil(n/2) contractions: n^2/2 MACs per line
 //    instead of n^2.
-//  * Three tile kernels, each a persistent CTA loop over (field, 32-column) tiles that
+//  * Three tile kernels, each a persistent CTA loop over (field, TC-column) tiles that
 //    hold ALL n samples of the transform axis in shared memory:
 //      pass X: transform along x (stride n^2), columns = flat (y,z)
 //      pass Y: transform along y (stride n),   columns = flat (x,z)
 //      pass Z: transform along z (contiguous), divide by D (fused epilogue), inverse z
 //    A solve is X, Y, Z, Y, X (DST-I is an involution up to the folded scale).
-//  * Every warp keeps its sine-matrix fragments in REGISTERS for the whole kernel (computed
-//    once with exact argument reduction), so the MMA loop only loads B fragments from
-//    shared memory; row strides are padded (≡ 4 mod 16 doubles) for conflict-free
-//    fragment loads.
+//  * Tiles stream in with cp.async (16-B LDGSTS, zero-fill for ragged columns) into a
+//    double buffer: the next tile's load overlaps the current tile's DMMA work.
+//  * Every warp keeps its sine-matrix fragments in REGISTERS for the whole kernel (loaded
+//    once from a table built at plan creation with exact argument reduction), so the MMA
+//    loop only loads B fragments from shared memory; row strides are padded
+//    (≡ 4 mod 16 doubles) for conflict-free fragment loads.
+//  * n = 128 (the throughput config) has its own instantiation with every size a
+//    compile-time constant: no predication in the MMA loop.
 //  * The batch is processed in chunks whose working set stays in the 126 MB L2, with the
 //    intermediate living in the output buffer (u may alias q): HBM sees ~one read of q
 //    and one write of u per solve.
 #include <algorithm>
+#include <cstdlib>
 
 #include "dpm_internal.h"
 
@@ -34,16 +39,25 @@ namespace {
 
 constexpr int NW = 8;         // warps per CTA
 constexpr int NT = NW * 32;   // threads per CTA
-constexpr int TC = 32;        // columns per tile
-constexpr int LDX = TC + 4;   // smem row stride (doubles) for passes X/Y (≡ 4 mod 16)
+constexpr int KSMAX_ALL = 16; // k-steps of the largest instance (n <= 128)
 
-__host__ __device__ inline int ldz_of(int n) { return ((n + 15) / 16) * 16 + 4; }
+__host__ __device__ constexpr int ldx_of(int tc) { return tc + 4; }            // ≡ 4 mod 16 for tc % 16 == 0
+__host__ __device__ constexpr int ldz_of(int n) { return ((n + 15) / 16) * 16 + 4; }
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
+
+__device__ __forceinline__ void cp_async16(unsigned smem_addr, const double* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr), "l"(gmem), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async8(unsigned smem_addr, const double* gmem, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_addr), "l"(gmem), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
 // Folded sine-matrix entry. matrix 0: odd outputs k = 2m+1 against s rows j (0-based, j < Po,
 // j == Pe is the middle sample when n is odd, weight sin(pi(2m+1)/2) = (-1)^m).
@@ -68,7 +82,7 @@ struct WarpRole {
   int ct0, ctstep;
 };
 
-__device__ WarpRole warp_role(int warp, int MTh) {
+__host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   WarpRole r;
   r.matrix = warp >> 2;
   const int wl = warp & 3;
@@ -78,7 +92,7 @@ __device__ WarpRole warp_role(int warp, int MTh) {
     r.nmt = (wl + 4 < MTh) ? 2 : 1;
     r.ct0 = 0;
     r.ctstep = 1;
-    r.nct = TC / 8;
+    r.nct = NCT;
   } else {
     const int G = 4 / MTh;
     const int cg = wl / MTh;
@@ -87,57 +101,87 @@ __device__ WarpRole warp_role(int warp, int MTh) {
     r.nmt = (cg < G) ? 1 : 0;
     r.ct0 = cg;
     r.ctstep = G;
-    r.nct = (cg < G) ? (TC / 8 - cg + G - 1) / G : 0;
+    r.nct = (cg < G) ? (NCT - cg + G - 1) / G : 0;
   }
   return r;
 }
 
-// One folded DST-I of every column of the smem tile, in place.
-// Element (row r, col c) lives at sm[r*rs + c*cs].  If DIVIDE, the epilogue multiplies
+// A-fragment table: tab[((warp*2 + t)*KSMAX_ALL + ks)*32 + lane], built once per plan.
+__global__ void afrag_table_kernel(double* tab, int n, int NCT) {
+  const int warp = blockIdx.x, t = blockIdx.y, ks = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Po = (n + 1) / 2, Pe = n / 2, MTh = (Po + 7) / 8, KS = (Po + 3) / 4;
+  const WarpRole role = warp_role(warp, MTh, NCT);
+  double v = 0.0;
+  if (t < role.nmt && ks < KS)
+    v = fold_entry(n, Po, Pe, role.matrix, role.mt[t] * 8 + (lane >> 2), ks * 4 + (lane & 3));
+  tab[((warp * 2 + t) * KSMAX_ALL + ks) * 32 + lane] = v;
+}
+
+// Compile-time geometry when NFIX > 0 (n = NFIX); runtime otherwise.
+template <int NFIX, int TC, int PASS>
+struct Geo {
+  int n, Po, Pe, MTh, KS, rs, cs, tile_elems;
+  __device__ __forceinline__ explicit Geo(int n_rt) {
+    n = NFIX ? NFIX : n_rt;
+    Po = (n + 1) / 2;
+    Pe = n / 2;
+    MTh = (Po + 7) / 8;
+    KS = (Po + 3) / 4;
+    rs = PASS < 2 ? ldx_of(TC) : 1;
+    cs = PASS < 2 ? 1 : ldz_of(n);
+    tile_elems = PASS < 2 ? n * ldx_of(TC) : TC * ldz_of(n);
+  }
+};
+
+extern __shared__ __align__(16) double sm[];
+
+// One folded DST-I of every column of the smem tile at sm[base ...], in place.
+// Element (row r, col c) lives at sm[base + r*rs + c*cs].  If DIVIDE, the epilogue multiplies
 // output (row k, column c) by scale / (((inv_dt + lam[a]) + lam[b]) + lam[k]) with
 // (a, b) = divmod(col0 + c, n) (pass Z after X and Y: spectral indices).
-template <int KSMAX, bool DIVIDE>
-__device__ __forceinline__ void fold_transform(double* sm, int rs, int cs, int n, int Po, int Pe, int KS,
-                                               const WarpRole& role, const double (&afr)[2][KSMAX],
-                                               const double* lam, double inv_dt, double scale, int col0,
-                                               bool rows_fast) {
+template <int NFIX, int KSMAX, int TC, int PASS, bool DIVIDE>
+__device__ __forceinline__ void fold_transform(const Geo<NFIX, TC, PASS>& G, int base, const WarpRole& role,
+                                               const double (&afr)[2][KSMAX], const double* lam, double inv_dt,
+                                               double scale, int col0) {
+  constexpr int NCT = TC / 8;
+  constexpr bool ROWS_FAST = PASS == 2;
+  const int n = G.n, Po = G.Po, Pe = G.Pe, rs = G.rs, cs = G.cs;
   const int tid = threadIdx.x, lane = tid & 31;
   // fold: s_j -> row j, d_j -> row n-1-j (middle row untouched)
   const int nf = Pe * TC;
   for (int idx = tid; idx < nf; idx += NT) {
     int j, c;
-    if (rows_fast) { j = idx % Pe; c = idx / Pe; } else { j = idx / TC; c = idx % TC; }
-    double* pa = sm + j * rs + c * cs;
-    double* pb = sm + (n - 1 - j) * rs + c * cs;
-    const double a = *pa, b = *pb;
-    *pa = a + b;
-    *pb = a - b;
+    if (ROWS_FAST) { j = idx % Pe; c = idx / Pe; } else { j = idx / TC; c = idx % TC; }
+    const int pa = base + j * rs + c * cs;
+    const int pb = base + (n - 1 - j) * rs + c * cs;
+    const double a = sm[pa], b = sm[pb];
+    sm[pa] = a + b;
+    sm[pb] = a - b;
   }
   __syncthreads();
 
-  double acc[2][TC / 8][2];
+  double acc[2][NCT][2];
 #pragma unroll
   for (int t = 0; t < 2; ++t)
 #pragma unroll
-    for (int ct = 0; ct < TC / 8; ++ct) acc[t][ct][0] = acc[t][ct][1] = 0.0;
+    for (int ct = 0; ct < NCT; ++ct) acc[t][ct][0] = acc[t][ct][1] = 0.0;
 
   if (role.nmt > 0) {
+    const int colb = base + ((role.ct0 * 8) + (lane >> 2)) * cs;
+    const int cstep = role.ctstep * 8 * cs;
 #pragma unroll
     for (int ks = 0; ks < KSMAX; ++ks) {
-      if (ks < KS) {
+      if (ks < G.KS) {
         const int j = ks * 4 + (lane & 3);
         const int r = (role.matrix == 0) ? (j < Po ? j : 0) : (j < Pe ? n - 1 - j : 0);
-        const double* rowp = sm + r * rs;
-        double b[TC / 8];
+        const int rowb = colb + r * rs;
+        double b[NCT];
 #pragma unroll
-        for (int ct = 0; ct < TC / 8; ++ct) {
-          b[ct] = 0.0;
-          if (ct < role.nct) b[ct] = rowp[((role.ct0 + ct * role.ctstep) * 8 + (lane >> 2)) * cs];
-        }
+        for (int ct = 0; ct < NCT; ++ct) b[ct] = (ct < role.nct) ? sm[rowb + ct * cstep] : 0.0;
 #pragma unroll
         for (int t = 0; t < 2; ++t)
 #pragma unroll
-          for (int ct = 0; ct < TC / 8; ++ct)
+          for (int ct = 0; ct < NCT; ++ct)
             if (t < role.nmt && ct < role.nct) dmma884(acc[t][ct], afr[t][ks], b[ct]);
       }
     }
@@ -152,21 +196,29 @@ __device__ __forceinline__ void fold_transform(double* sm, int rs, int cs, int n
       const int m = role.mt[t] * 8 + (lane >> 2);
       if (m >= P) continue;
       const int row = role.matrix == 0 ? 2 * m : 2 * m + 1;
+      const double lrow = DIVIDE ? lam[row] : 0.0;
 #pragma unroll
-      for (int ct = 0; ct < TC / 8; ++ct) {
+      for (int ct = 0; ct < NCT; ++ct) {
         if (ct >= role.nct) continue;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int c = (role.ct0 + ct * role.ctstep) * 8 + 2 * (lane & 3) + i;
-          double v = acc[t][ct][i];
-          if (DIVIDE) {
-            const int cg = col0 + c;
-            if (cg < n * n) {
-              const int a = cg / n, bb = cg - a * n;
-              v *= scale / (((inv_dt + lam[a]) + lam[bb]) + lam[row]);
-            }
+        const int c = (role.ct0 + ct * role.ctstep) * 8 + 2 * (lane & 3);
+        double v0 = acc[t][ct][0], v1 = acc[t][ct][1];
+        if (DIVIDE) {
+          const int cg = col0 + c;
+          if (cg < n * n) {
+            const int a = cg / n, bb = cg - a * n;
+            v0 *= scale / (((inv_dt + lam[a]) + lam[bb]) + lrow);
           }
-          sm[row * rs + c * cs] = v;
+          if (cg + 1 < n * n) {
+            const int a = (cg + 1) / n, bb = cg + 1 - a * n;
+            v1 *= scale / (((inv_dt + lam[a]) + lam[bb]) + lrow);
+          }
+        }
+        const int o = base + row * rs + c * cs;
+        if (PASS < 2) {
+          *reinterpret_cast<double2*>(&sm[o]) = make_double2(v0, v1);   // cs == 1, o even
+        } else {
+          sm[o] = v0;
+          sm[o + cs] = v1;
         }
       }
     }
@@ -183,99 +235,179 @@ __device__ __forceinline__ size_t goff(int n, int r, int cg) {
   return (size_t)cg * n + r;
 }
 
-template <int KSMAX, int PASS>
-__global__ void __launch_bounds__(NT, 2)
-dst_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields, int n,
-                const double* __restrict__ lam_g, double inv_dt, double scale) {
-  extern __shared__ double sm[];
-  const int Po = (n + 1) / 2, Pe = n / 2;
-  const int MTh = (Po + 7) / 8;
-  const int KS = (Po + 3) / 4;
-  const int rs = PASS < 2 ? LDX : 1;
-  const int cs = PASS < 2 ? 1 : ldz_of(n);
-  const int tile_elems = PASS < 2 ? n * LDX : TC * ldz_of(n);
-  double* lam = sm + tile_elems;
+// Issue the cp.async loads of one tile (VEC doubles per request; zero-fill ragged columns).
+template <int NFIX, int TC, int PASS, int VEC>
+__device__ __forceinline__ void load_tile(const Geo<NFIX, TC, PASS>& G, int base, const double* src, int col0) {
+  const int n = G.n, nn = n * n;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm) + 8u * (unsigned)base;
+  if (PASS < 2) {
+    constexpr int per_row = TC / VEC;
+    const int ne = n * per_row;
+    for (int idx = threadIdx.x; idx < ne; idx += NT) {
+      const int r = idx / per_row, c = (idx - r * per_row) * VEC;
+      const int cg = col0 + c;
+      const bool ok = cg < nn;
+      const double* g = ok ? src + goff<PASS>(n, r, cg) : src;
+      const unsigned sa = sbase + 8u * (unsigned)(r * G.rs + c * G.cs);
+      if (VEC == 2) cp_async16(sa, g, ok);
+      else cp_async8(sa, g, ok);
+    }
+  } else {
+    const int per_col = n / VEC;
+    const int ne = TC * per_col;
+    for (int idx = threadIdx.x; idx < ne; idx += NT) {
+      const int c = idx / per_col, r = (idx - c * per_col) * VEC;
+      const int cg = col0 + c;
+      const bool ok = cg < nn;
+      const double* g = ok ? src + goff<PASS>(n, r, cg) : src;
+      const unsigned sa = sbase + 8u * (unsigned)(r * G.rs + c * G.cs);
+      if (VEC == 2) cp_async16(sa, g, ok);
+      else cp_async8(sa, g, ok);
+    }
+  }
+}
+
+template <int NFIX, int TC, int PASS, int VEC>
+__device__ __forceinline__ void store_tile(const Geo<NFIX, TC, PASS>& G, int base, double* dst, int col0) {
+  const int n = G.n, nn = n * n;
+  if (PASS < 2) {
+    constexpr int per_row = TC / VEC;
+    const int ne = n * per_row;
+    for (int idx = threadIdx.x; idx < ne; idx += NT) {
+      const int r = idx / per_row, c = (idx - r * per_row) * VEC;
+      const int cg = col0 + c;
+      if (cg >= nn) continue;
+      const int o = base + r * G.rs + c * G.cs;
+      if (VEC == 2) __stcg(reinterpret_cast<double2*>(dst + goff<PASS>(n, r, cg)), *reinterpret_cast<const double2*>(&sm[o]));
+      else __stcg(dst + goff<PASS>(n, r, cg), sm[o]);
+    }
+  } else {
+    const int per_col = n / VEC;
+    const int ne = TC * per_col;
+    for (int idx = threadIdx.x; idx < ne; idx += NT) {
+      const int c = idx / per_col, r = (idx - c * per_col) * VEC;
+      const int cg = col0 + c;
+      if (cg >= nn) continue;
+      const int o = base + r * G.rs + c * G.cs;
+      if (VEC == 2) __stcg(reinterpret_cast<double2*>(dst + goff<PASS>(n, r, cg)), *reinterpret_cast<const double2*>(&sm[o]));
+      else __stcg(dst + goff<PASS>(n, r, cg), sm[o]);
+    }
+  }
+}
+
+template <int KSMAX, int TC>
+constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) ? 1 : 2; }
+
+template <int NFIX, int KSMAX, int TC, int PASS, int VEC>
+__global__ void __launch_bounds__(NT, min_blocks<KSMAX, TC>())
+dst_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields, int n_rt,
+                const double* __restrict__ lam_g, const double* __restrict__ atab, double inv_dt, double scale) {
+  const Geo<NFIX, TC, PASS> G(n_rt);
+  const int n = G.n;
+  double* lam = sm + 2 * G.tile_elems;
   if (PASS == 2)
     for (int i = threadIdx.x; i < n; i += NT) lam[i] = lam_g[i];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const WarpRole role = warp_role(warp, MTh);
+  const WarpRole role = warp_role(warp, G.MTh, TC / 8);
   double afr[2][KSMAX];
 #pragma unroll
   for (int t = 0; t < 2; ++t)
 #pragma unroll
-    for (int ks = 0; ks < KSMAX; ++ks)
-      afr[t][ks] = (t < role.nmt && ks < KS)
-                       ? fold_entry(n, Po, Pe, role.matrix, role.mt[t] * 8 + (lane >> 2), ks * 4 + (lane & 3))
-                       : 0.0;
+    for (int ks = 0; ks < KSMAX; ++ks) afr[t][ks] = __ldg(atab + ((warp * 2 + t) * KSMAX_ALL + ks) * 32 + lane);
 
   const int nn = n * n;
   const int tiles_per_field = (nn + TC - 1) / TC;
   const long ntiles = (long)nfields * tiles_per_field;
   const size_t field = (size_t)nn * n;
-  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  long tile = blockIdx.x;
+  if (tile < ntiles) {
+    const int f = (int)(tile / tiles_per_field);
+    load_tile<NFIX, TC, PASS, VEC>(G, 0, in + (size_t)f * field, (int)(tile - (long)f * tiles_per_field) * TC);
+  }
+  cp_async_commit();
+  int cur = 0;
+  for (; tile < ntiles; tile += gridDim.x, cur ^= 1) {
+    const long nxt = tile + gridDim.x;
+    if (nxt < ntiles) {
+      const int f = (int)(nxt / tiles_per_field);
+      load_tile<NFIX, TC, PASS, VEC>(G, (cur ^ 1) * G.tile_elems, in + (size_t)f * field,
+                                     (int)(nxt - (long)f * tiles_per_field) * TC);
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
     const int f = (int)(tile / tiles_per_field);
     const int col0 = (int)(tile - (long)f * tiles_per_field) * TC;
-    const double* src = in + (size_t)f * field;
-    double* dst = out + (size_t)f * field;
-    // load (zero-fill ragged columns)
-    const int ne = n * TC;
-    for (int idx = threadIdx.x; idx < ne; idx += NT) {
-      int r, c;
-      if (PASS == 2) { r = idx % n; c = idx / n; } else { r = idx / TC; c = idx % TC; }
-      const int cg = col0 + c;
-      sm[r * rs + c * cs] = (cg < nn) ? __ldcg(src + goff<PASS>(n, r, cg)) : 0.0;
-    }
-    __syncthreads();
-    fold_transform<KSMAX, PASS == 2>(sm, rs, cs, n, Po, Pe, KS, role, afr, lam, inv_dt, scale, col0,
-                                     PASS == 2);
-    if (PASS == 2)
-      fold_transform<KSMAX, false>(sm, rs, cs, n, Po, Pe, KS, role, afr, lam, inv_dt, scale, col0, true);
-    for (int idx = threadIdx.x; idx < ne; idx += NT) {
-      int r, c;
-      if (PASS == 2) { r = idx % n; c = idx / n; } else { r = idx / TC; c = idx % TC; }
-      const int cg = col0 + c;
-      if (cg < nn) __stcg(dst + goff<PASS>(n, r, cg), sm[r * rs + c * cs]);
-    }
+    const int base = cur * G.tile_elems;
+    fold_transform<NFIX, KSMAX, TC, PASS, PASS == 2>(G, base, role, afr, lam, inv_dt, scale, col0);
+    if (PASS == 2) fold_transform<NFIX, KSMAX, TC, PASS, false>(G, base, role, afr, lam, inv_dt, scale, col0);
+    store_tile<NFIX, TC, PASS, VEC>(G, base, out + (size_t)f * field, col0);
     __syncthreads();
   }
 }
 
-template <int KSMAX>
-struct PassSet {
-  static cudaError_t run(int pass, const double* in, double* out, int nfields, int n, const double* lam,
-                         double inv_dt, double scale, cudaStream_t s) {
-    const size_t smem = (size_t)(pass < 2 ? n * LDX : TC * ldz_of(n)) * 8 + (size_t)n * 8;
-    void (*k)(const double*, double*, int, int, const double*, double, double) =
-        pass == 0 ? dst_pass_kernel<KSMAX, 0> : pass == 1 ? dst_pass_kernel<KSMAX, 1> : dst_pass_kernel<KSMAX, 2>;
-    static int occ[3] = {0, 0, 0};
-    static int sms = 0;
-    if (!sms) {
-      int dev;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (!occ[pass]) {
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pass], k, NT, smem);
-      if (e != cudaSuccess) return e;
-      if (occ[pass] < 1) occ[pass] = 1;
-    }
-    const long ntiles = (long)nfields * ((n * n + TC - 1) / TC);
-    const int grid = (int)std::min<long>(ntiles, (long)sms * occ[pass]);
-    DPM_COUNT_LAUNCH(1);
-    k<<<grid, NT, smem, s>>>(in, out, nfields, n, lam, inv_dt, scale);
-    return cudaGetLastError();
+template <int NFIX, int KSMAX, int TC, int VEC>
+cudaError_t run_pass_t(int pass, const double* in, double* out, int nfields, int n, const double* lam,
+                       const double* atab, double inv_dt, double scale, cudaStream_t s) {
+  const size_t tile = (size_t)(pass < 2 ? n * ldx_of(TC) : TC * ldz_of(n));
+  const size_t smem = 2 * tile * 8 + (size_t)n * 8;
+  void (*k)(const double*, double*, int, int, const double*, const double*, double, double) =
+      pass == 0 ? dst_pass_kernel<NFIX, KSMAX, TC, 0, VEC>
+                : pass == 1 ? dst_pass_kernel<NFIX, KSMAX, TC, 1, VEC> : dst_pass_kernel<NFIX, KSMAX, TC, 2, VEC>;
+  static int sms = 0;
+  static int occ[3] = {0, 0, 0};
+  static size_t occ_smem[3] = {0, 0, 0};
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-};
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (!occ[pass] || occ_smem[pass] != smem) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[pass], k, NT, smem);
+    if (e != cudaSuccess) return e;
+    if (occ[pass] < 1) occ[pass] = 1;
+    occ_smem[pass] = smem;
+  }
+  const long ntiles = (long)nfields * ((n * n + TC - 1) / TC);
+  const int grid = (int)std::min<long>(ntiles, (long)sms * occ[pass]);
+  DPM_COUNT_LAUNCH(1);
+  k<<<grid, NT, smem, s>>>(in, out, nfields, n, lam, atab, inv_dt, scale);
+  return cudaGetLastError();
+}
 
-cudaError_t run_pass(int pass, const double* in, double* out, int nfields, int n, const double* lam, double inv_dt,
+// Column-tile width of the n = 128 instance (DPM_TC128 = 32 | 64 selects; default below).
+int tc128() {
+  static int v = [] {
+    const char* e = getenv("DPM_TC128");
+    return (e && atoi(e) == 64) ? 64 : 32;   // 32: 2 CTAs/SM, 61% of DMMA peak vs 53% for 64 (profiles/)
+  }();
+  return v;
+}
+
+int tc_for(int n) { return n == 128 ? tc128() : (n > 64 ? 64 : 32); }
+
+cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, int nfields, double inv_dt,
                      double scale, cudaStream_t s) {
+  const int n = p.n;
   const int Po = (n + 1) / 2, KS = (Po + 3) / 4;
-  if (KS <= 4) return PassSet<4>::run(pass, in, out, nfields, n, lam, inv_dt, scale, s);
-  if (KS <= 8) return PassSet<8>::run(pass, in, out, nfields, n, lam, inv_dt, scale, s);
-  return PassSet<16>::run(pass, in, out, nfields, n, lam, inv_dt, scale, s);
+  const bool even = (n % 2) == 0;
+  if (n == 128) {
+    if (tc128() == 32) return run_pass_t<128, 16, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
+    return run_pass_t<128, 16, 64, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
+  }
+  if (KS <= 4) {
+    return even ? run_pass_t<0, 4, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
+                : run_pass_t<0, 4, 32, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
+  }
+  if (KS <= 8) {
+    return even ? run_pass_t<0, 8, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
+                : run_pass_t<0, 8, 32, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
+  }
+  return even ? run_pass_t<0, 16, 64, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
+              : run_pass_t<0, 16, 64, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
 }
 
 __global__ void eig_kernel(double* lam, int n, double h) {
@@ -294,8 +426,11 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
   p.dt = dt;
   cudaError_t e = cudaMalloc(&p.lam, sizeof(double) * n);
   if (e != cudaSuccess) return e;
-  DPM_COUNT_LAUNCH(1);
+  e = cudaMalloc(&p.atab, sizeof(double) * NW * 2 * KSMAX_ALL * 32);
+  if (e != cudaSuccess) return e;
+  DPM_COUNT_LAUNCH(2);
   eig_kernel<<<(n + 127) / 128, 128>>>(p.lam, n, h);
+  afrag_table_kernel<<<dim3(NW, 2), KSMAX_ALL * 32>>>(p.atab, n, tc_for(n) / 8);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return cudaDeviceSynchronize();
@@ -303,7 +438,9 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
 
 void dst_plan_free(DstPlan& p) {
   if (p.lam) cudaFree(p.lam);
+  if (p.atab) cudaFree(p.atab);
   p.lam = nullptr;
+  p.atab = nullptr;
 }
 
 size_t dst_scratch_bytes(int, int) { return 0; }
@@ -312,8 +449,8 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
                             cudaStream_t s) {
   const int n = p.n;
   const size_t field_bytes = (size_t)n * n * n * 8;
-  // chunk so that the in-flight working set (~2 chunks) stays in L2
-  const size_t budget = (size_t)40 << 20;
+  // chunk so that the in-flight working set stays in the 126 MB L2
+  const size_t budget = (size_t)64 << 20;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(budget / field_bytes));
   const double inv_dt = 1.0 / p.dt;
   const double sc = 2.0 / (n + 1);
@@ -324,11 +461,11 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     const double* qi = q + b0 * fe;
     double* ui = u + b0 * fe;
     cudaError_t e;
-    if ((e = run_pass(0, qi, ui, nf, n, p.lam, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(1, ui, ui, nf, n, p.lam, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(2, ui, ui, nf, n, p.lam, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(1, ui, ui, nf, n, p.lam, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(0, ui, ui, nf, n, p.lam, inv_dt, scale, s)) != cudaSuccess) return e;
+    if ((e = run_pass(p, 0, qi, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    if ((e = run_pass(p, 1, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    if ((e = run_pass(p, 2, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    if ((e = run_pass(p, 1, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    if ((e = run_pass(p, 0, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
