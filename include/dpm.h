@@ -71,6 +71,7 @@ typedef struct {
   int64_t ghosts_in_nplus;   /* ghost nodes belonging to N+ (R5; 72 at cfg1)              */
   int32_t have_projection;   /* 1 once dpm_build_projection succeeded at the current dt    */
   double bep_cond_est;       /* κ(R) of the column-equilibrated BEP (diag ratio estimate)  */
+  int32_t solver;            /* dpm_solver in use                                          */
 } dpm_info;
 
 typedef struct dpm_ctx dpm_ctx;
@@ -106,6 +107,15 @@ dpm_status dpm_set_dt(dpm_ctx* ctx, double dt);
  * Asynchronous on `stream`.
  * ------------------------------------------------------------------------------- */
 dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t batch, void* stream);
+
+/* AP solver variant (both give the same u up to rounding):
+ *  DPM_SOLVER_DST3          DST-I along x, y and z, eigenvalue divide, inverse along z, y, x.
+ *  DPM_SOLVER_DST2_TRIDIAG  DST-I along x and y; each (a,b) line along z solves the tridiagonal
+ *                           (1/dt + λ_a + λ_b - D_zz) v = r exactly (constant-coefficient
+ *                           factorisation + Sherman-Morrison boundary term); inverse y, x.
+ *                           Two fewer transforms per solve.  Default. */
+typedef enum { DPM_SOLVER_DST3 = 0, DPM_SOLVER_DST2_TRIDIAG = 1 } dpm_solver;
+dpm_status dpm_set_solver(dpm_ctx* ctx, int32_t solver);
 
 /* Same operation through HOST buffers (pinned or pageable): H2D copy, solve, D2H copy,
    chunked through ctx-owned device staging. Synchronizes `stream` before returning. */

@@ -18,6 +18,8 @@ STATUS = {0: "DPM_OK", 1: "DPM_ERR_INVALID", 2: "DPM_ERR_OOM", 3: "DPM_ERR_CUDA"
           5: "DPM_ERR_RANK", 6: "DPM_ERR_NONFINITE"}
 SPHERE, ELLIPSOID = 0, 1
 BASIS_CAUCHY, BASIS_NEUMANN0 = 0, 1
+SOLVER_DST3, SOLVER_DST2_TRIDIAG = 0, 1
+SOLVERS = {"dst3": SOLVER_DST3, "dst2_tridiag": SOLVER_DST2_TRIDIAG}
 SETS = {"mplus": 0, "gamma": 1, "gamma_in": 2, "gamma_ex": 3, "band": 4, "nplus": 5}
 MAX_N = 128
 
@@ -35,7 +37,8 @@ class Info(C.Structure):
                 ("h", C.c_double), ("dt", C.c_double),
                 ("n_mplus", C.c_int64), ("n_gamma", C.c_int64), ("n_gamma_in", C.c_int64),
                 ("n_gamma_ex", C.c_int64), ("n_band", C.c_int64), ("n_nplus", C.c_int64),
-                ("ghosts_in_nplus", C.c_int64), ("have_projection", C.c_int32), ("bep_cond_est", C.c_double)]
+                ("ghosts_in_nplus", C.c_int64), ("have_projection", C.c_int32), ("bep_cond_est", C.c_double),
+                ("solver", C.c_int32)]
 
 
 class PksIC(C.Structure):
@@ -64,6 +67,7 @@ _sig = {
     "dpm_copy_extension": ([P, D, D], C.c_int),
     "dpm_set_dt": ([P, C.c_double], C.c_int),
     "dpm_aux_solve_batch": ([P, P, P, C.c_int64, P], C.c_int),
+    "dpm_set_solver": ([P, C.c_int32], C.c_int),
     "dpm_aux_solve_batch_host": ([P, P, P, C.c_int64, P], C.c_int),
     "dpm_potential_rhs": ([P, P, P, C.c_int32, P], C.c_int),
     "dpm_trace": ([P, P, P, C.c_int32, C.c_int64, P], C.c_int),

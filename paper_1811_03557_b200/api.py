@@ -83,6 +83,11 @@ class DPM:
     def set_dt(self, dt: float):
         self._chk(L.lib.dpm_set_dt(self._h, dt))
 
+    def set_solver(self, solver: str):
+        """"dst3" (3D DST-I) or "dst2_tridiag" (DST-I in x, y + exact tridiagonal solve in z)."""
+        self._chk(L.lib.dpm_set_solver(self._h, L.SOLVERS[solver]))
+        self.info = self.query()
+
     def aux_solve_batch(self, q: torch.Tensor, u: torch.Tensor = None, stream=None) -> torch.Tensor:
         _dev_f64(q, "q")
         if u is None:

@@ -124,6 +124,13 @@ dpm_status dpm_query(const dpm_ctx* ctx, dpm_info* out) {
   out->ghosts_in_nplus = ctx->ghosts_in_nplus;
   out->have_projection = ctx->have_projection;
   out->bep_cond_est = ctx->bep_cond;
+  out->solver = ctx->plan.solver;
+  return DPM_OK;
+}
+
+dpm_status dpm_set_solver(dpm_ctx* ctx, int32_t solver) {
+  if (!ctx || (solver != DPM_SOLVER_DST3 && solver != DPM_SOLVER_DST2_TRIDIAG)) return DPM_ERR_INVALID;
+  ctx->plan.solver = solver;
   return DPM_OK;
 }
 

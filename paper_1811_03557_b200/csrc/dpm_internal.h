@@ -22,6 +22,7 @@ struct DstPlan {
   double h = 0, dt = 0;
   double* lam = nullptr;  // device, n eigenvalues λ_m (R26)
   double* atab = nullptr; // device, per-warp folded sine-matrix DMMA A fragments
+  int solver = DPM_SOLVER_DST2_TRIDIAG;
 };
 
 struct dpm_ctx {

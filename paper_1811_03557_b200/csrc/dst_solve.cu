@@ -410,6 +410,125 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
               : run_pass_t<0, 16, 64, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Partial diagonalisation (DPM_SOLVER_DST2_TRIDIAG): after DST-I along x and y, every (a, b)
+// line along z solves  (σ_ab - D_zz) v = r  with σ_ab = 1/dt + λ_a + λ_b and zero Dirichlet ends.
+// h^2-scaled: T v = h^2 r, T = tridiag(-1, β, -1), β = 2 + h^2 σ_ab = μ + 1/μ, 0 < μ < 1.
+// Exact identity: T = A + μ e1 e1^T with A = μ^{-1} (I - μL)(I - μU) (L/U = sub/super shift), so
+//   A^{-1} r = μ z,  z = (I - μU)^{-1} (I - μL)^{-1} r   (two constant-coefficient recurrences)
+//   T^{-1} r = μ z - s · μ (μ z_0) / (1 + μ s_0),   s_k = (μ^{k+1} - μ^{2n+1-k}) / (1 - μ^2)
+// (Sherman-Morrison; s = A^{-1} e1 in closed form).  No division per element, no pivot table.
+// Tile: TL = 32 lines x n; lane = line, warp = one of 8 z-segments; each recurrence is a
+// segmented scan (local sweep, carry exchange through shared memory, geometric fix-up).
+constexpr int TL = 32;
+
+template <int NFIX>
+__global__ void __launch_bounds__(NT)
+ztri_kernel(double* __restrict__ u, long nlines, int n_rt, const double* __restrict__ lam_g, double inv_dt,
+            double h2, double rscale) {
+  extern __shared__ __align__(16) double zs[];
+  const int n = NFIX ? NFIX : n_rt;
+  const int LDT = n + 1;                    // odd stride: per-thread rows are bank-conflict free
+  double* tile = zs;
+  double* carry = zs + TL * LDT;            // [8][TL]
+  double* lam = carry + 8 * TL;
+  for (int i = threadIdx.x; i < n; i += NT) lam[i] = lam_g[i];
+  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int SEG = (n + 7) / 8;
+  const int k0 = min(n, s * SEG), k1 = min(n, k0 + SEG);
+  const int nn = n * n;
+  __syncthreads();
+  for (long l0 = (long)blockIdx.x * TL; l0 < nlines; l0 += (long)gridDim.x * TL) {
+    const int nl = (int)min((long)TL, nlines - l0);
+    const double* src = u + l0 * n;
+    for (int e = threadIdx.x; e < nl * n; e += NT) {
+      const int li = e / n;
+      tile[li * LDT + (e - li * n)] = __ldcg(src + e);
+    }
+    __syncthreads();
+    const bool valid = lane < nl;
+    double* row = tile + lane * LDT;
+    const int lf = (int)((l0 + lane) % nn);
+    const double hs = h2 * ((inv_dt + lam[lf / n]) + lam[lf % n]);
+    const double disc = sqrt(hs * (hs + 4.0));
+    const double beta = 2.0 + hs;
+    const double mu = 2.0 / (beta + disc);
+    const double muinv = 0.5 * (beta + disc);
+    const double one_m_mu2 = ((hs + disc) / (beta + disc)) * (1.0 + mu);   // 1 - μ^2 without cancellation
+    double muS = 1.0;
+    for (int i = 0; i < SEG; ++i) muS *= mu;
+    // forward: y_k = r_k + μ y_{k-1}
+    double y = 0.0;
+    if (valid)
+      for (int k = k0; k < k1; ++k) { y = fma(mu, y, rscale * row[k]); row[k] = y; }
+    carry[s * TL + lane] = y;
+    __syncthreads();
+    double Y = 0.0;
+    for (int t = 0; t < s; ++t) Y = fma(muS, Y, carry[t * TL + lane]);
+    double p = mu * Y;
+    if (valid)
+      for (int k = k0; k < k1; ++k) { row[k] += p; p *= mu; }
+    __syncthreads();
+    // backward: z_k = y_k + μ z_{k+1}
+    double z = 0.0;
+    if (valid)
+      for (int k = k1 - 1; k >= k0; --k) { z = fma(mu, z, row[k]); row[k] = z; }
+    carry[s * TL + lane] = z;
+    __syncthreads();
+    double Z = 0.0;
+    // segments after s are full (length SEG) except possibly the last non-empty one, whose
+    // incoming Z is 0, and empty ones, whose carry and incoming Z are 0: μ^SEG is exact here.
+    for (int t = 7; t > s; --t) Z = fma(muS, Z, carry[t * TL + lane]);
+    p = mu * Z;
+    if (valid)
+      for (int k = k1 - 1; k >= k0; --k) { row[k] += p; p *= mu; }
+    __syncthreads();
+    // Sherman-Morrison boundary correction
+    if (valid && k1 > k0) {
+      const double z0 = row[0];
+      const double inv = 1.0 / one_m_mu2;
+      const double s0 = (mu - pow(mu, 2.0 * n + 1.0)) * inv;
+      const double coef = mu * (mu * z0) / (1.0 + mu * s0);
+      double pA = pow(mu, (double)k1), pB = pow(mu, (double)(2 * n + 2 - k1));
+      for (int k = k1 - 1; k >= k0; --k) {
+        row[k] = mu * row[k] - coef * ((pA - pB) * inv);
+        pA *= muinv;
+        pB *= mu;
+      }
+    }
+    __syncthreads();
+    double* dst = u + l0 * n;
+    for (int e = threadIdx.x; e < nl * n; e += NT) {
+      const int li = e / n;
+      __stcg(dst + e, tile[li * LDT + (e - li * n)]);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
+  const int n = p.n;
+  const size_t smem = (size_t)(TL * (n + 1) + 8 * TL + n) * 8;
+  const long nlines = (long)nfields * n * n;
+  void (*k)(double*, long, int, const double*, double, double, double) = n == 128 ? ztri_kernel<128> : ztri_kernel<0>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
+  const long tiles = (nlines + TL - 1) / TL;
+  const int grid = (int)std::min<long>(tiles, (long)sms * std::max(1, occ));
+  const double sc = 2.0 / (n + 1);
+  DPM_COUNT_LAUNCH(1);
+  k<<<grid, NT, smem, s>>>(u, nlines, n, p.lam, 1.0 / p.dt, p.h * p.h, sc * sc * p.h * p.h);
+  return cudaGetLastError();
+}
+
 __global__ void eig_kernel(double* lam, int n, double h) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x + 1;
   if (m <= n) {
@@ -463,7 +582,11 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     cudaError_t e;
     if ((e = run_pass(p, 0, qi, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
     if ((e = run_pass(p, 1, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(p, 2, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    if (p.solver == DPM_SOLVER_DST2_TRIDIAG) {
+      if ((e = run_ztri(p, ui, nf, s)) != cudaSuccess) return e;
+    } else if ((e = run_pass(p, 2, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) {
+      return e;
+    }
     if ((e = run_pass(p, 1, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
     if ((e = run_pass(p, 0, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
   }

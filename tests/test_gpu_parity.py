@@ -36,15 +36,28 @@ def ctx_for(api, cfg, dt=None, n=None):
 
 
 # ------------------------------------------------------------------ S3 AP solve
+@pytest.mark.parametrize("solver", ["dst3", "dst2_tridiag"])
 @pytest.mark.parametrize("n", [4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 63, 64, 65, 100, 127, 128])
-def test_aux_solve_parity(api, n):
+def test_aux_solve_parity(api, n, solver):
     batch = 3 if n <= 64 else 1
     dt = 1e-3 if n % 2 else 1e-5
     c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    c.set_solver(solver)
     q = random_boxes(100 + n, batch, n)
     u = c.aux_solve_batch(torch.from_numpy(q).cuda()).cpu().numpy()
     uo = ap.solve(q, c.info["h"], dt)
     assert rel(u, uo) <= 1e-11, rel(u, uo)
+
+
+@pytest.mark.parametrize("solver", ["dst3", "dst2_tridiag"])
+@pytest.mark.parametrize("n,dt", [(128, 1.0), (33, 10.0), (64, 0.5 * (2.2 / 65) ** 2)])
+def test_aux_solve_parity_large_dt(api, n, dt, solver):
+    # large dt: the z operator approaches the pure Laplacian (μ -> 1 in the tridiagonal solver)
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    c.set_solver(solver)
+    q = random_boxes(7 + n, 1, n)
+    u = c.aux_solve_batch(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel(u, ap.solve(q, c.info["h"], dt)) <= 1e-11
 
 
 def test_aux_solve_inplace_chunked_and_empty(api):
