@@ -1,0 +1,11 @@
+# Full check on one B200: GPU tests, smoke, default bench, ncu launch list of the bench command.
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests_rc=$?
+tail -5 gpurun_out/gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
+tail -3 gpurun_out/smoke.log
+python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo bench_rc=$?
+cat gpurun_out/bench.log; tail -5 gpurun_out/bench.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-pks > gpurun_out/ncu_launch.log 2>&1; echo ncu_rc=$?
