@@ -23,6 +23,8 @@ struct DstPlan {
   double* lam = nullptr;  // device, n eigenvalues λ_m (R26)
   double* atab = nullptr; // device, per-warp folded sine-matrix DMMA A fragments
   int solver = DPM_SOLVER_DST2_TRIDIAG;
+  double* atab128 = nullptr;  // n = 128: A fragments of the prime-factor DST-I
+  int pfa = 1;            // n = 128: prime-factor DST-I for the x / y passes (DPM_PFA=0 disables)
 };
 
 struct dpm_ctx {
@@ -93,6 +95,11 @@ void dst_plan_free(DstPlan& p);
 cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_t batch, double* scratch,
                             size_t scratch_bytes, cudaStream_t s);
 size_t dst_scratch_bytes(int n, int chunk);
+
+// dst128.cu (n = 128 prime-factor DST-I passes)
+cudaError_t dst128_init();
+cudaError_t dst128_atab(double** tab);
+cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, const double* atab, cudaStream_t s);
 
 // setup.cu
 dpm_status setup_point_sets(dpm_ctx* ctx);

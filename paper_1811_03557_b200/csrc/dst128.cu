@@ -1,0 +1,537 @@
+// S3 at n = 128 — prime-factor (Good–Thomas) DST-I pass on the fp64 tensor pipe (DMMA).
+//
+// X_k = Σ_{j=1}^{128} x_j sin(π j k / 129)  (the DST-I of the fast Poisson solver)
+// is -½ Im of the length-258 DFT of the odd extension x̃ (x̃_0 = x̃_129 = 0, x̃_{258-j} = -x_j).
+// 258 = 2·3·43 with coprime factors, so with the input map j = CRT(j1, j2, j3) (j ≡ j1 mod 2,
+// j ≡ j2 mod 3, j ≡ j3 mod 43) and the output map k = (129 k1 + 86 k2 + 6 k3) mod 258 the DFT
+// becomes a 2 x 3 x 43 three-dimensional DFT with no twiddle factors:
+//   z[j1][j2][j3] = x̃[CRT(j1,j2,j3)],   odd symmetry  z[j1][-j2][-j3] = -z[j1][j2][j3].
+// Length-43 stage, per j1 (w(j3) = z[j1][1][j3]):
+//   σ(k3) = Σ_{j3=1}^{21} z[j1][0][j3] sin(2π j3 k3/43)                       (odd in k3)
+//   A(k3) = w(0) + Σ_{j3=1}^{21} (w(j3) + w(43-j3)) cos(2π j3 k3/43)           (even)
+//   B(k3) = Σ_{j3=1}^{21} (w(j3) - w(43-j3)) sin(2π j3 k3/43)                  (odd)
+// 3- and 2-point stages (closed form, all purely imaginary):
+//   τ(k2=0)/2 = σ + B,   τ(1)/2 = (σ - B/2) + (√3/2) A,   τ(2)/2 = (σ - B/2) - (√3/2) A
+//   X_k = τ_{j1=0}/2 + (-1)^{k1} τ_{j1=1}/2.
+// Work per line: 4 sine (21x21) and 2 cosine (22x22) contractions padded to 24x24 for DMMA.m8n8k4:
+// 3456 MACs per 128 outputs (27 MAC/point) instead of 8192 for the folded dense matrix.
+//
+// Kernel: persistent CTAs over tiles of 32 columns x all 128 rows of the transform axis (PASS 0:
+// x, stride n^2, columns = flat (y,z); PASS 1: y, stride n, columns = flat (x,z)).  Tiles stream in
+// with cp.async into a double buffer whose rows are the PERMUTED slots of the CRT map (so every
+// B fragment reads 4 consecutive slots: bank-conflict free with the ≡4 (mod 16) row pitch); the
+// odd-extension signs are applied to B fragments with a sign-bit XOR.  12 warps per CTA: warp =
+// (8-column n-tile, 8-row m-tile of k3); each runs the 6 products as 6 independent DMMA chains
+// (~80 registers, so 2 CTAs = 24 warps per SM hide the LDS -> DMMA latency).  The length-43
+// results are staged in the consumed tile and a warp-uniform butterfly (lane = column, k3 and
+// every output index compile-time) writes coalesced 256-byte rows straight to global memory.
+#include <algorithm>
+#include <cstdlib>
+#include <cmath>
+#include <cstdint>
+#include <utility>
+
+#include "dpm_internal.h"
+
+namespace {
+
+constexpr int N = 128, NN = N * N;
+constexpr int TC = 32;              // columns per tile
+constexpr int NTILE_N = TC / 8;     // 8-column n-tiles per tile
+constexpr int NWARP = 3 * NTILE_N;  // warp = (n-tile, m-tile)
+constexpr int NTHR = NWARP * 32;
+constexpr int LD = TC + 4;          // row pitch (doubles), ≡ 4 mod 16
+// slot layout (130 rows): W0 | U0 | W1 | U1 | 2 zero rows.  Entry e (0..23) of the U blocks is slot
+// UB + e with data at e = 1..21; the neighbours read at e = 0, 22, 23 are finite data or zero rows
+// and meet zero columns of S.  W blocks hold w(0..42) at WB + j3.
+constexpr int W0B = 0, U0B = 42, W1B = 64, U1B = 106, NSLOT = 130;
+constexpr int TILE = NSLOT * LD;    // doubles per buffer
+constexpr int ATAB = 2 * 3 * 6 * 32;  // A-fragment table entries (S and C', 3 m-tiles, 6 k-steps, 32 lanes)
+// staging rows (after the MMAs, inside the consumed buffer): σ0, σ1, B0, B1 at k3 = 1..21 and
+// A0, A1 at k3 = 0..21 -> 128 rows, so the two zero rows (128, 129) are never overwritten.
+constexpr int RS0 = 0, RS1 = 21, RB0 = 42, RB1 = 63, RA0 = 84, RA1 = 106;
+
+__constant__ uint8_t c_slot[N];     // slot of transform-axis row r (0-based; x_{r+1})
+__constant__ uint32_t c_usign[2];   // bit e: U block j1, entry e is -x (odd extension)
+__constant__ uint64_t c_wsign[2];   // bit j3: W block j1, entry j3 is -x
+
+struct Tables {
+  uint8_t slot[N];
+  uint32_t usign[2];
+  uint64_t wsign[2];
+};
+
+// CRT of (j mod 2, j mod 3, j mod 43) -> j in [0, 258)
+int crt258(int j1, int j2, int j3) {
+  for (int j = 0; j < 258; ++j)
+    if (j % 2 == j1 && j % 3 == j2 && j % 43 == j3) return j;
+  return -1;
+}
+
+Tables make_tables() {
+  Tables t{};
+  for (int r = 0; r < N; ++r) t.slot[r] = 255;
+  auto place = [&](int slot, int j) {   // x̃_j -> slot; returns true if the entry is -x
+    const int x = j < 129 ? j : 258 - j;
+    t.slot[x - 1] = (uint8_t)slot;
+    return j > 129;
+  };
+  for (int j1 = 0; j1 < 2; ++j1) {
+    const int ub = j1 ? U1B : U0B, wb = j1 ? W1B : W0B;
+    for (int e = 1; e <= 21; ++e)
+      if (place(ub + e, crt258(j1, 0, e))) t.usign[j1] |= 1u << e;
+    for (int j3 = 0; j3 < 43; ++j3)
+      if (place(wb + j3, crt258(j1, 1, j3))) t.wsign[j1] |= 1ull << j3;
+  }
+  return t;
+}
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double flip(double v, uint32_t signbit) {   // signbit: 0 or 0x80000000
+  return __hiloint2double(__double2hiint(v) ^ (int)signbit, __double2loint(v));
+}
+
+__device__ __forceinline__ void cp_async16(unsigned smem_addr, const double* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// global offset of (transform-axis row r, column cg) inside one field
+template <int PASS>
+__device__ __forceinline__ size_t goff(int r, int cg) {
+  if (PASS == 0) return (size_t)r * NN + cg;
+  return (size_t)(cg >> 7) * NN + (size_t)r * N + (cg & (N - 1));
+}
+
+// A fragments of the two 24x24 matrices (exact argument reduction mod 43):
+//   S[k3][e]  = sin(2π e k3/43)          k3, e in 1..21   (zero elsewhere)
+//   C'[k3][e] = (√3/2) cos(2π e k3/43)   k3, e in 0..21
+// tab[((mat*3 + mt)*6 + ks)*32 + lane] = entry (row 8mt + lane/4, column 4ks + lane%4).
+__global__ void pfa_atab_kernel(double* tab) {
+  const int mat = blockIdx.x / 18, mt = (blockIdx.x / 6) % 3, ks = blockIdx.x % 6, lane = threadIdx.x;
+  const int k3 = 8 * mt + (lane >> 2), e = 4 * ks + (lane & 3);
+  const double arg = 2.0 * (double)((e * k3) % 43) / 43.0;
+  double v;
+  if (mat == 0) v = (k3 <= 21 && e >= 1 && e <= 21) ? sinpi(arg) : 0.0;
+  else v = (k3 <= 21 && e <= 21) ? 0.86602540378443864676 * cospi(arg) : 0.0;
+  tab[blockIdx.x * 32 + lane] = v;
+}
+
+template <int PASS>
+__device__ __forceinline__ void load_tile(double* buf, const uint8_t* slot, const double* src, int col0) {
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(buf);
+  constexpr int PER_ROW = TC / 2;                  // 16-byte requests per row
+  const int c = 2 * (threadIdx.x % PER_ROW);
+  for (int r = threadIdx.x / PER_ROW; r < N; r += NTHR / PER_ROW)
+    cp_async16(sbase + 8u * (unsigned)(slot[r] * LD + c), src + goff<PASS>(r, col0 + c));
+}
+
+// Butterfly of one k3 row for one column (lane): the six staged length-43 results -> the (up to)
+// 12 outputs X_k whose CRT class has this k3 (or 43 - k3); k, validity and signs are constants.
+template <int PASS, int K3>
+__device__ __forceinline__ void bfly(const double* R, double* dcol) {
+  constexpr size_t STRIDE = PASS == 0 ? (size_t)NN : (size_t)N;
+  double s0 = 0.0, s1 = 0.0, b0 = 0.0, b1 = 0.0;   // σ(0) = B(0) = 0
+  if (K3 > 0) {
+    s0 = R[(RS0 + K3 - 1) * LD];
+    s1 = R[(RS1 + K3 - 1) * LD];
+    b0 = R[(RB0 + K3 - 1) * LD];
+    b1 = R[(RB1 + K3 - 1) * LD];
+  }
+  const double a0 = R[(RA0 + K3) * LD], a1 = R[(RA1 + K3) * LD];
+  const double P0 = s0 + b0, P1 = s1 + b1, Q0 = fma(-0.5, b0, s0), Q1 = fma(-0.5, b1, s1);
+  const double V[2][3] = {{P0 + P1, (Q0 + Q1) + (a0 + a1), (Q0 + Q1) - (a0 + a1)},
+                          {P0 - P1, (Q0 - Q1) + (a0 - a1), (Q0 - Q1) - (a0 - a1)}};
+#pragma unroll
+  for (int mir = 0; mir < 2; ++mir) {
+    if (mir && K3 == 0) break;
+    const int k3f = mir ? 43 - K3 : K3;
+#pragma unroll
+    for (int k1 = 0; k1 < 2; ++k1)
+#pragma unroll
+      for (int k2 = 0; k2 < 3; ++k2) {
+        const int k = (129 * k1 + 86 * k2 + 6 * k3f) % 258;
+        if (k < 1 || k > 128) continue;
+        // mirror k3f = 43 - k3 flips σ and B (P, Q) but not A:  -Q ± A = -(Q ∓ A)
+        const double v = !mir ? V[k1][k2] : (k2 == 0 ? -V[k1][0] : (k2 == 1 ? -V[k1][2] : -V[k1][1]));
+        __stcg(dcol + (size_t)(k - 1) * STRIDE, v);
+      }
+  }
+}
+
+template <int PASS, int... K3>
+__device__ __forceinline__ void bfly_list(const double* R, double* dcol, std::integer_sequence<int, K3...>) {
+  (bfly<PASS, K3>(R, dcol), ...);
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(NTHR, 2)
+dst128_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields,
+                   const double* __restrict__ atab) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ uint8_t slot[N];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kk = lane & 3, rq = lane >> 2;
+  const int nt = warp % NTILE_N, mt = warp / NTILE_N;
+
+  for (int r = threadIdx.x; r < N; r += NTHR) slot[r] = c_slot[r];
+  for (int i = threadIdx.x; i < 2 * 2 * LD; i += NTHR)       // zero rows 128, 129 of both buffers
+    smem[(i / (2 * LD)) * TILE + (128 + (i / LD) % 2) * LD + i % LD] = 0.0;
+  double aS[6], aC[6];
+#pragma unroll
+  for (int ks = 0; ks < 6; ++ks) {
+    aS[ks] = __ldg(atab + ((0 * 3 + mt) * 6 + ks) * 32 + lane);
+    aC[ks] = __ldg(atab + ((1 * 3 + mt) * 6 + ks) * 32 + lane);
+  }
+  // per-ks sign bits of this thread's B-fragment entries e = 4ks + kk
+  uint32_t su0 = 0, su1 = 0, sw0a = 0, sw0b = 0, sw1a = 0, sw1b = 0;
+#pragma unroll
+  for (int ks = 0; ks < 6; ++ks) {
+    const int e = 4 * ks + kk;
+    su0 |= ((c_usign[0] >> e) & 1u) << ks;
+    su1 |= ((c_usign[1] >> e) & 1u) << ks;
+    sw0a |= (uint32_t)((c_wsign[0] >> e) & 1u) << ks;
+    sw1a |= (uint32_t)((c_wsign[1] >> e) & 1u) << ks;
+    if (e >= 1) {
+      sw0b |= (uint32_t)((c_wsign[0] >> (43 - e)) & 1u) << ks;
+      sw1b |= (uint32_t)((c_wsign[1] >> (43 - e)) & 1u) << ks;
+    }
+  }
+  const double keep0 = kk == 0 ? 0.0 : 1.0;   // Wp(0) = w(0): drop the w(43) partner at e = 0
+  __syncthreads();
+
+  constexpr int TPF = NN / TC;   // tiles per field
+  const long ntiles = (long)nfields * TPF;
+  const size_t field = (size_t)NN * N;
+  long tile = blockIdx.x;
+  if (tile < ntiles) {
+    const int f = (int)(tile / TPF);
+    load_tile<PASS>(smem, slot, in + (size_t)f * field, (int)(tile - (long)f * TPF) * TC);
+  }
+  cp_async_commit();
+  const int bcol = nt * 8 + rq;           // B-fragment column within the tile
+  for (int cur = 0; tile < ntiles; tile += gridDim.x, cur ^= 1) {
+    const long nxt = tile + gridDim.x;
+    if (nxt < ntiles) {
+      const int f = (int)(nxt / TPF);
+      load_tile<PASS>(smem + (cur ^ 1) * TILE, slot, in + (size_t)f * field, (int)(nxt - (long)f * TPF) * TC);
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    double* T = smem + cur * TILE;
+
+    double sg0[2] = {0, 0}, sg1[2] = {0, 0}, bb0[2] = {0, 0}, bb1[2] = {0, 0}, aa0[2] = {0, 0}, aa1[2] = {0, 0};
+#pragma unroll
+    for (int ks = 0; ks < 6; ++ks) {
+      const int e = 4 * ks + kk;
+      const double u0 = flip(T[(U0B + e) * LD + bcol], ((su0 >> ks) & 1u) << 31);
+      const double u1 = flip(T[(U1B + e) * LD + bcol], ((su1 >> ks) & 1u) << 31);
+      const double w0a = flip(T[(W0B + e) * LD + bcol], ((sw0a >> ks) & 1u) << 31);
+      double w0b = flip(T[(W0B + 43 - e) * LD + bcol], ((sw0b >> ks) & 1u) << 31);
+      const double w1a = flip(T[(W1B + e) * LD + bcol], ((sw1a >> ks) & 1u) << 31);
+      double w1b = flip(T[(W1B + 43 - e) * LD + bcol], ((sw1b >> ks) & 1u) << 31);
+      if (ks == 0) {
+        w0b *= keep0;
+        w1b *= keep0;
+      }
+      dmma884(sg0, aS[ks], u0);
+      dmma884(sg1, aS[ks], u1);
+      dmma884(bb0, aS[ks], w0a - w0b);
+      dmma884(bb1, aS[ks], w1a - w1b);
+      dmma884(aa0, aC[ks], w0a + w0b);
+      dmma884(aa1, aC[ks], w1a + w1b);
+    }
+    // Stage the length-43 results in this warp's own (column, row) block of the consumed tile, so
+    // that the butterfly below runs with k3 uniform across each warp (lanes = columns).
+    __syncthreads();   // every warp has read its B fragments from T
+    {
+      const int k3 = 8 * mt + rq;
+      const int c = nt * 8 + 2 * kk;
+      if (k3 >= 1 && k3 <= 21) {
+        *reinterpret_cast<double2*>(T + (RS0 + k3 - 1) * LD + c) = make_double2(sg0[0], sg0[1]);
+        *reinterpret_cast<double2*>(T + (RS1 + k3 - 1) * LD + c) = make_double2(sg1[0], sg1[1]);
+        *reinterpret_cast<double2*>(T + (RB0 + k3 - 1) * LD + c) = make_double2(bb0[0], bb0[1]);
+        *reinterpret_cast<double2*>(T + (RB1 + k3 - 1) * LD + c) = make_double2(bb1[0], bb1[1]);
+      }
+      if (k3 <= 21) {
+        *reinterpret_cast<double2*>(T + (RA0 + k3) * LD + c) = make_double2(aa0[0], aa0[1]);
+        *reinterpret_cast<double2*>(T + (RA1 + k3) * LD + c) = make_double2(aa1[0], aa1[1]);
+      }
+    }
+    __syncthreads();
+    // 2x3 butterfly + output map: lane = column, warp w handles k3 = w, w + 12 with every output
+    // index and sign a compile-time constant (no per-element index arithmetic).
+    const int f = (int)(tile / TPF);
+    double* dcol = out + (size_t)f * field + goff<PASS>(0, (int)(tile - (long)f * TPF) * TC + lane);
+    const double* R = T + lane;
+    switch (warp) {
+      case 0: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 0, 12>{}); break;
+      case 1: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 1, 13>{}); break;
+      case 2: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 2, 14>{}); break;
+      case 3: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 3, 15>{}); break;
+      case 4: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 4, 16>{}); break;
+      case 5: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 5, 17>{}); break;
+      case 6: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 6, 18>{}); break;
+      case 7: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 7, 19>{}); break;
+      case 8: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 8, 20>{}); break;
+      case 9: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 9, 21>{}); break;
+      case 10: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 10>{}); break;
+      default: bfly_list<PASS>(R, dcol, std::integer_sequence<int, 11>{}); break;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Thread-per-column DFMA variant (default).  Same Good–Thomas factorisation, but every thread owns
+// one column: the length-43 stage runs as exact-size 21x21 / 22x22 dot products (2732 DFMA per
+// column vs 3456 padded DMMA MACs, no fragment shuffling) whose matrix entries are warp-uniform
+// constants (sin / (√3/2)cos of 2πm/43, m = e·k3 mod 43) and whose CRT rows and odd-extension
+// signs are compile-time constants.  A warp reads 32 consecutive columns, so every load and store
+// is one coalesced 256-byte row.  Per warp, shared memory holds the 64 prepared inputs of the
+// current half (IN) and the j1 = 0 butterfly operands (ST); the contraction streams IN in blocks
+// of 8 k3 rows (24 accumulator chains, ~80 registers).  No barriers.
+__constant__ double c_s43[43];   // sin(2π m/43)
+__constant__ double c_c43[43];   // (√3/2) cos(2π m/43)
+
+__host__ __device__ constexpr int crt_c(int j1, int j2, int j3) {
+  int j = 0;
+  while (!(j % 2 == j1 && j % 3 == j2 && j % 43 == j3)) ++j;
+  return j;
+}
+// x̃_j (j = CRT(...), j != 0, 129) = ±x_{row+1}
+__host__ __device__ constexpr int crow(int j) { return (j < 129 ? j : 258 - j) - 1; }
+__host__ __device__ constexpr bool cneg(int j) { return j > 129; }
+
+
+// z[j1][j2][e] for this lane's half j1 (0 for lanes 0-15, 1 for lanes 16-31), read from the warp's
+// RAW copy of the tile ([128 rows][16 columns], natural row order): both CRT rows and signs are
+// compile-time constants; the lane picks one with an integer select and applies the sign as a
+// sign-bit XOR (no divergence, nothing on the fp64 pipe).
+template <int J2, int E>
+__device__ __forceinline__ double ldz2(const double* raw, bool hi) {
+  constexpr int ja = crt_c(0, J2, E), jb = crt_c(1, J2, E);
+  const double v = raw[(hi ? crow(jb) : crow(ja)) * 16];
+  constexpr int sa = cneg(ja) ? (int)0x80000000 : 0, sb = cneg(jb) ? (int)0x80000000 : 0;
+  return __hiloint2double(__double2hiint(v) ^ (hi ? sb : sa), __double2loint(v));
+}
+
+// IN layout per warp (16 KB): (pin, qin) pairs for e = 1..21 at (e-1)*64 + 2*lane, then wp for
+// e = 0..21 at IN_W + e*32 + lane.
+constexpr int IN_W = 21 * 64, IN_SIZE = IN_W + 22 * 32, RAW_SIZE = 128 * 16;
+
+// Prepare this lane's half: pin(e) = u(e) + wm(e), qin(e) = u(e) - wm(e)/2 (e = 1..21), wp(e) (0..21)
+// with u(e) = z[j1][0][e], w(j3) = z[j1][1][j3], wm(e) = w(e) - w(43-e), wp(e) = w(e) + w(43-e).
+template <int... E>
+__device__ __forceinline__ void prep_half2(const double* raw, bool hi, double* in, int lane,
+                                           std::integer_sequence<int, E...>) {
+  in[IN_W + lane] = ldz2<1, 0>(raw, hi);
+  auto one = [&](auto ec) {
+    constexpr int e = decltype(ec)::value;
+    const double u = ldz2<0, e>(raw, hi);
+    const double wa = ldz2<1, e>(raw, hi), wb = ldz2<1, 43 - e>(raw, hi);
+    const double wm = wa - wb;
+    *reinterpret_cast<double2*>(in + (e - 1) * 64 + 2 * lane) = make_double2(u + wm, fma(-0.5, wm, u));
+    in[IN_W + e * 32 + lane] = wa + wb;
+  };
+  (one(std::integral_constant<int, E + 1>{}), ...);
+}
+
+// cp.async of one 16-column x 128-row tile (16-byte requests) into the warp's RAW buffer
+template <int PASS>
+__device__ __forceinline__ void load_raw(double* raw, const double* fieldbase, int c0, int lane) {
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(raw);
+  const int cc = 2 * (lane & 7);
+#pragma unroll 8
+  for (int r = lane >> 3; r < N; r += 4)
+    cp_async16(sb + 8u * (unsigned)(r * 16 + cc), fieldbase + goff<PASS>(r, c0 + cc));
+}
+
+// Contract one block of KB k3 rows starting at K0:  P = S·pin, Q = S·qin, R = C'·wp.
+// `in` points at this lane's IN slot (pairs at in + IN_PQ + e*64 (+lane*2 folded by the caller)).
+template <int K0, int KB, typename Emit>
+__device__ __forceinline__ void contract_block(const double* inpq, const double* inw, Emit&& emit) {
+  double P[KB], Q[KB], R[KB];
+#pragma unroll
+  for (int q = 0; q < KB; ++q) P[q] = Q[q] = R[q] = 0.0;
+#pragma unroll
+  for (int e = 0; e <= 21; ++e) {
+    const double w = inw[e * 32];
+    double2 pq = make_double2(0.0, 0.0);
+    if (e >= 1) pq = *reinterpret_cast<const double2*>(inpq + (e - 1) * 64);
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int k3 = K0 + q;
+      // only 22 + 21 distinct magnitudes (sin(2π(43-m)/43) = -sin, cos even): the compiler keeps
+      // them in (uniform) registers and applies the sign as a free operand negation
+      const int m = (e * k3) % 43;
+      const double cm = m <= 21 ? c_c43[m] : c_c43[43 - m];
+      R[q] = fma(w, cm, R[q]);
+      if (e >= 1 && k3 >= 1) {
+        const double sm = m <= 21 ? c_s43[m] : -c_s43[43 - m];
+        P[q] = fma(pq.x, sm, P[q]);
+        Q[q] = fma(pq.y, sm, Q[q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KB; ++q) emit(std::integral_constant<int, K0>{}, q, P[q], Q[q], R[q]);
+}
+
+// lanes 0-15: half j1 = 0 of columns 0..15; lanes 16-31: half j1 = 1 of the same columns.  The final
+// 2-point stage X_k = T0 ± T1 pairs lane l with l ^ 16 (one shuffle per operand): lane l writes the
+// k1 = 0 outputs, lane l + 16 the k1 = 1 outputs.  14 warps per SM, 16 KB of IN per warp.
+template <int PASS, int MINB>
+__global__ void __launch_bounds__(224, MINB)
+dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields) {
+  extern __shared__ __align__(16) double wsm[];   // [warp][IN 16 KB | RAW 16 KB]
+  const int lane = threadIdx.x & 31;
+  const bool hi = lane >= 16;
+  double* wbase = wsm + (threadIdx.x >> 5) * (IN_SIZE + RAW_SIZE);
+  double* raw = wbase + IN_SIZE;
+  const double* inpq = wbase + 2 * lane;
+  const double* inw = wbase + IN_W + lane;
+  constexpr size_t STRIDE = PASS == 0 ? (size_t)NN : (size_t)N;
+  constexpr int TPF = NN / 16;
+  const int ntiles = nfields * TPF;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const double sm1 = hi ? -1.0 : 1.0;
+  const size_t field = (size_t)NN * N;
+  if (gw < ntiles) {
+    const int f = gw / TPF;
+    load_raw<PASS>(raw, in + (size_t)f * field, (gw - f * TPF) * 16, lane);
+  }
+  cp_async_commit();
+  for (int t = gw; t < ntiles; t += nw) {
+    const int f = t / TPF, cg = (t - f * TPF) * 16 + (lane & 15);
+    double* ocol = out + (size_t)f * field + goff<PASS>(0, cg);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncwarp();
+    prep_half2(raw + (lane & 15), hi, wbase, lane, std::make_integer_sequence<int, 21>{});
+    __syncwarp();   // RAW consumed: prefetch the next tile under the contraction
+    const int tn = t + nw;
+    if (tn < ntiles) {
+      const int fn = tn / TPF;
+      load_raw<PASS>(raw, in + (size_t)fn * field, (tn - fn * TPF) * 16, lane);
+    }
+    cp_async_commit();
+    auto bfly = [&](auto k0c, int q, double P, double Q, double R) {
+      const int k3 = decltype(k0c)::value + q;
+      // lane l (j1 = 0) forms T0 + T1 (k1 = 0), lane l + 16 (j1 = 1) forms T0 - T1 (k1 = 1):
+      //   X = other ± mine  ->  fma(±1, mine, other)
+      const double Ps = fma(sm1, P, __shfl_xor_sync(0xffffffffu, P, 16));
+      const double Qs = fma(sm1, Q, __shfl_xor_sync(0xffffffffu, Q, 16));
+      const double Rs = fma(sm1, R, __shfl_xor_sync(0xffffffffu, R, 16));
+      // (for the hi lane Ps = T0 - T1 exactly as the k1 = 1 formula needs)
+      const double V[3] = {Ps, Qs + Rs, Qs - Rs};
+#pragma unroll
+      for (int mir = 0; mir < 2; ++mir) {
+        if (mir && k3 == 0) break;
+        const int k3f = mir ? 43 - k3 : k3;
+#pragma unroll
+        for (int k2 = 0; k2 < 3; ++k2) {
+          const int ka = (86 * k2 + 6 * k3f) % 258, kb = (129 + 86 * k2 + 6 * k3f) % 258;
+          const bool va = ka >= 1 && ka <= 128, vb = kb >= 1 && kb <= 128;
+          if (!va && !vb) continue;
+          // mirror k3f = 43 - k3 flips σ and B (P, Q) but not A:  -Q ± R = -(Q ∓ R)
+          const double v = !mir ? V[k2] : (k2 == 0 ? -V[0] : (k2 == 1 ? -V[2] : -V[1]));
+          if (hi ? vb : va) __stcg(ocol + (size_t)((hi ? kb : ka) - 1) * STRIDE, v);
+        }
+      }
+    };
+    // __syncwarp between blocks: keeps ptxas from interleaving the blocks' accumulator sets
+    __syncwarp();
+    contract_block<0, 8>(inpq, inw, bfly);
+    __syncwarp();
+    contract_block<8, 8>(inpq, inw, bfly);
+    __syncwarp();
+    contract_block<16, 6>(inpq, inw, bfly);
+    __syncwarp();
+  }
+}
+
+unsigned long long g_tables_ready = 0;   // bit d: constant tables uploaded on device d
+
+}  // namespace
+
+// Per-plan A-fragment table (device memory owned by the plan).
+cudaError_t dst128_atab(double** tab) {
+  cudaError_t e = cudaMalloc(tab, ATAB * sizeof(double));
+  if (e != cudaSuccess) return e;
+  DPM_COUNT_LAUNCH(1);
+  pfa_atab_kernel<<<ATAB / 32, 32>>>(*tab);
+  return cudaGetLastError();
+}
+
+cudaError_t dst128_init() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && (g_tables_ready >> dev) & 1ull) return cudaSuccess;
+  const Tables t = make_tables();
+  for (int r = 0; r < N; ++r)
+    if (t.slot[r] == 255) return cudaErrorInvalidValue;   // the CRT map must cover every row
+  cudaError_t e;
+  if ((e = cudaMemcpyToSymbol(c_slot, t.slot, sizeof(t.slot))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_usign, t.usign, sizeof(t.usign))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_wsign, t.wsign, sizeof(t.wsign))) != cudaSuccess) return e;
+  double s43[43], c43[43];
+  for (int m = 0; m < 43; ++m) {   // long double evaluation, rounded once to double
+    const long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)m / 43.0L;
+    s43[m] = (double)sinl(a);
+    c43[m] = (double)(0.866025403784438646763723170752936183L * cosl(a));
+  }
+  if ((e = cudaMemcpyToSymbol(c_s43, s43, sizeof(s43))) != cudaSuccess) return e;
+  if ((e = cudaMemcpyToSymbol(c_c43, c43, sizeof(c43))) != cudaSuccess) return e;
+  if (dev < 64) g_tables_ready |= 1ull << dev;
+  return cudaSuccess;
+}
+
+// One DST-I pass (scale 1) along x (pass 0) or y (pass 1) of nfields n=128 fields; out may == in.
+cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, const double* atab, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const int use_dmma = [] {
+    const char* v = getenv("DPM_DST128_DMMA");
+    return v && atoi(v) == 1;
+  }();
+  if (!use_dmma) {
+    const size_t smem = 7 * (IN_SIZE + RAW_SIZE) * sizeof(double);
+    static const int minb = [] {
+      const char* v = getenv("DPM_DST128F_MINB");
+      return v && atoi(v) == 2 ? 2 : 1;
+    }();
+    auto kf = minb == 1 ? (pass == 0 ? dst128f_kernel<0, 1> : dst128f_kernel<1, 1>)
+                        : (pass == 0 ? dst128f_kernel<0, 2> : dst128f_kernel<1, 2>);
+    cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, 224, smem);
+    const long warps = (long)nfields * (NN / 16);
+    const int grid = (int)std::min<long>((warps + 6) / 7, (long)sms * std::max(1, occ));
+    DPM_COUNT_LAUNCH(1);
+    kf<<<grid, 224, smem, s>>>(in, out, nfields);
+    return cudaGetLastError();
+  }
+  const size_t smem = 2 * (size_t)TILE * sizeof(double);
+  auto k = pass == 0 ? dst128_pass_kernel<0> : dst128_pass_kernel<1>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTHR, smem);
+  const long ntiles = (long)nfields * (NN / TC);
+  const int grid = (int)std::min<long>(ntiles, (long)sms * std::max(1, occ));
+  DPM_COUNT_LAUNCH(1);
+  k<<<grid, NTHR, smem, s>>>(in, out, nfields, atab);
+  return cudaGetLastError();
+}

@@ -394,6 +394,7 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
   const int n = p.n;
   const int Po = (n + 1) / 2, KS = (Po + 3) / 4;
   const bool even = (n % 2) == 0;
+  if (n == 128 && pass < 2 && p.pfa) return dst128_pass(pass, in, out, nfields, p.atab128, s);
   if (n == 128) {
     if (tc128() == 32) return run_pass_t<128, 16, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
     return run_pass_t<128, 16, 64, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
@@ -417,115 +418,145 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
 // Exact identity: T = A + μ e1 e1^T with A = μ^{-1} (I - μL)(I - μU) (L/U = sub/super shift), so
 //   A^{-1} r = μ z,  z = (I - μU)^{-1} (I - μL)^{-1} r   (two constant-coefficient recurrences)
 //   T^{-1} r = μ z - s · μ (μ z_0) / (1 + μ s_0),   s_k = (μ^{k+1} - μ^{2n+1-k}) / (1 - μ^2)
-// (Sherman-Morrison; s = A^{-1} e1 in closed form).  No division per element, no pivot table.
-// Tile: TL = 32 lines x n; lane = line, warp = one of 8 z-segments; each recurrence is a
-// segmented scan (local sweep, carry exchange through shared memory, geometric fix-up).
-constexpr int TL = 32;
+// (Sherman-Morrison; s = A^{-1} e1 in closed form).  Two divisions per line, no pivot table.
+//
+// One warp per line (every n <= 128): lane l holds z = 4l..4l+3;
+// each first-order recurrence is a local 4-step sweep plus a 5-step Kogge–Stone carry scan over the
+// warp with multipliers μ^4, μ^8, ..., so no shared memory, no barriers and one 1 KB line per warp
+// in flight; Sherman–Morrison powers μ^{k+1}, μ^{2n+1-k} by binary exponentiation per lane.
+__device__ __forceinline__ double ipow(double b, int e) {   // b^e, e >= 0
+  double r = 1.0;
+  while (e > 0) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
 
 template <int NFIX>
-__global__ void __launch_bounds__(NT)
-ztri_kernel(double* __restrict__ u, long nlines, int n_rt, const double* __restrict__ lam_g, double inv_dt,
-            double h2, double rscale) {
-  extern __shared__ __align__(16) double zs[];
+__global__ void __launch_bounds__(256)
+ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __restrict__ lam_g, double inv_dt,
+                 double h2, double rscale) {
+  __shared__ double lam[DPM_MAX_N];
   const int n = NFIX ? NFIX : n_rt;
-  const int LDT = n + 1;                    // odd stride: per-thread rows are bank-conflict free
-  double* tile = zs;
-  double* carry = zs + TL * LDT;            // [8][TL]
-  double* lam = carry + 8 * TL;
-  for (int i = threadIdx.x; i < n; i += NT) lam[i] = lam_g[i];
-  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
-  const int SEG = (n + 7) / 8;
-  const int k0 = min(n, s * SEG), k1 = min(n, k0 + SEG);
-  const int nn = n * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) lam[i] = lam_g[i];
   __syncthreads();
-  for (long l0 = (long)blockIdx.x * TL; l0 < nlines; l0 += (long)gridDim.x * TL) {
-    const int nl = (int)min((long)TL, nlines - l0);
-    const double* src = u + l0 * n;
-    for (int e = threadIdx.x; e < nl * n; e += NT) {
-      const int li = e / n;
-      tile[li * LDT + (e - li * n)] = __ldcg(src + e);
+  const int lane = threadIdx.x & 31;
+  const int w0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
+  const int nn = n * n, k0 = 4 * lane;
+  for (int line = w0; line < nlines; line += nw) {   // nlines < 2^31 (checked by the launcher)
+    double* L = u + (size_t)line * n;
+    double r[4];
+    if (NFIX == 128) {
+      const double2 a = __ldcg(reinterpret_cast<const double2*>(L + k0));
+      const double2 b = __ldcg(reinterpret_cast<const double2*>(L + k0 + 2));
+      r[0] = a.x; r[1] = a.y; r[2] = b.x; r[3] = b.y;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) r[i] = k0 + i < n ? __ldcg(L + k0 + i) : 0.0;
     }
-    __syncthreads();
-    const bool valid = lane < nl;
-    double* row = tile + lane * LDT;
-    const int lf = (int)((l0 + lane) % nn);
+    const int lf = line % nn;
     const double hs = h2 * ((inv_dt + lam[lf / n]) + lam[lf % n]);
     const double disc = sqrt(hs * (hs + 4.0));
-    const double beta = 2.0 + hs;
-    const double mu = 2.0 / (beta + disc);
-    const double muinv = 0.5 * (beta + disc);
-    const double one_m_mu2 = ((hs + disc) / (beta + disc)) * (1.0 + mu);   // 1 - μ^2 without cancellation
-    double muS = 1.0;
-    for (int i = 0; i < SEG; ++i) muS *= mu;
-    // forward: y_k = r_k + μ y_{k-1}
-    double y = 0.0;
-    if (valid)
-      for (int k = k0; k < k1; ++k) { y = fma(mu, y, rscale * row[k]); row[k] = y; }
-    carry[s * TL + lane] = y;
-    __syncthreads();
-    double Y = 0.0;
-    for (int t = 0; t < s; ++t) Y = fma(muS, Y, carry[t * TL + lane]);
-    double p = mu * Y;
-    if (valid)
-      for (int k = k0; k < k1; ++k) { row[k] += p; p *= mu; }
-    __syncthreads();
-    // backward: z_k = y_k + μ z_{k+1}
-    double z = 0.0;
-    if (valid)
-      for (int k = k1 - 1; k >= k0; --k) { z = fma(mu, z, row[k]); row[k] = z; }
-    carry[s * TL + lane] = z;
-    __syncthreads();
-    double Z = 0.0;
-    // segments after s are full (length SEG) except possibly the last non-empty one, whose
-    // incoming Z is 0, and empty ones, whose carry and incoming Z are 0: μ^SEG is exact here.
-    for (int t = 7; t > s; --t) Z = fma(muS, Z, carry[t * TL + lane]);
-    p = mu * Z;
-    if (valid)
-      for (int k = k1 - 1; k >= k0; --k) { row[k] += p; p *= mu; }
-    __syncthreads();
-    // Sherman-Morrison boundary correction
-    if (valid && k1 > k0) {
-      const double z0 = row[0];
-      const double inv = 1.0 / one_m_mu2;
-      const double s0 = (mu - pow(mu, 2.0 * n + 1.0)) * inv;
-      const double coef = mu * (mu * z0) / (1.0 + mu * s0);
-      double pA = pow(mu, (double)k1), pB = pow(mu, (double)(2 * n + 2 - k1));
-      for (int k = k1 - 1; k >= k0; --k) {
-        row[k] = mu * row[k] - coef * ((pA - pB) * inv);
-        pA *= muinv;
-        pB *= mu;
-      }
+    const double mu = 2.0 / ((2.0 + hs) + disc);
+    const double mu2 = mu * mu, mu3 = mu2 * mu, mu4 = mu2 * mu2;
+    double mp[5];   // μ^{4·2^s}
+    mp[0] = mu4;
+#pragma unroll
+    for (int q = 1; q < 5; ++q) mp[q] = mp[q - 1] * mp[q - 1];
+    // forward y_k = r_k + μ y_{k-1}
+    double y[4];
+    y[0] = rscale * r[0];
+    y[1] = fma(mu, y[0], rscale * r[1]);
+    y[2] = fma(mu, y[1], rscale * r[2]);
+    y[3] = fma(mu, y[2], rscale * r[3]);
+    double C = y[3];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double t = __shfl_up_sync(0xffffffffu, C, 1 << q);
+      C = fma(lane >= (1 << q) ? mp[q] : 0.0, t, C);
     }
-    __syncthreads();
-    double* dst = u + l0 * n;
-    for (int e = threadIdx.x; e < nl * n; e += NT) {
-      const int li = e / n;
-      __stcg(dst + e, tile[li * LDT + (e - li * n)]);
+    double cin = __shfl_up_sync(0xffffffffu, C, 1);
+    cin = lane == 0 ? 0.0 : cin;
+    y[0] = fma(mu, cin, y[0]);
+    y[1] = fma(mu2, cin, y[1]);
+    y[2] = fma(mu3, cin, y[2]);
+    y[3] = fma(mu4, cin, y[3]);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (k0 + i >= n) y[i] = 0.0;   // padding beyond the line: ghost values
+    // backward z_k = y_k + μ z_{k+1}
+    double z[4];
+    z[3] = y[3];
+    z[2] = fma(mu, z[3], y[2]);
+    z[1] = fma(mu, z[2], y[1]);
+    z[0] = fma(mu, z[1], y[0]);
+    double D = z[0];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const double t = __shfl_down_sync(0xffffffffu, D, 1 << q);
+      D = fma(lane + (1 << q) < 32 ? mp[q] : 0.0, t, D);
     }
-    __syncthreads();
+    double din = __shfl_down_sync(0xffffffffu, D, 1);
+    din = lane == 31 ? 0.0 : din;
+    z[3] = fma(mu, din, z[3]);
+    z[2] = fma(mu2, din, z[2]);
+    z[1] = fma(mu3, din, z[1]);
+    z[0] = fma(mu4, din, z[0]);
+    // T^{-1} r = μ z - c2 (μ^{k+1} - μ^{2n+1-k}),  c2 = μ^2 z_0 / (1 - μ^{2n+2})
+    // (Sherman–Morrison with s = A^{-1} e_1 in closed form; (1 + μ s_0)(1 - μ^2) = 1 - μ^{2n+2}).
+    // Powers by binary exponentiation over the lane bits with the μ^{4·2^s} table:
+    //   μ^{k0+1} = μ · μ^{4 lane},   μ^{2n-2-k0} = μ^{E} · μ^{4(NL-1-lane)},  E = 2n + 2 - 4 NL >= n - 1.
+    const int NL = (n + 3) >> 2;   // lanes holding line data
+    const int lr = max(0, NL - 1 - lane);
+    double P1 = 1.0, P2 = 1.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      P1 *= (lane >> q) & 1 ? mp[q] : 1.0;
+      P2 *= (lr >> q) & 1 ? mp[q] : 1.0;
+    }
+    const double muE = ipow(mu, 2 * n + 2 - 4 * NL);                 // warp-uniform exponent
+    const double mu4L = __shfl_sync(0xffffffffu, P1, NL - 1) * mu4;   // μ^{4 NL}
+    const double mu2n2 = muE * mu4L;                                  // μ^{2n+2}
+    const double zf = __shfl_sync(0xffffffffu, z[0], 0);
+    const double c2 = mu2 * zf / (1.0 - mu2n2);
+    const double pa = mu * P1, pb = muE * P2;
+    const double pas[4] = {pa, pa * mu, pa * mu2, pa * mu3};
+    const double pbs[4] = {pb * mu3, pb * mu2, pb * mu, pb};
+    double o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = fma(mu, z[i], -c2 * (pas[i] - pbs[i]));
+    if (NFIX == 128) {
+      __stcg(reinterpret_cast<double2*>(L + k0), make_double2(o[0], o[1]));
+      __stcg(reinterpret_cast<double2*>(L + k0 + 2), make_double2(o[2], o[3]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (k0 + i < n) __stcg(L + k0 + i, o[i]);
+    }
   }
 }
 
 cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
   const int n = p.n;
-  const size_t smem = (size_t)(TL * (n + 1) + 8 * TL + n) * 8;
   const long nlines = (long)nfields * n * n;
-  void (*k)(double*, long, int, const double*, double, double, double) = n == 128 ? ztri_kernel<128> : ztri_kernel<0>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  if (nlines >= (1L << 31)) return cudaErrorInvalidValue;
   static int sms = 0;
   if (!sms) {
     int dev;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  void (*k)(double*, int, int, const double*, double, double, double) =
+      n == 128 ? ztri_warp_kernel<128> : ztri_warp_kernel<0>;
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem);
-  const long tiles = (nlines + TL - 1) / TL;
-  const int grid = (int)std::min<long>(tiles, (long)sms * std::max(1, occ));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
+  const long blocks = (nlines + 7) / 8;
+  const int grid = (int)std::min<long>(blocks, (long)sms * std::max(1, occ));
   const double sc = 2.0 / (n + 1);
   DPM_COUNT_LAUNCH(1);
-  k<<<grid, NT, smem, s>>>(u, nlines, n, p.lam, 1.0 / p.dt, p.h * p.h, sc * sc * p.h * p.h);
+  k<<<grid, 256, 0, s>>>(u, (int)nlines, n, p.lam, 1.0 / p.dt, p.h * p.h, sc * sc * p.h * p.h);
   return cudaGetLastError();
 }
 
@@ -552,12 +583,20 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
   afrag_table_kernel<<<dim3(NW, 2), KSMAX_ALL * 32>>>(p.atab, n, tc_for(n) / 8);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (n == 128) {
+    const char* env = getenv("DPM_PFA");
+    p.pfa = !(env && atoi(env) == 0);
+    if (p.pfa && (e = dst128_init()) != cudaSuccess) return e;
+    if (p.pfa && (e = dst128_atab(&p.atab128)) != cudaSuccess) return e;
+  }
   return cudaDeviceSynchronize();
 }
 
 void dst_plan_free(DstPlan& p) {
   if (p.lam) cudaFree(p.lam);
   if (p.atab) cudaFree(p.atab);
+  if (p.atab128) cudaFree(p.atab128);
+  p.atab128 = nullptr;
   p.lam = nullptr;
   p.atab = nullptr;
 }
@@ -569,7 +608,10 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
   const int n = p.n;
   const size_t field_bytes = (size_t)n * n * n * 8;
   // chunk so that the in-flight working set stays in the 126 MB L2
-  const size_t budget = (size_t)64 << 20;
+  static const size_t budget = [] {
+    const char* v = getenv("DPM_CHUNK_MB");
+    return (size_t)(v ? atoi(v) : 112) << 20;
+  }();
   int64_t chunk = std::max<int64_t>(1, (int64_t)(budget / field_bytes));
   const double inv_dt = 1.0 / p.dt;
   const double sc = 2.0 / (n + 1);
