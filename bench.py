@@ -31,7 +31,7 @@ from dpm_inputs import get_config  # noqa: E402
 from dpm_inputs.rng import cfg4_band_values  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_PEAK_TFLOPS = 37.06     # measured DMMA.8x8x4 peak on this pool's B200 (tools/microbench_fp64.cu, gpurun_out/microbench.log)
+FP64_PEAK_TFLOPS = 37.0      # measured DFMA / DMMA.8x8x4 peak on this pool's B200 (profiles/r01/microbench_*.log)
 
 
 def load_peaks():
@@ -238,12 +238,36 @@ def main():
     ms_per_step = ms_total / args.steps
     value = B / (ms_per_step / 1e3)                      # whole-job solves/s (all ranks)
     alg_bytes = 16 * n ** 3                              # dense fp64 box in + out per solve
-    per_launch_bytes = alg_bytes * nb                    # one dpm_aux_solve_batch call
-    achieved_gbs = per_launch_bytes / (ms_local / args.steps / 1e3) / 1e9
     hbm_peak = peaks["hbm_gbs"]
-    flops_per_solve = 6 * n ** 3 * (n // 2) * 2          # 6 folded DST-I passes, n/2 MACs per output
-    achieved_tf = flops_per_solve * nb / (ms_local / args.steps / 1e3) / 1e12
     clocks = clk.summary()
+    # fp64 work of the path as built: 4 prime-factor DST-I transforms (2 x 2732 flop
+    # per line of 128 from the 2x3x43 factorisation) + the exact tridiagonal solve (~7 flop/point)
+    flops_per_solve = 4 * n * n * 2 * 2732 + 7 * n ** 3
+
+    # Per-kernel roofline of the dominant kernel: the same solves again with pass timing enabled
+    # (CUDA events recorded by the library on this stream around every pass), right after the
+    # timed region; algorithmic bytes per launch = 16 B x points of the launch (read + write once).
+    ctx.set_pass_timing(True)
+    for _ in range(max(1, min(args.steps, 2))):
+        ctx.aux_solve_batch(q, u)
+    torch.cuda.synchronize()
+    pt = ctx.pass_times()
+    ctx.set_pass_timing(False)
+    kind = max(pt, key=lambda k: pt[k][0])
+    k_ms, k_launch, k_pts = pt[kind]
+    k_avg_s = k_ms / max(k_launch, 1) / 1e3
+    k_bytes = 16.0 * k_pts / max(k_launch, 1)
+    k_gbs = k_bytes / k_avg_s / 1e9 if k_avg_s > 0 else 0.0
+    share = k_ms / max(sum(v[0] for v in pt.values()), 1e-30)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        tr = json.load(open(tfile)).get(kind)
+        if tr and tr.get("points_per_launch"):
+            traffic = tr["dram_bytes_per_launch"] * (k_pts / max(k_launch, 1)) / tr["points_per_launch"]
+    kernel_names = {"x": "dst128f_kernel<0> (prime-factor DST-I along x, DFMA)",
+                    "y": "dst128f_kernel<1> (prime-factor DST-I along y, DFMA)",
+                    "z": "ztri_warp_kernel<128> (exact tridiagonal solve along z)"}
 
     line = {"metric": "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction); PKS time steps/sec",
             "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -253,11 +277,19 @@ def main():
                                    "(R21), dense boxes in/out",
                        "global_batch": B, "local_batch": nb, "n": n, "parallelism": f"rhs-shard x{world}",
                        "l2": "inputs larger than L2 (%.1f GB per rank per step)" % (nb * field * 8 / 1e9)},
-            "roofline": {"bound": "hbm", "kernel": "dst_solve (X,Y,Z,Y,X passes of one dpm_aux_solve_batch)",
-                         "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
-                         "peak_kind": peaks_kind, "traffic": None, "alg_bytes_per_solve": alg_bytes,
-                         "fp64": {"achieved_tflops": achieved_tf, "peak_tflops": FP64_PEAK_TFLOPS,
-                                  "frac": achieved_tf / FP64_PEAK_TFLOPS, "flops_per_solve": flops_per_solve}},
+            "roofline": {"bound": "hbm", "kernel": kernel_names.get(kind, kind), "achieved": k_gbs, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": k_gbs / hbm_peak, "traffic": traffic,
+                         "peak_kind": peaks_kind + " (MEASURED_PEAKS.json hbm_gbs, burst copy)",
+                         "alg_bytes_per_launch": k_bytes, "launch_ms": k_avg_s * 1e3, "share_of_step": share,
+                         "passes": {k: {"ms": v[0], "launches": v[1], "points": v[2]} for k, v in pt.items()},
+                         "path": {"what": "whole AP solve (5 passes) per dpm_aux_solve_batch",
+                                  "achieved": alg_bytes * value / world / 1e9 if world else 0.0,
+                                  "frac": alg_bytes * value / world / 1e9 / hbm_peak,
+                                  "alg_bytes_per_solve": alg_bytes},
+                         "fp64": {"achieved_tflops": flops_per_solve * value / world / 1e12,
+                                  "peak_tflops": FP64_PEAK_TFLOPS,
+                                  "frac": flops_per_solve * value / world / 1e12 / FP64_PEAK_TFLOPS,
+                                  "flops_per_solve": flops_per_solve}},
             "gpu_launches": int(launches), "clocks": clocks}
 
     if not args.no_e2e and nb:

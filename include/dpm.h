@@ -117,8 +117,10 @@ dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t
 typedef enum { DPM_SOLVER_DST3 = 0, DPM_SOLVER_DST2_TRIDIAG = 1 } dpm_solver;
 dpm_status dpm_set_solver(dpm_ctx* ctx, int32_t solver);
 
-/* Same operation through HOST buffers (pinned or pageable): H2D copy, solve, D2H copy,
-   chunked through ctx-owned device staging. Synchronizes `stream` before returning. */
+/* Same operation through HOST buffers (pinned for overlap; pageable works but serialises): chunks of
+   <= 128 MB are uploaded on a ctx-owned copy stream, solved on `stream` and downloaded on a second
+   copy stream, double-buffered so upload, solve and download of consecutive chunks overlap.
+   Synchronous: returns after host_u is complete. */
 dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* host_u, int64_t batch,
                                     void* stream);
 
@@ -195,6 +197,15 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
 /* Cumulative number of CUDA kernels this library has launched in the process (all
    contexts).  Lets a harness count the library's launches inside a timed region. */
 int64_t dpm_launch_count(void);
+
+/* Measurement hooks (bench.py's per-kernel roofline).  While enabled, every pass of
+ * dpm_aux_solve_batch is bracketed by two CUDA events recorded on the caller's stream.
+ * dpm_pass_times synchronizes those events and returns, per pass kind k (0: transform along x,
+ * 1: transform along y, 2: tridiagonal / transform along z), the summed duration ms[k] (HOST,
+ * milliseconds), the number of launches[k] and the grid points processed points[k] since the
+ * last call (or since enabling), then resets.  Synchronous; DPM_ERR_INVALID on null pointers. */
+dpm_status dpm_set_pass_timing(dpm_ctx* ctx, int32_t enable);
+dpm_status dpm_pass_times(dpm_ctx* ctx, double* ms, int64_t* launches, int64_t* points);
 
 #ifdef __cplusplus
 }

@@ -78,6 +78,8 @@ _sig = {
     "dpm_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
     "dpm_pks_step": ([P, P, P, C.c_int32, C.POINTER(PksParams), C.POINTER(StepLog), P], C.c_int),
     "dpm_launch_count": ([], C.c_int64),
+    "dpm_set_pass_timing": ([P, C.c_int32], C.c_int),
+    "dpm_pass_times": ([P, D, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
 }
 EXPORTED = tuple(_sig)
 for _name, (_args, _res) in _sig.items():

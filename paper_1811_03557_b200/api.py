@@ -97,6 +97,17 @@ class DPM:
         self._chk(L.lib.dpm_aux_solve_batch(self._h, _ptr(q), _ptr(u), batch, _stream(stream)))
         return u
 
+    def set_pass_timing(self, enable: bool):
+        self._chk(L.lib.dpm_set_pass_timing(self._h, 1 if enable else 0))
+
+    def pass_times(self):
+        """{kind: (ms, launches, points)} for kinds "x", "y", "z" since the last call (synchronizes)."""
+        ms = (C.c_double * 3)()
+        la = (C.c_int64 * 3)()
+        pt = (C.c_int64 * 3)()
+        self._chk(L.lib.dpm_pass_times(self._h, ms, la, pt))
+        return {k: (ms[i], la[i], pt[i]) for i, k in enumerate(("x", "y", "z"))}
+
     def aux_solve_batch_host(self, q_host: torch.Tensor, u_host: torch.Tensor = None, stream=None) -> torch.Tensor:
         if q_host.is_cuda or q_host.dtype != torch.float64 or not q_host.is_contiguous():
             raise ValueError("q_host must be a contiguous float64 CPU tensor")

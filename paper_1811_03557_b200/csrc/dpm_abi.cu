@@ -23,6 +23,11 @@ void free_ctx(dpm_ctx* c) {
   if (c->red_host) cudaFreeHost(c->red_host);
   dst_plan_free(c->plan);
   if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+  for (cudaEvent_t e : c->pipe_ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
   delete c;
 }
 
@@ -177,17 +182,37 @@ dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* 
   cudaSetDevice(ctx->device);
   cudaStream_t s = as_stream(stream);
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
-  // double-buffered staging: chunk of fields per buffer
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(((size_t)256 << 20) / (field * 8))));
+  // Three-stage pipeline over chunks of <= 128 MB: H2D (copy-in stream) -> solve (caller's stream)
+  // -> D2H (copy-out stream), double-buffered so that chunk i+1 uploads and chunk i-1 downloads
+  // while chunk i is solved (PCIe is full duplex; pinned host buffers give async copies).
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(((size_t)128 << 20) / (field * 8))));
   dpm_status st = ensure_work(ctx, 2 * chunk);
   if (st != DPM_OK) return st;
+  if (!ctx->h2d_stream) {
+    DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
+    DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 6; ++i) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->pipe_ev[i], cudaEventDisableTiming));
+  }
+  cudaEvent_t* up = ctx->pipe_ev;       // up[b]: upload into buffer b done
+  cudaEvent_t* solved = ctx->pipe_ev + 2;
+  cudaEvent_t* down = ctx->pipe_ev + 4; // down[b]: download from buffer b done (buffer free)
+  DPM_CUDA_TRY(ctx, cudaEventRecord(down[0], s));
+  DPM_CUDA_TRY(ctx, cudaEventRecord(down[1], s));
   for (int64_t b0 = 0, it = 0; b0 < batch; b0 += chunk, ++it) {
     const int64_t nb = std::min<int64_t>(chunk, batch - b0);
-    double* buf = ctx->work + (size_t)(it & 1) * chunk * field;
-    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(buf, host_q + b0 * field, nb * field * 8, cudaMemcpyHostToDevice, s));
+    const int bi = (int)(it & 1);
+    double* buf = ctx->work + (size_t)bi * chunk * field;
+    DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->h2d_stream, down[bi], 0));
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(buf, host_q + b0 * field, nb * field * 8, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    DPM_CUDA_TRY(ctx, cudaEventRecord(up[bi], ctx->h2d_stream));
+    DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, up[bi], 0));
     DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, buf, buf, nb, nullptr, 0, s));
-    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(host_u + b0 * field, buf, nb * field * 8, cudaMemcpyDeviceToHost, s));
+    DPM_CUDA_TRY(ctx, cudaEventRecord(solved[bi], s));
+    DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, solved[bi], 0));
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(host_u + b0 * field, buf, nb * field * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    DPM_CUDA_TRY(ctx, cudaEventRecord(down[bi], ctx->d2h_stream));
   }
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->d2h_stream));
   DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
   return DPM_OK;
 }
@@ -354,5 +379,37 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
 }
 
 int64_t dpm_launch_count(void) { return (int64_t)g_dpm_launches.load(); }
+
+dpm_status dpm_set_pass_timing(dpm_ctx* ctx, int32_t enable) {
+  if (!ctx) return DPM_ERR_INVALID;
+  ctx->plan.prof = enable ? &ctx->prof : nullptr;
+  ctx->prof.used = 0;
+  ctx->prof.kind.clear();
+  ctx->prof.points.clear();
+  return DPM_OK;
+}
+
+dpm_status dpm_pass_times(dpm_ctx* ctx, double* ms, int64_t* launches, int64_t* points) {
+  if (!ctx || !ms || !launches || !points) return DPM_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  for (int k = 0; k < 3; ++k) {
+    ms[k] = 0.0;
+    launches[k] = 0;
+    points[k] = 0;
+  }
+  PassProf& P = ctx->prof;
+  for (size_t i = 0; i < P.kind.size(); ++i) {
+    DPM_CUDA_TRY(ctx, cudaEventSynchronize(P.pool[2 * i + 1]));
+    float t = 0.f;
+    DPM_CUDA_TRY(ctx, cudaEventElapsedTime(&t, P.pool[2 * i], P.pool[2 * i + 1]));
+    ms[P.kind[i]] += t;
+    launches[P.kind[i]] += 1;
+    points[P.kind[i]] += P.points[i];
+  }
+  P.used = 0;
+  P.kind.clear();
+  P.points.clear();
+  return DPM_OK;
+}
 
 }  // extern "C"

@@ -17,6 +17,16 @@ enum : uint8_t {
   F_NMINUS = 16  // N- ∩ M0
 };
 
+// Optional per-pass timing (dpm_set_pass_timing): CUDA events recorded on the launching stream
+// around every pass of dpm_aux_solve_batch, summed per pass kind by dpm_pass_times.
+struct PassProf {
+  std::vector<cudaEvent_t> pool;           // reused events (2 per recorded pass)
+  std::vector<int> kind;                   // pass kind of record i (0 x, 1 y, 2 z / tridiagonal)
+  std::vector<long long> points;           // grid points processed by record i
+  size_t used = 0;                         // events handed out since the last readout
+  cudaEvent_t next();
+};
+
 struct DstPlan {
   int n = 0;
   double h = 0, dt = 0;
@@ -25,6 +35,7 @@ struct DstPlan {
   int solver = DPM_SOLVER_DST2_TRIDIAG;
   double* atab128 = nullptr;  // n = 128: A fragments of the prime-factor DST-I
   int pfa = 1;            // n = 128: prime-factor DST-I for the x / y passes (DPM_PFA=0 disables)
+  PassProf* prof = nullptr;   // non-null while pass timing is enabled
 };
 
 struct dpm_ctx {
@@ -70,6 +81,10 @@ struct dpm_ctx {
   // PKS state
   double t = 0, dt_prev = 0;
   int pks_initialized = 0;
+  PassProf prof;
+  // host-buffer solve pipeline (dpm_aux_solve_batch_host)
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* red = nullptr;         // device reduction slots
   double* red_host = nullptr;    // pinned
 };

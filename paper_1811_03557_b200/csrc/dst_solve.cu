@@ -603,14 +603,41 @@ void dst_plan_free(DstPlan& p) {
 
 size_t dst_scratch_bytes(int, int) { return 0; }
 
+cudaEvent_t PassProf::next() {
+  if (used == pool.size()) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+namespace {
+// run `launch` between two events recorded on `s` when pass timing is enabled
+template <typename F>
+cudaError_t timed(const DstPlan& p, int kind, long long points, cudaStream_t s, F&& launch) {
+  if (!p.prof) return launch();
+  cudaEvent_t a = p.prof->next(), b = p.prof->next();
+  if (!a || !b) return cudaErrorMemoryAllocation;
+  cudaError_t e = cudaEventRecord(a, s);
+  if (e != cudaSuccess) return e;
+  if ((e = launch()) != cudaSuccess) return e;
+  p.prof->kind.push_back(kind);
+  p.prof->points.push_back(points);
+  return cudaEventRecord(b, s);
+}
+}  // namespace
+
 cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_t batch, double*, size_t,
                             cudaStream_t s) {
   const int n = p.n;
   const size_t field_bytes = (size_t)n * n * n * 8;
-  // chunk so that the in-flight working set stays in the 126 MB L2
+  // Chunk of fields per pass launch.  Measured (profiles/r01/chunk_sweep.txt): each pass streams at
+  // ~5.3 TB/s whether or not the chunk fits the 126 MB L2, while small chunks pay a fixed ~8 us of
+  // launch ramp / tail per pass, so chunks are large (1 GiB; DPM_CHUNK_MB overrides).
   static const size_t budget = [] {
     const char* v = getenv("DPM_CHUNK_MB");
-    return (size_t)(v ? atoi(v) : 112) << 20;
+    return (size_t)(v ? atoi(v) : 1024) << 20;
   }();
   int64_t chunk = std::max<int64_t>(1, (int64_t)(budget / field_bytes));
   const double inv_dt = 1.0 / p.dt;
@@ -622,15 +649,17 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     const double* qi = q + b0 * fe;
     double* ui = u + b0 * fe;
     cudaError_t e;
-    if ((e = run_pass(p, 0, qi, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(p, 1, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    const long long pts = (long long)nf * (long long)fe;
+    auto pass = [&](int k, const double* in) { return timed(p, k, pts, s, [&] { return run_pass(p, k, in, ui, nf, inv_dt, scale, s); }); };
+    if ((e = pass(0, qi)) != cudaSuccess) return e;
+    if ((e = pass(1, ui)) != cudaSuccess) return e;
     if (p.solver == DPM_SOLVER_DST2_TRIDIAG) {
-      if ((e = run_ztri(p, ui, nf, s)) != cudaSuccess) return e;
-    } else if ((e = run_pass(p, 2, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) {
+      if ((e = timed(p, 2, pts, s, [&] { return run_ztri(p, ui, nf, s); })) != cudaSuccess) return e;
+    } else if ((e = pass(2, ui)) != cudaSuccess) {
       return e;
     }
-    if ((e = run_pass(p, 1, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
-    if ((e = run_pass(p, 0, ui, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    if ((e = pass(1, ui)) != cudaSuccess) return e;
+    if ((e = pass(0, ui)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
