@@ -1,4 +1,5 @@
 // extern "C" entry points of libdpm.so (declared and documented in include/dpm.h).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -14,7 +15,7 @@ thread_local std::string g_create_err;
 void free_ctx(dpm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale,
+  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq,
                   c->lsq_ws, c->work, c->scratch, c->red};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -28,6 +29,12 @@ void free_ctx(dpm_ctx* c) {
   for (cudaEvent_t e : c->pipe_ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof.pool) cudaEventDestroy(e);
+  for (auto& g : c->pks_graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (c->graph_stream) cudaStreamDestroy(c->graph_stream);
+  if (c->pks_log) cudaFree(c->pks_log);
+  if (c->pks_log_host) cudaFreeHost(c->pks_log_host);
+  if (c->pks_backup) cudaFree(c->pks_backup);
   delete c;
 }
 
@@ -304,11 +311,91 @@ static double decode_key(double slot) {
   return v;
 }
 
+// Enqueue one PKS step (Steps 4a-7) at a fixed dt on stream s; `slot` receives red(3), dt_true
+// (device dt rule from the state at the start of the step) and the step statistics.
+static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_params* prm, double dt,
+                                   double* slot, double* backup, cudaStream_t s) {
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  double* fq = ctx->scratch;              // 2 boxes: f/dt on M+
+  double* wk = fq + 2 * field;            // 2 boxes: solves
+  double* gvec = wk + 2 * field;          // |gamma_in| x 2
+  double* ug = gvec + 2 * ngin;           // |gamma| x 2
+  double* coef = ug + 2 * ng;             // K x 2
+  if (backup) {
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(backup, rho, field * 8, cudaMemcpyDeviceToDevice, s));
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(backup + field, c, field * 8, cudaMemcpyDeviceToDevice, s));
+  }
+  if (prm->dt_rule == 0) {   // Step 3 on the device: did the speculative dt stay valid?
+    DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, slot, s));
+    DPM_CUDA_TRY(ctx, launch_dt_rule(ctx, slot, prm->chi, dt, prm->dt_cap, slot + 3, s));
+  }
+  // Step 4a: flux + IMEX right-hand sides, particular solutions
+  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s));
+  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+  // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp
+  DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
+  DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s));
+  // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
+  DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
+  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s));
+  return DPM_OK;
+}
+
+// Graph of K consecutive speculative steps at dt (captured once per (dt, K, params, fields), replayed).
+static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_params* prm, double dt, int K,
+                            dpm_ctx::PksGraph** out) {
+  for (auto& g : ctx->pks_graphs)
+    if (g.dt == dt && g.k == K && g.chi == prm->chi && g.cap == prm->dt_cap && g.rule == prm->dt_rule &&
+        g.clamp == prm->clamp && g.rho == rho && g.c == c) {
+      *out = &g;
+      return DPM_OK;
+    }
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  cudaStream_t cs = ctx->graph_stream;
+  PassProf* prof = ctx->plan.prof;
+  ctx->plan.prof = nullptr;   // no timing events inside graphs
+  const long long l0 = (long long)g_dpm_launches.load();
+  DPM_CUDA_TRY(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  dpm_status st = DPM_OK;
+  for (int i = 0; i < K && st == DPM_OK; ++i)
+    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs);
+  if (st == DPM_OK) {
+    cudaError_t e = cudaMemcpyAsync(ctx->pks_log_host, ctx->pks_log, (size_t)K * 16 * 8, cudaMemcpyDeviceToHost, cs);
+    if (e != cudaSuccess) { ctx->err = "capture memcpy"; st = DPM_ERR_CUDA; }
+  }
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+  ctx->plan.prof = prof;
+  const long long nk = (long long)g_dpm_launches.load() - l0;
+  g_dpm_launches.fetch_sub(nk);   // counted again on every replay
+  if (st != DPM_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ec != cudaSuccess) { ctx->err = std::string("graph capture: ") + cudaGetErrorString(ec); return DPM_ERR_CUDA; }
+  dpm_ctx::PksGraph g;
+  g.dt = dt; g.k = K; g.chi = prm->chi; g.cap = prm->dt_cap; g.rule = prm->dt_rule; g.clamp = prm->clamp;
+  g.rho = rho; g.c = c; g.launches = nk;
+  const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) { ctx->err = std::string("graph instantiate: ") + cudaGetErrorString(ei); return DPM_ERR_CUDA; }
+  if (ctx->pks_graphs.size() >= 8) {   // bounded cache
+    cudaGraphExecDestroy(ctx->pks_graphs.front().exec);
+    ctx->pks_graphs.erase(ctx->pks_graphs.begin());
+  }
+  ctx->pks_graphs.push_back(g);
+  *out = &ctx->pks_graphs.back();
+  return DPM_OK;
+}
+
 dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, const dpm_pks_params* prm,
                         dpm_step_log* log, void* stream) {
   if (!ctx || !rho || !c || !prm || nsteps < 0) return DPM_ERR_INVALID;
   if (!(prm->dt_cap > 0) || !(prm->chi > 0)) { ctx->err = "dt_cap and chi must be > 0"; return DPM_ERR_INVALID; }
   if (!ctx->pks_initialized) { ctx->t = 0.0; ctx->dt_prev = INFINITY; ctx->pks_initialized = 1; }
+  if (nsteps == 0) return DPM_OK;
   cudaSetDevice(ctx->device);
   cudaStream_t s = as_stream(stream);
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
@@ -317,63 +404,100 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
     if (ctx->scratch) cudaFree(ctx->scratch);
     ctx->scratch_bytes = (size_t)(4 * field + 2 * ngin + 2 * ng + 2 * ctx->K) * 8;
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, ctx->scratch_bytes));
+    for (auto& g : ctx->pks_graphs) cudaGraphExecDestroy(g.exec);   // captured with the old scratch
+    ctx->pks_graphs.clear();
   }
-  double* fq = ctx->scratch;              // 2 boxes: f/dt on M+
-  double* wk = fq + 2 * field;            // 2 boxes: solves
-  double* gvec = wk + 2 * field;          // |gamma_in| x 2
-  double* ug = gvec + 2 * ngin;           // |gamma| x 2
-  double* coef = ug + 2 * ng;             // K x 2
+  constexpr int KMAX = dpm_ctx::PKS_K;
+  if (!ctx->graph_stream) {
+    DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->graph_stream, cudaStreamNonBlocking));
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_log, KMAX * 16 * sizeof(double)));
+    DPM_CUDA_TRY(ctx, cudaMallocHost(&ctx->pks_log_host, KMAX * 16 * sizeof(double)));
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
+  }
+  cudaStream_t gs = ctx->graph_stream;
+  // the caller's prior work on `s` (e.g. dpm_pks_init) precedes the steps
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
   const double h = ctx->h;
-  for (int st = 0; st < nsteps; ++st) {
-    // Step 3: dt from the CFL condition (R19) and the dt rule (R13)
+  int done = 0;
+  double dt_next = NAN;   // dt already decided by a rejected speculation (device rule, exact)
+  while (done < nsteps) {
+    // Step 3: dt for the next batch.  Speculate dt_i = dt_{i-1}; the device evaluates the rule for
+    // every step of the batch and the batch is cut at the first step whose dt would decrease.
     double dt = prm->dt_cap;
     if (prm->dt_rule == 0) {
-      DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, ctx->red, s));
-      DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host, ctx->red, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-      DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-      double cfl = INFINITY;
-      for (int a = 0; a < 3; ++a) {
-        const double mx = ctx->red_host[a] / h;
-        if (mx > 0) cfl = std::fmin(cfl, h / (6.0 * prm->chi * mx));
+      if (!std::isnan(dt_next)) {
+        dt = dt_next;
+      } else if (std::isinf(ctx->dt_prev)) {   // first step: the rule on the host
+        DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, ctx->red, gs));
+        DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host, ctx->red, 3 * sizeof(double), cudaMemcpyDeviceToHost, gs));
+        DPM_CUDA_TRY(ctx, cudaStreamSynchronize(gs));
+        double cfl = INFINITY;
+        for (int a = 0; a < 3; ++a) {
+          const double mx = ctx->red_host[a] / h;
+          if (mx > 0) cfl = std::fmin(cfl, h / (6.0 * prm->chi * mx));
+        }
+        dt = std::fmin(std::fmin(ctx->dt_prev, prm->dt_cap), std::fmin(cfl, 0.5 * h * h));
+      } else {
+        dt = ctx->dt_prev;
       }
-      dt = std::fmin(std::fmin(ctx->dt_prev, prm->dt_cap), std::fmin(cfl, 0.5 * h * h));
     }
+    dt_next = NAN;
     // Step 2 / 4b: (re)build the BEP when dt differs from the one it was built at
     int rebuilt = 0;
     if (!ctx->have_projection || dt != ctx->dt_bep) {
       dpm_status r = dpm_set_dt(ctx, dt);
       if (r != DPM_OK) return r;
       ctx->have_projection = 0;
-      r = dpm_build_projection(ctx, nullptr, nullptr, stream);
+      r = dpm_build_projection(ctx, nullptr, nullptr, gs);
       if (r != DPM_OK) return r;
       rebuilt = 1;
     }
-    // Step 4a: flux + IMEX right-hand sides, particular solutions
-    DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s));
-    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
-    // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp
-    DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
-    DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s));
-    // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
-    DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
-    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
-    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
-    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-    ctx->dt_prev = dt;
-    ctx->t += dt;
-    if (ctx->red_host[12] != 0.0) { ctx->err = "non-finite value in the PKS step"; return DPM_ERR_NONFINITE; }
-    if (log) {
-      dpm_step_log& L = log[st];
-      L.t = ctx->t;
-      L.dt = dt;
-      L.mass = ctx->red_host[8] * h * h * h;
-      L.rho_max = decode_key(ctx->red_host[9]);
-      L.rho_min = -decode_key(ctx->red_host[10]);
-      L.c_min = -decode_key(ctx->red_host[11]);
-      L.rebuilt = rebuilt;
-      L.step = st;
+    const int K = std::min(KMAX, nsteps - done);
+    dpm_ctx::PksGraph* g = nullptr;
+    dpm_status st = pks_graph(ctx, rho, c, prm, dt, K, &g);
+    if (st != DPM_OK) return st;
+    DPM_CUDA_TRY(ctx, cudaGraphLaunch(g->exec, gs));
+    g_dpm_launches.fetch_add(g->launches);
+    DPM_CUDA_TRY(ctx, cudaStreamSynchronize(gs));
+    int accepted = K;
+    for (int i = 0; i < K; ++i) {
+      const double* L = ctx->pks_log_host + 16 * i;
+      if (prm->dt_rule == 0 && L[3] < dt) {   // this step needs a smaller dt: roll back to its start
+        DPM_CUDA_TRY(ctx, cudaMemcpyAsync(rho, ctx->pks_backup + (size_t)i * 2 * field, field * 8,
+                                          cudaMemcpyDeviceToDevice, gs));
+        DPM_CUDA_TRY(ctx, cudaMemcpyAsync(c, ctx->pks_backup + (size_t)i * 2 * field + field, field * 8,
+                                          cudaMemcpyDeviceToDevice, gs));
+        DPM_CUDA_TRY(ctx, cudaStreamSynchronize(gs));
+        dt_next = L[3];
+        accepted = i;
+        break;
+      }
+      ctx->dt_prev = dt;
+      ctx->t += dt;
+      if (L[8] != 0.0) {
+        if (i + 1 < K) {   // leave the state right after the failing step
+          DPM_CUDA_TRY(ctx, cudaMemcpyAsync(rho, ctx->pks_backup + (size_t)(i + 1) * 2 * field, field * 8,
+                                            cudaMemcpyDeviceToDevice, gs));
+          DPM_CUDA_TRY(ctx, cudaMemcpyAsync(c, ctx->pks_backup + (size_t)(i + 1) * 2 * field + field, field * 8,
+                                            cudaMemcpyDeviceToDevice, gs));
+          DPM_CUDA_TRY(ctx, cudaStreamSynchronize(gs));
+        }
+        ctx->err = "non-finite value in the PKS step";
+        return DPM_ERR_NONFINITE;
+      }
+      if (log) {
+        dpm_step_log& Lg = log[done + i];
+        Lg.t = ctx->t;
+        Lg.dt = dt;
+        Lg.mass = L[4] * h * h * h;
+        Lg.rho_max = decode_key(L[5]);
+        Lg.rho_min = -decode_key(L[6]);
+        Lg.c_min = -decode_key(L[7]);
+        Lg.rebuilt = (i == 0) ? rebuilt : 0;
+        Lg.step = done + i;
+      }
     }
+    done += accepted;
   }
   return DPM_OK;
 }

@@ -69,6 +69,7 @@ struct dpm_ctx {
   double* Q = nullptr;           // [K][n_gin]  equilibrated Q
   double* R = nullptr;           // [K][K] col-major upper triangular
   double* colscale = nullptr;    // [K]
+  double* Mlsq = nullptr;        // [K][n_gin] row-major: D R^{-1} Q^T (the LSQ apply operator)
   double bep_cond = 0;
   double* lsq_ws = nullptr;      // scratch
 
@@ -82,6 +83,21 @@ struct dpm_ctx {
   double t = 0, dt_prev = 0;
   int pks_initialized = 0;
   PassProf prof;
+  // PKS step graphs (dpm_pks_step): K speculative steps at a fixed dt captured once and replayed
+  static constexpr int PKS_K = 10;
+  struct PksGraph {
+    double dt = 0, chi = 0, cap = 0;
+    int k = 0, rule = 0, clamp = 0;
+    double* rho = nullptr;
+    double* c = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;
+  };
+  std::vector<PksGraph> pks_graphs;
+  cudaStream_t graph_stream = nullptr;
+  double* pks_log = nullptr;        // device [PKS_K][16]: red(3), dt_true, stats(5)
+  double* pks_log_host = nullptr;   // pinned mirror
+  double* pks_backup = nullptr;     // device [PKS_K][2][n^3]: state at the start of each step
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -142,3 +158,5 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
                              cudaStream_t s);
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s);
+cudaError_t launch_dt_rule(dpm_ctx* ctx, const double* red3, double chi, double dt_prev, double cap, double* dt_out,
+                           cudaStream_t s);

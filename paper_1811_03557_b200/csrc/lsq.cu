@@ -6,7 +6,9 @@
 // CholeskyQR2 gives an orthogonal Q to O(eps) when κ(A)^2 eps << 1 (κ of the equilibrated
 // BEP ≤ 1.85e4 at cfg1-3), and is built only from GEMM-shaped, fully
 // parallel steps plus a small K x K Cholesky.
-// Apply: coef = D R^{-1} Q^T g,  u_γ = E coef (extension operator), optional clamp (R17).
+// Apply: coef = M g with M = D R^{-1} Q^T formed once per factorisation (K x |γ_in|; one GEMV per
+// solve instead of a K-step back substitution), u_γ = E coef (extension operator),
+// optional clamp (R17).
 #include "dpm_internal.h"
 
 namespace {
@@ -127,49 +129,87 @@ __global__ void diag_ratio_kernel(const double* R, int K, double* out) {
   *out = mx / mn;
 }
 
-// z[c + r*K] = Q_c . g_r
-__global__ void qtg_kernel(const double* __restrict__ Q, int64_t m, int K, const double* __restrict__ g, int nrhs,
-                           double* z) {
+// R^{-1} of the upper-triangular K x K R (col-major), one column per thread (back substitution of e_j).
+__global__ void rinv_kernel(const double* __restrict__ R, int K, double* __restrict__ Ri) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  double* x = Ri + (size_t)j * K;
+  for (int i = K - 1; i > j; --i) x[i] = 0.0;
+  for (int i = j; i >= 0; --i) {
+    double v = (i == j) ? 1.0 : 0.0;
+    for (int k = i + 1; k <= j; ++k) v -= R[(size_t)k * K + i] * x[k];
+    x[i] = v / R[(size_t)i * K + i];
+  }
+}
+
+// M = diag(scale) R^{-1} Q^T  (K x m, row-major), Q col-major m x K (so Q^T rows are contiguous).
+// 32x32 output tiles, k-loop over 32-wide panels (R^{-1} upper: panels below the diagonal skipped).
+__global__ void lsq_operator_kernel(const double* __restrict__ Ri, const double* __restrict__ Q, const double* scale,
+                                    int K, int64_t m, double* __restrict__ M) {
+  const int c0 = blockIdx.y * 32;
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  __shared__ double sa[32][33], sb[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 256 threads: ty 0..7
+  double acc[4] = {0, 0, 0, 0};
+  for (int k0 = c0 - (c0 % 32); k0 < K; k0 += 32) {
+    for (int q = ty; q < 32; q += 8) {
+      const int c = c0 + q, k = k0 + tx;
+      sa[q][tx] = (c < K && k < K && k >= c) ? Ri[(size_t)k * K + c] : 0.0;   // Ri[c][k]
+      const int kk = k0 + q;
+      const int64_t i = i0 + tx;
+      sb[q][tx] = (kk < K && i < m) ? Q[(size_t)kk * m + i] : 0.0;             // Q^T[kk][i]
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const double b = sb[k][tx];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] += sa[ty + 8 * u][k] * b;
+    }
+    __syncthreads();
+  }
+  for (int u = 0; u < 4; ++u) {
+    const int c = c0 + ty + 8 * u;
+    const int64_t i = i0 + tx;
+    if (c < K && i < m) M[(size_t)c * m + i] = scale[c] * acc[u];
+  }
+}
+
+// coef[r][c] = Σ_i M[c][i] g[r][i]: one 128-thread block per (c, r)
+__global__ void lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K, const double* __restrict__ g, int nrhs,
+                                double* __restrict__ coef) {
   const int c = blockIdx.x, r = blockIdx.y;
-  const double* q = Q + (size_t)c * m;
-  const double* gr = g + (size_t)r * m;
+  const double* a = M + (size_t)c * m;
+  const double* b = g + (size_t)r * m;
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) s += q[i] * gr[i];
-  __shared__ double red[TB / 32];
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) s = fma(a[i], b[i], s);
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double red[4];
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0;
-    for (int w = 0; w < TB / 32; ++w) t += red[w];
-    z[(size_t)r * K + c] = t;
-  }
+  if (threadIdx.x == 0) coef[(size_t)r * K + c] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 
-// back substitution R x = z (one CTA per rhs), coef = scale .* x
-__global__ void backsub_kernel(const double* __restrict__ R, int K, double* z, const double* scale, double* coef) {
-  double* zr = z + (size_t)blockIdx.x * K;
-  for (int j = K - 1; j >= 0; --j) {
-    __syncthreads();
-    const double xj = zr[j] / R[(size_t)j * K + j];
-    __syncthreads();
-    if (threadIdx.x == 0) zr[j] = xj;
-    for (int i = threadIdx.x; i < j; i += blockDim.x) zr[i] -= R[(size_t)j * K + i] * xj;
-  }
+// u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
+// per block, coefficients staged in shared memory.
+__global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int r,
+                               int clamp, double* __restrict__ ug) {
+  extern __shared__ double sc[];   // K coefficients + 8 x 32 partial sums
+  const double* cr = coef + (size_t)r * K;
+  for (int c = threadIdx.x; c < K; c += blockDim.x) sc[c] = cr[c];
+  double* part = sc + K;
   __syncthreads();
-  for (int i = threadIdx.x; i < K; i += blockDim.x) coef[(size_t)blockIdx.x * K + i] = scale[i] * zr[i];
-}
-
-__global__ void extend_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int nrhs,
-                              int clamp, double* ug) {
-  const long tot = (long)ng * nrhs;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
-    const int r = (int)(t / ng);
-    const long g = t - (long)r * ng;
-    const double* cr = coef + (size_t)r * K;
-    double s = 0.0;
-    for (int c = 0; c < K; ++c) s += E[(size_t)c * ng + g] * cr[c];
-    ug[t] = clamp ? fmax(s, 0.0) : s;
+  const int gl = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * 32 + gl;
+  double s = 0.0;
+  if (g < ng)
+    for (int c = sl; c < K; c += 8) s = fma(E[(size_t)c * ng + g], sc[c], s);
+  part[sl * 32 + gl] = s;
+  __syncthreads();
+  if (sl == 0 && g < ng) {
+    double t = part[gl];
+    for (int q = 1; q < 8; ++q) t += part[q * 32 + gl];
+    ug[(size_t)r * ng + g] = clamp ? fmax(t, 0.0) : t;
   }
 }
 
@@ -218,6 +258,14 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   trmm_kernel<<<(K * K + 255) / 256, 256, 0, s>>>(R2, R1, ctx->R, K);
   DPM_COUNT_LAUNCH(1);
   diag_ratio_kernel<<<1, 1, 0, s>>>(ctx->R, K, dcond);
+  // apply operator M = D R^{-1} Q^T (K x |γ_in|): each LSQ solve is then one GEMV
+  if (!ctx->Mlsq) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->Mlsq, (size_t)m * K * sizeof(double)));
+  double* Ri = R1;   // R1 is free after the trmm
+  DPM_COUNT_LAUNCH(1);
+  rinv_kernel<<<(K + 63) / 64, 64, 0, s>>>(ctx->R, K, Ri);
+  DPM_COUNT_LAUNCH(1);
+  lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri, ctx->Q, ctx->colscale, K, m,
+                                                                                      ctx->Mlsq);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   int hfail = 0;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -234,16 +282,14 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
                       cudaStream_t s) {
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN], ng = ctx->counts[DPM_SET_GAMMA];
-  double* z = ctx->lsq_ws + 2 * (size_t)K * K + 16;
   DPM_COUNT_LAUNCH(1);
-  qtg_kernel<<<dim3(K, nrhs), TB, 0, s>>>(ctx->Q, m, K, g, nrhs, z);
-  DPM_COUNT_LAUNCH(1);
-  backsub_kernel<<<nrhs, 256, 0, s>>>(ctx->R, K, z, ctx->colscale, coef);
+  lsq_gemv_kernel<<<dim3(K, nrhs), 128, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
   if (u_gamma) {
-    const long tot = (long)ng * nrhs;
-    DPM_COUNT_LAUNCH(1);
-    extend_kernel<<<(int)std::min<long>((tot + TB - 1) / TB, 148 * 16), TB, 0, s>>>(ctx->E, ng, K, coef, nrhs, clamp,
-                                                                                 u_gamma);
+    const size_t smem = (size_t)(K + 256) * sizeof(double);
+    for (int r = 0; r < nrhs; ++r) {
+      DPM_COUNT_LAUNCH(1);
+      extend2_kernel<<<(unsigned)((ng + 31) / 32), 256, smem, s>>>(ctx->E, ng, K, coef, r, clamp, u_gamma);
+    }
   }
   return cudaGetLastError();
 }

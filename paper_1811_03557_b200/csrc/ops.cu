@@ -278,6 +278,18 @@ __global__ void pks_init_kernel(const uint8_t* __restrict__ flags, const int32_t
   }
 }
 
+// Step 3 dt rule on the device (R13), identical arithmetic to the host rule:
+//   cfl = min_a h / (6 χ max|Δc|_a / h),  dt = min(min(dt_prev, cap), min(cfl, h^2/2)).
+__global__ void dt_rule_kernel(const double* __restrict__ red3, double h, double chi, double dt_prev, double cap,
+                               double* dt_out) {
+  double cfl = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    const double mx = red3[a] / h;
+    if (mx > 0) cfl = fmin(cfl, h / (6.0 * chi * mx));
+  }
+  *dt_out = fmin(fmin(dt_prev, cap), fmin(cfl, 0.5 * h * h));
+}
+
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
 
 }  // namespace
@@ -347,6 +359,13 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
   DPM_COUNT_LAUNCH(1);
   green_rhs_kernel<<<grid_for(nn * nrhs), TB, 0, s>>>(ctx->flags, ctx->gmap, ctx->n, fq, u_gamma,
                                                       ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dt_rule(dpm_ctx* ctx, const double* red3, double chi, double dt_prev, double cap, double* dt_out,
+                           cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  dt_rule_kernel<<<1, 1, 0, s>>>(red3, ctx->h, chi, dt_prev, cap, dt_out);
   return cudaGetLastError();
 }
 
