@@ -216,3 +216,21 @@ def test_cfg4_full_batch_sampled(api):
         uo = ap.solve(qo, g.h, cfg.dt)
         assert rel(u[b].cpu().numpy(), uo) <= 1e-11
     assert torch.isfinite(u).all()
+
+
+def test_pks_parity_dt_decrease_rollback(api):
+    """cfg2 geometry with a weak c0 and a large dt cap: the CFL dt (R13) decreases at steps 1 and 2,
+    so the BEP is rebuilt (Step 4b) and the GPU's speculative K-step graphs must roll back
+    to the start of those steps.  Oracle: 3 builds, dt 2e-3 -> 1.231e-3 -> 1.199e-3."""
+    from dataclasses import replace
+    cfg = replace(get_config("cfg2"), ic_c=(1.0, 50.0), dt=2e-3, steps=14)
+    o = pks.PKSOracle(cfg, dt_rule=0)
+    ro, co, ologs = o.run()
+    assert o.builds == 3
+    _, rho, cc, logs = run_pks_gpu(api, cfg, 0)
+    assert rel(rho, ro) <= 1e-9, rel(rho, ro)
+    assert rel(cc, co) <= 1e-9, rel(cc, co)
+    assert [l["step"] for l in logs] == list(range(cfg.steps))
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
+        assert bool(lg["rebuilt"]) == bool(lo["rebuilt"])
