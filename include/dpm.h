@@ -194,6 +194,54 @@ dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* 
 dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, const dpm_pks_params* params,
                         dpm_step_log* log, void* stream);
 
+/* ---------------------------------------------------------------------------------
+ * Config 5: octant domain decomposition (the paper's DD: coupled BEPs sharing
+ * the interface Cauchy data P:477-480; duplicated equations + averaged effective density at
+ * points near several pieces, Case 2 P:562-571; octant pieces, bases and rules: SURVEY R24,
+ * R25, R31, listed in DESIGN.md §3).  One context per octant subdomain s (0..7, sign bits
+ * s = 4[σx<0] + 2[σy<0] + [σz<0]) in its canonical frame: grid = the box [lo, hi]^3 (cfg5:
+ * [-0.1, 1.1]^3), Ω_s = open octant ∩ ball(radius); physical coordinates x = σ ⊙ p.
+ * K = 2 (lmax_cap+1)^2 + 6 nφ global unknowns, nφ = (deg_if+1)(deg_if+2)/2:
+ *   [cap Y_ν | cap (d^2/2) Y_ν | plane x: φ, x φ | plane y: φ, y φ | plane z: φ, z φ],
+ *   φ_jk = P_j(s) P_k(t) (Legendre, j + k <= deg_if, by total degree then j descending),
+ *   (s, t) = the other two physical coordinates in axis order.
+ * The global least squares (all octants' BEP rows stacked, columns equilibrated) is a
+ * distributed CholeskyQR2; the caller sums, over all octants (NCCL all-reduce across ranks):
+ *   colnorm2 -> gram(pass 1) -> chol(1) -> gram(2) -> chol(2)    (once per dt)
+ *   per step: local_begin gives y_s (K x 2); C = Σ_s y_s; local_finish(C).
+ * All pointers are DEVICE unless stated; all calls are on `stream`; "synchronous" ones say so.
+ * ------------------------------------------------------------------------------- */
+dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius, int32_t lmax_cap,
+                             int32_t deg_if, double dt, int32_t device, dpm_ctx** out);
+/* n_rows = BEP rows of this octant (γ_in points x their pieces), K = global unknowns (HOST). */
+dpm_status dpm_dd_info(const dpm_ctx* ctx, int64_t* n_rows, int32_t* K);
+/* HOST [n_gamma] piece bits of every γ point (1 cap, 2 x-plane, 4 y-plane, 8 z-plane). */
+dpm_status dpm_dd_copy_assign(const dpm_ctx* ctx, uint8_t* host_bits);
+/* K AP solves of the potentials of the effective density columns at the ctx's dt, then the
+   BEP block B_s (n_rows x K column-major, kept in ctx; copied to B_out if non-NULL). */
+dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream);
+/* nrm2[c] = Σ_rows B_s[:, c]^2 (K). */
+dpm_status dpm_dd_colnorm2(dpm_ctx* ctx, double* nrm2, void* stream);
+/* pass 1: D = 1/sqrt(nrm2_sum) (synchronizes), Q1 = B_s D, G = Q1^T Q1;  pass 2: G = Q1^T Q1
+   with the pass-1 Q1.  G: K x K (upper triangle valid). */
+dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, double* G, void* stream);
+/* Cholesky of the summed Gram (pass 1: R1, Q1 <- Q1 R1^{-1}; pass 2: R2, Q <- Q1 R2^{-1},
+   R = R2 R1, M_s = D R^{-1} Q^T).  Synchronous; DPM_ERR_RANK on breakdown. */
+dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* stream);
+/* R31 initial state (rho, c on N+, [n][n][n]). */
+dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream);
+/* Local CFL bound h / (6 χ max|Δc|/h) (R19) -> *cfl_dt (HOST).  Synchronous. */
+dpm_status dpm_dd_cfl(dpm_ctx* ctx, const double* c, double chi, double* cfl_dt, void* stream);
+/* Step 4a-5 at the ctx's dt (the factorisation must be at this dt): flux + IMEX RHS, particular
+   solves, BEP right-hand sides on the rows, y = M_s g (K x 2, field-major). */
+dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* y,
+                              void* stream);
+/* Steps 5-7 with the global C (K x 2): u_γ = A C (clamped at 0 if clamp, R17), Green's formula
+   (R20), restriction to N+.  stats (HOST, 5): [h^3 Σ_{M+} ρ, max ρ, min ρ, min c, nonfinite].
+   Synchronous. */
+dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, double* rho, double* c,
+                               double* stats, void* stream);
+
 /* Cumulative number of CUDA kernels this library has launched in the process (all
    contexts).  Lets a harness count the library's launches inside a timed region. */
 int64_t dpm_launch_count(void);

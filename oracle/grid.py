@@ -113,10 +113,29 @@ class PointSets:
         return np.flatnonzero(m.ravel()).astype(np.int64)
 
 
+def octant_inside_mask(grid: Grid, radius=1.0) -> np.ndarray:
+    """cfg5 subdomain in its canonical frame: the open octant
+    {x, y, z > 0} ∩ {|x| < radius}, exact rationals; nodes on a plane or on the sphere go to M-."""
+    n = grid.n
+    lo, hi, r = _frac(grid.lo), _frac(grid.hi), _frac(radius)
+    xs = [lo + (i + 1) * (hi - lo) / (n + 1) for i in range(n)]
+    den = reduce(_lcm, [v.denominator for v in xs] + [r.denominator], 1)
+    X = np.array([int(v * den) for v in xs], dtype=object)
+    pos = X > 0
+    sq = X * X
+    tot = sq[:, None, None] + sq[None, :, None] + sq[None, None, :]
+    inside = np.asarray(tot < int(r * den) ** 2, dtype=bool)
+    return inside & pos[:, None, None] & pos[None, :, None] & pos[None, None, :]
+
+
 def point_sets(grid: Grid, kind: str, center, semi) -> PointSets:
     """Definition 1 on the (n+2)^3 lattice N0 including the ghost layer (R5)."""
+    return point_sets_from_mask(grid, inside_mask(grid, kind, center, semi))
+
+
+def point_sets_from_mask(grid: Grid, mplus: np.ndarray) -> PointSets:
+    """Definition 1 for a given M+ mask."""
     n = grid.n
-    mplus = inside_mask(grid, kind, center, semi)
     lat = np.zeros((n + 2,) * 3, dtype=bool)
     mp_lat = lat.copy()
     mp_lat[1:-1, 1:-1, 1:-1] = mplus

@@ -79,6 +79,18 @@ _sig = {
     "dpm_pks_step": ([P, P, P, C.c_int32, C.POINTER(PksParams), C.POINTER(StepLog), P], C.c_int),
     "dpm_launch_count": ([], C.c_int64),
     "dpm_set_pass_timing": ([P, C.c_int32], C.c_int),
+    "dpm_create_octant": ([C.POINTER(Grid), C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                           C.POINTER(P)], C.c_int),
+    "dpm_dd_info": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
+    "dpm_dd_copy_assign": ([P, C.POINTER(C.c_uint8)], C.c_int),
+    "dpm_dd_bep_block": ([P, P, P], C.c_int),
+    "dpm_dd_colnorm2": ([P, P, P], C.c_int),
+    "dpm_dd_gram": ([P, C.c_int32, P, P, P], C.c_int),
+    "dpm_dd_chol": ([P, C.c_int32, P, P], C.c_int),
+    "dpm_dd_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
+    "dpm_dd_cfl": ([P, P, C.c_double, D, P], C.c_int),
+    "dpm_dd_local_begin": ([P, P, P, C.c_double, P, P], C.c_int),
+    "dpm_dd_local_finish": ([P, P, C.c_int32, P, P, D, P], C.c_int),
     "dpm_pass_times": ([P, D, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
 }
 EXPORTED = tuple(_sig)

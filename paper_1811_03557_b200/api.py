@@ -194,3 +194,69 @@ def dpm_boundary_lsq(ctx: DPM, g, stream=None):
 
 def dpm_pks_step(ctx: DPM, rho, c, nsteps, **kw):
     return ctx.pks_step(rho, c, nsteps, **kw)
+
+
+class Octant(DPM):
+    """One config-5 octant subdomain (dpm_create_octant): canonical frame, box [lo, hi]^3."""
+
+    def __init__(self, n, lo, hi, octant, radius=1.0, lmax_cap=12, deg_if=12, dt=1e-5, device=0):
+        g = L.Grid(n, lo, hi)
+        h = C.c_void_p()
+        torch.cuda.init()
+        L.check(L.lib.dpm_create_octant(C.byref(g), octant, radius, lmax_cap, deg_if, dt, device, C.byref(h)))
+        self._h = h
+        self.device = torch.device("cuda", device)
+        self.n = n
+        self.octant = octant
+        self.info = self.query()
+        rows = C.c_int64()
+        K = C.c_int32()
+        self._chk(L.lib.dpm_dd_info(self._h, C.byref(rows), C.byref(K)))
+        self.n_rows, self.K = rows.value, K.value
+
+    def copy_assign(self) -> np.ndarray:
+        out = np.empty(max(self.info["n_gamma"], 1), dtype=np.uint8)
+        self._chk(L.lib.dpm_dd_copy_assign(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out[: self.info["n_gamma"]]
+
+    def _t(self, *shape):
+        return torch.empty(shape, dtype=torch.float64, device=self.device)
+
+    def bep_block(self, want=False, stream=None):
+        B = self._t(self.K, self.n_rows) if want else None       # row c = column c of B_s
+        self._chk(L.lib.dpm_dd_bep_block(self._h, _ptr(B), _stream(stream)))
+        return B
+
+    def colnorm2(self, stream=None):
+        out = self._t(self.K)
+        self._chk(L.lib.dpm_dd_colnorm2(self._h, _ptr(out), _stream(stream)))
+        return out
+
+    def gram(self, pass_, nrm2_sum=None, stream=None):
+        G = self._t(self.K, self.K)
+        self._chk(L.lib.dpm_dd_gram(self._h, pass_, _ptr(nrm2_sum), _ptr(G), _stream(stream)))
+        return G
+
+    def chol(self, pass_, G_sum, stream=None):
+        self._chk(L.lib.dpm_dd_chol(self._h, pass_, _ptr(_dev_f64(G_sum, "G_sum")), _stream(stream)))
+
+    def dd_pks_init(self, rho, c, center, rho_amp, rho_rate, c_amp, c_rate, stream=None):
+        ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate)
+        self._chk(L.lib.dpm_dd_pks_init(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), C.byref(ic),
+                                        _stream(stream)))
+
+    def cfl(self, c, chi=1.0, stream=None) -> float:
+        out = C.c_double()
+        self._chk(L.lib.dpm_dd_cfl(self._h, _ptr(_dev_f64(c, "c")), chi, C.byref(out), _stream(stream)))
+        return out.value
+
+    def local_begin(self, rho, c, chi=1.0, stream=None):
+        y = self._t(2, self.K)
+        self._chk(L.lib.dpm_dd_local_begin(self._h, _ptr(rho), _ptr(c), chi, _ptr(y), _stream(stream)))
+        return y
+
+    def local_finish(self, Cglob, rho, c, clamp=1, stream=None):
+        st = (C.c_double * 5)()
+        self._chk(L.lib.dpm_dd_local_finish(self._h, _ptr(_dev_f64(Cglob, "C")), clamp, _ptr(rho), _ptr(c), st,
+                                            _stream(stream)))
+        return {"mass": st[0], "rho_max": st[1], "rho_min": st[2], "c_min": st[3], "nonfinite": st[4]}

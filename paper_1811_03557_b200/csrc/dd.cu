@@ -1,0 +1,495 @@
+// Config 5: octant domain decomposition (the paper's DD with
+// duplicated equations and averaged effective densities, Case 2 P:562-571).
+//
+// One dpm_ctx per octant subdomain, in its canonical frame p (box [-0.1, 1.1]^3, Ω = open octant ∩
+// unit ball); physical coordinates x = σ ⊙ p.  Global unknowns (shared by all octants):
+//   [cap: Y_ν | (d^2/2) Y_ν], ν < (Lc+1)^2          zero-Neumann cap, d = |x| - 1
+//   [plane a: φ_jk | d φ_jk], j + k <= Li, a = x,y,z  2-term interface Cauchy data, d = x_a (R25)
+// φ_jk(s, t) = P_j(s) P_k(t) (Legendre) of the two other physical coordinates in increasing axis
+// order; (j, k) ordered by total degree g, then j = g..0.
+// Piece assignment: p ∈ γ is on piece π iff its foot on π's carrier lies within ε = 2h of π and
+// |distance to the carrier| < 2h.  Effective density A = mean of the assigned pieces' extension
+// rows (used for the potentials); BEP rows: one per (p ∈ γ_in, π ∈ pieces(p)): E_π[p] - (P_γ A)[p].
+// The global least squares over all octants is a distributed CholeskyQR2: Gram matrices and the
+// per-step M_s g_s vectors are summed across octants by the caller (NCCL all-reduce).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dpm_internal.h"
+#include "sh_device.cuh"
+
+namespace {
+
+constexpr int TB = 256;
+
+__device__ __forceinline__ void legendre_all(double x, int jmax, double* P) {
+  P[0] = 1.0;
+  if (jmax >= 1) P[1] = x;
+  for (int j = 1; j < jmax; ++j) P[j + 1] = ((2 * j + 1) * x * P[j] - j * P[j - 1]) / (j + 1);
+}
+
+__device__ __forceinline__ double dist_quarter_disc(double s, double t) {
+  const double ps = fmax(s, 0.0), pt = fmax(t, 0.0);
+  const double r = hypot(ps, pt);
+  const double sc = r > 1.0 ? 1.0 / r : 1.0;
+  return hypot(s - ps * sc, t - pt * sc);
+}
+
+__device__ __forceinline__ double dist_octant_cap(const double f[3]) {
+  double q[3], nq = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    q[a] = fmax(f[a], 0.0);
+    nq += q[a] * q[a];
+  }
+  nq = sqrt(nq);
+  double d2 = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    const double v = f[a] - (nq > 0 ? q[a] / nq : q[a]);
+    d2 += v * v;
+  }
+  return sqrt(d2);
+}
+
+// Per γ point: piece bits, every piece's extension row (Eraw) and the averaged density row (A).
+__global__ void dd_extension_kernel(const int64_t* gamma, int64_t ng, int n, double lo, double h, double radius,
+                                    double sx, double sy, double sz, int Lc, int Li, int nphi, int K, double* Eraw,
+                                    double* A, uint8_t* assign) {
+  const long g = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int64_t pidx = gamma[g];
+  const int i = (int)(pidx / ((long)n * n)), j = (int)((pidx / n) % n), k = (int)(pidx % n);
+  const double P[3] = {lo + (i + 1) * h, lo + (j + 1) * h, lo + (k + 1) * h};   // canonical
+  const double sg[3] = {sx, sy, sz};
+  double X[3];
+  for (int a = 0; a < 3; ++a) X[a] = sg[a] * P[a];                              // physical
+  const double eps = 2.0 * h;
+  const double r = sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]);
+  // assignment (frame-independent)
+  int bits = 0;
+  {
+    const double f[3] = {P[0] / r, P[1] / r, P[2] / r};
+    if (dist_octant_cap(f) <= eps && fabs(r - radius) < 2.0 * h) bits |= 1;
+  }
+  for (int a = 0; a < 3; ++a) {
+    const int o0 = a == 0 ? 1 : 0, o1 = a == 2 ? 1 : 2;
+    if (dist_quarter_disc(P[o0], P[o1]) <= eps && fabs(P[a]) < 2.0 * h) bits |= 2 << a;
+  }
+  assign[g] = (uint8_t)bits;
+  const int cnt = __popc(bits);
+  const double inv = cnt ? 1.0 / cnt : 0.0;
+  // cap block: Y(x/|x|), (d^2/2) Y, d = |x| - radius
+  const int nc = (Lc + 1) * (Lc + 1);
+  const double dcap = r - radius;
+  const double wc = 0.5 * dcap * dcap;
+  const double ac = (bits & 1) ? inv : 0.0;
+  real_sh_unit(X[0] / r, X[1] / r, X[2] / r, Lc, [&](int nu, double v) {
+    Eraw[(size_t)nu * ng + g] = v;
+    Eraw[(size_t)(nc + nu) * ng + g] = wc * v;
+    A[(size_t)nu * ng + g] = ac * v;
+    A[(size_t)(nc + nu) * ng + g] = ac * wc * v;
+  });
+  // plane blocks
+  double Ps[32], Pt[32];
+  for (int a = 0; a < 3; ++a) {
+    const int o0 = a == 0 ? 1 : 0, o1 = a == 2 ? 1 : 2;
+    legendre_all(X[o0], Li, Ps);
+    legendre_all(X[o1], Li, Pt);
+    const double d = X[a];
+    const double ap = (bits & (2 << a)) ? inv : 0.0;
+    const int c0 = 2 * nc + 2 * nphi * a;
+    int m = 0;
+    for (int gd = 0; gd <= Li; ++gd)
+      for (int jj = gd; jj >= 0; --jj, ++m) {
+        const double phi = Ps[jj] * Pt[gd - jj];
+        Eraw[(size_t)(c0 + m) * ng + g] = phi;
+        Eraw[(size_t)(c0 + nphi + m) * ng + g] = d * phi;
+        A[(size_t)(c0 + m) * ng + g] = ap * phi;
+        A[(size_t)(c0 + nphi + m) * ng + g] = ap * d * phi;
+      }
+  }
+}
+
+// B[i][c] = [c in block(piece_i)] Eraw[pos_i][c] - U_c[gamma[pos_i]]  (column-major n_rows x nc)
+__global__ void dd_bep_gather_kernel(const double* __restrict__ U, int ncols, size_t field,
+                                     const int64_t* __restrict__ gamma, int64_t ng, const int32_t* __restrict__ rows,
+                                     int64_t nrows, const double* __restrict__ Eraw, int c0, int nc, int nphi,
+                                     double* B) {
+  const long tot = (long)nrows * ncols;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
+    const int cl = (int)(t / nrows);
+    const long ri = t - (long)cl * nrows;
+    const int pos = rows[2 * ri], piece = rows[2 * ri + 1];
+    const int c = c0 + cl;
+    const int blk = c < 2 * nc ? 0 : 1 + (c - 2 * nc) / (2 * nphi);
+    double v = -U[(size_t)cl * field + gamma[pos]];
+    if (blk == piece) v += Eraw[(size_t)c * ng + pos];
+    B[(size_t)cl * nrows + ri] = v;
+  }
+}
+
+// g[r][i] = u_r[gamma[pos_i]]  (BEP right-hand sides replicated over a point's pieces)
+__global__ void dd_rows_trace_kernel(const double* __restrict__ U, size_t field, const int64_t* __restrict__ gamma,
+                                     const int32_t* __restrict__ rows, int64_t nrows, int nrhs, double* g) {
+  const long tot = (long)nrows * nrhs;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(t / nrows);
+    const long i = t - (long)r * nrows;
+    g[t] = U[(size_t)r * field + gamma[rows[2 * i]]];
+  }
+}
+
+__global__ void colsumsq_kernel(const double* __restrict__ B, int64_t m, double* out) {
+  const int c = blockIdx.x;
+  const double* col = B + (size_t)c * m;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) s = fma(col[i], col[i], s);
+  __shared__ double red[TB / 32];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int q = 0; q < TB / 32; ++q) t += red[q];
+    out[c] = t;
+  }
+}
+
+// R31 initial state: IC at the node on N+ (physical coordinates); on γ the average over the point's
+// pieces of the piece's extension of the IC Cauchy data (cap: u0(foot); plane: u0 + d ∂_a u0).
+__global__ void dd_ic_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap,
+                             const uint8_t* __restrict__ assign, int n, double lo, double h, double radius, double sx,
+                             double sy, double sz, dpm_pks_ic ic, double* rho, double* c) {
+  const long nn = (long)n * n * n;
+  const double sg[3] = {sx, sy, sz};
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    double a = 0.0, b = 0.0;
+    if (flags[p] & F_NPLUS) {
+      const int i = (int)(p / ((long)n * n)), j = (int)((p / n) % n), k = (int)(p % n);
+      const double X[3] = {sg[0] * (lo + (i + 1) * h), sg[1] * (lo + (j + 1) * h), sg[2] * (lo + (k + 1) * h)};
+      auto u0 = [&](const double F[3], double amp, double rate) {
+        double r2 = 0.0;
+        for (int q = 0; q < 3; ++q) r2 += (F[q] - ic.center[q]) * (F[q] - ic.center[q]);
+        return amp * exp(-rate * r2);
+      };
+      const int gp = gmap[p];
+      if (gp < 0) {
+        a = u0(X, ic.rho_amp, ic.rho_rate);
+        b = u0(X, ic.c_amp, ic.c_rate);
+      } else {
+        const int bits = assign[gp];
+        const double r = sqrt(X[0] * X[0] + X[1] * X[1] + X[2] * X[2]);
+        int cnt = 0;
+        if (bits & 1) {
+          const double F[3] = {radius * X[0] / r, radius * X[1] / r, radius * X[2] / r};
+          a += u0(F, ic.rho_amp, ic.rho_rate);
+          b += u0(F, ic.c_amp, ic.c_rate);
+          ++cnt;
+        }
+        for (int ax = 0; ax < 3; ++ax) {
+          if (!(bits & (2 << ax))) continue;
+          double F[3] = {X[0], X[1], X[2]};
+          F[ax] = 0.0;
+          const double d = X[ax];
+          const double ur = u0(F, ic.rho_amp, ic.rho_rate), uc = u0(F, ic.c_amp, ic.c_rate);
+          a += ur + d * (-2.0 * ic.rho_rate * (F[ax] - ic.center[ax]) * ur);
+          b += uc + d * (-2.0 * ic.c_rate * (F[ax] - ic.center[ax]) * uc);
+          ++cnt;
+        }
+        a /= cnt;
+        b /= cnt;
+      }
+    }
+    rho[p] = a;
+    c[p] = b;
+  }
+}
+
+int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
+
+}  // namespace
+
+dpm_status dd_setup(dpm_ctx* ctx) {
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  cudaStream_t s = ctx->setup_stream;
+  const int K = ctx->K;
+  DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_Eraw, (size_t)ng * K * sizeof(double)));
+  DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->E, (size_t)ng * K * sizeof(double)));
+  DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_assign, std::max<int64_t>(ng, 1)));
+  DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->foot, 8));   // unused for octants (IC computed from geometry)
+  DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dist, 8));
+  DPM_COUNT_LAUNCH(1);
+  dd_extension_kernel<<<(unsigned)((ng + 127) / 128), 128, 0, s>>>(
+      ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1], ctx->sigma[2],
+      ctx->Lc, ctx->Li, ctx->nphi, K, ctx->dd_Eraw, ctx->E, ctx->dd_assign);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  // BEP rows: γ_in points (ascending) x their pieces (cap, x, y, z order)
+  std::vector<uint8_t> bits(ng);
+  std::vector<int32_t> ginpos(ngin);
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(bits.data(), ctx->dd_assign, ng, cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ginpos.data(), ctx->gin_pos, ngin * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  std::vector<int32_t> rows;
+  for (int64_t i = 0; i < ng; ++i)
+    if (bits[i] == 0) {
+      ctx->err = "octant DD: a gamma point is on no boundary piece";
+      return DPM_ERR_INVALID;
+    }
+  for (int64_t q = 0; q < ngin; ++q)
+    for (int pc = 0; pc < 4; ++pc)
+      if (bits[ginpos[q]] & (1 << pc)) {
+        rows.push_back(ginpos[q]);
+        rows.push_back(pc);
+      }
+  ctx->n_rows = (int64_t)rows.size() / 2;
+  DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_rows, std::max<size_t>(rows.size(), 2) * sizeof(int32_t)));
+  DPM_CUDA_TRY(ctx, cudaMemcpy(ctx->dd_rows, rows.data(), rows.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  return DPM_OK;
+}
+
+namespace {
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+dpm_status dd_check(dpm_ctx* ctx) {
+  if (!ctx) return DPM_ERR_INVALID;
+  if (!ctx->dd) { ctx->err = "not an octant subdomain context"; return DPM_ERR_INVALID; }
+  cudaSetDevice(ctx->device);
+  return DPM_OK;
+}
+
+dpm_status dd_alloc(dpm_ctx* ctx) {
+  const size_t K = ctx->K, m = (size_t)std::max<int64_t>(ctx->n_rows, 1);
+  if (!ctx->dd_B) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_B, K * m * sizeof(double)));
+  if (!ctx->dd_Q) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_Q, K * m * sizeof(double)));
+  if (!ctx->dd_M) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_M, K * m * sizeof(double)));
+  if (!ctx->dd_R) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_R, 4 * K * K * sizeof(double) + 64));
+  if (!ctx->dd_D) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_D, K * sizeof(double)));
+  if (!ctx->dd_g) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_g, 2 * m * sizeof(double)));
+  return DPM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius, int32_t lmax_cap, int32_t deg_if,
+                             double dt, int32_t device, dpm_ctx** out) {
+  if (out) *out = nullptr;
+  if (!grid || !out || octant < 0 || octant > 7 || !(radius > 0) || lmax_cap < 0 || lmax_cap > 40 || deg_if < 0 ||
+      deg_if > 30 || !(grid->lo < 0 && grid->hi > radius))
+    return DPM_ERR_INVALID;
+  dpm_domain D{};
+  D.kind = DPM_OCTANT_CANON;
+  D.semi[0] = D.semi[1] = D.semi[2] = radius;
+  // dpm_create validates the grid and builds the point sets + AP plan; the extension data is ours
+  dpm_status st = dpm_create_impl(grid, &D, 0, dt, DPM_BASIS_NEUMANN0, device, out);
+  if (st != DPM_OK) return st;
+  dpm_ctx* ctx = *out;
+  ctx->dd = 1;
+  ctx->octant = octant;
+  for (int a = 0; a < 3; ++a) ctx->sigma[a] = ((octant >> (2 - a)) & 1) ? -1.0 : 1.0;
+  ctx->radius = radius;
+  ctx->Lc = lmax_cap;
+  ctx->Li = deg_if;
+  ctx->nphi = (deg_if + 1) * (deg_if + 2) / 2;
+  ctx->K = 2 * (lmax_cap + 1) * (lmax_cap + 1) + 6 * ctx->nphi;
+  ctx->lmax = lmax_cap;
+  if (ctx->E) { cudaFree(ctx->E); ctx->E = nullptr; }
+  if (ctx->foot) { cudaFree(ctx->foot); ctx->foot = nullptr; }
+  if (ctx->dist) { cudaFree(ctx->dist); ctx->dist = nullptr; }
+  st = dd_setup(ctx);
+  if (st != DPM_OK) {
+    dpm_destroy(ctx);
+    *out = nullptr;
+  }
+  return st;
+}
+
+dpm_status dpm_dd_info(const dpm_ctx* ctx, int64_t* n_rows, int32_t* K) {
+  if (!ctx || !ctx->dd || !n_rows || !K) return DPM_ERR_INVALID;
+  *n_rows = ctx->n_rows;
+  *K = ctx->K;
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_copy_assign(const dpm_ctx* ctx, uint8_t* host_bits) {
+  if (!ctx || !ctx->dd || !host_bits) return DPM_ERR_INVALID;
+  cudaSetDevice(ctx->device);
+  dpm_ctx* c = const_cast<dpm_ctx*>(ctx);
+  DPM_CUDA_TRY(c, cudaMemcpy(host_bits, ctx->dd_assign, ctx->counts[DPM_SET_GAMMA], cudaMemcpyDeviceToHost));
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if ((st = dd_alloc(ctx)) != DPM_OK) return st;
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  const int K = ctx->K;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA];
+  const int ch = (int)std::max<size_t>(1, std::min<size_t>((size_t)K, ((size_t)2 << 30) / (field * 8)));
+  if (ctx->work_boxes < (size_t)std::min(ch, K)) {
+    if (ctx->work) cudaFree(ctx->work);
+    ctx->work = nullptr;
+    ctx->work_boxes = 0;
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->work, (size_t)std::min(ch, K) * field * sizeof(double)));
+    ctx->work_boxes = std::min(ch, K);
+  }
+  const int nc = (ctx->Lc + 1) * (ctx->Lc + 1);
+  for (int a = 0; a < K; a += ch) {
+    const int ncol = std::min(ch, K - a);
+    DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, ncol, s));
+    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, ncol, nullptr, 0, s));
+    DPM_COUNT_LAUNCH(1);
+    dd_bep_gather_kernel<<<grid_for(ctx->n_rows * ncol), TB, 0, s>>>(
+        ctx->work, ncol, field, ctx->lists[DPM_SET_GAMMA], ng, ctx->dd_rows, ctx->n_rows, ctx->dd_Eraw, a, nc,
+        ctx->nphi, ctx->dd_B + (size_t)a * ctx->n_rows);
+    DPM_CUDA_TRY(ctx, cudaGetLastError());
+  }
+  if (B_out)
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(B_out, ctx->dd_B, (size_t)K * ctx->n_rows * 8, cudaMemcpyDeviceToDevice, s));
+  ctx->have_projection = 0;
+  ctx->dt_bep = ctx->dt;
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_colnorm2(dpm_ctx* ctx, double* nrm2, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!nrm2 || !ctx->dd_B) return DPM_ERR_STATE;
+  DPM_COUNT_LAUNCH(1);
+  colsumsq_kernel<<<ctx->K, TB, 0, as_stream(stream)>>>(ctx->dd_B, ctx->n_rows, nrm2);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, double* G, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!G || !ctx->dd_B || (pass != 1 && pass != 2) || (pass == 1 && !nrm2_sum)) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  const int K = ctx->K;
+  if (pass == 1) {   // D = 1/||column|| of the stacked system; Q1 <- B D
+    std::vector<double> h(K);
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(h.data(), nrm2_sum, K * 8, cudaMemcpyDeviceToHost, s));
+    DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    for (int c = 0; c < K; ++c) h[c] = h[c] > 0 ? 1.0 / std::sqrt(h[c]) : 1.0;
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->dd_D, h.data(), K * 8, cudaMemcpyHostToDevice, s));
+    DPM_CUDA_TRY(ctx, lsq_scale_cols(ctx->dd_B, ctx->n_rows, K, ctx->dd_D, ctx->dd_Q, s));
+  }
+  DPM_CUDA_TRY(ctx, lsq_gram(ctx->dd_Q, ctx->n_rows, K, G, s));
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!G_sum || (pass != 1 && pass != 2)) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  const size_t K = ctx->K;
+  double* R1 = ctx->dd_R;
+  double* R2 = R1 + K * K;
+  double* R = R2 + K * K;
+  double* W = R + K * K;
+  int* dfail = reinterpret_cast<int*>(W + K * K);
+  double* Rp = pass == 1 ? R1 : R2;
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(Rp, G_sum, K * K * 8, cudaMemcpyDeviceToDevice, s));
+  DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), s));
+  DPM_CUDA_TRY(ctx, lsq_cholesky(Rp, (int)K, dfail, s));
+  DPM_CUDA_TRY(ctx, lsq_trsm_rows(ctx->dd_Q, ctx->n_rows, (int)K, Rp, s));
+  if (pass == 2) {
+    DPM_CUDA_TRY(ctx, lsq_trmm(R2, R1, R, (int)K, s));
+    DPM_CUDA_TRY(ctx, lsq_build_operator(R, ctx->dd_Q, ctx->n_rows, (int)K, ctx->dd_D, ctx->dd_M, W, s));
+  }
+  int hfail = 0;
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (hfail) { ctx->err = "octant DD: CholeskyQR2 breakdown (stacked BEP rank deficient)"; return DPM_ERR_RANK; }
+  if (pass == 2) ctx->have_projection = 1;
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!rho || !c || !ic) return DPM_ERR_INVALID;
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  DPM_COUNT_LAUNCH(1);
+  dd_ic_kernel<<<grid_for(nn), TB, 0, as_stream(stream)>>>(ctx->flags, ctx->gmap, ctx->dd_assign, ctx->n, ctx->lo,
+                                                           ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1],
+                                                           ctx->sigma[2], *ic, rho, c);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_cfl(dpm_ctx* ctx, const double* c, double chi, double* cfl_dt, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!c || !cfl_dt || !(chi > 0)) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, ctx->red, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host, ctx->red, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  const double h = ctx->h;
+  double cfl = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    const double mx = ctx->red_host[a] / h;
+    if (mx > 0) cfl = std::fmin(cfl, h / (6.0 * chi * mx));
+  }
+  *cfl_dt = cfl;
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* y, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!rho || !c || !y) return DPM_ERR_INVALID;
+  if (!ctx->have_projection || ctx->dt_bep != ctx->dt) { ctx->err = "octant DD: no factorisation at this dt"; return DPM_ERR_STATE; }
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  const size_t need = 4 * field * 8;
+  if (!ctx->scratch || ctx->scratch_bytes < need) {
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    ctx->scratch_bytes = need;
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, need));
+  }
+  double* fq = ctx->scratch;
+  double* wk = fq + 2 * field;
+  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, ctx->dt, chi, fq, fq + field, s));          // Step 4a
+  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+  DPM_COUNT_LAUNCH(1);
+  dd_rows_trace_kernel<<<grid_for(ctx->n_rows * 2), TB, 0, s>>>(wk, field, ctx->lists[DPM_SET_GAMMA], ctx->dd_rows,
+                                                                ctx->n_rows, 2, ctx->dd_g);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  DPM_CUDA_TRY(ctx, lsq_gemv(ctx->dd_M, ctx->n_rows, ctx->K, ctx->dd_g, 2, y, s));           // y_s = M_s g_s
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, double* rho, double* c, double* stats,
+                               void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!C || !rho || !c || !stats || !ctx->scratch) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA];
+  double* fq = ctx->scratch;
+  double* wk = fq + 2 * field;
+  if (!ctx->dd_ug) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_ug, (size_t)2 * ng * sizeof(double) + 64));
+  double* ug = ctx->dd_ug;
+  DPM_CUDA_TRY(ctx, lsq_extend(ctx->E, ng, ctx->K, C, 2, clamp, ug, s));                   // u_γ = A C (R17)
+  DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));                                // R20
+  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  const double* R = ctx->red_host + 8;   // [mass_sum, rho_max, rho_min, c_min, nonfinite] (R18)
+  stats[0] = R[0] * ctx->h * ctx->h * ctx->h;
+  stats[1] = decode_key(R[1]);
+  stats[2] = -decode_key(R[2]);
+  stats[3] = -decode_key(R[3]);
+  stats[4] = R[4];
+  return DPM_OK;
+}
+
+}  // extern "C"

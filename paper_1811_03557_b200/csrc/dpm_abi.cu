@@ -16,6 +16,7 @@ void free_ctx(dpm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq,
+                  c->dd_Eraw, c->dd_assign, c->dd_rows, c->dd_B, c->dd_Q, c->dd_R, c->dd_M, c->dd_D, c->dd_g, c->dd_ug,
                   c->lsq_ws, c->work, c->scratch, c->red};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -63,12 +64,8 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 }  // namespace
 
-extern "C" {
-
-const char* dpm_last_error(const dpm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
-
-dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
-                      int32_t device, dpm_ctx** out) {
+dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
+                           int32_t device, dpm_ctx** out) {
   if (out) *out = nullptr;
   g_create_err.clear();
   if (!grid || !domain || !out) { g_create_err = "null argument"; return DPM_ERR_INVALID; }
@@ -77,15 +74,6 @@ dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lm
   if (!(dt > 0) || !std::isfinite(dt)) { g_create_err = "dt must be > 0"; return DPM_ERR_INVALID; }
   if (lmax < 0 || lmax > 40) { g_create_err = "lmax out of range"; return DPM_ERR_INVALID; }
   if (basis != DPM_BASIS_CAUCHY && basis != DPM_BASIS_NEUMANN0) { g_create_err = "bad basis"; return DPM_ERR_INVALID; }
-  if (domain->kind != DPM_SPHERE && domain->kind != DPM_ELLIPSOID) { g_create_err = "bad domain kind"; return DPM_ERR_INVALID; }
-  for (int a = 0; a < 3; ++a) {
-    const double s = domain->kind == DPM_SPHERE ? domain->semi[0] : domain->semi[a];
-    if (!(s > 0)) { g_create_err = "semi-axes must be > 0"; return DPM_ERR_INVALID; }
-    if (!(domain->center[a] - s > grid->lo && domain->center[a] + s < grid->hi)) {
-      g_create_err = "domain not strictly inside the box";
-      return DPM_ERR_INVALID;
-    }
-  }
   if (cudaSetDevice(device) != cudaSuccess) { g_create_err = "cudaSetDevice failed"; return DPM_ERR_CUDA; }
   dpm_ctx* ctx = new (std::nothrow) dpm_ctx();
   if (!ctx) return DPM_ERR_OOM;
@@ -103,7 +91,7 @@ dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lm
   dpm_status st = DPM_OK;
   if (cudaStreamCreateWithFlags(&ctx->setup_stream, cudaStreamNonBlocking) != cudaSuccess) st = DPM_ERR_CUDA;
   if (st == DPM_OK) st = setup_point_sets(ctx);
-  if (st == DPM_OK) st = setup_geometry(ctx);
+  if (st == DPM_OK && domain->kind != DPM_OCTANT_CANON) st = setup_geometry(ctx);
   if (st == DPM_OK && dst_plan_init(ctx->plan, ctx->n, ctx->h, dt) != cudaSuccess) { st = DPM_ERR_CUDA; ctx->err = "plan init"; }
   if (st == DPM_OK && cudaMalloc(&ctx->red, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
   if (st == DPM_OK && cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
@@ -114,6 +102,27 @@ dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lm
   }
   *out = ctx;
   return DPM_OK;
+}
+
+extern "C" {
+
+const char* dpm_last_error(const dpm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
+                      int32_t device, dpm_ctx** out) {
+  if (out) *out = nullptr;
+  g_create_err.clear();
+  if (!grid || !domain || !out) { g_create_err = "null argument"; return DPM_ERR_INVALID; }
+  if (domain->kind != DPM_SPHERE && domain->kind != DPM_ELLIPSOID) { g_create_err = "bad domain kind"; return DPM_ERR_INVALID; }
+  for (int a = 0; a < 3; ++a) {
+    const double s = domain->kind == DPM_SPHERE ? domain->semi[0] : domain->semi[a];
+    if (!(s > 0)) { g_create_err = "semi-axes must be > 0"; return DPM_ERR_INVALID; }
+    if (!(domain->center[a] - s > grid->lo && domain->center[a] + s < grid->hi)) {
+      g_create_err = "domain not strictly inside the box";
+      return DPM_ERR_INVALID;
+    }
+  }
+  return dpm_create_impl(grid, domain, lmax, dt, basis, device, out);
 }
 
 void dpm_destroy(dpm_ctx* ctx) { free_ctx(ctx); }
@@ -302,7 +311,9 @@ dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* 
   return DPM_OK;
 }
 
-static double decode_key(double slot) {
+}  // extern "C"
+
+double decode_key(double slot) {
   unsigned long long k;
   std::memcpy(&k, &slot, 8);
   unsigned long long x = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
@@ -310,6 +321,8 @@ static double decode_key(double slot) {
   std::memcpy(&v, &x, 8);
   return v;
 }
+
+extern "C" {
 
 // Enqueue one PKS step (Steps 4a-7) at a fixed dt on stream s; `slot` receives red(3), dt_true
 // (device dt rule from the state at the start of the step) and the step statistics.

@@ -8,6 +8,9 @@
 
 #include "../../include/dpm.h"
 
+// internal domain kind of an octant subdomain (dpm_create_octant), canonical frame (+,+,+)
+constexpr int DPM_OCTANT_CANON = 100;
+
 // point-flag bits for the uint8 mask over the n^3 interior
 enum : uint8_t {
   F_MPLUS = 1,   // M+
@@ -98,6 +101,24 @@ struct dpm_ctx {
   double* pks_log = nullptr;        // device [PKS_K][16]: red(3), dt_true, stats(5)
   double* pks_log_host = nullptr;   // pinned mirror
   double* pks_backup = nullptr;     // device [PKS_K][2][n^3]: state at the start of each step
+
+  // octant DD subdomain (dpm_create_octant)
+  int dd = 0;                       // 1 for an octant subdomain
+  int octant = 0;                   // s = 4[σx<0] + 2[σy<0] + [σz<0]
+  double sigma[3] = {1, 1, 1};
+  double radius = 1.0;
+  int Lc = 0, Li = 0, nphi = 0;
+  double* dd_Eraw = nullptr;        // [K][n_gamma]: each piece's extension (block-sparse by column)
+  uint8_t* dd_assign = nullptr;     // [n_gamma]: piece bits (1 cap, 2 x, 4 y, 8 z)
+  int32_t* dd_rows = nullptr;       // [n_rows][2]: (gamma position, piece) of the BEP rows
+  int64_t n_rows = 0;
+  double* dd_B = nullptr;           // [K][n_rows] BEP block
+  double* dd_Q = nullptr;           // [K][n_rows] equilibrated Q1 / Q
+  double* dd_R = nullptr;           // [3][K][K]: R1, R2, R
+  double* dd_M = nullptr;           // [K][n_rows] row-major: D R^{-1} Q^T
+  double* dd_D = nullptr;           // [K] global column scaling
+  double* dd_g = nullptr;           // [2][n_rows] per-step BEP right-hand sides
+  double* dd_ug = nullptr;          // [2][n_gamma] u_γ = A C
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -148,6 +169,25 @@ cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int n
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s);
 cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
                       cudaStream_t s);
+
+// lsq.cu building blocks (octant DD)
+cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s);
+cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s);
+cudaError_t lsq_trsm_rows(double* A, int64_t m, int K, const double* R, cudaStream_t s);
+cudaError_t lsq_trmm(const double* A, const double* B, double* C, int K, cudaStream_t s);
+cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scale, double* A, cudaStream_t s);
+cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int K, const double* scale, double* M,
+                               double* Ri_ws, cudaStream_t s);
+cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s);
+cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, int nrhs, int clamp, double* ug,
+                       cudaStream_t s);
+
+// dd.cu (octant DD setup)
+dpm_status dd_setup(dpm_ctx* ctx);
+// dpm_abi.cu
+dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
+                           int32_t device, dpm_ctx** out);
+double decode_key(double slot);   // order-preserving key of the reduction slots -> value
 
 // pks.cu
 cudaError_t launch_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, cudaStream_t s);

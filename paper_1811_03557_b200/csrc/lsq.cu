@@ -284,12 +284,71 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN], ng = ctx->counts[DPM_SET_GAMMA];
   DPM_COUNT_LAUNCH(1);
   lsq_gemv_kernel<<<dim3(K, nrhs), 128, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
-  if (u_gamma) {
-    const size_t smem = (size_t)(K + 256) * sizeof(double);
-    for (int r = 0; r < nrhs; ++r) {
-      DPM_COUNT_LAUNCH(1);
-      extend2_kernel<<<(unsigned)((ng + 31) / 32), 256, smem, s>>>(ctx->E, ng, K, coef, r, clamp, u_gamma);
-    }
+  if (u_gamma) return lsq_extend(ctx->E, ng, K, coef, nrhs, clamp, u_gamma, s);
+  return cudaGetLastError();
+}
+
+// ---- building blocks shared with the octant DD (dd.cu): distributed CholeskyQR2 ----
+cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(G, 0, (size_t)K * K * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  const int tiles = (K + 31) / 32;
+  const int64_t target_split = std::max<int64_t>(1, (148 * 4) / ((int64_t)tiles * (tiles + 1) / 2));
+  const int64_t rps = std::max<int64_t>(32, ((m + target_split - 1) / target_split + 31) / 32 * 32);
+  const int nsplit = (int)std::max<int64_t>(1, (m + rps - 1) / rps);
+  DPM_COUNT_LAUNCH(1);
+  gram_kernel<<<dim3(tiles, tiles, nsplit), TB, 0, s>>>(A, m, K, G, rps);
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  cholesky_kernel<<<1, 1024, 0, s>>>(G, K, dfail);
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_trsm_rows(double* A, int64_t m, int K, const double* R, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  DPM_COUNT_LAUNCH(1);
+  trsm_rows_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(A, m, K, R);
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_trmm(const double* A, const double* B, double* C, int K, cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  trmm_kernel<<<(K * K + 255) / 256, 256, 0, s>>>(A, B, C, K);
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scale, double* A, cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  scale_cols_kernel<<<148 * 8, TB, 0, s>>>(B, m, K, scale, A);
+  return cudaGetLastError();
+}
+
+// M = diag(scale) R^{-1} Q^T (K x m row-major); Ri_ws: K x K workspace
+cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int K, const double* scale, double* M,
+                               double* Ri_ws, cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  rinv_kernel<<<(K + 63) / 64, 64, 0, s>>>(R, K, Ri_ws);
+  if (m == 0) return cudaGetLastError();
+  DPM_COUNT_LAUNCH(1);
+  lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri_ws, Q, scale, K, m, M);
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  lsq_gemv_kernel<<<dim3(K, nrhs), 128, 0, s>>>(M, m, K, g, nrhs, coef);
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, int nrhs, int clamp, double* ug,
+                       cudaStream_t s) {
+  const size_t smem = (size_t)(K + 256) * sizeof(double);
+  for (int r = 0; r < nrhs; ++r) {
+    DPM_COUNT_LAUNCH(1);
+    extend2_kernel<<<(unsigned)((ng + 31) / 32), 256, smem, s>>>(E, ng, K, coef, r, clamp, ug);
   }
   return cudaGetLastError();
 }

@@ -4,10 +4,13 @@
 #include <cub/cub.cuh>
 
 #include "dpm_internal.h"
+#include "sh_device.cuh"
 
 namespace {
 
 __device__ __forceinline__ bool inside_domain(const dpm_domain& D, double x, double y, double z) {
+  if (D.kind == DPM_OCTANT_CANON)   // cfg5 subdomain in its canonical frame (R24): open octant ∩ ball
+    return x > 0.0 && y > 0.0 && z > 0.0 && x * x + y * y + z * z < D.semi[0] * D.semi[0];
   const double a = (x - D.center[0]) / D.semi[0];
   const double b = (y - D.center[1]) / D.semi[1];
   const double c = (z - D.center[2]) / D.semi[2];
@@ -136,12 +139,7 @@ __device__ void ellipsoid_foot(const double p[3], const double s[3], double x[3]
   *d = (t > 0 ? 1.0 : (t < 0 ? -1.0 : 0.0)) * sqrt(dd);
 }
 
-// Per gamma point: geometry, then all (L+1)^2 real SH by the fully-normalised
-// associated-Legendre recurrence in Cartesian form (pole-safe), written into E.
-//   P̂_m^m = P̂_{m-1}^{m-1} sqrt((2m+1)/(2m)),  P̂_{m+1}^m = z sqrt(2m+3) P̂_m^m,
-//   P̂_l^m = a_lm (z P̂_{l-1}^m - b_lm P̂_{l-2}^m),  a = sqrt((4l^2-1)/(l^2-m^2)),
-//   b = sqrt(((l-1)^2-m^2)/(4(l-1)^2-1));  C_m + i S_m = (x + i y)^m.
-//   Y_l0 = P̂_l^0,  Y_lm = sqrt2 P̂_l^m C_m,  Y_l,-m = sqrt2 P̂_l^m S_m.
+// Per gamma point: geometry, then all (L+1)^2 real SH (sh_device.cuh), written into E.
 __global__ void geometry_sh_kernel(const int64_t* gamma, int64_t ng, int n, double lo, double h, dpm_domain D,
                                    int lmax, int basis, double* foot, double* dist, double* E) {
   const long g = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -165,41 +163,10 @@ __global__ void geometry_sh_kernel(const int64_t* gamma, int64_t ng, int n, doub
   dist[g] = d;
   const double w = (basis == DPM_BASIS_CAUCHY) ? d : 0.5 * d * d;
   const int nsh = (lmax + 1) * (lmax + 1);
-  const double x = u[0], y = u[1], z = u[2];
-  double pmm = 0.28209479177387814347;   // 1/sqrt(4 pi)
-  double Cm = 1.0, Sm = 0.0;
-  for (int m = 0; m <= lmax; ++m) {
-    if (m > 0) {
-      pmm *= sqrt((2.0 * m + 1.0) / (2.0 * m));
-      const double Cn = x * Cm - y * Sm, Sn = x * Sm + y * Cm;
-      Cm = Cn;
-      Sm = Sn;
-    }
-    double p2 = 0.0, p1 = pmm;
-    for (int l = m; l <= lmax; ++l) {
-      double pl;
-      if (l == m) pl = pmm;
-      else if (l == m + 1) pl = z * sqrt(2.0 * m + 3.0) * pmm;
-      else {
-        const double a = sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m));
-        const double b = sqrt(((l - 1.0) * (l - 1.0) - (double)m * m) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
-        pl = a * (z * p1 - b * p2);
-      }
-      if (l > m) { p2 = p1; p1 = pl; }
-      if (m == 0) {
-        const int nu = l * l + l;
-        E[(size_t)nu * ng + g] = pl;
-        E[(size_t)(nsh + nu) * ng + g] = w * pl;
-      } else {
-        const double yc = 1.41421356237309504880 * pl * Cm, ys = 1.41421356237309504880 * pl * Sm;
-        const int nup = l * l + l + m, num = l * l + l - m;
-        E[(size_t)nup * ng + g] = yc;
-        E[(size_t)(nsh + nup) * ng + g] = w * yc;
-        E[(size_t)num * ng + g] = ys;
-        E[(size_t)(nsh + num) * ng + g] = w * ys;
-      }
-    }
-  }
+  real_sh_unit(u[0], u[1], u[2], lmax, [&](int nu, double v) {
+    E[(size_t)nu * ng + g] = v;
+    E[(size_t)(nsh + nu) * ng + g] = w * v;
+  });
 }
 
 }  // namespace

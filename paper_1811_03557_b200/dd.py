@@ -1,0 +1,89 @@
+"""Config 5 driver: the 8-octant domain decomposition.
+
+Each rank owns a set of octant contexts (one per GPU at 8 ranks; all 8 on one GPU at N=1).
+Everything numerical runs in libdpm.so; this module only sequences the ABI calls and performs
+the collectives of the distributed CholeskyQR2 / step:
+  * C3-equivalent (once per dt): all-reduce(sum) of the K column norms and of two K x K Gram
+    matrices;
+  * C4 (per step): all-reduce(min) of the local CFL bounds (the global dt, R13);
+  * C2 (per step): all-reduce(sum) of y_s = M_s g_s (K x 2) -> the global coefficients C.
+Local contributions are summed in octant order before the cross-rank all-reduce.
+"""
+from typing import Callable, List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+
+def _allreduce(t: torch.Tensor, op) -> torch.Tensor:
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=op)
+    return t
+
+
+class DDSolver:
+    def __init__(self, octants: Sequence, dt_cap: float, chi: float = 1.0, dt_rule: int = 0, clamp: int = 1):
+        self.octs = list(octants)
+        self.K = self.octs[0].K
+        self.h = self.octs[0].info["h"]
+        self.dt_cap, self.chi, self.dt_rule, self.clamp = dt_cap, chi, dt_rule, clamp
+        self.dt_prev = float("inf")
+        self.dt_bep: Optional[float] = None
+        self.builds = 0
+        self.t = 0.0
+        self.fields: List = []
+
+    # ---- global least squares (distributed CholeskyQR2) at dt
+    def _sum(self, parts: List[torch.Tensor]) -> torch.Tensor:
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        return _allreduce(acc, dist.ReduceOp.SUM)
+
+    def build(self, dt: float):
+        for o in self.octs:
+            o.set_dt(dt)
+            o.bep_block()
+        n2 = self._sum([o.colnorm2() for o in self.octs])
+        G1 = self._sum([o.gram(1, n2) for o in self.octs])
+        for o in self.octs:
+            o.chol(1, G1)
+        G2 = self._sum([o.gram(2) for o in self.octs])
+        for o in self.octs:
+            o.chol(2, G2)
+        self.dt_bep = dt
+        self.builds += 1
+
+    def init(self, center, rho_ic, c_ic):
+        self.fields = []
+        for o in self.octs:
+            n = o.n
+            rho = torch.zeros((n, n, n), dtype=torch.float64, device=o.device)
+            c = torch.zeros_like(rho)
+            o.dd_pks_init(rho, c, center, *rho_ic, *c_ic)
+            self.fields.append((rho, c))
+        self.dt_prev, self.t = float("inf"), 0.0
+
+    def step(self):
+        # Step 3 (R13) with the global CFL bound (C4)
+        if self.dt_rule == 0:
+            cfl = torch.tensor([min(o.cfl(c, self.chi) for o, (_, c) in zip(self.octs, self.fields))],
+                               dtype=torch.float64, device=self.octs[0].device)
+            cfl = float(_allreduce(cfl, dist.ReduceOp.MIN).item())
+            dt = min(min(self.dt_prev, self.dt_cap), min(cfl, 0.5 * self.h * self.h))
+        else:
+            dt = self.dt_cap
+        rebuilt = self.dt_bep is None or dt != self.dt_bep
+        if rebuilt:                                                   # Step 2 / 4b
+            self.build(dt)
+        ys = [o.local_begin(rho, c, self.chi) for o, (rho, c) in zip(self.octs, self.fields)]
+        Cg = self._sum(ys)                                            # C2: global coefficients
+        stats = [o.local_finish(Cg, rho, c, self.clamp) for o, (rho, c) in zip(self.octs, self.fields)]
+        self.dt_prev = dt
+        self.t += dt
+        mass = torch.tensor([sum(s["mass"] for s in stats)], dtype=torch.float64, device=self.octs[0].device)
+        mass = float(_allreduce(mass, dist.ReduceOp.SUM).item())
+        if any(s["nonfinite"] for s in stats):
+            raise FloatingPointError("non-finite value in the DD PKS step")
+        return {"t": self.t, "dt": dt, "rebuilt": rebuilt, "mass": mass,
+                "rho_max": max(s["rho_max"] for s in stats), "rho_min": min(s["rho_min"] for s in stats)}

@@ -14,7 +14,7 @@ LIB = os.path.join(ROOT, "paper_1811_03557_b200", "libdpm.so")
 def declared_symbols():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(dpm_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(dpm_[a-z_0-9]+)\s*\(", txt)))
 
 
 @pytest.fixture(scope="module")

@@ -1,0 +1,75 @@
+"""GPU parity of config 5's octant domain decomposition against oracle/dd.py.
+
+Reduced sizes the oracle finishes in seconds (n = 16 per octant, cap degree 4, interface degree 4);
+tolerances of R23: B blocks <= 1e-11, PKS fields after the steps <= 1e-9, dt <= 1e-12 relative,
+point sets and piece assignment bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dd as odd
+
+pytestmark = pytest.mark.gpu
+
+N, LC, LI = 16, 4, 4
+BOX = (-0.1, 1.1)
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1811_03557_b200 import api as A
+    assert torch.cuda.is_available()
+    return A
+
+
+@pytest.fixture(scope="module")
+def setup():
+    return odd.setup(N, LC, LI)
+
+
+def test_octant_sets_and_pieces(api, setup):
+    o = setup.octants[0]
+    for s in (0, 3, 7):
+        g = api.Octant(N, *BOX, s, 1.0, LC, LI, 1e-3)
+        for w in ["mplus", "gamma", "gamma_in", "gamma_ex", "band", "nplus"]:
+            assert np.array_equal(g.copy_set(w), o.ps.list(w)), w
+        bits = g.copy_assign()
+        ob = (o.assign * np.array([1, 2, 4, 8])).sum(axis=1)
+        assert np.array_equal(bits, ob)
+        assert g.K == setup.K and g.n_rows == len(o.rows)
+
+
+@pytest.mark.parametrize("s", [0, 5])
+def test_bep_block(api, setup, s):
+    dt = 1e-3
+    g = api.Octant(N, *BOX, s, 1.0, LC, LI, dt)
+    B = g.bep_block(want=True).cpu().numpy().T          # n_rows x K
+    Bo, _ = odd.bep_block(setup, setup.octants[s], dt)
+    assert rel(B, Bo) <= 1e-11, rel(B, Bo)
+
+
+def test_dd_pks_parity(api):
+    from paper_1811_03557_b200.dd import DDSolver
+    steps, cap = 3, 1e-3
+    o = odd.DDPKSOracle(N, LC, LI, cap, steps)
+    state, ologs = o.run()
+    octs = [api.Octant(N, *BOX, s, 1.0, LC, LI, cap) for s in range(8)]
+    sol = DDSolver(octs, cap)
+    sol.init((0.0, 0.0, 0.0), (1000.0, 100.0), (500.0, 50.0))
+    r0 = o.initial_state()
+    for (rho, c), (ro, co) in zip(sol.fields, r0):
+        assert rel(rho.cpu().numpy(), ro) <= 1e-13
+        assert rel(c.cpu().numpy(), co) <= 1e-13
+    logs = [sol.step() for _ in range(steps)]
+    for (rho, c), (ro, co) in zip(sol.fields, state):
+        assert rel(rho.cpu().numpy(), ro) <= 1e-9, rel(rho.cpu().numpy(), ro)
+        assert rel(c.cpu().numpy(), co) <= 1e-9, rel(c.cpu().numpy(), co)
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
+        assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
+    assert sol.builds == o.builds

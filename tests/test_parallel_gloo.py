@@ -67,3 +67,92 @@ def test_distributed_bep_matches_single(world):
         p.join(timeout=60)
     for r in range(world):
         assert np.array_equal(res[r], ref), r   # column sharding is exact (bit-identical columns)
+
+
+class _FakeOctant:
+    """Stand-in for api.Octant with the DD driver's interface: deterministic per-octant tensors,
+    so the collectives (column norms, Gram sums, dt min, coefficient sums) can be checked on CPU."""
+
+    K = 5
+
+    def __init__(self, s):
+        self.s = s
+        self.n = 4
+        self.device = torch.device("cpu")
+        self.info = {"h": 0.1}
+        self.seen = {}
+        g = torch.Generator().manual_seed(100 + s)
+        self.y = torch.rand((2, self.K), generator=g, dtype=torch.float64)
+        self.G = torch.rand((self.K, self.K), generator=g, dtype=torch.float64)
+
+    def set_dt(self, dt):
+        self.seen["dt"] = dt
+
+    def bep_block(self):
+        pass
+
+    def colnorm2(self):
+        return torch.full((self.K,), float(self.s + 1), dtype=torch.float64)
+
+    def gram(self, p, n2=None):
+        if p == 1:
+            self.seen["n2"] = n2.clone()
+        return self.G * p
+
+    def chol(self, p, G):
+        self.seen[f"G{p}"] = G.clone()
+
+    def dd_pks_init(self, rho, c, *a):
+        rho.fill_(1.0)
+        c.fill_(float(self.s))
+
+    def cfl(self, c, chi=1.0):
+        return 1e-3 * (1 + self.s)
+
+    def local_begin(self, rho, c, chi=1.0):
+        return self.y.clone()
+
+    def local_finish(self, C, rho, c, clamp=1):
+        self.seen["C"] = C.clone()
+        return {"mass": 1.0, "rho_max": 1.0, "rho_min": 0.0, "c_min": 0.0, "nonfinite": 0.0}
+
+
+def _dd_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1811_03557_b200.dd import DDSolver
+    per = 8 // world
+    octs = [_FakeOctant(s) for s in range(rank * per, (rank + 1) * per)]
+    sol = DDSolver(octs, dt_cap=1.0)
+    sol.init((0, 0, 0), (1, 1), (1, 1))
+    log = sol.step()
+    q.put((rank, log["dt"], log["mass"], octs[0].seen["n2"].numpy(), octs[0].seen["G2"].numpy(),
+           octs[0].seen["C"].numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_dd_collectives_match_single_process(world):
+    """8 octants on `world` gloo ranks vs all 8 in one process: same global norms, Gram sums,
+    dt (min over octants, R13 / C4) and coefficient sums (C2)."""
+    from paper_1811_03557_b200.dd import DDSolver
+    octs = [_FakeOctant(s) for s in range(8)]
+    ref = DDSolver(octs, dt_cap=1.0)
+    ref.init((0, 0, 0), (1, 1), (1, 1))
+    rlog = ref.step()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, dt, mass, n2, G2, C in outs:
+        assert dt == rlog["dt"] == min(1.0, 1e-3, 0.5 * 0.1 * 0.1)
+        assert abs(mass - rlog["mass"]) < 1e-12
+        np.testing.assert_allclose(n2, octs[0].seen["n2"].numpy(), rtol=1e-14)
+        np.testing.assert_allclose(G2, octs[0].seen["G2"].numpy(), rtol=1e-14)
+        np.testing.assert_allclose(C, octs[0].seen["C"].numpy(), rtol=1e-14)
