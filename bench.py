@@ -173,6 +173,40 @@ def bench_pks(api, torch, name, reps=3):
             "rebuilds": sum(l["rebuilt"] for l in logs), "final_mass": logs[-1]["mass"], "rho_max": logs[-1]["rho_max"]}
 
 
+def bench_dd(api, torch, world, rank, steps=None):
+    """cfg5: the 8-octant DD (R24) — octants sharded over the ranks (8/world each), the global
+    least squares and dt through NCCL all-reduces (DDSolver).  Steps/s excludes the BEP builds
+    (timed separately; 3 expected, SURVEY probe P12)."""
+    from paper_1811_03557_b200.dd import DDSolver
+    cfg = get_config("cfg5")
+    steps = steps or cfg.steps
+    per = 8 // world
+    mine = range(rank * per, (rank + 1) * per)
+    dev = torch.cuda.current_device()
+    octs = [api.Octant(cfg.n, cfg.lo, cfg.hi, s, 1.0, cfg.lmax, cfg.deg_if, cfg.dt, device=dev) for s in mine]
+    sol = DDSolver(octs, cfg.dt, chi=cfg.chi)
+    sol.init(cfg.ic_center, cfg.ic_rho, cfg.ic_c)
+    t_build, logs = 0.0, []
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        b0, ts = sol.builds, time.perf_counter()
+        logs.append(sol.step())
+        torch.cuda.synchronize()
+        if sol.builds > b0:
+            t_build += time.perf_counter() - ts
+    tot = time.perf_counter() - t0
+    out = {"octants": 8, "octants_per_rank": per, "n": cfg.n, "K": octs[0].K, "rows_per_octant": octs[0].n_rows,
+           "steps": steps, "total_s": tot, "builds": sol.builds, "build_s_incl_their_steps": t_build,
+           "steps_per_s_excl_builds": (steps - sol.builds) / max(tot - t_build, 1e-9),
+           "dt_first": logs[0]["dt"], "dt_last": logs[-1]["dt"], "t_end": logs[-1]["t"],
+           "mass_after_step1": logs[0]["mass"], "mass_end": logs[-1]["mass"], "rho_max_end": logs[-1]["rho_max"],
+           "note": "non-physical config (SURVEY §0 item 6: IC spike at the 8-octant corner); matches probe P12"}
+    del sol, octs
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap_ = argparse.ArgumentParser()
     ap_.add_argument("--gpus", type=int, default=1)
@@ -182,6 +216,7 @@ def main():
     ap_.add_argument("--no-e2e", action="store_true")
     ap_.add_argument("--no-cpu", action="store_true")
     ap_.add_argument("--no-pks", action="store_true")
+    ap_.add_argument("--no-dd", action="store_true")
     args = ap_.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
@@ -324,6 +359,16 @@ def main():
         del q, u
         torch.cuda.empty_cache()
         line["pks"] = {"cfg2": bench_pks(api, torch, "cfg2"), "cfg3": bench_pks(api, torch, "cfg3")}
+
+    if not args.no_dd and 8 % world == 0:
+        try:
+            del q, u
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        dd = bench_dd(api, torch, world, rank)
+        if rank == 0:
+            line["dd"] = {"cfg5": dd}
 
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -26,6 +26,7 @@ class Config:
     ic_rho: Tuple[float, float] = (1000.0, 100.0)
     ic_c: Tuple[float, float] = (500.0, 50.0)
     chi: float = 1.0             # R27: alpha = gamma_rho = gamma_c = chi = 1
+    deg_if: int = 0              # cfg5: interface polynomial degree (R24); lmax is the cap SH degree
 
     @property
     def K(self) -> int:
@@ -41,6 +42,10 @@ CONFIGS = {
                    steps=100, ic_center=(0.2, 0.0, 0.0)),
     "cfg4": Config("cfg4", 128, -1.1, 1.1, "sphere", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 16, "cauchy", 1e-5,
                    batch=578),
+    # cfg5 (R24, R3): 8 octant subdomains, each on its own canonical box [-0.1, 1.1]^3 with
+    # n = 128; cap SH degree 12 and interface degree 12 (K = 884); dt cap 1e-5; 50 steps.
+    "cfg5": Config("cfg5", 128, -0.1, 1.1, "octant8", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0), 12, "neumann0", 1e-5,
+                   steps=50, deg_if=12),
 }
 
 

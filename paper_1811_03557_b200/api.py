@@ -50,9 +50,9 @@ class DPM:
         return cls(cfg.n, cfg.lo, cfg.hi, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.dt, cfg.basis, device)
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and L is not None and getattr(L, "lib", None) is not None:
             L.lib.dpm_destroy(self._h)
-            self._h = None
+        self._h = None
 
     def __del__(self):
         self.close()

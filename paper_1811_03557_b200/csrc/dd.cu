@@ -396,7 +396,9 @@ dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* st
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(Rp, G_sum, K * K * 8, cudaMemcpyDeviceToDevice, s));
   DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), s));
   DPM_CUDA_TRY(ctx, lsq_cholesky(Rp, (int)K, dfail, s));
-  DPM_CUDA_TRY(ctx, lsq_trsm_rows(ctx->dd_Q, ctx->n_rows, (int)K, Rp, s));
+  // Q <- Q Rp^{-1} as a tiled GEMM with the explicit triangular inverse (into dd_M, then swap)
+  DPM_CUDA_TRY(ctx, lsq_mul_rinv(ctx->dd_Q, ctx->n_rows, (int)K, Rp, W, ctx->dd_M, s));
+  std::swap(ctx->dd_Q, ctx->dd_M);
   if (pass == 2) {
     DPM_CUDA_TRY(ctx, lsq_trmm(R2, R1, R, (int)K, s));
     DPM_CUDA_TRY(ctx, lsq_build_operator(R, ctx->dd_Q, ctx->n_rows, (int)K, ctx->dd_D, ctx->dd_M, W, s));

@@ -175,6 +175,8 @@ cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t 
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s);
 cudaError_t lsq_trsm_rows(double* A, int64_t m, int K, const double* R, cudaStream_t s);
 cudaError_t lsq_trmm(const double* A, const double* B, double* C, int K, cudaStream_t s);
+cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, double* Ri_ws, double* out,
+                         cudaStream_t s);   // out = A R^{-1} (R upper K x K)
 cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scale, double* A, cudaStream_t s);
 cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int K, const double* scale, double* M,
                                double* Ri_ws, cudaStream_t s);

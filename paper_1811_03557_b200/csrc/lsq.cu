@@ -67,33 +67,85 @@ __global__ void gram_kernel(const double* __restrict__ A, int64_t m, int K, doub
   }
 }
 
-// In-place Cholesky of the upper triangle of G (col-major, G[i + j*K] for i <= j) -> R upper.
-// Single CTA (K <= ~1000); right-looking. Sets *fail if a pivot is not positive.
-__global__ void cholesky_kernel(double* G, int K, int* fail) {
-  __shared__ double piv;
-  for (int k = 0; k < K; ++k) {
+
+// Blocked right-looking Cholesky G = R^T R (upper R, column-major K x K, upper triangle used),
+// block size CB: (1) unblocked factor of the diagonal block in shared memory (one CTA),
+// (2) row-panel solve R_kk^T X = G_k,j for the columns right of the block (one thread per column),
+// (3) trailing update G_ij -= Σ_{k in block} R_ki R_kj for i <= j (2D grid).
+constexpr int CB = 32;
+
+__global__ void chol_diag_kernel(double* G, int K, int k0, int* fail) {
+  __shared__ double a[CB][CB + 1];
+  const int nb = min(CB, K - k0);
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    a[i][j] = G[(size_t)(k0 + j) * K + k0 + i];
+  }
+  __syncthreads();
+  for (int k = 0; k < nb; ++k) {
     if (threadIdx.x == 0) {
-      const double d = G[(size_t)k * K + k];
+      const double d = a[k][k];
       if (!(d > 0.0)) *fail = 1;
-      piv = d > 0.0 ? sqrt(d) : 1.0;
-      G[(size_t)k * K + k] = piv;
+      a[k][k] = d > 0.0 ? sqrt(d) : 1.0;
     }
     __syncthreads();
-    for (int j = k + 1 + threadIdx.x; j < K; j += blockDim.x) G[(size_t)j * K + k] /= piv;
+    for (int j = k + 1 + threadIdx.x; j < nb; j += blockDim.x) a[k][j] /= a[k][k];
     __syncthreads();
-    // trailing update: G[i][j] -= R[k][i] R[k][j] for k < i <= j
-    const int rem = K - k - 1;
-    const long tot = (long)rem * rem;
-    for (long t = threadIdx.x; t < tot; t += blockDim.x) {
-      const int ii = k + 1 + (int)(t % rem), jj = k + 1 + (int)(t / rem);
-      if (ii <= jj) G[(size_t)jj * K + ii] -= G[(size_t)ii * K + k] * G[(size_t)jj * K + k];
+    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+      const int i = e % nb, j = e / nb;
+      if (i > k && j >= i) a[i][j] -= a[k][i] * a[k][j];
     }
     __syncthreads();
   }
-  // zero the strict lower triangle
-  for (long t = threadIdx.x; t < (long)K * K; t += blockDim.x) {
-    const int i = (int)(t % K), j = (int)(t / K);
-    if (i > j) G[t] = 0.0;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    G[(size_t)(k0 + j) * K + k0 + i] = (i <= j) ? a[i][j] : 0.0;
+  }
+}
+
+__global__ void chol_panel_kernel(double* G, int K, int k0) {
+  const int nb = min(CB, K - k0);
+  const int j = k0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= K) return;
+  double x[CB];
+  for (int i = 0; i < nb; ++i) {
+    double v = G[(size_t)j * K + k0 + i];
+    for (int q = 0; q < i; ++q) v -= G[(size_t)(k0 + i) * K + k0 + q] * x[q];
+    x[i] = v / G[(size_t)(k0 + i) * K + k0 + i];
+  }
+  for (int i = 0; i < nb; ++i) G[(size_t)j * K + k0 + i] = x[i];
+}
+
+__global__ void chol_update_kernel(double* G, int K, int k0) {
+  const int nb = min(CB, K - k0);
+  const int i = k0 + nb + blockIdx.y * 16 + threadIdx.y;
+  const int j = k0 + nb + blockIdx.x * 16 + threadIdx.x;
+  if (i >= K || j >= K || i > j) return;
+  double s = 0.0;
+  for (int q = 0; q < nb; ++q) s = fma(G[(size_t)i * K + k0 + q], G[(size_t)j * K + k0 + q], s);
+  G[(size_t)j * K + i] -= s;
+}
+
+__global__ void zero_lower_kernel(double* G, int K) {
+  const long t = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (t >= (long)K * K) return;
+  const int i = (int)(t % K), j = (int)(t / K);
+  if (i > j) G[t] = 0.0;
+}
+
+// Back substitution R x = e_j for every column j, one warp per column (the inner products over
+// the already-solved entries are warp-parallel): R^{-1}, upper triangular.
+__global__ void rinv_warp_kernel(const double* __restrict__ R, int K, double* __restrict__ Ri) {
+  const int j = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (j >= K) return;
+  double* x = Ri + (size_t)j * K;
+  for (int i = j + 1 + lane; i < K; i += 32) x[i] = 0.0;
+  for (int i = j; i >= 0; --i) {
+    double v = 0.0;
+    for (int k = i + 1 + lane; k <= j; k += 32) v = fma(R[(size_t)k * K + i], x[k], v);
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) x[i] = ((i == j ? 1.0 : 0.0) - v) / R[(size_t)i * K + i];
+    __syncwarp();
   }
 }
 
@@ -129,18 +181,6 @@ __global__ void diag_ratio_kernel(const double* R, int K, double* out) {
   *out = mx / mn;
 }
 
-// R^{-1} of the upper-triangular K x K R (col-major), one column per thread (back substitution of e_j).
-__global__ void rinv_kernel(const double* __restrict__ R, int K, double* __restrict__ Ri) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= K) return;
-  double* x = Ri + (size_t)j * K;
-  for (int i = K - 1; i > j; --i) x[i] = 0.0;
-  for (int i = j; i >= 0; --i) {
-    double v = (i == j) ? 1.0 : 0.0;
-    for (int k = i + 1; k <= j; ++k) v -= R[(size_t)k * K + i] * x[k];
-    x[i] = v / R[(size_t)i * K + i];
-  }
-}
 
 // M = diag(scale) R^{-1} Q^T  (K x m, row-major), Q col-major m x K (so Q^T rows are contiguous).
 // 32x32 output tiles, k-loop over 32-wide panels (R^{-1} upper: panels below the diagonal skipped).
@@ -175,43 +215,67 @@ __global__ void lsq_operator_kernel(const double* __restrict__ Ri, const double*
   }
 }
 
-// coef[r][c] = Σ_i M[c][i] g[r][i]: one 128-thread block per (c, r)
+// coef[r][c] = Σ_i M[c][i] g[r][i]: one 128-thread block per row c, all right-hand sides at once
+// (M is read once per apply).
+constexpr int GEMV_R = 4;
 __global__ void lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K, const double* __restrict__ g, int nrhs,
                                 double* __restrict__ coef) {
-  const int c = blockIdx.x, r = blockIdx.y;
+  const int c = blockIdx.x;
   const double* a = M + (size_t)c * m;
-  const double* b = g + (size_t)r * m;
-  double s = 0.0;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) s = fma(a[i], b[i], s);
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  __shared__ double red[4];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) coef[(size_t)r * K + c] = (red[0] + red[1]) + (red[2] + red[3]);
+  __shared__ double red[GEMV_R][4];
+  for (int r0 = 0; r0 < nrhs; r0 += GEMV_R) {
+    const int nr = min(GEMV_R, nrhs - r0);
+    double s[GEMV_R] = {0, 0, 0, 0};
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const double av = a[i];
+#pragma unroll
+      for (int q = 0; q < GEMV_R; ++q)
+        if (q < nr) s[q] = fma(av, g[(size_t)(r0 + q) * m + i], s[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < GEMV_R; ++q) {
+      for (int o = 16; o; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+      if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = s[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      const int q = threadIdx.x;
+      coef[(size_t)(r0 + q) * K + c] = (red[q][0] + red[q][1]) + (red[q][2] + red[q][3]);
+    }
+    __syncthreads();
+  }
 }
 
 // u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
-// per block, coefficients staged in shared memory.
-__global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int r,
-                               int clamp, double* __restrict__ ug) {
-  extern __shared__ double sc[];   // K coefficients + 8 x 32 partial sums
-  const double* cr = coef + (size_t)r * K;
-  for (int c = threadIdx.x; c < K; c += blockDim.x) sc[c] = cr[c];
-  double* part = sc + K;
+// per block, up to 2 right-hand sides per pass (E read once), coefficients staged in shared memory.
+__global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int r0,
+                               int nr, int clamp, double* __restrict__ ug) {
+  extern __shared__ double sc[];   // nr * K coefficients + 2 x 8 x 32 partial sums
+  for (int i = threadIdx.x; i < nr * K; i += blockDim.x) sc[i] = coef[(size_t)r0 * K + i];
+  double* part = sc + nr * K;
   __syncthreads();
   const int gl = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * 32 + gl;
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0;
   if (g < ng)
-    for (int c = sl; c < K; c += 8) s = fma(E[(size_t)c * ng + g], sc[c], s);
-  part[sl * 32 + gl] = s;
+    for (int c = sl; c < K; c += 8) {
+      const double e = E[(size_t)c * ng + g];
+      s0 = fma(e, sc[c], s0);
+      if (nr > 1) s1 = fma(e, sc[K + c], s1);
+    }
+  part[sl * 32 + gl] = s0;
+  part[256 + sl * 32 + gl] = s1;
   __syncthreads();
-  if (sl == 0 && g < ng) {
-    double t = part[gl];
-    for (int q = 1; q < 8; ++q) t += part[q * 32 + gl];
-    ug[(size_t)r * ng + g] = clamp ? fmax(t, 0.0) : t;
+  if (sl < nr && g < ng) {
+    double t = part[sl * 256 + gl];
+    for (int q = 1; q < 8; ++q) t += part[sl * 256 + q * 32 + gl];
+    ug[(size_t)(r0 + sl) * ng + g] = clamp ? fmax(t, 0.0) : t;
   }
 }
+
+}  // namespace
+cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s);
+namespace {
 
 dpm_status chol_qr_pass(dpm_ctx* ctx, double* A, int64_t m, int K, double* Rout, int* dfail, cudaStream_t s) {
   DPM_CUDA_TRY(ctx, cudaMemsetAsync(Rout, 0, (size_t)K * K * sizeof(double), s));
@@ -221,8 +285,8 @@ dpm_status chol_qr_pass(dpm_ctx* ctx, double* A, int64_t m, int K, double* Rout,
   const int nsplit = (int)((m + rps - 1) / rps);
   DPM_COUNT_LAUNCH(1);
   gram_kernel<<<dim3(tiles, tiles, nsplit), TB, 0, s>>>(A, m, K, Rout, rps);
-  DPM_COUNT_LAUNCH(1);
-  cholesky_kernel<<<1, 1024, 0, s>>>(Rout, K, dfail);
+  cudaError_t ce = lsq_cholesky(Rout, K, dfail, s);
+  if (ce != cudaSuccess) { ctx->err = cudaGetErrorString(ce); return DPM_ERR_CUDA; }
   DPM_COUNT_LAUNCH(1);
   trsm_rows_kernel<<<(m + 127) / 128, 128, 0, s>>>(A, m, K, Rout);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
@@ -262,7 +326,7 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   if (!ctx->Mlsq) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->Mlsq, (size_t)m * K * sizeof(double)));
   double* Ri = R1;   // R1 is free after the trmm
   DPM_COUNT_LAUNCH(1);
-  rinv_kernel<<<(K + 63) / 64, 64, 0, s>>>(ctx->R, K, Ri);
+  rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(ctx->R, K, Ri);
   DPM_COUNT_LAUNCH(1);
   lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri, ctx->Q, ctx->colscale, K, m,
                                                                                       ctx->Mlsq);
@@ -283,12 +347,72 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN], ng = ctx->counts[DPM_SET_GAMMA];
   DPM_COUNT_LAUNCH(1);
-  lsq_gemv_kernel<<<dim3(K, nrhs), 128, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
+  lsq_gemv_kernel<<<K, 128, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
   if (u_gamma) return lsq_extend(ctx->E, ng, K, coef, nrhs, clamp, u_gamma, s);
   return cudaGetLastError();
 }
 
+// C = A T (m x K, column-major, ld m) for A m x K column-major and T K x K column-major upper
+// triangular: 64 x 64 output tiles, 16-deep k panels, 4 x 4 outputs per thread (k panels below the
+// diagonal of T are skipped).  Replaces the row-by-row triangular solve A <- A R^{-1} (T = R^{-1}).
+__global__ void __launch_bounds__(256) gemm_upper_kernel(const double* __restrict__ A, int64_t m, int K,
+                                                          const double* __restrict__ T, double* __restrict__ Cm) {
+  const int64_t i0 = (int64_t)blockIdx.x * 64;
+  const int j0 = blockIdx.y * 64;
+  __shared__ double sA[16][65], sT[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const int kend = min(K, j0 + 64);
+  for (int k0 = 0; k0 < kend; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int r = e & 63, kk = e >> 6;
+      const int64_t i = i0 + r;
+      const int k = k0 + kk;
+      sA[kk][r] = (i < m && k < K) ? A[(size_t)k * m + i] : 0.0;
+      const int kk2 = e & 15, c = e >> 4;
+      const int k2 = k0 + kk2, j = j0 + c;
+      sT[kk2][c] = (k2 < K && j < K && k2 <= j) ? T[(size_t)j * K + k2] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double av[4], tv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sA[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) tv[b] = sT[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], tv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t i = i0 + ty + 16 * a;
+      const int j = j0 + tx + 16 * b;
+      if (i < m && j < K) Cm[(size_t)j * m + i] = acc[a][b];
+    }
+}
+
 // ---- building blocks shared with the octant DD (dd.cu): distributed CholeskyQR2 ----
+cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, double* Ri_ws, double* out,
+                         cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(R, K, Ri_ws);
+  if (m == 0) return cudaGetLastError();
+  DPM_COUNT_LAUNCH(1);
+  gemm_upper_kernel<<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, Ri_ws, out);
+  return cudaGetLastError();
+}
+
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(G, 0, (size_t)K * K * sizeof(double), s);
   if (e != cudaSuccess) return e;
@@ -302,8 +426,18 @@ cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t 
 }
 
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s) {
+  for (int k0 = 0; k0 < K; k0 += CB) {
+    DPM_COUNT_LAUNCH(1);
+    chol_diag_kernel<<<1, 256, 0, s>>>(G, K, k0, dfail);
+    const int rest = K - k0 - std::min(CB, K - k0);
+    if (rest > 0) {
+      DPM_COUNT_LAUNCH(2);
+      chol_panel_kernel<<<(rest + 127) / 128, 128, 0, s>>>(G, K, k0);
+      chol_update_kernel<<<dim3((rest + 15) / 16, (rest + 15) / 16), dim3(16, 16), 0, s>>>(G, K, k0);
+    }
+  }
   DPM_COUNT_LAUNCH(1);
-  cholesky_kernel<<<1, 1024, 0, s>>>(G, K, dfail);
+  zero_lower_kernel<<<(unsigned)(((long)K * K + 255) / 256), 256, 0, s>>>(G, K);
   return cudaGetLastError();
 }
 
@@ -330,7 +464,7 @@ cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scal
 cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int K, const double* scale, double* M,
                                double* Ri_ws, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
-  rinv_kernel<<<(K + 63) / 64, 64, 0, s>>>(R, K, Ri_ws);
+  rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(R, K, Ri_ws);
   if (m == 0) return cudaGetLastError();
   DPM_COUNT_LAUNCH(1);
   lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri_ws, Q, scale, K, m, M);
@@ -339,16 +473,17 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
 
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
-  lsq_gemv_kernel<<<dim3(K, nrhs), 128, 0, s>>>(M, m, K, g, nrhs, coef);
+  lsq_gemv_kernel<<<K, 128, 0, s>>>(M, m, K, g, nrhs, coef);
   return cudaGetLastError();
 }
 
 cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, int nrhs, int clamp, double* ug,
                        cudaStream_t s) {
-  const size_t smem = (size_t)(K + 256) * sizeof(double);
-  for (int r = 0; r < nrhs; ++r) {
+  for (int r = 0; r < nrhs; r += 2) {
+    const int nr = std::min(2, nrhs - r);
+    const size_t smem = (size_t)(nr * K + 512) * sizeof(double);
     DPM_COUNT_LAUNCH(1);
-    extend2_kernel<<<(unsigned)((ng + 31) / 32), 256, smem, s>>>(E, ng, K, coef, r, clamp, ug);
+    extend2_kernel<<<(unsigned)((ng + 31) / 32), 256, smem, s>>>(E, ng, K, coef, r, nr, clamp, ug);
   }
   return cudaGetLastError();
 }
