@@ -249,7 +249,8 @@ int64_t dpm_launch_count(void);
 /* Measurement hooks (bench.py's per-kernel roofline).  While enabled, every pass of
  * dpm_aux_solve_batch is bracketed by two CUDA events recorded on the caller's stream.
  * dpm_pass_times synchronizes those events and returns, per pass kind k (0: transform along x,
- * 1: transform along y, 2: tridiagonal / transform along z), the summed duration ms[k] (HOST,
+ * 1: transform along y, or the fused y / z / y plane pass at n = 128, 2: tridiagonal / transform
+ * along z), the summed duration ms[k] (HOST,
  * milliseconds), the number of launches[k] and the grid points processed points[k] since the
  * last call (or since enabling), then resets.  Synchronous; DPM_ERR_INVALID on null pointers. */
 dpm_status dpm_set_pass_timing(dpm_ctx* ctx, int32_t enable);

@@ -38,6 +38,7 @@ struct DstPlan {
   int solver = DPM_SOLVER_DST2_TRIDIAG;
   double* atab128 = nullptr;  // n = 128: A fragments of the prime-factor DST-I
   int pfa = 1;            // n = 128: prime-factor DST-I for the x / y passes (DPM_PFA=0 disables)
+  int plane = 1;          // n = 128: fused y / z / y plane pass (DPM_PLANE=0 disables)
   PassProf* prof = nullptr;   // non-null while pass timing is enabled
 };
 
@@ -152,6 +153,8 @@ size_t dst_scratch_bytes(int n, int chunk);
 cudaError_t dst128_init();
 cudaError_t dst128_atab(double** tab);
 cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, const double* atab, cudaStream_t s);
+cudaError_t plane128_pass(double* u, int nfields, const double* lam, double inv_dt, double h2, double rscale,
+                          cudaStream_t s);
 
 // setup.cu
 dpm_status setup_point_sets(dpm_ctx* ctx);

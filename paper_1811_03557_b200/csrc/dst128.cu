@@ -31,6 +31,8 @@
 #include <cstdint>
 #include <utility>
 
+#include <cooperative_groups.h>
+
 #include "dpm_internal.h"
 
 namespace {
@@ -457,6 +459,205 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fused plane pass: after the x transform every x-mode plane a ([y][z], 128 x 128,
+// contiguous) is independent.  One 2-CTA cluster per plane; CTA r holds columns z in [64r, 64r+64)
+// of the plane in shared memory (pitch 65: conflict-free for both the column-wise transforms and
+// the row-wise recurrences) and runs, on chip:
+//   (1) y forward DST-I of its 64 columns (thread-per-column DFMA, same factorisation as above,
+//       inputs held in registers so the outputs overwrite the column in place),
+//   (2) the exact z tridiagonal solve of every y-mode row b, split at z = 64 between the two CTAs:
+//       each CTA solves its half with a zero interface value, the halves exchange one boundary value
+//       per row through distributed shared memory, solve the 2x2 interface system and add the
+//       closed-form homogeneous responses g_L[k] = μ^{64-k}(1-μ^{2(k+1)})/(1-μ^{130}), g_R[k] = g_L[63-k],
+//   (3) y inverse DST-I,
+// replacing three streaming passes over the field (y, z, y) by one.
+constexpr int PHC = 64;          // columns per CTA
+constexpr int PPITCH = 65;       // row pitch (doubles)
+constexpr int PTHR = 128;        // 4 warps x 16 columns x 2 halves
+
+template <int J2, int E>
+__device__ __forceinline__ double ldzp(const double* colp, bool hi) {
+  constexpr int ja = crt_c(0, J2, E), jb = crt_c(1, J2, E);
+  const double v = colp[(hi ? crow(jb) : crow(ja)) * PPITCH];
+  constexpr int sa = cneg(ja) ? (int)0x80000000 : 0, sb = cneg(jb) ? (int)0x80000000 : 0;
+  return __hiloint2double(__double2hiint(v) ^ (hi ? sb : sa), __double2loint(v));
+}
+
+template <int... E>
+__device__ __forceinline__ void prep_regs(const double* colp, bool hi, double (&pin)[22], double (&qin)[22],
+                                          double (&wp)[22], std::integer_sequence<int, E...>) {
+  wp[0] = ldzp<1, 0>(colp, hi);
+  pin[0] = qin[0] = 0.0;
+  auto one = [&](auto ec) {
+    constexpr int e = decltype(ec)::value;
+    const double u = ldzp<0, e>(colp, hi);
+    const double wa = ldzp<1, e>(colp, hi), wb = ldzp<1, 43 - e>(colp, hi);
+    const double wm = wa - wb;
+    pin[e] = u + wm;
+    qin[e] = fma(-0.5, wm, u);
+    wp[e] = wa + wb;
+  };
+  (one(std::integral_constant<int, E + 1>{}), ...);
+}
+
+template <int K0, int KB, typename Emit>
+__device__ __forceinline__ void contract_regs(const double (&pin)[22], const double (&qin)[22],
+                                              const double (&wp)[22], Emit&& emit) {
+  double P[KB], Q[KB], R[KB];
+#pragma unroll
+  for (int q = 0; q < KB; ++q) P[q] = Q[q] = R[q] = 0.0;
+#pragma unroll
+  for (int e = 0; e <= 21; ++e)
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int k3 = K0 + q;
+      const int m = (e * k3) % 43;
+      const double cm = m <= 21 ? c_c43[m] : c_c43[43 - m];
+      R[q] = fma(wp[e], cm, R[q]);
+      if (e >= 1 && k3 >= 1) {
+        const double sm = m <= 21 ? c_s43[m] : -c_s43[43 - m];
+        P[q] = fma(pin[e], sm, P[q]);
+        Q[q] = fma(qin[e], sm, Q[q]);
+      }
+    }
+#pragma unroll
+  for (int q = 0; q < KB; ++q) emit(std::integral_constant<int, K0>{}, q, P[q], Q[q], R[q]);
+}
+
+// In-place DST-I along the rows (y) of this CTA's 64 columns.
+__device__ __forceinline__ void plane_ydst(double* P) {
+  const int lane = threadIdx.x & 31;
+  const bool hi = lane >= 16;
+  const int col = (threadIdx.x >> 5) * 16 + (lane & 15);
+  double* colp = P + col;
+  double pin[22], qin[22], wp[22];
+  prep_regs(colp, hi, pin, qin, wp, std::make_integer_sequence<int, 21>{});
+  __syncwarp();   // both halves of every column have read their inputs: outputs may overwrite it
+  const double sm1 = hi ? -1.0 : 1.0;
+  auto bfly = [&](auto k0c, int q, double Pv, double Qv, double Rv) {
+    const int k3 = decltype(k0c)::value + q;
+    const double Ps = fma(sm1, Pv, __shfl_xor_sync(0xffffffffu, Pv, 16));
+    const double Qs = fma(sm1, Qv, __shfl_xor_sync(0xffffffffu, Qv, 16));
+    const double Rs = fma(sm1, Rv, __shfl_xor_sync(0xffffffffu, Rv, 16));
+    const double V[3] = {Ps, Qs + Rs, Qs - Rs};
+#pragma unroll
+    for (int mir = 0; mir < 2; ++mir) {
+      if (mir && k3 == 0) break;
+      const int k3f = mir ? 43 - k3 : k3;
+#pragma unroll
+      for (int k2 = 0; k2 < 3; ++k2) {
+        const int ka = (86 * k2 + 6 * k3f) % 258, kb = (129 + 86 * k2 + 6 * k3f) % 258;
+        const bool va = ka >= 1 && ka <= 128, vb = kb >= 1 && kb <= 128;
+        if (!va && !vb) continue;
+        const double v = !mir ? V[k2] : (k2 == 0 ? -V[0] : (k2 == 1 ? -V[2] : -V[1]));
+        if (hi ? vb : va) colp[((hi ? kb : ka) - 1) * PPITCH] = v;
+      }
+    }
+  };
+  contract_regs<0, 6>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<6, 6>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<12, 6>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<18, 4>(pin, qin, wp, bfly);
+  __syncwarp();
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHR, 2)
+plane128_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double inv_dt, double h2, double rscale) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double psm[];
+  double* P = psm;                           // [128 rows][PPITCH]
+  double* lam = psm + N * PPITCH;            // [128]
+  double* xch = lam + N;                     // [128] boundary value received from the partner
+  const int rank = (int)cluster.block_rank();
+  const long plane = blockIdx.x >> 1;        // field * 128 + a
+  const int a = (int)(plane & (N - 1));
+  double* gp = u + (size_t)plane * NN + (size_t)rank * PHC;
+  for (int i = threadIdx.x; i < N; i += PTHR) lam[i] = lam_g[i];
+  // load the half plane: rows of 64 contiguous doubles, 8-byte cp.async (all in flight at once)
+  {
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(P);
+#pragma unroll 16
+    for (int e = threadIdx.x; e < N * PHC; e += PTHR) {
+      const int r = e >> 6, c = e & 63;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (unsigned)(r * PPITCH + c)),
+                   "l"(gp + (size_t)r * N + c));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+  plane_ydst(P);
+  __syncthreads();
+  // z tridiagonal per y-mode row b = threadIdx.x, on this CTA's half (local k = 0..63)
+  {
+    const int b = threadIdx.x;
+    double* row = P + b * PPITCH;
+    const double hs = h2 * ((inv_dt + lam[a]) + lam[b]);
+    const double disc = sqrt(hs * (hs + 4.0));
+    const double mu = 2.0 / ((2.0 + hs) + disc);
+    constexpr int M = PHC;
+    // A^{-1} r = μ z: forward y_k = r_k + μ y_{k-1}, backward z_k = y_k + μ z_{k+1}
+    double y = 0.0;
+    for (int k = 0; k < M; ++k) {
+      y = fma(mu, y, rscale * row[k]);
+      row[k] = y;
+    }
+    double z = 0.0;
+    for (int k = M - 1; k >= 0; --k) {
+      z = fma(mu, z, row[k]);
+      row[k] = z;
+    }
+    // local Dirichlet solve x_k = μ z_k - c2 (μ^{k+1} - μ^{2M+1-k}),  c2 = μ^2 z_0 / (1 - μ^{2M+2});
+    // only the interface entry is needed before the exchange (x_63 left, x_0 right)
+    double muM = mu;                                       // μ^M, M = 64 = 2^6
+#pragma unroll
+    for (int q = 0; q < 6; ++q) muM *= muM;
+    const double mu2M1 = muM * muM * mu;                   // μ^{2M+1}
+    const double den = 1.0 - mu2M1 * mu;                   // 1 - μ^{2M+2}
+    const double c2 = mu * mu * row[0] / den;
+    const double mine = rank == 0 ? fma(mu, row[M - 1], -c2 * (muM - muM * mu * mu))   // k = 63
+                                  : fma(mu, row[0], -c2 * (mu - mu2M1));                // k = 0
+    // interface: left half (rank 0) owns z = 63 (local 63), right half (rank 1) owns z = 64 (local 0)
+    double* peer = cluster.map_shared_rank(xch, rank ^ 1);
+    peer[b] = mine;
+    cluster.sync();
+    const double other = xch[b];
+    const double x63 = rank == 0 ? mine : other, y0 = rank == 0 ? other : mine;
+    const double gam = mu * (1.0 - muM * muM) / den;       // g_L[63] = g_R[0]
+    const double v63 = (x63 + y0 * gam) / (1.0 - gam * gam);
+    const double v64 = y0 + v63 * gam;
+    const double w = (rank == 0 ? v64 : v63) / den;
+    // final: v_k = μ z_k - c2 (μ^{k+1} - μ^{2M+1-k}) + w (g1_k - g2_k) with the homogeneous response
+    //   left  g_L[k] den = μ^{M-k} - μ^{M+k+2},   right g_R[k] den = μ^{k+1} - μ^{2M+1-k}
+    // (the right response is the same power pair as the Sherman–Morrison term)
+    const double imu = 1.0 / mu;
+    double pa = mu, pb = mu2M1;                            // μ^{k+1}, μ^{2M+1-k}
+    double ga = rank == 0 ? muM : mu;                      // left: μ^{M-k};   right: μ^{k+1}
+    double gb = rank == 0 ? muM * mu * mu : mu2M1;         // left: μ^{M+k+2}; right: μ^{2M+1-k}
+    const double fa = rank == 0 ? imu : mu, fb = rank == 0 ? mu : imu;
+    for (int k = 0; k < M; ++k) {
+      row[k] = fma(mu, row[k], fma(w, ga - gb, -c2 * (pa - pb)));
+      pa *= mu;
+      pb *= imu;
+      ga *= fa;
+      gb *= fb;
+    }
+  }
+  __syncthreads();
+  plane_ydst(P);
+  __syncthreads();
+  for (int e = threadIdx.x; e < N * PHC; e += PTHR) {
+    const int r = e >> 6, c = e & 63;
+    __stcg(gp + (size_t)r * N + c, P[r * PPITCH + c]);
+  }
+  // (all DSMEM writes into this CTA completed before the cluster barrier above)
+}
+
 unsigned long long g_tables_ready = 0;   // bit d: constant tables uploaded on device d
 
 }  // namespace
@@ -533,5 +734,18 @@ cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, co
   const int grid = (int)std::min<long>(ntiles, (long)sms * std::max(1, occ));
   DPM_COUNT_LAUNCH(1);
   k<<<grid, NTHR, smem, s>>>(in, out, nfields, atab);
+  return cudaGetLastError();
+}
+
+// Fused y-DST / z-tridiagonal / inverse y-DST over nfields n = 128 fields (in place), after the x pass.
+cudaError_t plane128_pass(double* u, int nfields, const double* lam, double inv_dt, double h2, double rscale,
+                          cudaStream_t s) {
+  const size_t smem = ((size_t)N * PPITCH + 2 * N) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(plane128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long ctas = 2L * nfields * N;
+  if (ctas > 2147483647L) return cudaErrorInvalidValue;
+  DPM_COUNT_LAUNCH(1);
+  plane128_kernel<<<(unsigned)ctas, PTHR, smem, s>>>(u, lam, inv_dt, h2, rscale);
   return cudaGetLastError();
 }

@@ -586,6 +586,8 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
   if (n == 128) {
     const char* env = getenv("DPM_PFA");
     p.pfa = !(env && atoi(env) == 0);
+    const char* envp = getenv("DPM_PLANE");
+    p.plane = !(envp && atoi(envp) == 0);
     if (p.pfa && (e = dst128_init()) != cudaSuccess) return e;
     if (p.pfa && (e = dst128_atab(&p.atab128)) != cudaSuccess) return e;
   }
@@ -652,6 +654,16 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     const long long pts = (long long)nf * (long long)fe;
     auto pass = [&](int k, const double* in) { return timed(p, k, pts, s, [&] { return run_pass(p, k, in, ui, nf, inv_dt, scale, s); }); };
     if ((e = pass(0, qi)) != cudaSuccess) return e;
+    if (n == 128 && p.pfa && p.plane && p.solver == DPM_SOLVER_DST2_TRIDIAG) {
+      // fused y / z / y pass over the x-mode planes, then the inverse x pass
+      const double sc2 = 2.0 / (n + 1);
+      if ((e = timed(p, 1, pts, s, [&] {
+             return plane128_pass(ui, nf, p.lam, inv_dt, p.h * p.h, sc2 * sc2 * p.h * p.h, s);
+           })) != cudaSuccess)
+        return e;
+      if ((e = pass(0, ui)) != cudaSuccess) return e;
+      continue;
+    }
     if ((e = pass(1, ui)) != cudaSuccess) return e;
     if (p.solver == DPM_SOLVER_DST2_TRIDIAG) {
       if ((e = timed(p, 2, pts, s, [&] { return run_ztri(p, ui, nf, s); })) != cudaSuccess) return e;
