@@ -301,7 +301,8 @@ def main():
         if tr and tr.get("points_per_launch"):
             traffic = tr["dram_bytes_per_launch"] * (k_pts / max(k_launch, 1)) / tr["points_per_launch"]
     kernel_names = {"x": "dst128f_kernel<0> (prime-factor DST-I along x, DFMA)",
-                    "y": "dst128f_kernel<1> (prime-factor DST-I along y, DFMA)",
+                    "y": "plane128_kernel (fused y-DST / z tridiagonal / inverse y-DST per x-mode plane, 2-CTA "
+                         "clusters)" if pt["z"][1] == 0 else "dst128f_kernel<1> (prime-factor DST-I along y, DFMA)",
                     "z": "ztri_warp_kernel<128> (exact tridiagonal solve along z)"}
 
     line = {"metric": "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction); PKS time steps/sec",
@@ -317,7 +318,7 @@ def main():
                          "peak_kind": peaks_kind + " (MEASURED_PEAKS.json hbm_gbs, burst copy)",
                          "alg_bytes_per_launch": k_bytes, "launch_ms": k_avg_s * 1e3, "share_of_step": share,
                          "passes": {k: {"ms": v[0], "launches": v[1], "points": v[2]} for k, v in pt.items()},
-                         "path": {"what": "whole AP solve (5 passes) per dpm_aux_solve_batch",
+                         "path": {"what": "whole AP solve (x pass, fused plane pass, x pass) per dpm_aux_solve_batch",
                                   "achieved": alg_bytes * value / world / 1e9 if world else 0.0,
                                   "frac": alg_bytes * value / world / 1e9 / hbm_peak,
                                   "alg_bytes_per_solve": alg_bytes},

@@ -40,6 +40,8 @@ struct DstPlan {
   int pfa = 1;            // n = 128: prime-factor DST-I for the x / y passes (DPM_PFA=0 disables)
   int plane = 1;          // n = 128: fused y / z / y plane pass (DPM_PLANE=0 disables)
   PassProf* prof = nullptr;   // non-null while pass timing is enabled
+  cudaStream_t side = nullptr;                    // second chunk stream (DPM_STREAMS=2)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 struct dpm_ctx {

@@ -472,6 +472,9 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
 //       closed-form homogeneous responses g_L[k] = μ^{64-k}(1-μ^{2(k+1)})/(1-μ^{130}), g_R[k] = g_L[63-k],
 //   (3) y inverse DST-I,
 // replacing three streaming passes over the field (y, z, y) by one.
+#ifndef PLANE_KB
+#define PLANE_KB 6
+#endif
 constexpr int PHC = 64;          // columns per CTA
 constexpr int PPITCH = 65;       // row pitch (doubles)
 constexpr int PTHR = 128;        // 4 warps x 16 columns x 2 halves
@@ -555,6 +558,27 @@ __device__ __forceinline__ void plane_ydst(double* P) {
       }
     }
   };
+#if PLANE_KB == 8
+  contract_regs<0, 8>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<8, 8>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<16, 6>(pin, qin, wp, bfly);
+  __syncwarp();
+#elif PLANE_KB == 4
+  contract_regs<0, 4>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<4, 4>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<8, 4>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<12, 4>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<16, 4>(pin, qin, wp, bfly);
+  __syncwarp();
+  contract_regs<20, 2>(pin, qin, wp, bfly);
+  __syncwarp();
+#else
   contract_regs<0, 6>(pin, qin, wp, bfly);
   __syncwarp();
   contract_regs<6, 6>(pin, qin, wp, bfly);
@@ -563,6 +587,7 @@ __device__ __forceinline__ void plane_ydst(double* P) {
   __syncwarp();
   contract_regs<18, 4>(pin, qin, wp, bfly);
   __syncwarp();
+#endif
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHR, 2)

@@ -595,6 +595,10 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
 }
 
 void dst_plan_free(DstPlan& p) {
+  if (p.side) cudaStreamDestroy(p.side);
+  if (p.ev_fork) cudaEventDestroy(p.ev_fork);
+  if (p.ev_join) cudaEventDestroy(p.ev_join);
+  p.side = nullptr;
   if (p.lam) cudaFree(p.lam);
   if (p.atab) cudaFree(p.atab);
   if (p.atab128) cudaFree(p.atab128);
@@ -646,10 +650,29 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
   const double sc = 2.0 / (n + 1);
   const double scale = sc * sc * sc;
   const size_t fe = (size_t)n * n * n;
-  for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+  // Optional: alternate chunks over two streams (DPM_STREAMS=2) so one chunk's launch ramp and
+  // tail overlap the next chunk's passes.
+  static const int nstreams = [] {
+    const char* v = getenv("DPM_STREAMS");
+    return v && atoi(v) == 2 ? 2 : 1;
+  }();
+  const cudaStream_t s0 = s;
+  const bool two = nstreams == 2 && batch > chunk && !p.prof;
+  if (two) {
+    if (!p.side) {
+      cudaStreamCreateWithFlags(&const_cast<DstPlan&>(p).side, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&const_cast<DstPlan&>(p).ev_fork, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&const_cast<DstPlan&>(p).ev_join, cudaEventDisableTiming);
+    }
+    cudaEventRecord(p.ev_fork, s0);
+    cudaStreamWaitEvent(p.side, p.ev_fork, 0);
+  }
+  int64_t ci = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++ci) {
     const int nf = (int)std::min<int64_t>(chunk, batch - b0);
     const double* qi = q + b0 * fe;
     double* ui = u + b0 * fe;
+    if (two) s = (ci & 1) ? p.side : s0;
     cudaError_t e;
     const long long pts = (long long)nf * (long long)fe;
     auto pass = [&](int k, const double* in) { return timed(p, k, pts, s, [&] { return run_pass(p, k, in, ui, nf, inv_dt, scale, s); }); };
@@ -672,6 +695,10 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     }
     if ((e = pass(1, ui)) != cudaSuccess) return e;
     if ((e = pass(0, ui)) != cudaSuccess) return e;
+  }
+  if (two) {
+    cudaEventRecord(p.ev_join, p.side);
+    cudaStreamWaitEvent(s0, p.ev_join, 0);
   }
   return cudaSuccess;
 }

@@ -50,7 +50,8 @@ def test_aux_solve_parity(api, n, solver):
 
 
 @pytest.mark.parametrize("solver", ["dst3", "dst2_tridiag"])
-@pytest.mark.parametrize("n,dt", [(128, 1.0), (33, 10.0), (64, 0.5 * (2.2 / 65) ** 2)])
+@pytest.mark.parametrize("n,dt", [(128, 1.0), (128, 0.5 * (2.2 / 129) ** 2), (128, 1e-8), (33, 10.0),
+                                  (64, 0.5 * (2.2 / 65) ** 2)])
 def test_aux_solve_parity_large_dt(api, n, dt, solver):
     # large dt: the z operator approaches the pure Laplacian (μ -> 1 in the tridiagonal solver)
     c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
@@ -58,6 +59,18 @@ def test_aux_solve_parity_large_dt(api, n, dt, solver):
     q = random_boxes(7 + n, 1, n)
     u = c.aux_solve_batch(torch.from_numpy(q).cuda()).cpu().numpy()
     assert rel(u, ap.solve(q, c.info["h"], dt)) <= 1e-11
+
+
+def test_aux_solve_128_batch_chunked_inplace(api):
+    # n = 128: x pass -> fused plane pass (2-CTA clusters, split z solve) -> x pass, in place,
+    # over more than one 1 GiB chunk is too large for the oracle; 3 fields, u aliasing q
+    n, dt = 128, 2e-4
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    q = random_boxes(11, 3, n)
+    t = torch.from_numpy(q).cuda()
+    c.aux_solve_batch(t, t)
+    uo = ap.solve(q, c.info["h"], dt)
+    assert rel(t.cpu().numpy(), uo) <= 1e-11
 
 
 def test_aux_solve_inplace_chunked_and_empty(api):

@@ -1,6 +1,5 @@
-for cm in 224 1024 20000; do
-DPM_CHUNK_MB=$cm python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-pks > gpurun_out/b$cm.log 2>&1
+for cfg in "1 1024" "2 64" "2 128" "2 256" "1 64"; do set -- $cfg
+DPM_STREAMS=$1 DPM_CHUNK_MB=$2 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --no-pks --no-dd > gpurun_out/b.log 2>&1
 python -c "
-import json; d=json.loads(open('gpurun_out/b$cm.log').read().strip().splitlines()[-1]); r=d['roofline']
-print('CHUNK_MB=$cm', round(d['value']), round(d['ms_per_step'],2), {k:(round(v['ms']/v['launches']*1e3,1), round(16*v['points']/v['launches']/(v['ms']/v['launches']/1e3)/1e12,2)) for k,v in r['passes'].items()})"
+import json; d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]); print('streams=$1 chunkMB=$2', round(d['value']), round(d['ms_per_step'],2))"
 done
