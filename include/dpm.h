@@ -230,17 +230,20 @@ dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, doubl
 dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* stream);
 /* R31 initial state (rho, c on N+, [n][n][n]). */
 dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream);
-/* Local CFL bound h / (6 χ max|Δc|/h) (R19) -> *cfl_dt (HOST).  Synchronous. */
+/* Local CFL bound h / (6 χ max|Δc|/h) (R19) -> *cfl_dt (HOST).  Synchronous; with
+   cfl_dt == NULL it only enqueues the reduction and dpm_dd_cfl_result() (synchronous) returns it. */
 dpm_status dpm_dd_cfl(dpm_ctx* ctx, const double* c, double chi, double* cfl_dt, void* stream);
+dpm_status dpm_dd_cfl_result(dpm_ctx* ctx, double chi, double* cfl_dt, void* stream);
 /* Step 4a-5 at the ctx's dt (the factorisation must be at this dt): flux + IMEX RHS, particular
    solves, BEP right-hand sides on the rows, y = M_s g (K x 2, field-major). */
 dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* y,
                               void* stream);
 /* Steps 5-7 with the global C (K x 2): u_γ = A C (clamped at 0 if clamp, R17), Green's formula
-   (R20), restriction to N+.  stats (HOST, 5): [h^3 Σ_{M+} ρ, max ρ, min ρ, min c, nonfinite].
-   Synchronous. */
+   (R20), restriction to N+.  stats (HOST, 5): [h^3 Σ_{M+} ρ, max ρ, min ρ, min c, nonfinite];
+   synchronous when stats != NULL, otherwise asynchronous and dpm_dd_stats() (synchronous) reads them. */
 dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, double* rho, double* c,
                                double* stats, void* stream);
+dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream);
 
 /* Cumulative number of CUDA kernels this library has launched in the process (all
    contexts).  Lets a harness count the library's launches inside a timed region. */

@@ -89,6 +89,8 @@ _sig = {
     "dpm_dd_chol": ([P, C.c_int32, P, P], C.c_int),
     "dpm_dd_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
     "dpm_dd_cfl": ([P, P, C.c_double, D, P], C.c_int),
+    "dpm_dd_cfl_result": ([P, C.c_double, D, P], C.c_int),
+    "dpm_dd_stats": ([P, D, P], C.c_int),
     "dpm_dd_local_begin": ([P, P, P, C.c_double, P, P], C.c_int),
     "dpm_dd_local_finish": ([P, P, C.c_int32, P, P, D, P], C.c_int),
     "dpm_pass_times": ([P, D, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),

@@ -21,6 +21,14 @@ def _stream(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
 def _dev_f64(t: torch.Tensor, name: str):
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
@@ -250,8 +258,26 @@ class Octant(DPM):
         self._chk(L.lib.dpm_dd_cfl(self._h, _ptr(_dev_f64(c, "c")), chi, C.byref(out), _stream(stream)))
         return out.value
 
+    def cfl_async(self, c, chi=1.0, stream=None):
+        self._chk(L.lib.dpm_dd_cfl(self._h, _ptr(_dev_f64(c, "c")), chi, None, _stream(stream)))
+
+    def cfl_result(self, chi=1.0, stream=None) -> float:
+        out = C.c_double()
+        self._chk(L.lib.dpm_dd_cfl_result(self._h, chi, C.byref(out), _stream(stream)))
+        return out.value
+
+    def stats(self, stream=None):
+        st = (C.c_double * 5)()
+        self._chk(L.lib.dpm_dd_stats(self._h, st, _stream(stream)))
+        return {"mass": st[0], "rho_max": st[1], "rho_min": st[2], "c_min": st[3], "nonfinite": st[4]}
+
+    def local_finish_async(self, Cglob, rho, c, clamp=1, stream=None):
+        self._chk(L.lib.dpm_dd_local_finish(self._h, _ptr(_dev_f64(Cglob, "C")), clamp, _ptr(rho), _ptr(c), None,
+                                            _stream(stream)))
+
     def local_begin(self, rho, c, chi=1.0, stream=None):
-        y = self._t(2, self.K)
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            y = self._t(2, self.K)
         self._chk(L.lib.dpm_dd_local_begin(self._h, _ptr(rho), _ptr(c), chi, _ptr(y), _stream(stream)))
         return y
 

@@ -427,11 +427,19 @@ dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_i
 dpm_status dpm_dd_cfl(dpm_ctx* ctx, const double* c, double chi, double* cfl_dt, void* stream) {
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
-  if (!c || !cfl_dt || !(chi > 0)) return DPM_ERR_INVALID;
+  if (!c || !(chi > 0)) return DPM_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
   DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, ctx->red, s));
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host, ctx->red, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (!cfl_dt) return DPM_OK;   // asynchronous form: dpm_dd_cfl_result() later
+  return dpm_dd_cfl_result(ctx, chi, cfl_dt, stream);
+}
+
+dpm_status dpm_dd_cfl_result(dpm_ctx* ctx, double chi, double* cfl_dt, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!cfl_dt || !(chi > 0)) return DPM_ERR_INVALID;
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(as_stream(stream)));
   const double h = ctx->h;
   double cfl = INFINITY;
   for (int a = 0; a < 3; ++a) {
@@ -471,7 +479,7 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
                                void* stream) {
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
-  if (!C || !rho || !c || !stats || !ctx->scratch) return DPM_ERR_INVALID;
+  if (!C || !rho || !c || !ctx->scratch) return DPM_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA];
@@ -484,7 +492,15 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
   DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (!stats) return DPM_OK;   // asynchronous form: dpm_dd_stats() later
+  return dpm_dd_stats(ctx, stats, stream);
+}
+
+dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!stats) return DPM_ERR_INVALID;
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(as_stream(stream)));
   const double* R = ctx->red_host + 8;   // [mass_sum, rho_max, rho_min, c_min, nonfinite] (R18)
   stats[0] = R[0] * ctx->h * ctx->h * ctx->h;
   stats[1] = decode_key(R[1]);

@@ -402,6 +402,52 @@ __global__ void __launch_bounds__(256) gemm_upper_kernel(const double* __restric
     }
 }
 
+// G(i, j) += Σ_{r in this block's rows} A(r, i) A(r, j) for the upper 64 x 64 tiles (i <= j tiles);
+// A m x K column-major; 16-row panels, 4 x 4 outputs per thread, atomics over the row splits.
+__global__ void __launch_bounds__(256) gram64_kernel(const double* __restrict__ A, int64_t m, int K, double* G,
+                                                      int64_t rows_per_split) {
+  const int bi = blockIdx.x * 64, bj = blockIdx.y * 64;
+  if (bj < bi) return;
+  const int64_t r0 = (int64_t)blockIdx.z * rows_per_split, r1 = min(m, r0 + rows_per_split);
+  __shared__ double sa[16][65], sb[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t rr = r0; rr < r1; rr += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int r = e & 15, c = e >> 4;
+      const int64_t row = rr + r;
+      const bool ok = row < r1;
+      sa[r][c] = (ok && bi + c < K) ? A[(size_t)(bi + c) * m + row] : 0.0;
+      sb[r][c] = (ok && bj + c < K) ? A[(size_t)(bj + c) * m + row] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sa[r][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = sb[r][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = bi + ty + 16 * a, j = bj + tx + 16 * b;
+      if (i < K && j < K && i <= j) atomicAdd(G + (size_t)j * K + i, acc[a][b]);
+    }
+}
+
 // ---- building blocks shared with the octant DD (dd.cu): distributed CholeskyQR2 ----
 cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, double* Ri_ws, double* out,
                          cudaStream_t s) {
@@ -416,12 +462,13 @@ cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, dou
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(G, 0, (size_t)K * K * sizeof(double), s);
   if (e != cudaSuccess) return e;
-  const int tiles = (K + 31) / 32;
-  const int64_t target_split = std::max<int64_t>(1, (148 * 4) / ((int64_t)tiles * (tiles + 1) / 2));
-  const int64_t rps = std::max<int64_t>(32, ((m + target_split - 1) / target_split + 31) / 32 * 32);
+  const int tiles = (K + 63) / 64;
+  const int64_t upper = (int64_t)tiles * (tiles + 1) / 2;
+  const int64_t target_split = std::max<int64_t>(1, (148 * 4) / upper);
+  const int64_t rps = std::max<int64_t>(64, ((m + target_split - 1) / target_split + 15) / 16 * 16);
   const int nsplit = (int)std::max<int64_t>(1, (m + rps - 1) / rps);
   DPM_COUNT_LAUNCH(1);
-  gram_kernel<<<dim3(tiles, tiles, nsplit), TB, 0, s>>>(A, m, K, G, rps);
+  gram64_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, s>>>(A, m, K, G, rps);
   return cudaGetLastError();
 }
 

@@ -32,6 +32,8 @@ class DDSolver:
         self.builds = 0
         self.t = 0.0
         self.fields: List = []
+        # one CUDA stream per local octant: the octants' small kernels overlap on the GPU
+        self.streams = [torch.cuda.Stream(o.device) if o.device.type == "cuda" else None for o in self.octs]
 
     # ---- global least squares (distributed CholeskyQR2) at dt
     def _sum(self, parts: List[torch.Tensor]) -> torch.Tensor:
@@ -64,21 +66,48 @@ class DDSolver:
             self.fields.append((rho, c))
         self.dt_prev, self.t = float("inf"), 0.0
 
+    def _on(self, i):
+        st = self.streams[i]
+        return torch.cuda.stream(st) if st is not None else _Null()
+
     def step(self):
+        main = torch.cuda.current_stream() if self.streams[0] is not None else None
+        for st in self.streams:
+            if st is not None:
+                st.wait_stream(main)
         # Step 3 (R13) with the global CFL bound (C4)
         if self.dt_rule == 0:
-            cfl = torch.tensor([min(o.cfl(c, self.chi) for o, (_, c) in zip(self.octs, self.fields))],
-                               dtype=torch.float64, device=self.octs[0].device)
+            for i, (o, (_, c)) in enumerate(zip(self.octs, self.fields)):
+                o.cfl_async(c, self.chi, stream=self.streams[i])
+            cfl = min(o.cfl_result(self.chi, stream=self.streams[i]) for i, o in enumerate(self.octs))
+            cfl = torch.tensor([cfl], dtype=torch.float64, device=self.octs[0].device)
             cfl = float(_allreduce(cfl, dist.ReduceOp.MIN).item())
             dt = min(min(self.dt_prev, self.dt_cap), min(cfl, 0.5 * self.h * self.h))
         else:
             dt = self.dt_cap
         rebuilt = self.dt_bep is None or dt != self.dt_bep
         if rebuilt:                                                   # Step 2 / 4b
+            for st in self.streams:
+                if st is not None:
+                    st.synchronize()
             self.build(dt)
-        ys = [o.local_begin(rho, c, self.chi) for o, (rho, c) in zip(self.octs, self.fields)]
+            for st in self.streams:
+                if st is not None:
+                    st.wait_stream(main)
+        ys = [o.local_begin(rho, c, self.chi, stream=self.streams[i])
+              for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields))]
+        for st in self.streams:
+            if st is not None:
+                main.wait_stream(st)
         Cg = self._sum(ys)                                            # C2: global coefficients
-        stats = [o.local_finish(Cg, rho, c, self.clamp) for o, (rho, c) in zip(self.octs, self.fields)]
+        for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields)):
+            if self.streams[i] is not None:
+                self.streams[i].wait_stream(main)
+            o.local_finish_async(Cg, rho, c, self.clamp, stream=self.streams[i])
+        stats = [o.stats(stream=self.streams[i]) for i, o in enumerate(self.octs)]
+        for st in self.streams:
+            if st is not None:
+                main.wait_stream(st)
         self.dt_prev = dt
         self.t += dt
         mass = torch.tensor([sum(s["mass"] for s in stats)], dtype=torch.float64, device=self.octs[0].device)
@@ -87,3 +116,11 @@ class DDSolver:
             raise FloatingPointError("non-finite value in the DD PKS step")
         return {"t": self.t, "dt": dt, "rebuilt": rebuilt, "mass": mass,
                 "rho_max": max(s["rho_max"] for s in stats), "rho_min": min(s["rho_min"] for s in stats)}
+
+
+class _Null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False

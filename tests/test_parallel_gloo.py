@@ -106,14 +106,19 @@ class _FakeOctant:
         rho.fill_(1.0)
         c.fill_(float(self.s))
 
-    def cfl(self, c, chi=1.0):
+    def cfl_async(self, c, chi=1.0, stream=None):
+        pass
+
+    def cfl_result(self, chi=1.0, stream=None):
         return 1e-3 * (1 + self.s)
 
-    def local_begin(self, rho, c, chi=1.0):
+    def local_begin(self, rho, c, chi=1.0, stream=None):
         return self.y.clone()
 
-    def local_finish(self, C, rho, c, clamp=1):
+    def local_finish_async(self, C, rho, c, clamp=1, stream=None):
         self.seen["C"] = C.clone()
+
+    def stats(self, stream=None):
         return {"mass": 1.0, "rho_max": 1.0, "rho_min": 0.0, "c_min": 0.0, "nonfinite": 0.0}
 
 

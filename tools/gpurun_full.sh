@@ -7,7 +7,7 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; 
 tail -3 gpurun_out/smoke.log
 python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo bench_rc=$?
 cat gpurun_out/bench.log; tail -5 gpurun_out/bench.err
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"dst128|ztri" -c 40 --csv --log-file gpurun_out/launches.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"dst128|ztri|plane" -c 60 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-pks > gpurun_out/ncu_launch.log 2>&1; echo ncu_rc=$?
 ncu --set full --clock-control none --import-source on -k regex:"dst128f_kernel" -s 2 -c 2 -o gpurun_out/prof_full \
   python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-pks > gpurun_out/ncu_full.log 2>&1; echo ncu_full_rc=$?
