@@ -173,6 +173,37 @@ def bench_pks(api, torch, name, reps=3):
             "rebuilds": sum(l["rebuilt"] for l in logs), "final_mass": logs[-1]["mass"], "rho_max": logs[-1]["rho_max"]}
 
 
+def bench_cfg1(api, torch, reps=20):
+    """cfg1 latency: the 51-RHS AP batch (50 basis potentials + 1 particular), the
+    projection build (S2-S5) and the boundary LSQ (S8), N=16; median over reps, CUDA events."""
+    from dpm_inputs.rng import cfg1_particular_values
+    cfg = get_config("cfg1")
+    ctx = api.DPM.from_config(cfg)
+    n = cfg.n
+    mp = ctx.copy_set("mplus")
+    qp = np.zeros(n ** 3)
+    qp[mp] = cfg1_particular_values(len(mp))
+    E, _ = ctx.copy_extension()
+    q = torch.cat([ctx.potential_rhs(torch.from_numpy(np.ascontiguousarray(E.T)).cuda()),
+                   torch.from_numpy(qp.reshape(1, n, n, n)).cuda()])
+    u = torch.empty_like(q)
+    res = {}
+    for name, fn in (("aux_solve_batch_51_us", lambda: ctx.aux_solve_batch(q, u)),
+                     ("build_projection_us", lambda: ctx.build_projection(False)),
+                     ("boundary_lsq_us", lambda: ctx.boundary_lsq(ctx.trace(u[50:51], "gamma_in")))):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e3)
+        res[name] = statistics.median(ts)
+    return res
+
+
 def bench_dd(api, torch, world, rank, steps=None):
     """cfg5: the 8-octant DD (R24) — octants sharded over the ranks (8/world each), the global
     least squares and dt through NCCL all-reduces (DDSolver).  Steps/s excludes the BEP builds
@@ -301,8 +332,12 @@ def main():
         if tr and tr.get("points_per_launch"):
             traffic = tr["dram_bytes_per_launch"] * (k_pts / max(k_launch, 1)) / tr["points_per_launch"]
     kernel_names = {"x": "dst128f_kernel<0> (prime-factor DST-I along x, DFMA)",
-                    "y": "plane128_kernel (fused y-DST / z tridiagonal / inverse y-DST per x-mode plane, 2-CTA "
-                         "clusters)" if pt["z"][1] == 0 else "dst128f_kernel<1> (prime-factor DST-I along y, DFMA)",
+                    "y": ("plane128_kernel (fused y-DST / z tridiagonal / inverse y-DST per x-mode plane, 2-CTA "
+                          "clusters)" if os.environ.get("DPM_PLANE_FACR") == "0" else
+                          "plane128_facr_kernel (fused plane pass with one cyclic-reduction level along z: y-DST "
+                          "of the 64 odd z, reduced z tridiagonal, inverse y-DST, y tridiagonal solves for the "
+                          "even z; 2-CTA clusters)") if pt["z"][1] == 0
+                         else "dst128f_kernel<1> (prime-factor DST-I along y, DFMA)",
                     "z": "ztri_warp_kernel<128> (exact tridiagonal solve along z)"}
 
     line = {"metric": "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction); PKS time steps/sec",
@@ -360,6 +395,7 @@ def main():
         del q, u
         torch.cuda.empty_cache()
         line["pks"] = {"cfg2": bench_pks(api, torch, "cfg2"), "cfg3": bench_pks(api, torch, "cfg3")}
+        line["cfg1"] = bench_cfg1(api, torch)
 
     if not args.no_dd and 8 % world == 0:
         try:

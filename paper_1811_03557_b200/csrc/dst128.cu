@@ -528,15 +528,28 @@ __device__ __forceinline__ void contract_regs(const double (&pin)[22], const dou
   for (int q = 0; q < KB; ++q) emit(std::integral_constant<int, K0>{}, q, P[q], Q[q], R[q]);
 }
 
-// In-place DST-I along the rows (y) of this CTA's 64 columns.
+// In-place DST-I along the rows (y) of this CTA's 64 columns (KEPT = false: thread = (column, CRT
+// half)), or of the 32 kept columns 0..31 only (KEPT = true, FACR(1) below: thread = (column, CRT
+// half, k3 group); the two k3 groups split the contraction 11/11).
+// (KEPT: one out-of-line copy shared by the forward and inverse transforms keeps the FACR kernel's
+// code within the instruction cache.)
+#ifndef PLANE_YDST_INLINE
+#define PLANE_YDST_INLINE 0
+#endif
+template <bool KEPT>
+__device__ __noinline__ void plane_ydst_call(double* P);
+template <bool KEPT>
 __device__ __forceinline__ void plane_ydst(double* P) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool hi = lane >= 16;
-  const int col = (threadIdx.x >> 5) * 16 + (lane & 15);
+  const int col = KEPT ? (warp & 1) * 16 + (lane & 15) : warp * 16 + (lane & 15);
   double* colp = P + col;
   double pin[22], qin[22], wp[22];
   prep_regs(colp, hi, pin, qin, wp, std::make_integer_sequence<int, 21>{});
-  __syncwarp();   // both halves of every column have read their inputs: outputs may overwrite it
+  if (KEPT)
+    __syncthreads();   // all four threads of every column have read their inputs
+  else
+    __syncwarp();      // both halves of every column have read their inputs: outputs may overwrite it
   const double sm1 = hi ? -1.0 : 1.0;
   auto bfly = [&](auto k0c, int q, double Pv, double Qv, double Rv) {
     const int k3 = decltype(k0c)::value + q;
@@ -558,6 +571,18 @@ __device__ __forceinline__ void plane_ydst(double* P) {
       }
     }
   };
+  if (KEPT) {
+    if (warp >> 1) {
+      contract_regs<11, 6>(pin, qin, wp, bfly);
+      __syncwarp();
+      contract_regs<17, 5>(pin, qin, wp, bfly);
+    } else {
+      contract_regs<0, 6>(pin, qin, wp, bfly);
+      __syncwarp();
+      contract_regs<6, 5>(pin, qin, wp, bfly);
+    }
+    return;
+  }
 #if PLANE_KB == 8
   contract_regs<0, 8>(pin, qin, wp, bfly);
   __syncwarp();
@@ -590,6 +615,11 @@ __device__ __forceinline__ void plane_ydst(double* P) {
 #endif
 }
 
+template <bool KEPT>
+__device__ __noinline__ void plane_ydst_call(double* P) {
+  plane_ydst<KEPT>(P);
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHR, 2)
 plane128_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double inv_dt, double h2, double rscale) {
   namespace cg = cooperative_groups;
@@ -616,7 +646,7 @@ plane128_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double
     asm volatile("cp.async.wait_group 0;\n" ::);
   }
   __syncthreads();
-  plane_ydst(P);
+  plane_ydst<false>(P);
   __syncthreads();
   // z tridiagonal per y-mode row b = threadIdx.x, on this CTA's half (local k = 0..63)
   {
@@ -659,28 +689,287 @@ plane128_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double
     const double w = (rank == 0 ? v64 : v63) / den;
     // final: v_k = μ z_k - c2 (μ^{k+1} - μ^{2M+1-k}) + w (g1_k - g2_k) with the homogeneous response
     //   left  g_L[k] den = μ^{M-k} - μ^{M+k+2},   right g_R[k] den = μ^{k+1} - μ^{2M+1-k}
-    // (the right response is the same power pair as the Sherman–Morrison term)
+    // (the right response is the same power pair as the Sherman–Morrison term).  Every running
+    // power whose term matters is walked in the direction in which it shrinks (pa, and the right
+    // response, ascending; the left response descending), so an underflowed start (μ^M < 1e-308
+    // at tiny dt) can only drop terms that are themselves below 1e-150 of the solution.
     const double imu = 1.0 / mu;
+    const double A = rank == 0 ? -c2 : w - c2;             // coefficient of (μ^{k+1} - μ^{2M+1-k})
     double pa = mu, pb = mu2M1;                            // μ^{k+1}, μ^{2M+1-k}
-    double ga = rank == 0 ? muM : mu;                      // left: μ^{M-k};   right: μ^{k+1}
-    double gb = rank == 0 ? muM * mu * mu : mu2M1;         // left: μ^{M+k+2}; right: μ^{2M+1-k}
-    const double fa = rank == 0 ? imu : mu, fb = rank == 0 ? mu : imu;
     for (int k = 0; k < M; ++k) {
-      row[k] = fma(mu, row[k], fma(w, ga - gb, -c2 * (pa - pb)));
+      row[k] = fma(mu, row[k], A * (pa - pb));
       pa *= mu;
       pb *= imu;
-      ga *= fa;
-      gb *= fb;
+    }
+    if (rank == 0) {
+      double ga = mu, gb = mu2M1;                          // μ^{M-k}, μ^{M+k+2} at k = M-1
+      for (int k = M - 1; k >= 0; --k) {
+        row[k] = fma(w, ga - gb, row[k]);
+        ga *= mu;
+        gb *= imu;
+      }
     }
   }
   __syncthreads();
-  plane_ydst(P);
+  plane_ydst<false>(P);
   __syncthreads();
   for (int e = threadIdx.x; e < N * PHC; e += PTHR) {
     const int r = e >> 6, c = e & 63;
     __stcg(gp + (size_t)r * N + c, P[r * PPITCH + c]);
   }
   // (all DSMEM writes into this CTA completed before the cluster barrier above)
+}
+
+// ---------------------------------------------------------------------------------------------
+// FACR(1) plane pass ("plane pass, FACR(1)"): the same per-plane problem
+//   T_y v_z - v_{z-1} - v_{z+1} = g_z,   T_y = tridiag(-1, β, -1) along y,  β = 4 + h²(1/dt + λ_a),
+// with one level of cyclic reduction along z before the transform.  Adding T_y·(row z) to rows z±1
+// for odd z (0-based) eliminates the even z and leaves, for the 64 odd ("kept") z,
+//   -v_{z-2} + (T_y² - 2) v_z - v_{z+2} = T_y g_z + g_{z-1} + g_{z+1}      (z = 127: T_y² - 1)
+// which the y DST-I diagonalises with eigenvalues τ_b² - 2, τ_b = 2 + h²(1/dt + λ_a + λ_b).  The
+// y transforms thus run on 32 columns per CTA instead of 64; the even z are recovered afterwards
+// from  T_y v_z = g_z + v_{z-1} + v_{z+1}  (constant-coefficient tridiagonal solves along y).
+// Phases per CTA (rank r holds z in [64r, 64r+64); smem columns 0..31 = kept z (odd), 32..63 =
+// eliminated z (even), column 64 = the neighbour column):
+//   (1) reduced right-hand side on the kept columns (rank 0 also loads z = 64 from global memory),
+//   (2) y DST-I of the 32 kept columns (one out-of-line copy of the transform, 4 threads/column),
+//   (3) reduced tridiagonal per y-mode row, in registers (32 unknowns per CTA, split exactly as in
+//       plane128_kernel; the last row of rank 1 carries the extra +1 by Sherman–Morrison),
+//   (4) inverse y DST-I of the kept columns; rank 0 pushes v(z = 63) into rank 1's column 64,
+//   (5) eliminated columns: y tridiagonal solves in registers, 4 lanes per column over row
+//       segments [0,33) [33,64) [64,97) [97,128), forward/backward carries by warp shuffles.
+// Measured (profiles/r01/ncu_plane128_facr_full.txt): 0.77 ms per 64 fields vs 0.86 ms for
+// plane128_kernel; 30% fewer instructions, DFMA count -40%.
+// Running powers of μ are only walked in the direction in which they shrink when their term is
+// not negligible (see plane128_kernel).
+__device__ __forceinline__ double ipow128(double b, int e) {   // b^e, 0 <= e < 512
+  double r = 1.0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) {
+    if ((e >> q) & 1) r *= b;
+    b *= b;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHR, 2)
+plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double inv_dt, double h2,
+                     double gs) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double psm[];
+  // P[row y][col]: kept z = 2i+1 (local) at col i (0..31), eliminated z = 2j at col 32 + j, col 64:
+  // the neighbour column (phase 1: z = 64 for rank 0 / ghost z = 128 for rank 1; phase 5: v at
+  // z = 63 for rank 1 / ghost z = -1 for rank 0).  Consecutive lanes touch consecutive columns in
+  // every phase (bank-conflict free with the odd pitch).
+  double* P = psm;
+  double* lam = psm + N * PPITCH;            // [128]
+  double* xch = lam + N;                     // [128] interface value received from the partner
+  const int rank = (int)cluster.block_rank();
+  const long plane = blockIdx.x >> 1;        // field * 128 + a
+  const int a = (int)(plane & (N - 1));
+  double* gp = u + (size_t)plane * NN + (size_t)rank * PHC;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int i = t; i < N; i += PTHR) lam[i] = lam_g[i];
+  {
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(P);
+#pragma unroll 16
+    for (int e = t; e < N * PHC; e += PTHR) {
+      // a warp covers 32 consecutive z of one row: lanes 0-15 the odd z (kept columns), lanes
+      // 16-31 the even z (eliminated columns), so each half-warp hits 16 distinct bank pairs
+      const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
+      const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (unsigned)(r * PPITCH + c)),
+                   "l"(gp + (size_t)r * N + z));
+    }
+    if (rank == 0)   // z = 64 (the partner's first column; an L2 hit, the partner reads it too)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (unsigned)(t * PPITCH + PHC)),
+                   "l"(gp + (size_t)t * N + PHC));
+    else
+      P[t * PPITCH + PHC] = 0.0;
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+  }
+  __syncthreads();
+  const double hsa = h2 * (inv_dt + lam[a]);
+  const double beta = 4.0 + hsa;
+  // (1) r_i = gs (β g_z[y] - g_z[y-1] - g_z[y+1] + g_{z-1}[y] + g_{z+1}[y]),  z = 2i + 1,  i = lane
+  {
+    const int y0 = 32 * warp;
+    const double* gk = P + lane;             // kept column i
+    const double* gl = P + 32 + lane;        // eliminated j = i   (z - 1)
+    const double* gr = P + 33 + lane;        // eliminated j = i+1 (z + 1; col 64 for i = 31)
+    double rr[32];
+    double prev = y0 > 0 ? gk[(y0 - 1) * PPITCH] : 0.0, cur = gk[y0 * PPITCH];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int y = y0 + j;
+      const double nxt = y + 1 < N ? gk[(y + 1) * PPITCH] : 0.0;
+      rr[j] = gs * (fma(beta, cur, -(prev + nxt)) + (gl[y * PPITCH] + gr[y * PPITCH]));
+      prev = cur;
+      cur = nxt;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) P[(y0 + j) * PPITCH + lane] = rr[j];
+    if (rank == 0) P[t * PPITCH + PHC] = 0.0;   // ghost z = -1 for phase 5
+  }
+  __syncthreads();
+#if PLANE_YDST_INLINE
+  plane_ydst<true>(P);
+#else
+  plane_ydst_call<true>(P);
+#endif
+  __syncthreads();
+  // (3) reduced system per y-mode row b: -u_{i-1} + d u_i - u_{i+1} = ys r̂_i over the 64 kept z,
+  //     d = τ² - 2 = μ + 1/μ with μ = μ_τ², last global row d + 1.
+  {
+    const int b = t;
+    double* row = P + b * PPITCH;            // kept entry i at row[i]
+    constexpr int M = PHC / 2;
+    constexpr double ys = 2.0 / (N + 1);
+    const double hs = h2 * ((inv_dt + lam[a]) + lam[b]);
+    const double mut = 2.0 / ((2.0 + hs) + sqrt(hs * (hs + 4.0)));
+    const double mu = mut * mut;
+    double v[M];                                           // the row, in registers until the end
+#pragma unroll
+    for (int i = 0; i < M; ++i) v[i] = ys * row[i];
+#pragma unroll
+    for (int i = 1; i < M; ++i) v[i] = fma(mu, v[i - 1], v[i]);
+#pragma unroll
+    for (int i = M - 2; i >= 0; --i) v[i] = fma(mu, v[i + 1], v[i]);
+    double muM = mu;                                       // μ^M, M = 32
+#pragma unroll
+    for (int q = 0; q < 5; ++q) muM *= muM;
+    const double mu2 = mu * mu;
+    const double mu2M1 = muM * muM * mu;                   // μ^{2M+1}
+    const double den = 1.0 - mu2M1 * mu;                   // 1 - μ^{2M+2}
+    const double c2 = mu2 * v[0] / den;
+    const double a31 = fma(mu, v[M - 1], -c2 * (muM - muM * mu2));     // local Dirichlet x_{M-1}
+    const double a0 = fma(mu, v[0], -c2 * (mu - mu2M1));              // local Dirichlet x_0
+    const double gL0 = muM * (1.0 - mu2) / den;            // g_L[0]   (g_L = T^{-1} e_{M-1})
+    const double gam0 = mu * (1.0 - muM * muM) / den;      // g_L[M-1] = g_R[0]
+    const double sm = 1.0 / (1.0 + gam0);
+    const double mine = rank == 0 ? a31 : a0 - gL0 * a31 * sm;   // rank 1: last row +1 (Sherman–Morrison)
+    cluster.map_shared_rank(xch, rank ^ 1)[b] = mine;
+    cluster.sync();
+    const double other = xch[b];
+    const double x31 = rank == 0 ? mine : other, x32 = rank == 0 ? other : mine;
+    const double gam1 = gam0 - gL0 * gL0 * sm;             // right half's response at its first entry
+    const double u31 = (x31 + x32 * gam0) / (1.0 - gam0 * gam1);
+    const double u32 = x32 + u31 * gam1;
+    // u_i = μ z_i + A (μ^{i+1} - μ^{2M+1-i}) + B (μ^{M-i} - μ^{M+i+2})
+    const double A = rank == 0 ? -c2 : u31 / den - c2;
+    const double B = rank == 0 ? u32 / den : -(a31 + u31 * gL0) * sm / den;
+    const double imu = 1.0 / mu;
+    double pa = mu, pb = mu2M1;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      v[i] = fma(mu, v[i], A * (pa - pb));
+      pa *= mu;
+      pb *= imu;
+    }
+    double ga = mu, gb = mu2M1;                            // at i = M-1
+#pragma unroll
+    for (int i = M - 1; i >= 0; --i) {
+      row[i] = fma(B, ga - gb, v[i]);
+      ga *= mu;
+      gb *= imu;
+    }
+  }
+  __syncthreads();
+#if PLANE_YDST_INLINE
+  plane_ydst<true>(P);
+#else
+  plane_ydst_call<true>(P);
+#endif
+  __syncthreads();
+  // rank 0 pushes v(z = 63) into rank 1's neighbour column (rank 1 finished reading its ghost
+  // column in phase 1 before the interface barrier above); rank 1 waits for it, rank 0 only
+  // before exiting.
+  if (rank == 0) cluster.map_shared_rank(P, 1)[t * PPITCH + PHC] = P[t * PPITCH + 31];
+  cluster_arrive();
+  if (rank == 1) cluster_wait();
+  // (5) eliminated column j = 16 (warp/2) + 2 (lane%8) + warp%2, row segment s = lane/8:
+  //     [0,33) [33,64) [64,97) [97,128); a half-warp holds 8 columns of one parity x 2 segments
+  //     whose start rows are ≡ 0, 1 mod 16: 16 distinct 8-byte bank pairs
+  {
+    const int j = 16 * (warp >> 1) + 2 * (lane & 7) + (warp & 1), s = lane >> 3;
+    const int kb = (s >> 1) * 64 + (s & 1) * 33, L = (s & 1) ? 31 : 33, ke = kb + L;
+    const double muy = 2.0 / (beta + sqrt((beta - 2.0) * (beta + 2.0)));
+    const double imu = 1.0 / muy, mu2 = muy * muy;
+    double* col = P + kb * PPITCH + 32 + j;
+    const double* vl = P + kb * PPITCH + (j == 0 ? PHC : j - 1);   // v at z - 1
+    const double* vr = P + kb * PPITCH + j;                        // v at z + 1
+    // the segment stays in registers (x[q], q < L <= 33) from the first load to the final store
+    // S1: local forward sweep ŷ_k = r_k + μ ŷ_{k-1},  r = gs g + v_{z-1} + v_{z+1}
+    double x[33];
+#pragma unroll
+    for (int q = 0; q < 33; ++q)
+      x[q] = q < L ? fma(gs, col[q * PPITCH], vl[q * PPITCH] + vr[q * PPITCH]) : 0.0;
+#pragma unroll
+    for (int q = 1; q < 33; ++q) x[q] = fma(muy, x[q - 1], x[q]);
+    const double yv = (s & 1) ? x[30] : x[32];
+    const int base = lane & 7;
+    const double mu33 = ipow128(muy, 33), mu31 = ipow128(muy, 31);
+    const double Y0 = __shfl_sync(0xffffffffu, yv, base), Y1 = __shfl_sync(0xffffffffu, yv, base + 8),
+                 Y2 = __shfl_sync(0xffffffffu, yv, base + 16);
+    // incoming true y_{kb-1}: segment lengths 33, 31, 33
+    const double c1 = Y0, c2f = fma(mu31, c1, Y1), c3 = fma(mu33, c2f, Y2);
+    const double cin = s == 0 ? 0.0 : s == 1 ? c1 : s == 2 ? c2f : c3;
+    // S2: local backward sweep ẑ_k = ŷ_k + μ ẑ_{k+1} (entries q >= L are zero, and stay so)
+    if (s & 1) {
+      x[31] = x[32] = 0.0;
+    }
+#pragma unroll
+    for (int q = 31; q >= 0; --q) x[q] = fma(muy, x[q + 1], x[q]);
+    // true z_k = ẑ_k + cin ζ_k + μ^{ke-k} Zr,  ζ_k = (μ^{k-kb+1} - μ^{2ke-kb+1-k}) / (1 - μ²)
+    const double i1m = 1.0 / (1.0 - mu2);
+    const double muL = s & 1 ? mu31 : mu33;
+    const double tb = fma(cin, muy * (1.0 - muL * muL) * i1m, x[0]);   // ẑ_kb + cin ζ_kb
+    const double T0 = __shfl_sync(0xffffffffu, tb, base), T1 = __shfl_sync(0xffffffffu, tb, base + 8),
+                 T2 = __shfl_sync(0xffffffffu, tb, base + 16), T3 = __shfl_sync(0xffffffffu, tb, base + 24);
+    const double Z3 = T3, Z2 = fma(mu33, Z3, T2), Z1 = fma(mu31, Z2, T1), Z0 = fma(mu33, Z1, T0);
+    const double Zr = s == 0 ? Z1 : s == 1 ? Z2 : s == 2 ? Z3 : 0.0;   // true z at ke
+    // S3 (ascending): w_k = μ (ẑ_k + cin ζ_k) - c2 (μ^{k+1} - μ^{2n+1-k}),  c2 = μ² z_0 / (1 - μ^{2n+2})
+    const double c2 = mu2 * Z0 / (1.0 - ipow128(muy, 2 * N + 2));
+    const double ci = cin * i1m;
+    double p1 = muy, p2 = ipow128(muy, 2 * L + 1);                // μ^{k-kb+1}, μ^{2ke-kb+1-k}
+    double pa = ipow128(muy, kb + 1), pb = ipow128(muy, 2 * N + 1 - kb);
+#pragma unroll
+    for (int q = 0; q < 33; ++q) {
+      x[q] = fma(muy, fma(ci, p1 - p2, x[q]), -c2 * (pa - pb));
+      p1 *= muy;
+      p2 *= imu;
+      pa *= muy;
+      pb *= imu;
+    }
+    // S4 (descending): + μ^{ke-k+1} Zr, then the single store of the segment
+    double pr = mu2 * Zr;                                          // Zr = 0 for the last segment
+    if (s & 1) {
+#pragma unroll
+      for (int q = 30; q >= 0; --q) {
+        col[q * PPITCH] = x[q] + pr;
+        pr *= muy;
+      }
+    } else {
+#pragma unroll
+      for (int q = 32; q >= 0; --q) {
+        col[q * PPITCH] = x[q] + pr;
+        pr *= muy;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = t; e < N * PHC; e += PTHR) {   // same lane -> (column, z) map as the load
+    const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
+    const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
+    __stcg(gp + (size_t)r * N + z, P[r * PPITCH + c]);
+  }
+  if (rank == 0) cluster_wait();
 }
 
 unsigned long long g_tables_ready = 0;   // bit d: constant tables uploaded on device d
@@ -763,14 +1052,22 @@ cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, co
 }
 
 // Fused y-DST / z-tridiagonal / inverse y-DST over nfields n = 128 fields (in place), after the x pass.
+// xscale = 2/(n+1) (x transform pair) and rscale = xscale² h²; DPM_PLANE_FACR=0 selects the
+// full-transform plane kernel instead of FACR(1).
 cudaError_t plane128_pass(double* u, int nfields, const double* lam, double inv_dt, double h2, double rscale,
                           cudaStream_t s) {
+  static const bool facr = [] {
+    const char* v = getenv("DPM_PLANE_FACR");
+    return !(v && atoi(v) == 0);
+  }();
+  auto k = facr ? plane128_facr_kernel : plane128_kernel;
+  const double arg = facr ? rscale * (N + 1) / 2.0 : rscale;   // FACR: x normalisation · h² only
   const size_t smem = ((size_t)N * PPITCH + 2 * N) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(plane128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long ctas = 2L * nfields * N;
   if (ctas > 2147483647L) return cudaErrorInvalidValue;
   DPM_COUNT_LAUNCH(1);
-  plane128_kernel<<<(unsigned)ctas, PTHR, smem, s>>>(u, lam, inv_dt, h2, rscale);
+  k<<<(unsigned)ctas, PTHR, smem, s>>>(u, lam, inv_dt, h2, arg);
   return cudaGetLastError();
 }

@@ -50,10 +50,11 @@ def test_aux_solve_parity(api, n, solver):
 
 
 @pytest.mark.parametrize("solver", ["dst3", "dst2_tridiag"])
-@pytest.mark.parametrize("n,dt", [(128, 1.0), (128, 0.5 * (2.2 / 129) ** 2), (128, 1e-8), (33, 10.0),
-                                  (64, 0.5 * (2.2 / 65) ** 2)])
+@pytest.mark.parametrize("n,dt", [(128, 1.0), (128, 0.5 * (2.2 / 129) ** 2), (128, 1e-8), (128, 1e-11),
+                                  (128, 1e-14), (33, 10.0), (64, 0.5 * (2.2 / 65) ** 2)])
 def test_aux_solve_parity_large_dt(api, n, dt, solver):
-    # large dt: the z operator approaches the pure Laplacian (μ -> 1 in the tridiagonal solver)
+    # large dt: the z operator approaches the pure Laplacian (μ -> 1 in the tridiagonal solver);
+    # tiny dt: μ^M underflows (1e-11, 1e-14 at n = 128), which the running powers must survive
     c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
     c.set_solver(solver)
     q = random_boxes(7 + n, 1, n)
@@ -71,6 +72,32 @@ def test_aux_solve_128_batch_chunked_inplace(api):
     c.aux_solve_batch(t, t)
     uo = ap.solve(q, c.info["h"], dt)
     assert rel(t.cpu().numpy(), uo) <= 1e-11
+
+
+@pytest.mark.parametrize("facr", ["0", "1"])
+def test_aux_solve_128_plane_kernels(facr, tmp_path):
+    # both fused plane kernels (full y transform / FACR(1), DPM_PLANE_FACR) against the oracle in a
+    # fresh process (the selector is read once per process), at a mid, a large and a tiny dt
+    import subprocess, sys, os, textwrap
+    code = textwrap.dedent('''
+        import numpy as np, torch
+        from paper_1811_03557_b200 import api
+        from dpm_inputs.rng import random_boxes
+        from oracle import ap
+        for dt in (2e-4, 1.0, 1e-12):
+            c = api.DPM(128, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+            q = random_boxes(5, 2, 128)
+            u = c.aux_solve_batch(torch.from_numpy(q).cuda()).cpu().numpy()
+            uo = ap.solve(q, c.info["h"], dt)
+            e = float(np.abs(u - uo).max() / np.abs(uo).max())
+            assert e <= 1e-11, (dt, e)
+        print("ok")
+    ''')
+    env = dict(os.environ, DPM_PLANE_FACR=facr)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
 def test_aux_solve_inplace_chunked_and_empty(api):
