@@ -204,6 +204,30 @@ def bench_cfg1(api, torch, reps=20):
     return res
 
 
+def bench_bep(api, torch, reps=3):
+    """NEXT-1: the Step-4b rebuild at the cfg4 geometry (K = 578 BEP columns, N=128):
+    dpm_bep_columns over all K (sparse-in / gamma-out fused path unless DPM_BEP_FUSED=0) and the
+    whole dpm_build_projection (columns + CholeskyQR2 factorisation); median of reps, CUDA events."""
+    cfg = get_config("cfg4")
+    ctx = api.DPM.from_config(cfg)
+    K = ctx.K
+    res = {"K": K, "fused": os.environ.get("DPM_BEP_FUSED") != "0"}
+    for name, fn in (("columns_ms", lambda: ctx.bep_columns(0, K)),
+                     ("rebuild_ms", lambda: ctx.build_projection(False))):
+        fn()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[name] = statistics.median(ts)
+    res["columns_per_s"] = K / (res["columns_ms"] / 1e3)
+    return res
+
+
 def bench_dd(api, torch, world, rank, steps=None):
     """cfg5: the 8-octant DD (R24) — octants sharded over the ranks (8/world each), the global
     least squares and dt through NCCL all-reduces (DDSolver).  Steps/s excludes the BEP builds
@@ -396,6 +420,7 @@ def main():
         torch.cuda.empty_cache()
         line["pks"] = {"cfg2": bench_pks(api, torch, "cfg2"), "cfg3": bench_pks(api, torch, "cfg3")}
         line["cfg1"] = bench_cfg1(api, torch)
+        line["bep_rebuild_cfg4"] = bench_bep(api, torch)
 
     if not args.no_dd and 8 % world == 0:
         try:

@@ -23,6 +23,7 @@ void free_ctx(dpm_ctx* c) {
   for (auto* l : c->lists)
     if (l) cudaFree(l);
   if (c->red_host) cudaFreeHost(c->red_host);
+  bep_fused_free(c);
   dst_plan_free(c->plan);
   if (c->setup_stream) cudaStreamDestroy(c->setup_stream);
   if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
@@ -259,8 +260,14 @@ dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, do
   dpm_status st = ensure_work(ctx, std::min(ch, c1 - c0));
   if (st != DPM_OK) return st;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  const bool fused = bep_fused_enabled(ctx);
   for (int a = c0; a < c1; a += ch) {
     const int nc = std::min(ch, c1 - a);
+    if (fused) {   // sparse-in / γ-out (bep_fused.cu)
+      DPM_CUDA_TRY(ctx, bep_columns_fused(ctx, a, nc, PgE ? PgE + (size_t)(a - c0) * ng : nullptr,
+                                          B ? B + (size_t)(a - c0) * ngin : nullptr, s));
+      continue;
+    }
     DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, nc, s));
     DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, nc, nullptr, 0, s));
     DPM_CUDA_TRY(ctx, launch_bep_gather(ctx, ctx->work, a, nc, PgE ? PgE + (size_t)(a - c0) * ng : nullptr,

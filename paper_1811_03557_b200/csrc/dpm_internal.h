@@ -122,6 +122,11 @@ struct dpm_ctx {
   double* dd_D = nullptr;           // [K] global column scaling
   double* dd_g = nullptr;           // [2][n_rows] per-step BEP right-hand sides
   double* dd_ug = nullptr;          // [2][n_gamma] u_γ = A C
+  // fused BEP column build at n = 128 (bep_fused.cu)
+  uint32_t* bepf_btab = nullptr;     // [n^2][8] band x-line table (mask, start); built on first use
+  int32_t* bepf_bpos = nullptr;      // [n_band] line-major position of band point b
+  double* bepf_qb = nullptr;         // [cols][n_band] band values of the potential RHS (line-major)
+  int bepf_cols = 0;
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -150,6 +155,8 @@ void dst_plan_free(DstPlan& p);
 cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_t batch, double* scratch,
                             size_t scratch_bytes, cudaStream_t s);
 size_t dst_scratch_bytes(int n, int chunk);
+// the passes between the two x transforms (partial diagonalisation only), in place on x-transformed fields
+cudaError_t dst_solve_middle(const DstPlan& p, double* u, int64_t batch, cudaStream_t s);
 
 // dst128.cu (n = 128 prime-factor DST-I passes)
 cudaError_t dst128_init();
@@ -157,6 +164,10 @@ cudaError_t dst128_atab(double** tab);
 cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, const double* atab, cudaStream_t s);
 cudaError_t plane128_pass(double* u, int nfields, const double* lam, double inv_dt, double h2, double rscale,
                           cudaStream_t s);
+// forward x pass of the fused BEP build (bep_fused.cu) from x-line-major band values vals[f*ldv + .]
+// through the band line table tab ([n^2][8] u32: 128-bit x mask, start)
+cudaError_t dst128_xpass_sparse(double* out, int nfields, const uint32_t* tab, const double* vals, int64_t ldv,
+                                cudaStream_t s);
 
 // setup.cu
 dpm_status setup_point_sets(dpm_ctx* ctx);
@@ -165,6 +176,8 @@ dpm_status setup_geometry(dpm_ctx* ctx);
 // ops.cu
 cudaError_t launch_potential_rhs(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
                                  cudaStream_t s);
+cudaError_t launch_potential_band(const dpm_ctx* ctx, const double* v, int64_t ldv, double* qb, int nrhs,
+                                  const int32_t* pos, cudaStream_t s);
 cudaError_t launch_trace(const dpm_ctx* ctx, const double* u, double* out, int which, int64_t batch,
                          cudaStream_t s);
 cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int ncols, double* PgE,
@@ -178,7 +191,6 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
 // lsq.cu building blocks (octant DD)
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s);
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s);
-cudaError_t lsq_trsm_rows(double* A, int64_t m, int K, const double* R, cudaStream_t s);
 cudaError_t lsq_trmm(const double* A, const double* B, double* C, int K, cudaStream_t s);
 cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, double* Ri_ws, double* out,
                          cudaStream_t s);   // out = A R^{-1} (R upper K x K)
@@ -207,3 +219,8 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
                                   cudaStream_t s);
 cudaError_t launch_dt_rule(dpm_ctx* ctx, const double* red3, double chi, double dt_prev, double cap, double* dt_out,
                            cudaStream_t s);
+
+// bep_fused.cu (sparse-in / gamma-out BEP columns)
+bool bep_fused_enabled(const dpm_ctx* ctx);
+cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double* B, cudaStream_t s);
+void bep_fused_free(dpm_ctx* c);

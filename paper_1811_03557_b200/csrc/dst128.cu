@@ -390,9 +390,56 @@ __device__ __forceinline__ void contract_block(const double* inpq, const double*
 // lanes 0-15: half j1 = 0 of columns 0..15; lanes 16-31: half j1 = 1 of the same columns.  The final
 // 2-point stage X_k = T0 ± T1 pairs lane l with l ^ 16 (one shuffle per operand): lane l writes the
 // k1 = 0 outputs, lane l + 16 the k1 = 1 outputs.  14 warps per SM, 16 KB of IN per warp.
-template <int PASS, int MINB>
+// MODE 0: dense in / dense out.  MODE 1 (sparse in; the fused BEP build, bep_fused.cu, forward x
+// pass): the tile is gathered from the compact band values of the field, stored x-line-major: per
+// x-line L (= a column of the x pass) a 32-byte entry tab[L] = {128-bit mask of the x positions
+// holding band points, start of the line's values}.  The tile is zeroed and only the set rows are
+// copied (cp.async, issued for the next tile under the contraction): no zero-filled box is read.
+// (A γ-out variant of the inverse pass, writing only the γ outputs through the γ line table, was
+// measured slower than the dense inverse pass + gather: the per-output slot arithmetic adds ~40%
+// instructions to this instruction-bound kernel.)
+struct LineEntry {
+  uint32_t m[4];
+  int32_t start;
+};
+
+__device__ __forceinline__ LineEntry load_line(const uint32_t* __restrict__ tab, int line) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(tab) + 2 * (size_t)line);
+  const int32_t st = __ldg(reinterpret_cast<const int32_t*>(tab) + 8 * (size_t)line + 4);
+  return LineEntry{{a.x, a.y, a.z, a.w}, st};
+}
+
+// zero the tile, then cp.async (8-byte) only the band values of the lane's line into their rows;
+// the two lanes of a column take alternate set bits.  Issued for the next tile under the contraction.
+template <int PASS>
+__device__ __forceinline__ void load_raw_lines(double* raw, const uint32_t* __restrict__ tab,
+                                               const double* __restrict__ vals, int c0, int lane) {
+  const int cc = lane & 15, h = lane >> 4;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)   // 128 x 16 doubles: 4 per lane per 16-byte store
+    *reinterpret_cast<double4*>(raw + (i * 32 + lane) * 4) = make_double4(0.0, 0.0, 0.0, 0.0);
+  __syncwarp();
+  const LineEntry e = load_line(tab, c0 + cc);
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(raw);
+  int slot = e.start;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t m = e.m[w];
+    for (int k = 0; m; ++k) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      if ((k & 1) == h)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (unsigned)((32 * w + b) * 16 + cc)),
+                     "l"(vals + slot + k));
+    }
+    slot += __popc(e.m[w]);
+  }
+}
+
+template <int PASS, int MINB, int MODE = 0>
 __global__ void __launch_bounds__(224, MINB)
-dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields) {
+dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields,
+               const uint32_t* __restrict__ tab = nullptr, const double* vals = nullptr, int64_t ldv = 0) {
   extern __shared__ __align__(16) double wsm[];   // [warp][IN 16 KB | RAW 16 KB]
   const int lane = threadIdx.x & 31;
   const bool hi = lane >= 16;
@@ -408,7 +455,10 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
   const size_t field = (size_t)NN * N;
   if (gw < ntiles) {
     const int f = gw / TPF;
-    load_raw<PASS>(raw, in + (size_t)f * field, (gw - f * TPF) * 16, lane);
+    if (MODE == 1)
+      load_raw_lines<PASS>(raw, tab, vals + (size_t)f * ldv, (gw - f * TPF) * 16, lane);
+    else
+      load_raw<PASS>(raw, in + (size_t)f * field, (gw - f * TPF) * 16, lane);
   }
   cp_async_commit();
   for (int t = gw; t < ntiles; t += nw) {
@@ -421,7 +471,10 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
     const int tn = t + nw;
     if (tn < ntiles) {
       const int fn = tn / TPF;
-      load_raw<PASS>(raw, in + (size_t)fn * field, (tn - fn * TPF) * 16, lane);
+      if (MODE == 1)
+        load_raw_lines<PASS>(raw, tab, vals + (size_t)fn * ldv, (tn - fn * TPF) * 16, lane);
+      else
+        load_raw<PASS>(raw, in + (size_t)fn * field, (tn - fn * TPF) * 16, lane);
     }
     cp_async_commit();
     auto bfly = [&](auto k0c, int q, double P, double Q, double R) {
@@ -1077,7 +1130,7 @@ cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, co
     const long warps = (long)nfields * (NN / 16);
     const int grid = (int)std::min<long>((warps + 6) / 7, (long)sms * std::max(1, occ));
     DPM_COUNT_LAUNCH(1);
-    kf<<<grid, 224, smem, s>>>(in, out, nfields);
+    kf<<<grid, 224, smem, s>>>(in, out, nfields, nullptr, nullptr, 0);
     return cudaGetLastError();
   }
   const size_t smem = 2 * (size_t)TILE * sizeof(double);
@@ -1090,6 +1143,28 @@ cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, co
   const int grid = (int)std::min<long>(ntiles, (long)sms * std::max(1, occ));
   DPM_COUNT_LAUNCH(1);
   k<<<grid, NTHR, smem, s>>>(in, out, nfields, atab);
+  return cudaGetLastError();
+}
+
+// forward x pass of the fused BEP build (MODE 1 above): same grid as the dense pass.
+cudaError_t dst128_xpass_sparse(double* out, int nfields, const uint32_t* tab, const double* vals, int64_t ldv,
+                                cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = 7 * (IN_SIZE + RAW_SIZE) * sizeof(double);
+  auto kf = dst128f_kernel<0, 1, 1>;
+  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, 224, smem);
+  const long warps = (long)nfields * (NN / 16);
+  const int grid = (int)std::min<long>((warps + 6) / 7, (long)sms * std::max(1, occ));
+  DPM_COUNT_LAUNCH(1);
+  kf<<<grid, 224, smem, s>>>(nullptr, out, nfields, tab, vals, ldv);
   return cudaGetLastError();
 }
 

@@ -634,6 +634,39 @@ cudaError_t timed(const DstPlan& p, int kind, long long points, cudaStream_t s, 
 }
 }  // namespace
 
+namespace {
+// The passes between the two x transforms of the partial-diagonalisation solver, in place on nf
+// x-transformed fields: the fused plane pass at n = 128, else y DST, z tridiagonal,
+// y DST.
+cudaError_t middle_passes(const DstPlan& p, double* ui, int nf, double inv_dt, double scale, cudaStream_t s) {
+  const int n = p.n;
+  const long long pts = (long long)nf * n * n * n;
+  if (n == 128 && p.pfa && p.plane) {
+    const double sc2 = 2.0 / (n + 1);
+    return timed(p, 1, pts, s, [&] { return plane128_pass(ui, nf, p.lam, inv_dt, p.h * p.h, sc2 * sc2 * p.h * p.h, s); });
+  }
+  auto pass = [&](int k) { return timed(p, k, pts, s, [&] { return run_pass(p, k, ui, ui, nf, inv_dt, scale, s); }); };
+  cudaError_t e;
+  if ((e = pass(1)) != cudaSuccess) return e;
+  if ((e = timed(p, 2, pts, s, [&] { return run_ztri(p, ui, nf, s); })) != cudaSuccess) return e;
+  return pass(1);
+}
+}  // namespace
+
+cudaError_t dst_solve_middle(const DstPlan& p, double* u, int64_t batch, cudaStream_t s) {
+  if (p.solver != DPM_SOLVER_DST2_TRIDIAG) return cudaErrorInvalidValue;
+  const int n = p.n;
+  const size_t fe = (size_t)n * n * n;
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(((size_t)1024 << 20) / (fe * 8)));
+  const double sc = 2.0 / (n + 1);
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int nf = (int)std::min<int64_t>(chunk, batch - b0);
+    cudaError_t e = middle_passes(p, u + b0 * fe, nf, 1.0 / p.dt, sc * sc * sc, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_t batch, double*, size_t,
                             cudaStream_t s) {
   const int n = p.n;
@@ -677,23 +710,13 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     const long long pts = (long long)nf * (long long)fe;
     auto pass = [&](int k, const double* in) { return timed(p, k, pts, s, [&] { return run_pass(p, k, in, ui, nf, inv_dt, scale, s); }); };
     if ((e = pass(0, qi)) != cudaSuccess) return e;
-    if (n == 128 && p.pfa && p.plane && p.solver == DPM_SOLVER_DST2_TRIDIAG) {
-      // fused y / z / y pass over the x-mode planes, then the inverse x pass
-      const double sc2 = 2.0 / (n + 1);
-      if ((e = timed(p, 1, pts, s, [&] {
-             return plane128_pass(ui, nf, p.lam, inv_dt, p.h * p.h, sc2 * sc2 * p.h * p.h, s);
-           })) != cudaSuccess)
-        return e;
-      if ((e = pass(0, ui)) != cudaSuccess) return e;
-      continue;
-    }
-    if ((e = pass(1, ui)) != cudaSuccess) return e;
     if (p.solver == DPM_SOLVER_DST2_TRIDIAG) {
-      if ((e = timed(p, 2, pts, s, [&] { return run_ztri(p, ui, nf, s); })) != cudaSuccess) return e;
-    } else if ((e = pass(2, ui)) != cudaSuccess) {
-      return e;
+      if ((e = middle_passes(p, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+    } else {
+      if ((e = pass(1, ui)) != cudaSuccess) return e;
+      if ((e = pass(2, ui)) != cudaSuccess) return e;
+      if ((e = pass(1, ui)) != cudaSuccess) return e;
     }
-    if ((e = pass(1, ui)) != cudaSuccess) return e;
     if ((e = pass(0, ui)) != cudaSuccess) return e;
   }
   if (two) {

@@ -37,37 +37,6 @@ __global__ void scale_cols_kernel(const double* __restrict__ B, int64_t m, int K
     A[t] = B[t] * scale[t / m];
 }
 
-// G = A^T A (K x K, col-major), tiled 32x32 over (i, j) with partial sums over row-chunks.
-// grid: (ceil(K/32), ceil(K/32), nsplit); atomics combine the row-chunks (G pre-zeroed).
-__global__ void gram_kernel(const double* __restrict__ A, int64_t m, int K, double* G, int64_t rows_per_split) {
-  const int bi = blockIdx.x * 32, bj = blockIdx.y * 32;
-  if (bj < bi) return;   // upper tiles only; mirrored at the end
-  const int64_t r0 = blockIdx.z * rows_per_split, r1 = min(m, r0 + rows_per_split);
-  __shared__ double sa[32][33], sb[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 256 threads: ty 0..7
-  double acc[4] = {0, 0, 0, 0};
-  for (int64_t r = r0; r < r1; r += 32) {
-    for (int q = ty; q < 32; q += 8) {
-      const int64_t row = r + tx;
-      sa[q][tx] = (row < r1 && bi + q < K) ? A[(size_t)(bi + q) * m + row] : 0.0;
-      sb[q][tx] = (row < r1 && bj + q < K) ? A[(size_t)(bj + q) * m + row] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      const double b = sb[tx][rr];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += sa[ty + 8 * u][rr] * b;
-    }
-    __syncthreads();
-  }
-  for (int u = 0; u < 4; ++u) {
-    const int i = bi + ty + 8 * u, j = bj + tx;
-    if (i < K && j < K && j >= i) atomicAdd(G + (size_t)j * K + i, acc[u]);
-  }
-}
-
-
 // Blocked right-looking Cholesky G = R^T R (upper R, column-major K x K, upper triangle used),
 // block size CB: (1) unblocked factor of the diagonal block in shared memory (one CTA),
 // (2) row-panel solve R_kk^T X = G_k,j for the columns right of the block (one thread per column),
@@ -146,17 +115,6 @@ __global__ void rinv_warp_kernel(const double* __restrict__ R, int K, double* __
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) x[i] = ((i == j ? 1.0 : 0.0) - v) / R[(size_t)i * K + i];
     __syncwarp();
-  }
-}
-
-// A <- A R^{-1} row by row: x^T R = a^T  (forward substitution over columns).
-__global__ void trsm_rows_kernel(double* A, int64_t m, int K, const double* __restrict__ R) {
-  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (row >= m) return;
-  for (int j = 0; j < K; ++j) {
-    double v = A[(size_t)j * m + row];
-    for (int i = 0; i < j; ++i) v -= A[(size_t)i * m + row] * R[(size_t)j * K + i];
-    A[(size_t)j * m + row] = v / R[(size_t)j * K + j];
   }
 }
 
@@ -277,19 +235,14 @@ __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, 
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s);
 namespace {
 
-dpm_status chol_qr_pass(dpm_ctx* ctx, double* A, int64_t m, int K, double* Rout, int* dfail, cudaStream_t s) {
-  DPM_CUDA_TRY(ctx, cudaMemsetAsync(Rout, 0, (size_t)K * K * sizeof(double), s));
-  const int tiles = (K + 31) / 32;
-  const int64_t target_split = std::max<int64_t>(1, (148 * 4) / ((int64_t)tiles * (tiles + 1) / 2));
-  const int64_t rps = std::max<int64_t>(32, ((m + target_split - 1) / target_split + 31) / 32 * 32);
-  const int nsplit = (int)((m + rps - 1) / rps);
-  DPM_COUNT_LAUNCH(1);
-  gram_kernel<<<dim3(tiles, tiles, nsplit), TB, 0, s>>>(A, m, K, Rout, rps);
-  cudaError_t ce = lsq_cholesky(Rout, K, dfail, s);
-  if (ce != cudaSuccess) { ctx->err = cudaGetErrorString(ce); return DPM_ERR_CUDA; }
-  DPM_COUNT_LAUNCH(1);
-  trsm_rows_kernel<<<(m + 127) / 128, 128, 0, s>>>(A, m, K, Rout);
-  DPM_CUDA_TRY(ctx, cudaGetLastError());
+// one CholeskyQR pass: R = chol(AᵀA) (upper; 64 x 64-tiled Gram), out = A R⁻¹ (R⁻¹ by warp-parallel
+// back substitution, then a tiled upper-triangular GEMM; out != A).  Same building blocks as the
+// octant DD's distributed CholeskyQR2.
+dpm_status chol_qr_pass(dpm_ctx* ctx, const double* A, int64_t m, int K, double* Rout, double* Ri_ws, double* out,
+                        int* dfail, cudaStream_t s) {
+  DPM_CUDA_TRY(ctx, lsq_gram(A, m, K, Rout, s));
+  DPM_CUDA_TRY(ctx, lsq_cholesky(Rout, K, dfail, s));
+  DPM_CUDA_TRY(ctx, lsq_mul_rinv(A, m, K, Rout, Ri_ws, out, s));
   return DPM_OK;
 }
 
@@ -308,22 +261,24 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   if (!ctx->lsq_ws) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->lsq_ws, (size_t)(3 * K * K + 2 * 1024 * K + 16) * sizeof(double)));
   double* R1 = ctx->lsq_ws;
   double* R2 = R1 + (size_t)K * K;
-  int* dfail = (int*)(R2 + (size_t)K * K);
+  double* Riw = R2 + (size_t)K * K;
+  int* dfail = (int*)(Riw + (size_t)K * K);
   double* dcond = (double*)(dfail + 4);
+  if (!ctx->Mlsq) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->Mlsq, (size_t)m * K * sizeof(double)));
   DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), s));
   DPM_COUNT_LAUNCH(1);
   colnorm_kernel<<<K, TB, 0, s>>>(B, m, ctx->colscale);
   DPM_COUNT_LAUNCH(1);
   scale_cols_kernel<<<148 * 8, TB, 0, s>>>(B, m, K, ctx->colscale, ctx->Q);
   dpm_status st;
-  if ((st = chol_qr_pass(ctx, ctx->Q, m, K, R1, dfail, s)) != DPM_OK) return st;
-  if ((st = chol_qr_pass(ctx, ctx->Q, m, K, R2, dfail, s)) != DPM_OK) return st;
+  // CholeskyQR2 ping-pong: Q -> Mlsq (scratch until the operator is formed) -> Q
+  if ((st = chol_qr_pass(ctx, ctx->Q, m, K, R1, Riw, ctx->Mlsq, dfail, s)) != DPM_OK) return st;
+  if ((st = chol_qr_pass(ctx, ctx->Mlsq, m, K, R2, Riw, ctx->Q, dfail, s)) != DPM_OK) return st;
   DPM_COUNT_LAUNCH(1);
   trmm_kernel<<<(K * K + 255) / 256, 256, 0, s>>>(R2, R1, ctx->R, K);
   DPM_COUNT_LAUNCH(1);
   diag_ratio_kernel<<<1, 1, 0, s>>>(ctx->R, K, dcond);
   // apply operator M = D R^{-1} Q^T (K x |γ_in|): each LSQ solve is then one GEMV
-  if (!ctx->Mlsq) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->Mlsq, (size_t)m * K * sizeof(double)));
   double* Ri = R1;   // R1 is free after the trmm
   DPM_COUNT_LAUNCH(1);
   rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(ctx->R, K, Ri);
@@ -485,13 +440,6 @@ cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s) {
   }
   DPM_COUNT_LAUNCH(1);
   zero_lower_kernel<<<(unsigned)(((long)K * K + 255) / 256), 256, 0, s>>>(G, K);
-  return cudaGetLastError();
-}
-
-cudaError_t lsq_trsm_rows(double* A, int64_t m, int K, const double* R, cudaStream_t s) {
-  if (m == 0) return cudaSuccess;
-  DPM_COUNT_LAUNCH(1);
-  trsm_rows_kernel<<<(unsigned)((m + 127) / 128), 128, 0, s>>>(A, m, K, R);
   return cudaGetLastError();
 }
 

@@ -53,6 +53,20 @@ __global__ void potential_rhs_kernel(const int32_t* __restrict__ gmap, const int
   }
 }
 
+// the same values compacted to the band: qb[r][b] = q_r(band[b])  (fused BEP build, bep_fused.cu)
+__global__ void potential_band_kernel(const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
+                                      int64_t nband, const double* __restrict__ v, int64_t ldv, double* qb,
+                                      int nrhs, int n, double diag, double off, const int32_t* __restrict__ pos) {
+  const long total = (long)nband * nrhs;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
+    const int r = (int)(t / nband);
+    const long b = t - (long)r * nband;
+    int i, j, k;
+    ijk(band[b], n, i, j, k);
+    qb[(size_t)r * nband + (pos ? pos[b] : b)] = lop_gamma(gmap, v + (size_t)r * ldv, n, i, j, k, diag, off);
+  }
+}
+
 __global__ void trace_kernel(const double* __restrict__ u, const int64_t* __restrict__ list, int64_t m, double* out,
                              int64_t batch, size_t field) {
   const long total = (long)m * batch;
@@ -305,6 +319,17 @@ cudaError_t launch_potential_rhs(const dpm_ctx* ctx, const double* v, int64_t ld
   DPM_COUNT_LAUNCH(1);
   potential_rhs_kernel<<<grid_for(nb * nrhs), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, q, nrhs, n,
                                                           diag, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_potential_band(const dpm_ctx* ctx, const double* v, int64_t ldv, double* qb, int nrhs,
+                                  const int32_t* pos, cudaStream_t s) {
+  const int64_t nb = ctx->counts[DPM_SET_BAND];
+  if (nb * nrhs == 0) return cudaSuccess;
+  const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
+  DPM_COUNT_LAUNCH(1);
+  potential_band_kernel<<<grid_for(nb * nrhs), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, qb, nrhs,
+                                                           ctx->n, diag, off, pos);
   return cudaGetLastError();
 }
 

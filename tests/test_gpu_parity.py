@@ -196,6 +196,61 @@ def test_cfg1_outputs(api):
     assert rel(U, o["U"][:-1]) <= 1e-11
 
 
+# ------------------------------------------------------------------ NEXT-1: fused BEP columns
+def _bep_oracle_columns(cfg, cols):
+    g, ps = grid.point_sets_for(cfg)
+    E, d, unit, foot = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.basis)
+    gam, gin = ps.list("gamma"), ps.list("gamma_in")
+    pos = {int(p): i for i, p in enumerate(gam)}
+    gin_pos = np.array([pos[int(p)] for p in gin])
+    n = cfg.n
+    out = []
+    for c in cols:
+        q = dpm.potential_rhs(E[:, c], g, ps, cfg.dt)
+        u = ap.solve(q.reshape(1, n, n, n), g.h, cfg.dt)[0].ravel()
+        out.append((u[gam], E[gin_pos, c] - u[gin]))
+    return out
+
+
+@pytest.mark.parametrize("name,cols", [("cfg1", (0, 7, 49)), ("cfg2", (0, 5, 40, 97)), ("cfg3", (0, 33, 161)),
+                                       ("cfg4", (0, 1, 17, 300, 577))])
+def test_bep_columns_fused_vs_oracle(api, name, cols):
+    # sparse-in / γ-out BEP columns (bep_fused.cu, the default dpm_bep_columns path): potential RHS
+    # from the band values, x DST-I straight from them, middle passes, inverse x DST-I at γ only;
+    # against the oracle's potential RHS -> AP solve -> trace, column by column, at full size for cfg4
+    cfg = get_config(name)
+    c = api.DPM.from_config(cfg)
+    ref = _bep_oracle_columns(cfg, cols)
+    for col, (pg_o, b_o) in zip(cols, ref):
+        PgE, B = c.bep_columns(col, col + 1)
+        assert rel(PgE.cpu().numpy()[0], pg_o) <= 1e-11, (name, col)
+        assert rel(B.cpu().numpy()[0], b_o) <= 1e-11, (name, col)
+
+
+def test_bep_columns_fused_matches_dense_path_cfg4(tmp_path):
+    # all 578 cfg4 columns: fused path vs the dense path (zero fill + scatter + 3 full passes +
+    # gather, DPM_BEP_FUSED=0) in separate processes (the selector is read once per process)
+    import os, subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent('''
+        import sys, numpy as np, torch
+        from dpm_inputs import get_config
+        from paper_1811_03557_b200 import api
+        c = api.DPM.from_config(get_config("cfg4"))
+        PgE, B = c.bep_columns(0, c.K)
+        np.save(sys.argv[1], PgE.cpu().numpy()); np.save(sys.argv[2], B.cpu().numpy())
+    ''')
+    outs = {}
+    for f in ("1", "0"):
+        a, b = str(tmp_path / f"pg{f}.npy"), str(tmp_path / f"b{f}.npy")
+        r = subprocess.run([sys.executable, "-c", code, a, b], cwd=root, env=dict(os.environ, DPM_BEP_FUSED=f),
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr
+        outs[f] = (np.load(a), np.load(b))
+    assert rel(outs["1"][0], outs["0"][0]) <= 1e-12
+    assert rel(outs["1"][1], outs["0"][1]) <= 1e-12
+
+
 def test_state_errors(api):
     from paper_1811_03557_b200._lib import DPMError, DPM_ERR_STATE, DPM_ERR_RANK
     cfg = get_config("cfg1")
