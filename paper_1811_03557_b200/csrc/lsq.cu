@@ -102,19 +102,73 @@ __global__ void zero_lower_kernel(double* G, int K) {
   if (i > j) G[t] = 0.0;
 }
 
-// Back substitution R x = e_j for every column j, one warp per column (the inner products over
-// the already-solved entries are warp-parallel): R^{-1}, upper triangular.
-__global__ void rinv_warp_kernel(const double* __restrict__ R, int K, double* __restrict__ Ri) {
-  const int j = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
-  if (j >= K) return;
-  double* x = Ri + (size_t)j * K;
-  for (int i = j + 1 + lane; i < K; i += 32) x[i] = 0.0;
-  for (int i = j; i >= 0; --i) {
+// Blocked inverse of an upper-triangular K x K R (col-major) by 32 x 32 tiles, nb = ceil(K/32):
+//   X_bb = R_bb^{-1} (all diagonal tiles in parallel), then for each block diagonal d = 1..nb-1
+//   X_{b,b+d} = -X_bb Σ_{k=b+1}^{b+d} R_{b,k} X_{k,b+d}   (independent tiles: one CTA each).
+// Replaces a column-by-column back substitution whose K-step dependent chain of strided reads
+// took ~1 ms at K = 578.  Entries beyond K are treated as the identity (never written).
+constexpr int RT = 32;
+
+__device__ __forceinline__ double rt_at(const double* R, int K, int i, int j) {   // padded R
+  return (i < K && j < K) ? R[(size_t)j * K + i] : (i == j ? 1.0 : 0.0);
+}
+
+// one warp per diagonal tile: lane i computes row i of the inverse (x_i R = e_i, forward over j)
+__global__ void rinv_diag_kernel(const double* __restrict__ R, int K, double* __restrict__ Ri) {
+  __shared__ double a[RT][RT + 1], x[RT][RT + 1];
+  const int b0 = blockIdx.x * RT, i = threadIdx.x;
+  for (int e = 0; e < RT; ++e) a[i][e] = rt_at(R, K, b0 + i, b0 + e);   // a[row][col]
+  __syncwarp();
+  for (int j = 0; j < RT; ++j) {
+    double v = (i == j) ? 1.0 : 0.0;
+    if (j > i) {
+      v = 0.0;
+      for (int k = i; k < j; ++k) v = fma(x[i][k], a[k][j], v);
+      v = -v;
+    }
+    x[i][j] = j < i ? 0.0 : v / a[j][j];
+  }
+  __syncwarp();
+  for (int j = 0; j < RT; ++j)
+    if (b0 + i < K && b0 + j < K) Ri[(size_t)(b0 + j) * K + b0 + i] = x[i][j];
+}
+
+// tile (b, b + d) of the inverse for the block diagonal d (grid: nb - d CTAs of 256 threads)
+__global__ void __launch_bounds__(256) rinv_offdiag_kernel(const double* __restrict__ R, int K, int d,
+                                                           double* __restrict__ Ri) {
+  __shared__ double sa[RT][RT + 1], sb[RT][RT + 1];
+  const int b = blockIdx.x, c = b + d;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // output (row ty + 8u, col tx)
+  double acc[4] = {0, 0, 0, 0};
+  // tile loads: lanes run over the (contiguous, col-major) row index
+  for (int k = b + 1; k <= c; ++k) {   // T = Σ_k R_{b,k} X_{k,c}
+    for (int q = ty; q < RT; q += 8) {
+      sa[tx][q] = rt_at(R, K, b * RT + tx, k * RT + q);                     // R_{b,k}[tx][q]
+      const int r = k * RT + tx, col = c * RT + q;
+      sb[tx][q] = (r < K && col < K) ? Ri[(size_t)col * K + r] : (r == col ? 1.0 : 0.0);   // X_{k,c}[tx][q]
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int l = 0; l < RT; ++l) {
+      const double bv = sb[l][tx];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(sa[ty + 8 * u][l], bv, acc[u]);
+    }
+    __syncthreads();
+  }
+  // X_{b,c} = -X_bb T
+  for (int u = 0; u < 4; ++u) sb[ty + 8 * u][tx] = acc[u];
+  for (int q = ty; q < RT; q += 8) {
+    const int r = b * RT + tx, col = b * RT + q;
+    sa[tx][q] = (r < K && col < K) ? Ri[(size_t)col * K + r] : (r == col ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int u = 0; u < 4; ++u) {   // output (row tx, col ty + 8u): lanes store consecutive rows
+    const int q = ty + 8 * u;
     double v = 0.0;
-    for (int k = i + 1 + lane; k <= j; k += 32) v = fma(R[(size_t)k * K + i], x[k], v);
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) x[i] = ((i == j ? 1.0 : 0.0) - v) / R[(size_t)i * K + i];
-    __syncwarp();
+    for (int l = tx; l < RT; ++l) v = fma(sa[tx][l], sb[l][q], v);
+    const int r = b * RT + tx, col = c * RT + q;
+    if (r < K && col < K) Ri[(size_t)col * K + r] = -v;
   }
 }
 
@@ -280,8 +334,7 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   diag_ratio_kernel<<<1, 1, 0, s>>>(ctx->R, K, dcond);
   // apply operator M = D R^{-1} Q^T (K x |γ_in|): each LSQ solve is then one GEMV
   double* Ri = R1;   // R1 is free after the trmm
-  DPM_COUNT_LAUNCH(1);
-  rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(ctx->R, K, Ri);
+  DPM_CUDA_TRY(ctx, lsq_rinv(ctx->R, K, Ri, s));
   DPM_COUNT_LAUNCH(1);
   lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri, ctx->Q, ctx->colscale, K, m,
                                                                                       ctx->Mlsq);
@@ -403,12 +456,25 @@ __global__ void __launch_bounds__(256) gram64_kernel(const double* __restrict__ 
     }
 }
 
+// R^{-1} (upper triangular, col-major; lower triangle of Ri zeroed) by the blocked kernels above
+cudaError_t lsq_rinv(const double* R, int K, double* Ri, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(Ri, 0, (size_t)K * K * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  const int nb = (K + RT - 1) / RT;
+  DPM_COUNT_LAUNCH(1);
+  rinv_diag_kernel<<<nb, RT, 0, s>>>(R, K, Ri);
+  for (int d = 1; d < nb; ++d) {
+    DPM_COUNT_LAUNCH(1);
+    rinv_offdiag_kernel<<<nb - d, 256, 0, s>>>(R, K, d, Ri);
+  }
+  return cudaGetLastError();
+}
+
 // ---- building blocks shared with the octant DD (dd.cu): distributed CholeskyQR2 ----
 cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, double* Ri_ws, double* out,
                          cudaStream_t s) {
-  DPM_COUNT_LAUNCH(1);
-  rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(R, K, Ri_ws);
-  if (m == 0) return cudaGetLastError();
+  cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
+  if (e != cudaSuccess || m == 0) return e;
   DPM_COUNT_LAUNCH(1);
   gemm_upper_kernel<<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, Ri_ws, out);
   return cudaGetLastError();
@@ -458,9 +524,8 @@ cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scal
 // M = diag(scale) R^{-1} Q^T (K x m row-major); Ri_ws: K x K workspace
 cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int K, const double* scale, double* M,
                                double* Ri_ws, cudaStream_t s) {
-  DPM_COUNT_LAUNCH(1);
-  rinv_warp_kernel<<<(K + 7) / 8, 256, 0, s>>>(R, K, Ri_ws);
-  if (m == 0) return cudaGetLastError();
+  cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
+  if (e != cudaSuccess || m == 0) return e;
   DPM_COUNT_LAUNCH(1);
   lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri_ws, Q, scale, K, m, M);
   return cudaGetLastError();
