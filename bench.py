@@ -330,9 +330,15 @@ def main():
     alg_bytes = 16 * n ** 3                              # dense fp64 box in + out per solve
     hbm_peak = peaks["hbm_gbs"]
     clocks = clk.summary()
-    # fp64 work of the path as built: 4 prime-factor DST-I transforms (2 x 2732 flop
-    # per line of 128 from the 2x3x43 factorisation) + the exact tridiagonal solve (~7 flop/point)
-    flops_per_solve = 4 * n * n * 2 * 2732 + 7 * n ** 3
+    # fp64 work of the path as built: prime-factor DST-I transforms at 2 x 2732 flop per
+    # line of 128 (2x3x43 factorisation) - two x passes over n^2 lines, and with the FACR(1) plane
+    # pass two y transforms over the n^2/2 odd-z lines plus ~15 flop/point of recurrences (reduced
+    # RHS, reduced z tridiagonal, even-z y tridiagonal); the full-transform plane kernel
+    # (DPM_PLANE_FACR=0): four transforms + ~7 flop/point
+    if os.environ.get("DPM_PLANE_FACR") == "0":
+        flops_per_solve = 4 * n * n * 2 * 2732 + 7 * n ** 3
+    else:
+        flops_per_solve = 3 * n * n * 2 * 2732 + 15 * n ** 3
 
     # Per-kernel roofline of the dominant kernel: the same solves again with pass timing enabled
     # (CUDA events recorded by the library on this stream around every pass), right after the
