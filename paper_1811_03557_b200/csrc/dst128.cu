@@ -836,6 +836,24 @@ __device__ __forceinline__ void st_async(unsigned remote, double v, unsigned rem
                : "memory");
 }
 
+// Optional phase timing (build with -DFACR_PHASE_TIMING=1, read with dpm_debug_facr_phases; not in
+// the default library): clock64 at the phase boundaries of the first FACR_TCTAS CTAs, thread 0.
+#ifndef FACR_PHASE_TIMING
+#define FACR_PHASE_TIMING 0
+#endif
+constexpr int FACR_TCTAS = 4096, FACR_TPH = 9;
+#if FACR_PHASE_TIMING
+__device__ unsigned long long g_facr_ph[FACR_TCTAS][FACR_TPH];
+#define FACR_MARK(k)                                                              \
+  do {                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x < FACR_TCTAS) g_facr_ph[blockIdx.x][k] = clock64(); \
+  } while (0)
+#else
+#define FACR_MARK(k) \
+  do {               \
+  } while (0)
+#endif
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PTHR, 2)
 plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double inv_dt, double h2,
                      double gs) {
@@ -856,6 +874,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   const int a = (int)(plane & (N - 1));
   double* gp = u + (size_t)plane * NN + (size_t)rank * PHC;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  FACR_MARK(0);
   if (t == 0) {
     mbar_init(bar0, 1);
     mbar_init(bar1, 1);
@@ -883,6 +902,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     asm volatile("cp.async.wait_group 0;\n" ::);
   }
   __syncthreads();
+  FACR_MARK(1);
   const double hsa = h2 * (inv_dt + lam[a]);
   const double beta = 4.0 + hsa;
   // (1) r_i = gs (β g_z[y] - g_z[y-1] - g_z[y+1] + g_{z-1}[y] + g_{z+1}[y]),  z = 2i + 1,  i = lane
@@ -907,12 +927,14 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     if (rank == 0) P[t * PPITCH + PHC] = 0.0;   // ghost z = -1 for phase 5
   }
   __syncthreads();
+  FACR_MARK(2);
 #if PLANE_YDST_INLINE
   plane_ydst<true>(P);
 #else
   plane_ydst_call<true>(P);
 #endif
   __syncthreads();
+  FACR_MARK(3);
   // (3) reduced system per y-mode row b: -u_{i-1} + d u_i - u_{i+1} = ys r̂_i over the 64 kept z,
   //     d = τ² - 2 = μ + 1/μ with μ = μ_τ², last global row d + 1.
   {
@@ -972,12 +994,14 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     }
   }
   __syncthreads();
+  FACR_MARK(4);
 #if PLANE_YDST_INLINE
   plane_ydst<true>(P);
 #else
   plane_ydst_call<true>(P);
 #endif
   __syncthreads();
+  FACR_MARK(5);
   // rank 0 pushes v(z = 63) into rank 1's neighbour column (rank 1 finished reading its ghost
   // column in phase 1 before the interface barrier above); rank 1 waits for it, rank 0 only
   // before exiting.
@@ -987,12 +1011,13 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     if (t == 0) mbar_expect_tx(bar1, N * sizeof(double));
     mbar_wait(bar1, 0);
   }
+  FACR_MARK(6);
   // (5) eliminated column j = 16 (warp/2) + 2 (lane%8) + warp%2, row segment s = lane/8:
   //     [0,33) [33,64) [64,97) [97,128); a half-warp holds 8 columns of one parity x 2 segments
   //     whose start rows are ≡ 0, 1 mod 16: 16 distinct 8-byte bank pairs
   {
     const int j = 16 * (warp >> 1) + 2 * (lane & 7) + (warp & 1), s = lane >> 3;
-    const int kb = (s >> 1) * 64 + (s & 1) * 33, L = (s & 1) ? 31 : 33, ke = kb + L;
+    const int kb = (s >> 1) * 64 + (s & 1) * 33, L = (s & 1) ? 31 : 33;
     const double muy = 2.0 / (beta + sqrt((beta - 2.0) * (beta + 2.0)));
     const double imu = 1.0 / muy, mu2 = muy * muy;
     double* col = P + kb * PPITCH + 32 + j;
@@ -1058,11 +1083,13 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     }
   }
   __syncthreads();
+  FACR_MARK(7);
   for (int e = t; e < N * PHC; e += PTHR) {   // same lane -> (column, z) map as the load
     const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
     const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
     __stcg(gp + (size_t)r * N + z, P[r * PPITCH + c]);
   }
+  FACR_MARK(8);
   // no exit barrier: each CTA has consumed every remote store aimed at it (its mbarrier waits), and
   // issues none after its partner's last wait
 }
@@ -1188,3 +1215,10 @@ cudaError_t plane128_pass(double* u, int nfields, const double* lam, double inv_
   k<<<(unsigned)ctas, PTHR, smem, s>>>(u, lam, inv_dt, h2, arg);
   return cudaGetLastError();
 }
+
+#if FACR_PHASE_TIMING
+extern "C" int dpm_debug_facr_phases(unsigned long long* host, int nctas) {
+  const int n = nctas < FACR_TCTAS ? nctas : FACR_TCTAS;
+  return (int)cudaMemcpyFromSymbol(host, g_facr_ph, (size_t)n * FACR_TPH * sizeof(unsigned long long));
+}
+#endif

@@ -265,6 +265,22 @@ def test_state_errors(api):
     assert e.value.status == DPM_ERR_RANK
 
 
+def test_pks_nonfinite_reported(api):
+    # a non-finite step output is DPM_ERR_NONFINITE (not a silent NaN field)
+    from paper_1811_03557_b200._lib import DPMError, DPM_ERR_NONFINITE
+    cfg = get_config("cfg2")
+    c = api.DPM.from_config(cfg)
+    n = cfg.n
+    rho = torch.zeros((n, n, n), dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    mp = c.copy_set("mplus")
+    rho.view(-1)[int(mp[len(mp) // 2])] = float("nan")
+    with pytest.raises(DPMError) as e:
+        c.pks_step(rho, cc, 3, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=1)
+    assert e.value.status == DPM_ERR_NONFINITE
+
+
 # ------------------------------------------------------------------ PKS (cfg2, cfg3)
 def run_pks_gpu(api, cfg, dt_rule=0):
     c = api.DPM.from_config(cfg)
