@@ -238,11 +238,12 @@ __global__ void lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K, 
   for (int r0 = 0; r0 < nrhs; r0 += GEMV_R) {
     const int nr = min(GEMV_R, nrhs - r0);
     double s[GEMV_R] = {0, 0, 0, 0};
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const double av = a[i];
+#pragma unroll 8
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {   // unrolled: 8 rows of loads in flight
+      const double av = __ldg(a + i);
 #pragma unroll
       for (int q = 0; q < GEMV_R; ++q)
-        if (q < nr) s[q] = fma(av, g[(size_t)(r0 + q) * m + i], s[q]);
+        if (q < nr) s[q] = fma(av, __ldg(g + (size_t)(r0 + q) * m + i), s[q]);
     }
 #pragma unroll
     for (int q = 0; q < GEMV_R; ++q) {

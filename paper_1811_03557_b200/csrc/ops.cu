@@ -118,17 +118,19 @@ __device__ __forceinline__ double minmod3(double a, double b, double c) {
   return 0.0;
 }
 
-// minmod slope of cell q along axis ax; 0 unless q and both neighbours are in N+ (R15).
-// Ghost cells hold 0, so their slope is 0.
-__device__ __forceinline__ double slope(const double* __restrict__ rho, const uint8_t* __restrict__ flags, int n, int i,
-                                        int j, int k, int ax, double h) {
+// h x the minmod slope of cell q along axis ax; 0 unless q and both neighbours are in N+
+// (R15).  Ghost cells hold 0, so their slope is 0.  The three minmod arguments share the positive
+// factor 1/h, so the limiter runs on the unscaled differences (x2 and x1/2 are exact): the same
+// choice as with the divided slopes, and h s enters the reconstruction r0 ± (h/2) s directly.
+__device__ __forceinline__ double slope_h(const double* __restrict__ rho, const uint8_t* __restrict__ flags, int n,
+                                          int i, int j, int k, int ax) {
   if (!interior(n, i, j, k)) return 0.0;
   if (!(flags[flat(n, i, j, k)] & F_NPLUS)) return 0.0;
   const int di = ax == 0, dj = ax == 1, dk = ax == 2;
   if (!nplus_at(flags, n, i + di, j + dj, k + dk) || !nplus_at(flags, n, i - di, j - dj, k - dk)) return 0.0;
   const double r0 = rho[flat(n, i, j, k)];
   const double rp = valat(rho, n, i + di, j + dj, k + dk), rm = valat(rho, n, i - di, j - dj, k - dk);
-  return minmod3(2.0 * (rp - r0) / h, (rp - rm) / (2.0 * h), 2.0 * (r0 - rm) / h);
+  return minmod3(2.0 * (rp - r0), 0.5 * (rp - rm), 2.0 * (r0 - rm));
 }
 
 __device__ __forceinline__ void umax_atomic(double* addr, double v) {
@@ -178,20 +180,21 @@ __global__ void flux_rhs_kernel(const double* __restrict__ rho, const double* __
     int i, j, k;
     ijk(p, n, i, j, k);
     const double r0 = rho[p], c0 = c[p];
+    const double ih = 1.0 / h, idt = 1.0 / dt;   // (fp64 division is a long sequence: once per thread)
     double g = 0.0;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
       const int di = ax == 0, dj = ax == 1, dk = ax == 2;
       const double cE = valat(c, n, i + di, j + dj, k + dk), cW = valat(c, n, i - di, j - dj, k - dk);
       const double rE = valat(rho, n, i + di, j + dj, k + dk), rW = valat(rho, n, i - di, j - dj, k - dk);
-      const double gE = (cE - c0) / h, gW = (c0 - cW) / h;
-      const double s0 = slope(rho, flags, n, i, j, k, ax, h);
-      const double rhoE = gE > 0 ? r0 + 0.5 * h * s0 : rE - 0.5 * h * slope(rho, flags, n, i + di, j + dj, k + dk, ax, h);
-      const double rhoW = gW > 0 ? rW + 0.5 * h * slope(rho, flags, n, i - di, j - dj, k - dk, ax, h) : r0 - 0.5 * h * s0;
-      g += (chi * rhoE * gE - chi * rhoW * gW) / h;
+      const double gE = (cE - c0) * ih, gW = (c0 - cW) * ih;   // upwind choice: the sign of the difference
+      const double s0 = slope_h(rho, flags, n, i, j, k, ax);
+      const double rhoE = gE > 0 ? r0 + 0.5 * s0 : rE - 0.5 * slope_h(rho, flags, n, i + di, j + dj, k + dk, ax);
+      const double rhoW = gW > 0 ? rW + 0.5 * slope_h(rho, flags, n, i - di, j - dj, k - dk, ax) : r0 - 0.5 * s0;
+      g += (chi * rhoE * gE - chi * rhoW * gW) * ih;
     }
-    fq_rho[p] = (r0 - dt * g) / dt;
-    fq_c[p] = ((1.0 - dt) * c0 + dt * r0) / dt;
+    fq_rho[p] = (r0 - dt * g) * idt;
+    fq_c[p] = ((1.0 - dt) * c0 + dt * r0) * idt;
   }
 }
 
