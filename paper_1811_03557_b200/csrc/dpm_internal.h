@@ -39,6 +39,7 @@ struct DstPlan {
   double* atab128 = nullptr;  // n = 128: A fragments of the prime-factor DST-I
   int pfa = 1;            // n = 128: prime-factor DST-I for the x / y passes (DPM_PFA=0 disables)
   int plane = 1;          // n = 128: fused y / z / y plane pass (DPM_PLANE=0 disables)
+  double* sinmat = nullptr;   // n <= 64: device n x n sine matrix of the fused small-n plane pass
   PassProf* prof = nullptr;   // non-null while pass timing is enabled
   cudaStream_t side = nullptr;                    // second chunk stream (DPM_STREAMS=2)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

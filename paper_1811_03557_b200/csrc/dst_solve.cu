@@ -538,6 +538,180 @@ ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __r
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Fused plane pass for n <= 64 (the PKS configs cfg2 / cfg3, whose AP batches hold only 2 fields):
+// one CTA per x-mode plane a ([y][z], n x n, contiguous) with the plane and the sine matrix in
+// shared memory: y DST-I (S^T P, 4 x 4 register tiles), the exact z tridiagonal of every y-mode row
+// (warp per row, 2 entries per lane: the recurrences, Kogge–Stone carries and Sherman–Morrison of
+// ztri_warp_kernel), inverse y DST-I.  One launch instead of three (y, z, y).
+constexpr int PSN = 64, PSP = 65;   // largest n, shared-memory row pitch
+
+__global__ void sinmat_kernel(double* S, int n) {   // S[j][k] = sin(π (j+1)(k+1)/(n+1)), exact reduction
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  const int j = e / n, k = e % n;
+  S[e] = sinpi((double)(((j + 1) * (k + 1)) % (2 * (n + 1))) / (double)(n + 1));
+}
+
+// P <- S^T P in place (S symmetric); thread (rb, cb) = (t / 16, t % 16) owns rows 4rb..4rb+3 and
+// columns cb + 16j; S and P are zero-padded to 64 x 64.  (512 threads with 2 x 4 tiles: slower.)
+constexpr int PS_THREADS = 256;
+__device__ __forceinline__ void ps_apply(const double* S, double* P, int n) {
+  const int t = threadIdx.x, rb = t >> 4, cb = t & 15;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  if (4 * rb < n) {
+    if ((n & 1) == 0) {
+      // folded: sin(π(N-j)k/N) = (-1)^{k+1} sin(πjk/N), N = n + 1, so output row b (k = b + 1) needs
+      // x_y + x_{n-1-y} (b even) or x_y - x_{n-1-y} (b odd) over y < n/2 only: half the products
+#pragma unroll 2
+      for (int y = 0; y < n / 2; ++y) {
+        double sv[4], ap[4], am[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sv[i] = S[y * PSP + 4 * rb + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double p1 = P[y * PSP + cb + 16 * j], p2 = P[(n - 1 - y) * PSP + cb + 16 * j];
+          ap[j] = p1 + p2;
+          am[j] = p1 - p2;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(sv[i], (i & 1) ? am[j] : ap[j], acc[i][j]);
+      }
+    } else {
+#pragma unroll 4
+      for (int y = 0; y < n; ++y) {
+        double sv[4], pv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sv[i] = S[y * PSP + 4 * rb + i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pv[j] = P[y * PSP + cb + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(sv[i], pv[j], acc[i][j]);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (4 * rb + i < n && cb + 16 * j < n) P[(4 * rb + i) * PSP + cb + 16 * j] = acc[i][j];
+  __syncthreads();
+}
+
+// exact solve of (hs + 2) v_k - v_{k-1} - v_{k+1} = rscale r_k (k < n <= 64, zero ends) in place, one
+// warp; mu = μ(hs) and inv_den = 1/(1 - μ^{2n+2}) come precomputed (lane-parallel over the warp's rows)
+__device__ __forceinline__ void ps_tri_row(double* row, int n, double mu, double inv_den, double rscale) {
+  const int lane = threadIdx.x & 31, k0 = 2 * lane;
+  const double mu2 = mu * mu;
+  double mp[7];   // μ^{2·2^q}
+  mp[0] = mu2;
+#pragma unroll
+  for (int q = 1; q < 7; ++q) mp[q] = mp[q - 1] * mp[q - 1];
+  const double r0 = k0 < n ? row[k0] : 0.0, r1 = k0 + 1 < n ? row[k0 + 1] : 0.0;
+  // forward y_k = r_k + μ y_{k-1}
+  double y0 = rscale * r0, y1 = fma(mu, y0, rscale * r1);
+  double C = y1;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const double tq = __shfl_up_sync(0xffffffffu, C, 1 << q);
+    if (lane >= (1 << q)) C = fma(mp[q], tq, C);
+  }
+  double cin = __shfl_up_sync(0xffffffffu, C, 1);
+  cin = lane == 0 ? 0.0 : cin;
+  y0 = fma(mu, cin, y0);
+  y1 = fma(mu2, cin, y1);
+  if (k0 >= n) y0 = 0.0;
+  if (k0 + 1 >= n) y1 = 0.0;
+  // backward z_k = y_k + μ z_{k+1}
+  double z1 = y1, z0 = fma(mu, y1, y0);
+  double D = z0;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const double tq = __shfl_down_sync(0xffffffffu, D, 1 << q);
+    if (lane + (1 << q) < 32) D = fma(mp[q], tq, D);
+  }
+  double din = __shfl_down_sync(0xffffffffu, D, 1);
+  din = lane == 31 ? 0.0 : din;
+  z1 = fma(mu, din, z1);
+  z0 = fma(mu2, din, z0);
+  // T^{-1} r = μ z - c2 (μ^{k+1} - μ^{2n+1-k}),  c2 = μ^2 z_0 / (1 - μ^{2n+2});  direct powers
+  // μ^{2 lane} and μ^{2(n - lane)} from the bits of lane and n - lane
+  const double zf = __shfl_sync(0xffffffffu, z0, 0);
+  const double c2 = mu2 * zf * inv_den;
+  const int rl = max(0, n - lane);
+  double pl = 1.0, pr = 1.0;
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    if ((lane >> q) & 1) pl *= mp[q];
+    if ((rl >> q) & 1) pr *= mp[q];
+  }
+  const double pa0 = mu * pl;   // μ^{k0+1}
+  const double pb1 = pr;        // μ^{2n-k0} = μ^{2n+1-(k0+1)}
+  if (k0 < n) row[k0] = fma(mu, z0, -c2 * (pa0 - pb1 * mu));
+  if (k0 + 1 < n) row[k0 + 1] = fma(mu, z1, -c2 * (pa0 * mu - pb1));
+}
+
+__global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restrict__ u, int n, const double* __restrict__ S_g,
+                                                          const double* __restrict__ lam_g, double inv_dt, double h2,
+                                                          double rscale) {
+  extern __shared__ double psm_small[];
+  double* S = psm_small;           // [64][PSP]
+  double* P = S + PSN * PSP;       // [64][PSP]
+  double* lam = P + PSN * PSP;     // [64]
+  const long plane = blockIdx.x;   // field * n + a
+  const int a = (int)(plane % n), t = threadIdx.x;
+  double* g = u + (size_t)plane * n * n;
+  for (int e = t; e < PSN * PSN; e += blockDim.x) {
+    const int r = e / PSN, c = e % PSN;
+    const bool in = r < n && c < n;
+    S[r * PSP + c] = in ? __ldg(S_g + r * n + c) : 0.0;
+    P[r * PSP + c] = in ? g[(size_t)r * n + c] : 0.0;
+  }
+  for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
+  __syncthreads();
+  ps_apply(S, P, n);
+  {
+    // warp w solves rows b = w + 8 i (i < 8); lane i first computes μ and 1/(1 - μ^{2n+2}) of row i
+    const int w = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
+    double mu_l = 0.5, id_l = 1.0;
+    const int bl = w + nw * lane;
+    if (lane < 8 && bl < n) {
+      const double hs = h2 * ((inv_dt + lam[a]) + lam[bl]);
+      mu_l = 2.0 / ((2.0 + hs) + sqrt(hs * (hs + 4.0)));
+      id_l = 1.0 / (1.0 - ipow(mu_l, 2 * n + 2));
+    }
+    for (int i = 0; i < 8; ++i) {
+      const int b = w + nw * i;
+      const double mu = __shfl_sync(0xffffffffu, mu_l, i), id = __shfl_sync(0xffffffffu, id_l, i);
+      if (b < n) ps_tri_row(P + b * PSP, n, mu, id, rscale);
+    }
+  }
+  __syncthreads();
+  ps_apply(S, P, n);
+  for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
+}
+
+cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
+  const int n = p.n;
+  const size_t smem = (2 * (size_t)PSN * PSP + PSN) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(plane_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const double sc = 2.0 / (n + 1);
+  DPM_COUNT_LAUNCH(1);
+  plane_small_kernel<<<(unsigned)((long)nfields * n), PS_THREADS, smem, s>>>(u, n, p.sinmat, p.lam, 1.0 / p.dt, p.h * p.h,
+                                                                       sc * sc * p.h * p.h);
+  return cudaGetLastError();
+}
+
 cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
   const int n = p.n;
   const long nlines = (long)nfields * n * n;
@@ -583,6 +757,15 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
   afrag_table_kernel<<<dim3(NW, 2), KSMAX_ALL * 32>>>(p.atab, n, tc_for(n) / 8);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (n <= PSN) {   // fused small-n plane pass (DPM_PLANE_SMALL=0 disables)
+    const char* envs = getenv("DPM_PLANE_SMALL");
+    if (!(envs && atoi(envs) == 0)) {
+      if ((e = cudaMalloc(&p.sinmat, sizeof(double) * n * n)) != cudaSuccess) return e;
+      DPM_COUNT_LAUNCH(1);
+      sinmat_kernel<<<(n * n + 255) / 256, 256>>>(p.sinmat, n);
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+  }
   if (n == 128) {
     const char* env = getenv("DPM_PFA");
     p.pfa = !(env && atoi(env) == 0);
@@ -602,7 +785,9 @@ void dst_plan_free(DstPlan& p) {
   if (p.lam) cudaFree(p.lam);
   if (p.atab) cudaFree(p.atab);
   if (p.atab128) cudaFree(p.atab128);
+  if (p.sinmat) cudaFree(p.sinmat);
   p.atab128 = nullptr;
+  p.sinmat = nullptr;
   p.lam = nullptr;
   p.atab = nullptr;
 }
@@ -645,6 +830,7 @@ cudaError_t middle_passes(const DstPlan& p, double* ui, int nf, double inv_dt, d
     const double sc2 = 2.0 / (n + 1);
     return timed(p, 1, pts, s, [&] { return plane128_pass(ui, nf, p.lam, inv_dt, p.h * p.h, sc2 * sc2 * p.h * p.h, s); });
   }
+  if (n <= PSN && p.sinmat) return timed(p, 1, pts, s, [&] { return run_plane_small(p, ui, nf, s); });
   auto pass = [&](int k) { return timed(p, k, pts, s, [&] { return run_pass(p, k, ui, ui, nf, inv_dt, scale, s); }); };
   cudaError_t e;
   if ((e = pass(1)) != cudaSuccess) return e;
