@@ -230,11 +230,12 @@ __global__ void lsq_operator_kernel(const double* __restrict__ Ri, const double*
 // coef[r][c] = Σ_i M[c][i] g[r][i]: one 128-thread block per row c, all right-hand sides at once
 // (M is read once per apply).
 constexpr int GEMV_R = 4;
+constexpr int GEMV_T = 512;   // threads per row: 16 warps of loads in flight per row block
 __global__ void lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K, const double* __restrict__ g, int nrhs,
                                 double* __restrict__ coef) {
   const int c = blockIdx.x;
   const double* a = M + (size_t)c * m;
-  __shared__ double red[GEMV_R][4];
+  __shared__ double red[GEMV_R][GEMV_T / 32];
   for (int r0 = 0; r0 < nrhs; r0 += GEMV_R) {
     const int nr = min(GEMV_R, nrhs - r0);
     double s[GEMV_R] = {0, 0, 0, 0};
@@ -253,7 +254,10 @@ __global__ void lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K, 
     __syncthreads();
     if (threadIdx.x < nr) {
       const int q = threadIdx.x;
-      coef[(size_t)(r0 + q) * K + c] = (red[q][0] + red[q][1]) + (red[q][2] + red[q][3]);
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < GEMV_T / 32; ++w) v += red[q][w];
+      coef[(size_t)(r0 + q) * K + c] = v;
     }
     __syncthreads();
   }
@@ -356,7 +360,7 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN], ng = ctx->counts[DPM_SET_GAMMA];
   DPM_COUNT_LAUNCH(1);
-  lsq_gemv_kernel<<<K, 128, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
+  lsq_gemv_kernel<<<K, GEMV_T, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
   if (u_gamma) return lsq_extend(ctx->E, ng, K, coef, nrhs, clamp, u_gamma, s);
   return cudaGetLastError();
 }
@@ -534,7 +538,7 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
 
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
-  lsq_gemv_kernel<<<K, 128, 0, s>>>(M, m, K, g, nrhs, coef);
+  lsq_gemv_kernel<<<K, GEMV_T, 0, s>>>(M, m, K, g, nrhs, coef);
   return cudaGetLastError();
 }
 
