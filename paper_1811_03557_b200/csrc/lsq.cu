@@ -43,46 +43,58 @@ __global__ void scale_cols_kernel(const double* __restrict__ B, int64_t m, int K
 // (3) trailing update G_ij -= Σ_{k in block} R_ki R_kj for i <= j (2D grid).
 constexpr int CB = 32;
 
+// one warp: unblocked factor of the diagonal block in shared memory (warp barriers only)
 __global__ void chol_diag_kernel(double* G, int K, int k0, int* fail) {
   __shared__ double a[CB][CB + 1];
-  const int nb = min(CB, K - k0);
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+  const int nb = min(CB, K - k0), lane = threadIdx.x;
+  for (int e = lane; e < nb * nb; e += 32) {
     const int i = e % nb, j = e / nb;
     a[i][j] = G[(size_t)(k0 + j) * K + k0 + i];
   }
-  __syncthreads();
+  __syncwarp();
   for (int k = 0; k < nb; ++k) {
-    if (threadIdx.x == 0) {
-      const double d = a[k][k];
-      if (!(d > 0.0)) *fail = 1;
-      a[k][k] = d > 0.0 ? sqrt(d) : 1.0;
+    const double d = a[k][k];
+    const double r = d > 0.0 ? sqrt(d) : 1.0;
+    if (lane == 0 && !(d > 0.0)) *fail = 1;
+    __syncwarp();
+    const int j = lane;   // row k right of the diagonal: a[k][j] /= r
+    if (j > k && j < nb) a[k][j] /= r;
+    if (lane == 0) a[k][k] = r;
+    __syncwarp();
+    if (j > k && j < nb) {   // trailing update, column j (lane): a[i][j] -= a[k][i] a[k][j], k < i <= j
+      const double akj = a[k][j];
+      for (int i = k + 1; i <= j; ++i) a[i][j] -= a[k][i] * akj;
     }
-    __syncthreads();
-    for (int j = k + 1 + threadIdx.x; j < nb; j += blockDim.x) a[k][j] /= a[k][k];
-    __syncthreads();
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-      const int i = e % nb, j = e / nb;
-      if (i > k && j >= i) a[i][j] -= a[k][i] * a[k][j];
-    }
-    __syncthreads();
+    __syncwarp();
   }
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+  for (int e = lane; e < nb * nb; e += 32) {
     const int i = e % nb, j = e / nb;
     G[(size_t)(k0 + j) * K + k0 + i] = (i <= j) ? a[i][j] : 0.0;
   }
 }
 
-__global__ void chol_panel_kernel(double* G, int K, int k0) {
-  const int nb = min(CB, K - k0);
-  const int j = k0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= K) return;
-  double x[CB];
-  for (int i = 0; i < nb; ++i) {
-    double v = G[(size_t)j * K + k0 + i];
-    for (int q = 0; q < i; ++q) v -= G[(size_t)(k0 + i) * K + k0 + q] * x[q];
-    x[i] = v / G[(size_t)(k0 + i) * K + k0 + i];
+// row-panel solve R_kk^T X = G_k,j for the columns j right of the block: one warp per column, lane =
+// row of the panel; R_kk (and 1/diag) staged in shared memory once per CTA
+constexpr int CHOL_PW = 8;   // warps (columns) per CTA
+__global__ void __launch_bounds__(32 * CHOL_PW) chol_panel_kernel(double* G, int K, int k0) {
+  __shared__ double r[CB][CB + 1], rd[CB];
+  const int nb = min(CB, K - k0), lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, j = e / nb;
+    r[i][j] = G[(size_t)(k0 + j) * K + k0 + i];
   }
-  for (int i = 0; i < nb; ++i) G[(size_t)j * K + k0 + i] = x[i];
+  __syncthreads();
+  if (threadIdx.x < nb) rd[threadIdx.x] = 1.0 / r[threadIdx.x][threadIdx.x];
+  __syncthreads();
+  const int j = k0 + nb + blockIdx.x * CHOL_PW + w;
+  if (j >= K) return;
+  double gv = lane < nb ? G[(size_t)j * K + k0 + lane] : 0.0;
+  for (int q = 0; q < nb; ++q) {   // x_q = g_q / R_qq, then g_i -= R_qi x_q for i > q
+    const double xq = __shfl_sync(0xffffffffu, gv, q) * rd[q];
+    if (lane == q) gv = xq;
+    else if (lane > q && lane < nb) gv = fma(-r[q][lane], xq, gv);
+  }
+  if (lane < nb) G[(size_t)j * K + k0 + lane] = gv;
 }
 
 __global__ void chol_update_kernel(double* G, int K, int k0) {
@@ -501,11 +513,11 @@ cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t 
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s) {
   for (int k0 = 0; k0 < K; k0 += CB) {
     DPM_COUNT_LAUNCH(1);
-    chol_diag_kernel<<<1, 256, 0, s>>>(G, K, k0, dfail);
+    chol_diag_kernel<<<1, 32, 0, s>>>(G, K, k0, dfail);
     const int rest = K - k0 - std::min(CB, K - k0);
     if (rest > 0) {
       DPM_COUNT_LAUNCH(2);
-      chol_panel_kernel<<<(rest + 127) / 128, 128, 0, s>>>(G, K, k0);
+      chol_panel_kernel<<<(rest + CHOL_PW - 1) / CHOL_PW, 32 * CHOL_PW, 0, s>>>(G, K, k0);
       chol_update_kernel<<<dim3((rest + 15) / 16, (rest + 15) / 16), dim3(16, 16), 0, s>>>(G, K, k0);
     }
   }
