@@ -41,65 +41,64 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+_POLLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+arg = sys.argv[1]
+h = pynvml.nvmlDeviceGetHandleByUUID(arg) if arg.startswith("GPU-") else pynvml.nvmlDeviceGetHandleByIndex(int(arg))
+get = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+while True:
+    print("%.6f,%d,%d,%d" % (time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), mx, int(get(h))), flush=True)
+    time.sleep(0.005)
+"""
+
+
 class ClockSampler:
-    """SM clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md clocks line):
-    NVML polled every 5 ms from a thread (the timed region is ~0.1 s), nvidia-smi -lms 50 as fallback."""
+    """SM clocks and throttle reasons DURING the timed region (B200_PROFILING.md clocks line): an NVML
+    poller subprocess (5 ms, wall-clock stamped; unaffected by the GIL) started before the warm-up;
+    only the samples between mark_start() and mark_end() are summarised."""
 
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
-        self.index = index
+        self.index = str(index)
+        try:   # NVML does not see CUDA_VISIBLE_DEVICES: address the device by its UUID
+            import torch
+            uid = str(torch.cuda.get_device_properties(index).uuid)
+            self.index = uid if uid.startswith("GPU-") else "GPU-" + uid
+        except Exception:
+            pass
         self.proc = None
         self.lines = []
-        self.samples = []          # (sm_mhz, max_mhz, reason bitmask) from NVML
-        self.stop = threading.Event()
-        self.nvml = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.nvml = (pynvml, h)
-            self.t = threading.Thread(target=self._poll, daemon=True)
-            self.t.start()
-            return self
-        except Exception:
-            self.nvml = None
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.proc = subprocess.Popen([sys.executable, "-c", _POLLER, self.index], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 10
+            while not self.lines and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)   # first sample in: the poller is running
         except Exception:
             self.proc = None
         return self
-
-    def _poll(self):
-        nv, h = self.nvml
-        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self.stop.is_set():
-            try:
-                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, int(get_reasons(h))))
-            except Exception:
-                pass
-            self.stop.wait(0.005)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(0.02)   # let the samples of the last few ms arrive
+
     def __exit__(self, *a):
-        self.stop.set()
-        if self.nvml:
-            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -109,30 +108,21 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        if self.nvml:
-            for f, m, bits in self.samples:
-                sm.append(float(f))
-                mx = float(m)
-                for nm in self.NAMES:
-                    if bits & self.BITS[nm]:
-                        reasons.add(nm)
-            src = "nvml 5 ms"
-        else:
-            for ln in self.lines:
-                f = [x.strip() for x in ln.split(",")]
-                if len(f) < 9:
-                    continue
-                try:
-                    sm.append(float(f[1]))
-                    mx = float(f[2])
-                except ValueError:
-                    continue
-                for nm, v in zip(self.NAMES, f[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-            src = "nvidia-smi 50 ms"
+        for ln in list(self.lines):
+            try:
+                ts, f, m, bits = ln.split(",")
+                ts, f, m, bits = float(ts), float(f), float(m), int(bits)
+            except ValueError:
+                continue
+            if self.t0 is not None and not (self.t0 <= ts <= (self.t1 or ts)):
+                continue
+            sm.append(f)
+            mx = m
+            for nm in self.NAMES:
+                if bits & self.BITS[nm]:
+                    reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm), "source": src}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvml poller, 5 ms"}
 
 
 def dist_setup():
@@ -190,7 +180,10 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def bench_pks(api, torch, name, reps=3):
+def bench_pks(api, torch, name, reps=20, hbm_peak=None):
+    """the step loop repeated `reps` times from the same IC (median); setup
+    (create + first BEP build) timed separately; hbm_frac against the ~96 N^3 B of a step (2 solves x 2
+    fields x 16 N^3 + the stencil's reads and writes)."""
     cfg = get_config(name)
     ctx = api.DPM.from_config(cfg)
     n = cfg.n
@@ -210,8 +203,40 @@ def bench_pks(api, torch, name, reps=3):
         torch.cuda.synchronize()
         per.append((time.perf_counter() - t0) / cfg.steps)
     ms = 1e3 * statistics.median(per)
-    return {"steps": cfg.steps, "ms_per_step": ms, "steps_per_s": 1e3 / ms, "setup_ms_incl_bep_build": setup_ms,
-            "rebuilds": sum(l["rebuilt"] for l in logs), "final_mass": logs[-1]["mass"], "rho_max": logs[-1]["rho_max"]}
+    out = {"steps": cfg.steps, "reps": reps, "ms_per_step": ms, "steps_per_s": 1e3 / ms,
+           "setup_ms_incl_bep_build": setup_ms, "rebuilds": sum(l["rebuilt"] for l in logs),
+           "final_mass": logs[-1]["mass"], "rho_max": logs[-1]["rho_max"], "hbm_bytes_per_step": 96 * n ** 3}
+    if hbm_peak:
+        out["hbm_frac"] = 96 * n ** 3 * (1e3 / ms) / (hbm_peak * 1e9)
+    return out
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def fps_reference_rate(cfg, vals, band, workers, nsolves=3):
+    """A CPU fast-Poisson-solver reference analogous to the paper's FFTW3 + OpenMP, SURVEY §8(d):
+    scipy.fft.dstn / idstn (type 1) with `workers` threads and the eigenvalue divide; solves/s.  Timing
+    context only (not the oracle, not the product path)."""
+    import scipy.fft as sf
+    n, h = cfg.n, (cfg.hi - cfg.lo) / (cfg.n + 1)
+    lam = (4.0 / h ** 2) * np.sin(np.arange(1, n + 1) * np.pi / (2 * (n + 1))) ** 2
+    D = 1.0 / cfg.dt + lam[:, None, None] + lam[None, :, None] + lam[None, None, :]
+    q = np.zeros(n ** 3)
+    q[band] = vals[0]
+    q = q.reshape(n, n, n)
+    sf.idstn(sf.dstn(q, type=1, workers=workers) / D, type=1, workers=workers)   # warm-up
+    t0 = time.perf_counter()
+    for _ in range(nsolves):
+        sf.idstn(sf.dstn(q, type=1, workers=workers) / D, type=1, workers=workers)
+    return nsolves / (time.perf_counter() - t0)
 
 
 def bench_cfg1(api, torch, reps=20):
@@ -347,19 +372,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        ctx.aux_solve_batch(q, u)
-    barrier()
-    peaks, peaks_kind = load_peaks()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = L.dpm_launch_count()
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            ctx.aux_solve_batch(q, u)
         barrier()
+        peaks, peaks_kind = load_peaks()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = L.dpm_launch_count()
+        barrier()
+        clk.mark_start()
         ev0.record(stream)
         for _ in range(args.steps):
             ctx.aux_solve_batch(q, u)
         ev1.record(stream)
         barrier()
+        clk.mark_end()
     launches = L.dpm_launch_count() - l0
     ms_local = ev0.elapsed_time(ev1)
     t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
@@ -458,14 +485,28 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import grid
         _, ps = grid.point_sets_for(cfg)
-        rate, secs = oracle_sample_rate(cfg, 3, vals[:3], ps.list("band"))
+        band = ps.list("band")
+        rate, secs = oracle_sample_rate(cfg, 3, vals[:3], band)
         line["cpu_baseline"] = {"value": rate, "unit": "solves/s", "cores": host_cores(), "kind": "oracle",
-                                "sample": "3 of the 578 cfg4 RHS (direct-summation DST, numpy BLAS), %.1f s" % secs}
+                                "sample": "3 of the 578 cfg4 RHS (direct-summation DST, numpy BLAS), %.1f s" % secs,
+                                "model": cpu_model()}
+        try:   # the same oracle on one BLAS thread, and a scipy.fft fast-Poisson reference
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                r1, s1 = oracle_sample_rate(cfg, 1, vals[:1], band)
+            line["cpu_baseline"]["one_core"] = {"value": r1, "sample": "1 RHS, %.1f s" % s1}
+            line["cpu_baseline"]["fps_reference"] = {
+                "what": "scipy.fft dstn/idstn type 1 + eigenvalue divide (the paper's FFTW3 + OpenMP analogue)",
+                "value": fps_reference_rate(cfg, vals, band, host_cores()), "workers": host_cores(),
+                "value_1_worker": fps_reference_rate(cfg, vals, band, 1), "unit": "solves/s"}
+        except Exception as e:   # timing context only
+            line["cpu_baseline"]["extra_error"] = repr(e)
 
     if rank == 0 and world == 1 and not args.no_pks:
         del q, u
         torch.cuda.empty_cache()
-        line["pks"] = {"cfg2": bench_pks(api, torch, "cfg2"), "cfg3": bench_pks(api, torch, "cfg3")}
+        line["pks"] = {"cfg2": bench_pks(api, torch, "cfg2", hbm_peak=hbm_peak),
+                       "cfg3": bench_pks(api, torch, "cfg3", hbm_peak=hbm_peak)}
         line["cfg1"] = bench_cfg1(api, torch)
         line["bep_rebuild_cfg4"] = bench_bep(api, torch)
 
