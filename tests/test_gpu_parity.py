@@ -100,6 +100,31 @@ def test_aux_solve_128_plane_kernels(facr, tmp_path):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("small", ["0", "1"])
+def test_aux_solve_small_n_plane_paths(small):
+    # n <= 64: fused small-n plane kernel (default) and the y / z / y passes (DPM_PLANE_SMALL=0), both
+    # against the oracle in a fresh process (selector read at plan creation), even and odd n, dt extremes
+    import subprocess, sys, os, textwrap
+    code = textwrap.dedent('''
+        import numpy as np, torch
+        from paper_1811_03557_b200 import api
+        from dpm_inputs.rng import random_boxes
+        from oracle import ap
+        for n, dt in ((64, 2e-5), (64, 10.0), (32, 1e-12), (33, 1e-3), (17, 1.0), (4, 1e-3)):
+            c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+            q = random_boxes(n, 3, n)
+            u = c.aux_solve_batch(torch.from_numpy(q).cuda()).cpu().numpy()
+            uo = ap.solve(q, c.info["h"], dt)
+            e = float(np.abs(u - uo).max() / np.abs(uo).max())
+            assert e <= 1e-11, (n, dt, e)
+        print("ok")
+    ''')
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, DPM_PLANE_SMALL=small), cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_aux_solve_inplace_chunked_and_empty(api):
     n = 32
     c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, 2e-4, "cauchy")
