@@ -43,33 +43,34 @@ __global__ void scale_cols_kernel(const double* __restrict__ B, int64_t m, int K
 // (3) trailing update G_ij -= Σ_{k in block} R_ki R_kj for i <= j (2D grid).
 constexpr int CB = 32;
 
-// one warp: unblocked factor of the diagonal block in shared memory (warp barriers only)
+// one warp: unblocked factor of the diagonal block with lane j holding column j in registers
+// (row-k values by shuffle; a short last block is padded with the identity)
 __global__ void chol_diag_kernel(double* G, int K, int k0, int* fail) {
-  __shared__ double a[CB][CB + 1];
-  const int nb = min(CB, K - k0), lane = threadIdx.x;
-  for (int e = lane; e < nb * nb; e += 32) {
-    const int i = e % nb, j = e / nb;
-    a[i][j] = G[(size_t)(k0 + j) * K + k0 + i];
-  }
-  __syncwarp();
-  for (int k = 0; k < nb; ++k) {
-    const double d = a[k][k];
-    const double r = d > 0.0 ? sqrt(d) : 1.0;
-    if (lane == 0 && !(d > 0.0)) *fail = 1;
-    __syncwarp();
-    const int j = lane;   // row k right of the diagonal: a[k][j] /= r
-    if (j > k && j < nb) a[k][j] /= r;
-    if (lane == 0) a[k][k] = r;
-    __syncwarp();
-    if (j > k && j < nb) {   // trailing update, column j (lane): a[i][j] -= a[k][i] a[k][j], k < i <= j
-      const double akj = a[k][j];
-      for (int i = k + 1; i <= j; ++i) a[i][j] -= a[k][i] * akj;
+  const int nb = min(CB, K - k0), j = threadIdx.x;
+  double a[CB];   // a[i] = G(k0 + i, k0 + j), upper part used
+#pragma unroll
+  for (int i = 0; i < CB; ++i)
+    a[i] = (i < nb && j < nb) ? G[(size_t)(k0 + j) * K + k0 + i] : (i == j ? 1.0 : 0.0);
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < CB; ++k) {
+    const double d = __shfl_sync(0xffffffffu, a[k], k);   // a(k, k)
+    bad |= !(d > 0.0);
+    const double r = d > 0.0 ? sqrt(d) : 1.0, ir = 1.0 / r;
+    if (j == k) a[k] = r;
+    else if (j > k) a[k] *= ir;                            // row k right of the diagonal
+    const double akj = a[k];
+#pragma unroll
+    for (int i = k + 1; i < CB; ++i) {                     // a(i, j) -= a(k, i) a(k, j), k < i <= j
+      const double aki = __shfl_sync(0xffffffffu, a[k], i);
+      if (i <= j && j > k) a[i] = fma(-aki, akj, a[i]);
     }
-    __syncwarp();
   }
-  for (int e = lane; e < nb * nb; e += 32) {
-    const int i = e % nb, j = e / nb;
-    G[(size_t)(k0 + j) * K + k0 + i] = (i <= j) ? a[i][j] : 0.0;
+  if (j == 0 && bad) *fail = 1;
+  if (j < nb) {
+#pragma unroll
+    for (int i = 0; i < CB; ++i)
+      if (i < nb) G[(size_t)(k0 + j) * K + k0 + i] = (i <= j) ? a[i] : 0.0;
   }
 }
 
@@ -206,39 +207,6 @@ __global__ void diag_ratio_kernel(const double* R, int K, double* out) {
 }
 
 
-// M = diag(scale) R^{-1} Q^T  (K x m, row-major), Q col-major m x K (so Q^T rows are contiguous).
-// 32x32 output tiles, k-loop over 32-wide panels (R^{-1} upper: panels below the diagonal skipped).
-__global__ void lsq_operator_kernel(const double* __restrict__ Ri, const double* __restrict__ Q, const double* scale,
-                                    int K, int64_t m, double* __restrict__ M) {
-  const int c0 = blockIdx.y * 32;
-  const int64_t i0 = (int64_t)blockIdx.x * 32;
-  __shared__ double sa[32][33], sb[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 256 threads: ty 0..7
-  double acc[4] = {0, 0, 0, 0};
-  for (int k0 = c0 - (c0 % 32); k0 < K; k0 += 32) {
-    for (int q = ty; q < 32; q += 8) {
-      const int c = c0 + q, k = k0 + tx;
-      sa[q][tx] = (c < K && k < K && k >= c) ? Ri[(size_t)k * K + c] : 0.0;   // Ri[c][k]
-      const int kk = k0 + q;
-      const int64_t i = i0 + tx;
-      sb[q][tx] = (kk < K && i < m) ? Q[(size_t)kk * m + i] : 0.0;             // Q^T[kk][i]
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const double b = sb[k][tx];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) acc[u] += sa[ty + 8 * u][k] * b;
-    }
-    __syncthreads();
-  }
-  for (int u = 0; u < 4; ++u) {
-    const int c = c0 + ty + 8 * u;
-    const int64_t i = i0 + tx;
-    if (c < K && i < m) M[(size_t)c * m + i] = scale[c] * acc[u];
-  }
-}
-
 // coef[r][c] = Σ_i M[c][i] g[r][i]: one 128-thread block per row c, all right-hand sides at once
 // (M is read once per apply).
 constexpr int GEMV_R = 4;
@@ -319,6 +287,11 @@ dpm_status chol_qr_pass(dpm_ctx* ctx, const double* A, int64_t m, int K, double*
 
 }  // namespace
 
+template <bool TRANS>
+__global__ void __launch_bounds__(256) gemm_tri_kernel(const double* __restrict__ A, int64_t m, int K,
+                                                        const double* __restrict__ T, const double* __restrict__ scale,
+                                                        double* __restrict__ Cm);
+
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN];
@@ -353,8 +326,8 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   double* Ri = R1;   // R1 is free after the trmm
   DPM_CUDA_TRY(ctx, lsq_rinv(ctx->R, K, Ri, s));
   DPM_COUNT_LAUNCH(1);
-  lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri, ctx->Q, ctx->colscale, K, m,
-                                                                                      ctx->Mlsq);
+  gemm_tri_kernel<true><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(ctx->Q, m, K, Ri, ctx->colscale,
+                                                                                        ctx->Mlsq);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   int hfail = 0;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -377,11 +350,15 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
   return cudaGetLastError();
 }
 
-// C = A T (m x K, column-major, ld m) for A m x K column-major and T K x K column-major upper
-// triangular: 64 x 64 output tiles, 16-deep k panels, 4 x 4 outputs per thread (k panels below the
-// diagonal of T are skipped).  Replaces the row-by-row triangular solve A <- A R^{-1} (T = R^{-1}).
-__global__ void __launch_bounds__(256) gemm_upper_kernel(const double* __restrict__ A, int64_t m, int K,
-                                                          const double* __restrict__ T, double* __restrict__ Cm) {
+// C = A T' (m x K, column-major, ld m) for A m x K column-major and a triangular K x K factor from T
+// (column-major): TRANS = false: T' = T upper (C = A T; replaces the row-by-row solve A <- A R^{-1} with
+// T = R^{-1}); TRANS = true: T' = T^T lower (C = A T^T, so C^T = T A^T: the LSQ operator
+// M = D R^{-1} Q^T stored as its transpose, with the column scale D).  64 x 64 output tiles, 16-deep
+// k panels, 4 x 4 outputs per thread; k panels outside the triangle are skipped.
+template <bool TRANS>
+__global__ void __launch_bounds__(256) gemm_tri_kernel(const double* __restrict__ A, int64_t m, int K,
+                                                        const double* __restrict__ T, const double* __restrict__ scale,
+                                                        double* __restrict__ Cm) {
   const int64_t i0 = (int64_t)blockIdx.x * 64;
   const int j0 = blockIdx.y * 64;
   __shared__ double sA[16][65], sT[16][65];
@@ -391,16 +368,22 @@ __global__ void __launch_bounds__(256) gemm_upper_kernel(const double* __restric
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  const int kend = min(K, j0 + 64);
-  for (int k0 = 0; k0 < kend; k0 += 16) {
+  const int kbeg = TRANS ? j0 - (j0 % 16) : 0, kend = TRANS ? K : min(K, j0 + 64);
+  for (int k0 = kbeg; k0 < kend; k0 += 16) {
     for (int e = threadIdx.x; e < 16 * 64; e += 256) {
       const int r = e & 63, kk = e >> 6;
       const int64_t i = i0 + r;
       const int k = k0 + kk;
       sA[kk][r] = (i < m && k < K) ? A[(size_t)k * m + i] : 0.0;
-      const int kk2 = e & 15, c = e >> 4;
-      const int k2 = k0 + kk2, j = j0 + c;
-      sT[kk2][c] = (k2 < K && j < K && k2 <= j) ? T[(size_t)j * K + k2] : 0.0;
+      if (TRANS) {   // T'(k, j) = T(j, k) for k >= j: consecutive j are consecutive in memory
+        const int c = e & 63, kk2 = e >> 6;
+        const int k2 = k0 + kk2, j = j0 + c;
+        sT[kk2][c] = (k2 < K && j < K && k2 >= j) ? T[(size_t)k2 * K + j] : 0.0;
+      } else {
+        const int kk2 = e & 15, c = e >> 4;
+        const int k2 = k0 + kk2, j = j0 + c;
+        sT[kk2][c] = (k2 < K && j < K && k2 <= j) ? T[(size_t)j * K + k2] : 0.0;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -423,7 +406,7 @@ __global__ void __launch_bounds__(256) gemm_upper_kernel(const double* __restric
     for (int b = 0; b < 4; ++b) {
       const int64_t i = i0 + ty + 16 * a;
       const int j = j0 + tx + 16 * b;
-      if (i < m && j < K) Cm[(size_t)j * m + i] = acc[a][b];
+      if (i < m && j < K) Cm[(size_t)j * m + i] = scale ? scale[j] * acc[a][b] : acc[a][b];
     }
 }
 
@@ -493,7 +476,7 @@ cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, dou
   cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
   if (e != cudaSuccess || m == 0) return e;
   DPM_COUNT_LAUNCH(1);
-  gemm_upper_kernel<<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, Ri_ws, out);
+  gemm_tri_kernel<false><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, Ri_ws, nullptr, out);
   return cudaGetLastError();
 }
 
@@ -544,7 +527,7 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
   cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
   if (e != cudaSuccess || m == 0) return e;
   DPM_COUNT_LAUNCH(1);
-  lsq_operator_kernel<<<dim3((unsigned)((m + 31) / 32), (K + 31) / 32), 256, 0, s>>>(Ri_ws, Q, scale, K, m, M);
+  gemm_tri_kernel<true><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(Q, m, K, Ri_ws, scale, M);
   return cudaGetLastError();
 }
 
