@@ -228,6 +228,12 @@ dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, doubl
 /* Cholesky of the summed Gram (pass 1: R1, Q1 <- Q1 R1^{-1}; pass 2: R2, Q <- Q1 R2^{-1},
    R = R2 R1, M_s = D R^{-1} Q^T).  Synchronous; DPM_ERR_RANK on breakdown. */
 dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* stream);
+/* The same pass for another octant of the SAME device and K whose dpm_dd_chol(pass) with the same
+   G_sum has completed (src): copies the K x K factors and their inverses from src instead of
+   refactoring, then forms this octant's Q (and, pass 2, M_s).  Asynchronous on stream.
+   DPM_ERR_INVALID for a src on another device / with another K; DPM_ERR_STATE (pass 2) if src has
+   no projection. */
+dpm_status dpm_dd_chol_copy(dpm_ctx* ctx, int32_t pass, const dpm_ctx* src, void* stream);
 /* R31 initial state (rho, c on N+, [n][n][n]). */
 dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream);
 /* Local CFL bound h / (6 χ max|Δc|/h) (R19) -> *cfl_dt (HOST).  Synchronous; with

@@ -248,6 +248,10 @@ class Octant(DPM):
     def chol(self, pass_, G_sum, stream=None):
         self._chk(L.lib.dpm_dd_chol(self._h, pass_, _ptr(_dev_f64(G_sum, "G_sum")), _stream(stream)))
 
+    def chol_copy(self, pass_, src: "Octant", stream=None):
+        """The same CholeskyQR pass from `src` (same device, same summed Gram, already factored)."""
+        self._chk(L.lib.dpm_dd_chol_copy(self._h, pass_, src._h, _stream(stream)))
+
     def dd_pks_init(self, rho, c, center, rho_amp, rho_rate, c_amp, c_rate, stream=None):
         ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate)
         self._chk(L.lib.dpm_dd_pks_init(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), C.byref(ic),

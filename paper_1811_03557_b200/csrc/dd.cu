@@ -262,7 +262,7 @@ dpm_status dd_alloc(dpm_ctx* ctx) {
   if (!ctx->dd_B) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_B, K * m * sizeof(double)));
   if (!ctx->dd_Q) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_Q, K * m * sizeof(double)));
   if (!ctx->dd_M) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_M, K * m * sizeof(double)));
-  if (!ctx->dd_R) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_R, 4 * K * K * sizeof(double) + 64));
+  if (!ctx->dd_R) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_R, 5 * K * K * sizeof(double) + 64));   // R1 R2 R W W2 fail
   if (!ctx->dd_D) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_D, K * sizeof(double)));
   if (!ctx->dd_g) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_g, 2 * m * sizeof(double)));
   return DPM_OK;
@@ -381,6 +381,7 @@ dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, doubl
   return DPM_OK;
 }
 
+// dd_R layout: R1 | R2 | R = R2 R1 | W = Rp^{-1} of the last pass | W2 = R^{-1} | fail flag
 dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* stream) {
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
@@ -391,23 +392,58 @@ dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* st
   double* R2 = R1 + K * K;
   double* R = R2 + K * K;
   double* W = R + K * K;
-  int* dfail = reinterpret_cast<int*>(W + K * K);
+  double* W2 = W + K * K;
+  int* dfail = reinterpret_cast<int*>(W2 + K * K);
   double* Rp = pass == 1 ? R1 : R2;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(Rp, G_sum, K * K * 8, cudaMemcpyDeviceToDevice, s));
   DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), s));
   DPM_CUDA_TRY(ctx, lsq_cholesky(Rp, (int)K, dfail, s));
-  // Q <- Q Rp^{-1} as a tiled GEMM with the explicit triangular inverse (into dd_M, then swap)
-  DPM_CUDA_TRY(ctx, lsq_mul_rinv(ctx->dd_Q, ctx->n_rows, (int)K, Rp, W, ctx->dd_M, s));
+  // Q <- Q Rp^{-1}: explicit triangular inverse W, then a tiled GEMM (into dd_M, then swap)
+  DPM_CUDA_TRY(ctx, lsq_rinv(Rp, (int)K, W, s));
+  DPM_CUDA_TRY(ctx, lsq_mul_upper(ctx->dd_Q, ctx->n_rows, (int)K, W, ctx->dd_M, s));
   std::swap(ctx->dd_Q, ctx->dd_M);
   if (pass == 2) {
     DPM_CUDA_TRY(ctx, lsq_trmm(R2, R1, R, (int)K, s));
-    DPM_CUDA_TRY(ctx, lsq_build_operator(R, ctx->dd_Q, ctx->n_rows, (int)K, ctx->dd_D, ctx->dd_M, W, s));
+    DPM_CUDA_TRY(ctx, lsq_rinv(R, (int)K, W2, s));
+    DPM_CUDA_TRY(ctx, lsq_operator_from_rinv(W2, ctx->dd_Q, ctx->n_rows, (int)K, ctx->dd_D, ctx->dd_M, s));
   }
   int hfail = 0;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
   DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
   if (hfail) { ctx->err = "octant DD: CholeskyQR2 breakdown (stacked BEP rank deficient)"; return DPM_ERR_RANK; }
   if (pass == 2) ctx->have_projection = 1;
+  return DPM_OK;
+}
+
+// The same pass from an octant already factored with the same summed Gram on this device: the
+// K x K factors and inverses are copied, only the octant's own GEMMs run.
+dpm_status dpm_dd_chol_copy(dpm_ctx* ctx, int32_t pass, const dpm_ctx* src, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!src || !src->dd || !src->dd_R || src->K != ctx->K || src->device != ctx->device || (pass != 1 && pass != 2))
+    return DPM_ERR_INVALID;
+  if (pass == 2 && !src->have_projection) { ctx->err = "dd_chol_copy: source not factored"; return DPM_ERR_STATE; }
+  cudaStream_t s = as_stream(stream);
+  const size_t K = ctx->K, KK = K * K * 8;
+  double* R1 = ctx->dd_R;
+  double* R2 = R1 + K * K;
+  double* R = R2 + K * K;
+  double* W = R + K * K;
+  double* W2 = W + K * K;
+  const double* sR1 = src->dd_R;
+  if (pass == 1) {
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(R1, sR1, KK, cudaMemcpyDeviceToDevice, s));
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(W, sR1 + 3 * K * K, KK, cudaMemcpyDeviceToDevice, s));
+  } else {   // R2, R, W = R2^{-1}, W2 = R^{-1}
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(R2, sR1 + K * K, 4 * KK, cudaMemcpyDeviceToDevice, s));
+  }
+  DPM_CUDA_TRY(ctx, lsq_mul_upper(ctx->dd_Q, ctx->n_rows, (int)K, W, ctx->dd_M, s));
+  std::swap(ctx->dd_Q, ctx->dd_M);
+  if (pass == 2) {
+    DPM_CUDA_TRY(ctx, lsq_operator_from_rinv(W2, ctx->dd_Q, ctx->n_rows, (int)K, ctx->dd_D, ctx->dd_M, s));
+    ctx->have_projection = 1;
+  }
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
   return DPM_OK;
 }
 

@@ -192,6 +192,9 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
 // lsq.cu building blocks (octant DD)
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s);
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s);
+cudaError_t lsq_mul_upper(const double* A, int64_t m, int K, const double* T, double* out, cudaStream_t s);
+cudaError_t lsq_operator_from_rinv(const double* Ri, const double* Q, int64_t m, int K, const double* scale, double* M,
+                                   cudaStream_t s);
 // R^{-1} of an upper-triangular K x K R (col-major), blocked by 32 x 32 tiles
 cudaError_t lsq_rinv(const double* R, int K, double* Ri, cudaStream_t s);
 cudaError_t lsq_trmm(const double* A, const double* B, double* C, int K, cudaStream_t s);

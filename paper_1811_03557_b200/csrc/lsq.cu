@@ -480,6 +480,23 @@ cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, dou
   return cudaGetLastError();
 }
 
+// out = A T with T = an already inverted upper-triangular factor (tiled GEMM; out != A)
+cudaError_t lsq_mul_upper(const double* A, int64_t m, int K, const double* T, double* out, cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  DPM_COUNT_LAUNCH(1);
+  gemm_tri_kernel<false><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, T, nullptr, out);
+  return cudaGetLastError();
+}
+
+// M = diag(scale) Ri Q^T (stored K x m row-major) from an already inverted Ri = R^{-1}
+cudaError_t lsq_operator_from_rinv(const double* Ri, const double* Q, int64_t m, int K, const double* scale, double* M,
+                                   cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  DPM_COUNT_LAUNCH(1);
+  gemm_tri_kernel<true><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(Q, m, K, Ri, scale, M);
+  return cudaGetLastError();
+}
+
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(G, 0, (size_t)K * K * sizeof(double), s);
   if (e != cudaSuccess) return e;

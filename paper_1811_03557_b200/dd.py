@@ -48,13 +48,22 @@ class DDSolver:
             o.bep_block()
         n2 = self._sum([o.colnorm2() for o in self.octs])
         G1 = self._sum([o.gram(1, n2) for o in self.octs])
-        for o in self.octs:
-            o.chol(1, G1)
+        self._chol(1, G1)
         G2 = self._sum([o.gram(2) for o in self.octs])
-        for o in self.octs:
-            o.chol(2, G2)
+        self._chol(2, G2)
         self.dt_bep = dt
         self.builds += 1
+
+    def _chol(self, pass_, G):
+        # every octant of this rank factors the same summed Gram: once per device, copied to the rest
+        first = {}
+        for o in self.octs:
+            src = first.get(str(o.device))
+            if src is None:
+                o.chol(pass_, G)
+                first[str(o.device)] = o
+            else:
+                o.chol_copy(pass_, src)
 
     def init(self, center, rho_ic, c_ic):
         self.fields = []

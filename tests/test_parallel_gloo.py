@@ -102,6 +102,10 @@ class _FakeOctant:
     def chol(self, p, G):
         self.seen[f"G{p}"] = G.clone()
 
+    def chol_copy(self, p, src):
+        self.seen[f"G{p}"] = src.seen[f"G{p}"].clone()
+        self.seen[f"copy{p}"] = src.s
+
     def dd_pks_init(self, rho, c, *a):
         rho.fill_(1.0)
         c.fill_(float(self.s))
@@ -132,6 +136,9 @@ def _dd_worker(rank, world, port, q):
     sol = DDSolver(octs, dt_cap=1.0)
     sol.init((0, 0, 0), (1, 1), (1, 1))
     log = sol.step()
+    # one factorisation per device: the rank's other octants copy it from the first
+    assert all(o.seen.get("copy1") == octs[0].s and o.seen.get("copy2") == octs[0].s for o in octs[1:])
+    assert "copy1" not in octs[0].seen
     q.put((rank, log["dt"], log["mass"], octs[0].seen["n2"].numpy(), octs[0].seen["G2"].numpy(),
            octs[0].seen["C"].numpy()))
     dist.destroy_process_group()
