@@ -110,6 +110,112 @@ __global__ void dd_extension_kernel(const int64_t* gamma, int64_t ng, int n, dou
   }
 }
 
+// u_γ[r][g] = Σ_c A[g][c] C[r][c] (r = 0, 1; optionally clamped at 0, R17) with the basis evaluated
+// on the fly instead of streaming the n_gamma x K matrix A (~0.6 GB per octant at n = 128) every
+// step: per γ point the piece weights (assignment bits), the real SH of the cap block and the
+// Legendre products of the plane blocks, exactly as dd_extension_kernel builds A (the SH recursion
+// coefficients come from shared-memory tables computed with the same expressions: identical values),
+// contracted with the two coefficient vectors held in shared memory.  Pieces of weight 0 are skipped.
+__global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __restrict__ gamma, int64_t ng, int n,
+                                                            double lo, double h, double radius, double sx, double sy,
+                                                            double sz, int Lc, int Li, int nphi, int K,
+                                                            const uint8_t* __restrict__ assign,
+                                                            const double* __restrict__ C, int clamp, double* ug) {
+  extern __shared__ double fly_sm[];
+  double* c0v = fly_sm;                        // [K]
+  double* c1v = c0v + K;                       // [K]
+  const int L1 = Lc + 1;
+  double* ta = c1v + K;                        // [L1][L1]: a_lm
+  double* tb = ta + L1 * L1;                   // [L1][L1]: b_lm
+  double* tpm = tb + L1 * L1;                  // [L1]: sqrt((2m+1)/(2m))
+  double* tz = tpm + L1;                       // [L1]: sqrt(2m+3)
+  for (int i = threadIdx.x; i < K; i += blockDim.x) {
+    c0v[i] = C[i];
+    c1v[i] = C[K + i];
+  }
+  for (int e = threadIdx.x; e < L1 * L1; e += blockDim.x) {
+    const int l = e / L1, m = e % L1;
+    ta[e] = (l >= m + 2) ? sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m)) : 0.0;
+    tb[e] = (l >= m + 2) ? sqrt(((l - 1.0) * (l - 1.0) - (double)m * m) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0)) : 0.0;
+  }
+  for (int m = threadIdx.x; m < L1; m += blockDim.x) {
+    tpm[m] = m > 0 ? sqrt((2.0 * m + 1.0) / (2.0 * m)) : 1.0;
+    tz[m] = sqrt(2.0 * m + 3.0);
+  }
+  __syncthreads();
+  const int nc = L1 * L1;
+  const double sg[3] = {sx, sy, sz};
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pidx = gamma[g];
+    const int i = (int)(pidx / ((long)n * n)), j = (int)((pidx / n) % n), k = (int)(pidx % n);
+    const double P[3] = {lo + (i + 1) * h, lo + (j + 1) * h, lo + (k + 1) * h};
+    double X[3];
+    for (int a = 0; a < 3; ++a) X[a] = sg[a] * P[a];
+    const double r = sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]);
+    const int bits = assign[g];
+    const int cnt = __popc(bits);
+    const double inv = cnt ? 1.0 / cnt : 0.0;
+    double s0 = 0.0, s1 = 0.0;
+    if (bits & 1) {   // cap: Y(x/|x|), (d^2/2) Y
+      const double x = X[0] / r, y = X[1] / r, z = X[2] / r;
+      const double dcap = r - radius, wc = 0.5 * dcap * dcap;
+      double t0 = 0.0, t1 = 0.0;
+      double pmm = 0.28209479177387814347, Cm = 1.0, Sm = 0.0;
+      for (int m = 0; m <= Lc; ++m) {
+        if (m > 0) {
+          pmm *= tpm[m];
+          const double Cn = x * Cm - y * Sm, Sn = x * Sm + y * Cm;
+          Cm = Cn;
+          Sm = Sn;
+        }
+        double p2 = 0.0, p1 = pmm;
+        for (int l = m; l <= Lc; ++l) {
+          double pl;
+          if (l == m) pl = pmm;
+          else if (l == m + 1) pl = z * tz[m] * pmm;
+          else pl = ta[l * L1 + m] * (z * p1 - tb[l * L1 + m] * p2);
+          if (l > m) { p2 = p1; p1 = pl; }
+          if (m == 0) {
+            const int nu = l * l + l;
+            t0 = fma(pl, fma(wc, c0v[nc + nu], c0v[nu]), t0);
+            t1 = fma(pl, fma(wc, c1v[nc + nu], c1v[nu]), t1);
+          } else {
+            const double vc = 1.41421356237309504880 * pl * Cm, vs = 1.41421356237309504880 * pl * Sm;
+            const int nup = l * l + l + m, nun = l * l + l - m;
+            t0 = fma(vc, fma(wc, c0v[nc + nup], c0v[nup]), t0);
+            t1 = fma(vc, fma(wc, c1v[nc + nup], c1v[nup]), t1);
+            t0 = fma(vs, fma(wc, c0v[nc + nun], c0v[nun]), t0);
+            t1 = fma(vs, fma(wc, c1v[nc + nun], c1v[nun]), t1);
+          }
+        }
+      }
+      s0 = fma(inv, t0, s0);
+      s1 = fma(inv, t1, s1);
+    }
+    for (int a = 0; a < 3; ++a) {   // planes: φ_jk = P_j P_k of the in-plane coordinates, {φ, d φ}
+      if (!(bits & (2 << a))) continue;
+      const int o0 = a == 0 ? 1 : 0, o1 = a == 2 ? 1 : 2;
+      double Ps[32], Pt[32];
+      legendre_all(X[o0], Li, Ps);
+      legendre_all(X[o1], Li, Pt);
+      const double d = X[a];
+      const int cb = 2 * nc + 2 * nphi * a;
+      double t0 = 0.0, t1 = 0.0;
+      int m = 0;
+      for (int gd = 0; gd <= Li; ++gd)
+        for (int jj = gd; jj >= 0; --jj, ++m) {
+          const double phi = Ps[jj] * Pt[gd - jj];
+          t0 = fma(phi, fma(d, c0v[cb + nphi + m], c0v[cb + m]), t0);
+          t1 = fma(phi, fma(d, c1v[cb + nphi + m], c1v[cb + m]), t1);
+        }
+      s0 = fma(inv, t0, s0);
+      s1 = fma(inv, t1, s1);
+    }
+    ug[g] = clamp ? fmax(s0, 0.0) : s0;
+    ug[ng + g] = clamp ? fmax(s1, 0.0) : s1;
+  }
+}
+
 // B[i][c] = [c in block(piece_i)] Eraw[pos_i][c] - U_c[gamma[pos_i]]  (column-major n_rows x nc)
 __global__ void dd_bep_gather_kernel(const double* __restrict__ U, int ncols, size_t field,
                                      const int64_t* __restrict__ gamma, int64_t ng, const int32_t* __restrict__ rows,
@@ -523,7 +629,16 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
   double* wk = fq + 2 * field;
   if (!ctx->dd_ug) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_ug, (size_t)2 * ng * sizeof(double) + 64));
   double* ug = ctx->dd_ug;
-  DPM_CUDA_TRY(ctx, lsq_extend(ctx->E, ng, ctx->K, C, 2, clamp, ug, s));                   // u_γ = A C (R17)
+  {   // u_γ = A C (R17), the basis evaluated on the fly (dd_extend_fly_kernel)
+    const int L1 = ctx->Lc + 1;
+    const size_t smem = (2 * (size_t)ctx->K + 2 * L1 * L1 + 2 * L1) * sizeof(double);
+    DPM_CUDA_TRY(ctx, cudaFuncSetAttribute(dd_extend_fly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DPM_COUNT_LAUNCH(1);
+    dd_extend_fly_kernel<<<(unsigned)std::min<int64_t>((ng + 127) / 128, 148 * 8), 128, smem, s>>>(
+        ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1],
+        ctx->sigma[2], ctx->Lc, ctx->Li, ctx->nphi, ctx->K, ctx->dd_assign, C, clamp, ug);
+    DPM_CUDA_TRY(ctx, cudaGetLastError());
+  }
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));                                // R20
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
   DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));

@@ -207,40 +207,62 @@ __global__ void diag_ratio_kernel(const double* R, int K, double* out) {
 }
 
 
-// coef[r][c] = Σ_i M[c][i] g[r][i]: one 128-thread block per row c, all right-hand sides at once
-// (M is read once per apply).
-constexpr int GEMV_R = 4;
-constexpr int GEMV_T = 512;   // threads per row: 16 warps of loads in flight per row block
-__global__ void lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K, const double* __restrict__ g, int nrhs,
-                                double* __restrict__ coef) {
-  const int c = blockIdx.x;
-  const double* a = M + (size_t)c * m;
-  __shared__ double red[GEMV_R][GEMV_T / 32];
-  for (int r0 = 0; r0 < nrhs; r0 += GEMV_R) {
-    const int nr = min(GEMV_R, nrhs - r0);
-    double s[GEMV_R] = {0, 0, 0, 0};
-#pragma unroll 8
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {   // unrolled: 8 rows of loads in flight
-      const double av = __ldg(a + i);
+// coef[r][c] = Σ_i M[c][i] g[r][i]: a 256-thread block per GEMV_ROWS rows of M, right-hand sides 2 at
+// a time (each g element loaded once per GEMV_ROWS rows); 4 rows when that still gives >= 148 blocks
+// (the DD / cfg4 operators), else 1 (small K: parallelism over rows matters more)
+constexpr int GEMV_RC = 2, GEMV_T = 256;
+template <int GEMV_ROWS>
+__global__ void __launch_bounds__(GEMV_T) lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K,
+                                                          const double* __restrict__ g, int nrhs,
+                                                          double* __restrict__ coef) {
+  const int c0 = blockIdx.x * GEMV_ROWS;
+  __shared__ double red[GEMV_ROWS * GEMV_RC][GEMV_T / 32];
+  const double* a[GEMV_ROWS];
 #pragma unroll
-      for (int q = 0; q < GEMV_R; ++q)
-        if (q < nr) s[q] = fma(av, __ldg(g + (size_t)(r0 + q) * m + i), s[q]);
+  for (int q = 0; q < GEMV_ROWS; ++q) a[q] = M + (size_t)min(c0 + q, K - 1) * m;
+  for (int r0 = 0; r0 < nrhs; r0 += GEMV_RC) {
+    const int nr = min(GEMV_RC, nrhs - r0);
+    const double* g0 = g + (size_t)r0 * m;
+    const double* g1 = g + (size_t)(r0 + (nr > 1 ? 1 : 0)) * m;
+    double acc[GEMV_ROWS][GEMV_RC];
+#pragma unroll
+    for (int q = 0; q < GEMV_ROWS; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < m; i += GEMV_T) {
+      const double x0 = __ldg(g0 + i), x1 = __ldg(g1 + i);
+#pragma unroll
+      for (int q = 0; q < GEMV_ROWS; ++q) {
+        const double av = __ldg(a[q] + i);
+        acc[q][0] = fma(av, x0, acc[q][0]);
+        acc[q][1] = fma(av, x1, acc[q][1]);
+      }
     }
 #pragma unroll
-    for (int q = 0; q < GEMV_R; ++q) {
-      for (int o = 16; o; o >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
-      if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = s[q];
-    }
+    for (int q = 0; q < GEMV_ROWS; ++q)
+#pragma unroll
+      for (int r = 0; r < GEMV_RC; ++r) {
+        double v = acc[q][r];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[q * GEMV_RC + r][threadIdx.x >> 5] = v;
+      }
     __syncthreads();
-    if (threadIdx.x < nr) {
-      const int q = threadIdx.x;
+    if (threadIdx.x < GEMV_ROWS * GEMV_RC) {
+      const int q = threadIdx.x / GEMV_RC, r = threadIdx.x % GEMV_RC;
       double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < GEMV_T / 32; ++w) v += red[q][w];
-      coef[(size_t)(r0 + q) * K + c] = v;
+      for (int w = 0; w < GEMV_T / 32; ++w) v += red[threadIdx.x][w];
+      if (c0 + q < K && r < nr) coef[(size_t)(r0 + r) * K + c0 + q] = v;
     }
     __syncthreads();
   }
+}
+
+void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
+  DPM_COUNT_LAUNCH(1);
+  if (K >= 4 * 148)
+    lsq_gemv_kernel<4><<<(K + 3) / 4, GEMV_T, 0, s>>>(M, m, K, g, nrhs, coef);
+  else
+    lsq_gemv_kernel<1><<<K, GEMV_T, 0, s>>>(M, m, K, g, nrhs, coef);
 }
 
 // u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
@@ -344,8 +366,7 @@ cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gam
                       cudaStream_t s) {
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN], ng = ctx->counts[DPM_SET_GAMMA];
-  DPM_COUNT_LAUNCH(1);
-  lsq_gemv_kernel<<<K, GEMV_T, 0, s>>>(ctx->Mlsq, m, K, g, nrhs, coef);
+  launch_gemv(ctx->Mlsq, m, K, g, nrhs, coef, s);
   if (u_gamma) return lsq_extend(ctx->E, ng, K, coef, nrhs, clamp, u_gamma, s);
   return cudaGetLastError();
 }
@@ -549,8 +570,7 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
 }
 
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
-  DPM_COUNT_LAUNCH(1);
-  lsq_gemv_kernel<<<K, GEMV_T, 0, s>>>(M, m, K, g, nrhs, coef);
+  launch_gemv(M, m, K, g, nrhs, coef, s);
   return cudaGetLastError();
 }
 
