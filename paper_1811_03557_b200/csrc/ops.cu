@@ -8,6 +8,9 @@
 namespace {
 
 constexpr int TB = 256;
+#ifndef STENCIL_MINB
+#define STENCIL_MINB 4   // stencil kernels: <= 64 registers, 32 warps per SM (latency-bound gathers)
+#endif
 
 __device__ __forceinline__ void ijk(long p, int n, int& i, int& j, int& k) {
   i = (int)(p / ((long)n * n));
@@ -138,7 +141,7 @@ __device__ __forceinline__ void umax_atomic(double* addr, double v) {
   atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
 }
 
-__global__ void cfl_kernel(const double* __restrict__ c, const uint8_t* __restrict__ flags, int n, double* out3) {
+__global__ void __launch_bounds__(TB, STENCIL_MINB) cfl_kernel(const double* __restrict__ c, const uint8_t* __restrict__ flags, int n, double* out3) {
   __shared__ double red[3][TB / 32];
   double mx[3] = {0, 0, 0};
   const long nn = (long)n * n * n;
@@ -167,7 +170,7 @@ __global__ void cfl_kernel(const double* __restrict__ c, const uint8_t* __restri
 
 // g and the IMEX right-hand sides, written scaled for the ABI operator:
 // fq_rho = (rho - dt g)/dt, fq_c = ((1-dt) c + dt rho)/dt on M+, 0 elsewhere.
-__global__ void flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
+__global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
                                 const uint8_t* __restrict__ flags, int n, double h, double dt, double chi,
                                 double* __restrict__ fq_rho, double* __restrict__ fq_c) {
   const long nn = (long)n * n * n;
@@ -199,7 +202,7 @@ __global__ void flux_rhs_kernel(const double* __restrict__ rho, const double* __
 }
 
 // combined Green RHS (R20): q_r = fq_r on M+, (I/dt - Δ_h)[u_γ,r] on the band, 0 elsewhere
-__global__ void green_rhs_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap, int n,
+__global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap, int n,
                                  const double* __restrict__ fq, const double* __restrict__ ug, int64_t ng, double* q,
                                  int nrhs, double diag, double off) {
   const long nn = (long)n * n * n;
@@ -219,7 +222,7 @@ __global__ void green_rhs_kernel(const uint8_t* __restrict__ flags, const int32_
 }
 
 // restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite]
-__global__ void restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
+__global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
                                 double* c, double* stats) {
   const long nn = (long)n * n * n;
   double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY;
