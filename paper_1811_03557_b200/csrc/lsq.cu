@@ -210,8 +210,8 @@ __global__ void diag_ratio_kernel(const double* R, int K, double* out) {
 // coef[r][c] = Σ_i M[c][i] g[r][i]: a 256-thread block per GEMV_ROWS rows of M, right-hand sides 2 at
 // a time (each g element loaded once per GEMV_ROWS rows); 4 rows when that still gives >= 148 blocks
 // (the DD / cfg4 operators), else 1 (small K: parallelism over rows matters more)
-constexpr int GEMV_RC = 2, GEMV_T = 256;
-template <int GEMV_ROWS>
+constexpr int GEMV_RC = 2;
+template <int GEMV_ROWS, int GEMV_T>
 __global__ void __launch_bounds__(GEMV_T) lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K,
                                                           const double* __restrict__ g, int nrhs,
                                                           double* __restrict__ coef) {
@@ -260,9 +260,9 @@ __global__ void __launch_bounds__(GEMV_T) lsq_gemv_kernel(const double* __restri
 void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
   if (K >= 4 * 148)
-    lsq_gemv_kernel<4><<<(K + 3) / 4, GEMV_T, 0, s>>>(M, m, K, g, nrhs, coef);
+    lsq_gemv_kernel<4, 512><<<(K + 3) / 4, 512, 0, s>>>(M, m, K, g, nrhs, coef);
   else
-    lsq_gemv_kernel<1><<<K, GEMV_T, 0, s>>>(M, m, K, g, nrhs, coef);
+    lsq_gemv_kernel<1, 256><<<K, 256, 0, s>>>(M, m, K, g, nrhs, coef);
 }
 
 // u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
