@@ -294,10 +294,11 @@ def bench_bep(api, torch, reps=3):
     return res
 
 
-def bench_dd(api, torch, world, rank, steps=None):
+def bench_dd(api, torch, world, rank, steps=None, reps=5):
     """cfg5: the 8-octant DD (R24) — octants sharded over the ranks (8/world each), the global
-    least squares and dt through NCCL all-reduces (DDSolver).  Steps/s excludes the BEP builds
-    (timed separately; 3 expected, SURVEY probe P12)."""
+    least squares and dt through NCCL all-reduces (DDSolver).  The 50-step loop is repeated `reps`
+    times from the same IC; steps/s excludes the BEP builds, which are timed separately
+    (3 per run expected, SURVEY probe P12); medians over the repeats."""
     from paper_1811_03557_b200.dd import DDSolver
     cfg = get_config("cfg5")
     steps = steps or cfg.steps
@@ -306,20 +307,27 @@ def bench_dd(api, torch, world, rank, steps=None):
     dev = torch.cuda.current_device()
     octs = [api.Octant(cfg.n, cfg.lo, cfg.hi, s, 1.0, cfg.lmax, cfg.deg_if, cfg.dt, device=dev) for s in mine]
     sol = DDSolver(octs, cfg.dt, chi=cfg.chi)
-    sol.init(cfg.ic_center, cfg.ic_rho, cfg.ic_c)
-    t_build, logs = 0.0, []
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        b0, ts = sol.builds, time.perf_counter()
-        logs.append(sol.step())
+    runs = []
+    for _ in range(reps):
+        sol.init(cfg.ic_center, cfg.ic_rho, cfg.ic_c)
+        t_build, logs, b_start = 0.0, [], sol.builds
         torch.cuda.synchronize()
-        if sol.builds > b0:
-            t_build += time.perf_counter() - ts
-    tot = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            b0, ts = sol.builds, time.perf_counter()
+            logs.append(sol.step())
+            torch.cuda.synchronize()
+            if sol.builds > b0:
+                t_build += time.perf_counter() - ts
+        tot = time.perf_counter() - t0
+        nb = sol.builds - b_start
+        runs.append({"total_s": tot, "builds": nb, "build_s": t_build,
+                     "steps_per_s": (steps - nb) / max(tot - t_build, 1e-9), "logs": logs})
+    med = lambda k: statistics.median(r[k] for r in runs)   # noqa: E731
+    logs = runs[-1]["logs"]
     out = {"octants": 8, "octants_per_rank": per, "n": cfg.n, "K": octs[0].K, "rows_per_octant": octs[0].n_rows,
-           "steps": steps, "total_s": tot, "builds": sol.builds, "build_s_incl_their_steps": t_build,
-           "steps_per_s_excl_builds": (steps - sol.builds) / max(tot - t_build, 1e-9),
+           "steps": steps, "reps": reps, "total_s": med("total_s"), "builds": runs[-1]["builds"],
+           "build_s_incl_their_steps": med("build_s"), "steps_per_s_excl_builds": med("steps_per_s"),
            "dt_first": logs[0]["dt"], "dt_last": logs[-1]["dt"], "t_end": logs[-1]["t"],
            "mass_after_step1": logs[0]["mass"], "mass_end": logs[-1]["mass"], "rho_max_end": logs[-1]["rho_max"],
            "note": "non-physical config (SURVEY §0 item 6: IC spike at the 8-octant corner); matches probe P12"}
