@@ -250,6 +250,21 @@ dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, 
 dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, double* rho, double* c,
                                double* stats, void* stream);
 dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream);
+/* The same step in phases over CALLER-OWNED 2-field buffers ([2][n][n][n] fp64, DEVICE), so that a
+   rank runs each of the step's two AP solves for all its octants as one dpm_aux_solve_batch (the AP
+   operator depends only on n, h, dt, which the octants share):
+     dpm_dd_local_begin  = dpm_dd_rhs -> dpm_aux_solve_batch(fq -> wk) -> dpm_dd_lsq_rhs
+     dpm_dd_local_finish = dpm_dd_green_rhs -> dpm_aux_solve_batch(wk, in place) -> dpm_dd_restrict
+   dpm_dd_rhs: fq = the scaled IMEX RHS of Step 4a (R15, R16); DPM_ERR_STATE without a
+   factorisation at the ctx's dt.  dpm_dd_lsq_rhs: BEP rows of the AP solutions wk, y = M_s g_s (K x 2).
+   dpm_dd_green_rhs: u_γ = A C (clamped if clamp, R17), Green RHS from fq and u_γ into wk (R20).
+   dpm_dd_restrict: restriction of the Green solutions wk to N+ into rho, c with the step statistics
+   (read by dpm_dd_stats).  All asynchronous on stream. */
+dpm_status dpm_dd_rhs(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* fq, void* stream);
+dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* stream);
+dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const double* fq, double* wk,
+                            void* stream);
+dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* c, void* stream);
 
 /* Cumulative number of CUDA kernels this library has launched in the process (all
    contexts).  Lets a harness count the library's launches inside a timed region. */

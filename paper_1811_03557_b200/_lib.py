@@ -88,6 +88,10 @@ _sig = {
     "dpm_dd_gram": ([P, C.c_int32, P, P, P], C.c_int),
     "dpm_dd_chol": ([P, C.c_int32, P, P], C.c_int),
     "dpm_dd_chol_copy": ([P, C.c_int32, P, P], C.c_int),
+    "dpm_dd_rhs": ([P, P, P, C.c_double, P, P], C.c_int),
+    "dpm_dd_lsq_rhs": ([P, P, P, P], C.c_int),
+    "dpm_dd_green_rhs": ([P, P, C.c_int32, P, P, P], C.c_int),
+    "dpm_dd_restrict": ([P, P, P, P, P], C.c_int),
     "dpm_dd_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
     "dpm_dd_cfl": ([P, P, C.c_double, D, P], C.c_int),
     "dpm_dd_cfl_result": ([P, C.c_double, D, P], C.c_int),

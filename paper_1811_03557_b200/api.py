@@ -248,6 +248,25 @@ class Octant(DPM):
     def chol(self, pass_, G_sum, stream=None):
         self._chk(L.lib.dpm_dd_chol(self._h, pass_, _ptr(_dev_f64(G_sum, "G_sum")), _stream(stream)))
 
+    # phase-level step (batched AP solves across octants; see include/dpm.h)
+    def dd_rhs(self, rho, c, chi, fq, stream=None):
+        self._chk(L.lib.dpm_dd_rhs(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), chi,
+                                   _ptr(_dev_f64(fq, "fq")), _stream(stream)))
+
+    def dd_lsq_rhs(self, wk, stream=None):
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            y = self._t(2, self.K)
+        self._chk(L.lib.dpm_dd_lsq_rhs(self._h, _ptr(_dev_f64(wk, "wk")), _ptr(y), _stream(stream)))
+        return y
+
+    def dd_green_rhs(self, C, clamp, fq, wk, stream=None):
+        self._chk(L.lib.dpm_dd_green_rhs(self._h, _ptr(_dev_f64(C, "C")), clamp, _ptr(_dev_f64(fq, "fq")),
+                                         _ptr(_dev_f64(wk, "wk")), _stream(stream)))
+
+    def dd_restrict(self, wk, rho, c, stream=None):
+        self._chk(L.lib.dpm_dd_restrict(self._h, _ptr(_dev_f64(wk, "wk")), _ptr(_dev_f64(rho, "rho")),
+                                        _ptr(_dev_f64(c, "c")), _stream(stream)))
+
     def chol_copy(self, pass_, src: "Octant", stream=None):
         """The same CholeskyQR pass from `src` (same device, same summed Gram, already factored)."""
         self._chk(L.lib.dpm_dd_chol_copy(self._h, pass_, src._h, _stream(stream)))

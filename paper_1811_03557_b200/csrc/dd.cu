@@ -375,6 +375,22 @@ dpm_status dd_alloc(dpm_ctx* ctx) {
 }
 }  // namespace
 
+namespace {
+// u_γ = A C (R17), the basis evaluated on the fly (dd_extend_fly_kernel); ug: 2 x n_gamma
+cudaError_t dd_extend_fly(dpm_ctx* ctx, const double* C, int clamp, double* ug, cudaStream_t s) {
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA];
+  const int L1 = ctx->Lc + 1;
+  const size_t smem = (2 * (size_t)ctx->K + 2 * L1 * L1 + 2 * L1) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(dd_extend_fly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  DPM_COUNT_LAUNCH(1);
+  dd_extend_fly_kernel<<<(unsigned)std::min<int64_t>((ng + 127) / 128, 148 * 8), 128, smem, s>>>(
+      ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1], ctx->sigma[2],
+      ctx->Lc, ctx->Li, ctx->nphi, ctx->K, ctx->dd_assign, C, clamp, ug);
+  return cudaGetLastError();
+}
+}  // namespace
+
 extern "C" {
 
 dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius, int32_t lmax_cap, int32_t deg_if,
@@ -592,6 +608,58 @@ dpm_status dpm_dd_cfl_result(dpm_ctx* ctx, double chi, double* cfl_dt, void* str
   return DPM_OK;
 }
 
+
+// Phase-level pieces of the DD step (caller-owned 2-field buffers), so that a rank can run each of
+// the step's two AP solves for all its octants as one batched dpm_aux_solve_batch (the AP operator
+// depends only on n, h and dt, shared by the octants).  local_begin = rhs + solve + lsq_rhs;
+// local_finish = green_rhs + solve + restrict.
+dpm_status dpm_dd_rhs(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* fq, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!rho || !c || !fq) return DPM_ERR_INVALID;
+  if (!ctx->have_projection || ctx->dt_bep != ctx->dt) { ctx->err = "octant DD: no factorisation at this dt"; return DPM_ERR_STATE; }
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, ctx->dt, chi, fq, fq + field, as_stream(stream)));   // Step 4a
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!wk || !y) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
+  if (!ctx->dd_g) return DPM_ERR_STATE;
+  DPM_COUNT_LAUNCH(1);
+  dd_rows_trace_kernel<<<grid_for(ctx->n_rows * 2), TB, 0, s>>>(wk, field, ctx->lists[DPM_SET_GAMMA], ctx->dd_rows,
+                                                                ctx->n_rows, 2, ctx->dd_g);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  DPM_CUDA_TRY(ctx, lsq_gemv(ctx->dd_M, ctx->n_rows, ctx->K, ctx->dd_g, 2, y, s));           // y_s = M_s g_s
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const double* fq, double* wk, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!C || !fq || !wk) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA];
+  if (!ctx->dd_ug) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_ug, (size_t)2 * ng * sizeof(double) + 64));
+  DPM_CUDA_TRY(ctx, dd_extend_fly(ctx, C, clamp, ctx->dd_ug, s));
+  DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ctx->dd_ug, wk, 2, s));                        // R20
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* c, void* stream) {
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!wk || !rho || !c) return DPM_ERR_INVALID;
+  cudaStream_t s = as_stream(stream);
+  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  return DPM_OK;   // dpm_dd_stats() reads the statistics
+}
+
 dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* y, void* stream) {
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
@@ -629,16 +697,7 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
   double* wk = fq + 2 * field;
   if (!ctx->dd_ug) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_ug, (size_t)2 * ng * sizeof(double) + 64));
   double* ug = ctx->dd_ug;
-  {   // u_γ = A C (R17), the basis evaluated on the fly (dd_extend_fly_kernel)
-    const int L1 = ctx->Lc + 1;
-    const size_t smem = (2 * (size_t)ctx->K + 2 * L1 * L1 + 2 * L1) * sizeof(double);
-    DPM_CUDA_TRY(ctx, cudaFuncSetAttribute(dd_extend_fly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    DPM_COUNT_LAUNCH(1);
-    dd_extend_fly_kernel<<<(unsigned)std::min<int64_t>((ng + 127) / 128, 148 * 8), 128, smem, s>>>(
-        ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1],
-        ctx->sigma[2], ctx->Lc, ctx->Li, ctx->nphi, ctx->K, ctx->dd_assign, C, clamp, ug);
-    DPM_CUDA_TRY(ctx, cudaGetLastError());
-  }
+  DPM_CUDA_TRY(ctx, dd_extend_fly(ctx, C, clamp, ug, s));                                   // u_γ = A C (R17)
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));                                // R20
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
   DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));

@@ -65,6 +65,43 @@ class DDSolver:
             else:
                 o.chol_copy(pass_, src)
 
+    def _batched(self):
+        # several octants on one CUDA device with the phase-level entry points: the step's two AP
+        # solves run as one batch of 2 x (octants) fields each (one dpm_aux_solve_batch)
+        return (len(self.octs) > 1 and all(hasattr(o, "dd_rhs") for o in self.octs)
+                and len({str(o.device) for o in self.octs}) == 1 and self.octs[0].device.type == "cuda")
+
+    def _step_batched(self, main):
+        o0 = self.octs[0]
+        nf = 2 * len(self.octs)
+        if getattr(self, "_fq", None) is None or self._fq.shape[0] != nf:
+            n = o0.n
+            self._fq = torch.empty((nf, n, n, n), dtype=torch.float64, device=o0.device)
+            self._wk = torch.empty_like(self._fq)
+        fq, wk = self._fq, self._wk
+        for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields)):   # Step 4a, per octant stream
+            o.dd_rhs(rho, c, self.chi, fq[2 * i:2 * i + 2], stream=self.streams[i])
+        for st in self.streams:
+            main.wait_stream(st)
+        o0.aux_solve_batch(fq, wk, stream=main)                        # all particular solves at once
+        ys = []
+        for i, o in enumerate(self.octs):
+            self.streams[i].wait_stream(main)
+            ys.append(o.dd_lsq_rhs(wk[2 * i:2 * i + 2], stream=self.streams[i]))
+        for st in self.streams:
+            main.wait_stream(st)
+        Cg = self._sum(ys)                                            # C2: global coefficients
+        for i, o in enumerate(self.octs):
+            self.streams[i].wait_stream(main)
+            o.dd_green_rhs(Cg, self.clamp, fq[2 * i:2 * i + 2], wk[2 * i:2 * i + 2], stream=self.streams[i])
+        for st in self.streams:
+            main.wait_stream(st)
+        o0.aux_solve_batch(wk, wk, stream=main)                        # all Green solves at once
+        for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields)):
+            self.streams[i].wait_stream(main)
+            o.dd_restrict(wk[2 * i:2 * i + 2], rho, c, stream=self.streams[i])
+        return [o.stats(stream=self.streams[i]) for i, o in enumerate(self.octs)]
+
     def init(self, center, rho_ic, c_ic):
         self.fields = []
         for o in self.octs:
@@ -103,17 +140,20 @@ class DDSolver:
             for st in self.streams:
                 if st is not None:
                     st.wait_stream(main)
-        ys = [o.local_begin(rho, c, self.chi, stream=self.streams[i])
-              for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields))]
-        for st in self.streams:
-            if st is not None:
-                main.wait_stream(st)
-        Cg = self._sum(ys)                                            # C2: global coefficients
-        for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields)):
-            if self.streams[i] is not None:
-                self.streams[i].wait_stream(main)
-            o.local_finish_async(Cg, rho, c, self.clamp, stream=self.streams[i])
-        stats = [o.stats(stream=self.streams[i]) for i, o in enumerate(self.octs)]
+        if self._batched():
+            stats = self._step_batched(main)
+        else:
+            ys = [o.local_begin(rho, c, self.chi, stream=self.streams[i])
+                  for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields))]
+            for st in self.streams:
+                if st is not None:
+                    main.wait_stream(st)
+            Cg = self._sum(ys)                                        # C2: global coefficients
+            for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields)):
+                if self.streams[i] is not None:
+                    self.streams[i].wait_stream(main)
+                o.local_finish_async(Cg, rho, c, self.clamp, stream=self.streams[i])
+            stats = [o.stats(stream=self.streams[i]) for i, o in enumerate(self.octs)]
         for st in self.streams:
             if st is not None:
                 main.wait_stream(st)
