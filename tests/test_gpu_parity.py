@@ -276,6 +276,20 @@ def test_bep_columns_fused_matches_dense_path_cfg4(tmp_path):
     assert rel(outs["1"][1], outs["0"][1]) <= 1e-12
 
 
+def test_boundary_lsq_large_K_row_tail(api):
+    # K = 2 (18 + 1)^2 = 722 >= 592 takes the 4-rows-per-block GEMV with a partial last block (722 % 4 = 2);
+    # the factorised least squares (CholeskyQR2 -> M = D R^-1 Q^T -> GEMV) against numpy lstsq on the
+    # device's own B, for 3 right-hand sides
+    c = api.DPM(64, -1.0, 1.0, "sphere", (0, 0, 0), (0.8, 0.8, 0.8), 18, 2e-5, "cauchy")
+    assert c.K == 722 and c.K % 4 == 2
+    _, B = c.build_projection()
+    Bh = B.cpu().numpy().T                                 # |γ_in| x K
+    g = np.random.default_rng(4).uniform(-1, 1, size=(3, Bh.shape[0]))
+    coef, _ = c.boundary_lsq(torch.from_numpy(g).cuda())
+    ref = np.linalg.lstsq(Bh, g.T, rcond=None)[0].T
+    assert rel(coef.cpu().numpy(), ref) <= 1e-8
+
+
 def test_state_errors(api):
     from paper_1811_03557_b200._lib import DPMError, DPM_ERR_STATE, DPM_ERR_RANK
     cfg = get_config("cfg1")
