@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __res
   const double sg[3] = {sx, sy, sz};
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
     const int64_t pidx = gamma[g];
-    const int i = (int)(pidx / ((long)n * n)), j = (int)((pidx / n) % n), k = (int)(pidx % n);
+    const unsigned up = (unsigned)pidx, un = (unsigned)n, q = up / un;   // n^3 < 2^31: 32-bit division
+    const int k = (int)(up - q * un), i = (int)(q / un), j = (int)(q - (unsigned)i * un);
     const double P[3] = {lo + (i + 1) * h, lo + (j + 1) * h, lo + (k + 1) * h};
     double X[3];
     for (int a = 0; a < 3; ++a) X[a] = sg[a] * P[a];

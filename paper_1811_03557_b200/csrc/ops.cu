@@ -12,10 +12,14 @@ constexpr int TB = 256;
 #define STENCIL_MINB 4   // stencil kernels: <= 64 registers, 32 warps per SM (latency-bound gathers)
 #endif
 
+// flat index -> (i, j, k); n^3 <= DPM_MAX_N^3 < 2^31, so two 32-bit divisions (the 64-bit ones are
+// long emulated sequences and dominated the per-point cost of the stencil kernels)
 __device__ __forceinline__ void ijk(long p, int n, int& i, int& j, int& k) {
-  i = (int)(p / ((long)n * n));
-  j = (int)((p / n) % n);
-  k = (int)(p % n);
+  const unsigned up = (unsigned)p, un = (unsigned)n;
+  const unsigned q = up / un;
+  k = (int)(up - q * un);
+  i = (int)(q / un);
+  j = (int)(q - (unsigned)i * un);
 }
 
 __device__ __forceinline__ long flat(int n, int i, int j, int k) { return ((long)i * n + j) * n + k; }
