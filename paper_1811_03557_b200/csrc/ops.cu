@@ -210,18 +210,17 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8
                                  const double* __restrict__ fq, const double* __restrict__ ug, int64_t ng, double* q,
                                  int nrhs, double diag, double off) {
   const long nn = (long)n * n * n;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < nn * nrhs; t += (long)gridDim.x * blockDim.x) {
-    const int r = (int)(t / nn);
-    const long p = t - (long)r * nn;
-    const uint8_t f = flags[p];
-    double v = 0.0;
-    if (f & F_MPLUS) v = fq[t];
-    else if (f & F_BAND) {
-      int i, j, k;
-      ijk(p, n, i, j, k);
-      v = lop_gamma(gmap, ug + (size_t)r * ng, n, i, j, k, diag, off);
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    const uint8_t f = flags[p];   // the point's flag, shared by the right-hand sides
+    int i = 0, j = 0, k = 0;
+    if (!(f & F_MPLUS) && (f & F_BAND)) ijk(p, n, i, j, k);
+    for (int r = 0; r < nrhs; ++r) {
+      const size_t t = (size_t)r * nn + p;
+      double v = 0.0;
+      if (f & F_MPLUS) v = fq[t];
+      else if (f & F_BAND) v = lop_gamma(gmap, ug + (size_t)r * ng, n, i, j, k, diag, off);
+      q[t] = v;
     }
-    q[t] = v;
   }
 }
 
@@ -315,6 +314,8 @@ __global__ void dt_rule_kernel(const double* __restrict__ red3, double h, double
 }
 
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
+// kernels ending in per-block atomics on a few addresses (CFL maxima, step statistics): 4 blocks per SM
+int grid_reduce(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 4)); }
 
 }  // namespace
 
@@ -375,7 +376,7 @@ cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaS
   cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(double), s);
   if (e != cudaSuccess) return e;
   DPM_COUNT_LAUNCH(1);
-  cfl_kernel<<<grid_for(nn), TB, 0, s>>>(c, ctx->flags, ctx->n, out3);
+  cfl_kernel<<<grid_reduce(nn), TB, 0, s>>>(c, ctx->flags, ctx->n, out3);
   return cudaGetLastError();
 }
 
@@ -392,7 +393,7 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
   DPM_COUNT_LAUNCH(1);
-  green_rhs_kernel<<<grid_for(nn * nrhs), TB, 0, s>>>(ctx->flags, ctx->gmap, ctx->n, fq, u_gamma,
+  green_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(ctx->flags, ctx->gmap, ctx->n, fq, u_gamma,
                                                       ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
   return cudaGetLastError();
 }
@@ -410,6 +411,6 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
   cudaError_t e = cudaMemsetAsync(stats, 0, 5 * sizeof(double), s);
   if (e != cudaSuccess) return e;
   DPM_COUNT_LAUNCH(1);
-  restrict_kernel<<<grid_for(nn), TB, 0, s>>>(ctx->flags, ctx->n, u, rho, c, stats);
+  restrict_kernel<<<grid_reduce(nn), TB, 0, s>>>(ctx->flags, ctx->n, u, rho, c, stats);
   return cudaGetLastError();
 }
