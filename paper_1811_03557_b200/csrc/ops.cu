@@ -106,18 +106,6 @@ __device__ __forceinline__ double valat(const double* __restrict__ f, int n, int
   return interior(n, i, j, k) ? f[flat(n, i, j, k)] : 0.0;
 }
 
-// N+ membership of a lattice point (interior flag; a face ghost is in N+ iff its unique
-// interior neighbour is in M+, R5; anything else is not).
-__device__ __forceinline__ bool nplus_at(const uint8_t* __restrict__ flags, int n, int i, int j, int k) {
-  if (interior(n, i, j, k)) return flags[flat(n, i, j, k)] & F_NPLUS;
-  const int oi = (i < 0) || (i >= n), oj = (j < 0) || (j >= n), ok = (k < 0) || (k >= n);
-  if (oi + oj + ok != 1) return false;
-  const int a = i < 0 ? 0 : (i >= n ? n - 1 : i);
-  const int b = j < 0 ? 0 : (j >= n ? n - 1 : j);
-  const int c = k < 0 ? 0 : (k >= n ? n - 1 : k);
-  if (i < -1 || i > n || j < -1 || j > n || k < -1 || k > n) return false;
-  return flags[flat(n, a, b, c)] & F_MPLUS;
-}
 
 __device__ __forceinline__ double minmod3(double a, double b, double c) {
   if (a > 0 && b > 0 && c > 0) return fmin(a, fmin(b, c));
@@ -125,20 +113,10 @@ __device__ __forceinline__ double minmod3(double a, double b, double c) {
   return 0.0;
 }
 
-// h x the minmod slope of cell q along axis ax; 0 unless q and both neighbours are in N+
-// (R15).  Ghost cells hold 0, so their slope is 0.  The three minmod arguments share the positive
-// factor 1/h, so the limiter runs on the unscaled differences (x2 and x1/2 are exact): the same
-// choice as with the divided slopes, and h s enters the reconstruction r0 ± (h/2) s directly.
-__device__ __forceinline__ double slope_h(const double* __restrict__ rho, const uint8_t* __restrict__ flags, int n,
-                                          int i, int j, int k, int ax) {
-  if (!interior(n, i, j, k)) return 0.0;
-  if (!(flags[flat(n, i, j, k)] & F_NPLUS)) return 0.0;
-  const int di = ax == 0, dj = ax == 1, dk = ax == 2;
-  if (!nplus_at(flags, n, i + di, j + dj, k + dk) || !nplus_at(flags, n, i - di, j - dj, k - dk)) return 0.0;
-  const double r0 = rho[flat(n, i, j, k)];
-  const double rp = valat(rho, n, i + di, j + dj, k + dk), rm = valat(rho, n, i - di, j - dj, k - dk);
-  return minmod3(2.0 * (rp - r0), 0.5 * (rp - rm), 2.0 * (r0 - rm));
-}
+// minmod slopes: nonzero only if the cell and both neighbours along the axis are in N+
+// (R15); the three minmod arguments share the positive factor 1/h, so the limiter runs on the unscaled
+// differences (x2 and x1/2 are exact) and h s enters the reconstruction r0 ± (h/2) s directly
+// (evaluated inside flux_rhs_kernel).
 
 __device__ __forceinline__ void umax_atomic(double* addr, double v) {
   // non-negative doubles order like their bit patterns
@@ -177,7 +155,12 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) cfl_kernel(const double* __r
 __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
                                 const uint8_t* __restrict__ flags, int n, double h, double dt, double chi,
                                 double* __restrict__ fq_rho, double* __restrict__ fq_c) {
+  // Per axis the stencil's values (ρ and flags at offsets -2..2, c at ±1) are loaded up front with
+  // predicated loads (0 outside the box, like valat), then the N+ tests (interior flag; a face ghost is
+  // in N+ iff its unique interior neighbour is in M+, R5; anything further out is not), the minmod
+  // slopes and the upwind choice are evaluated from registers, without dependent load chains.
   const long nn = (long)n * n * n;
+  const double ih = 1.0 / h, idt = 1.0 / dt;
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     if (!(flags[p] & F_MPLUS)) {
       fq_rho[p] = 0.0;
@@ -187,17 +170,39 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
     int i, j, k;
     ijk(p, n, i, j, k);
     const double r0 = rho[p], c0 = c[p];
-    const double ih = 1.0 / h, idt = 1.0 / dt;   // (fp64 division is a long sequence: once per thread)
     double g = 0.0;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
-      const int di = ax == 0, dj = ax == 1, dk = ax == 2;
-      const double cE = valat(c, n, i + di, j + dj, k + dk), cW = valat(c, n, i - di, j - dj, k - dk);
-      const double rE = valat(rho, n, i + di, j + dj, k + dk), rW = valat(rho, n, i - di, j - dj, k - dk);
+      const int cd = ax == 0 ? i : (ax == 1 ? j : k);
+      const long st = ax == 0 ? (long)n * n : (ax == 1 ? (long)n : 1L);
+      double R[5];
+      uint8_t Fr[5];
+#pragma unroll
+      for (int o = 0; o < 5; ++o) {
+        const int pos = cd + o - 2;
+        const bool in = pos >= 0 && pos < n;
+        R[o] = in ? rho[p + (o - 2) * st] : 0.0;
+        Fr[o] = in ? flags[p + (o - 2) * st] : (uint8_t)0;
+      }
+      const double cE = cd + 1 < n ? c[p + st] : 0.0, cW = cd >= 1 ? c[p - st] : 0.0;
+      bool np[5];
+#pragma unroll
+      for (int o = 0; o < 5; ++o) {
+        const int pos = cd + o - 2;
+        if (pos >= 0 && pos < n) np[o] = Fr[o] & F_NPLUS;
+        else if (pos == -1) np[o] = o + 1 < 5 && (Fr[o + 1 < 5 ? o + 1 : 4] & F_MPLUS);
+        else if (pos == n) np[o] = o >= 1 && (Fr[o >= 1 ? o - 1 : 0] & F_MPLUS);
+        else np[o] = false;
+      }
+      auto sl = [&](int o) -> double {   // h x the slope at offset o - 2 (o = 1, 2, 3), as slope_h
+        const int pos = cd + o - 2;
+        if (!(pos >= 0 && pos < n) || !np[o] || !np[o - 1] || !np[o + 1]) return 0.0;
+        return minmod3(2.0 * (R[o + 1] - R[o]), 0.5 * (R[o + 1] - R[o - 1]), 2.0 * (R[o] - R[o - 1]));
+      };
       const double gE = (cE - c0) * ih, gW = (c0 - cW) * ih;   // upwind choice: the sign of the difference
-      const double s0 = slope_h(rho, flags, n, i, j, k, ax);
-      const double rhoE = gE > 0 ? r0 + 0.5 * s0 : rE - 0.5 * slope_h(rho, flags, n, i + di, j + dj, k + dk, ax);
-      const double rhoW = gW > 0 ? rW + 0.5 * slope_h(rho, flags, n, i - di, j - dj, k - dk, ax) : r0 - 0.5 * s0;
+      const double s0 = sl(2);
+      const double rhoE = gE > 0 ? r0 + 0.5 * s0 : R[3] - 0.5 * sl(3);
+      const double rhoW = gW > 0 ? R[1] + 0.5 * sl(1) : r0 - 0.5 * s0;
       g += (chi * rhoE * gE - chi * rhoW * gW) * ih;
     }
     fq_rho[p] = (r0 - dt * g) * idt;
