@@ -122,17 +122,13 @@ __global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __res
                                                             const uint8_t* __restrict__ assign,
                                                             const double* __restrict__ C, int clamp, double* ug) {
   extern __shared__ double fly_sm[];
-  double* c0v = fly_sm;                        // [K]
-  double* c1v = c0v + K;                       // [K]
+  double2* cv = reinterpret_cast<double2*>(fly_sm);   // [K]: (C[0][c], C[1][c]) — one 16-byte load per basis value
   const int L1 = Lc + 1;
-  double* ta = c1v + K;                        // [L1][L1]: a_lm
+  double* ta = fly_sm + 2 * K;                 // [L1][L1]: a_lm
   double* tb = ta + L1 * L1;                   // [L1][L1]: b_lm
   double* tpm = tb + L1 * L1;                  // [L1]: sqrt((2m+1)/(2m))
   double* tz = tpm + L1;                       // [L1]: sqrt(2m+3)
-  for (int i = threadIdx.x; i < K; i += blockDim.x) {
-    c0v[i] = C[i];
-    c1v[i] = C[K + i];
-  }
+  for (int i = threadIdx.x; i < K; i += blockDim.x) cv[i] = make_double2(C[i], C[K + i]);
   for (int e = threadIdx.x; e < L1 * L1; e += blockDim.x) {
     const int l = e / L1, m = e % L1;
     ta[e] = (l >= m + 2) ? sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m)) : 0.0;
@@ -178,15 +174,17 @@ __global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __res
           if (l > m) { p2 = p1; p1 = pl; }
           if (m == 0) {
             const int nu = l * l + l;
-            t0 = fma(pl, fma(wc, c0v[nc + nu], c0v[nu]), t0);
-            t1 = fma(pl, fma(wc, c1v[nc + nu], c1v[nu]), t1);
+            const double2 a = cv[nu], d = cv[nc + nu];
+            t0 = fma(pl, fma(wc, d.x, a.x), t0);
+            t1 = fma(pl, fma(wc, d.y, a.y), t1);
           } else {
             const double vc = 1.41421356237309504880 * pl * Cm, vs = 1.41421356237309504880 * pl * Sm;
             const int nup = l * l + l + m, nun = l * l + l - m;
-            t0 = fma(vc, fma(wc, c0v[nc + nup], c0v[nup]), t0);
-            t1 = fma(vc, fma(wc, c1v[nc + nup], c1v[nup]), t1);
-            t0 = fma(vs, fma(wc, c0v[nc + nun], c0v[nun]), t0);
-            t1 = fma(vs, fma(wc, c1v[nc + nun], c1v[nun]), t1);
+            const double2 ap = cv[nup], dp = cv[nc + nup], an = cv[nun], dn = cv[nc + nun];
+            t0 = fma(vc, fma(wc, dp.x, ap.x), t0);
+            t1 = fma(vc, fma(wc, dp.y, ap.y), t1);
+            t0 = fma(vs, fma(wc, dn.x, an.x), t0);
+            t1 = fma(vs, fma(wc, dn.y, an.y), t1);
           }
         }
       }
@@ -206,8 +204,9 @@ __global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __res
       for (int gd = 0; gd <= Li; ++gd)
         for (int jj = gd; jj >= 0; --jj, ++m) {
           const double phi = Ps[jj] * Pt[gd - jj];
-          t0 = fma(phi, fma(d, c0v[cb + nphi + m], c0v[cb + m]), t0);
-          t1 = fma(phi, fma(d, c1v[cb + nphi + m], c1v[cb + m]), t1);
+          const double2 a = cv[cb + m], e = cv[cb + nphi + m];
+          t0 = fma(phi, fma(d, e.x, a.x), t0);
+          t1 = fma(phi, fma(d, e.y, a.y), t1);
         }
       s0 = fma(inv, t0, s0);
       s1 = fma(inv, t1, s1);
