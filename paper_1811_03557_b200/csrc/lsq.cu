@@ -313,6 +313,9 @@ template <bool TRANS>
 __global__ void __launch_bounds__(256) gemm_tri_kernel(const double* __restrict__ A, int64_t m, int K,
                                                         const double* __restrict__ T, const double* __restrict__ scale,
                                                         double* __restrict__ Cm);
+template <bool TRANS>
+cudaError_t launch_gemm_tri(const double* A, int64_t m, int K, const double* T, const double* scale, double* C,
+                            cudaStream_t s);
 
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   const int K = ctx->K;
@@ -347,10 +350,7 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   // apply operator M = D R^{-1} Q^T (K x |γ_in|): each LSQ solve is then one GEMV
   double* Ri = R1;   // R1 is free after the trmm
   DPM_CUDA_TRY(ctx, lsq_rinv(ctx->R, K, Ri, s));
-  DPM_COUNT_LAUNCH(1);
-  gemm_tri_kernel<true><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(ctx->Q, m, K, Ri, ctx->colscale,
-                                                                                        ctx->Mlsq);
-  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  DPM_CUDA_TRY(ctx, launch_gemm_tri<true>(ctx->Q, m, K, Ri, ctx->colscale, ctx->Mlsq, s));
   int hfail = 0;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->bep_cond, dcond, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -496,25 +496,201 @@ cudaError_t lsq_mul_rinv(const double* A, int64_t m, int K, const double* R, dou
                          cudaStream_t s) {
   cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
   if (e != cudaSuccess || m == 0) return e;
-  DPM_COUNT_LAUNCH(1);
-  gemm_tri_kernel<false><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, Ri_ws, nullptr, out);
-  return cudaGetLastError();
+  return launch_gemm_tri<false>(A, m, K, Ri_ws, nullptr, out, s);
 }
 
 // out = A T with T = an already inverted upper-triangular factor (tiled GEMM; out != A)
 cudaError_t lsq_mul_upper(const double* A, int64_t m, int K, const double* T, double* out, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  DPM_COUNT_LAUNCH(1);
-  gemm_tri_kernel<false><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(A, m, K, T, nullptr, out);
-  return cudaGetLastError();
+  return launch_gemm_tri<false>(A, m, K, T, nullptr, out, s);
 }
 
 // M = diag(scale) Ri Q^T (stored K x m row-major) from an already inverted Ri = R^{-1}
 cudaError_t lsq_operator_from_rinv(const double* Ri, const double* Q, int64_t m, int K, const double* scale, double* M,
                                    cudaStream_t s) {
   if (m == 0) return cudaSuccess;
+  return launch_gemm_tri<true>(Q, m, K, Ri, scale, M, s);
+}
+
+// ---- fp64 tensor-pipe (DMMA.m8n8k4) versions of the Gram and the triangular GEMMs (DPM_LSQ_DMMA, default) ----
+// 64 x 64 output tile per CTA, 8 warps each owning 2 x 4 fragment tiles of 8 x 8 (rows 16 (w/2)..,
+// columns 32 (w%2)..), k staged 32 at a time by 8-byte cp.async (row counts may be odd) into shared
+// memory laid out so every fragment load hits each 8-byte bank pair twice.
+__device__ __forceinline__ void dmma_884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cpasync8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src));
+}
+constexpr int DG_RK = 32, DG_PG = 36;   // Gram: rows per stage, pitch of the [column][row] stage (36 = 4 mod 16)
+
+// G(i, j) += Σ_r A(r, i) A(r, j) over this CTA's row split, upper 64 x 64 tiles (atomics over splits)
+__global__ void __launch_bounds__(256) gram_dmma_kernel(const double* __restrict__ A, int64_t m, int K, double* G,
+                                                        int64_t rows_per_split) {
+  const int bi = blockIdx.x * 64, bj = blockIdx.y * 64;
+  if (bj < bi) return;
+  extern __shared__ __align__(16) double gsm[];   // sI[2][64 DG_PG] | sJ[2][64 DG_PG]
+  double (*sI)[64 * DG_PG] = reinterpret_cast<double (*)[64 * DG_PG]>(gsm);
+  double (*sJ)[64 * DG_PG] = reinterpret_cast<double (*)[64 * DG_PG]>(gsm + 2 * 64 * DG_PG);
+  const int64_t r0 = (int64_t)blockIdx.z * rows_per_split, r1 = min(m, r0 + rows_per_split);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wi = 16 * (w >> 1), wj = 32 * (w & 1);
+  const bool diag = bi == bj;
+  auto stage = [&](int buf, int64_t rr) {   // rows rr .. rr+31 of columns bi.., bj.. -> [col][row]
+    for (int e = t; e < 64 * DG_RK; e += 256) {
+      const int c = e >> 5, r = e & 31;
+      const int64_t row = rr + r;
+      double* di = &sI[buf][c * DG_PG + r];
+      if (row < r1 && bi + c < K) cpasync8(di, A + (size_t)(bi + c) * m + row); else *di = 0.0;
+      if (!diag) {
+        double* dj = &sJ[buf][c * DG_PG + r];
+        if (row < r1 && bj + c < K) cpasync8(dj, A + (size_t)(bj + c) * m + row); else *dj = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int buf = 0;
+  if (r0 < r1) stage(0, r0);
+  for (int64_t rr = r0; rr < r1; rr += DG_RK, buf ^= 1) {
+    if (rr + DG_RK < r1) {
+      stage(buf ^ 1, rr + DG_RK);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* XI = sI[buf];
+    const double* XJ = diag ? sI[buf] : sJ[buf];
+#pragma unroll
+    for (int ks = 0; ks < DG_RK / 4; ++ks) {
+      const int kr = 4 * ks + (lane & 3);
+      double af[2], bf[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) af[a] = XI[(wi + 8 * a + (lane >> 2)) * DG_PG + kr];   // A_frag[i][k] = A(k, i)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = XJ[(wj + 8 * b + (lane >> 2)) * DG_PG + kr];   // B_frag[k][j] = A(k, j)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_884(acc[a][b], af[a], bf[b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = bi + wi + 8 * a + (lane >> 2), j = bj + wj + 8 * b + 2 * (lane & 3) + h;
+        if (i < K && j < K && i <= j) atomicAdd(G + (size_t)j * K + i, acc[a][b][h]);
+      }
+}
+
+constexpr int DT_RK = 32, DT_P = 72;   // tri-GEMM: k per stage, pitch of the [k][64] stages (72 = 8 mod 16)
+
+// C = A T' (m x K column-major) with T' = T upper (TRANS = false) or T^T lower with the column scale
+// (TRANS = true: the LSQ operator), as gemm_tri_kernel but on the fp64 tensor pipe
+template <bool TRANS>
+__global__ void __launch_bounds__(256) gemm_tri_dmma_kernel(const double* __restrict__ A, int64_t m, int K,
+                                                            const double* __restrict__ T,
+                                                            const double* __restrict__ scale, double* __restrict__ Cm) {
+  extern __shared__ __align__(16) double tsm[];   // sA[2][DT_RK][DT_P] | sT[2][DT_RK][DT_P]
+  double* sA = tsm;
+  double* sT = tsm + 2 * DT_RK * DT_P;
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int j0 = blockIdx.y * 64;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wr = 16 * (w >> 1), wj = 32 * (w & 1);
+  const int kbeg = TRANS ? j0 : 0, kend = TRANS ? K : min(K, j0 + 64);
+  auto stage = [&](int buf, int k0) {
+    double* a = sA + buf * DT_RK * DT_P;
+    double* tt = sT + buf * DT_RK * DT_P;
+    for (int e = t; e < DT_RK * 64; e += 256) {
+      const int kk = e >> 6, c = e & 63;
+      const int k = k0 + kk;
+      const int64_t r = r0 + c;
+      if (r < m && k < K) cpasync8(a + kk * DT_P + c, A + (size_t)k * m + r); else a[kk * DT_P + c] = 0.0;
+      const int j = j0 + c;
+      const bool nz = k < K && j < K && (TRANS ? k >= j : k <= j);
+      if (nz) cpasync8(tt + kk * DT_P + c, TRANS ? T + (size_t)k * K + j : T + (size_t)j * K + k);
+      else tt[kk * DT_P + c] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int buf = 0;
+  if (kbeg < kend) stage(0, kbeg);
+  for (int k0 = kbeg; k0 < kend; k0 += DT_RK, buf ^= 1) {
+    if (k0 + DT_RK < kend) {
+      stage(buf ^ 1, k0 + DT_RK);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* a = sA + buf * DT_RK * DT_P;
+    const double* tt = sT + buf * DT_RK * DT_P;
+#pragma unroll
+    for (int ks = 0; ks < DT_RK / 4; ++ks) {
+      const int kk = 4 * ks + (lane & 3);
+      double af[2], bf[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) af[x] = a[kk * DT_P + wr + 8 * x + (lane >> 2)];   // A_frag[r][k] = A(r, k)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bf[y] = tt[kk * DT_P + wj + 8 * y + (lane >> 2)];  // B_frag[k][j] = T'(k, j)
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_884(acc[x][y], af[x], bf[y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = r0 + wr + 8 * x + (lane >> 2);
+        const int j = j0 + wj + 8 * y + 2 * (lane & 3) + h;
+        if (r < m && j < K) Cm[(size_t)j * m + r] = scale ? scale[j] * acc[x][y][h] : acc[x][y][h];
+      }
+}
+
+static bool lsq_dmma() {
+  static const bool on = [] {
+    const char* v = getenv("DPM_LSQ_DMMA");
+    return !(v && atoi(v) == 0);
+  }();
+  return on;
+}
+
+template <bool TRANS>
+cudaError_t launch_gemm_tri(const double* A, int64_t m, int K, const double* T, const double* scale, double* C,
+                            cudaStream_t s) {
+  const dim3 grid((unsigned)((m + 63) / 64), (K + 63) / 64);
   DPM_COUNT_LAUNCH(1);
-  gemm_tri_kernel<true><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(Q, m, K, Ri, scale, M);
+  if (lsq_dmma()) {
+    const size_t smem = 4 * DT_RK * DT_P * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tri_dmma_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    gemm_tri_dmma_kernel<TRANS><<<grid, 256, smem, s>>>(A, m, K, T, scale, C);
+  } else {
+    gemm_tri_kernel<TRANS><<<grid, 256, 0, s>>>(A, m, K, T, scale, C);
+  }
   return cudaGetLastError();
 }
 
@@ -527,7 +703,13 @@ cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t 
   const int64_t rps = std::max<int64_t>(64, ((m + target_split - 1) / target_split + 15) / 16 * 16);
   const int nsplit = (int)std::max<int64_t>(1, (m + rps - 1) / rps);
   DPM_COUNT_LAUNCH(1);
-  gram64_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, s>>>(A, m, K, G, rps);
+  if (lsq_dmma()) {
+    const size_t smem = 4 * 64 * DG_PG * sizeof(double);
+    if ((e = cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return e;
+    gram_dmma_kernel<<<dim3(tiles, tiles, nsplit), 256, smem, s>>>(A, m, K, G, (rps + DG_RK - 1) / DG_RK * DG_RK);
+  } else
+    gram64_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, s>>>(A, m, K, G, rps);
   return cudaGetLastError();
 }
 
@@ -564,9 +746,7 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
                                double* Ri_ws, cudaStream_t s) {
   cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
   if (e != cudaSuccess || m == 0) return e;
-  DPM_COUNT_LAUNCH(1);
-  gemm_tri_kernel<true><<<dim3((unsigned)((m + 63) / 64), (K + 63) / 64), 256, 0, s>>>(Q, m, K, Ri_ws, scale, M);
-  return cudaGetLastError();
+  return launch_gemm_tri<true>(Q, m, K, Ri_ws, scale, M, s);
 }
 
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
