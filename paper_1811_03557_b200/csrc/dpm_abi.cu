@@ -95,6 +95,7 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   if (st == DPM_OK && domain->kind != DPM_OCTANT_CANON) st = setup_geometry(ctx);
   if (st == DPM_OK && dst_plan_init(ctx->plan, ctx->n, ctx->h, dt) != cudaSuccess) { st = DPM_ERR_CUDA; ctx->err = "plan init"; }
   if (st == DPM_OK && cudaMalloc(&ctx->red, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
+  if (st == DPM_OK && cudaMemset(ctx->red, 0, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_CUDA;   // [63]: ticket
   if (st == DPM_OK && cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
   if (st != DPM_OK) {
     g_create_err = ctx->err.empty() ? "dpm_create failed" : ctx->err;
@@ -347,8 +348,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
     DPM_CUDA_TRY(ctx, cudaMemcpyAsync(backup + field, c, field * 8, cudaMemcpyDeviceToDevice, s));
   }
   if (prm->dt_rule == 0) {   // Step 3 on the device: did the speculative dt stay valid?
-    DPM_CUDA_TRY(ctx, launch_cfl_reduce(ctx, c, slot, s));
-    DPM_CUDA_TRY(ctx, launch_dt_rule(ctx, slot, prm->chi, dt, prm->dt_cap, slot + 3, s));
+    DPM_CUDA_TRY(ctx, launch_cfl_dt(ctx, c, slot, prm->chi, dt, prm->dt_cap, slot + 3, s));
   }
   // Step 4a: flux + IMEX right-hand sides, particular solutions
   DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s));

@@ -223,8 +223,9 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
                              cudaStream_t s);
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s);
-cudaError_t launch_dt_rule(dpm_ctx* ctx, const double* red3, double chi, double dt_prev, double cap, double* dt_out,
-                           cudaStream_t s);
+// CFL maxima + the Step-3 dt rule in one kernel (ticket in ctx->red[63], zero at creation)
+cudaError_t launch_cfl_dt(dpm_ctx* ctx, const double* c, double* out3, double chi, double dt_prev, double cap,
+                          double* dt_out, cudaStream_t s);
 
 // bep_fused.cu (sparse-in / gamma-out BEP columns)
 bool bep_fused_enabled(const dpm_ctx* ctx);

@@ -306,17 +306,56 @@ __global__ void pks_init_kernel(const uint8_t* __restrict__ flags, const int32_t
   }
 }
 
-// Step 3 dt rule on the device (R13), identical arithmetic to the host rule:
-//   cfl = min_a h / (6 χ max|Δc|_a / h),  dt = min(min(dt_prev, cap), min(cfl, h^2/2)).
-__global__ void dt_rule_kernel(const double* __restrict__ red3, double h, double chi, double dt_prev, double cap,
-                               double* dt_out) {
-  double cfl = INFINITY;
-  for (int a = 0; a < 3; ++a) {
-    const double mx = red3[a] / h;
-    if (mx > 0) cfl = fmin(cfl, h / (6.0 * chi * mx));
+// CFL maxima (as cfl_kernel) fused with the Step-3 dt rule on the device (R13, the host rule's
+// arithmetic: cfl = min_a h / (6 χ max|Δc|_a / h), dt = min(min(dt_prev, cap), min(cfl, h^2/2))): the
+// last block to finish (threadfence + ticket) evaluates the rule from the reduced maxima and resets
+// the ticket.
+__global__ void __launch_bounds__(TB, STENCIL_MINB) cfl_dt_kernel(const double* __restrict__ c,
+                                                                  const uint8_t* __restrict__ flags, int n,
+                                                                  double* out3, unsigned* ticket, double h, double chi,
+                                                                  double dt_prev, double cap, double* dt_out) {
+  __shared__ double red[3][TB / 32];
+  __shared__ bool last;
+  double mx[3] = {0, 0, 0};
+  const long nn = (long)n * n * n;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    if (!(flags[p] & F_MPLUS)) continue;
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    const double c0 = c[p];
+    mx[0] = fmax(mx[0], fmax(fabs(valat(c, n, i + 1, j, k) - c0), fabs(c0 - valat(c, n, i - 1, j, k))));
+    mx[1] = fmax(mx[1], fmax(fabs(valat(c, n, i, j + 1, k) - c0), fabs(c0 - valat(c, n, i, j - 1, k))));
+    mx[2] = fmax(mx[2], fmax(fabs(valat(c, n, i, j, k + 1) - c0), fabs(c0 - valat(c, n, i, j, k - 1))));
   }
-  *dt_out = fmin(fmin(dt_prev, cap), fmin(cfl, 0.5 * h * h));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int a = 0; a < 3; ++a) {
+    double v = mx[a];
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[a][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int q = 0; q < TB / 32; ++q) v = fmax(v, red[threadIdx.x][q]);
+    umax_atomic(out3 + threadIdx.x, v);
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* r3 = out3;
+    double cfl = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+      const double m = r3[a] / h;
+      if (m > 0) cfl = fmin(cfl, h / (6.0 * chi * m));
+    }
+    *dt_out = fmin(fmin(dt_prev, cap), fmin(cfl, 0.5 * h * h));
+    *ticket = 0u;
+  }
 }
+
 
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
 // kernels ending in per-block atomics on a few addresses (CFL maxima, step statistics): 4 blocks per SM
@@ -403,12 +442,17 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
   return cudaGetLastError();
 }
 
-cudaError_t launch_dt_rule(dpm_ctx* ctx, const double* red3, double chi, double dt_prev, double cap, double* dt_out,
-                           cudaStream_t s) {
+cudaError_t launch_cfl_dt(dpm_ctx* ctx, const double* c, double* out3, double chi, double dt_prev, double cap,
+                          double* dt_out, cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(double), s);
+  if (e != cudaSuccess) return e;
   DPM_COUNT_LAUNCH(1);
-  dt_rule_kernel<<<1, 1, 0, s>>>(red3, ctx->h, chi, dt_prev, cap, dt_out);
+  cfl_dt_kernel<<<grid_reduce(nn), TB, 0, s>>>(c, ctx->flags, ctx->n, out3, reinterpret_cast<unsigned*>(ctx->red + 63),
+                                               ctx->h, chi, dt_prev, cap, dt_out);
   return cudaGetLastError();
 }
+
 
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s) {
