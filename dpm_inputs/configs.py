@@ -17,7 +17,7 @@ class Config:
     center: Tuple[float, float, float]
     semi: Tuple[float, float, float]   # sphere: (r, r, r)
     lmax: int                    # spherical-harmonic degree L
-    basis: str                   # "cauchy" {Y, d*Y} | "neumann0" {Y, d^2/2*Y}  (R9)
+    basis: str                   # "cauchy" {Y, d*Y} | "neumann0" {Y, d^2/2*Y}  (R9); "*_zonal": P_l^0 only
     dt: float                    # AP dt (cfg1, cfg4) or the PKS dt cap (cfg2, cfg3, cfg5)
     steps: int = 0               # PKS steps (0 = not a PKS config)
     batch: int = 0               # number of RHS in the throughput config
@@ -30,7 +30,7 @@ class Config:
 
     @property
     def K(self) -> int:
-        return 2 * (self.lmax + 1) ** 2
+        return 2 * (self.lmax + 1) if self.basis.endswith("_zonal") else 2 * (self.lmax + 1) ** 2
 
 
 CONFIGS = {

@@ -54,8 +54,15 @@ typedef struct { int32_t kind; double center[3]; double semi[3]; } dpm_domain;
 
 /* Extension-operator column sets; K = 2 (lmax+1)^2 columns,
    column c = comp*(lmax+1)^2 + nu, nu = l^2 + l + m (real SH without Condon-Shortley
-   phase, R8).  comp 0: Y_nu(foot);  comp 1: d*Y_nu (CAUCHY) or (d^2/2)*Y_nu (NEUMANN0). */
-typedef enum { DPM_BASIS_CAUCHY = 0, DPM_BASIS_NEUMANN0 = 1 } dpm_basis;
+   phase, R8).  comp 0: Y_nu(foot);  comp 1: d*Y_nu (CAUCHY) or (d^2/2)*Y_nu (NEUMANN0).
+   The *_ZONAL sets are the paper's own basis (only the zonal modes
+   phi_nu = P_nu^0(cos θ), the unnormalised Legendre polynomial of the foot point's polar
+   angle about +z): K = 2 (lmax+1) columns, c = comp*(lmax+1) + l, same comp rule;
+   lmax <= DPM_MAX_ZONAL_L (the paper's Test B uses up to 500 harmonics). */
+typedef enum {
+  DPM_BASIS_CAUCHY = 0, DPM_BASIS_NEUMANN0 = 1, DPM_BASIS_CAUCHY_ZONAL = 2, DPM_BASIS_NEUMANN0_ZONAL = 3
+} dpm_basis;
+#define DPM_MAX_ZONAL_L 1000
 
 /* Point sets of Definition 1. BAND = M- ∩ dil7(gamma) = support of every
    difference-potential right-hand side (R21). NPLUS = N+ restricted to M0. */

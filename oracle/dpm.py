@@ -8,7 +8,8 @@ Literal definitions, column by column (no fusion, no batching tricks):
 * trace Tr_γ, Tr_γin and P_γ = Tr_γ P_{N+γ}.
 * extension operator with spectral Cauchy data:
   columns c = comp*(L+1)^2 + ν (R9): comp 0 -> Y_ν(foot);
-  comp 1 -> d Y_ν ("cauchy", 2-term u, du/dn) or (d^2/2) Y_ν ("neumann0").
+  comp 1 -> d Y_ν ("cauchy", 2-term u, du/dn) or (d^2/2) Y_ν ("neumann0", P:273-275);
+  "*_zonal": Y_ν replaced by the paper's zonal modes P_l^0(cos θ), l = 0..L, K = 2 (L+1).
 * reduced BEP (`eqn:BEP_recast` P:287-290): B = Tr_γin (E - P_γ E).
 * least squares: numpy.linalg.lstsq (SVD) and an independent plain
   Householder QR (``householder_lstsq``) used as a cross-check.
@@ -28,13 +29,14 @@ def gamma_points(g: grid.Grid, ps: grid.PointSets) -> np.ndarray:
 
 
 def extension_matrix(g, ps, kind, center, semi, lmax, basis):
-    """E (|γ| × K), K = 2 (L+1)^2, plus (d, unit) of the gamma points."""
+    """E (|γ| × K), K = 2 (L+1)^2 (full real SH) or 2 (L+1) (zonal), plus (d, unit) of
+    the gamma points."""
     P = gamma_points(g, ps)
     foot, d, unit = geometry.geometry(P, kind, center, semi)
-    Y = sh.real_sh(lmax, unit)
-    if basis == "cauchy":
+    Y = sh.zonal(lmax, unit) if basis.endswith("_zonal") else sh.real_sh(lmax, unit)
+    if basis in ("cauchy", "cauchy_zonal"):
         second = d[:, None] * Y
-    elif basis == "neumann0":
+    elif basis in ("neumann0", "neumann0_zonal"):
         second = 0.5 * (d ** 2)[:, None] * Y
     else:
         raise ValueError(basis)

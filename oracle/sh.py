@@ -32,6 +32,19 @@ def assoc_legendre(lmax: int, x: np.ndarray) -> np.ndarray:
     return P
 
 
+def zonal(lmax: int, unit: np.ndarray) -> np.ndarray:
+    """phi[:, l] = P_l^0(cos θ), l = 0..lmax (the zonal modes, unnormalised Legendre
+    polynomials of cos θ = u_z), by Bonnet's recurrence (l+1) P_{l+1} = (2l+1) x P_l - l P_{l-1}."""
+    x = np.clip(np.asarray(unit, dtype=np.float64)[:, 2], -1.0, 1.0)
+    P = np.zeros((x.shape[0], lmax + 1))
+    P[:, 0] = 1.0
+    if lmax >= 1:
+        P[:, 1] = x
+    for l in range(1, lmax):
+        P[:, l + 1] = ((2 * l + 1) * x * P[:, l] - l * P[:, l - 1]) / (l + 1)
+    return P
+
+
 def real_sh(lmax: int, unit: np.ndarray) -> np.ndarray:
     """Y[:, ν] for ν = l^2 + l + m, shape (npts, (lmax+1)^2)."""
     u = np.asarray(unit, dtype=np.float64)

@@ -17,7 +17,9 @@ DPM_OK, DPM_ERR_INVALID, DPM_ERR_OOM, DPM_ERR_CUDA, DPM_ERR_STATE, DPM_ERR_RANK,
 STATUS = {0: "DPM_OK", 1: "DPM_ERR_INVALID", 2: "DPM_ERR_OOM", 3: "DPM_ERR_CUDA", 4: "DPM_ERR_STATE",
           5: "DPM_ERR_RANK", 6: "DPM_ERR_NONFINITE"}
 SPHERE, ELLIPSOID = 0, 1
-BASIS_CAUCHY, BASIS_NEUMANN0 = 0, 1
+BASIS_CAUCHY, BASIS_NEUMANN0, BASIS_CAUCHY_ZONAL, BASIS_NEUMANN0_ZONAL = 0, 1, 2, 3
+BASES = {"cauchy": BASIS_CAUCHY, "neumann0": BASIS_NEUMANN0,
+         "cauchy_zonal": BASIS_CAUCHY_ZONAL, "neumann0_zonal": BASIS_NEUMANN0_ZONAL}
 SOLVER_DST3, SOLVER_DST2_TRIDIAG = 0, 1
 SOLVERS = {"dst3": SOLVER_DST3, "dst2_tridiag": SOLVER_DST2_TRIDIAG}
 SETS = {"mplus": 0, "gamma": 1, "gamma_in": 2, "gamma_ex": 3, "band": 4, "nplus": 5}

@@ -43,7 +43,9 @@ class DPM:
         g = L.Grid(n, lo, hi)
         d = L.Domain(L.SPHERE if kind == "sphere" else L.ELLIPSOID, (C.c_double * 3)(*center),
                      (C.c_double * 3)(*semi))
-        b = L.BASIS_CAUCHY if basis == "cauchy" else L.BASIS_NEUMANN0
+        if basis not in L.BASES:
+            raise ValueError(f"basis must be one of {sorted(L.BASES)}, got {basis!r}")
+        b = L.BASES[basis]
         h = C.c_void_p()
         torch.cuda.init()
         L.check(L.lib.dpm_create(C.byref(g), C.byref(d), lmax, dt, b, device, C.byref(h)))

@@ -4,6 +4,8 @@ Tolerances (BASELINE.json north_star): relative L∞ = max|a-b|/max|
 b = oracle; AP solves, P_γE, B, u_γ <= 1e-11; C <= 1e-10; PKS ρ, c <= 1e-9; dt <= 1e-12;
 point sets bit-exact.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -183,6 +185,46 @@ def test_extension_matrix(api, name):
     assert rel(Eg, E) <= 1e-12
 
 
+@pytest.mark.parametrize("name,basis,lmax", [("cfg1", "cauchy_zonal", 12), ("cfg2", "neumann0_zonal", 60),
+                                              ("cfg3", "neumann0_zonal", 400), ("cfg4", "cauchy_zonal", 1000)])
+def test_extension_matrix_zonal(api, name, basis, lmax):
+    # the paper's zonal basis up to DPM_MAX_ZONAL_L; the sphere and the ellipsoid
+    cfg = dataclasses.replace(get_config(name), basis=basis, lmax=lmax)
+    c = api.DPM.from_config(cfg)
+    assert c.K == 2 * (lmax + 1) == cfg.K
+    g, ps = grid.point_sets_for(cfg)
+    E, d, unit, foot = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.basis)
+    Eg, dg = c.copy_extension()
+    assert rel(Eg, E) <= 1e-12
+
+
+def test_zonal_basis_limits(api):
+    cfg = get_config("cfg2")
+    with pytest.raises(ValueError):
+        api.DPM.from_config(dataclasses.replace(cfg, basis="zonal"))
+    with pytest.raises(RuntimeError):
+        api.DPM.from_config(dataclasses.replace(cfg, basis="cauchy_zonal", lmax=1001))
+    with pytest.raises(RuntimeError):
+        api.DPM.from_config(dataclasses.replace(cfg, basis="cauchy", lmax=41))
+
+
+def test_cfg1_outputs_zonal(api):
+    # cfg1 with the paper's zonal 2-term basis (K = 26): P_γE, B, C, u_γ against the oracle
+    cfg = dataclasses.replace(get_config("cfg1"), basis="cauchy_zonal", lmax=12)
+    o = dpm.cfg1_outputs(cfg)
+    c = api.DPM.from_config(cfg)
+    PgE, B = c.build_projection()
+    assert rel(PgE.cpu().numpy().T, o["PgE"]) <= 1e-11
+    assert rel(B.cpu().numpy().T, o["B"]) <= 1e-11
+    mp = c.copy_set("mplus")
+    q = np.zeros(cfg.n ** 3)
+    q[mp] = cfg1_particular_values(len(mp))
+    up = c.aux_solve_batch(torch.from_numpy(q.reshape(1, cfg.n, cfg.n, cfg.n)).cuda())
+    coef, ug = c.boundary_lsq(c.trace(up, "gamma_in"))
+    assert rel(coef.cpu().numpy()[0], o["C"]) <= 1e-10
+    assert rel(ug.cpu().numpy()[0], o["E"] @ o["C"]) <= 1e-11
+
+
 # ------------------------------------------------------------------ S2/S4 kernels
 def test_potential_rhs_and_trace(api):
     cfg = get_config("cfg2")
@@ -346,6 +388,18 @@ def test_pks_parity(api, name, dt_rule):
         assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
         assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
     assert sum(l["rebuilt"] for l in logs) == o.builds
+
+
+def test_pks_parity_zonal(api):
+    # cfg2 with the paper's zonal 3-term basis {P_l^0, d²/2 P_l^0}, L = 6 (K = 14)
+    cfg = dataclasses.replace(get_config("cfg2"), basis="neumann0_zonal")
+    o = pks.PKSOracle(cfg, dt_rule=0)
+    rho0, rho, cc, logs = run_pks_gpu(api, cfg, 0)
+    ro, co, ologs = o.run()
+    assert rel(rho, ro) <= 1e-9, rel(rho, ro)
+    assert rel(cc, co) <= 1e-9, rel(cc, co)
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
 
 
 # ------------------------------------------------------------------ cfg4 at full size (bench launch config)

@@ -1,4 +1,4 @@
-"""Pins for oracle/sh.py (real SH, R8) and oracle/geometry.py (feet, d, angles; R10)."""
+"""Pins for oracle/sh.py (real SH, R8; zonal modes) and oracle/geometry.py (feet, d, angles; R10)."""
 import math
 
 import numpy as np
@@ -87,3 +87,48 @@ def test_ellipsoid_cfg3_geometry():
     gin = ps.gamma_in.ravel()[ps.list("gamma")]
     assert np.array_equal(d < 0, gin)
     assert np.abs(d).max() < 2 * g.h
+
+
+# ------------------------------------------------------------------ zonal modes
+def test_zonal_closed_forms_and_endpoints():
+    x = np.linspace(-1, 1, 41)
+    u = np.stack([np.sqrt(1 - x * x), np.zeros_like(x), x], axis=1)
+    P = sh.zonal(5, u)
+    assert np.array_equal(P[:, 0], np.ones_like(x))
+    assert np.allclose(P[:, 1], x, atol=1e-16)
+    assert np.allclose(P[:, 2], (3 * x ** 2 - 1) / 2, atol=1e-15)
+    assert np.allclose(P[:, 3], (5 * x ** 3 - 3 * x) / 2, atol=1e-15)
+    assert np.allclose(P[:, 4], (35 * x ** 4 - 30 * x ** 2 + 3) / 8, atol=1e-15)
+    L = 500   # P_l(1) = 1, P_l(-1) = (-1)^l (the paper's Test B uses up to 500 harmonics)
+    E = sh.zonal(L, np.array([[0.0, 0.0, 1.0], [0.0, 0.0, -1.0]]))
+    assert np.abs(E[0] - 1).max() < 1e-12
+    assert np.abs(E[1] - (-1.0) ** np.arange(L + 1)).max() < 1e-12
+
+
+def test_zonal_vs_scipy_and_orthogonality():
+    rng = np.random.default_rng(11)
+    v = rng.normal(size=(200, 3))
+    u = v / np.linalg.norm(v, axis=1)[:, None]
+    L = 300
+    P = sh.zonal(L, u)
+    for l in (0, 1, 2, 7, 40, 150, 300):
+        assert np.abs(P[:, l] - scipy.special.eval_legendre(l, u[:, 2])).max() < 1e-12, l
+    # ∫_{-1}^{1} P_l P_m dx = 2/(2l+1) δ_lm, exactly by Gauss-Legendre with L+1 nodes
+    x, w = np.polynomial.legendre.leggauss(61)
+    Q = sh.zonal(60, np.stack([np.sqrt(1 - x * x), 0 * x, x], axis=1))
+    G = (Q * w[:, None]).T @ Q
+    assert np.abs(G - np.diag(2.0 / (2 * np.arange(61) + 1))).max() < 1e-13
+    # the m = 0 real SH are the normalised zonal modes (R8): Y_l0 = sqrt((2l+1)/(4π)) P_l
+    Y = sh.real_sh(12, u)
+    for l in range(13):
+        assert np.abs(Y[:, l * l + l] - math.sqrt((2 * l + 1) / (4 * math.pi)) * P[:, l]).max() < 1e-13
+
+
+def test_zonal_extension_matrix_layout():
+    cfg = get_config("cfg2")
+    g, ps = grid.point_sets_for(cfg)
+    E, d, unit, foot = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, 9, "neumann0_zonal")
+    assert E.shape == (len(ps.list("gamma")), 20)
+    P = scipy.special.eval_legendre(np.arange(10)[None, :], unit[:, 2:3])
+    assert np.abs(E[:, :10] - P).max() < 1e-13
+    assert np.abs(E[:, 10:] - 0.5 * d[:, None] ** 2 * P).max() < 1e-15
