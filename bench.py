@@ -294,6 +294,16 @@ def bench_bep(api, torch, reps=3):
     return res
 
 
+def bench_test_b(N=127, harmonics=150):
+    """NEXT-4: the paper's Test B single domain, the
+    Step-4b-every-step regime near blow-up: PKS steps until Δ||ρ||∞ >= 1000; blow-up time
+    against the paper's t_min (Table 7), steps/s of the whole run including the rebuilds."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+    import test_b
+    res, logs = test_b.run(N, harmonics)
+    return res
+
+
 def bench_dd(api, torch, world, rank, steps=None, reps=5):
     """cfg5: the 8-octant DD (R24) — octants sharded over the ranks (8/world each), the global
     least squares and dt through NCCL all-reduces (DDSolver).  The 50-step loop is repeated `reps`
@@ -517,6 +527,7 @@ def main():
                        "cfg3": bench_pks(api, torch, "cfg3", hbm_peak=hbm_peak)}
         line["cfg1"] = bench_cfg1(api, torch)
         line["bep_rebuild_cfg4"] = bench_bep(api, torch)
+        line["test_b"] = bench_test_b()
 
     if not args.no_dd and 8 % world == 0:
         try:

@@ -30,7 +30,8 @@ class Config:
 
     @property
     def K(self) -> int:
-        return 2 * (self.lmax + 1) if self.basis.endswith("_zonal") else 2 * (self.lmax + 1) ** 2
+        nb = self.lmax + 1 if self.basis.endswith("_zonal") else (self.lmax + 1) ** 2
+        return nb if self.basis.startswith("neumann0_2term") else 2 * nb
 
 
 CONFIGS = {
@@ -51,3 +52,22 @@ CONFIGS = {
 
 def get_config(name: str) -> Config:
     return CONFIGS[name]
+
+
+def paper_mesh(N: int, r: float):
+    """The paper's single-domain mesh: N cells per axis on [-r-2h, r+2h]^3, h = 2r/(N-4),
+    cell centres at -r-2h + (j-1/2)h.  In this repo's convention (R1: box faces = ghost nodes,
+    n unknowns, node i at lo + (i+1)h) that is n = N, lo = -r - 5h/2, hi = r + 5h/2."""
+    h = 2.0 * r / (N - 4)
+    return N, -r - 2.5 * h, r + 2.5 * h, h
+
+
+def test_b_config(N: int = 127, harmonics: int = 150) -> Config:
+    """The paper's Test B, single domain: sphere r = 0.5 at the origin,
+    rho0 = 2000 exp(-100 (x^2 + y^2 + (z - 0.25)^2)), c0 = 0; the 2-term extension with zero
+    Neumann data (beta = 0) and `harmonics` zonal modes; dt = 0.5 h^2 before blow-up
+    and the CFL rule after."""
+    n, lo, hi, h = paper_mesh(N, 0.5)
+    return Config(f"testB{N}", n, lo, hi, "sphere", (0.0, 0.0, 0.0), (0.5, 0.5, 0.5), harmonics - 1,
+                  "neumann0_2term_zonal", 0.5 * h * h, ic_center=(0.0, 0.0, 0.25), ic_rho=(2000.0, 100.0),
+                  ic_c=(0.0, 1.0))

@@ -43,7 +43,7 @@ typedef enum {
   DPM_ERR_NONFINITE = 6  /* a PKS step produced a non-finite value                         */
 } dpm_status;
 
-#define DPM_MAX_N 128    /* largest n the AP-solve kernels are instantiated for            */
+#define DPM_MAX_N 256    /* largest n the AP-solve kernels are instantiated for            */
 
 typedef struct { int32_t n; double lo, hi; } dpm_grid;
 
@@ -58,9 +58,14 @@ typedef struct { int32_t kind; double center[3]; double semi[3]; } dpm_domain;
    The *_ZONAL sets are the paper's own basis (only the zonal modes
    phi_nu = P_nu^0(cos θ), the unnormalised Legendre polynomial of the foot point's polar
    angle about +z): K = 2 (lmax+1) columns, c = comp*(lmax+1) + l, same comp rule;
-   lmax <= DPM_MAX_ZONAL_L (the paper's Test B uses up to 500 harmonics). */
+   lmax <= DPM_MAX_ZONAL_L (the paper's Test B uses up to 500 harmonics).
+   NEUMANN0 is the 3-term extension (beta = 1 in P:263-267) with du/dn = 0;
+   the *_2TERM sets are the 2-term extension with du/dn = 0 (beta = 0: pi = u|Γ, the d-term
+   vanishes), one component: K = (lmax+1)^2 or (lmax+1) (zonal), c = nu or l.  The
+   paper uses it for Test B. */
 typedef enum {
-  DPM_BASIS_CAUCHY = 0, DPM_BASIS_NEUMANN0 = 1, DPM_BASIS_CAUCHY_ZONAL = 2, DPM_BASIS_NEUMANN0_ZONAL = 3
+  DPM_BASIS_CAUCHY = 0, DPM_BASIS_NEUMANN0 = 1, DPM_BASIS_CAUCHY_ZONAL = 2, DPM_BASIS_NEUMANN0_ZONAL = 3,
+  DPM_BASIS_NEUMANN0_2TERM = 4, DPM_BASIS_NEUMANN0_2TERM_ZONAL = 5
 } dpm_basis;
 #define DPM_MAX_ZONAL_L 1000
 

@@ -9,7 +9,8 @@ Literal definitions, column by column (no fusion, no batching tricks):
 * extension operator with spectral Cauchy data:
   columns c = comp*(L+1)^2 + ν (R9): comp 0 -> Y_ν(foot);
   comp 1 -> d Y_ν ("cauchy", 2-term u, du/dn) or (d^2/2) Y_ν ("neumann0", P:273-275);
-  "*_zonal": Y_ν replaced by the paper's zonal modes P_l^0(cos θ), l = 0..L, K = 2 (L+1).
+  "*_zonal": Y_ν replaced by the paper's zonal modes P_l^0(cos θ), l = 0..L (P:293), K = 2 (L+1);
+  "neumann0_2term[_zonal]": the 2-term extension (β = 0) with ∂u/∂n = 0, comp 0 only.
 * reduced BEP (`eqn:BEP_recast` P:287-290): B = Tr_γin (E - P_γ E).
 * least squares: numpy.linalg.lstsq (SVD) and an independent plain
   Householder QR (``householder_lstsq``) used as a cross-check.
@@ -34,6 +35,8 @@ def extension_matrix(g, ps, kind, center, semi, lmax, basis):
     P = gamma_points(g, ps)
     foot, d, unit = geometry.geometry(P, kind, center, semi)
     Y = sh.zonal(lmax, unit) if basis.endswith("_zonal") else sh.real_sh(lmax, unit)
+    if basis in ("neumann0_2term", "neumann0_2term_zonal"):   # β = 0 with ∂u/∂n = 0: π = u|Γ
+        return Y, d, unit, foot
     if basis in ("cauchy", "cauchy_zonal"):
         second = d[:, None] * Y
     elif basis in ("neumann0", "neumann0_zonal"):

@@ -18,8 +18,10 @@ STATUS = {0: "DPM_OK", 1: "DPM_ERR_INVALID", 2: "DPM_ERR_OOM", 3: "DPM_ERR_CUDA"
           5: "DPM_ERR_RANK", 6: "DPM_ERR_NONFINITE"}
 SPHERE, ELLIPSOID = 0, 1
 BASIS_CAUCHY, BASIS_NEUMANN0, BASIS_CAUCHY_ZONAL, BASIS_NEUMANN0_ZONAL = 0, 1, 2, 3
+BASIS_NEUMANN0_2TERM, BASIS_NEUMANN0_2TERM_ZONAL = 4, 5
 BASES = {"cauchy": BASIS_CAUCHY, "neumann0": BASIS_NEUMANN0,
-         "cauchy_zonal": BASIS_CAUCHY_ZONAL, "neumann0_zonal": BASIS_NEUMANN0_ZONAL}
+         "cauchy_zonal": BASIS_CAUCHY_ZONAL, "neumann0_zonal": BASIS_NEUMANN0_ZONAL,
+         "neumann0_2term": BASIS_NEUMANN0_2TERM, "neumann0_2term_zonal": BASIS_NEUMANN0_2TERM_ZONAL}
 SOLVER_DST3, SOLVER_DST2_TRIDIAG = 0, 1
 SOLVERS = {"dst3": SOLVER_DST3, "dst2_tridiag": SOLVER_DST2_TRIDIAG}
 SETS = {"mplus": 0, "gamma": 1, "gamma_in": 2, "gamma_ex": 3, "band": 4, "nplus": 5}

@@ -73,8 +73,8 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   if (grid->n < 4 || grid->n > DPM_MAX_N) { g_create_err = "n out of range [4, DPM_MAX_N]"; return DPM_ERR_INVALID; }
   if (!(grid->lo < grid->hi)) { g_create_err = "lo >= hi"; return DPM_ERR_INVALID; }
   if (!(dt > 0) || !std::isfinite(dt)) { g_create_err = "dt must be > 0"; return DPM_ERR_INVALID; }
-  if (basis < DPM_BASIS_CAUCHY || basis > DPM_BASIS_NEUMANN0_ZONAL) { g_create_err = "bad basis"; return DPM_ERR_INVALID; }
-  const bool zonal = basis == DPM_BASIS_CAUCHY_ZONAL || basis == DPM_BASIS_NEUMANN0_ZONAL;
+  if (basis < DPM_BASIS_CAUCHY || basis > DPM_BASIS_NEUMANN0_2TERM_ZONAL) { g_create_err = "bad basis"; return DPM_ERR_INVALID; }
+  const bool zonal = basis_zonal(basis);
   if (lmax < 0 || lmax > (zonal ? DPM_MAX_ZONAL_L : 40)) { g_create_err = "lmax out of range"; return DPM_ERR_INVALID; }
   if (cudaSetDevice(device) != cudaSuccess) { g_create_err = "cudaSetDevice failed"; return DPM_ERR_CUDA; }
   dpm_ctx* ctx = new (std::nothrow) dpm_ctx();
@@ -89,7 +89,7 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   if (domain->kind == DPM_SPHERE) ctx->domain.semi[1] = ctx->domain.semi[2] = domain->semi[0];
   ctx->lmax = lmax;
   ctx->basis = basis;
-  ctx->K = zonal ? 2 * (lmax + 1) : 2 * (lmax + 1) * (lmax + 1);
+  ctx->K = basis_ncomp(basis) * (zonal ? lmax + 1 : (lmax + 1) * (lmax + 1));
   dpm_status st = DPM_OK;
   if (cudaStreamCreateWithFlags(&ctx->setup_stream, cudaStreamNonBlocking) != cudaSuccess) st = DPM_ERR_CUDA;
   if (st == DPM_OK) st = setup_point_sets(ctx);

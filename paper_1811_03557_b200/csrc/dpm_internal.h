@@ -210,6 +210,12 @@ cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, i
 // dd.cu (octant DD setup)
 dpm_status dd_setup(dpm_ctx* ctx);
 // dpm_abi.cu
+// extension column sets (dpm.h dpm_basis): zonal modes only / number of components (1 or 2)
+__host__ __device__ inline bool basis_zonal(int b) {
+  return b == DPM_BASIS_CAUCHY_ZONAL || b == DPM_BASIS_NEUMANN0_ZONAL || b == DPM_BASIS_NEUMANN0_2TERM_ZONAL;
+}
+__host__ __device__ inline int basis_ncomp(int b) { return b == DPM_BASIS_NEUMANN0_2TERM || b == DPM_BASIS_NEUMANN0_2TERM_ZONAL ? 1 : 2; }
+
 dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
                            int32_t device, dpm_ctx** out);
 double decode_key(double slot);   // order-preserving key of the reduction slots -> value

@@ -39,7 +39,13 @@ namespace {
 
 constexpr int NW = 8;         // warps per CTA
 constexpr int NT = NW * 32;   // threads per CTA
-constexpr int KSMAX_ALL = 16; // k-steps of the largest instance (n <= 128)
+constexpr int KSMAX_ALL = 16; // k-steps of the largest register-fragment instance (n <= 128)
+// n in (128, 256] (the paper's N = 255 / 260 meshes): 4 m-tiles per warp and 32 k-steps, i.e. 128
+// A values per lane - too many for registers, so those fragments are read from the (L1/L2-resident)
+// table inside the MMA loop, each one reused over the warp's column tiles.
+constexpr int MT_BIG = 4, KS_BIG = 32;
+__host__ __device__ constexpr int mt_of(int n) { return n > 128 ? MT_BIG : 2; }
+__host__ __device__ constexpr int ks_of(int n) { return n > 128 ? KS_BIG : KSMAX_ALL; }
 
 __host__ __device__ constexpr int ldx_of(int tc) { return tc + 4; }            // ≡ 4 mod 16 for tc % 16 == 0
 __host__ __device__ constexpr int ldz_of(int n) { return ((n + 15) / 16) * 16 + 4; }
@@ -76,8 +82,8 @@ __device__ double fold_entry(int n, int Po, int Pe, int matrix, int m, int j) {
 
 struct WarpRole {
   int matrix;   // 0 odd / 1 even
-  int nmt;      // m-tiles owned (0..2)
-  int mt[2];    // local m-tile indices
+  int nmt;      // m-tiles owned (0..MT_BIG)
+  int mt[MT_BIG];   // local m-tile indices
   int nct;      // column tiles handled
   int ct0, ctstep;
 };
@@ -86,9 +92,19 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   WarpRole r;
   r.matrix = warp >> 2;
   const int wl = warp & 3;
-  if (MTh >= 4) {
+  if (MTh > 8) {   // n > 128: m-tiles wl, wl + 4, wl + 8, wl + 12
+    r.nmt = 0;
+    for (int t = 0; t < MT_BIG; ++t) {
+      r.mt[t] = wl + 4 * t;
+      if (wl + 4 * t < MTh) r.nmt = t + 1;
+    }
+    r.ct0 = 0;
+    r.ctstep = 1;
+    r.nct = NCT;
+  } else if (MTh >= 4) {
     r.mt[0] = wl;
     r.mt[1] = wl + 4;
+    r.mt[2] = r.mt[3] = 0;
     r.nmt = (wl + 4 < MTh) ? 2 : 1;
     r.ct0 = 0;
     r.ctstep = 1;
@@ -97,7 +113,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
     const int G = 4 / MTh;
     const int cg = wl / MTh;
     r.mt[0] = wl % MTh;
-    r.mt[1] = 0;
+    r.mt[1] = r.mt[2] = r.mt[3] = 0;
     r.nmt = (cg < G) ? 1 : 0;
     r.ct0 = cg;
     r.ctstep = G;
@@ -106,15 +122,16 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   return r;
 }
 
-// A-fragment table: tab[((warp*2 + t)*KSMAX_ALL + ks)*32 + lane], built once per plan.
+// A-fragment table: tab[((warp*mt_of(n) + t)*ks_of(n) + ks)*32 + lane], built once per plan.
 __global__ void afrag_table_kernel(double* tab, int n, int NCT) {
   const int warp = blockIdx.x, t = blockIdx.y, ks = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int MTM = mt_of(n), KSM = ks_of(n);
   const int Po = (n + 1) / 2, Pe = n / 2, MTh = (Po + 7) / 8, KS = (Po + 3) / 4;
   const WarpRole role = warp_role(warp, MTh, NCT);
   double v = 0.0;
   if (t < role.nmt && ks < KS)
     v = fold_entry(n, Po, Pe, role.matrix, role.mt[t] * 8 + (lane >> 2), ks * 4 + (lane & 3));
-  tab[((warp * 2 + t) * KSMAX_ALL + ks) * 32 + lane] = v;
+  tab[((warp * MTM + t) * KSM + ks) * 32 + lane] = v;
 }
 
 // Compile-time geometry when NFIX > 0 (n = NFIX); runtime otherwise.
@@ -139,10 +156,10 @@ extern __shared__ __align__(16) double sm[];
 // Element (row r, col c) lives at sm[base + r*rs + c*cs].  If DIVIDE, the epilogue multiplies
 // output (row k, column c) by scale / (((inv_dt + lam[a]) + lam[b]) + lam[k]) with
 // (a, b) = divmod(col0 + c, n) (pass Z after X and Y: spectral indices).
-template <int NFIX, int KSMAX, int TC, int PASS, bool DIVIDE>
+template <int NFIX, int KSMAX, int TC, int PASS, bool DIVIDE, int MT>
 __device__ __forceinline__ void fold_transform(const Geo<NFIX, TC, PASS>& G, int base, const WarpRole& role,
-                                               const double (&afr)[2][KSMAX], const double* lam, double inv_dt,
-                                               double scale, int col0) {
+                                               const double (&afr)[2][MT == 2 ? KSMAX : 1], const double* atw,
+                                               const double* lam, double inv_dt, double scale, int col0) {
   constexpr int NCT = TC / 8;
   constexpr bool ROWS_FAST = PASS == 2;
   const int n = G.n, Po = G.Po, Pe = G.Pe, rs = G.rs, cs = G.cs;
@@ -160,9 +177,9 @@ __device__ __forceinline__ void fold_transform(const Geo<NFIX, TC, PASS>& G, int
   }
   __syncthreads();
 
-  double acc[2][NCT][2];
+  double acc[MT][NCT][2];
 #pragma unroll
-  for (int t = 0; t < 2; ++t)
+  for (int t = 0; t < MT; ++t)
 #pragma unroll
     for (int ct = 0; ct < NCT; ++ct) acc[t][ct][0] = acc[t][ct][1] = 0.0;
 
@@ -179,10 +196,14 @@ __device__ __forceinline__ void fold_transform(const Geo<NFIX, TC, PASS>& G, int
 #pragma unroll
         for (int ct = 0; ct < NCT; ++ct) b[ct] = (ct < role.nct) ? sm[rowb + ct * cstep] : 0.0;
 #pragma unroll
-        for (int t = 0; t < 2; ++t)
+        for (int t = 0; t < MT; ++t) {
+          double a;
+          if constexpr (MT == 2) a = afr[t][ks];
+          else a = t < role.nmt ? __ldg(atw + (t * KSMAX + ks) * 32) : 0.0;
 #pragma unroll
           for (int ct = 0; ct < NCT; ++ct)
-            if (t < role.nmt && ct < role.nct) dmma884(acc[t][ct], afr[t][ks], b[ct]);
+            if (t < role.nmt && ct < role.nct) dmma884(acc[t][ct], a, b[ct]);
+        }
       }
     }
   }
@@ -191,7 +212,7 @@ __device__ __forceinline__ void fold_transform(const Geo<NFIX, TC, PASS>& G, int
   if (role.nmt > 0) {
     const int P = role.matrix == 0 ? Po : Pe;
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < MT; ++t) {
       if (t >= role.nmt) continue;
       const int m = role.mt[t] * 8 + (lane >> 2);
       if (m >= P) continue;
@@ -296,9 +317,9 @@ __device__ __forceinline__ void store_tile(const Geo<NFIX, TC, PASS>& G, int bas
 }
 
 template <int KSMAX, int TC>
-constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) ? 1 : 2; }
+constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) || KSMAX > 16 ? 1 : 2; }
 
-template <int NFIX, int KSMAX, int TC, int PASS, int VEC>
+template <int NFIX, int KSMAX, int TC, int PASS, int VEC, int MT = 2>
 __global__ void __launch_bounds__(NT, min_blocks<KSMAX, TC>())
 dst_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields, int n_rt,
                 const double* __restrict__ lam_g, const double* __restrict__ atab, double inv_dt, double scale) {
@@ -310,11 +331,14 @@ dst_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfi
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const WarpRole role = warp_role(warp, G.MTh, TC / 8);
-  double afr[2][KSMAX];
+  double afr[2][MT == 2 ? KSMAX : 1];
+  const double* atw = atab + (size_t)warp * MT * KSMAX * 32 + lane;   // MT_BIG: read in the MMA loop
+  if constexpr (MT == 2) {
 #pragma unroll
-  for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < 2; ++t)
 #pragma unroll
-    for (int ks = 0; ks < KSMAX; ++ks) afr[t][ks] = __ldg(atab + ((warp * 2 + t) * KSMAX_ALL + ks) * 32 + lane);
+      for (int ks = 0; ks < KSMAX; ++ks) afr[t][ks] = __ldg(atab + ((warp * 2 + t) * KSMAX_ALL + ks) * 32 + lane);
+  }
 
   const int nn = n * n;
   const int tiles_per_field = (nn + TC - 1) / TC;
@@ -340,21 +364,21 @@ dst_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfi
     const int f = (int)(tile / tiles_per_field);
     const int col0 = (int)(tile - (long)f * tiles_per_field) * TC;
     const int base = cur * G.tile_elems;
-    fold_transform<NFIX, KSMAX, TC, PASS, PASS == 2>(G, base, role, afr, lam, inv_dt, scale, col0);
-    if (PASS == 2) fold_transform<NFIX, KSMAX, TC, PASS, false>(G, base, role, afr, lam, inv_dt, scale, col0);
+    fold_transform<NFIX, KSMAX, TC, PASS, PASS == 2, MT>(G, base, role, afr, atw, lam, inv_dt, scale, col0);
+    if (PASS == 2) fold_transform<NFIX, KSMAX, TC, PASS, false, MT>(G, base, role, afr, atw, lam, inv_dt, scale, col0);
     store_tile<NFIX, TC, PASS, VEC>(G, base, out + (size_t)f * field, col0);
     __syncthreads();
   }
 }
 
-template <int NFIX, int KSMAX, int TC, int VEC>
+template <int NFIX, int KSMAX, int TC, int VEC, int MT = 2>
 cudaError_t run_pass_t(int pass, const double* in, double* out, int nfields, int n, const double* lam,
                        const double* atab, double inv_dt, double scale, cudaStream_t s) {
   const size_t tile = (size_t)(pass < 2 ? n * ldx_of(TC) : TC * ldz_of(n));
   const size_t smem = 2 * tile * 8 + (size_t)n * 8;
   void (*k)(const double*, double*, int, int, const double*, const double*, double, double) =
-      pass == 0 ? dst_pass_kernel<NFIX, KSMAX, TC, 0, VEC>
-                : pass == 1 ? dst_pass_kernel<NFIX, KSMAX, TC, 1, VEC> : dst_pass_kernel<NFIX, KSMAX, TC, 2, VEC>;
+      pass == 0 ? dst_pass_kernel<NFIX, KSMAX, TC, 0, VEC, MT>
+                : pass == 1 ? dst_pass_kernel<NFIX, KSMAX, TC, 1, VEC, MT> : dst_pass_kernel<NFIX, KSMAX, TC, 2, VEC, MT>;
   static int sms = 0;
   static int occ[3] = {0, 0, 0};
   static size_t occ_smem[3] = {0, 0, 0};
@@ -387,7 +411,7 @@ int tc128() {
   return v;
 }
 
-int tc_for(int n) { return n == 128 ? tc128() : (n > 64 ? 64 : 32); }
+int tc_for(int n) { return n == 128 ? tc128() : (n > 128 ? 32 : (n > 64 ? 64 : 32)); }
 
 cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, int nfields, double inv_dt,
                      double scale, cudaStream_t s) {
@@ -406,6 +430,10 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
   if (KS <= 8) {
     return even ? run_pass_t<0, 8, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
                 : run_pass_t<0, 8, 32, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
+  }
+  if (n > 128) {   // 128 < n <= 256: TC = 32 (two 74 KB tiles), A fragments from the table
+    return even ? run_pass_t<0, KS_BIG, 32, 2, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
+                : run_pass_t<0, KS_BIG, 32, 1, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
   }
   return even ? run_pass_t<0, 16, 64, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
               : run_pass_t<0, 16, 64, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
@@ -434,7 +462,7 @@ __device__ __forceinline__ double ipow(double b, int e) {   // b^e, e >= 0
   return r;
 }
 
-template <int NFIX>
+template <int NFIX, int PER = 4>
 __global__ void __launch_bounds__(256)
 ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __restrict__ lam_g, double inv_dt,
                  double h2, double rscale) {
@@ -444,34 +472,39 @@ ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __r
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int w0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
-  const int nn = n * n, k0 = 4 * lane;
+  const int nn = n * n, k0 = PER * lane;
   for (int line = w0; line < nlines; line += nw) {   // nlines < 2^31 (checked by the launcher)
     double* L = u + (size_t)line * n;
-    double r[4];
-    if (NFIX == 128) {
-      const double2 a = __ldcg(reinterpret_cast<const double2*>(L + k0));
-      const double2 b = __ldcg(reinterpret_cast<const double2*>(L + k0 + 2));
-      r[0] = a.x; r[1] = a.y; r[2] = b.x; r[3] = b.y;
+    double r[PER];
+    if (NFIX == 32 * PER) {
+#pragma unroll
+      for (int i = 0; i < PER; i += 2) {
+        const double2 a = __ldcg(reinterpret_cast<const double2*>(L + k0 + i));
+        r[i] = a.x;
+        r[i + 1] = a.y;
+      }
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) r[i] = k0 + i < n ? __ldcg(L + k0 + i) : 0.0;
+      for (int i = 0; i < PER; ++i) r[i] = k0 + i < n ? __ldcg(L + k0 + i) : 0.0;
     }
     const int lf = line % nn;
     const double hs = h2 * ((inv_dt + lam[lf / n]) + lam[lf % n]);
     const double disc = sqrt(hs * (hs + 4.0));
     const double mu = 2.0 / ((2.0 + hs) + disc);
-    const double mu2 = mu * mu, mu3 = mu2 * mu, mu4 = mu2 * mu2;
-    double mp[5];   // μ^{4·2^s}
-    mp[0] = mu4;
+    double mpow[PER + 1];   // μ^0 .. μ^PER
+    mpow[0] = 1.0;
+#pragma unroll
+    for (int i = 1; i <= PER; ++i) mpow[i] = mpow[i - 1] * mu;
+    double mp[5];   // μ^{PER·2^s}
+    mp[0] = mpow[PER];
 #pragma unroll
     for (int q = 1; q < 5; ++q) mp[q] = mp[q - 1] * mp[q - 1];
     // forward y_k = r_k + μ y_{k-1}
-    double y[4];
+    double y[PER];
     y[0] = rscale * r[0];
-    y[1] = fma(mu, y[0], rscale * r[1]);
-    y[2] = fma(mu, y[1], rscale * r[2]);
-    y[3] = fma(mu, y[2], rscale * r[3]);
-    double C = y[3];
+#pragma unroll
+    for (int i = 1; i < PER; ++i) y[i] = fma(mu, y[i - 1], rscale * r[i]);
+    double C = y[PER - 1];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
       const double t = __shfl_up_sync(0xffffffffu, C, 1 << q);
@@ -479,19 +512,16 @@ ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __r
     }
     double cin = __shfl_up_sync(0xffffffffu, C, 1);
     cin = lane == 0 ? 0.0 : cin;
-    y[0] = fma(mu, cin, y[0]);
-    y[1] = fma(mu2, cin, y[1]);
-    y[2] = fma(mu3, cin, y[2]);
-    y[3] = fma(mu4, cin, y[3]);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < PER; ++i) y[i] = fma(mpow[i + 1], cin, y[i]);
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
       if (k0 + i >= n) y[i] = 0.0;   // padding beyond the line: ghost values
     // backward z_k = y_k + μ z_{k+1}
-    double z[4];
-    z[3] = y[3];
-    z[2] = fma(mu, z[3], y[2]);
-    z[1] = fma(mu, z[2], y[1]);
-    z[0] = fma(mu, z[1], y[0]);
+    double z[PER];
+    z[PER - 1] = y[PER - 1];
+#pragma unroll
+    for (int i = PER - 2; i >= 0; --i) z[i] = fma(mu, z[i + 1], y[i]);
     double D = z[0];
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
@@ -500,15 +530,14 @@ ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __r
     }
     double din = __shfl_down_sync(0xffffffffu, D, 1);
     din = lane == 31 ? 0.0 : din;
-    z[3] = fma(mu, din, z[3]);
-    z[2] = fma(mu2, din, z[2]);
-    z[1] = fma(mu3, din, z[1]);
-    z[0] = fma(mu4, din, z[0]);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) z[i] = fma(mpow[PER - i], din, z[i]);
     // T^{-1} r = μ z - c2 (μ^{k+1} - μ^{2n+1-k}),  c2 = μ^2 z_0 / (1 - μ^{2n+2})
     // (Sherman–Morrison with s = A^{-1} e_1 in closed form; (1 + μ s_0)(1 - μ^2) = 1 - μ^{2n+2}).
-    // Powers by binary exponentiation over the lane bits with the μ^{4·2^s} table:
-    //   μ^{k0+1} = μ · μ^{4 lane},   μ^{2n-2-k0} = μ^{E} · μ^{4(NL-1-lane)},  E = 2n + 2 - 4 NL >= n - 1.
-    const int NL = (n + 3) >> 2;   // lanes holding line data
+    // Powers by binary exponentiation over the lane bits with the μ^{PER·2^s} table:
+    //   μ^{k0+1} = μ · μ^{PER lane},  μ^{2n+2-PER-k0} = μ^{E} · μ^{PER(NL-1-lane)},
+    //   E = 2n + 2 - PER·NL >= n + 3 - PER.
+    const int NL = (n + PER - 1) / PER;   // lanes holding line data
     const int lr = max(0, NL - 1 - lane);
     double P1 = 1.0, P2 = 1.0;
 #pragma unroll
@@ -516,23 +545,21 @@ ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __r
       P1 *= (lane >> q) & 1 ? mp[q] : 1.0;
       P2 *= (lr >> q) & 1 ? mp[q] : 1.0;
     }
-    const double muE = ipow(mu, 2 * n + 2 - 4 * NL);                 // warp-uniform exponent
-    const double mu4L = __shfl_sync(0xffffffffu, P1, NL - 1) * mu4;   // μ^{4 NL}
-    const double mu2n2 = muE * mu4L;                                  // μ^{2n+2}
+    const double muE = ipow(mu, 2 * n + 2 - PER * NL);                         // warp-uniform exponent
+    const double muPL = __shfl_sync(0xffffffffu, P1, NL - 1) * mpow[PER];      // μ^{PER NL}
+    const double mu2n2 = muE * muPL;                                           // μ^{2n+2}
     const double zf = __shfl_sync(0xffffffffu, z[0], 0);
-    const double c2 = mu2 * zf / (1.0 - mu2n2);
+    const double c2 = mpow[2] * zf / (1.0 - mu2n2);
     const double pa = mu * P1, pb = muE * P2;
-    const double pas[4] = {pa, pa * mu, pa * mu2, pa * mu3};
-    const double pbs[4] = {pb * mu3, pb * mu2, pb * mu, pb};
-    double o[4];
+    double o[PER];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = fma(mu, z[i], -c2 * (pas[i] - pbs[i]));
-    if (NFIX == 128) {
-      __stcg(reinterpret_cast<double2*>(L + k0), make_double2(o[0], o[1]));
-      __stcg(reinterpret_cast<double2*>(L + k0 + 2), make_double2(o[2], o[3]));
+    for (int i = 0; i < PER; ++i) o[i] = fma(mu, z[i], -c2 * (pa * mpow[i] - pb * mpow[PER - 1 - i]));
+    if (NFIX == 32 * PER) {
+#pragma unroll
+      for (int i = 0; i < PER; i += 2) __stcg(reinterpret_cast<double2*>(L + k0 + i), make_double2(o[i], o[i + 1]));
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < PER; ++i)
         if (k0 + i < n) __stcg(L + k0 + i, o[i]);
     }
   }
@@ -723,7 +750,7 @@ cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   void (*k)(double*, int, int, const double*, double, double, double) =
-      n == 128 ? ztri_warp_kernel<128> : ztri_warp_kernel<0>;
+      n == 128 ? ztri_warp_kernel<128, 4> : (n > 128 ? ztri_warp_kernel<0, 8> : ztri_warp_kernel<0, 4>);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const long blocks = (nlines + 7) / 8;
@@ -750,11 +777,11 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
   p.dt = dt;
   cudaError_t e = cudaMalloc(&p.lam, sizeof(double) * n);
   if (e != cudaSuccess) return e;
-  e = cudaMalloc(&p.atab, sizeof(double) * NW * 2 * KSMAX_ALL * 32);
+  e = cudaMalloc(&p.atab, sizeof(double) * NW * mt_of(n) * ks_of(n) * 32);
   if (e != cudaSuccess) return e;
   DPM_COUNT_LAUNCH(2);
   eig_kernel<<<(n + 127) / 128, 128>>>(p.lam, n, h);
-  afrag_table_kernel<<<dim3(NW, 2), KSMAX_ALL * 32>>>(p.atab, n, tc_for(n) / 8);
+  afrag_table_kernel<<<dim3(NW, mt_of(n)), ks_of(n) * 32>>>(p.atab, n, tc_for(n) / 8);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (n <= PSN) {   // fused small-n plane pass (DPM_PLANE_SMALL=0 disables)

@@ -162,14 +162,15 @@ __global__ void geometry_sh_kernel(const int64_t* gamma, int64_t ng, int n, doub
   for (int a = 0; a < 3; ++a) foot[g * 3 + a] = X[a] + D.center[a];
   dist[g] = d;
   const double w = (basis == DPM_BASIS_CAUCHY || basis == DPM_BASIS_CAUCHY_ZONAL) ? d : 0.5 * d * d;
-  if (basis == DPM_BASIS_CAUCHY_ZONAL || basis == DPM_BASIS_NEUMANN0_ZONAL) {
+  const bool two = basis_ncomp(basis) == 2;
+  if (basis_zonal(basis)) {
     // phi_l = P_l^0(cos θ), cos θ = u_z; (l+1) P_{l+1} = (2l+1) x P_l - l P_{l-1}
     const double x = u[2];
     double pm = 1.0, pl = x;
     for (int l = 0; l <= lmax; ++l) {
       const double v = l == 0 ? 1.0 : pl;
       E[(size_t)l * ng + g] = v;
-      E[(size_t)(lmax + 1 + l) * ng + g] = w * v;
+      if (two) E[(size_t)(lmax + 1 + l) * ng + g] = w * v;
       if (l >= 1) {
         const double nx = ((2 * l + 1) * x * pl - l * pm) / (l + 1);
         pm = pl;
@@ -181,7 +182,7 @@ __global__ void geometry_sh_kernel(const int64_t* gamma, int64_t ng, int n, doub
   const int nsh = (lmax + 1) * (lmax + 1);
   real_sh_unit(u[0], u[1], u[2], lmax, [&](int nu, double v) {
     E[(size_t)nu * ng + g] = v;
-    E[(size_t)(nsh + nu) * ng + g] = w * v;
+    if (two) E[(size_t)(nsh + nu) * ng + g] = w * v;
   });
 }
 

@@ -132,3 +132,14 @@ def test_zonal_extension_matrix_layout():
     P = scipy.special.eval_legendre(np.arange(10)[None, :], unit[:, 2:3])
     assert np.abs(E[:, :10] - P).max() < 1e-13
     assert np.abs(E[:, 10:] - 0.5 * d[:, None] ** 2 * P).max() < 1e-15
+
+
+def test_two_term_extension_is_first_component():
+    # β = 0 with ∂u/∂n = 0: π = u|Γ, so E is the comp-0 block of the 3-term set
+    cfg = get_config("cfg2")
+    g, ps = grid.point_sets_for(cfg)
+    for full, two in (("neumann0", "neumann0_2term"), ("neumann0_zonal", "neumann0_2term_zonal")):
+        E3 = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, 5, full)[0]
+        E2 = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, 5, two)[0]
+        assert E2.shape[1] * 2 == E3.shape[1]
+        assert np.array_equal(E2, E3[:, :E2.shape[1]])
