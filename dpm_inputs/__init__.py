@@ -17,5 +17,5 @@ Configurations (BASELINE.json ``configs``; readings R1-R31 of SURVEY.md §8(c)):
   spherical shell band of r=1 (R21).
 * cfg5 - 8-octant DD (R24), N=128 per octant (not built in round 1).
 """
-from .configs import CONFIGS, Config, get_config, paper_mesh, test_b_config  # noqa: F401
+from .configs import CONFIGS, Config, get_config, paper_mesh, test_a_config, test_b_config  # noqa: F401
 from .rng import uniform_values, cfg1_particular_values, cfg4_band_values  # noqa: F401

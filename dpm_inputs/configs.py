@@ -62,6 +62,15 @@ def paper_mesh(N: int, r: float):
     return N, -r - 2.5 * h, r + 2.5 * h, h
 
 
+def test_a_config(N: int, dt: float = 1e-8, steps: int = 100) -> Config:
+    """The paper's Test A for the convergence study, single domain: sphere
+    r = 0.5, rho0 = 1000 exp(-100 r^2), c0 = 500 exp(-50 r^2); the 3-term extension (beta = 1) with
+    one zonal harmonic per term; fixed dt = 1e-8 to T = 1e-6 (Tables 1-3)."""
+    n, lo, hi, h = paper_mesh(N, 0.5)
+    return Config(f"testA{N}", n, lo, hi, "sphere", (0.0, 0.0, 0.0), (0.5, 0.5, 0.5), 0, "neumann0_zonal", dt,
+                  steps=steps, ic_rho=(1000.0, 100.0), ic_c=(500.0, 50.0))
+
+
 def test_b_config(N: int = 127, harmonics: int = 150) -> Config:
     """The paper's Test B, single domain: sphere r = 0.5 at the origin,
     rho0 = 2000 exp(-100 (x^2 + y^2 + (z - 0.25)^2)), c0 = 0; the 2-term extension with zero

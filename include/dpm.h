@@ -43,7 +43,7 @@ typedef enum {
   DPM_ERR_NONFINITE = 6  /* a PKS step produced a non-finite value                         */
 } dpm_status;
 
-#define DPM_MAX_N 256    /* largest n the AP-solve kernels are instantiated for            */
+#define DPM_MAX_N 320    /* largest n the AP-solve kernels are instantiated for            */
 
 typedef struct { int32_t n; double lo, hi; } dpm_grid;
 
@@ -192,6 +192,8 @@ typedef struct {
   double t, dt, mass, rho_max, rho_min, c_min;  /* mass = h^3 Σ_{M+} rho (R18)   */
   int32_t rebuilt;                              /* 1 if Step 4b rebuilt the BEP  */
   int32_t step;
+  double rho_max_mplus;   /* max of rho over M+: the paper's ||rho||_inf (eq. sd-norm:max);
+                             rho_max above is over N+ (includes gamma_ex) */
 } dpm_step_log;
 
 /* Initial state (R14): IC at the node on M+\gamma, at the foot point on gamma, 0 elsewhere.

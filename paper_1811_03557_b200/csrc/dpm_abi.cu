@@ -516,6 +516,7 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
         Lg.c_min = -decode_key(L[7]);
         Lg.rebuilt = (i == 0) ? rebuilt : 0;
         Lg.step = done + i;
+        Lg.rho_max_mplus = decode_key(L[9]);
       }
     }
     done += accepted;

@@ -40,10 +40,10 @@ namespace {
 constexpr int NW = 8;         // warps per CTA
 constexpr int NT = NW * 32;   // threads per CTA
 constexpr int KSMAX_ALL = 16; // k-steps of the largest register-fragment instance (n <= 128)
-// n in (128, 256] (the paper's N = 255 / 260 meshes): 4 m-tiles per warp and 32 k-steps, i.e. 128
-// A values per lane - too many for registers, so those fragments are read from the (L1/L2-resident)
-// table inside the MMA loop, each one reused over the warp's column tiles.
-constexpr int MT_BIG = 4, KS_BIG = 32;
+// n in (128, 320] (the paper's N = 132 / 255 / 260 meshes): up to 5 m-tiles per warp and 40 k-steps,
+// i.e. up to 200 A values per lane - too many for registers, so those fragments are read from the
+// (L1/L2-resident) table inside the MMA loop, each one reused over the warp's column tiles.
+constexpr int MT_BIG = 5, KS_BIG = 40;
 __host__ __device__ constexpr int mt_of(int n) { return n > 128 ? MT_BIG : 2; }
 __host__ __device__ constexpr int ks_of(int n) { return n > 128 ? KS_BIG : KSMAX_ALL; }
 
@@ -92,7 +92,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   WarpRole r;
   r.matrix = warp >> 2;
   const int wl = warp & 3;
-  if (MTh > 8) {   // n > 128: m-tiles wl, wl + 4, wl + 8, wl + 12
+  if (MTh > 8) {   // n > 128: m-tiles wl, wl + 4, wl + 8, ...
     r.nmt = 0;
     for (int t = 0; t < MT_BIG; ++t) {
       r.mt[t] = wl + 4 * t;
@@ -104,7 +104,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   } else if (MTh >= 4) {
     r.mt[0] = wl;
     r.mt[1] = wl + 4;
-    r.mt[2] = r.mt[3] = 0;
+    r.mt[2] = r.mt[3] = r.mt[4] = 0;
     r.nmt = (wl + 4 < MTh) ? 2 : 1;
     r.ct0 = 0;
     r.ctstep = 1;
@@ -113,7 +113,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
     const int G = 4 / MTh;
     const int cg = wl / MTh;
     r.mt[0] = wl % MTh;
-    r.mt[1] = r.mt[2] = r.mt[3] = 0;
+    r.mt[1] = r.mt[2] = r.mt[3] = r.mt[4] = 0;
     r.nmt = (cg < G) ? 1 : 0;
     r.ct0 = cg;
     r.ctstep = G;
@@ -124,7 +124,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
 
 // A-fragment table: tab[((warp*mt_of(n) + t)*ks_of(n) + ks)*32 + lane], built once per plan.
 __global__ void afrag_table_kernel(double* tab, int n, int NCT) {
-  const int warp = blockIdx.x, t = blockIdx.y, ks = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = blockIdx.x, t = blockIdx.y, ks = blockIdx.z, lane = threadIdx.x;
   const int MTM = mt_of(n), KSM = ks_of(n);
   const int Po = (n + 1) / 2, Pe = n / 2, MTh = (Po + 7) / 8, KS = (Po + 3) / 4;
   const WarpRole role = warp_role(warp, MTh, NCT);
@@ -431,7 +431,7 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
     return even ? run_pass_t<0, 8, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
                 : run_pass_t<0, 8, 32, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
   }
-  if (n > 128) {   // 128 < n <= 256: TC = 32 (two 74 KB tiles), A fragments from the table
+  if (n > 128) {   // 128 < n <= 320: TC = 32 (two tiles of <= 92 KB), A fragments from the table
     return even ? run_pass_t<0, KS_BIG, 32, 2, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
                 : run_pass_t<0, KS_BIG, 32, 1, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
   }
@@ -750,7 +750,8 @@ cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   void (*k)(double*, int, int, const double*, double, double, double) =
-      n == 128 ? ztri_warp_kernel<128, 4> : (n > 128 ? ztri_warp_kernel<0, 8> : ztri_warp_kernel<0, 4>);
+      n == 128 ? ztri_warp_kernel<128, 4>
+               : (n > 256 ? ztri_warp_kernel<0, 10> : (n > 128 ? ztri_warp_kernel<0, 8> : ztri_warp_kernel<0, 4>));
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const long blocks = (nlines + 7) / 8;
@@ -781,7 +782,7 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
   if (e != cudaSuccess) return e;
   DPM_COUNT_LAUNCH(2);
   eig_kernel<<<(n + 127) / 128, 128>>>(p.lam, n, h);
-  afrag_table_kernel<<<dim3(NW, mt_of(n)), ks_of(n) * 32>>>(p.atab, n, tc_for(n) / 8);
+  afrag_table_kernel<<<dim3(NW, mt_of(n), ks_of(n)), 32>>>(p.atab, n, tc_for(n) / 8);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (n <= PSN) {   // fused small-n plane pass (DPM_PLANE_SMALL=0 disables)

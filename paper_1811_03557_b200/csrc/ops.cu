@@ -229,11 +229,12 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8
   }
 }
 
-// restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite]
+// restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite,
+// rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max)]
 __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
                                 double* c, double* stats) {
   const long nn = (long)n * n * n;
-  double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY;
+  double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY, rmaxm = -INFINITY;
   int bad = 0;
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     const uint8_t f = flags[p];
@@ -245,12 +246,15 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
       rmax = fmax(rmax, a);
       rmin = fmin(rmin, a);
       cmin = fmin(cmin, b);
-      if (f & F_MPLUS) msum += a;
+      if (f & F_MPLUS) {
+        msum += a;
+        rmaxm = fmax(rmaxm, a);
+      }
     }
     rho[p] = a;
     c[p] = b;
   }
-  __shared__ double red[4][TB / 32];
+  __shared__ double red[5][TB / 32];
   __shared__ int sbad;
   if (threadIdx.x == 0) sbad = 0;
   __syncthreads();
@@ -260,13 +264,16 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
     rmin = fmin(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
     cmin = fmin(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+    rmaxm = fmax(rmaxm, __shfl_xor_sync(0xffffffffu, rmaxm, o));
   }
   if (bad) atomicOr(&sbad, 1);
-  if (lane == 0) { red[0][w] = msum; red[1][w] = rmax; red[2][w] = rmin; red[3][w] = cmin; }
+  if (lane == 0) { red[0][w] = msum; red[1][w] = rmax; red[2][w] = rmin; red[3][w] = cmin; red[4][w] = rmaxm; }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0, a = -INFINITY, b = INFINITY, d = INFINITY;
-    for (int q = 0; q < TB / 32; ++q) { s += red[0][q]; a = fmax(a, red[1][q]); b = fmin(b, red[2][q]); d = fmin(d, red[3][q]); }
+    double s = 0, a = -INFINITY, b = INFINITY, d = INFINITY, am = -INFINITY;
+    for (int q = 0; q < TB / 32; ++q) {
+      s += red[0][q]; a = fmax(a, red[1][q]); b = fmin(b, red[2][q]); d = fmin(d, red[3][q]); am = fmax(am, red[4][q]);
+    }
     atomicAdd(stats + 0, s);
     // max via bit patterns on the ordered transform
     auto key = [](double v) {
@@ -277,6 +284,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     atomicMax((unsigned long long*)(stats + 2), key(-b));
     atomicMax((unsigned long long*)(stats + 3), key(-d));
     if (sbad) atomicAdd(stats + 4, 1.0);
+    atomicMax((unsigned long long*)(stats + 5), key(am));
   }
 }
 
@@ -457,7 +465,7 @@ cudaError_t launch_cfl_dt(dpm_ctx* ctx, const double* c, double* out3, double ch
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
-  cudaError_t e = cudaMemsetAsync(stats, 0, 5 * sizeof(double), s);
+  cudaError_t e = cudaMemsetAsync(stats, 0, 6 * sizeof(double), s);
   if (e != cudaSuccess) return e;
   DPM_COUNT_LAUNCH(1);
   restrict_kernel<<<grid_reduce(nn), TB, 0, s>>>(ctx->flags, ctx->n, u, rho, c, stats);

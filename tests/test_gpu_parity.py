@@ -40,10 +40,10 @@ def ctx_for(api, cfg, dt=None, n=None):
 # ------------------------------------------------------------------ S3 AP solve
 @pytest.mark.parametrize("solver", ["dst3", "dst2_tridiag"])
 @pytest.mark.parametrize("n", [4, 5, 7, 8, 12, 16, 17, 24, 31, 32, 33, 48, 63, 64, 65, 100, 127, 128,
-                               129, 160, 200, 255, 256])
+                               129, 132, 160, 200, 255, 256, 257, 260, 300, 320])
 def test_aux_solve_parity(api, n, solver):
-    # n in (128, 256]: the paper's N = 255 / 260 meshes (table-read A fragments, 8 z per lane)
-    batch = 3 if n <= 64 else (2 if n in (129, 255) else 1)
+    # n in (128, 320]: the paper's N = 132 / 255 / 260 meshes (table-read A fragments, 8 or 10 z per lane)
+    batch = 3 if n <= 64 else (2 if n in (129, 255, 257) else 1)
     dt = 1e-3 if n % 2 else 1e-5
     c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
     c.set_solver(solver)
@@ -56,7 +56,7 @@ def test_aux_solve_parity(api, n, solver):
 @pytest.mark.parametrize("solver", ["dst3", "dst2_tridiag"])
 @pytest.mark.parametrize("n,dt", [(128, 1.0), (128, 0.5 * (2.2 / 129) ** 2), (128, 1e-8), (128, 1e-11),
                                   (128, 1e-14), (33, 10.0), (64, 0.5 * (2.2 / 65) ** 2), (255, 1.0),
-                                  (255, 1e-12), (256, 0.5 * (1.0 / 251) ** 2)])
+                                  (255, 1e-12), (256, 0.5 * (1.0 / 251) ** 2), (260, 1e-8), (320, 1e-3)])
 def test_aux_solve_parity_large_dt(api, n, dt, solver):
     # large dt: the z operator approaches the pure Laplacian (μ -> 1 in the tridiagonal solver);
     # tiny dt: μ^M underflows (1e-11, 1e-14 at n = 128), which the running powers must survive
@@ -461,3 +461,23 @@ def test_paper_test_b_blowup_time():
     assert abs(res["t_stop"] - 0.079744) <= 0.01 * 0.079744, res
     assert res["rebuilds"] >= 10 and res["steps_cfl"] >= 10   # the CFL / Step-4b regime was reached
     assert res["rho_min"] > -1e-2                                 # positivity up to rounding (measured -3e-4)
+
+
+# ------------------------------------------------------------------ NEXT-2: the paper's Test A convergence
+def test_paper_test_a_max_density_convergence():
+    # Test A, SD, the paper's meshes N = 36/68/132/260, 3-term extension with one
+    # zonal harmonic per term, dt = 1e-8 to T = 1e-6: E_rel of ||ρ^i||∞ against the
+    # Richardson limit of the two finest meshes (the paper's reference, N = 516, exceeds DPM_MAX_N).
+    # Paper (Table 3, SD): 1.0196e-1 / 2.6378e-2 / 6.3461e-3 / 1.2724e-3, rates 1.95 / 2.06 / 2.32.
+    # Measured: 8.16e-2 / 2.10e-2 / 5.26e-3 / 1.32e-3, rates 1.96 / 1.99 / 2.00.
+    import os, sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import test_a
+    res = test_a.run((36, 68, 132, 260))
+    rows = {r["N"]: r for r in res["rows"]}
+    for N in (68, 132):
+        assert 1.8 <= rows[N]["rate"] <= 2.2, rows[N]
+    for N in (36, 68, 132, 260):
+        assert 0.7 <= rows[N]["E_rel"] / rows[N]["paper_E_rel"] <= 1.3, rows[N]
+        assert abs(rows[N]["mass_drift"]) < 1e-12                     # conservation
+        assert abs(rows[N]["t_end"] - 1e-6) < 1e-18

@@ -1,0 +1,69 @@
+"""The paper's Test A convergence of the max density (P:662-666 eq. sd-conv-max-density-in-space,
+Table 3 at P:786-805), single domain, on one GPU.
+
+For each mesh N (paper convention) runs 100 PKS steps at the fixed dt = 1e-8 to T = 1e-6
+and records ||ρ^i||∞ over M+  per step.  The paper's reference is the N = 516 solution;
+here the reference series is the Richardson extrapolation (second order, h halves between the
+paper's meshes) of the two finest meshes run, and
+
+    E_rel(N) = sqrt(Σ_i (||ρ^i_N||∞ - R_i)^2 Δt) / sqrt(Σ_i R_i^2 Δt)
+
+is compared with the paper's E_rel (SD column of Table 3): 1.0196e-01 (36), 2.6378e-02 (68),
+6.3461e-03 (132), 1.2724e-03 (260).
+
+    python tools/test_a.py [--N 36 68 132 260]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from dpm_inputs import test_a_config  # noqa: E402
+from paper_1811_03557_b200 import api  # noqa: E402
+
+PAPER_E_REL = {36: 1.0196e-01, 68: 2.6378e-02, 132: 6.3461e-03, 260: 1.2724e-03}
+
+
+def series(N):
+    cfg = test_a_config(N)
+    ctx = api.DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    c = torch.zeros_like(rho)
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=1, clamp=1)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    s = np.array([lg["rho_max_mplus"] for lg in logs])
+    return s, {"N": N, "h": ctx.info["h"], "K": ctx.K, "rho_max_T": float(s[-1]), "t_end": logs[-1]["t"],
+               "mass_drift": logs[-1]["mass"] / logs[0]["mass"] - 1.0, "wall_s": wall}
+
+
+def run(Ns=(36, 68, 132, 260)):
+    Ns = sorted(Ns)
+    S, info = {}, {}
+    for N in Ns:
+        S[N], info[N] = series(N)
+    f, c = Ns[-1], Ns[-2]
+    R = (4.0 * S[f] - S[c]) / 3.0          # Richardson, p = 2, h_c = 2 h_f
+    rows = []
+    for N in Ns:
+        e = float(np.sqrt(np.sum((S[N] - R) ** 2)) / np.sqrt(np.sum(R ** 2)))
+        rows.append(dict(info[N], E_rel=e, paper_E_rel=PAPER_E_REL.get(N)))
+    for a, b in zip(rows, rows[1:]):
+        b["rate"] = math.log2(a["E_rel"] / b["E_rel"]) if b["E_rel"] > 0 else None
+    return {"test": "A", "reference": f"Richardson of N={c} and N={f} (the paper's: N=516)", "rows": rows}
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", type=int, nargs="+", default=[36, 68, 132, 260])
+    a = ap.parse_args()
+    print(json.dumps(run(a.N)))

@@ -36,10 +36,10 @@ def run(N=127, harmonics=150, t_end=0.2, max_steps=100000):
         out = ctx.pks_step(rho, c, chunk, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=0, clamp=1)
         for lg in out:
             logs.append(lg)
-            if lg["rho_max"] - prev_max >= 1000.0:
+            if lg["rho_max_mplus"] - prev_max >= 1000.0:   # P:1026 with ||ρ||∞ over M+ 
                 stop = lg
                 break
-            prev_max = lg["rho_max"]
+            prev_max = lg["rho_max_mplus"]
         if stop is None and logs[-1]["t"] >= t_end:
             break
         # near blow-up the BEP is rebuilt every step: shorter calls keep the overshoot small
@@ -48,7 +48,7 @@ def run(N=127, harmonics=150, t_end=0.2, max_steps=100000):
     wall = time.perf_counter() - t0
     res = {
         "test": "B", "N": N, "harmonics": harmonics, "K": ctx.K, "h": ctx.info["h"], "dt0": cfg.dt,
-        "t_stop": stop["t"] if stop else None, "rho_max_stop": stop["rho_max"] if stop else None,
+        "t_stop": stop["t"] if stop else None, "rho_max_stop": stop["rho_max_mplus"] if stop else None,
         "steps": len(logs), "rebuilds": sum(int(l["rebuilt"]) for l in logs),
         "steps_cfl": sum(1 for l in logs if l["dt"] < cfg.dt), "dt_min": min(l["dt"] for l in logs),
         "mass0": logs[0]["mass"], "mass_end": logs[-1]["mass"], "rho_min": min(l["rho_min"] for l in logs),
