@@ -481,3 +481,17 @@ def test_paper_test_a_max_density_convergence():
         assert 0.7 <= rows[N]["E_rel"] / rows[N]["paper_E_rel"] <= 1.3, rows[N]
         assert abs(rows[N]["mass_drift"]) < 1e-12                     # conservation
         assert abs(rows[N]["t_end"] - 1e-6) < 1e-18
+
+
+def test_paper_test_a_time_convergence_rates():
+    # Tables 4-5: dt = 1e-7/τ to T = 1e-6 against τ* = 512; the printed SD rates
+    # 1.05 / 1.10 (ρ and c) are first order against that reference.  Run on N = 132 (the rates do
+    # not depend on the mesh; the full N = 255 table is tools/test_a.py --time, profiles/r01).
+    import os, sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import test_a
+    res = test_a.run_time(132, taus=(16, 32, 64))
+    r = res["rows"]
+    assert abs(r[1]["rate_rho"] - 1.05) < 0.03 and abs(r[2]["rate_rho"] - 1.10) < 0.03, r
+    assert abs(r[1]["rate_c"] - 1.05) < 0.03 and abs(r[2]["rate_c"] - 1.10) < 0.03, r
+    assert all(abs(x["t_end"] - 1e-6) < 1e-18 for x in r)

@@ -12,6 +12,14 @@ is compared with the paper's E_rel (SD column of Table 3): 1.0196e-01 (36), 2.63
 6.3461e-03 (132), 1.2724e-03 (260).
 
     python tools/test_a.py [--N 36 68 132 260]
+    python tools/test_a.py --time [--N 255]        # Tables 4-5: convergence in time
+
+Convergence in time (P:667-670 eq. sd-conv-in-time, Tables 4-5 at P:812-870): on the fixed mesh
+N = 255, dt = 1e-7/τ (τ = 16 ... 256) to T = 1e-6, E_t = max over M+ of |ρ_τ - ρ_ref| (and c) at
+T against the run at τ* = 512 (the printed rates 1.05 / 1.10 / 1.22 / 1.58 are exactly
+log2((1/τ - 1/512)/(1/2τ - 1/512)), so the paper's reference is dt* = 1e-7/512).
+Paper (SD): E_t(ρ) 8.2335e-03 / 3.9846e-03 / 1.8596e-03 / 7.9700e-04 / 2.6567e-04,
+            E_t(c) 6.1248e-08 / 2.9665e-08 / 1.3889e-08 / 5.9737e-09 / 2.0236e-09.
 """
 import argparse
 import json
@@ -28,6 +36,8 @@ from dpm_inputs import test_a_config  # noqa: E402
 from paper_1811_03557_b200 import api  # noqa: E402
 
 PAPER_E_REL = {36: 1.0196e-01, 68: 2.6378e-02, 132: 6.3461e-03, 260: 1.2724e-03}
+PAPER_E_T_RHO = {16: 8.2335e-03, 32: 3.9846e-03, 64: 1.8596e-03, 128: 7.9700e-04, 256: 2.6567e-04}
+PAPER_E_T_C = {16: 6.1248e-08, 32: 2.9665e-08, 64: 1.3889e-08, 128: 5.9737e-09, 256: 2.0236e-09}
 
 
 def series(N):
@@ -62,8 +72,40 @@ def run(Ns=(36, 68, 132, 260)):
     return {"test": "A", "reference": f"Richardson of N={c} and N={f} (the paper's: N=516)", "rows": rows}
 
 
+def final_state(N, tau):
+    dt = 1e-7 / tau
+    cfg = test_a_config(N, dt=dt, steps=10 * tau)
+    ctx = api.DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    c = torch.zeros_like(rho)
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    t0 = time.perf_counter()
+    logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=dt, dt_rule=1, clamp=1)
+    torch.cuda.synchronize()
+    mp = torch.from_numpy(ctx.copy_set("mplus")).cuda()
+    return rho.reshape(-1)[mp], c.reshape(-1)[mp], logs[-1]["t"], time.perf_counter() - t0
+
+
+def run_time(N=255, taus=(16, 32, 64, 128, 256), tau_ref=512):
+    rr, cr, tr, wr = final_state(N, tau_ref)
+    rows = []
+    for tau in taus:
+        r, c, t, w = final_state(N, tau)
+        rows.append({"tau": tau, "dt": 1e-7 / tau, "t_end": t, "wall_s": w,
+                     "E_t_rho": float((r - rr).abs().max()), "paper_E_t_rho": PAPER_E_T_RHO.get(tau),
+                     "E_t_c": float((c - cr).abs().max()), "paper_E_t_c": PAPER_E_T_C.get(tau)})
+    for a, b in zip(rows, rows[1:]):
+        b["rate_rho"] = math.log2(a["E_t_rho"] / b["E_t_rho"])
+        b["rate_c"] = math.log2(a["E_t_c"] / b["E_t_c"])
+    return {"test": "A-time", "N": N, "tau_ref": tau_ref, "t_end_ref": tr, "wall_ref_s": wr, "rows": rows}
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--N", type=int, nargs="+", default=[36, 68, 132, 260])
+    ap.add_argument("--N", type=int, nargs="+", default=None)
+    ap.add_argument("--time", action="store_true")
     a = ap.parse_args()
-    print(json.dumps(run(a.N)))
+    if a.time:
+        print(json.dumps(run_time(a.N[0] if a.N else 255)))
+    else:
+        print(json.dumps(run(a.N or [36, 68, 132, 260])))
