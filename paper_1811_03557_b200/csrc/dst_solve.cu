@@ -183,7 +183,32 @@ __device__ __forceinline__ void fold_transform(const Geo<NFIX, TC, PASS>& G, int
 #pragma unroll
     for (int ct = 0; ct < NCT; ++ct) acc[t][ct][0] = acc[t][ct][1] = 0.0;
 
-  if (role.nmt > 0) {
+  if (MT > 2 && role.nmt > 0) {   // table-read A fragments, prefetched one k-step ahead
+    const int colb = base + ((role.ct0 * 8) + (lane >> 2)) * cs;
+    double an[MT];
+#pragma unroll
+    for (int t = 0; t < MT; ++t) an[t] = t < role.nmt ? __ldg(atw + t * KSMAX * 32) : 0.0;
+#pragma unroll 2
+    for (int ks = 0; ks < G.KS; ++ks) {
+      double a[MT];
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        a[t] = an[t];
+        an[t] = (t < role.nmt && ks + 1 < G.KS) ? __ldg(atw + (t * KSMAX + ks + 1) * 32) : 0.0;
+      }
+      const int j = ks * 4 + (lane & 3);
+      const int r = (role.matrix == 0) ? (j < Po ? j : 0) : (j < Pe ? n - 1 - j : 0);
+      const int rowb = colb + r * rs;
+      double b[NCT];
+#pragma unroll
+      for (int ct = 0; ct < NCT; ++ct) b[ct] = sm[rowb + ct * 8 * cs];
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int ct = 0; ct < NCT; ++ct)
+          if (t < role.nmt) dmma884(acc[t][ct], a[t], b[ct]);
+    }
+  } else if (role.nmt > 0) {
     const int colb = base + ((role.ct0 * 8) + (lane >> 2)) * cs;
     const int cstep = role.ctstep * 8 * cs;
 #pragma unroll
@@ -317,7 +342,7 @@ __device__ __forceinline__ void store_tile(const Geo<NFIX, TC, PASS>& G, int bas
 }
 
 template <int KSMAX, int TC>
-constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) || KSMAX > 16 ? 1 : 2; }
+constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) || (KSMAX > 16 && TC > 16) ? 1 : 2; }
 
 template <int NFIX, int KSMAX, int TC, int PASS, int VEC, int MT = 2>
 __global__ void __launch_bounds__(NT, min_blocks<KSMAX, TC>())
@@ -431,7 +456,16 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
     return even ? run_pass_t<0, 8, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
                 : run_pass_t<0, 8, 32, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
   }
-  if (n > 128) {   // 128 < n <= 320: TC = 32 (two tiles of <= 92 KB), A fragments from the table
+  if (n > 128) {   // 128 < n <= 320: A fragments from the table (prefetched one k-step ahead);
+    // TC = 16 (2 CTAs = 16 warps per SM) beats TC = 32 (1 CTA, twice the A reuse) by 5-8% at
+    // n = 132 / 255 (tools/big_n_profile.py); DPM_TCBIG=32 selects the latter
+    static const int tcb = [] {
+      const char* e = getenv("DPM_TCBIG");
+      return (e && atoi(e) == 32) ? 32 : 16;
+    }();
+    if (tcb == 16)
+      return even ? run_pass_t<0, KS_BIG, 16, 2, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
+                  : run_pass_t<0, KS_BIG, 16, 1, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
     return even ? run_pass_t<0, KS_BIG, 32, 2, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
                 : run_pass_t<0, KS_BIG, 32, 1, MT_BIG>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
   }
