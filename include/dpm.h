@@ -92,6 +92,9 @@ typedef struct dpm_ctx dpm_ctx;
  * Setup (P:40-60 auxiliary cube + Def. 1; P:263-299 extension data).
  * Builds the point sets on the device (fp64 classification; ties -> M-, R6), the
  * gamma geometry (foot point, signed distance d, SH angles; R10) and E (|gamma| x K).
+ * 4 <= n <= DPM_MAX_N; basis one of dpm_basis; 0 <= lmax <= 40 for the full-SH sets,
+ * <= DPM_MAX_ZONAL_L for the zonal ones (DPM_ERR_INVALID otherwise).  The paper's mesh
+ * (N cells on [-r-2h, r+2h]^3, h = 2r/(N-4)) is n = N, lo = -r-5h/2, hi = r+5h/2.
  * Synchronous (uses an internal stream and waits). *out is NULL on failure.
  * ------------------------------------------------------------------------------- */
 dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt,
