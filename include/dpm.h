@@ -43,7 +43,7 @@ typedef enum {
   DPM_ERR_NONFINITE = 6  /* a PKS step produced a non-finite value                         */
 } dpm_status;
 
-#define DPM_MAX_N 320    /* largest n the AP-solve kernels are instantiated for            */
+#define DPM_MAX_N 520    /* largest n the AP-solve kernels are instantiated for            */
 
 typedef struct { int32_t n; double lo, hi; } dpm_grid;
 

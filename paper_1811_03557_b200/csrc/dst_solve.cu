@@ -43,9 +43,10 @@ constexpr int KSMAX_ALL = 16; // k-steps of the largest register-fragment instan
 // n in (128, 320] (the paper's N = 132 / 255 / 260 meshes): up to 5 m-tiles per warp and 40 k-steps,
 // i.e. up to 200 A values per lane - too many for registers, so those fragments are read from the
 // (L1/L2-resident) table inside the MMA loop, each one reused over the warp's column tiles.
-constexpr int MT_BIG = 5, KS_BIG = 40;
-__host__ __device__ constexpr int mt_of(int n) { return n > 128 ? MT_BIG : 2; }
-__host__ __device__ constexpr int ks_of(int n) { return n > 128 ? KS_BIG : KSMAX_ALL; }
+// n in (320, 520] (the paper's N = 516 reference mesh): 9 m-tiles and 65 k-steps per warp.
+constexpr int MT_BIG = 5, KS_BIG = 40, MT_HUGE = 9, KS_HUGE = 65;
+__host__ __device__ constexpr int mt_of(int n) { return n > 320 ? MT_HUGE : (n > 128 ? MT_BIG : 2); }
+__host__ __device__ constexpr int ks_of(int n) { return n > 320 ? KS_HUGE : (n > 128 ? KS_BIG : KSMAX_ALL); }
 
 __host__ __device__ constexpr int ldx_of(int tc) { return tc + 4; }            // ≡ 4 mod 16 for tc % 16 == 0
 __host__ __device__ constexpr int ldz_of(int n) { return ((n + 15) / 16) * 16 + 4; }
@@ -82,8 +83,8 @@ __device__ double fold_entry(int n, int Po, int Pe, int matrix, int m, int j) {
 
 struct WarpRole {
   int matrix;   // 0 odd / 1 even
-  int nmt;      // m-tiles owned (0..MT_BIG)
-  int mt[MT_BIG];   // local m-tile indices
+  int nmt;      // m-tiles owned (0..MT_HUGE)
+  int mt[MT_HUGE];  // local m-tile indices
   int nct;      // column tiles handled
   int ct0, ctstep;
 };
@@ -94,7 +95,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   const int wl = warp & 3;
   if (MTh > 8) {   // n > 128: m-tiles wl, wl + 4, wl + 8, ...
     r.nmt = 0;
-    for (int t = 0; t < MT_BIG; ++t) {
+    for (int t = 0; t < MT_HUGE; ++t) {
       r.mt[t] = wl + 4 * t;
       if (wl + 4 * t < MTh) r.nmt = t + 1;
     }
@@ -104,7 +105,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
   } else if (MTh >= 4) {
     r.mt[0] = wl;
     r.mt[1] = wl + 4;
-    r.mt[2] = r.mt[3] = r.mt[4] = 0;
+    for (int t = 2; t < MT_HUGE; ++t) r.mt[t] = 0;
     r.nmt = (wl + 4 < MTh) ? 2 : 1;
     r.ct0 = 0;
     r.ctstep = 1;
@@ -113,7 +114,7 @@ __host__ __device__ inline WarpRole warp_role(int warp, int MTh, int NCT) {
     const int G = 4 / MTh;
     const int cg = wl / MTh;
     r.mt[0] = wl % MTh;
-    r.mt[1] = r.mt[2] = r.mt[3] = r.mt[4] = 0;
+    for (int t = 1; t < MT_HUGE; ++t) r.mt[t] = 0;
     r.nmt = (cg < G) ? 1 : 0;
     r.ct0 = cg;
     r.ctstep = G;
@@ -342,7 +343,7 @@ __device__ __forceinline__ void store_tile(const Geo<NFIX, TC, PASS>& G, int bas
 }
 
 template <int KSMAX, int TC>
-constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) || (KSMAX > 16 && TC > 16) ? 1 : 2; }
+constexpr int min_blocks() { return (KSMAX >= 16 && TC >= 64) || (KSMAX > 16 && TC > 16) || KSMAX > KS_BIG ? 1 : 2; }
 
 template <int NFIX, int KSMAX, int TC, int PASS, int VEC, int MT = 2>
 __global__ void __launch_bounds__(NT, min_blocks<KSMAX, TC>())
@@ -455,6 +456,10 @@ cudaError_t run_pass(const DstPlan& p, int pass, const double* in, double* out, 
   if (KS <= 8) {
     return even ? run_pass_t<0, 8, 32, 2>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
                 : run_pass_t<0, 8, 32, 1>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
+  }
+  if (n > 320) {   // 320 < n <= 520: 9 m-tiles x 65 k-steps per warp, 16-column tiles (2 x 83 KB), 1 CTA/SM
+    return even ? run_pass_t<0, KS_HUGE, 16, 2, MT_HUGE>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s)
+                : run_pass_t<0, KS_HUGE, 16, 1, MT_HUGE>(pass, in, out, nfields, n, p.lam, p.atab, inv_dt, scale, s);
   }
   if (n > 128) {   // 128 < n <= 320: A fragments from the table (prefetched one k-step ahead);
     // TC = 16 (2 CTAs = 16 warps per SM) beats TC = 32 (1 CTA, twice the A reuse) by 5-8% at
@@ -785,7 +790,8 @@ cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
   }
   void (*k)(double*, int, int, const double*, double, double, double) =
       n == 128 ? ztri_warp_kernel<128, 4>
-               : (n > 256 ? ztri_warp_kernel<0, 10> : (n > 128 ? ztri_warp_kernel<0, 8> : ztri_warp_kernel<0, 4>));
+               : (n > 320 ? ztri_warp_kernel<0, 17>
+                  : (n > 256 ? ztri_warp_kernel<0, 10> : (n > 128 ? ztri_warp_kernel<0, 8> : ztri_warp_kernel<0, 4>)));
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, 0);
   const long blocks = (nlines + 7) / 8;
