@@ -203,6 +203,14 @@ typedef struct {
    Resets t and the dt history. Asynchronous. */
 dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream);
 
+/* The paper's per-step diagnostics of a state, HOST out[3] = {mass h^3 Σ_{M+} rho (R18),
+   second moment M_h = h^3 Σ_{M+} |x - center|^2 rho (eq. sd-norm:second-moment), free energy
+   E_h = h^3 Σ_{M+} {rho ln rho - rho c + c^2/2 + [(c_{j+1}-c_{j-1})^2 + (c_{k+1}-c_{k-1})^2 +
+   (c_{l+1}-c_{l-1})^2]/(8h^2)} (eq. sd-norm:free-energy)}; rho ln rho := 0 for rho <= 0, c = 0 on the
+   ghost layer, |x - center| from the domain centre (R35).  rho, c: device [n][n][n].  Synchronizes
+   `stream`.  Single-domain contexts (DPM_ERR_INVALID for octants). */
+dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out, void* stream);
+
 /* Advance nsteps steps in place. Each step: CFL (device reduction) -> dt (host decides,
    stream synchronized once per step) -> [Step 4b rebuild when dt decreased] -> flux +
    IMEX RHS -> 2 particular AP solves -> Tr_gamma_in -> LSQ -> u_gamma = E C,

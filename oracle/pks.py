@@ -183,3 +183,28 @@ class PKSOracle:
             log["mass"] = self.mass(rho)
             logs.append(log)
         return rho, c, logs
+
+
+def diagnostics(rho: np.ndarray, c: np.ndarray, g: grid.Grid, ps: grid.PointSets, center) -> dict:
+    """Mass (R18), second moment M_h (eq. sd-norm:second-moment) and free energy E_h
+    (eq. sd-norm:free-energy) of a state on M+, literally:
+      M_h = Σ_{M+} h^3 |x - x_c|^2 ρ̄,
+      E_h = Σ_{M+} h^3 { ρ̄ ln ρ̄ - ρ̄ c + c^2/2 + [(c_{j+1}-c_{j-1})^2 + (c_{k+1}-c_{k-1})^2
+                                                  + (c_{l+1}-c_{l-1})^2] / (8 h^2) }.
+    Readings (R35): |x - x_c| from the domain centre (the paper's domain is centred at the origin);
+    ρ̄ ln ρ̄ := 0 for ρ̄ <= 0 (its limit at 0); c at ghost nodes is 0 (the state's ghost values)."""
+    h = g.h
+    x = g.coords()
+    X, Y, Z = np.meshgrid(x - center[0], x - center[1], x - center[2], indexing="ij")
+    m = ps.mplus
+    r, cc = rho[m], c[m]
+    second = h ** 3 * np.sum((X[m] ** 2 + Y[m] ** 2 + Z[m] ** 2) * r)
+    cp = np.zeros(tuple(s + 2 for s in c.shape))
+    cp[1:-1, 1:-1, 1:-1] = c
+    gx = cp[2:, 1:-1, 1:-1] - cp[:-2, 1:-1, 1:-1]
+    gy = cp[1:-1, 2:, 1:-1] - cp[1:-1, :-2, 1:-1]
+    gz = cp[1:-1, 1:-1, 2:] - cp[1:-1, 1:-1, :-2]
+    rlnr = np.where(r > 0, r * np.log(np.where(r > 0, r, 1.0)), 0.0)
+    grad = (gx[m] ** 2 + gy[m] ** 2 + gz[m] ** 2) / (8.0 * h * h)
+    free = h ** 3 * np.sum(rlnr - r * cc + 0.5 * cc * cc + grad)
+    return {"mass": h ** 3 * np.sum(r), "second_moment": second, "free_energy": free}

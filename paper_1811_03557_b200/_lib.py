@@ -81,6 +81,7 @@ _sig = {
     "dpm_build_projection": ([P, P, P, P], C.c_int),
     "dpm_boundary_lsq": ([P, P, P, P, C.c_int32, P], C.c_int),
     "dpm_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
+    "dpm_pks_diagnostics": ([P, P, P, C.POINTER(C.c_double), P], C.c_int),
     "dpm_pks_step": ([P, P, P, C.c_int32, C.POINTER(PksParams), C.POINTER(StepLog), P], C.c_int),
     "dpm_launch_count": ([], C.c_int64),
     "dpm_set_pass_timing": ([P, C.c_int32], C.c_int),

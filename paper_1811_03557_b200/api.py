@@ -178,6 +178,13 @@ class DPM:
         self._chk(L.lib.dpm_pks_init(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), C.byref(ic),
                                      _stream(stream)))
 
+    def pks_diagnostics(self, rho, c, stream=None):
+        """{mass, second_moment, free_energy} of a state (dpm_pks_diagnostics)."""
+        out = (C.c_double * 3)()
+        self._chk(L.lib.dpm_pks_diagnostics(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), out,
+                                            _stream(stream)))
+        return {"mass": out[0], "second_moment": out[1], "free_energy": out[2]}
+
     def pks_step(self, rho, c, nsteps, chi=1.0, dt_cap=1e-4, dt_rule=0, clamp=1, stream=None):
         prm = L.PksParams(chi, dt_cap, dt_rule, clamp)
         logs = (L.StepLog * max(nsteps, 1))()

@@ -320,6 +320,19 @@ dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* 
   return DPM_OK;
 }
 
+dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out, void* stream) {
+  if (!ctx || !rho || !c || !out) return DPM_ERR_INVALID;
+  if (ctx->domain.kind == DPM_OCTANT_CANON) { ctx->err = "diagnostics: single-domain contexts only"; return DPM_ERR_INVALID; }
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  DPM_CUDA_TRY(ctx, launch_diagnostics(ctx, rho, c, ctx->red + 16, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 16, ctx->red + 16, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  const double h3 = ctx->h * ctx->h * ctx->h;
+  for (int i = 0; i < 3; ++i) out[i] = ctx->red_host[16 + i] * h3;
+  return DPM_OK;
+}
+
 }  // extern "C"
 
 double decode_key(double slot) {

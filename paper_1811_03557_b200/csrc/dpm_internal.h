@@ -227,6 +227,7 @@ cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, do
                             double* fq_rho, double* fq_c, cudaStream_t s);
 cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
                              cudaStream_t s);
+cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s);
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s);
 // CFL maxima + the Step-3 dt rule in one kernel (ticket in ctx->red[63], zero at creation)

@@ -229,6 +229,43 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8
   }
 }
 
+// Paper diagnostics on M+ (P:683-699): out += [Σ ρ̄, Σ |x - x_c|^2 ρ̄, Σ {ρ̄ ln ρ̄ - ρ̄ c + c^2/2 + |c_{+1} - c_{-1}|^2 / (8h^2)}]
+// (the host multiplies by h^3); ρ̄ ln ρ̄ := 0 for ρ̄ <= 0, c = 0 beyond the box (ghost layer).
+__global__ void __launch_bounds__(TB, STENCIL_MINB) diag_kernel(const uint8_t* __restrict__ flags, int n, double lo, double h,
+                                                        double cx, double cy, double cz, const double* __restrict__ rho,
+                                                        const double* __restrict__ c, double* out) {
+  const int nn = n * n * n;
+  double sm0 = 0.0, sm1 = 0.0, sm2 = 0.0;
+  const double inv8h2 = 1.0 / (8.0 * h * h);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < nn; p += gridDim.x * blockDim.x) {
+    if (!(flags[p] & F_MPLUS)) continue;
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    const double r = rho[p], cc = c[p];
+    const double x = lo + (i + 1) * h - cx, y = lo + (j + 1) * h - cy, z = lo + (k + 1) * h - cz;
+    const double gx = (i + 1 < n ? c[p + n * n] : 0.0) - (i > 0 ? c[p - n * n] : 0.0);
+    const double gy = (j + 1 < n ? c[p + n] : 0.0) - (j > 0 ? c[p - n] : 0.0);
+    const double gz = (k + 1 < n ? c[p + 1] : 0.0) - (k > 0 ? c[p - 1] : 0.0);
+    sm0 += r;
+    sm1 += (x * x + y * y + z * z) * r;
+    sm2 += (r > 0.0 ? r * log(r) : 0.0) - r * cc + 0.5 * cc * cc + (gx * gx + gy * gy + gz * gz) * inv8h2;
+  }
+  __shared__ double red[3][TB / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    sm0 += __shfl_xor_sync(0xffffffffu, sm0, o);
+    sm1 += __shfl_xor_sync(0xffffffffu, sm1, o);
+    sm2 += __shfl_xor_sync(0xffffffffu, sm2, o);
+  }
+  if (lane == 0) { red[0][w] = sm0; red[1][w] = sm1; red[2][w] = sm2; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int q = 0; q < TB / 32; ++q) t += red[threadIdx.x][q];
+    atomicAdd(out + threadIdx.x, t);
+  }
+}
+
 // restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite,
 // rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max)]
 __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
@@ -461,6 +498,16 @@ cudaError_t launch_cfl_dt(dpm_ctx* ctx, const double* c, double* out3, double ch
   return cudaGetLastError();
 }
 
+
+cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  DPM_COUNT_LAUNCH(1);
+  diag_kernel<<<grid_reduce(nn), TB, 0, s>>>(ctx->flags, ctx->n, ctx->lo, ctx->h, ctx->domain.center[0],
+                                             ctx->domain.center[1], ctx->domain.center[2], rho, c, out3);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s) {

@@ -496,3 +496,54 @@ def test_paper_test_a_time_convergence_rates():
     assert abs(r[1]["rate_rho"] - 1.05) < 0.03 and abs(r[2]["rate_rho"] - 1.10) < 0.03, r
     assert abs(r[1]["rate_c"] - 1.05) < 0.03 and abs(r[2]["rate_c"] - 1.10) < 0.03, r
     assert all(abs(x["t_end"] - 1e-6) < 1e-18 for x in r)
+
+
+# ------------------------------------------------------------------ diagnostics
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_pks_diagnostics_parity(api, name):
+    # dpm_pks_diagnostics on a stepped GPU state vs the oracle's formulas on the same state
+    cfg = get_config(name)
+    c = api.DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    c.pks_step(rho, cc, 5, chi=cfg.chi, dt_cap=cfg.dt)
+    d = c.pks_diagnostics(rho, cc)
+    g, ps = grid.point_sets_for(cfg)
+    o = pks.diagnostics(rho.cpu().numpy(), cc.cpu().numpy(), g, ps, cfg.center)
+    for k in o:
+        assert abs(d[k] - o[k]) <= 1e-12 * abs(o[k]), (k, d[k], o[k])
+
+
+def test_paper_free_energy_and_second_moment_trends():
+    # the free energy decreases in time (second law); P:1074 (Test B): the second moment
+    # increases as the cells move to the boundary and the free energy decreases.
+    from dpm_inputs import test_a_config, test_b_config
+    cfg = test_a_config(68)
+    c = api_mod().DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    E = [c.pks_diagnostics(rho, cc)["free_energy"]]
+    for _ in range(20):
+        c.pks_step(rho, cc, 5, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=1)
+        E.append(c.pks_diagnostics(rho, cc)["free_energy"])
+    assert all(b < a for a, b in zip(E, E[1:])), E
+    cfg = test_b_config(127, 150)
+    c = api_mod().DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    M, E = [], []
+    for _ in range(12):
+        c.pks_step(rho, cc, 100, chi=cfg.chi, dt_cap=cfg.dt)
+        d = c.pks_diagnostics(rho, cc)
+        M.append(d["second_moment"])
+        E.append(d["free_energy"])
+    assert all(b > a for a, b in zip(M, M[1:])), M
+    assert all(b < a for a, b in zip(E, E[1:])), E
+
+
+def api_mod():
+    from paper_1811_03557_b200 import api as A
+    return A

@@ -1,4 +1,6 @@
 """Pins for oracle/pks.py: the FV/IMEX scheme, CFL, Steps 3-7."""
+import math
+
 import numpy as np
 import pytest
 
@@ -98,3 +100,60 @@ def test_cfg2_run_survey_probe_values():
     assert abs(m0 / 5.5683279893 - 1) < 1e-9
     # positivity (Thm 3) up to round-off
     assert rho.min() > -1e-9 * rho.max() and c.min() > -1e-9 * c.max()
+
+
+# ------------------------------------------------------------------ diagnostics
+def _diag_loops(rho, c, g, ps, center):
+    """Brute force over the nodes with explicit neighbour lookups (independent of the padded-array form)."""
+    n, h = g.n, g.h
+    x = g.coords()
+    mass = second = free = 0.0
+    cv = lambda i, j, k: c[i, j, k] if 0 <= i < n and 0 <= j < n and 0 <= k < n else 0.0   # noqa: E731
+    for i in range(n):
+        for j in range(n):
+            for k in range(n):
+                if not ps.mplus[i, j, k]:
+                    continue
+                r, cc = rho[i, j, k], c[i, j, k]
+                mass += r
+                second += ((x[i] - center[0]) ** 2 + (x[j] - center[1]) ** 2 + (x[k] - center[2]) ** 2) * r
+                g2 = ((cv(i + 1, j, k) - cv(i - 1, j, k)) ** 2 + (cv(i, j + 1, k) - cv(i, j - 1, k)) ** 2
+                      + (cv(i, j, k + 1) - cv(i, j, k - 1)) ** 2)
+                free += (r * math.log(r) if r > 0 else 0.0) - r * cc + 0.5 * cc * cc + g2 / (8 * h * h)
+    return {"mass": h ** 3 * mass, "second_moment": h ** 3 * second, "free_energy": h ** 3 * free}
+
+
+def test_diagnostics_brute_force_and_closed_forms():
+    cfg = get_config("cfg1")
+    g, ps = grid.point_sets_for(cfg)
+    rng = np.random.default_rng(3)
+    rho = rng.uniform(-0.1, 2.0, size=(g.n,) * 3)     # includes ρ <= 0 (ρ ln ρ := 0, R35)
+    c = rng.uniform(0.0, 3.0, size=(g.n,) * 3)
+    d = pks.diagnostics(rho, c, g, ps, cfg.center)
+    b = _diag_loops(rho, c, g, ps, cfg.center)
+    for k in d:
+        assert abs(d[k] - b[k]) <= 1e-12 * abs(b[k]), k
+    # constant state on cfg2 (no M+ node next to the ghost layer there, unlike cfg1's 72, R5):
+    # no gradient term, E = h^3 |M+| (ρ ln ρ - ρ c + c^2/2)
+    cfg = get_config("cfg2")
+    g, ps = grid.point_sets_for(cfg)
+    assert ps.ghosts_in_nplus == 0
+    nm = int(ps.mplus.sum())
+    d = pks.diagnostics(np.full((g.n,) * 3, 2.0), np.full((g.n,) * 3, 3.0), g, ps, cfg.center)
+    assert abs(d["free_energy"] - g.h ** 3 * nm * (2 * math.log(2) - 6 + 4.5)) < 1e-13 * nm * g.h ** 3
+    assert abs(d["mass"] - 2 * g.h ** 3 * nm) < 1e-12
+    # linear c = a x: the central difference is exact, gradient term h^3 |M+| a^2 / 2
+    a = 1.7
+    X = np.broadcast_to(g.coords()[:, None, None], (g.n,) * 3)
+    d = pks.diagnostics(np.zeros((g.n,) * 3), a * X, g, ps, cfg.center)
+    ref = g.h ** 3 * (0.5 * a * a * np.sum(X[ps.mplus] ** 2) + nm * a * a / 2)
+    assert abs(d["free_energy"] - ref) < 1e-12 * ref
+
+
+def test_second_moment_continuum_limit():
+    # ρ = 1 on M+ of the unit ball: M_h -> ∫_B |x|^2 dx = 4π/5 (first order in h: staircase boundary)
+    cfg = get_config("cfg2")
+    g, ps = grid.point_sets_for(cfg)
+    d = pks.diagnostics(np.ones((g.n,) * 3), np.zeros((g.n,) * 3), g, ps, cfg.center)
+    assert abs(d["second_moment"] / (4 * math.pi / 5) - 1) < 0.1
+    assert abs(d["mass"] / (4 * math.pi / 3) - 1) < 0.1
