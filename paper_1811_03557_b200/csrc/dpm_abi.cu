@@ -357,15 +357,12 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   double* gvec = wk + 2 * field;          // |gamma_in| x 2
   double* ug = gvec + 2 * ngin;           // |gamma| x 2
   double* coef = ug + 2 * ng;             // K x 2
-  if (backup) {
-    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(backup, rho, field * 8, cudaMemcpyDeviceToDevice, s));
-    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(backup + field, c, field * 8, cudaMemcpyDeviceToDevice, s));
-  }
   if (prm->dt_rule == 0) {   // Step 3 on the device: did the speculative dt stay valid?
     DPM_CUDA_TRY(ctx, launch_cfl_dt(ctx, c, slot, prm->chi, dt, prm->dt_cap, slot + 3, s));
   }
   // Step 4a: flux + IMEX right-hand sides, particular solutions
-  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s));
+  // (the flux kernel also writes the step's rollback copy of rho, c into `backup` when non-null)
+  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup));
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
   // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp
   DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
