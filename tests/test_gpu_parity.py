@@ -394,6 +394,10 @@ def test_pks_parity(api, name, dt_rule):
         assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
         assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
     assert sum(l["rebuilt"] for l in logs) == o.builds
+    # the step log's ||ρ||∞ over M+  and over N+ against the final fields
+    g, ps = grid.point_sets_for(cfg)
+    assert logs[-1]["rho_max_mplus"] == rho[ps.mplus].max()
+    assert logs[-1]["rho_max"] == rho[ps.nplus].max()
 
 
 @pytest.mark.parametrize("basis", ["neumann0_zonal", "neumann0_2term_zonal"])
