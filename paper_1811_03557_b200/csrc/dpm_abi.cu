@@ -202,24 +202,26 @@ dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* 
   cudaStream_t s = as_stream(stream);
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   // Three-stage pipeline over chunks of <= 128 MB: H2D (copy-in stream) -> solve (caller's stream)
-  // -> D2H (copy-out stream), double-buffered so that chunk i+1 uploads and chunk i-1 downloads
-  // while chunk i is solved (PCIe is full duplex; pinned host buffers give async copies).
+  // -> D2H (copy-out stream) over a ring of NBUF device buffers, so that chunk i+1 uploads and chunk
+  // i-1 downloads while chunk i is solved (PCIe is full duplex; pinned host buffers give async
+  // copies).  Three buffers: with two, the upload of chunk i+1 waited for the download of chunk i-1
+  // (same buffer) and the two directions serialized at every buffer switch.
+  constexpr int NBUF = 3;
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)(((size_t)128 << 20) / (field * 8))));
-  dpm_status st = ensure_work(ctx, 2 * chunk);
+  dpm_status st = ensure_work(ctx, NBUF * chunk);
   if (st != DPM_OK) return st;
   if (!ctx->h2d_stream) {
     DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
     DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 6; ++i) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->pipe_ev[i], cudaEventDisableTiming));
+    for (int i = 0; i < 3 * NBUF; ++i) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->pipe_ev[i], cudaEventDisableTiming));
   }
-  cudaEvent_t* up = ctx->pipe_ev;       // up[b]: upload into buffer b done
-  cudaEvent_t* solved = ctx->pipe_ev + 2;
-  cudaEvent_t* down = ctx->pipe_ev + 4; // down[b]: download from buffer b done (buffer free)
-  DPM_CUDA_TRY(ctx, cudaEventRecord(down[0], s));
-  DPM_CUDA_TRY(ctx, cudaEventRecord(down[1], s));
+  cudaEvent_t* up = ctx->pipe_ev;              // up[b]: upload into buffer b done
+  cudaEvent_t* solved = ctx->pipe_ev + NBUF;
+  cudaEvent_t* down = ctx->pipe_ev + 2 * NBUF; // down[b]: download from buffer b done (buffer free)
+  for (int b = 0; b < NBUF; ++b) DPM_CUDA_TRY(ctx, cudaEventRecord(down[b], s));
   for (int64_t b0 = 0, it = 0; b0 < batch; b0 += chunk, ++it) {
     const int64_t nb = std::min<int64_t>(chunk, batch - b0);
-    const int bi = (int)(it & 1);
+    const int bi = (int)(it % NBUF);
     double* buf = ctx->work + (size_t)bi * chunk * field;
     DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->h2d_stream, down[bi], 0));
     DPM_CUDA_TRY(ctx, cudaMemcpyAsync(buf, host_q + b0 * field, nb * field * 8, cudaMemcpyHostToDevice, ctx->h2d_stream));

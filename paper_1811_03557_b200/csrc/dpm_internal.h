@@ -130,7 +130,7 @@ struct dpm_ctx {
   int bepf_cols = 0;
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-  cudaEvent_t pipe_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
   double* red = nullptr;         // device reduction slots
   double* red_host = nullptr;    // pinned
 };
