@@ -551,3 +551,14 @@ def test_paper_free_energy_and_second_moment_trends():
 def api_mod():
     from paper_1811_03557_b200 import api as A
     return A
+
+
+@pytest.mark.parametrize("N", [36, 68, 127, 132])
+def test_point_sets_bit_exact_paper_meshes(api, N):
+    # the paper's meshes used by tools/test_a.py / test_b.py: GPU sets bit-exact vs the oracle
+    from dpm_inputs import test_a_config
+    cfg = test_a_config(N)
+    c = api.DPM.from_config(cfg)
+    g, ps = grid.point_sets_for(cfg)
+    for w in ["mplus", "gamma", "gamma_in", "gamma_ex", "band", "nplus"]:
+        assert np.array_equal(c.copy_set(w), ps.list(w)), (N, w)

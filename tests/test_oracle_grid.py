@@ -89,3 +89,20 @@ def test_gamma_scaling():
         g = grid.Grid(n, -1.1, 1.1)
         sizes.append(grid.point_sets(g, "sphere", (0, 0, 0), (1, 1, 1)).gamma.sum())
     assert 0.2 <= sizes[0] / sizes[1] <= 0.35
+
+
+@pytest.mark.parametrize("N", [36, 68, 132])
+def test_paper_mesh_point_sets(N):
+    # the paper's mesh convention through dpm_inputs.paper_mesh: h = 2r/(N-4), cell centres at
+    # -r + (j - 5/2) h, against the survey's independent exact-integer counts (probe P1)
+    from dpm_inputs import paper_mesh
+    n, lo, hi, h = paper_mesh(N, 0.5)
+    assert n == N and abs(h - 1.0 / (N - 4)) < 1e-16
+    g = grid.Grid(n, lo, hi)
+    assert abs(g.h - h) < 1e-15
+    x = g.coords()
+    assert np.allclose(x, -0.5 + (np.arange(1, N + 1) - 2.5) * h, atol=1e-14)
+    ps = grid.point_sets(g, "sphere", (0.0, 0.0, 0.0), (0.5, 0.5, 0.5))
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "point_set_counts.json")))["paper_meshes"][str(N)]
+    assert len(ps.list("gamma")) == ref["gamma"]
+    assert len(ps.list("gamma_in")) == ref["gamma_in"]
