@@ -182,6 +182,9 @@ typedef struct {
   double center[3];        /* Gaussian centre                                    */
   double rho_amp, rho_rate;/* rho0 = rho_amp * exp(-rho_rate |x - center|^2)      */
   double c_amp, c_rate;    /* c0   = c_amp   * exp(-c_rate   |x - center|^2)      */
+  int32_t rho_cell_average;/* 1: rho-bar on M+ \ gamma is the cell average of rho0 over
+                              [x - h/2, x + h/2]^3 (the paper evolves cell averages, P:86;
+                              R36), in closed form via erf; 0: node values (R14)         */
 } dpm_pks_ic;
 
 typedef struct {
@@ -199,7 +202,8 @@ typedef struct {
                              rho_max above is over N+ (includes gamma_ex) */
 } dpm_step_log;
 
-/* Initial state (R14): IC at the node on M+\gamma, at the foot point on gamma, 0 elsewhere.
+/* Initial state (R14): IC at the node on M+\gamma (or, for rho with ic->rho_cell_average, its
+   cell average there, R36), at the foot point on gamma, 0 elsewhere.
    Resets t and the dt history. Asynchronous. */
 dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream);
 

@@ -19,7 +19,10 @@ SURVEY.md §8(c) R13-R20 (listed in DESIGN.md):
 State: ρ̄ and c as [n][n][n] arrays holding values on N+ ∩ M0 (0 elsewhere); ghost
 nodes of N+ hold 0 (Dirichlet AP, R5).
 """
+import math
+
 import numpy as np
+import scipy.special
 
 from . import ap, dpm, grid
 
@@ -120,8 +123,11 @@ class PKSOracle:
         self.builds = 0
         self.t = 0.0
 
-    def initial_state(self):
-        """R14: IC at the node on M+ \\ γ, at the foot point on γ; 0 elsewhere."""
+    def initial_state(self, rho_cell_average: bool = False):
+        """R14: IC at the node on M+ \\ γ, at the foot point on γ; 0 elsewhere.  With rho_cell_average
+        (R36; the paper evolves cell averages ρ̄), ρ̄ on M+ \\ γ is the average of ρ0 over the cell
+        [x - h/2, x + h/2]^3: for A exp(-a |x - x0|^2) the product over the axes of
+        sqrt(π/a) (erf(√a (s + h/2)) - erf(√a (s - h/2))) / (2h), s = x - x0."""
         cfg, g, ps = self.cfg, self.g, self.ps
         n = g.n
         x = g.coords()
@@ -132,6 +138,18 @@ class PKSOracle:
             return A * np.exp(-a * ((XX - c0[0]) ** 2 + (YY - c0[1]) ** 2 + (ZZ - c0[2]) ** 2))
 
         rho = np.where(ps.nplus, ic(*cfg.ic_rho, X, Y, Z), 0.0)
+        if rho_cell_average:
+            A, a = cfg.ic_rho
+            h = g.h
+
+            def avg1(s):
+                if a <= 0:
+                    return np.ones_like(s)
+                q = math.sqrt(a)
+                return math.sqrt(math.pi / a) * (scipy.special.erf(q * (s + h / 2)) - scipy.special.erf(q * (s - h / 2))) / (2 * h)
+
+            cell = A * avg1(X - c0[0]) * avg1(Y - c0[1]) * avg1(Z - c0[2])
+            rho = np.where(ps.mplus, cell, rho)    # γ_in values are overwritten by the foot values below
         c = np.where(ps.nplus, ic(*cfg.ic_c, X, Y, Z), 0.0)
         gidx = ps.list("gamma")
         F = self.foot

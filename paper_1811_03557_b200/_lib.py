@@ -47,7 +47,7 @@ class Info(C.Structure):
 
 class PksIC(C.Structure):
     _fields_ = [("center", C.c_double * 3), ("rho_amp", C.c_double), ("rho_rate", C.c_double),
-                ("c_amp", C.c_double), ("c_rate", C.c_double)]
+                ("c_amp", C.c_double), ("c_rate", C.c_double), ("rho_cell_average", C.c_int32)]
 
 
 class PksParams(C.Structure):

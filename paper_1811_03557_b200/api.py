@@ -173,8 +173,9 @@ class DPM:
         self._chk(L.lib.dpm_boundary_lsq(self._h, _ptr(g), _ptr(coef), _ptr(ug), nrhs, _stream(stream)))
         return coef, ug
 
-    def pks_init(self, rho: torch.Tensor, c: torch.Tensor, center, rho_amp, rho_rate, c_amp, c_rate, stream=None):
-        ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate)
+    def pks_init(self, rho: torch.Tensor, c: torch.Tensor, center, rho_amp, rho_rate, c_amp, c_rate, stream=None,
+                 rho_cell_average=False):
+        ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate, 1 if rho_cell_average else 0)
         self._chk(L.lib.dpm_pks_init(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), C.byref(ic),
                                      _stream(stream)))
 

@@ -329,6 +329,14 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
   }
 }
 
+// cell average of exp(-rate s^2) over [s - h/2, s + h/2] (R36): sqrt(π/rate) (erf(√rate (s + h/2)) -
+// erf(√rate (s - h/2))) / (2h); 1 for rate = 0
+__device__ __forceinline__ double gauss_cell_avg1(double s, double rate, double h) {
+  if (!(rate > 0.0)) return 1.0;
+  const double q = sqrt(rate);
+  return 0.88622692545275801365 / q * (erf(q * (s + 0.5 * h)) - erf(q * (s - 0.5 * h))) / h;   // sqrt(π)/2
+}
+
 __global__ void pks_init_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap,
                                 const double* __restrict__ foot, int n, double lo, double h, dpm_pks_ic ic, double* rho,
                                 double* c) {
@@ -349,6 +357,9 @@ __global__ void pks_init_kernel(const uint8_t* __restrict__ flags, const int32_t
                         (z - ic.center[2]) * (z - ic.center[2]);
       a = ic.rho_amp * exp(-ic.rho_rate * r2);
       b = ic.c_amp * exp(-ic.c_rate * r2);
+      if (ic.rho_cell_average && g < 0 && (f & F_MPLUS))   // R36: ρ̄0 = cell average on M+ \ γ
+        a = ic.rho_amp * gauss_cell_avg1(x - ic.center[0], ic.rho_rate, h) *
+            gauss_cell_avg1(y - ic.center[1], ic.rho_rate, h) * gauss_cell_avg1(z - ic.center[2], ic.rho_rate, h);
     }
     rho[p] = a;
     c[p] = b;

@@ -471,21 +471,36 @@ def test_paper_test_b_blowup_time():
 # ------------------------------------------------------------------ NEXT-2: the paper's Test A convergence
 def test_paper_test_a_max_density_convergence():
     # Test A, SD, the paper's meshes N = 36/68/132/260, 3-term extension with one
-    # zonal harmonic per term, dt = 1e-8 to T = 1e-6: E_rel of ||ρ^i||∞ against the
-    # paper's reference, the N = 516 run.
+    # zonal harmonic per term, dt = 1e-8 to T = 1e-6, ρ̄0 as cell averages (R36): E_rel of
+    # ||ρ^i||∞ against the paper's reference, the N = 516 run.
     # Paper (Table 3, SD): 1.0196e-1 / 2.6378e-2 / 6.3461e-3 / 1.2724e-3, rates 1.95 / 2.06 / 2.32.
-    # Measured: 8.13e-2 / 2.06e-2 / 4.94e-3 / 9.89e-4 (0.78-0.80 x the paper's), rates 1.98 / 2.06 / 2.32.
+    # Measured: 1.0214e-1 / 2.6407e-2 / 6.3518e-3 / 1.2735e-3 (+0.08 ... +0.18%), rates 1.95 / 2.06 / 2.32.
+    # (With node-value ICs, R14: 0.78-0.80 x the paper's values, same rates.)
     import os, sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
     import test_a
+    test_a.IC_CELL = True
     res = test_a.run((36, 68, 132, 260, 516))
     rows = {r["N"]: r for r in res["rows"]}
     for N, paper_rate in ((68, 1.95), (132, 2.06), (260, 2.32)):
-        assert abs(rows[N]["rate"] - paper_rate) <= 0.05, rows[N]
+        assert abs(rows[N]["rate"] - paper_rate) <= 0.01, rows[N]
     for N in (36, 68, 132, 260):
-        assert 0.7 <= rows[N]["E_rel"] / rows[N]["paper_E_rel"] <= 1.0, rows[N]
+        assert abs(rows[N]["E_rel"] / rows[N]["paper_E_rel"] - 1) <= 0.005, rows[N]
         assert abs(rows[N]["mass_drift"]) < 1e-12                     # conservation
         assert abs(rows[N]["t_end"] - 1e-6) < 1e-18
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_pks_init_cell_average_parity(api, name):
+    # R36: ρ̄0 = cell average of the Gaussian IC on M+ \ γ (erf closed form), against the oracle
+    cfg = get_config(name)
+    c = api.DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c, rho_cell_average=True)
+    ro, co = pks.PKSOracle(cfg).initial_state(rho_cell_average=True)
+    assert rel(rho.cpu().numpy(), ro) <= 1e-14
+    assert rel(cc.cpu().numpy(), co) <= 1e-14
 
 
 def test_paper_test_a_time_convergence_rates():

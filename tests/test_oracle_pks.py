@@ -157,3 +157,30 @@ def test_second_moment_continuum_limit():
     d = pks.diagnostics(np.ones((g.n,) * 3), np.zeros((g.n,) * 3), g, ps, cfg.center)
     assert abs(d["second_moment"] / (4 * math.pi / 5) - 1) < 0.1
     assert abs(d["mass"] / (4 * math.pi / 3) - 1) < 0.1
+
+
+def test_cell_average_initial_state():
+    # R36: ρ̄0 on M+ \ γ is the cell average of ρ0 = A exp(-a |x - x0|^2); against tensor-product
+    # Gauss-Legendre quadrature over the cell (exact to ~1e-15 for these smooth integrands)
+    cfg = get_config("cfg3")   # off-centre IC (0.2, 0, 0) on the ellipsoid
+    o = pks.PKSOracle(cfg)
+    rho_pt, _ = o.initial_state()
+    rho, c = o.initial_state(rho_cell_average=True)
+    g, ps = o.g, o.ps
+    x = g.coords()
+    t, w = np.polynomial.legendre.leggauss(16)
+    A, a = cfg.ic_rho
+    x0 = np.asarray(cfg.ic_center)
+    inner = ps.mplus & ~ps.gamma
+    idx = np.argwhere(inner)
+    rng = np.random.default_rng(0)
+    for i, j, k in idx[rng.choice(len(idx), 25, replace=False)]:
+        pts = [x[q] + 0.5 * g.h * t for q in (i, j, k)]
+        f = [np.sum(0.5 * w * np.exp(-a * (pts[d] - x0[d]) ** 2)) for d in range(3)]
+        ref = A * f[0] * f[1] * f[2]
+        assert abs(rho[i, j, k] - ref) <= 1e-13 * A, (i, j, k)
+    # γ keeps the foot-point values (R14) and c stays a point value
+    assert np.array_equal(rho[ps.gamma], rho_pt[ps.gamma])
+    assert np.array_equal(c, o.initial_state()[1])
+    # averaging a peaked Gaussian lowers the maximum
+    assert rho[inner].max() < rho_pt[inner].max()

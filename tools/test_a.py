@@ -40,12 +40,15 @@ PAPER_E_T_RHO = {16: 8.2335e-03, 32: 3.9846e-03, 64: 1.8596e-03, 128: 7.9700e-04
 PAPER_E_T_C = {16: 6.1248e-08, 32: 2.9665e-08, 64: 1.3889e-08, 128: 5.9737e-09, 256: 2.0236e-09}
 
 
+IC_CELL = True   # ρ̄0 as cell averages (R36, the paper's reading: Table 3 to ~0.1%); False: node values (R14)
+
+
 def series(N):
     cfg = test_a_config(N)
     ctx = api.DPM.from_config(cfg)
     rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
     c = torch.zeros_like(rho)
-    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c, rho_cell_average=IC_CELL)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=1, clamp=1)
@@ -56,7 +59,7 @@ def series(N):
                "mass_drift": logs[-1]["mass"] / logs[0]["mass"] - 1.0, "wall_s": wall}
 
 
-def run(Ns=(36, 68, 132, 260)):
+def run(Ns=(36, 68, 132, 260, 516)):
     Ns = sorted(Ns)
     S, info = {}, {}
     for N in Ns:
@@ -74,8 +77,8 @@ def run(Ns=(36, 68, 132, 260)):
         rows.append(dict(info[N], E_rel=e, paper_E_rel=PAPER_E_REL.get(N)))
     for a, b in zip(rows, rows[1:]):
         b["rate"] = math.log2(a["E_rel"] / b["E_rel"]) if b["E_rel"] > 0 else None
-    return {"test": "A", "reference": ref, "rows": rows,
-            "reference_run": info[f] if f == 516 else None}
+    return {"test": "A", "reference": ref, "ic": "cell averages (R36)" if IC_CELL else "node values (R14)",
+            "rows": rows, "reference_run": info[f] if f == 516 else None}
 
 
 def final_state(N, tau):
@@ -84,7 +87,7 @@ def final_state(N, tau):
     ctx = api.DPM.from_config(cfg)
     rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
     c = torch.zeros_like(rho)
-    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c, rho_cell_average=IC_CELL)
     t0 = time.perf_counter()
     logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=dt, dt_rule=1, clamp=1)
     torch.cuda.synchronize()
@@ -110,7 +113,10 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--N", type=int, nargs="+", default=None)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--ic", choices=["cell", "point"], default="cell",
+                    help="ρ̄0 on M+ \\ γ: cell averages (R36, default) or node values (R14)")
     a = ap.parse_args()
+    IC_CELL = a.ic == "cell"
     if a.time:
         print(json.dumps(run_time(a.N[0] if a.N else 255)))
     else:

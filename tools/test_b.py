@@ -22,12 +22,13 @@ from dpm_inputs import test_b_config  # noqa: E402
 from paper_1811_03557_b200 import api  # noqa: E402
 
 
-def run(N=127, harmonics=150, t_end=0.2, max_steps=100000):
+def run(N=127, harmonics=150, t_end=0.2, max_steps=100000, cell_average=True):
     cfg = test_b_config(N, harmonics)
     ctx = api.DPM.from_config(cfg)
     rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
     c = torch.zeros_like(rho)
-    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    # ρ̄0 as cell averages (R36, the paper's reading; node values with cell_average=False, R14)
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c, rho_cell_average=cell_average)
     torch.cuda.synchronize()
     logs, prev_max, stop = [], float(rho.max()), None
     t0 = time.perf_counter()
@@ -48,6 +49,7 @@ def run(N=127, harmonics=150, t_end=0.2, max_steps=100000):
     wall = time.perf_counter() - t0
     res = {
         "test": "B", "N": N, "harmonics": harmonics, "K": ctx.K, "h": ctx.info["h"], "dt0": cfg.dt,
+        "ic": "cell averages (R36)" if cell_average else "node values (R14)",
         "t_stop": stop["t"] if stop else None, "rho_max_stop": stop["rho_max_mplus"] if stop else None,
         "steps": len(logs), "rebuilds": sum(int(l["rebuilt"]) for l in logs),
         "steps_cfl": sum(1 for l in logs if l["dt"] < cfg.dt), "dt_min": min(l["dt"] for l in logs),
@@ -63,8 +65,9 @@ if __name__ == "__main__":
     ap.add_argument("--N", type=int, default=127)
     ap.add_argument("--harmonics", type=int, default=150)
     ap.add_argument("--log", default=None, help="write the per-step log (JSON) here")
+    ap.add_argument("--ic", choices=["cell", "point"], default="cell")
     a = ap.parse_args()
-    res, logs = run(a.N, a.harmonics)
+    res, logs = run(a.N, a.harmonics, cell_average=a.ic == "cell")
     if a.log:
         json.dump(logs, open(a.log, "w"))
     print(json.dumps(res))
