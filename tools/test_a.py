@@ -81,9 +81,9 @@ def run(Ns=(36, 68, 132, 260, 516)):
             "rows": rows, "reference_run": info[f] if f == 516 else None}
 
 
-def final_state(N, tau):
-    dt = 1e-7 / tau
-    cfg = test_a_config(N, dt=dt, steps=10 * tau)
+def final_state(N, tau, T=1e-6, dT=1e-7):
+    dt = dT / tau
+    cfg = test_a_config(N, dt=dt, steps=int(round(T / dt)))
     ctx = api.DPM.from_config(cfg)
     rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
     c = torch.zeros_like(rho)
@@ -95,12 +95,12 @@ def final_state(N, tau):
     return rho.reshape(-1)[mp], c.reshape(-1)[mp], logs[-1]["t"], time.perf_counter() - t0
 
 
-def run_time(N=255, taus=(16, 32, 64, 128, 256), tau_ref=512):
-    rr, cr, tr, wr = final_state(N, tau_ref)
+def run_time(N=255, taus=(16, 32, 64, 128, 256), tau_ref=512, T=1e-6, dT=1e-7):
+    rr, cr, tr, wr = final_state(N, tau_ref, T, dT)
     rows = []
     for tau in taus:
-        r, c, t, w = final_state(N, tau)
-        rows.append({"tau": tau, "dt": 1e-7 / tau, "t_end": t, "wall_s": w,
+        r, c, t, w = final_state(N, tau, T, dT)
+        rows.append({"tau": tau, "dt": dT / tau, "t_end": t, "wall_s": w,
                      "E_t_rho": float((r - rr).abs().max()), "paper_E_t_rho": PAPER_E_T_RHO.get(tau),
                      "E_t_c": float((c - cr).abs().max()), "paper_E_t_c": PAPER_E_T_C.get(tau)})
     for a, b in zip(rows, rows[1:]):
