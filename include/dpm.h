@@ -192,6 +192,9 @@ typedef struct {
   double dt_cap;           /* configured dt                                      */
   int32_t dt_rule;         /* 0: dt_i = min(dt_{i-1}, dt_cap, CFL, h^2/2) (R13); 1: fixed dt_cap */
   int32_t clamp;           /* 1: u_gamma = max(u_gamma, 0) (R17)                  */
+  int32_t coupling;        /* 0: the printed IMEX step (the c equation uses rho-bar^i);
+                              1: sequential, the c equation uses rho-bar^{i+1} (an alternative
+                              reading probed against Table 4)           */
 } dpm_pks_params;
 
 typedef struct {

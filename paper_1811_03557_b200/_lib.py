@@ -51,7 +51,8 @@ class PksIC(C.Structure):
 
 
 class PksParams(C.Structure):
-    _fields_ = [("chi", C.c_double), ("dt_cap", C.c_double), ("dt_rule", C.c_int32), ("clamp", C.c_int32)]
+    _fields_ = [("chi", C.c_double), ("dt_cap", C.c_double), ("dt_rule", C.c_int32), ("clamp", C.c_int32),
+                ("coupling", C.c_int32)]
 
 
 class StepLog(C.Structure):

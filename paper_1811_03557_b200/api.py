@@ -186,8 +186,8 @@ class DPM:
                                             _stream(stream)))
         return {"mass": out[0], "second_moment": out[1], "free_energy": out[2]}
 
-    def pks_step(self, rho, c, nsteps, chi=1.0, dt_cap=1e-4, dt_rule=0, clamp=1, stream=None):
-        prm = L.PksParams(chi, dt_cap, dt_rule, clamp)
+    def pks_step(self, rho, c, nsteps, chi=1.0, dt_cap=1e-4, dt_rule=0, clamp=1, stream=None, coupling=0):
+        prm = L.PksParams(chi, dt_cap, dt_rule, clamp, coupling)
         logs = (L.StepLog * max(nsteps, 1))()
         self._chk(L.lib.dpm_pks_step(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), nsteps,
                                      C.byref(prm), logs, _stream(stream)))

@@ -365,6 +365,21 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   // Step 4a: flux + IMEX right-hand sides, particular solutions
   // (the flux kernel also writes the step's rollback copy of rho, c into `backup` when non-null)
   DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup));
+  if (prm->coupling == 1) {   // sequential: the whole ρ step, then the c step from ρ̄^{i+1}
+    const int K = ctx->K;
+    for (int r = 0; r < 2; ++r) {
+      double* fr = fq + r * field;
+      double* wr = wk + r * field;
+      if (r == 1) DPM_CUDA_TRY(ctx, launch_fc_seq(ctx, c, wk, dt, fr, s));
+      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fr, wr, 1, nullptr, 0, s));
+      DPM_CUDA_TRY(ctx, launch_trace(ctx, wr, gvec + r * ngin, DPM_SET_GAMMA_IN, 1, s));
+      DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec + r * ngin, coef + (size_t)r * K, ug + r * ng, 1, prm->clamp, s));
+      DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fr, ug + r * ng, wr, 1, s));
+      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wr, wr, 1, nullptr, 0, s));
+    }
+    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s));
+    return DPM_OK;
+  }
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
   // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp
   DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
@@ -381,7 +396,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
                             dpm_ctx::PksGraph** out) {
   for (auto& g : ctx->pks_graphs)
     if (g.dt == dt && g.k == K && g.chi == prm->chi && g.cap == prm->dt_cap && g.rule == prm->dt_rule &&
-        g.clamp == prm->clamp && g.rho == rho && g.c == c) {
+        g.clamp == prm->clamp && g.coupling == prm->coupling && g.rho == rho && g.c == c) {
       *out = &g;
       return DPM_OK;
     }
@@ -410,6 +425,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   if (ec != cudaSuccess) { ctx->err = std::string("graph capture: ") + cudaGetErrorString(ec); return DPM_ERR_CUDA; }
   dpm_ctx::PksGraph g;
   g.dt = dt; g.k = K; g.chi = prm->chi; g.cap = prm->dt_cap; g.rule = prm->dt_rule; g.clamp = prm->clamp;
+  g.coupling = prm->coupling;
   g.rho = rho; g.c = c; g.launches = nk;
   const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -427,6 +443,7 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
                         dpm_step_log* log, void* stream) {
   if (!ctx || !rho || !c || !prm || nsteps < 0) return DPM_ERR_INVALID;
   if (!(prm->dt_cap > 0) || !(prm->chi > 0)) { ctx->err = "dt_cap and chi must be > 0"; return DPM_ERR_INVALID; }
+  if (prm->coupling != 0 && prm->coupling != 1) { ctx->err = "coupling must be 0 or 1"; return DPM_ERR_INVALID; }
   if (!ctx->pks_initialized) { ctx->t = 0.0; ctx->dt_prev = INFINITY; ctx->pks_initialized = 1; }
   if (nsteps == 0) return DPM_OK;
   cudaSetDevice(ctx->device);

@@ -94,7 +94,7 @@ struct dpm_ctx {
   static constexpr int PKS_K = 10;
   struct PksGraph {
     double dt = 0, chi = 0, cap = 0;
-    int k = 0, rule = 0, clamp = 0;
+    int k = 0, rule = 0, clamp = 0, coupling = 0;
     double* rho = nullptr;
     double* c = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -226,6 +226,7 @@ cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaS
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi,
                             double* fq_rho, double* fq_c, cudaStream_t s,
                             double* backup = nullptr);
+cudaError_t launch_fc_seq(dpm_ctx* ctx, const double* c, const double* rho_new, double dt, double* fq_c, cudaStream_t s);
 cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
                              cudaStream_t s);
 cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s);

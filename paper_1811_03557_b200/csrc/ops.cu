@@ -492,6 +492,22 @@ cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, do
   return cudaGetLastError();
 }
 
+// sequential coupling (dpm_pks_params.coupling = 1): f_c / dt = ((1 - dt) c + dt ρ̄^{i+1}) / dt on M+
+__global__ void __launch_bounds__(TB, STENCIL_MINB) fc_seq_kernel(const uint8_t* __restrict__ flags, long nn,
+                                                          const double* __restrict__ c, const double* __restrict__ rho_new,
+                                                          double dt, double* __restrict__ fq_c) {
+  const double idt = 1.0 / dt;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x)
+    fq_c[p] = (flags[p] & F_MPLUS) ? ((1.0 - dt) * c[p] + dt * rho_new[p]) * idt : 0.0;
+}
+
+cudaError_t launch_fc_seq(dpm_ctx* ctx, const double* c, const double* rho_new, double dt, double* fq_c, cudaStream_t s) {
+  const long nn = (long)ctx->n * ctx->n * ctx->n;
+  DPM_COUNT_LAUNCH(1);
+  fc_seq_kernel<<<grid_for(nn), TB, 0, s>>>(ctx->flags, nn, c, rho_new, dt, fq_c);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
                              cudaStream_t s) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;

@@ -81,7 +81,7 @@ def run(Ns=(36, 68, 132, 260, 516)):
             "rows": rows, "reference_run": info[f] if f == 516 else None}
 
 
-def final_state(N, tau, T=1e-6, dT=1e-7):
+def final_state(N, tau, T=1e-6, dT=1e-7, coupling=0):
     dt = dT / tau
     cfg = test_a_config(N, dt=dt, steps=int(round(T / dt)))
     ctx = api.DPM.from_config(cfg)
@@ -89,17 +89,17 @@ def final_state(N, tau, T=1e-6, dT=1e-7):
     c = torch.zeros_like(rho)
     ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c, rho_cell_average=IC_CELL)
     t0 = time.perf_counter()
-    logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=dt, dt_rule=1, clamp=1)
+    logs = ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=dt, dt_rule=1, clamp=1, coupling=coupling)
     torch.cuda.synchronize()
     mp = torch.from_numpy(ctx.copy_set("mplus")).cuda()
     return rho.reshape(-1)[mp], c.reshape(-1)[mp], logs[-1]["t"], time.perf_counter() - t0
 
 
-def run_time(N=255, taus=(16, 32, 64, 128, 256), tau_ref=512, T=1e-6, dT=1e-7):
-    rr, cr, tr, wr = final_state(N, tau_ref, T, dT)
+def run_time(N=255, taus=(16, 32, 64, 128, 256), tau_ref=512, T=1e-6, dT=1e-7, coupling=0):
+    rr, cr, tr, wr = final_state(N, tau_ref, T, dT, coupling)
     rows = []
     for tau in taus:
-        r, c, t, w = final_state(N, tau, T, dT)
+        r, c, t, w = final_state(N, tau, T, dT, coupling)
         rows.append({"tau": tau, "dt": dT / tau, "t_end": t, "wall_s": w,
                      "E_t_rho": float((r - rr).abs().max()), "paper_E_t_rho": PAPER_E_T_RHO.get(tau),
                      "E_t_c": float((c - cr).abs().max()), "paper_E_t_c": PAPER_E_T_C.get(tau)})
