@@ -109,7 +109,7 @@ def cfl_dt(c: np.ndarray, ps: grid.PointSets, h: float, chi: float) -> float:
 class PKSOracle:
     """Steps 1-8 for one single-domain configuration."""
 
-    def __init__(self, cfg, dt_rule: int = 0, clamp: bool = True):
+    def __init__(self, cfg, dt_rule: int = 0, clamp: bool = True, coupling: int = 0):
         self.cfg = cfg
         self.g, self.ps = grid.point_sets_for(cfg)
         self.E, self.d, self.unit, self.foot = dpm.extension_matrix(
@@ -117,6 +117,7 @@ class PKSOracle:
         self.gin_pos = np.searchsorted(self.ps.list("gamma"), self.ps.list("gamma_in"))
         self.dt_rule = dt_rule
         self.clamp = clamp
+        self.coupling = coupling   # 1: the c equation uses ρ̄^{i+1} (sequential; not the printed P:89-96)
         self.dt_prev = np.inf
         self.dt_bep = None
         self.B = None
@@ -176,7 +177,10 @@ class PKSOracle:
         f_rho, f_c = assemble_rhs(rho, c, gconv, dt)                                # Step 4a
         out = []
         us = []
-        for f in (f_rho, f_c):
+        for r in range(2):
+            if r == 1 and self.coupling == 1:
+                _, f_c = assemble_rhs(out[0], c, gconv, dt)                         # c from ρ̄^{i+1}
+            f = (f_rho, f_c)[r]
             up = ap.solve(dpm.particular_rhs(f, ps, dt), h, dt)                      # G f
             rhs = up.reshape(-1)[ps.list("gamma_in")]
             C = dpm.lstsq(self.B, rhs)                                              # Step 5

@@ -577,3 +577,19 @@ def test_point_sets_bit_exact_paper_meshes(api, N):
     g, ps = grid.point_sets_for(cfg)
     for w in ["mplus", "gamma", "gamma_in", "gamma_ex", "band", "nplus"]:
         assert np.array_equal(c.copy_set(w), ps.list(w)), (N, w)
+
+
+def test_pks_parity_sequential_coupling(api):
+    # dpm_pks_params.coupling = 1 (c from ρ̄^{i+1}; the Table 4 probe) against the oracle's same variant
+    cfg = get_config("cfg2")
+    o = pks.PKSOracle(cfg, dt_rule=0, coupling=1)
+    c = api.DPM.from_config(cfg)
+    rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+    cc = torch.zeros_like(rho)
+    c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    logs = c.pks_step(rho, cc, cfg.steps, chi=cfg.chi, dt_cap=cfg.dt, coupling=1)
+    ro, co, ologs = o.run()
+    assert rel(rho.cpu().numpy(), ro) <= 1e-9
+    assert rel(cc.cpu().numpy(), co) <= 1e-9
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]

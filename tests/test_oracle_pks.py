@@ -184,3 +184,15 @@ def test_cell_average_initial_state():
     assert np.array_equal(c, o.initial_state()[1])
     # averaging a peaked Gaussian lowers the maximum
     assert rho[inner].max() < rho_pt[inner].max()
+
+
+def test_sequential_coupling_variant():
+    # coupling = 1 changes only the c equation's ρ̄ (ρ̄^{i+1} instead of ρ̄^i): after one step ρ is
+    # identical and c differs by dt (ρ̄^{i+1} - ρ̄^i) through the c solve
+    cfg = get_config("cfg2")
+    a, b = pks.PKSOracle(cfg, dt_rule=1), pks.PKSOracle(cfg, dt_rule=1, coupling=1)
+    r0, c0 = a.initial_state()
+    ra, ca, _ = a.step(r0, c0)
+    rb, cb, _ = b.step(r0, c0)
+    assert np.array_equal(ra, rb)
+    assert 0 < np.abs(ca - cb).max() < 1e-2 * np.abs(ca).max()
