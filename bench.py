@@ -304,6 +304,19 @@ def bench_test_b(N=127, harmonics=150):
     return res
 
 
+def bench_test_a():
+    """NEXT-2: the paper's Test A convergence of the max density (Table 3)
+    on the paper's meshes N = 36/68/132/260 against its N = 516 reference run, ρ̄0 as cell averages (R36):
+    E_rel and rates next to the paper's."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+    import test_a
+    test_a.IC_CELL = True
+    res = test_a.run((36, 68, 132, 260, 516))
+    return {"reference": res["reference"], "ic": res["ic"],
+            "rows": [{k: r.get(k) for k in ("N", "E_rel", "paper_E_rel", "rate", "wall_s")} for r in res["rows"]],
+            "reference_wall_s": res["reference_run"]["wall_s"]}
+
+
 def bench_dd(api, torch, world, rank, steps=None, reps=5):
     """cfg5: the 8-octant DD (R24) — octants sharded over the ranks (8/world each), the global
     least squares and dt through NCCL all-reduces (DDSolver).  The 50-step loop is repeated `reps`
@@ -528,6 +541,7 @@ def main():
         line["cfg1"] = bench_cfg1(api, torch)
         line["bep_rebuild_cfg4"] = bench_bep(api, torch)
         line["test_b"] = bench_test_b()
+        line["test_a"] = bench_test_a()
 
     if not args.no_dd and 8 % world == 0:
         try:
