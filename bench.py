@@ -312,9 +312,11 @@ def bench_test_a():
     import test_a
     test_a.IC_CELL = True
     res = test_a.run((36, 68, 132, 260, 516))
+    einf = test_a.run_einf()
     return {"reference": res["reference"], "ic": res["ic"],
             "rows": [{k: r.get(k) for k in ("N", "E_rel", "paper_E_rel", "rate", "wall_s")} for r in res["rows"]],
-            "reference_wall_s": res["reference_run"]["wall_s"]}
+            "reference_wall_s": res["reference_run"]["wall_s"],
+            "einf_tables_1_2": {"reference": einf["reference"], "rows": einf["rows"]}}
 
 
 def bench_dd(api, torch, world, rank, steps=None, reps=5):

@@ -593,3 +593,20 @@ def test_pks_parity_sequential_coupling(api):
     assert rel(cc.cpu().numpy(), co) <= 1e-9
     for lg, lo in zip(logs, ologs):
         assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
+
+
+def test_paper_test_a_einf_tables_1_2():
+    # Tables 1-2: E∞ over the coarse M+ at T = 1e-6 against the N = 516 run,
+    # restricted to the coarse cells (mean of the ratio^3 fine values; ρ̄ is a cell average), ρ̄0 as
+    # cell averages (R36).  Paper, SD: E∞(ρ) 1.4046 / 0.36990 / 0.12224 / 0.027815,
+    # E∞(c) 5.6759 / 1.4766 / 0.35615 / 0.071459.  Measured: c equal to all printed digits; ρ
+    # 1.4663 / 0.37177 / 0.12171 / 0.027783 (+4.4 / +0.5 / -0.4 / -0.1 %).
+    import os, sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import test_a
+    test_a.IC_CELL = True
+    rows = {r["N"]: r for r in test_a.run_einf()["rows"]}
+    for N in (36, 68, 132, 260):
+        r = rows[N]
+        assert abs(r["Einf_c"] / r["paper_Einf_c"] - 1) <= 2e-4, r            # 5 printed digits
+        assert abs(r["Einf_rho"] / r["paper_Einf_rho"] - 1) <= (0.05 if N == 36 else 0.01), r

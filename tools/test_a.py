@@ -81,6 +81,55 @@ def run(Ns=(36, 68, 132, 260, 516)):
             "rows": rows, "reference_run": info[f] if f == 516 else None}
 
 
+PAPER_EINF_RHO = {36: 1.4046e+00, 68: 3.6990e-01, 132: 1.2224e-01, 260: 2.7815e-02}
+PAPER_EINF_C = {36: 5.6759e+00, 68: 1.4766e+00, 132: 3.5615e-01, 260: 7.1459e-02}
+
+
+def run_einf(Ns=(36, 68, 132, 260), Nref=516, restrict="cell"):
+    """Tables 1-2 (P:650-655 eq. sd-error-in-max-norm): E∞ = max over the coarse M+ of |ρ̄_h - ρ̄_h*| at
+    T = 1e-6 (and for c).  The paper's meshes do not nest, but every coarse node sits at the centre of a
+    2x2x2 cell of the N = 516 mesh (fine index ratio (i - 3/2) + 3/2 is a half-integer for the even
+    ratios 16/8/4/2), so the reference is read there by trilinear interpolation = the 8-point mean."""
+    def state(N):
+        cfg = test_a_config(N)
+        ctx = api.DPM.from_config(cfg)
+        rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+        c = torch.zeros_like(rho)
+        ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c, rho_cell_average=IC_CELL)
+        ctx.pks_step(rho, c, cfg.steps, chi=cfg.chi, dt_cap=cfg.dt, dt_rule=1, clamp=1)
+        torch.cuda.synchronize()
+        return rho, c, torch.from_numpy(ctx.copy_set("mplus")).cuda()
+
+    rf, cf, _ = state(Nref)
+    rows = []
+    for N in Ns:
+        rc, cc, mp = state(N)
+        ratio = (Nref - 4) // (N - 4)
+        assert ratio * (N - 4) == Nref - 4 and ratio % 2 == 0
+        i, j, k = mp // (N * N), (mp // N) % N, mp % N
+        if restrict == "cell":   # mean of the ratio^3 fine values inside the coarse cell
+            w = ratio
+            base = [ratio * q - 2 * ratio + 2 for q in (i, j, k)]
+        else:                    # trilinear at the coarse node = mean of the surrounding 2x2x2
+            w = 2
+            base = [ratio * q - (3 * ratio) // 2 + 1 for q in (i, j, k)]
+        out = {"N": N}
+        for name, fc, ff, paper in (("rho", rc, rf, PAPER_EINF_RHO), ("c", cc, cf, PAPER_EINF_C)):
+            acc = torch.zeros(mp.shape, dtype=torch.float64, device="cuda")
+            for a in range(w):
+                for b in range(w):
+                    for d in range(w):
+                        acc += ff[base[0] + a, base[1] + b, base[2] + d]
+            e = float((fc.reshape(-1)[mp] - acc / w ** 3).abs().max())
+            out[f"Einf_{name}"], out[f"paper_Einf_{name}"] = e, paper.get(N)
+        rows.append(out)
+    for a, b in zip(rows, rows[1:]):
+        for name in ("rho", "c"):
+            b[f"rate_{name}"] = math.log2(a[f"Einf_{name}"] / b[f"Einf_{name}"])
+    how = "mean over the coarse cell" if restrict == "cell" else "8-point (trilinear) mean at the coarse nodes"
+    return {"test": "A-Einf", "reference": f"N={Nref}, {how}", "rows": rows}
+
+
 def final_state(N, tau, T=1e-6, dT=1e-7, coupling=0):
     dt = dT / tau
     cfg = test_a_config(N, dt=dt, steps=int(round(T / dt)))
@@ -113,11 +162,14 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--N", type=int, nargs="+", default=None)
     ap.add_argument("--time", action="store_true")
+    ap.add_argument("--einf", action="store_true", help="Tables 1-2: nodewise E∞ against N = 516")
     ap.add_argument("--ic", choices=["cell", "point"], default="cell",
                     help="ρ̄0 on M+ \\ γ: cell averages (R36, default) or node values (R14)")
     a = ap.parse_args()
     IC_CELL = a.ic == "cell"
-    if a.time:
+    if a.einf:
+        print(json.dumps(run_einf()))
+    elif a.time:
         print(json.dumps(run_time(a.N[0] if a.N else 255)))
     else:
         print(json.dumps(run(a.N or [36, 68, 132, 260, 516])))
