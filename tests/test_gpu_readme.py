@@ -16,3 +16,6 @@ def test_readme_example_runs():
     assert ns["u"].shape == (4, 128, 128, 128)
     assert ns["coef"].shape == (4, ns["ctx"].K)
     assert len(ns["logs"]) == 10 and all(l["mass"] > 0 for l in ns["logs"])
+    assert ns["diag"]["free_energy"] < 0 or ns["diag"]["free_energy"] > 0   # finite
+    assert len(ns["ta_logs"]) == 100 and abs(ns["ta_logs"][-1]["t"] - 1e-6) < 1e-18
+    assert abs(ns["ta_logs"][-1]["rho_max_mplus"] - 1126.89) < 0.05   # ||ρ̄||∞ at T on N = 68, cell-average IC
