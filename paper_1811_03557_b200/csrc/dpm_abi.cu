@@ -364,7 +364,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   }
   // Step 4a: flux + IMEX right-hand sides, particular solutions
   // (the flux kernel also writes the step's rollback copy of rho, c into `backup` when non-null)
-  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup));
+  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup, slot + 4));
   if (prm->coupling == 1) {   // sequential: the whole ρ step, then the c step from ρ̄^{i+1}
     const int K = ctx->K;
     for (int r = 0; r < 2; ++r) {
@@ -377,7 +377,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
       DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fr, ug + r * ng, wr, 1, s));
       DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wr, wr, 1, nullptr, 0, s));
     }
-    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s));
+    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
     return DPM_OK;
   }
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
@@ -387,7 +387,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
-  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s));
+  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
   return DPM_OK;
 }
 

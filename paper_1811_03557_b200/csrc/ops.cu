@@ -154,13 +154,15 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) cfl_kernel(const double* __r
 // fq_rho = (rho - dt g)/dt, fq_c = ((1-dt) c + dt rho)/dt on M+, 0 elsewhere.
 __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
                                 const uint8_t* __restrict__ flags, int n, double h, double dt, double chi,
-                                double* __restrict__ fq_rho, double* __restrict__ fq_c, double* __restrict__ backup) {
+                                double* __restrict__ fq_rho, double* __restrict__ fq_c, double* __restrict__ backup,
+                                double* __restrict__ zero6) {
   // Per axis the stencil's values (ρ and flags at offsets -2..2, c at ±1) are loaded up front with
   // predicated loads (0 outside the box, like valat), then the N+ tests (interior flag; a face ghost is
   // in N+ iff its unique interior neighbour is in M+, R5; anything further out is not), the minmod
   // slopes and the upwind choice are evaluated from registers, without dependent load chains.
   const long nn = (long)n * n * n;
   const double ih = 1.0 / h, idt = 1.0 / dt;
+  if (zero6 && blockIdx.x == 0 && threadIdx.x < 6) zero6[threadIdx.x] = 0.0;   // this step's statistics slot
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     if (backup) {   // the step's rollback copy of the state (speculative PKS graphs), fused with the read
       backup[p] = rho[p];
@@ -485,10 +487,10 @@ cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaS
 }
 
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi, double* fq_rho,
-                            double* fq_c, cudaStream_t s, double* backup) {
+                            double* fq_c, cudaStream_t s, double* backup, double* zero6) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   DPM_COUNT_LAUNCH(1);
-  flux_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(rho, c, ctx->flags, ctx->n, ctx->h, dt, chi, fq_rho, fq_c, backup);
+  flux_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(rho, c, ctx->flags, ctx->n, ctx->h, dt, chi, fq_rho, fq_c, backup, zero6);
   return cudaGetLastError();
 }
 
@@ -541,10 +543,12 @@ cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c,
 }
 
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, bool zeroed) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
-  cudaError_t e = cudaMemsetAsync(stats, 0, 6 * sizeof(double), s);
-  if (e != cudaSuccess) return e;
+  if (!zeroed) {   // (zeroed: an earlier kernel of the step cleared the 6 slots)
+    cudaError_t e = cudaMemsetAsync(stats, 0, 6 * sizeof(double), s);
+    if (e != cudaSuccess) return e;
+  }
   DPM_COUNT_LAUNCH(1);
   restrict_kernel<<<grid_reduce(nn), TB, 0, s>>>(ctx->flags, ctx->n, u, rho, c, stats);
   return cudaGetLastError();
