@@ -359,12 +359,11 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   double* gvec = wk + 2 * field;          // |gamma_in| x 2
   double* ug = gvec + 2 * ngin;           // |gamma| x 2
   double* coef = ug + 2 * ng;             // K x 2
-  if (prm->dt_rule == 0) {   // Step 3 on the device: did the speculative dt stay valid?
-    DPM_CUDA_TRY(ctx, launch_cfl_dt(ctx, c, slot, prm->chi, dt, prm->dt_cap, slot + 3, s));
-  }
-  // Step 4a: flux + IMEX right-hand sides, particular solutions
-  // (the flux kernel also writes the step's rollback copy of rho, c into `backup` when non-null)
-  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup, slot + 4));
+  // Step 3 on the device (did the speculative dt stay valid? slot[3] <- the rule's dt, from the CFL
+  // maxima accumulated in slot[0..2]) and Step 4a (flux + IMEX right-hand sides) in one kernel; it also
+  // writes the step's rollback copy of rho, c into `backup` when non-null and zeroes the statistics slot
+  DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup, slot + 4,
+                                    prm->dt_rule == 0 ? slot : nullptr, dt, prm->dt_cap, slot + 3));
   if (prm->coupling == 1) {   // sequential: the whole ρ step, then the c step from ρ̄^{i+1}
     const int K = ctx->K;
     for (int r = 0; r < 2; ++r) {
@@ -461,6 +460,7 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
   if (!ctx->graph_stream) {
     DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->graph_stream, cudaStreamNonBlocking));
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_log, KMAX * 16 * sizeof(double)));
+    DPM_CUDA_TRY(ctx, cudaMemset(ctx->pks_log, 0, KMAX * 16 * sizeof(double)));   // CFL maxima start at 0
     DPM_CUDA_TRY(ctx, cudaMallocHost(&ctx->pks_log_host, KMAX * 16 * sizeof(double)));
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
   }

@@ -225,7 +225,8 @@ cudaError_t launch_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
 cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaStream_t s);
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi,
                             double* fq_rho, double* fq_c, cudaStream_t s,
-                            double* backup = nullptr, double* zero6 = nullptr);
+                            double* backup = nullptr, double* zero6 = nullptr, double* cfl_out3 = nullptr,
+                            double dt_prev = 0, double cap = 0, double* dt_out = nullptr);
 cudaError_t launch_fc_seq(dpm_ctx* ctx, const double* c, const double* rho_new, double dt, double* fq_c, cudaStream_t s);
 cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
                              cudaStream_t s);
@@ -234,9 +235,6 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
                                   cudaStream_t s,
                                   bool zeroed = false);
 // CFL maxima + the Step-3 dt rule in one kernel (ticket in ctx->red[63], zero at creation)
-cudaError_t launch_cfl_dt(dpm_ctx* ctx, const double* c, double* out3, double chi, double dt_prev, double cap,
-                          double* dt_out, cudaStream_t s);
-
 // bep_fused.cu (sparse-in / gamma-out BEP columns)
 bool bep_fused_enabled(const dpm_ctx* ctx);
 cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double* B, cudaStream_t s);

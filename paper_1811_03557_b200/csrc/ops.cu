@@ -152,10 +152,21 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) cfl_kernel(const double* __r
 
 // g and the IMEX right-hand sides, written scaled for the ABI operator:
 // fq_rho = (rho - dt g)/dt, fq_c = ((1-dt) c + dt rho)/dt on M+, 0 elsewhere.
+// The Step-3 CFL maxima and device dt rule fused into the flux kernel (the same face differences
+// |c_{+1} - c| and |c - c_{-1}| of every M+ point it loads anyway): maxima by per-block atomics into
+// out3, the last block (ticket) evaluates the rule into dt_out and re-zeroes out3 for the next use
+// (the slot is zero from allocation), so a step needs neither a memset nor a separate CFL kernel.
+struct CflFuse {
+  double* out3 = nullptr;   // null: no CFL (fixed dt)
+  unsigned* ticket = nullptr;
+  double chi = 0, dt_prev = 0, cap = 0;
+  double* dt_out = nullptr;
+};
+
 __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
                                 const uint8_t* __restrict__ flags, int n, double h, double dt, double chi,
                                 double* __restrict__ fq_rho, double* __restrict__ fq_c, double* __restrict__ backup,
-                                double* __restrict__ zero6) {
+                                double* __restrict__ zero6, CflFuse cf) {
   // Per axis the stencil's values (ρ and flags at offsets -2..2, c at ±1) are loaded up front with
   // predicated loads (0 outside the box, like valat), then the N+ tests (interior flag; a face ghost is
   // in N+ iff its unique interior neighbour is in M+, R5; anything further out is not), the minmod
@@ -163,6 +174,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
   const long nn = (long)n * n * n;
   const double ih = 1.0 / h, idt = 1.0 / dt;
   if (zero6 && blockIdx.x == 0 && threadIdx.x < 6) zero6[threadIdx.x] = 0.0;   // this step's statistics slot
+  double cmx[3] = {0.0, 0.0, 0.0};
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     if (backup) {   // the step's rollback copy of the state (speculative PKS graphs), fused with the read
       backup[p] = rho[p];
@@ -179,6 +191,12 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
     double g = 0.0;
 #pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
+      if (cf.out3) {   // (cE, cW below: c at ±1 along the axis, 0 outside the box, as valat)
+        const long st0 = ax == 0 ? (long)n * n : (ax == 1 ? (long)n : 1L);
+        const int cd0 = ax == 0 ? i : (ax == 1 ? j : k);
+        const double e = cd0 + 1 < n ? c[p + st0] : 0.0, w = cd0 >= 1 ? c[p - st0] : 0.0;
+        cmx[ax] = fmax(cmx[ax], fmax(fabs(e - c0), fabs(c0 - w)));
+      }
       const int cd = ax == 0 ? i : (ax == 1 ? j : k);
       const long st = ax == 0 ? (long)n * n : (ax == 1 ? (long)n : 1L);
       double R[5];
@@ -213,6 +231,37 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
     }
     fq_rho[p] = (r0 - dt * g) * idt;
     fq_c[p] = ((1.0 - dt) * c0 + dt * r0) * idt;
+  }
+  if (!cf.out3) return;   // (uniform across the grid)
+  __shared__ double red[3][TB / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int a = 0; a < 3; ++a) {
+    double v = cmx[a];
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[a][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int q = 0; q < TB / 32; ++q) v = fmax(v, red[threadIdx.x][q]);
+    umax_atomic(cf.out3 + threadIdx.x, v);
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(cf.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    volatile double* r3 = cf.out3;
+    double cfl = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+      const double m = r3[a] / h;
+      if (m > 0) cfl = fmin(cfl, h / (6.0 * cf.chi * m));
+      r3[a] = 0.0;   // ready for the slot's next use
+    }
+    *cf.dt_out = fmin(fmin(cf.dt_prev, cf.cap), fmin(cfl, 0.5 * h * h));
+    *cf.ticket = 0u;
   }
 }
 
@@ -368,57 +417,6 @@ __global__ void pks_init_kernel(const uint8_t* __restrict__ flags, const int32_t
   }
 }
 
-// CFL maxima (as cfl_kernel) fused with the Step-3 dt rule on the device (R13, the host rule's
-// arithmetic: cfl = min_a h / (6 χ max|Δc|_a / h), dt = min(min(dt_prev, cap), min(cfl, h^2/2))): the
-// last block to finish (threadfence + ticket) evaluates the rule from the reduced maxima and resets
-// the ticket.
-__global__ void __launch_bounds__(TB, STENCIL_MINB) cfl_dt_kernel(const double* __restrict__ c,
-                                                                  const uint8_t* __restrict__ flags, int n,
-                                                                  double* out3, unsigned* ticket, double h, double chi,
-                                                                  double dt_prev, double cap, double* dt_out) {
-  __shared__ double red[3][TB / 32];
-  __shared__ bool last;
-  double mx[3] = {0, 0, 0};
-  const long nn = (long)n * n * n;
-  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
-    if (!(flags[p] & F_MPLUS)) continue;
-    int i, j, k;
-    ijk(p, n, i, j, k);
-    const double c0 = c[p];
-    mx[0] = fmax(mx[0], fmax(fabs(valat(c, n, i + 1, j, k) - c0), fabs(c0 - valat(c, n, i - 1, j, k))));
-    mx[1] = fmax(mx[1], fmax(fabs(valat(c, n, i, j + 1, k) - c0), fabs(c0 - valat(c, n, i, j - 1, k))));
-    mx[2] = fmax(mx[2], fmax(fabs(valat(c, n, i, j, k + 1) - c0), fabs(c0 - valat(c, n, i, j, k - 1))));
-  }
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int a = 0; a < 3; ++a) {
-    double v = mx[a];
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) red[a][w] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < 3) {
-    double v = 0;
-    for (int q = 0; q < TB / 32; ++q) v = fmax(v, red[threadIdx.x][q]);
-    umax_atomic(out3 + threadIdx.x, v);
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    const volatile double* r3 = out3;
-    double cfl = INFINITY;
-    for (int a = 0; a < 3; ++a) {
-      const double m = r3[a] / h;
-      if (m > 0) cfl = fmin(cfl, h / (6.0 * chi * m));
-    }
-    *dt_out = fmin(fmin(dt_prev, cap), fmin(cfl, 0.5 * h * h));
-    *ticket = 0u;
-  }
-}
-
-
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
 // kernels ending in per-block atomics on a few addresses (CFL maxima, step statistics): 4 blocks per SM
 int grid_reduce(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 4)); }
@@ -487,10 +485,20 @@ cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaS
 }
 
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi, double* fq_rho,
-                            double* fq_c, cudaStream_t s, double* backup, double* zero6) {
+                            double* fq_c, cudaStream_t s, double* backup, double* zero6, double* cfl_out3,
+                            double dt_prev, double cap, double* dt_out) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
+  CflFuse cf;
+  if (cfl_out3) {
+    cf.out3 = cfl_out3;
+    cf.ticket = reinterpret_cast<unsigned*>(ctx->red + 63);
+    cf.chi = chi;
+    cf.dt_prev = dt_prev;
+    cf.cap = cap;
+    cf.dt_out = dt_out;
+  }
   DPM_COUNT_LAUNCH(1);
-  flux_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(rho, c, ctx->flags, ctx->n, ctx->h, dt, chi, fq_rho, fq_c, backup, zero6);
+  flux_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(rho, c, ctx->flags, ctx->n, ctx->h, dt, chi, fq_rho, fq_c, backup, zero6, cf);
   return cudaGetLastError();
 }
 
@@ -520,16 +528,6 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
   return cudaGetLastError();
 }
 
-cudaError_t launch_cfl_dt(dpm_ctx* ctx, const double* c, double* out3, double chi, double dt_prev, double cap,
-                          double* dt_out, cudaStream_t s) {
-  const long nn = (long)ctx->n * ctx->n * ctx->n;
-  cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(double), s);
-  if (e != cudaSuccess) return e;
-  DPM_COUNT_LAUNCH(1);
-  cfl_dt_kernel<<<grid_reduce(nn), TB, 0, s>>>(c, ctx->flags, ctx->n, out3, reinterpret_cast<unsigned*>(ctx->red + 63),
-                                               ctx->h, chi, dt_prev, cap, dt_out);
-  return cudaGetLastError();
-}
 
 
 cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s) {
