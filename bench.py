@@ -6,8 +6,9 @@ PKS time steps/sec".  The headline `value` is config 4: batched N=128 fp64 auxil
 solves (I/dt - Δ_h)u = q, dt = 1e-5, 578 RHS of seeded U(-1,1) values on the spherical
 shell band around r = 1 (R21), scattered into dense boxes; inputs resident in HBM.
 One "step" = one dpm_aux_solve_batch call over this rank's shard of the 578 RHS
-(sharded by RHS across ranks, no data-path collective: "scaling": "weak" in the sense
-that ranks solve disjoint shards of the fixed 578-RHS workload — see DESIGN.md).
+(sharded by RHS across ranks, no data-path collective; the 578-RHS workload is fixed as N grows, so
+"scaling": "strong" — see DESIGN.md §8).  With --gpus N > 1 and no WORLD_SIZE in the environment,
+bench.py re-executes itself under torch.distributed.run with N ranks.
 PKS steps/s for configs 2 and 3 are reported in the "pks" object (rank 0, N=1 only).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -31,6 +32,9 @@ from dpm_inputs import get_config  # noqa: E402
 from dpm_inputs.rng import cfg4_band_values  # noqa: E402
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction); PKS time steps/sec"   # BASELINE.json
+WORKLOAD = ("cfg4: N=128 box [-1.1,1.1]^3, dt=1e-5, 578 RHS U(-1,1) on the r=1 shell band (R21), dense boxes "
+            "in/out")
 FP64_PEAK_TFLOPS = 37.0      # measured DFMA / DMMA.8x8x4 peak on this pool's B200 (profiles/r01/microbench_*.log)
 
 
@@ -144,6 +148,15 @@ def oracle_sample_rate(cfg, nsolves, vals, band):
     return nsolves / dt, dt
 
 
+def oracle_baseline(cfg, vals, band, per_rep=20, reps=5):
+    """cpu_baseline (tier contract): the oracle as it stands on the host cores, one warm-up
+    solve, then the median of `reps` repetitions of `per_rep` solves of the cfg4 RHS (a bounded sample)."""
+    oracle_sample_rate(cfg, 1, vals, band)
+    runs = [oracle_sample_rate(cfg, per_rep, vals, band) for _ in range(reps)]
+    rates = sorted(r for r, _ in runs)
+    return statistics.median(rates), sum(t for _, t in runs), per_rep, reps
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -151,8 +164,15 @@ def host_cores():
         return os.cpu_count()
 
 
+def workload_config(B, nb, n, world, field):
+    return {"workload": WORKLOAD, "global_batch": B, "local_batch": nb, "n": n, "parallelism": f"rhs-shard x{world}",
+            "l2": "inputs larger than L2 (%.1f GB per rank per step)" % (nb * field * 8 / 1e9)}
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only)."""
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0 only; other ranks exit 0).
+    Same metric, unit, config and higher_is_better as our arm; each step solves a bounded sample of 2 of
+    the 578 cfg4 RHS (direct-summation DST)."""
     if rank != 0:
         return
     cfg = get_config("cfg4")
@@ -161,21 +181,25 @@ def run_reference(args, world, rank):
     band = ps.list("band")
     vals = cfg4_band_values(cfg.batch, len(band))
     per_step = 2
-    for _ in range(args.warmup):
-        oracle_sample_rate(cfg, 1, vals, band)
-    times = []
-    for _ in range(args.steps):
-        _, t = oracle_sample_rate(cfg, per_step, vals, band)
-        times.append(t)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=host_cores()):   # torchrun exports OMP_NUM_THREADS=1 to every rank
+        for _ in range(args.warmup):
+            oracle_sample_rate(cfg, 1, vals, band)
+        times = []
+        for _ in range(args.steps):
+            _, t = oracle_sample_rate(cfg, per_step, vals, band)
+            times.append(t)
     tot = sum(times)
     value = per_step * args.steps / tot
-    line = {"impl": "reference", "metric": "fp64 auxiliary solves/sec at N=128", "value": value, "unit": "solves/s",
+    n, B = cfg.n, cfg.batch
+    per = -(-B // world)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg4: N=128 box [-1.1,1.1]^3, dt=1e-5, 578 RHS U(-1,1) on the r=1 shell band",
-                       "global_batch": cfg.batch, "n": cfg.n, "parallelism": "rhs-shard"},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(B, per, n, world, n ** 3),
             "cpu_baseline": {"value": value, "unit": "solves/s", "cores": host_cores(), "kind": "oracle",
-                             "sample": f"{per_step} of the 578 cfg4 RHS per step (direct-summation DST, numpy)"},
+                             "sample": f"{per_step} of the 578 cfg4 RHS per step (direct-summation DST, numpy)",
+                             "model": cpu_model()},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -294,6 +318,28 @@ def bench_bep(api, torch, reps=3):
     return res
 
 
+def bench_bep_distributed(ctx, torch, dist, world, rank, reps=3):
+    """C1 at N > 1: parallel.build_projection_distributed (columns sharded over ranks, NCCL all-gather of
+    B, local CholeskyQR2) at the cfg4 geometry; median of reps of the max over ranks."""
+    from paper_1811_03557_b200 import parallel
+    parallel.build_projection_distributed(ctx, world, rank)
+    ts = []
+    for _ in range(reps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        parallel.build_projection_distributed(ctx, world, rank)
+        e1.record()
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ts.append(float(t.item()))
+    c0, c1 = parallel.shard_range(ctx.K, world, rank)
+    return {"K": ctx.K, "ranks": world, "columns_per_rank": c1 - c0, "build_ms": statistics.median(ts),
+            "collective": "all_gather of the |gamma_in| x K reduced BEP (NCCL)"}
+
+
 def bench_test_b(N=127, harmonics=150):
     """NEXT-4: the paper's Test B single domain, the
     Step-4b-every-step regime near blow-up: PKS steps until Δ||ρ||∞ >= 1000; blow-up time
@@ -361,6 +407,29 @@ def bench_dd(api, torch, world, rank, steps=None, reps=5):
     return out
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_cmd(n, argv, port):
+    """The torchrun command bench.py re-executes itself under for --gpus N > 1 without WORLD_SIZE."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def spawn_ranks(n):
+    """One process per GPU over NCCL (rank 0 prints the JSON line); NCCL's init lines go to stderr so the
+    ranks can be counted."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    r = subprocess.run(spawn_cmd(n, sys.argv[1:], free_port()), env=env)
+    sys.exit(r.returncode)
+
+
 def main():
     ap_ = argparse.ArgumentParser()
     ap_.add_argument("--gpus", type=int, default=1)
@@ -372,7 +441,11 @@ def main():
     ap_.add_argument("--no-pks", action="store_true")
     ap_.add_argument("--no-dd", action="store_true")
     args = ap_.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     world, rank, local = dist_setup()
+    if "WORLD_SIZE" in os.environ and world != args.gpus and rank == 0:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)\n")
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
@@ -471,14 +544,11 @@ def main():
                          else "dst128f_kernel<1> (prime-factor DST-I along y, DFMA)",
                     "z": "ztri_warp_kernel<128> (exact tridiagonal solve along z)"}
 
-    line = {"metric": "fp64 auxiliary solves/sec at N=128 (HBM-roofline fraction); PKS time steps/sec",
+    line = {"metric": METRIC,
             "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg4: N=128 box [-1.1,1.1]^3, dt=1e-5, 578 RHS U(-1,1) on the r=1 shell band "
-                                   "(R21), dense boxes in/out",
-                       "global_batch": B, "local_batch": nb, "n": n, "parallelism": f"rhs-shard x{world}",
-                       "l2": "inputs larger than L2 (%.1f GB per rank per step)" % (nb * field * 8 / 1e9)},
+            "config": workload_config(B, nb, n, world, field),
             "roofline": {"bound": "hbm", "kernel": kernel_names.get(kind, kind), "achieved": k_gbs, "peak": hbm_peak,
                          "unit": "GB/s", "frac": k_gbs / hbm_peak, "traffic": traffic,
                          "peak_kind": peaks_kind + " (MEASURED_PEAKS.json hbm_gbs, burst copy)",
@@ -519,9 +589,10 @@ def main():
         from oracle import grid
         _, ps = grid.point_sets_for(cfg)
         band = ps.list("band")
-        rate, secs = oracle_sample_rate(cfg, 3, vals[:3], band)
+        rate, secs, per_rep, reps = oracle_baseline(cfg, vals[:20], band)
         line["cpu_baseline"] = {"value": rate, "unit": "solves/s", "cores": host_cores(), "kind": "oracle",
-                                "sample": "3 of the 578 cfg4 RHS (direct-summation DST, numpy BLAS), %.1f s" % secs,
+                                "sample": "median of %d repetitions of %d of the 578 cfg4 RHS after 1 warm-up solve "
+                                          "(direct-summation DST, numpy BLAS), %.1f s" % (reps, per_rep, secs),
                                 "model": cpu_model()}
         try:   # the same oracle on one BLAS thread, and a scipy.fft fast-Poisson reference
             from threadpoolctl import threadpool_limits
@@ -544,6 +615,16 @@ def main():
         line["bep_rebuild_cfg4"] = bench_bep(api, torch)
         line["test_b"] = bench_test_b()
         line["test_a"] = bench_test_a()
+
+    if world > 1:
+        # C1: one BEP build of the cfg4 geometry with its K = 578 columns sharded over the
+        # ranks, one all-gather of B, redundant factorisation on every rank; CUDA events, max over ranks
+        try:
+            del q, u
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        line["bep_build_distributed_cfg4"] = bench_bep_distributed(ctx, torch, dist, world, rank)
 
     if not args.no_dd and 8 % world == 0:
         try:

@@ -84,13 +84,18 @@ typedef struct {
   int32_t have_projection;   /* 1 once dpm_build_projection succeeded at the current dt    */
   double bep_cond_est;       /* κ(R) of the column-equilibrated BEP (diag ratio estimate)  */
   int32_t solver;            /* dpm_solver in use                                          */
+  int64_t n_exact_ties;      /* nodes within 1e-11 of the boundary in fp64, decided in exact integer
+                                arithmetic on the host (R6: the constants read as their shortest
+                                round-trip decimals; ties -> M-)                                  */
+  int64_t n_exact_ties_inside; /* of those, the nodes placed in M+                                */
 } dpm_info;
 
 typedef struct dpm_ctx dpm_ctx;
 
 /* ---------------------------------------------------------------------------------
  * Setup (P:40-60 auxiliary cube + Def. 1; P:263-299 extension data).
- * Builds the point sets on the device (fp64 classification; ties -> M-, R6), the
+ * Builds the point sets on the device (exact classification, ties -> M-, R6: an fp64 test decides
+ * every node farther than 1e-11 from the boundary, the rest are decided exactly on the host), the
  * gamma geometry (foot point, signed distance d, SH angles; R10) and E (|gamma| x K).
  * 4 <= n <= DPM_MAX_N; basis one of dpm_basis; 0 <= lmax <= 40 for the full-SH sets,
  * <= DPM_MAX_ZONAL_L for the zonal ones (DPM_ERR_INVALID otherwise).  The paper's mesh
@@ -218,11 +223,17 @@ dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* 
    `stream`.  Single-domain contexts (DPM_ERR_INVALID for octants). */
 dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out, void* stream);
 
-/* Advance nsteps steps in place. Each step: CFL (device reduction) -> dt (host decides,
-   stream synchronized once per step) -> [Step 4b rebuild when dt decreased] -> flux +
-   IMEX RHS -> 2 particular AP solves -> Tr_gamma_in -> LSQ -> u_gamma = E C,
-   clamp -> combined Green's-formula RHS (R20) -> 2 AP solves -> restrict to N+.
-   log (HOST, nullable) receives nsteps entries. DPM_ERR_NONFINITE on NaN/Inf. */
+/* Advance nsteps steps in place (Steps 3-7).  Each step: flux + IMEX RHS ->
+   2 particular AP solves -> Tr_gamma_in -> LSQ -> u_gamma = E C, clamp (R17) -> combined Green's-formula
+   RHS (R20) -> 2 AP solves -> restriction to N+.
+   Step 3 (R13) runs speculatively: up to 10 consecutive steps at dt_i = dt_{i-1} are replayed as one
+   CUDA graph on a ctx-owned stream; every step also evaluates the dt rule on the device from its own
+   input state and saves that state.  The host reads the batch's log once; at the first step whose rule
+   asks for a smaller dt the state is rolled back to that step's saved input, the BEP is rebuilt at the
+   new dt (Step 4b) and stepping resumes.  The accepted dt sequence equals the host rule's.  The
+   first step of a run evaluates the rule on the host.  The caller's `stream` is synchronized on entry
+   and the call returns after the last step (synchronous).  log (HOST, nullable) receives nsteps
+   entries.  DPM_ERR_NONFINITE on NaN/Inf (the state is left right after the failing step). */
 dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, const dpm_pks_params* params,
                         dpm_step_log* log, void* stream);
 

@@ -129,7 +129,8 @@ def piece_assignment(g: grid.Grid, ps: grid.PointSets) -> np.ndarray:
     return assign
 
 
-def setup(n: int, Lc: int, Li: int) -> DDSetup:
+def setup(n: int, Lc: int, Li: int, which=None) -> DDSetup:
+    """All 8 octants (which=None) or only the listed ones (the others are None: memory at n = 128)."""
     g = grid.Grid(n, *BOX)
     ps = grid.point_sets_from_mask(g, grid.octant_inside_mask(g))
     h = g.h
@@ -144,6 +145,9 @@ def setup(n: int, Lc: int, Li: int) -> DDSetup:
     rows = np.array([(q, k) for q in gin_pos for k in range(4) if assign[q, k]], dtype=np.int64).reshape(-1, 2)
     octs = []
     for s, sigma in enumerate(octant_signs()):
+        if which is not None and s not in which:
+            octs.append(None)
+            continue
         E = np.zeros((len(P), K))
         X = sigma * P                                  # physical coordinates
         # cap: foot on the unit sphere, d = |x| - 1 (+ outside), zero Neumann -> {Y, d^2/2 Y}
@@ -171,8 +175,7 @@ def setup(n: int, Lc: int, Li: int) -> DDSetup:
 
 def bep_block(st: DDSetup, o: Octant, dt: float):
     """Rows E_π[p] - (P_γ A)[p] for (p, π) in o.rows, and the potential columns' γ trace."""
-    U = dpm.potential_columns(o.A, o.g, o.ps, dt)      # K AP solves (P:196-207)
-    PgA = dpm.trace(U, o.ps.list("gamma")).T           # |γ| × K
+    PgA = dpm.potential_trace(o.A, o.g, o.ps, dt, o.ps.list("gamma"))   # K AP solves (P:196-207), |γ| × K
     B = np.zeros((len(o.rows), st.K))
     for i, (q, k) in enumerate(o.rows):
         blk = st.blocks[PIECES[k]]
@@ -300,3 +303,108 @@ class DDPKSOracle:
             log["mass"] = self.mass(state)
             logs.append(log)
         return state, logs
+
+
+# ---- config 5 at its configured size through the exact 8-fold reflection symmetry -----------------
+# The octants share the canonical-frame grid, sets, pieces and rows; octant s's extension is octant 0's
+# with column signs, E_s = E_0 diag(S_s) (real SH and Legendre products are even or odd under each
+# reflection x_a -> -x_a, and d = x_a on the planes flips with σ_a), hence A_s = A_0 diag(S_s) and
+# B_s = B_0 diag(S_s).  For an IC symmetric under all 8 reflections (cfg5: centred at the origin) every
+# octant's canonical state is the same, so g_s = g_0 and the stacked least squares
+#     min_C Σ_s || B_0 S_s C - g_0 ||^2
+# is the one of `stacked_lstsq`.  With B_0 = Q R (thin QR) each term is || R S_s C - Q^T g_0 ||^2 plus a
+# constant, so the (8K x K) system [R S_s]_s C = [Q^T g_0]_s has the same minimiser (SURVEY probe P9/P12
+# used the same reduction).  Its column norms are those of the stacked matrix (= sqrt(8) |B_0[:, c]|).
+
+def column_signs(st: DDSetup, sigmas=None) -> np.ndarray:
+    """(8, K) S_s with E_s = E_0 diag(S_s), read off the extension of octant 0's γ points under each σ
+    (asserted to be exactly ±1 on every column)."""
+    o0 = st.octants[0]
+    P = dpm.gamma_points(o0.g, o0.ps)
+    P = P[:: max(1, len(P) // 4000)]        # a few thousand γ points determine every column's sign
+    blocks = st.blocks
+    out = np.ones((8, st.K))
+    r = np.linalg.norm(P, axis=1)
+    def ext(sig):
+        X = sig * P
+        Y = sh.real_sh(st.Lc, X / r[:, None])
+        cols = [Y, 0.5 * ((r - 1.0) ** 2)[:, None] * Y]
+        for a in range(3):
+            o = [b for b in range(3) if b != a]
+            phi = plane_basis(st.Li, X[:, o[0]], X[:, o[1]])
+            cols += [phi, X[:, a][:, None] * phi]
+        return np.concatenate(cols, axis=1)
+    E0 = ext(octant_signs()[0])
+    q = np.argmax(np.abs(E0), axis=0)
+    for s, sig in enumerate(octant_signs()):
+        Es = ext(sig)
+        ratio = Es[q, np.arange(st.K)] / E0[q, np.arange(st.K)]
+        assert np.allclose(np.abs(ratio), 1.0, rtol=1e-12, atol=0), "extension not ±1 under reflection"
+        assert np.allclose(Es, E0 * np.sign(ratio), rtol=0, atol=1e-13 * np.abs(E0).max())
+        out[s] = np.sign(ratio)
+    assert len(blocks) == 4
+    return out
+
+
+def stacked_lstsq_symmetric(B0: np.ndarray, signs: np.ndarray, g0: np.ndarray) -> np.ndarray:
+    """`stacked_lstsq` of the blocks B_0 diag(S_s) with the common right-hand side g_0, through the
+    thin QR of B_0 (see the block comment above); g0 may hold several columns."""
+    Q, R = np.linalg.qr(B0)
+    z = Q.T @ g0
+    Bst = np.concatenate([R * s for s in signs], axis=0)                 # R S_s
+    zst = np.concatenate([z] * len(signs), axis=0)
+    D = 1.0 / np.linalg.norm(Bst, axis=0)
+    y = np.linalg.lstsq(Bst * D, zst, rcond=None)[0]
+    return (D[:, None] * y) if y.ndim > 1 else D * y
+
+
+class DDPKSOracleSymmetric(DDPKSOracle):
+    """DDPKSOracle for an IC symmetric under the 8 reflections, simulating octant 0 only (every octant's
+    canonical state is the same): the global dt is octant 0's rule, the global C the symmetric stacked
+    least squares.  Same steps and readings as DDPKSOracle.step, one octant's arithmetic."""
+
+    def __init__(self, n, Lc, Li, dt_cap, steps, **kw):
+        self.st = setup(n, Lc, Li, which=(0,))
+        self.signs = column_signs(self.st)
+        self.dt_cap, self.steps = dt_cap, steps
+        self.chi = kw.get("chi", 1.0)
+        self.center = kw.get("center", (0.0, 0.0, 0.0))
+        assert all(c == 0.0 for c in self.center), "the reduction needs an origin-centred (symmetric) IC"
+        self.rho_ic, self.c_ic = kw.get("rho_ic", (1000.0, 100.0)), kw.get("c_ic", (500.0, 50.0))
+        self.clamp = kw.get("clamp", True)
+        self.dt_prev, self.dt_bep, self.B0, self.builds, self.t = np.inf, None, None, 0, 0.0
+
+    def initial_state(self):
+        st = self.st
+        full = DDSetup(st.n, st.Lc, st.Li, st.K, st.blocks, [st.octants[0]])
+        return ic_fields(full, self.center, self.rho_ic, self.c_ic)[0]
+
+    def step(self, state):
+        o = self.st.octants[0]
+        h, chi = o.g.h, self.chi
+        rho, c = state
+        dt = min(self.dt_prev, self.dt_cap, pks.cfl_dt(c, o.ps, h, chi), 0.5 * h * h)   # Step 3 + R13
+        rebuilt = False
+        if self.B0 is None or dt != self.dt_bep:                                       # Step 2 / 4b
+            self.B0 = bep_block(self.st, o, dt)[0]
+            self.dt_bep = dt
+            self.builds += 1
+            rebuilt = True
+        gconv = pks.convection(rho, c, o.ps, h, chi)
+        frhs = pks.assemble_rhs(rho, c, gconv, dt)                                      # Step 4a
+        new = []
+        for f in frhs:
+            up = ap.solve(dpm.particular_rhs(f, o.ps, dt), h, dt)
+            g0 = dpm.trace(up, o.ps.list("gamma"))[o.rows[:, 0]]
+            C = stacked_lstsq_symmetric(self.B0, self.signs, g0)                        # Step 5 (global)
+            ug = o.A @ C
+            if self.clamp:
+                ug = np.maximum(ug, 0.0)                                                # R17
+            new.append(dpm.green(ug, f, o.g, o.ps, dt))                                 # Steps 6-7 (R20)
+        self.dt_prev = dt
+        self.t += dt
+        return tuple(new), dict(dt=dt, rebuilt=rebuilt, t=self.t)
+
+    def mass(self, state):
+        o = self.st.octants[0]
+        return 8 * o.g.h ** 3 * state[0][o.ps.mplus].sum()

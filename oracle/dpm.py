@@ -67,10 +67,25 @@ def particular_rhs(f_mplus_box: np.ndarray, ps, dt: float) -> np.ndarray:
     return q
 
 
-def potential_columns(E: np.ndarray, g, ps, dt: float) -> np.ndarray:
-    """u_c = AP solve of potential_rhs(E[:, c]) for every column, shape (K, n, n, n)."""
-    Q = np.stack([potential_rhs(E[:, c], g, ps, dt) for c in range(E.shape[1])])
-    return ap.solve(Q, g.h, dt)
+def potential_columns(E: np.ndarray, g, ps, dt: float, chunk: int = 32) -> np.ndarray:
+    """u_c = AP solve of potential_rhs(E[:, c]) for every column, shape (K, n, n, n).  The columns are
+    independent; they are solved `chunk` at a time only to bound the host memory of the batch."""
+    K = E.shape[1]
+    U = np.empty((K, g.n, g.n, g.n))
+    for c0 in range(0, K, chunk):
+        Q = np.stack([potential_rhs(E[:, c], g, ps, dt) for c in range(c0, min(K, c0 + chunk))])
+        U[c0:c0 + len(Q)] = ap.solve(Q, g.h, dt)
+    return U
+
+
+def potential_trace(E: np.ndarray, g, ps, dt: float, idx: np.ndarray, chunk: int = 16) -> np.ndarray:
+    """Tr_idx of potential_columns(E): (len(idx), K), without holding all K boxes (large n)."""
+    K = E.shape[1]
+    out = np.empty((len(idx), K))
+    for c0 in range(0, K, chunk):
+        c1 = min(K, c0 + chunk)
+        out[:, c0:c1] = trace(potential_columns(E[:, c0:c1], g, ps, dt, 1 if g.n >= 64 else chunk), idx).T
+    return out
 
 
 def trace(U: np.ndarray, idx: np.ndarray) -> np.ndarray:

@@ -42,7 +42,7 @@ class Info(C.Structure):
                 ("n_mplus", C.c_int64), ("n_gamma", C.c_int64), ("n_gamma_in", C.c_int64),
                 ("n_gamma_ex", C.c_int64), ("n_band", C.c_int64), ("n_nplus", C.c_int64),
                 ("ghosts_in_nplus", C.c_int64), ("have_projection", C.c_int32), ("bep_cond_est", C.c_double),
-                ("solver", C.c_int32)]
+                ("solver", C.c_int32), ("n_exact_ties", C.c_int64), ("n_exact_ties_inside", C.c_int64)]
 
 
 class PksIC(C.Structure):

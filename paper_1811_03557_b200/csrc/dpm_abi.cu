@@ -149,6 +149,8 @@ dpm_status dpm_query(const dpm_ctx* ctx, dpm_info* out) {
   out->have_projection = ctx->have_projection;
   out->bep_cond_est = ctx->bep_cond;
   out->solver = ctx->plan.solver;
+  out->n_exact_ties = ctx->exact_ties;
+  out->n_exact_ties_inside = ctx->exact_ties_inside;
   return DPM_OK;
 }
 
@@ -395,7 +397,8 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
                             dpm_ctx::PksGraph** out) {
   for (auto& g : ctx->pks_graphs)
     if (g.dt == dt && g.k == K && g.chi == prm->chi && g.cap == prm->dt_cap && g.rule == prm->dt_rule &&
-        g.clamp == prm->clamp && g.coupling == prm->coupling && g.rho == rho && g.c == c) {
+        g.clamp == prm->clamp && g.coupling == prm->coupling && g.rho == rho && g.c == c &&
+        g.solver == ctx->plan.solver) {
       *out = &g;
       return DPM_OK;
     }
@@ -425,6 +428,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   dpm_ctx::PksGraph g;
   g.dt = dt; g.k = K; g.chi = prm->chi; g.cap = prm->dt_cap; g.rule = prm->dt_rule; g.clamp = prm->clamp;
   g.coupling = prm->coupling;
+  g.solver = ctx->plan.solver;   // dst_solve_batch reads it at capture time
   g.rho = rho; g.c = c; g.launches = nk;
   const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
   cudaGraphDestroy(graph);

@@ -60,6 +60,8 @@ struct dpm_ctx {
   int64_t* lists[6] = {nullptr}; // dpm_set order
   int64_t counts[6] = {0};
   int64_t ghosts_in_nplus = 0;
+  int64_t exact_ties = 0;         // nodes within the fp64 tie band, decided exactly on the host (R6)
+  int64_t exact_ties_inside = 0;  // of those, the ones in M+
   int32_t* gin_pos = nullptr;    // [n_gamma_in] position of gamma_in points inside gamma
 
   // gamma geometry + extension matrix (device)
@@ -94,7 +96,7 @@ struct dpm_ctx {
   static constexpr int PKS_K = 10;
   struct PksGraph {
     double dt = 0, chi = 0, cap = 0;
-    int k = 0, rule = 0, clamp = 0, coupling = 0;
+    int k = 0, rule = 0, clamp = 0, coupling = 0, solver = 0;
     double* rho = nullptr;
     double* c = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -234,7 +236,6 @@ cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c,
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s,
                                   bool zeroed = false);
-// CFL maxima + the Step-3 dt rule in one kernel (ticket in ctx->red[63], zero at creation)
 // bep_fused.cu (sparse-in / gamma-out BEP columns)
 bool bep_fused_enabled(const dpm_ctx* ctx);
 cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double* B, cudaStream_t s);

@@ -3,27 +3,59 @@
 // extension matrix E = [Y | d Y] or [Y | d^2/2 Y] (R9).
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
 #include "dpm_internal.h"
 #include "sh_device.cuh"
 
 namespace {
 
-__device__ __forceinline__ bool inside_domain(const dpm_domain& D, double x, double y, double z) {
-  if (D.kind == DPM_OCTANT_CANON)   // cfg5 subdomain in its canonical frame (R24): open octant ∩ ball
-    return x > 0.0 && y > 0.0 && z > 0.0 && x * x + y * y + z * z < D.semi[0] * D.semi[0];
+// fp64 membership value and a near-tie flag.  The decision is exact (R6) by construction: the fp64
+// test decides every node whose value is farther than 1e-11 (relative) from the boundary, and the
+// host re-decides the flagged rest in exact integer arithmetic (exact_inside below).  The fp64 error
+// of Σ((x - c)/s)^2 is a few ulp, far below the flag band.
+constexpr double TIE_BAND = 1e-11;
+constexpr uint8_t F_TIE = 128;   // transient flag bit: resolved on the host before dilation
+
+__device__ __forceinline__ uint8_t classify_node(const dpm_domain& D, double x, double y, double z, double scale) {
+  if (D.kind == DPM_OCTANT_CANON) {   // cfg5 subdomain in its canonical frame (R24): open octant ∩ ball
+    const double r2 = D.semi[0] * D.semi[0];
+    const double v = x * x + y * y + z * z;
+    const double tb = TIE_BAND * scale;
+    if (fabs(x) <= tb || fabs(y) <= tb || fabs(z) <= tb || fabs(v - r2) <= TIE_BAND * r2) return F_TIE;
+    return (x > 0.0 && y > 0.0 && z > 0.0 && v < r2) ? F_MPLUS : 0;
+  }
   const double a = (x - D.center[0]) / D.semi[0];
   const double b = (y - D.center[1]) / D.semi[1];
   const double c = (z - D.center[2]) / D.semi[2];
-  return a * a + b * b + c * c < 1.0;   // open interior; ties -> M- (R6)
+  const double v = a * a + b * b + c * c;
+  if (fabs(v - 1.0) <= TIE_BAND) return F_TIE;
+  return v < 1.0 ? F_MPLUS : 0;   // open interior; ties -> M- (R6)
 }
 
-__global__ void classify_kernel(uint8_t* flags, int n, double lo, double h, dpm_domain D) {
+__global__ void classify_kernel(uint8_t* flags, int n, double lo, double h, double scale, dpm_domain D,
+                                unsigned long long* nties) {
   const long nn = (long)n * n * n;
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     const int i = (int)(p / ((long)n * n)), j = (int)((p / n) % n), k = (int)(p % n);
     const double x = lo + (i + 1) * h, y = lo + (j + 1) * h, z = lo + (k + 1) * h;
-    flags[p] = inside_domain(D, x, y, z) ? F_MPLUS : 0;
+    const uint8_t f = classify_node(D, x, y, z, scale);
+    flags[p] = f;
+    if (f == F_TIE) atomicAdd(nties, 1ull);
   }
+}
+
+__global__ void tie_list_kernel(const uint8_t* flags, long nn, int64_t* list, unsigned long long* cnt) {
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x)
+    if (flags[p] == F_TIE) list[atomicAdd(cnt, 1ull)] = p;
+}
+
+__global__ void tie_set_kernel(uint8_t* flags, const int64_t* list, const uint8_t* val, long m) {
+  const long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i < m) flags[list[i]] = val[i];
 }
 
 // N± (within M0), gamma; counts ghost nodes of N+ (a face ghost has exactly one interior
@@ -186,6 +218,188 @@ __global__ void geometry_sh_kernel(const int64_t* gamma, int64_t ng, int n, doub
   });
 }
 
+// ---- exact classification of near-tie nodes (R6) -------------------------------------------------
+// The configuration constants are read as decimals, the shortest decimal that round-trips the double
+// (the oracle's Fraction(repr(x)), oracle/grid.py).  With every constant scaled to one power of ten,
+// lo = L 10^e, hi = H 10^e, c_a = C_a 10^e, s_a = S_a 10^e, node i sits at x_i - c_a =
+// X_a(i) 10^e / (n+1) with the integer X_a(i) = L (n+1) + (i+1)(H - L) - C_a (n+1), and
+//   Σ_a ((x_a - c_a)/s_a)^2 < 1   <=>   Σ_a X_a^2 Π_{b≠a} S_b^2 < (n+1)^2 Π_b S_b^2,
+//   octant (c = 0, radius R 10^e): X_a > 0 for all a and Σ_a X_a^2 < (n+1)^2 R^2.
+// Small sign-magnitude big integers (base 2^32) evaluate it for the few flagged nodes.
+struct BigInt {
+  bool neg = false;
+  std::vector<uint32_t> m;   // little-endian magnitude, no leading zero limbs
+  static BigInt from_u64(unsigned long long v, bool neg = false) {
+    BigInt r;
+    while (v) { r.m.push_back((uint32_t)v); v >>= 32; }
+    r.neg = neg && !r.m.empty();
+    return r;
+  }
+  bool zero() const { return m.empty(); }
+};
+
+int cmp_mag(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+  if (a.size() != b.size()) return a.size() < b.size() ? -1 : 1;
+  for (size_t i = a.size(); i-- > 0;)
+    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  return 0;
+}
+
+std::vector<uint32_t> add_mag(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {
+  std::vector<uint32_t> r(std::max(a.size(), b.size()) + 1, 0);
+  unsigned long long carry = 0;
+  for (size_t i = 0; i + 1 < r.size(); ++i) {
+    const unsigned long long s = carry + (i < a.size() ? a[i] : 0) + (i < b.size() ? b[i] : 0);
+    r[i] = (uint32_t)s;
+    carry = s >> 32;
+  }
+  r.back() = (uint32_t)carry;
+  while (!r.empty() && r.back() == 0) r.pop_back();
+  return r;
+}
+
+std::vector<uint32_t> sub_mag(const std::vector<uint32_t>& a, const std::vector<uint32_t>& b) {   // |a| >= |b|
+  std::vector<uint32_t> r(a.size(), 0);
+  long long borrow = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    long long d = (long long)a[i] - (i < b.size() ? b[i] : 0) - borrow;
+    borrow = d < 0;
+    if (d < 0) d += (1ll << 32);
+    r[i] = (uint32_t)d;
+  }
+  while (!r.empty() && r.back() == 0) r.pop_back();
+  return r;
+}
+
+BigInt add(const BigInt& a, const BigInt& b) {
+  BigInt r;
+  if (a.neg == b.neg) {
+    r.m = add_mag(a.m, b.m);
+    r.neg = a.neg;
+  } else if (cmp_mag(a.m, b.m) >= 0) {
+    r.m = sub_mag(a.m, b.m);
+    r.neg = a.neg;
+  } else {
+    r.m = sub_mag(b.m, a.m);
+    r.neg = b.neg;
+  }
+  if (r.m.empty()) r.neg = false;
+  return r;
+}
+
+BigInt neg(BigInt a) {
+  if (!a.zero()) a.neg = !a.neg;
+  return a;
+}
+
+BigInt mul(const BigInt& a, const BigInt& b) {
+  BigInt r;
+  if (a.zero() || b.zero()) return r;
+  std::vector<unsigned long long> acc(a.m.size() + b.m.size() + 1, 0);
+  r.m.assign(a.m.size() + b.m.size(), 0);
+  for (size_t i = 0; i < a.m.size(); ++i) {
+    unsigned long long carry = 0;
+    for (size_t j = 0; j < b.m.size(); ++j) {
+      const unsigned long long t = (unsigned long long)a.m[i] * b.m[j] + r.m[i + j] + carry;
+      r.m[i + j] = (uint32_t)t;
+      carry = t >> 32;
+    }
+    size_t k = i + b.m.size();
+    while (carry) {
+      const unsigned long long t = (unsigned long long)r.m[k] + carry;
+      r.m[k++] = (uint32_t)t;
+      carry = t >> 32;
+    }
+  }
+  while (!r.m.empty() && r.m.back() == 0) r.m.pop_back();
+  r.neg = a.neg != b.neg && !r.m.empty();
+  return r;
+}
+
+int cmp(const BigInt& a, const BigInt& b) {   // sign-aware
+  if (a.neg != b.neg) return a.neg ? -1 : 1;
+  const int c = cmp_mag(a.m, b.m);
+  return a.neg ? -c : c;
+}
+
+// x = D 10^e with D an integer: the shortest decimal that round-trips the double (Python's repr).
+struct Decimal {
+  BigInt D;
+  int e = 0;
+};
+
+Decimal to_decimal(double x) {
+  char buf[64];
+  for (int p = 1; p <= 17; ++p) {
+    std::snprintf(buf, sizeof buf, "%.*e", p - 1, x);
+    if (std::strtod(buf, nullptr) == x) break;
+  }
+  Decimal d;
+  const char* c = buf;
+  bool ng = false;
+  if (*c == '-') { ng = true; ++c; }
+  int frac_digits = 0;
+  bool after_point = false;
+  BigInt ten = BigInt::from_u64(10);
+  for (; *c && *c != 'e'; ++c) {
+    if (*c == '.') { after_point = true; continue; }
+    d.D = add(mul(d.D, ten), BigInt::from_u64((unsigned long long)(*c - '0')));
+    if (after_point) ++frac_digits;
+  }
+  const int ex = (*c == 'e') ? std::atoi(c + 1) : 0;
+  d.e = ex - frac_digits;
+  if (ng) d.D = neg(d.D);
+  return d;
+}
+
+BigInt scaled(const Decimal& d, int e) {   // D 10^(d.e - e), d.e >= e
+  BigInt r = d.D;
+  const BigInt ten = BigInt::from_u64(10);
+  for (int k = d.e; k > e; --k) r = mul(r, ten);
+  return r;
+}
+
+// Exact M+ membership of node (i, j, k) (R6); octant: the canonical-frame subdomain (R24).
+struct ExactClassifier {
+  int n = 0;
+  bool octant = false;
+  BigInt L, HL, C[3], W[3], rhs;   // X_a(i) = L (n+1) + (i+1) HL - C_a (n+1)
+  ExactClassifier(int n_, double lo, double hi, const dpm_domain& Dm) : n(n_) {
+    octant = Dm.kind == DPM_OCTANT_CANON;
+    std::vector<Decimal> ds = {to_decimal(lo), to_decimal(hi)};
+    for (int a = 0; a < 3; ++a) ds.push_back(to_decimal(octant ? 0.0 : Dm.center[a]));
+    for (int a = 0; a < 3; ++a) ds.push_back(to_decimal(Dm.semi[a]));
+    int e = 0;
+    for (auto& d : ds) e = std::min(e, d.e);
+    std::vector<BigInt> v;
+    for (auto& d : ds) v.push_back(scaled(d, e));
+    const BigInt np1 = BigInt::from_u64((unsigned long long)(n + 1));
+    L = mul(v[0], np1);
+    HL = add(v[1], neg(v[0]));
+    for (int a = 0; a < 3; ++a) C[a] = mul(v[2 + a], np1);
+    const BigInt np1sq = mul(np1, np1);
+    if (octant) {
+      for (int a = 0; a < 3; ++a) W[a] = BigInt::from_u64(1);
+      rhs = mul(np1sq, mul(v[5], v[5]));
+    } else {
+      BigInt S2[3];
+      for (int a = 0; a < 3; ++a) S2[a] = mul(v[5 + a], v[5 + a]);
+      for (int a = 0; a < 3; ++a) W[a] = mul(S2[(a + 1) % 3], S2[(a + 2) % 3]);
+      rhs = mul(np1sq, mul(S2[0], mul(S2[1], S2[2])));
+    }
+  }
+  bool inside(int64_t p) const {
+    const int idx[3] = {(int)(p / ((int64_t)n * n)), (int)((p / n) % n), (int)(p % n)};
+    BigInt sum;
+    for (int a = 0; a < 3; ++a) {
+      const BigInt X = add(add(L, mul(BigInt::from_u64((unsigned long long)(idx[a] + 1)), HL)), neg(C[a]));
+      if (octant && (X.neg || X.zero())) return false;   // on or behind a coordinate plane -> M-
+      sum = add(sum, mul(mul(X, X), W[a]));
+    }
+    return cmp(sum, rhs) < 0;   // ties -> M- (R6)
+  }
+};
+
 }  // namespace
 
 dpm_status setup_point_sets(dpm_ctx* ctx) {
@@ -199,8 +413,44 @@ dpm_status setup_point_sets(dpm_ctx* ctx) {
   DPM_CUDA_TRY(ctx, cudaMemsetAsync(dghost, 0, 8, s));
   const int T = 256;
   const int G = (int)std::min<long>((nn + T - 1) / T, 148L * 32);
+  unsigned long long* dties;
+  DPM_CUDA_TRY(ctx, cudaMalloc(&dties, 16));
+  DPM_CUDA_TRY(ctx, cudaMemsetAsync(dties, 0, 16, s));
   DPM_COUNT_LAUNCH(1);
-  classify_kernel<<<G, T, 0, s>>>(ctx->flags, n, ctx->lo, ctx->h, ctx->domain);
+  classify_kernel<<<G, T, 0, s>>>(ctx->flags, n, ctx->lo, ctx->h, std::max(std::fabs(ctx->lo), std::fabs(ctx->hi)),
+                                   ctx->domain, dties);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  unsigned long long hties = 0;
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hties, dties, 8, cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  ctx->exact_ties = (int64_t)hties;
+  if (hties) {   // R6: re-decide the near-tie nodes exactly on the host
+    int64_t* dlist;
+    uint8_t* dval;
+    DPM_CUDA_TRY(ctx, cudaMalloc(&dlist, hties * sizeof(int64_t)));
+    DPM_CUDA_TRY(ctx, cudaMalloc(&dval, hties));
+    DPM_COUNT_LAUNCH(1);
+    tie_list_kernel<<<G, T, 0, s>>>(ctx->flags, nn, dlist, dties + 1);
+    std::vector<int64_t> list(hties);
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(list.data(), dlist, hties * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    const ExactClassifier ex(n, ctx->lo, ctx->hi, ctx->domain);
+    std::vector<uint8_t> val(hties);
+    int64_t in = 0;
+    for (size_t i = 0; i < list.size(); ++i) {
+      val[i] = ex.inside(list[i]) ? F_MPLUS : 0;
+      in += val[i] != 0;
+    }
+    ctx->exact_ties_inside = in;
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(dval, val.data(), hties, cudaMemcpyHostToDevice, s));
+    DPM_COUNT_LAUNCH(1);
+    tie_set_kernel<<<(int)((hties + 255) / 256), 256, 0, s>>>(ctx->flags, dlist, dval, (long)hties);
+    DPM_CUDA_TRY(ctx, cudaGetLastError());
+    DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    cudaFree(dlist);
+    cudaFree(dval);
+  }
+  cudaFree(dties);
   DPM_COUNT_LAUNCH(1);
   dilate_kernel<<<G, T, 0, s>>>(ctx->flags, n, dghost);
   DPM_COUNT_LAUNCH(1);

@@ -73,3 +73,24 @@ def test_dd_pks_parity(api):
         assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
         assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
     assert sol.builds == o.builds
+
+
+def test_dd_pks_parity_per_octant_abi_path(api):
+    # The path every rank takes with ONE octant (8 GPUs): DDSolver's non-batched branch, i.e. the
+    # per-octant dpm_dd_local_begin / dpm_dd_local_finish calls (their own scratch and launches), with the
+    # coefficient sums formed across the 8 octant contexts as the all-reduce would across ranks.
+    from paper_1811_03557_b200.dd import DDSolver
+    steps, cap = 3, 1e-3
+    o = odd.DDPKSOracle(N, LC, LI, cap, steps)
+    state, ologs = o.run()
+    octs = [api.Octant(N, *BOX, s, 1.0, LC, LI, cap) for s in range(8)]
+    sol = DDSolver(octs, cap)
+    sol._batched = lambda: False
+    sol.init((0.0, 0.0, 0.0), (1000.0, 100.0), (500.0, 50.0))
+    logs = [sol.step() for _ in range(steps)]
+    for (rho, c), (ro, co) in zip(sol.fields, state):
+        assert rel(rho.cpu().numpy(), ro) <= 1e-9, rel(rho.cpu().numpy(), ro)
+        assert rel(c.cpu().numpy(), co) <= 1e-9, rel(c.cpu().numpy(), co)
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
+        assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])

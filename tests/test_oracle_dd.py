@@ -101,3 +101,30 @@ def test_reflection_symmetry_of_coupled_pks():
         assert np.abs(rho - ref[0]).max() <= 1e-10 * np.abs(ref[0]).max()
         assert np.abs(c - ref[1]).max() <= 1e-10 * np.abs(ref[1]).max()
     assert logs[0]["rebuilt"] and o.builds >= 1
+
+
+def test_column_signs_match_the_octant_extensions():
+    # E_s = E_0 diag(S_s) for every octant (the reflection parity of the cap SH and plane Legendre bases)
+    st = dd.setup(16, 4, 4)
+    S = dd.column_signs(st)
+    E0 = st.octants[0].Eraw
+    for s, o in enumerate(st.octants):
+        assert np.abs(o.Eraw - E0 * S[s]).max() <= 1e-13 * np.abs(E0).max()
+        assert np.abs(o.A - st.octants[0].A * S[s]).max() <= 1e-13 * np.abs(E0).max()
+    assert set(np.unique(S)) == {-1.0, 1.0}
+
+
+def test_symmetric_reduction_equals_the_stacked_oracle():
+    # the one-octant symmetric oracle (used for cfg5 at its configured size) against the full 8-octant
+    # stacked oracle on the same symmetric IC: same dt sequence, same fields in every octant
+    steps, cap = 3, 1e-3
+    full = dd.DDPKSOracle(16, 4, 4, cap, steps)
+    sym = dd.DDPKSOracleSymmetric(16, 4, 4, cap, steps)
+    sf, lf = full.run()
+    ss, ls = sym.run()
+    for (ro, co) in sf:
+        assert np.abs(ro - ss[0]).max() <= 1e-12 * np.abs(ro).max()
+        assert np.abs(co - ss[1]).max() <= 1e-12 * np.abs(co).max()
+    for a, b in zip(lf, ls):
+        assert a["dt"] == b["dt"] and a["rebuilt"] == b["rebuilt"]
+        assert abs(a["mass"] - b["mass"]) <= 1e-12 * abs(a["mass"])

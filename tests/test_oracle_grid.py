@@ -106,3 +106,25 @@ def test_paper_mesh_point_sets(N):
     ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "point_set_counts.json")))["paper_meshes"][str(N)]
     assert len(ps.list("gamma")) == ref["gamma"]
     assert len(ps.list("gamma_in")) == ref["gamma_in"]
+
+
+def _exact_ties_sphere(n):
+    # nodes exactly on the unit sphere in [-1.1, 1.1]^3 (R6 closed form: 121 (X²+Y²+Z²) = 100 (n+1)²,
+    # X = 2i - n + 1), counted by brute force over integer triples
+    X = 2 * np.arange(n) - n + 1
+    s = (X[:, None, None] ** 2 + X[None, :, None] ** 2 + X[None, None, :] ** 2) * 121
+    return int((s == 100 * (n + 1) ** 2).sum())
+
+
+@pytest.mark.parametrize("n,ties", [(65, 150), (16, 0), (32, 0), (128, 0)])
+def test_sphere_tie_meshes_and_rule(n, ties):
+    # R6 ties -> M-: the advisor's n = 65 mesh has nodes exactly on Γ (the GPU tie test uses it); the
+    # configured meshes have none.  The oracle's exact classification puts every tie in M-.
+    assert _exact_ties_sphere(n) == ties
+    if ties:
+        g = grid.Grid(n, -1.1, 1.1)
+        m = grid.inside_mask(g, "sphere", (0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+        X = 2 * np.arange(n) - n + 1
+        s = (X[:, None, None] ** 2 + X[None, :, None] ** 2 + X[None, None, :] ** 2) * 121
+        assert not m[s == 100 * (n + 1) ** 2].any()
+        assert np.array_equal(m, s < 100 * (n + 1) ** 2)

@@ -196,3 +196,50 @@ def test_sequential_coupling_variant():
     rb, cb, _ = b.step(r0, c0)
     assert np.array_equal(ra, rb)
     assert 0 < np.abs(ca - cb).max() < 1e-2 * np.abs(ca).max()
+    # the c equation does not involve g, so the sequential c^{i+1} is exactly the printed
+    # scheme's c output from the state (ρ̄^{i+1}, c^i) at the same dt
+    _, c_seq, _ = pks.PKSOracle(cfg, dt_rule=1).step(ra, c0)
+    assert np.abs(cb - c_seq).max() <= 1e-13 * np.abs(cb).max()
+
+
+@pytest.mark.parametrize("s", [2.0, -3.0])
+def test_upwind_direction_hand_computed(cfg2_sets, s):
+    # the face value of ρ is the LEFT reconstruction ρ_j + h/2 σ_j where ∇c > 0 and the RIGHT
+    # one ρ_{j+1} - h/2 σ_{j+1} otherwise.  ρ̄ = e^{kx} (non-constant and not linear, so the two sides
+    # differ), c = s x (∇c = s on every x face, 0 on the y and z faces).  Where the x stencil j-2..j+2
+    # lies in N+, minmod picks the central slope σ_j = e^{k x_j} sinh(kh)/h (kh = 0.3), so by hand
+    #   s > 0:  g_j = χ s (1 + sinh(kh)/2)(e^{k x_j} - e^{k x_{j-1}}) / h,
+    #   s < 0:  g_j = χ s (1 - sinh(kh)/2)(e^{k x_{j+1}} - e^{k x_j}) / h.
+    # Swapping the upwind direction changes g by ~2e-3 relative, far above the 1e-12 tolerance.
+    g, ps = cfg2_sets
+    n, h = g.n, g.h
+    k = 0.3 / h
+    chi = 1.7
+    x = g.coords()
+    X = np.broadcast_to(x[:, None, None], (n, n, n))
+    rho = np.where(ps.nplus, np.exp(k * X), 0.0)
+    c = np.where(ps.nplus, s * X, 0.0)
+    gconv = pks.convection(rho, c, ps, h, chi)
+    npl = ps.nplus_lat
+    ok = np.ones((n, n, n), dtype=bool)
+    for d in (-2, -1, 0, 1, 2):
+        ok &= np.roll(npl, -d, axis=0)[1:-1, 1:-1, 1:-1]   # node i + d along x in N+
+    ok &= ps.mplus
+    ok[:2] = False                                          # no wrap-around of np.roll
+    ok[-2:] = False
+    # the y / z neighbours of a checked cell must be in N+ too (their faces carry ∇c = 0 -> no flux,
+    # but c must be the same linear function there)
+    for ax in (1, 2):
+        for d in (-1, 1):
+            ok &= np.roll(npl, -d, axis=ax)[1:-1, 1:-1, 1:-1]
+    e = np.exp(k * X)
+    em, ep = np.exp(k * (X - h)), np.exp(k * (X + h))
+    sh = np.sinh(k * h)
+    if s > 0:
+        want = chi * s * (1 + sh / 2) * (e - em) / h
+    else:
+        want = chi * s * (1 - sh / 2) * (ep - e) / h
+    assert ok.sum() > 1000
+    assert np.abs(gconv[ok] - want[ok]).max() <= 1e-12 * np.abs(want[ok]).max()
+    wrong = chi * s * ((1 - sh / 2) * (ep - e) if s > 0 else (1 + sh / 2) * (e - em)) / h
+    assert np.abs(wrong[ok] - want[ok]).max() > 1e-4 * np.abs(want[ok]).max()

@@ -143,3 +143,42 @@ def test_two_term_extension_is_first_component():
         E2 = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, 5, two)[0]
         assert E2.shape[1] * 2 == E3.shape[1]
         assert np.array_equal(E2, E3[:, :E2.shape[1]])
+
+
+def ellipsoid_mms_error(n, lmax=10, dt=1e-2):
+    """SURVEY probe P10: zero-Neumann manufactured solution on the cfg3 ellipsoid (0.9, 0.6, 0.5) in
+    [-1, 1]^3, u* = cos(π q) + (q - 1)^2 x, q = Σ x_a^2 / s_a^2 (∇u* = 0 on q = 1), (I/dt - Δ)u = f,
+    L = 10 with {Y, d^2/2 Y} evaluated at R10's foot point / parametric angles.  The Laplacian in closed
+    form: Δ cos(π q) = -π^2 cos(π q)|∇q|^2 - π sin(π q) Δq, Δ((q-1)^2 x) = x(2|∇q|^2 + 2(q-1)Δq)
+    + 4(q-1) ∂_x q."""
+    from dpm_inputs.configs import Config
+    from oracle import ap, dpm
+    a, b, c = 0.9, 0.6, 0.5
+    cfg = Config("mms-ell", n, -1.0, 1.0, "ellipsoid", (0, 0, 0), (a, b, c), lmax, "neumann0", dt)
+    g, ps = grid.point_sets_for(cfg)
+    x = g.coords()
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    q = X ** 2 / a ** 2 + Y ** 2 / b ** 2 + Z ** 2 / c ** 2
+    g2 = 4 * (X ** 2 / a ** 4 + Y ** 2 / b ** 4 + Z ** 2 / c ** 4)
+    lq = 2 * (1 / a ** 2 + 1 / b ** 2 + 1 / c ** 2)
+    ustar = np.cos(np.pi * q) + (q - 1) ** 2 * X
+    lap = (-np.pi ** 2 * np.cos(np.pi * q) * g2 - np.pi * np.sin(np.pi * q) * lq
+           + X * (2 * g2 + 2 * (q - 1) * lq) + 8 * (q - 1) * X / a ** 2)
+    f = dt * (ustar / dt - lap)                             # L u* = (I - dt Δ) u*
+    E, d, unit, foot = dpm.extension_matrix(g, ps, cfg.kind, cfg.center, cfg.semi, cfg.lmax, cfg.basis)
+    _, B, _ = dpm.projection_and_bep(E, g, ps, dt)
+    up = ap.solve(dpm.particular_rhs(f, ps, dt), g.h, dt)
+    C = dpm.lstsq(B, up.reshape(-1)[ps.list("gamma_in")])
+    u = dpm.green(E @ C, f, g, ps, dt)
+    return np.abs(u - ustar)[ps.mplus].max()
+
+
+@pytest.mark.slow
+def test_ellipsoid_manufactured_solution_pins_r10():
+    # R10 (foot = closest point, d = signed distance, angles from (x'/a, y'/b, z'/c)) on a non-round
+    # ellipsoid: the survey's independent probe P10 measured 2.21e-2 (N = 32) and 7.05e-3 (N = 64),
+    # rate 1.65 (SURVEY.md §8(c) "Geometry" pin).  The round-ellipsoid test above cannot see the angle
+    # reading; this one can.
+    e32, e64 = ellipsoid_mms_error(32), ellipsoid_mms_error(64)
+    assert abs(e32 / 2.21e-2 - 1) < 0.01 and abs(e64 / 7.05e-3 - 1) < 0.01, (e32, e64)
+    assert 1.5 < np.log2(e32 / e64) < 1.8
