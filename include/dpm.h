@@ -256,7 +256,23 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
  * ------------------------------------------------------------------------------- */
 dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius, int32_t lmax_cap,
                              int32_t deg_if, double dt, int32_t device, dpm_ctx** out);
-/* n_rows = BEP rows of this octant (γ_in points x their pieces), K = global unknowns (HOST). */
+/* NEXT-3 — the paper's own two-subdomain DD, Case 1 (Z ∩ Γ = ∅, numerical setup P:594-641):
+ * Ω = ball of radius r2 at the origin split by the interface Z = {|x| = r1} into Ω1 = ball r1 (sub = 0)
+ * and Ω2 = shell r1 < |x| < r2 (sub = 1), each on its own grid (the paper's "N1/N2" meshes, P:627:
+ * n = N_l, h_l = 2 r_l/(N_l - 4), lo = -r_l - 5h_l/2).  Pieces: Z (piece 0, assignment bit 1) and Γ
+ * (piece 1, bit 2); Ω1's discrete boundary ζ1 is all Z, a point of Ω2's γ ∪ ζ2 is on the nearer sphere
+ * (R38).  Global unknowns, K = 3 (mz+1) + 2 (mg+1), zonal basis φ_l = P_l(cos θ):
+ *   [Z: φ | d φ | (d²/2) φ, d = |x| - r1 — the interface Cauchy data u, ∂_n u, ∂²_n u shared by both
+ *    subdomains (interface conditions P:477-480) | Γ: φ | (d²/2) φ, d = |x| - r2 (zero Neumann)].
+ * The returned context is a DD subdomain: every dpm_dd_* call below applies (BEP rows on ζ1,in or
+ * γ_in ∪ ζ2,in: the reduced BEPs eqn:reduced_DD1_BEP1/2; the stacked least squares over both
+ * subdomains by the same distributed CholeskyQR2, summed over the two contexts).  dpm_dd_pks_init (R38):
+ * the IC at the node on N+, at the foot r2 x/|x| on Γ's points (R14); with rho_cell_average the cell
+ * average (R36) of ρ on M+ and on the interface points.  DPM_ERR_INVALID on bad arguments or a box that
+ * does not strictly contain the subdomain. */
+dpm_status dpm_create_dd1(const dpm_grid* grid, int32_t sub, double r1, double r2, int32_t mz, int32_t mg, double dt,
+                          int32_t device, dpm_ctx** out);
+/* n_rows = BEP rows of this subdomain (γ_in points x their pieces), K = global unknowns (HOST). */
 dpm_status dpm_dd_info(const dpm_ctx* ctx, int64_t* n_rows, int32_t* K);
 /* HOST [n_gamma] piece bits of every γ point (1 cap, 2 x-plane, 4 y-plane, 8 z-plane). */
 dpm_status dpm_dd_copy_assign(const dpm_ctx* ctx, uint8_t* host_bits);
@@ -288,8 +304,9 @@ dpm_status dpm_dd_cfl_result(dpm_ctx* ctx, double chi, double* cfl_dt, void* str
 dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* y,
                               void* stream);
 /* Steps 5-7 with the global C (K x 2): u_γ = A C (clamped at 0 if clamp, R17), Green's formula
-   (R20), restriction to N+.  stats (HOST, 5): [h^3 Σ_{M+} ρ, max ρ, min ρ, min c, nonfinite];
-   synchronous when stats != NULL, otherwise asynchronous and dpm_dd_stats() (synchronous) reads them. */
+   (R20), restriction to N+.  stats (HOST, 6): [h^3 Σ_{M+} ρ, max ρ over N+, min ρ, min c, nonfinite,
+   max ρ over M+ (the paper's ||ρ||_inf, eq. dd-norm:max)]; synchronous when stats != NULL, otherwise
+   asynchronous and dpm_dd_stats() (synchronous, the same 6 values) reads them. */
 dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, double* rho, double* c,
                                double* stats, void* stream);
 dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream);

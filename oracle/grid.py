@@ -67,6 +67,23 @@ def inside_mask(grid: Grid, kind: str, center, semi) -> np.ndarray:
     return np.asarray(tot < den, dtype=bool)
 
 
+def shell_inside_mask(grid: Grid, r_in, r_out, center=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """Boolean [n][n][n]: node strictly inside the spherical shell r_in < |x - c| < r_out (the outer
+    subdomain Ω2 of the paper's concentric domain decomposition, Case 1), exact
+    rationals; nodes on either sphere go to M- (R6)."""
+    n = grid.n
+    lo, hi = _frac(grid.lo), _frac(grid.hi)
+    terms = []
+    for a in range(3):
+        c = _frac(center[a])
+        terms.append([((lo + (i + 1) * (hi - lo) / (n + 1)) - c) ** 2 for i in range(n)])
+    ri, ro = _frac(r_in) ** 2, _frac(r_out) ** 2
+    den = reduce(_lcm, [v.denominator for t in terms for v in t] + [ri.denominator, ro.denominator], 1)
+    ints = [np.array([int(v * den) for v in t], dtype=object) for t in terms]
+    tot = ints[0][:, None, None] + ints[1][None, :, None] + ints[2][None, None, :]
+    return np.asarray((tot > int(ri * den)) & (tot < int(ro * den)), dtype=bool)
+
+
 def _dilate7(mask_lat: np.ndarray) -> np.ndarray:
     """Union of 7-point stencils of the True points, within the lattice."""
     out = mask_lat.copy()

@@ -88,6 +88,8 @@ _sig = {
     "dpm_set_pass_timing": ([P, C.c_int32], C.c_int),
     "dpm_create_octant": ([C.POINTER(Grid), C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_double, C.c_int32,
                            C.POINTER(P)], C.c_int),
+    "dpm_create_dd1": ([C.POINTER(Grid), C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_double,
+                        C.c_int32, C.POINTER(P)], C.c_int),
     "dpm_dd_info": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
     "dpm_dd_copy_assign": ([P, C.POINTER(C.c_uint8)], C.c_int),
     "dpm_dd_bep_block": ([P, P, P], C.c_int),

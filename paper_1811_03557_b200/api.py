@@ -281,8 +281,8 @@ class Octant(DPM):
         """The same CholeskyQR pass from `src` (same device, same summed Gram, already factored)."""
         self._chk(L.lib.dpm_dd_chol_copy(self._h, pass_, src._h, _stream(stream)))
 
-    def dd_pks_init(self, rho, c, center, rho_amp, rho_rate, c_amp, c_rate, stream=None):
-        ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate)
+    def dd_pks_init(self, rho, c, center, rho_amp, rho_rate, c_amp, c_rate, stream=None, rho_cell_average=0):
+        ic = L.PksIC((C.c_double * 3)(*center), rho_amp, rho_rate, c_amp, c_rate, int(rho_cell_average))
         self._chk(L.lib.dpm_dd_pks_init(self._h, _ptr(_dev_f64(rho, "rho")), _ptr(_dev_f64(c, "c")), C.byref(ic),
                                         _stream(stream)))
 
@@ -300,9 +300,10 @@ class Octant(DPM):
         return out.value
 
     def stats(self, stream=None):
-        st = (C.c_double * 5)()
+        st = (C.c_double * 6)()
         self._chk(L.lib.dpm_dd_stats(self._h, st, _stream(stream)))
-        return {"mass": st[0], "rho_max": st[1], "rho_min": st[2], "c_min": st[3], "nonfinite": st[4]}
+        return {"mass": st[0], "rho_max": st[1], "rho_min": st[2], "c_min": st[3], "nonfinite": st[4],
+                "rho_max_mplus": st[5]}
 
     def local_finish_async(self, Cglob, rho, c, clamp=1, stream=None):
         self._chk(L.lib.dpm_dd_local_finish(self._h, _ptr(_dev_f64(Cglob, "C")), clamp, _ptr(rho), _ptr(c), None,
@@ -315,7 +316,29 @@ class Octant(DPM):
         return y
 
     def local_finish(self, Cglob, rho, c, clamp=1, stream=None):
-        st = (C.c_double * 5)()
+        st = (C.c_double * 6)()
         self._chk(L.lib.dpm_dd_local_finish(self._h, _ptr(_dev_f64(Cglob, "C")), clamp, _ptr(rho), _ptr(c), st,
                                             _stream(stream)))
-        return {"mass": st[0], "rho_max": st[1], "rho_min": st[2], "c_min": st[3], "nonfinite": st[4]}
+        return {"mass": st[0], "rho_max": st[1], "rho_min": st[2], "c_min": st[3], "nonfinite": st[4],
+                "rho_max_mplus": st[5]}
+
+
+class CaseOneSubdomain(Octant):
+    """One subdomain of the paper's two-subdomain DD, Case 1 (dpm_create_dd1, NEXT-3): sub 0 = Ω1, the
+    ball r1; sub 1 = Ω2, the shell r1 < |x| < r2; grid (n, lo, hi) its own auxiliary cube.  Every
+    dpm_dd_* method of Octant applies."""
+
+    def __init__(self, n, lo, hi, sub, r1=0.25, r2=0.5, mz=0, mg=0, dt=1e-8, device=0):
+        g = L.Grid(n, lo, hi)
+        h = C.c_void_p()
+        torch.cuda.init()
+        L.check(L.lib.dpm_create_dd1(C.byref(g), sub, r1, r2, mz, mg, dt, device, C.byref(h)))
+        self._h = h
+        self.device = torch.device("cuda", device)
+        self.n = n
+        self.sub = sub
+        self.info = self.query()
+        rows = C.c_int64()
+        K = C.c_int32()
+        self._chk(L.lib.dpm_dd_info(self._h, C.byref(rows), C.byref(K)))
+        self.n_rows, self.K = rows.value, K.value

@@ -216,10 +216,16 @@ __global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __res
   }
 }
 
+// column block of each boundary piece: piece p owns columns [start[p], start[p+1])
+struct PieceBlocks {
+  int start[6];
+  int npieces;
+};
+
 // B[i][c] = [c in block(piece_i)] Eraw[pos_i][c] - U_c[gamma[pos_i]]  (column-major n_rows x nc)
 __global__ void dd_bep_gather_kernel(const double* __restrict__ U, int ncols, size_t field,
                                      const int64_t* __restrict__ gamma, int64_t ng, const int32_t* __restrict__ rows,
-                                     int64_t nrows, const double* __restrict__ Eraw, int c0, int nc, int nphi,
+                                     int64_t nrows, const double* __restrict__ Eraw, int c0, PieceBlocks pb,
                                      double* B) {
   const long tot = (long)nrows * ncols;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
@@ -227,7 +233,8 @@ __global__ void dd_bep_gather_kernel(const double* __restrict__ U, int ncols, si
     const long ri = t - (long)cl * nrows;
     const int pos = rows[2 * ri], piece = rows[2 * ri + 1];
     const int c = c0 + cl;
-    const int blk = c < 2 * nc ? 0 : 1 + (c - 2 * nc) / (2 * nphi);
+    int blk = 0;
+    for (int p = 1; p < pb.npieces; ++p) blk += c >= pb.start[p];
     double v = -U[(size_t)cl * field + gamma[pos]];
     if (blk == piece) v += Eraw[(size_t)c * ng + pos];
     B[(size_t)cl * nrows + ri] = v;
@@ -313,6 +320,97 @@ __global__ void dd_ic_kernel(const uint8_t* __restrict__ flags, const int32_t* _
 
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
 
+// ---- NEXT-3: the paper's two-subdomain DD, Case 1 (concentric, Z ∩ Γ = ∅) ----
+// Pieces: Z (the interface |x| = r1, piece 0, bit 1) and Γ (|x| = r2, piece 1, bit 2).  Ω1 (sub 0):
+// every point of ζ1 is on Z; Ω2 (sub 1): a point of γ ∪ ζ2 is on the nearer sphere (reading R38).
+// Columns (zonal basis φ_l = P_l(cos θ), cos θ = x_z/|x|):
+//   Z: [φ | d φ | (d²/2) φ], l <= mz, d = |x| - r1 (3-term, u, ∂_n u, ∂²_n u shared by Ω1 and Ω2:
+//      the interface conditions P:477-480);   Γ: [φ | (d²/2) φ], l <= mg, d = |x| - r2 (zero Neumann).
+__device__ __forceinline__ int dd1_piece(int sub, double r, double r1, double r2) {
+  return (sub == 0 || fabs(r - r1) < fabs(r - r2)) ? 0 : 1;
+}
+
+__global__ void dd1_extension_kernel(const int64_t* gamma, int64_t ng, int n, double lo, double h, int sub,
+                                     double r1, double r2, int mz, int mg, int K, double* Eraw, double* A,
+                                     uint8_t* assign) {
+  const long g = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int64_t pidx = gamma[g];
+  const int i = (int)(pidx / ((long)n * n)), j = (int)((pidx / n) % n), k = (int)(pidx % n);
+  const double P[3] = {lo + (i + 1) * h, lo + (j + 1) * h, lo + (k + 1) * h};
+  const double r = sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]);
+  const int piece = dd1_piece(sub, r, r1, r2);
+  assign[g] = (uint8_t)(1 << piece);
+  for (int c = 0; c < K; ++c) {
+    Eraw[(size_t)c * ng + g] = 0.0;
+    A[(size_t)c * ng + g] = 0.0;
+  }
+  const double x = fmin(fmax(P[2] / r, -1.0), 1.0);
+  const int M = piece == 0 ? mz : mg;
+  const double d = r - (piece == 0 ? r1 : r2);
+  const double w2 = 0.5 * (d * d);
+  const int c0 = piece == 0 ? 0 : 3 * (mz + 1);
+  double pm = 1.0, pl = x;
+  for (int l = 0; l <= M; ++l) {   // Bonnet: (l+1) P_{l+1} = (2l+1) x P_l - l P_{l-1}
+    const double v = l == 0 ? 1.0 : pl;
+    double cols[3];
+    int nc = 0;
+    cols[nc++] = v;
+    if (piece == 0) cols[nc++] = d * v;
+    cols[nc++] = w2 * v;
+    for (int q = 0; q < nc; ++q) {
+      const size_t c = (size_t)(c0 + q * (M + 1) + l);
+      Eraw[c * ng + g] = cols[q];
+      A[c * ng + g] = cols[q];
+    }
+    if (l >= 1) {
+      const double nx = ((2 * l + 1) * x * pl - l * pm) / (l + 1);
+      pm = pl;
+      pl = nx;
+    }
+  }
+}
+
+// Initial state (R38): the IC at the node on N+, except on Γ's γ points (the foot r2 x/|x|, R14); with
+// ic.rho_cell_average, ρ̄ is the cell average (R36) on M+ and on the interface points ζ.
+__global__ void dd1_ic_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap,
+                              const uint8_t* __restrict__ assign, int n, double lo, double h, double r2, dpm_pks_ic ic,
+                              double* rho, double* c) {
+  const long nn = (long)n * n * n;
+  for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
+    const uint8_t f = flags[p];
+    double a = 0.0, b = 0.0;
+    if (f & F_NPLUS) {
+      const int i = (int)(p / ((long)n * n)), j = (int)((p / n) % n), k = (int)(p % n);
+      double X[3] = {lo + (i + 1) * h, lo + (j + 1) * h, lo + (k + 1) * h};
+      const int gp = gmap[p];
+      const bool onG = gp >= 0 && (assign[gp] & 2);
+      auto gauss = [&](const double F[3], double amp, double rate) {
+        double q2 = 0.0;
+        for (int q = 0; q < 3; ++q) q2 += (F[q] - ic.center[q]) * (F[q] - ic.center[q]);
+        return amp * exp(-rate * q2);
+      };
+      a = gauss(X, ic.rho_amp, ic.rho_rate);
+      b = gauss(X, ic.c_amp, ic.c_rate);
+      if (ic.rho_cell_average && ((f & F_MPLUS) || (gp >= 0 && (assign[gp] & 1)))) {
+        auto avg1 = [&](double s) {
+          const double q = sqrt(ic.rho_rate);
+          return 0.88622692545275801365 / q * (erf(q * (s + 0.5 * h)) - erf(q * (s - 0.5 * h))) / h;
+        };
+        a = ic.rho_amp * avg1(X[0] - ic.center[0]) * avg1(X[1] - ic.center[1]) * avg1(X[2] - ic.center[2]);
+      }
+      if (onG) {
+        const double r = sqrt(X[0] * X[0] + X[1] * X[1] + X[2] * X[2]);
+        const double F[3] = {r2 * (X[0] / r), r2 * (X[1] / r), r2 * (X[2] / r)};
+        a = gauss(F, ic.rho_amp, ic.rho_rate);
+        b = gauss(F, ic.c_amp, ic.c_rate);
+      }
+    }
+    rho[p] = a;
+    c[p] = b;
+  }
+}
+
 }  // namespace
 
 dpm_status dd_setup(dpm_ctx* ctx) {
@@ -325,9 +423,14 @@ dpm_status dd_setup(dpm_ctx* ctx) {
   DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->foot, 8));   // unused for octants (IC computed from geometry)
   DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dist, 8));
   DPM_COUNT_LAUNCH(1);
-  dd_extension_kernel<<<(unsigned)((ng + 127) / 128), 128, 0, s>>>(
-      ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1], ctx->sigma[2],
-      ctx->Lc, ctx->Li, ctx->nphi, K, ctx->dd_Eraw, ctx->E, ctx->dd_assign);
+  if (ctx->dd == 2)
+    dd1_extension_kernel<<<(unsigned)((ng + 127) / 128), 128, 0, s>>>(
+        ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->dd1_sub, ctx->dd1_r1, ctx->dd1_r2, ctx->dd1_mz,
+        ctx->dd1_mg, K, ctx->dd_Eraw, ctx->E, ctx->dd_assign);
+  else
+    dd_extension_kernel<<<(unsigned)((ng + 127) / 128), 128, 0, s>>>(
+        ctx->lists[DPM_SET_GAMMA], ng, ctx->n, ctx->lo, ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1],
+        ctx->sigma[2], ctx->Lc, ctx->Li, ctx->nphi, K, ctx->dd_Eraw, ctx->E, ctx->dd_assign);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   // BEP rows: γ_in points (ascending) x their pieces (cap, x, y, z order)
   std::vector<uint8_t> bits(ng);
@@ -338,7 +441,7 @@ dpm_status dd_setup(dpm_ctx* ctx) {
   std::vector<int32_t> rows;
   for (int64_t i = 0; i < ng; ++i)
     if (bits[i] == 0) {
-      ctx->err = "octant DD: a gamma point is on no boundary piece";
+      ctx->err = "DD: a gamma point is on no boundary piece";
       return DPM_ERR_INVALID;
     }
   for (int64_t q = 0; q < ngin; ++q)
@@ -358,7 +461,7 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 dpm_status dd_check(dpm_ctx* ctx) {
   if (!ctx) return DPM_ERR_INVALID;
-  if (!ctx->dd) { ctx->err = "not an octant subdomain context"; return DPM_ERR_INVALID; }
+  if (!ctx->dd) { ctx->err = "not a DD subdomain context"; return DPM_ERR_INVALID; }
   cudaSetDevice(ctx->device);
   return DPM_OK;
 }
@@ -379,6 +482,7 @@ namespace {
 // u_γ = A C (R17), the basis evaluated on the fly (dd_extend_fly_kernel); ug: 2 x n_gamma
 cudaError_t dd_extend_fly(dpm_ctx* ctx, const double* C, int clamp, double* ug, cudaStream_t s) {
   const int64_t ng = ctx->counts[DPM_SET_GAMMA];
+  if (ctx->dd == 2) return lsq_extend(ctx->E, ng, ctx->K, C, 2, clamp, ug, s);   // A is small: |γ| x K
   const int L1 = ctx->Lc + 1;
   const size_t smem = (2 * (size_t)ctx->K + 2 * L1 * L1 + 2 * L1) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(dd_extend_fly_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -415,6 +519,54 @@ dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius
   ctx->nphi = (deg_if + 1) * (deg_if + 2) / 2;
   ctx->K = 2 * (lmax_cap + 1) * (lmax_cap + 1) + 6 * ctx->nphi;
   ctx->lmax = lmax_cap;
+  ctx->dd_npieces = 4;
+  ctx->dd_blk[0] = 0;
+  for (int p = 1; p <= 4; ++p) ctx->dd_blk[p] = 2 * (lmax_cap + 1) * (lmax_cap + 1) + 2 * ctx->nphi * (p - 1);
+  if (ctx->E) { cudaFree(ctx->E); ctx->E = nullptr; }
+  if (ctx->foot) { cudaFree(ctx->foot); ctx->foot = nullptr; }
+  if (ctx->dist) { cudaFree(ctx->dist); ctx->dist = nullptr; }
+  st = dd_setup(ctx);
+  if (st != DPM_OK) {
+    dpm_destroy(ctx);
+    *out = nullptr;
+  }
+  return st;
+}
+
+dpm_status dpm_create_dd1(const dpm_grid* grid, int32_t sub, double r1, double r2, int32_t mz, int32_t mg, double dt,
+                          int32_t device, dpm_ctx** out) {
+  if (out) *out = nullptr;
+  if (!grid || !out || (sub != 0 && sub != 1) || !(r1 > 0) || !(r2 > r1) || mz < 0 || mg < 0 ||
+      mz > DPM_MAX_ZONAL_L || mg > DPM_MAX_ZONAL_L)
+    return DPM_ERR_INVALID;
+  const double ro = sub == 0 ? r1 : r2;
+  if (!(grid->lo < -ro && grid->hi > ro)) return DPM_ERR_INVALID;   // the subdomain strictly inside the box
+  dpm_domain D{};
+  if (sub == 0) {
+    D.kind = DPM_SPHERE;
+    D.semi[0] = D.semi[1] = D.semi[2] = r1;
+  } else {
+    D.kind = DPM_SHELL_CANON;
+    D.semi[0] = r2;
+    D.semi[1] = r1;
+  }
+  // dpm_create validates the grid and builds the point sets + AP plan; the extension data is ours
+  dpm_status st = dpm_create_impl(grid, &D, 0, dt, DPM_BASIS_NEUMANN0_2TERM_ZONAL, device, out);
+  if (st != DPM_OK) return st;
+  dpm_ctx* ctx = *out;
+  ctx->dd = 2;
+  ctx->dd1_sub = sub;
+  ctx->dd1_r1 = r1;
+  ctx->dd1_r2 = r2;
+  ctx->dd1_mz = mz;
+  ctx->dd1_mg = mg;
+  ctx->radius = ro;
+  ctx->K = 3 * (mz + 1) + 2 * (mg + 1);
+  ctx->lmax = mz;
+  ctx->dd_npieces = 2;
+  ctx->dd_blk[0] = 0;
+  ctx->dd_blk[1] = 3 * (mz + 1);
+  ctx->dd_blk[2] = ctx->K;
   if (ctx->E) { cudaFree(ctx->E); ctx->E = nullptr; }
   if (ctx->foot) { cudaFree(ctx->foot); ctx->foot = nullptr; }
   if (ctx->dist) { cudaFree(ctx->dist); ctx->dist = nullptr; }
@@ -457,15 +609,17 @@ dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream) {
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->work, (size_t)std::min(ch, K) * field * sizeof(double)));
     ctx->work_boxes = std::min(ch, K);
   }
-  const int nc = (ctx->Lc + 1) * (ctx->Lc + 1);
   for (int a = 0; a < K; a += ch) {
     const int ncol = std::min(ch, K - a);
     DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, ncol, s));
     DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, ncol, nullptr, 0, s));
     DPM_COUNT_LAUNCH(1);
+    PieceBlocks pb{};
+    pb.npieces = ctx->dd_npieces;
+    for (int p = 0; p <= ctx->dd_npieces && p < 6; ++p) pb.start[p] = ctx->dd_blk[p];
     dd_bep_gather_kernel<<<grid_for(ctx->n_rows * ncol), TB, 0, s>>>(
-        ctx->work, ncol, field, ctx->lists[DPM_SET_GAMMA], ng, ctx->dd_rows, ctx->n_rows, ctx->dd_Eraw, a, nc,
-        ctx->nphi, ctx->dd_B + (size_t)a * ctx->n_rows);
+        ctx->work, ncol, field, ctx->lists[DPM_SET_GAMMA], ng, ctx->dd_rows, ctx->n_rows, ctx->dd_Eraw, a, pb,
+        ctx->dd_B + (size_t)a * ctx->n_rows);
     DPM_CUDA_TRY(ctx, cudaGetLastError());
   }
   if (B_out)
@@ -575,9 +729,13 @@ dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_i
   if (!rho || !c || !ic) return DPM_ERR_INVALID;
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   DPM_COUNT_LAUNCH(1);
-  dd_ic_kernel<<<grid_for(nn), TB, 0, as_stream(stream)>>>(ctx->flags, ctx->gmap, ctx->dd_assign, ctx->n, ctx->lo,
-                                                           ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1],
-                                                           ctx->sigma[2], *ic, rho, c);
+  if (ctx->dd == 2)
+    dd1_ic_kernel<<<grid_for(nn), TB, 0, as_stream(stream)>>>(ctx->flags, ctx->gmap, ctx->dd_assign, ctx->n, ctx->lo,
+                                                              ctx->h, ctx->dd1_r2, *ic, rho, c);
+  else
+    dd_ic_kernel<<<grid_for(nn), TB, 0, as_stream(stream)>>>(ctx->flags, ctx->gmap, ctx->dd_assign, ctx->n, ctx->lo,
+                                                             ctx->h, ctx->radius, ctx->sigma[0], ctx->sigma[1],
+                                                             ctx->sigma[2], *ic, rho, c);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   return DPM_OK;
 }
@@ -656,7 +814,7 @@ dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* 
   if (!wk || !rho || !c) return DPM_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
   DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
-  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 6 * sizeof(double), cudaMemcpyDeviceToHost, s));
   return DPM_OK;   // dpm_dd_stats() reads the statistics
 }
 
@@ -701,7 +859,7 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));                                // R20
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
   DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
-  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 6 * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (!stats) return DPM_OK;   // asynchronous form: dpm_dd_stats() later
   return dpm_dd_stats(ctx, stats, stream);
 }
@@ -711,12 +869,13 @@ dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream) {
   if (st != DPM_OK) return st;
   if (!stats) return DPM_ERR_INVALID;
   DPM_CUDA_TRY(ctx, cudaStreamSynchronize(as_stream(stream)));
-  const double* R = ctx->red_host + 8;   // [mass_sum, rho_max, rho_min, c_min, nonfinite] (R18)
+  const double* R = ctx->red_host + 8;   // [mass_sum, rho_max, rho_min, c_min, nonfinite, rho_max M+] (R18)
   stats[0] = R[0] * ctx->h * ctx->h * ctx->h;
   stats[1] = decode_key(R[1]);
   stats[2] = -decode_key(R[2]);
   stats[3] = -decode_key(R[3]);
   stats[4] = R[4];
+  stats[5] = decode_key(R[5]);
   return DPM_OK;
 }
 

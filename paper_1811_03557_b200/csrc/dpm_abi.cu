@@ -93,7 +93,7 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   dpm_status st = DPM_OK;
   if (cudaStreamCreateWithFlags(&ctx->setup_stream, cudaStreamNonBlocking) != cudaSuccess) st = DPM_ERR_CUDA;
   if (st == DPM_OK) st = setup_point_sets(ctx);
-  if (st == DPM_OK && domain->kind != DPM_OCTANT_CANON) st = setup_geometry(ctx);
+  if (st == DPM_OK && domain->kind < DPM_OCTANT_CANON) st = setup_geometry(ctx);   // DD subdomains: their own
   if (st == DPM_OK && dst_plan_init(ctx->plan, ctx->n, ctx->h, dt) != cudaSuccess) { st = DPM_ERR_CUDA; ctx->err = "plan init"; }
   if (st == DPM_OK && cudaMalloc(&ctx->red, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
   if (st == DPM_OK && cudaMemset(ctx->red, 0, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_CUDA;   // [63]: ticket
@@ -326,7 +326,7 @@ dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* 
 
 dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out, void* stream) {
   if (!ctx || !rho || !c || !out) return DPM_ERR_INVALID;
-  if (ctx->domain.kind == DPM_OCTANT_CANON) { ctx->err = "diagnostics: single-domain contexts only"; return DPM_ERR_INVALID; }
+  if (ctx->dd) { ctx->err = "diagnostics: single-domain contexts only"; return DPM_ERR_INVALID; }
   cudaSetDevice(ctx->device);
   cudaStream_t s = as_stream(stream);
   DPM_CUDA_TRY(ctx, launch_diagnostics(ctx, rho, c, ctx->red + 16, s));

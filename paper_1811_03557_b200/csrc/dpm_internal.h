@@ -10,6 +10,9 @@
 
 // internal domain kind of an octant subdomain (dpm_create_octant), canonical frame (+,+,+)
 constexpr int DPM_OCTANT_CANON = 100;
+// internal domain kind of the Case-1 DD outer subdomain (dpm_create_dd1, NEXT-3): the open shell
+// semi[1] < |x| < semi[0] centred at the origin
+constexpr int DPM_SHELL_CANON = 101;
 
 // point-flag bits for the uint8 mask over the n^3 interior
 enum : uint8_t {
@@ -125,6 +128,11 @@ struct dpm_ctx {
   double* dd_D = nullptr;           // [K] global column scaling
   double* dd_g = nullptr;           // [2][n_rows] per-step BEP right-hand sides
   double* dd_ug = nullptr;          // [2][n_gamma] u_γ = A C
+  int dd_blk[6] = {0};              // first column of each piece's block (dd_blk[npieces] = K)
+  int dd_npieces = 0;
+  // Case-1 two-subdomain DD (dd == 2, dpm_create_dd1, NEXT-3): Ω1 = ball r1 (sub 0) or Ω2 = shell (sub 1)
+  int dd1_sub = 0, dd1_mz = 0, dd1_mg = 0;
+  double dd1_r1 = 0, dd1_r2 = 0;
   // fused BEP column build at n = 128 (bep_fused.cu)
   uint32_t* bepf_btab = nullptr;     // [n^2][8] band x-line table (mask, start); built on first use
   int32_t* bepf_bpos = nullptr;      // [n_band] line-major position of band point b

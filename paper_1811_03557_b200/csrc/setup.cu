@@ -21,6 +21,12 @@ constexpr double TIE_BAND = 1e-11;
 constexpr uint8_t F_TIE = 128;   // transient flag bit: resolved on the host before dilation
 
 __device__ __forceinline__ uint8_t classify_node(const dpm_domain& D, double x, double y, double z, double scale) {
+  if (D.kind == DPM_SHELL_CANON) {    // NEXT-3 Ω2: open shell semi[1] < |x| < semi[0]
+    const double ro2 = D.semi[0] * D.semi[0], ri2 = D.semi[1] * D.semi[1];
+    const double v = x * x + y * y + z * z;
+    if (fabs(v - ro2) <= TIE_BAND * ro2 || fabs(v - ri2) <= TIE_BAND * ri2) return F_TIE;
+    return (v > ri2 && v < ro2) ? F_MPLUS : 0;
+  }
   if (D.kind == DPM_OCTANT_CANON) {   // cfg5 subdomain in its canonical frame (R24): open octant ∩ ball
     const double r2 = D.semi[0] * D.semi[0];
     const double v = x * x + y * y + z * z;
@@ -362,12 +368,13 @@ BigInt scaled(const Decimal& d, int e) {   // D 10^(d.e - e), d.e >= e
 // Exact M+ membership of node (i, j, k) (R6); octant: the canonical-frame subdomain (R24).
 struct ExactClassifier {
   int n = 0;
-  bool octant = false;
-  BigInt L, HL, C[3], W[3], rhs;   // X_a(i) = L (n+1) + (i+1) HL - C_a (n+1)
+  bool octant = false, shell = false;
+  BigInt L, HL, C[3], W[3], rhs, rhs_in;   // X_a(i) = L (n+1) + (i+1) HL - C_a (n+1)
   ExactClassifier(int n_, double lo, double hi, const dpm_domain& Dm) : n(n_) {
     octant = Dm.kind == DPM_OCTANT_CANON;
+    shell = Dm.kind == DPM_SHELL_CANON;   // semi[0] = outer, semi[1] = inner radius, centre 0
     std::vector<Decimal> ds = {to_decimal(lo), to_decimal(hi)};
-    for (int a = 0; a < 3; ++a) ds.push_back(to_decimal(octant ? 0.0 : Dm.center[a]));
+    for (int a = 0; a < 3; ++a) ds.push_back(to_decimal(octant || shell ? 0.0 : Dm.center[a]));
     for (int a = 0; a < 3; ++a) ds.push_back(to_decimal(Dm.semi[a]));
     int e = 0;
     for (auto& d : ds) e = std::min(e, d.e);
@@ -378,9 +385,10 @@ struct ExactClassifier {
     HL = add(v[1], neg(v[0]));
     for (int a = 0; a < 3; ++a) C[a] = mul(v[2 + a], np1);
     const BigInt np1sq = mul(np1, np1);
-    if (octant) {
+    if (octant || shell) {
       for (int a = 0; a < 3; ++a) W[a] = BigInt::from_u64(1);
       rhs = mul(np1sq, mul(v[5], v[5]));
+      if (shell) rhs_in = mul(np1sq, mul(v[6], v[6]));
     } else {
       BigInt S2[3];
       for (int a = 0; a < 3; ++a) S2[a] = mul(v[5 + a], v[5 + a]);
@@ -396,6 +404,7 @@ struct ExactClassifier {
       if (octant && (X.neg || X.zero())) return false;   // on or behind a coordinate plane -> M-
       sum = add(sum, mul(mul(X, X), W[a]));
     }
+    if (shell && cmp(sum, rhs_in) <= 0) return false;   // on or inside the inner sphere -> M-
     return cmp(sum, rhs) < 0;   // ties -> M- (R6)
   }
 };

@@ -1,6 +1,10 @@
-"""Config 5 driver: the 8-octant domain decomposition.
+"""DD driver: config 5's 8-octant domain decomposition and
+the paper's two-subdomain Case-1 DD (NEXT-3; api.CaseOneSubdomain), which share the phase
+ABI and the distributed least squares.
 
-Each rank owns a set of octant contexts (one per GPU at 8 ranks; all 8 on one GPU at N=1).
+Each rank owns a set of subdomain contexts (one per GPU at 8 ranks; all on one GPU at N=1).
+Subdomains may have different grids (Case 1: N1/N2 meshes): the global Δt takes the minimum of every
+subdomain's CFL bound and 0.5 h_l^2 (R13).
 Everything numerical runs in libdpm.so; this module only sequences the ABI calls and performs
 the collectives of the distributed CholeskyQR2 / step:
   * C3-equivalent (once per dt): all-reduce(sum) of the K column norms and of two K x K Gram
@@ -25,7 +29,8 @@ class DDSolver:
     def __init__(self, octants: Sequence, dt_cap: float, chi: float = 1.0, dt_rule: int = 0, clamp: int = 1):
         self.octs = list(octants)
         self.K = self.octs[0].K
-        self.h = self.octs[0].info["h"]
+        assert all(o.K == self.K for o in self.octs), "subdomains must share the global unknowns"
+        self.h = min(o.info["h"] for o in self.octs)
         self.dt_cap, self.chi, self.dt_rule, self.clamp = dt_cap, chi, dt_rule, clamp
         self.dt_prev = float("inf")
         self.dt_bep: Optional[float] = None
@@ -69,7 +74,8 @@ class DDSolver:
         # several octants on one CUDA device with the phase-level entry points: the step's two AP
         # solves run as one batch of 2 x (octants) fields each (one dpm_aux_solve_batch)
         return (len(self.octs) > 1 and all(hasattr(o, "dd_rhs") for o in self.octs)
-                and len({str(o.device) for o in self.octs}) == 1 and self.octs[0].device.type == "cuda")
+                and len({str(o.device) for o in self.octs}) == 1 and self.octs[0].device.type == "cuda"
+                and len({(o.n, o.info["h"]) for o in self.octs}) == 1)   # one AP operator for all fields
 
     def _step_batched(self, main):
         o0 = self.octs[0]
@@ -102,13 +108,13 @@ class DDSolver:
             o.dd_restrict(wk[2 * i:2 * i + 2], rho, c, stream=self.streams[i])
         return [o.stats(stream=self.streams[i]) for i, o in enumerate(self.octs)]
 
-    def init(self, center, rho_ic, c_ic):
+    def init(self, center, rho_ic, c_ic, rho_cell_average=0):
         self.fields = []
         for o in self.octs:
             n = o.n
             rho = torch.zeros((n, n, n), dtype=torch.float64, device=o.device)
             c = torch.zeros_like(rho)
-            o.dd_pks_init(rho, c, center, *rho_ic, *c_ic)
+            o.dd_pks_init(rho, c, center, *rho_ic, *c_ic, rho_cell_average=rho_cell_average)
             self.fields.append((rho, c))
         self.dt_prev, self.t = float("inf"), 0.0
 
@@ -125,10 +131,12 @@ class DDSolver:
         if self.dt_rule == 0:
             for i, (o, (_, c)) in enumerate(zip(self.octs, self.fields)):
                 o.cfl_async(c, self.chi, stream=self.streams[i])
-            cfl = min(o.cfl_result(self.chi, stream=self.streams[i]) for i, o in enumerate(self.octs))
+            # local min of every subdomain's CFL bound and 0.5 h_l^2, then the global min across ranks
+            cfl = min(min(o.cfl_result(self.chi, stream=self.streams[i]), 0.5 * o.info["h"] ** 2)
+                      for i, o in enumerate(self.octs))
             cfl = torch.tensor([cfl], dtype=torch.float64, device=self.octs[0].device)
             cfl = float(_allreduce(cfl, dist.ReduceOp.MIN).item())
-            dt = min(min(self.dt_prev, self.dt_cap), min(cfl, 0.5 * self.h * self.h))
+            dt = min(min(self.dt_prev, self.dt_cap), cfl)
         else:
             dt = self.dt_cap
         rebuilt = self.dt_bep is None or dt != self.dt_bep
@@ -163,8 +171,13 @@ class DDSolver:
         mass = float(_allreduce(mass, dist.ReduceOp.SUM).item())
         if any(s["nonfinite"] for s in stats):
             raise FloatingPointError("non-finite value in the DD PKS step")
+        rmax = torch.tensor([max(s["rho_max"] for s in stats), max(s.get("rho_max_mplus", 0.0) for s in stats)],
+                            dtype=torch.float64, device=self.octs[0].device)
+        rmax = _allreduce(rmax, dist.ReduceOp.MAX)
         return {"t": self.t, "dt": dt, "rebuilt": rebuilt, "mass": mass,
-                "rho_max": max(s["rho_max"] for s in stats), "rho_min": min(s["rho_min"] for s in stats)}
+                "rho_max": float(rmax[0]), "rho_max_mplus": float(rmax[1]),
+                "rho_min": min(s["rho_min"] for s in stats),
+                "per_subdomain": [dict(s) for s in stats]}
 
 
 class _Null:

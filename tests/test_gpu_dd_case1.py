@@ -1,0 +1,72 @@
+"""GPU parity of NEXT-3, the paper's two-subdomain DD, Case 1, against oracle/dd_case1.py.
+
+Meshes are the paper's "N1/N2" pairs at the sizes the oracle runs in seconds: 20/20
+(h1/h2 = 1/2) and 20/12 (h1/h2 = 1/4), Test A's IC, one zonal harmonic per term.
+Tolerances (R23): point sets and piece assignment bit-exact, BEP row blocks <= 1e-11, fields after 10
+coupled PKS steps <= 1e-9, dt <= 1e-12, mass <= 1e-9."""
+import numpy as np
+import pytest
+import torch
+
+from dpm_inputs import paper_mesh
+from oracle import dd_case1 as dc
+
+pytestmark = pytest.mark.gpu
+
+SETS = ["mplus", "gamma", "gamma_in", "gamma_ex", "band", "nplus"]
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1811_03557_b200 import api as A
+    assert torch.cuda.is_available()
+    return A
+
+
+def subdomains(api, N1, N2, dt, mz=0, mg=0):
+    out = []
+    for sub, (N, r) in enumerate(((N1, 0.25), (N2, 0.5))):
+        n, lo, hi, _ = paper_mesh(N, r)
+        out.append(api.CaseOneSubdomain(n, lo, hi, sub, 0.25, 0.5, mz, mg, dt))
+    return out
+
+
+@pytest.mark.parametrize("N1,N2,mz,mg", [(20, 20, 0, 0), (20, 12, 0, 0), (36, 20, 3, 2)])
+def test_sets_pieces_and_bep_rows(api, N1, N2, mz, mg):
+    dt = 1e-8
+    o = dc.CaseOneDD(N1, N2, dt, 1, Mz=mz, Mg=mg)
+    for g, s in zip(subdomains(api, N1, N2, dt, mz, mg), o.subs):
+        for w in SETS:
+            assert np.array_equal(g.copy_set(w), s.ps.list(w)), (s.name, w)
+        assert np.array_equal(g.copy_assign(), np.where(s.piece == dc.Z_PIECE, 1, 2)), s.name
+        assert g.K == o.K and g.n_rows == len(s.gin_pos)
+        B = g.bep_block(want=True).cpu().numpy().T
+        Bo = dc.bep_rows(s, dt)
+        assert rel(B, Bo) <= 1e-11, (s.name, rel(B, Bo))
+
+
+@pytest.mark.parametrize("N1,N2,dt_rule,cell", [(20, 20, 1, 0), (20, 12, 1, 1), (20, 20, 0, 1)])
+def test_case1_pks_parity(api, N1, N2, dt_rule, cell):
+    from paper_1811_03557_b200.dd import DDSolver
+    steps = 10
+    cap = 1e-8 if dt_rule == 1 else 1e-5      # dt_rule 0: Δt = min(cap, CFL, 0.5 h1^2) (R13)
+    o = dc.CaseOneDD(N1, N2, cap, steps, dt_rule=dt_rule, rho_cell_average=bool(cell))
+    state, ologs = o.run()
+    subs = subdomains(api, N1, N2, cap)
+    sol = DDSolver(subs, cap, dt_rule=dt_rule)
+    sol.init((0.0, 0.0, 0.0), (1000.0, 100.0), (500.0, 50.0), rho_cell_average=cell)
+    s0 = o.initial_state()
+    for (rho, c), (ro, co) in zip(sol.fields, s0):
+        assert rel(rho.cpu().numpy(), ro) <= 1e-13 and rel(c.cpu().numpy(), co) <= 1e-13
+    logs = [sol.step() for _ in range(steps)]
+    for (rho, c), (ro, co) in zip(sol.fields, state):
+        assert rel(rho.cpu().numpy(), ro) <= 1e-9, rel(rho.cpu().numpy(), ro)
+        assert rel(c.cpu().numpy(), co) <= 1e-9, rel(c.cpu().numpy(), co)
+    for lg, lo in zip(logs, ologs):
+        assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
+        assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
+    assert sol.builds == o.builds

@@ -106,7 +106,7 @@ class _FakeOctant:
         self.seen[f"G{p}"] = src.seen[f"G{p}"].clone()
         self.seen[f"copy{p}"] = src.s
 
-    def dd_pks_init(self, rho, c, *a):
+    def dd_pks_init(self, rho, c, *a, **kw):
         rho.fill_(1.0)
         c.fill_(float(self.s))
 
