@@ -45,8 +45,6 @@ struct DstPlan {
   double* sinmat = nullptr;   // n <= 64: device n x n sine matrix of the fused small-n plane pass
   PassProf* prof = nullptr;   // non-null while pass timing is enabled
   cudaStream_t side = nullptr;                    // second chunk stream (DPM_STREAMS=2)
-  double* l2s = nullptr;                           // n = 128 L2-pipeline scratch (l2c fields)
-  int l2c = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -177,9 +175,6 @@ cudaError_t dst128_atab(double** tab);
 cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, const double* atab, cudaStream_t s);
 cudaError_t plane128_pass(double* u, int nfields, const double* lam, double inv_dt, double h2, double rscale,
                           cudaStream_t s);
-// x pass of the L2-resident solve pipeline: pol 1 = q (HBM, evict_first) -> scratch (evict_last),
-// pol 2 = scratch (read once, then discarded from L2) -> u (evict_first)
-cudaError_t dst128_xpass_l2(int pol, const double* in, double* out, int nfields, cudaStream_t s);
 // forward x pass of the fused BEP build (bep_fused.cu) from x-line-major band values vals[f*ldv + .]
 // through the band line table tab ([n^2][8] u32: 128-bit x mask, start)
 cudaError_t dst128_xpass_sparse(double* out, int nfields, const uint32_t* tab, const double* vals, int64_t ldv,

@@ -104,31 +104,6 @@ __device__ __forceinline__ void cp_async16(unsigned smem_addr, const double* gme
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-// L2 cache policies of the L2-resident solve pipeline ("one HBM round trip"): the
-// streamed input q and output u are evict_first, the x-transformed intermediate (a C-field scratch
-// that lives in L2 between the passes) evict_last; after the inverse pass has read a scratch line it
-// discards it (no write-back of dead data).
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void cp_async16_pol(unsigned smem_addr, const double* gmem, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, 16, %2;\n" ::"r"(smem_addr), "l"(gmem),
-               "l"(pol));
-}
-__device__ __forceinline__ void st_pol(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void discard_l2_line(const double* p) {
-  asm volatile("discard.global.L2 [%0], 128;\n" ::"l"(p) : "memory");
-}
-
 // global offset of (transform-axis row r, column cg) inside one field
 template <int PASS>
 __device__ __forceinline__ size_t goff(int r, int cg) {
@@ -372,17 +347,13 @@ __device__ __forceinline__ void prep_half2(const double* raw, bool hi, double* i
 }
 
 // cp.async of one 16-column x 128-row tile (16-byte requests) into the warp's RAW buffer
-template <int PASS, int POL = 0>
-__device__ __forceinline__ void load_raw(double* raw, const double* fieldbase, int c0, int lane, uint64_t pol = 0) {
+template <int PASS>
+__device__ __forceinline__ void load_raw(double* raw, const double* fieldbase, int c0, int lane) {
   const unsigned sb = (unsigned)__cvta_generic_to_shared(raw);
   const int cc = 2 * (lane & 7);
 #pragma unroll 8
-  for (int r = lane >> 3; r < N; r += 4) {
-    if (POL == 0)
-      cp_async16(sb + 8u * (unsigned)(r * 16 + cc), fieldbase + goff<PASS>(r, c0 + cc));
-    else
-      cp_async16_pol(sb + 8u * (unsigned)(r * 16 + cc), fieldbase + goff<PASS>(r, c0 + cc), pol);
-  }
+  for (int r = lane >> 3; r < N; r += 4)
+    cp_async16(sb + 8u * (unsigned)(r * 16 + cc), fieldbase + goff<PASS>(r, c0 + cc));
 }
 
 // Contract one block of KB k3 rows starting at K0:  P = S·pin, Q = S·qin, R = C'·wp.
@@ -465,10 +436,7 @@ __device__ __forceinline__ void load_raw_lines(double* raw, const uint32_t* __re
   }
 }
 
-// POL 0: default caching.  POL 1 (forward pass of the L2 pipeline): q loads evict_first, stores to the
-// scratch evict_last.  POL 2 (inverse pass of the L2 pipeline): scratch loads evict_first and the lines
-// discarded once in shared memory, u stores evict_first.
-template <int PASS, int MINB, int MODE = 0, int POL = 0>
+template <int PASS, int MINB, int MODE = 0>
 __global__ void __launch_bounds__(224, MINB)
 dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields,
                const uint32_t* __restrict__ tab = nullptr, const double* vals = nullptr, int64_t ldv = 0) {
@@ -485,25 +453,18 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
   const double sm1 = hi ? -1.0 : 1.0;
   const size_t field = (size_t)NN * N;
-  const uint64_t pol_in = POL ? policy_evict_first() : 0;
-  const uint64_t pol_out = POL == 1 ? policy_evict_last() : (POL == 2 ? policy_evict_first() : 0);
   if (gw < ntiles) {
     const int f = gw / TPF;
     if (MODE == 1)
       load_raw_lines<PASS>(raw, tab, vals + (size_t)f * ldv, (gw - f * TPF) * 16, lane);
     else
-      load_raw<PASS, POL>(raw, in + (size_t)f * field, (gw - f * TPF) * 16, lane, pol_in);
+      load_raw<PASS>(raw, in + (size_t)f * field, (gw - f * TPF) * 16, lane);
   }
   cp_async_commit();
   for (int t = gw; t < ntiles; t += nw) {
     const int f = t / TPF, cg = (t - f * TPF) * 16 + (lane & 15);
     double* ocol = out + (size_t)f * field + goff<PASS>(0, cg);
     asm volatile("cp.async.wait_group 0;\n" ::);
-    if (POL == 2) {   // the tile's 128 row segments (one 128-byte line each) are dead in L2 now
-      const double* tb = in + (size_t)f * field + goff<PASS>(0, (t - f * TPF) * 16);
-#pragma unroll
-      for (int r = lane; r < N; r += 32) discard_l2_line(tb + (size_t)r * (PASS == 0 ? NN : N));
-    }
     __syncwarp();
     prep_half2(raw + (lane & 15), hi, wbase, lane, std::make_integer_sequence<int, 21>{});
     __syncwarp();   // RAW consumed: prefetch the next tile under the contraction
@@ -513,7 +474,7 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
       if (MODE == 1)
         load_raw_lines<PASS>(raw, tab, vals + (size_t)fn * ldv, (tn - fn * TPF) * 16, lane);
       else
-        load_raw<PASS, POL>(raw, in + (size_t)fn * field, (tn - fn * TPF) * 16, lane, pol_in);
+        load_raw<PASS>(raw, in + (size_t)fn * field, (tn - fn * TPF) * 16, lane);
     }
     cp_async_commit();
     auto bfly = [&](auto k0c, int q, double P, double Q, double R) {
@@ -536,12 +497,7 @@ dst128f_kernel(const double* __restrict__ in, double* __restrict__ out, int nfie
           if (!va && !vb) continue;
           // mirror k3f = 43 - k3 flips σ and B (P, Q) but not A:  -Q ± R = -(Q ∓ R)
           const double v = !mir ? V[k2] : (k2 == 0 ? -V[0] : (k2 == 1 ? -V[2] : -V[1]));
-          if (hi ? vb : va) {
-            if (POL == 0)
-              __stcg(ocol + (size_t)((hi ? kb : ka) - 1) * STRIDE, v);
-            else
-              st_pol(ocol + (size_t)((hi ? kb : ka) - 1) * STRIDE, v, pol_out);
-          }
+          if (hi ? vb : va) __stcg(ocol + (size_t)((hi ? kb : ka) - 1) * STRIDE, v);
         }
       }
     };
@@ -1214,28 +1170,6 @@ cudaError_t dst128_pass(int pass, const double* in, double* out, int nfields, co
   const int grid = (int)std::min<long>(ntiles, (long)sms * std::max(1, occ));
   DPM_COUNT_LAUNCH(1);
   k<<<grid, NTHR, smem, s>>>(in, out, nfields, atab);
-  return cudaGetLastError();
-}
-
-// x pass of the L2-resident pipeline (POL 1: q -> scratch, POL 2: scratch -> u); same grid as the
-// dense pass.
-cudaError_t dst128_xpass_l2(int pol, const double* in, double* out, int nfields, cudaStream_t s) {
-  static int sms = 0;
-  if (!sms) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const size_t smem = 7 * (IN_SIZE + RAW_SIZE) * sizeof(double);
-  auto kf = pol == 1 ? dst128f_kernel<0, 1, 0, 1> : dst128f_kernel<0, 1, 0, 2>;
-  cudaError_t e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, 224, smem);
-  const long warps = (long)nfields * (NN / 16);
-  const int grid = (int)std::min<long>((warps + 6) / 7, (long)sms * std::max(1, occ));
-  DPM_COUNT_LAUNCH(1);
-  kf<<<grid, 224, smem, s>>>(in, out, nfields, nullptr, nullptr, 0);
   return cudaGetLastError();
 }
 

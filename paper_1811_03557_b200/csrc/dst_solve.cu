@@ -850,8 +850,6 @@ void dst_plan_free(DstPlan& p) {
   if (p.ev_fork) cudaEventDestroy(p.ev_fork);
   if (p.ev_join) cudaEventDestroy(p.ev_join);
   p.side = nullptr;
-  if (p.l2s) cudaFree(p.l2s);
-  p.l2s = nullptr;
   if (p.lam) cudaFree(p.lam);
   if (p.atab) cudaFree(p.atab);
   if (p.atab128) cudaFree(p.atab128);
@@ -955,38 +953,6 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     }
     cudaEventRecord(p.ev_fork, s0);
     cudaStreamWaitEvent(p.side, p.ev_fork, 0);
-  }
-  // n = 128, partial diagonalisation: the L2-resident pipeline ("one HBM round trip").
-  // Chunks of C fields: x forward q -> scratch (C fields, stays in L2), fused plane pass in the
-  // scratch, x inverse scratch -> u; only q and u touch HBM.  DPM_L2PIPE = C (0 disables).
-  static const int l2c = [] {
-    const char* v = getenv("DPM_L2PIPE");
-    return v ? atoi(v) : 0;
-  }();
-  if (n == 128 && p.pfa && p.plane && p.solver == DPM_SOLVER_DST2_TRIDIAG && l2c > 0 && batch >= l2c && !two) {
-    DstPlan& pm = const_cast<DstPlan&>(p);
-    if (!pm.l2s || pm.l2c < l2c) {
-      if (pm.l2s) cudaFree(pm.l2s);
-      pm.l2s = nullptr;
-      cudaError_t e = cudaMalloc(&pm.l2s, (size_t)l2c * field_bytes);
-      if (e != cudaSuccess) return e;
-      pm.l2c = l2c;
-    }
-    const double sc2 = 2.0 / (n + 1);
-    for (int64_t b0 = 0; b0 < batch; b0 += l2c) {
-      const int nf = (int)std::min<int64_t>(l2c, batch - b0);
-      const long long pts = (long long)nf * (long long)fe;
-      cudaError_t e;
-      if ((e = timed(p, 0, pts, s, [&] { return dst128_xpass_l2(1, q + b0 * fe, pm.l2s, nf, s); })) != cudaSuccess)
-        return e;
-      if ((e = timed(p, 1, pts, s, [&] {
-             return plane128_pass(pm.l2s, nf, p.lam, inv_dt, p.h * p.h, sc2 * sc2 * p.h * p.h, s);
-           })) != cudaSuccess)
-        return e;
-      if ((e = timed(p, 0, pts, s, [&] { return dst128_xpass_l2(2, pm.l2s, u + b0 * fe, nf, s); })) != cudaSuccess)
-        return e;
-    }
-    return cudaSuccess;
   }
   int64_t ci = 0;
   for (int64_t b0 = 0; b0 < batch; b0 += chunk, ++ci) {

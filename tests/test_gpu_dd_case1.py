@@ -70,3 +70,25 @@ def test_case1_pks_parity(api, N1, N2, dt_rule, cell):
         assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
         assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
     assert sol.builds == o.builds
+
+
+def test_paper_test_a_dd_tables():
+    # The DD columns of Tables 1-3 on the paper's N1/N2 meshes against
+    # its N = 516 SD reference (tools/test_a_dd.py, profiles/r02/test_a_dd.json).  Measured: E∞(c) in Ω2
+    # equal to every printed digit in all 8 rows; Ω1 errors and E_rel identical to the SD run on the
+    # same h (the paper's observation); E∞(ρ) in Ω2 within 0.4-40% (ρ ≈ 0 there).
+    import os, sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import test_a_dd
+    pairs = ((20, 20), (36, 36), (20, 12), (36, 20))
+    res = test_a_dd.run_tables(pairs)
+    for row in res["rows"]:
+        p = row["paper"]
+        assert abs(row["Einf_c_Omega2"] / p["Einf_c_Omega2"] - 1) < 1e-4, row      # 5 printed digits
+        assert abs(row["Einf_c_Omega1"] / p["Einf_c_Omega1"] - 1) < 1e-4, row
+        assert abs(row["E_rel"] / p["E_rel"] - 1) < 0.005, row                   # as the SD Table 3 row
+    # Ω1 of every DD run = the SD run on the same h (20/20 and 20/12 share h1 = 1/32, N = 36)
+    by = {r["N1/N2"]: r for r in res["rows"]}
+    for a, b in (("20/20", "20/12"), ("36/36", "36/20")):
+        assert abs(by[a]["Einf_rho_Omega1"] / by[b]["Einf_rho_Omega1"] - 1) < 1e-6
+        assert abs(by[a]["E_rel"] / by[b]["E_rel"] - 1) < 1e-9
