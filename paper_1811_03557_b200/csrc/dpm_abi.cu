@@ -1,12 +1,21 @@
 // extern "C" entry points of libdpm.so (declared and documented in include/dpm.h).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
 #include "dpm_internal.h"
 
 std::atomic<long long> g_dpm_launches{0};
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DPM_PDL");
+    return !(v && atoi(v) == 0);
+  }();
+  return on;
+}
 
 namespace {
 

@@ -150,6 +150,32 @@ struct dpm_ctx {
 extern std::atomic<long long> g_dpm_launches;
 #define DPM_COUNT_LAUNCH(k) (g_dpm_launches.fetch_add((k), std::memory_order_relaxed))
 
+// Programmatic dependent launch (PDL) for the chain of small kernels of a PKS step (and every other use
+// of these kernels): they are launched with cudaLaunchAttributeProgrammaticStreamSerialization and begin
+// with pdl_prologue(): griddepcontrol.wait (before any global memory access; a no-op when launched
+// without the attribute) then griddepcontrol.launch_dependents, so the next kernel of the stream is
+// launched while this one runs and its CTAs wait on the GPU instead of the launch latency being paid
+// between the two.  DPM_PDL=0 launches them plainly.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" :::);
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // helpers
 #define DPM_CUDA_TRY(ctx, call)                                                       \
   do {                                                                                \

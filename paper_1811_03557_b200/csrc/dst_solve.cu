@@ -349,6 +349,7 @@ template <int NFIX, int KSMAX, int TC, int PASS, int VEC, int MT = 2>
 __global__ void __launch_bounds__(NT, min_blocks<KSMAX, TC>())
 dst_pass_kernel(const double* __restrict__ in, double* __restrict__ out, int nfields, int n_rt,
                 const double* __restrict__ lam_g, const double* __restrict__ atab, double inv_dt, double scale) {
+  pdl_prologue();
   const Geo<NFIX, TC, PASS> G(n_rt);
   const int n = G.n;
   double* lam = sm + 2 * G.tile_elems;
@@ -424,8 +425,7 @@ cudaError_t run_pass_t(int pass, const double* in, double* out, int nfields, int
   const long ntiles = (long)nfields * ((n * n + TC - 1) / TC);
   const int grid = (int)std::min<long>(ntiles, (long)sms * occ[pass]);
   DPM_COUNT_LAUNCH(1);
-  k<<<grid, NT, smem, s>>>(in, out, nfields, n, lam, atab, inv_dt, scale);
-  return cudaGetLastError();
+  return launch_pdl(k, grid, NT, smem, s, in, out, nfields, n, lam, atab, inv_dt, scale);
 }
 
 // Column-tile width of the n = 128 instance (DPM_TC128 = 32 | 64 selects; default below).
@@ -729,6 +729,7 @@ __device__ __forceinline__ void ps_tri_row(double* row, int n, double mu, double
 __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restrict__ u, int n, const double* __restrict__ S_g,
                                                           const double* __restrict__ lam_g, double inv_dt, double h2,
                                                           double rscale) {
+  pdl_prologue();
   extern __shared__ double psm_small[];
   double* S = psm_small;           // [64][PSP]
   double* P = S + PSN * PSP;       // [64][PSP]
@@ -773,9 +774,8 @@ cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream
   if (e != cudaSuccess) return e;
   const double sc = 2.0 / (n + 1);
   DPM_COUNT_LAUNCH(1);
-  plane_small_kernel<<<(unsigned)((long)nfields * n), PS_THREADS, smem, s>>>(u, n, p.sinmat, p.lam, 1.0 / p.dt, p.h * p.h,
-                                                                       sc * sc * p.h * p.h);
-  return cudaGetLastError();
+  return launch_pdl(plane_small_kernel, (unsigned)((long)nfields * n), PS_THREADS, smem, s, u, n,
+                    (const double*)p.sinmat, (const double*)p.lam, 1.0 / p.dt, p.h * p.h, sc * sc * p.h * p.h);
 }
 
 cudaError_t run_ztri(const DstPlan& p, double* u, int nfields, cudaStream_t s) {

@@ -215,6 +215,7 @@ template <int GEMV_ROWS, int GEMV_T>
 __global__ void __launch_bounds__(GEMV_T) lsq_gemv_kernel(const double* __restrict__ M, int64_t m, int K,
                                                           const double* __restrict__ g, int nrhs,
                                                           double* __restrict__ coef) {
+  pdl_prologue();
   const int c0 = blockIdx.x * GEMV_ROWS;
   __shared__ double red[GEMV_ROWS * GEMV_RC][GEMV_T / 32];
   const double* a[GEMV_ROWS];
@@ -260,15 +261,16 @@ __global__ void __launch_bounds__(GEMV_T) lsq_gemv_kernel(const double* __restri
 void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
   if (K >= 4 * 148)
-    lsq_gemv_kernel<4, 512><<<(K + 3) / 4, 512, 0, s>>>(M, m, K, g, nrhs, coef);
+    launch_pdl(lsq_gemv_kernel<4, 512>, (K + 3) / 4, 512, 0, s, M, m, K, g, nrhs, coef);
   else
-    lsq_gemv_kernel<1, 256><<<K, 256, 0, s>>>(M, m, K, g, nrhs, coef);
+    launch_pdl(lsq_gemv_kernel<1, 256>, K, 256, 0, s, M, m, K, g, nrhs, coef);
 }
 
 // u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
 // per block, up to 2 right-hand sides per pass (E read once), coefficients staged in shared memory.
 __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int r0,
                                int nr, int clamp, double* __restrict__ ug) {
+  pdl_prologue();
   extern __shared__ double sc[];   // nr * K coefficients + 2 x 8 x 32 partial sums
   for (int i = threadIdx.x; i < nr * K; i += blockDim.x) sc[i] = coef[(size_t)r0 * K + i];
   double* part = sc + nr * K;
@@ -760,7 +762,7 @@ cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, i
     const int nr = std::min(2, nrhs - r);
     const size_t smem = (size_t)(nr * K + 512) * sizeof(double);
     DPM_COUNT_LAUNCH(1);
-    extend2_kernel<<<(unsigned)((ng + 31) / 32), 256, smem, s>>>(E, ng, K, coef, r, nr, clamp, ug);
+    launch_pdl(extend2_kernel, (unsigned)((ng + 31) / 32), 256, smem, s, E, ng, K, coef, r, nr, clamp, ug);
   }
   return cudaGetLastError();
 }

@@ -76,6 +76,7 @@ __global__ void potential_band_kernel(const int32_t* __restrict__ gmap, const in
 
 __global__ void trace_kernel(const double* __restrict__ u, const int64_t* __restrict__ list, int64_t m, double* out,
                              int64_t batch, size_t field) {
+  pdl_prologue();
   const long total = (long)m * batch;
   for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
     const long b = t / m, i = t - b * m;
@@ -171,6 +172,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
   // predicated loads (0 outside the box, like valat), then the N+ tests (interior flag; a face ghost is
   // in N+ iff its unique interior neighbour is in M+, R5; anything further out is not), the minmod
   // slopes and the upwind choice are evaluated from registers, without dependent load chains.
+  pdl_prologue();
   const long nn = (long)n * n * n;
   const double ih = 1.0 / h, idt = 1.0 / dt;
   if (zero6 && blockIdx.x == 0 && threadIdx.x < 6) zero6[threadIdx.x] = 0.0;   // this step's statistics slot
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
 __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap, int n,
                                  const double* __restrict__ fq, const double* __restrict__ ug, int64_t ng, double* q,
                                  int nrhs, double diag, double off) {
+  pdl_prologue();
   const long nn = (long)n * n * n;
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     const uint8_t f = flags[p];   // the point's flag, shared by the right-hand sides
@@ -325,6 +328,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) diag_kernel(const uint8_t* _
 // rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max)]
 __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
                                 double* c, double* stats) {
+  pdl_prologue();
   const long nn = (long)n * n * n;
   double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY, rmaxm = -INFINITY;
   int bad = 0;
@@ -453,8 +457,8 @@ cudaError_t launch_trace(const dpm_ctx* ctx, const double* u, double* out, int w
   const int64_t m = ctx->counts[which];
   if (m * batch == 0) return cudaSuccess;
   DPM_COUNT_LAUNCH(1);
-  trace_kernel<<<grid_for(m * batch), TB, 0, s>>>(u, ctx->lists[which], m, out, batch, (size_t)n * n * n);
-  return cudaGetLastError();
+  return launch_pdl(trace_kernel, grid_for(m * batch), TB, 0, s, u, (const int64_t*)ctx->lists[which], m, out, batch,
+                    (size_t)n * n * n);
 }
 
 cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int ncols, double* PgE, double* B,
@@ -498,8 +502,8 @@ cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, do
     cf.dt_out = dt_out;
   }
   DPM_COUNT_LAUNCH(1);
-  flux_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(rho, c, ctx->flags, ctx->n, ctx->h, dt, chi, fq_rho, fq_c, backup, zero6, cf);
-  return cudaGetLastError();
+  return launch_pdl(flux_rhs_kernel, grid_for(nn), TB, 0, s, rho, c, (const uint8_t*)ctx->flags, ctx->n, ctx->h, dt, chi,
+                    fq_rho, fq_c, backup, zero6, cf);
 }
 
 // sequential coupling (dpm_pks_params.coupling = 1): f_c / dt = ((1 - dt) c + dt ρ̄^{i+1}) / dt on M+
@@ -523,9 +527,8 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
   DPM_COUNT_LAUNCH(1);
-  green_rhs_kernel<<<grid_for(nn), TB, 0, s>>>(ctx->flags, ctx->gmap, ctx->n, fq, u_gamma,
-                                                      ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
-  return cudaGetLastError();
+  return launch_pdl(green_rhs_kernel, grid_for(nn), TB, 0, s, (const uint8_t*)ctx->flags, (const int32_t*)ctx->gmap,
+                    ctx->n, fq, u_gamma, (int64_t)ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
 }
 
 
@@ -548,6 +551,5 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
     if (e != cudaSuccess) return e;
   }
   DPM_COUNT_LAUNCH(1);
-  restrict_kernel<<<grid_reduce(nn), TB, 0, s>>>(ctx->flags, ctx->n, u, rho, c, stats);
-  return cudaGetLastError();
+  return launch_pdl(restrict_kernel, grid_reduce(nn), TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats);
 }
