@@ -208,6 +208,10 @@ typedef struct {
   int32_t step;
   double rho_max_mplus;   /* max of rho over M+: the paper's ||rho||_inf (eq. sd-norm:max);
                              rho_max above is over N+ (includes gamma_ex) */
+  double clamp_max;       /* max over gamma and both fields of max(-u_gamma, 0) before the clamp of R17
+                             (how far the reconstructed density went negative; NaN with coupling = 1) */
+  double lsq_resid;       /* BEP least-squares residual of the step, max over rho and c of
+                             ||B C - g||_2 / ||g||_2 (NaN with coupling = 1) */
 } dpm_step_log;
 
 /* Initial state (R14): IC at the node on M+\gamma (or, for rho with ic->rho_cell_average, its

@@ -177,6 +177,7 @@ class PKSOracle:
         f_rho, f_c = assemble_rhs(rho, c, gconv, dt)                                # Step 4a
         out = []
         us = []
+        resid, clamp_max = 0.0, 0.0
         for r in range(2):
             if r == 1 and self.coupling == 1:
                 _, f_c = assemble_rhs(out[0], c, gconv, dt)                         # c from ρ̄^{i+1}
@@ -184,14 +185,16 @@ class PKSOracle:
             up = ap.solve(dpm.particular_rhs(f, ps, dt), h, dt)                      # G f
             rhs = up.reshape(-1)[ps.list("gamma_in")]
             C = dpm.lstsq(self.B, rhs)                                              # Step 5
+            resid = max(resid, np.linalg.norm(self.B @ C - rhs) / np.linalg.norm(rhs))   # BEP LSQ residual
             u_gamma = self.E @ C
+            clamp_max = max(clamp_max, float(np.max(np.maximum(-u_gamma, 0.0))))     # R17 clamp magnitude
             if self.clamp:
                 u_gamma = np.maximum(u_gamma, 0.0)                                  # R17
             out.append(dpm.green(u_gamma, f, g, ps, dt))                            # Steps 6-7 (R20)
             us.append(u_gamma)
         self.dt_prev = dt
         self.t += dt
-        return out[0], out[1], dict(dt=dt, rebuilt=rebuilt, t=self.t)
+        return out[0], out[1], dict(dt=dt, rebuilt=rebuilt, t=self.t, lsq_resid=resid, clamp_max=clamp_max)
 
     def mass(self, rho):
         h = self.g.h

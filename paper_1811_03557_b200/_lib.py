@@ -58,7 +58,7 @@ class PksParams(C.Structure):
 class StepLog(C.Structure):
     _fields_ = [("t", C.c_double), ("dt", C.c_double), ("mass", C.c_double), ("rho_max", C.c_double),
                 ("rho_min", C.c_double), ("c_min", C.c_double), ("rebuilt", C.c_int32), ("step", C.c_int32),
-                ("rho_max_mplus", C.c_double)]
+                ("rho_max_mplus", C.c_double), ("clamp_max", C.c_double), ("lsq_resid", C.c_double)]
 
 
 P = C.c_void_p

@@ -9,12 +9,14 @@
 
 std::atomic<long long> g_dpm_launches{0};
 
+thread_local int g_pdl_scope = 0;
+
 bool pdl_enabled() {
-  static const bool on = [] {
+  static const int mode = [] {
     const char* v = getenv("DPM_PDL");
-    return !(v && atoi(v) == 0);
+    return v ? atoi(v) : 1;
   }();
-  return on;
+  return mode == 2 || (mode == 1 && g_pdl_scope > 0);
 }
 
 namespace {
@@ -46,6 +48,10 @@ void free_ctx(dpm_ctx* c) {
   if (c->pks_log) cudaFree(c->pks_log);
   if (c->pks_log_host) cudaFreeHost(c->pks_log_host);
   if (c->pks_backup) cudaFree(c->pks_backup);
+  if (c->resid_ws) cudaFree(c->resid_ws);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  for (cudaEvent_t e : c->ev_side)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -359,10 +365,12 @@ double decode_key(double slot) {
 
 extern "C" {
 
+constexpr size_t RESID_WS = 4 * 64 + 2;   // lsq_residual workspace per step slot
+
 // Enqueue one PKS step (Steps 4a-7) at a fixed dt on stream s; `slot` receives red(3), dt_true
 // (device dt rule from the state at the start of the step) and the step statistics.
 static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_params* prm, double dt,
-                                   double* slot, double* backup, cudaStream_t s) {
+                                   double* slot, double* backup, cudaStream_t s, double* rwsp) {
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
   double* fq = ctx->scratch;              // 2 boxes: f/dt on M+
@@ -391,13 +399,23 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
     return DPM_OK;
   }
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
-  // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp
+  // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp (its magnitude -> slot[10])
   DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
-  DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s));
+  DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s, slot + 10));
+  // the step's BEP least-squares residual ||B C - g|| / ||g|| -> slot[11], on a forked branch
+  // of the graph (off the critical path), joined before the step ends (gvec / coef are reused)
+  const bool fork = rwsp && ctx->side_stream;
+  if (fork) {
+    DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[0], s));
+    DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->ev_side[0], 0));
+    DPM_CUDA_TRY(ctx, lsq_residual(ctx->B, ngin, ctx->K, coef, gvec, 2, rwsp, slot + 11, ctx->side_stream));
+    DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[1], ctx->side_stream));
+  }
   // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
   DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
+  if (fork) DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
   return DPM_OK;
 }
 
@@ -418,8 +436,12 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   const long long l0 = (long long)g_dpm_launches.load();
   DPM_CUDA_TRY(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   dpm_status st = DPM_OK;
+  const int pdl = ctx->n <= 32;   // programmatic dependent launch within the step graph (dpm_internal.h)
+  g_pdl_scope += pdl;
   for (int i = 0; i < K && st == DPM_OK; ++i)
-    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs);
+    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs,
+                          ctx->resid_ws + (size_t)i * RESID_WS);
+  g_pdl_scope -= pdl;
   if (st == DPM_OK) {
     cudaError_t e = cudaMemcpyAsync(ctx->pks_log_host, ctx->pks_log, (size_t)K * 16 * 8, cudaMemcpyDeviceToHost, cs);
     if (e != cudaSuccess) { ctx->err = "capture memcpy"; st = DPM_ERR_CUDA; }
@@ -476,6 +498,10 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
     DPM_CUDA_TRY(ctx, cudaMemset(ctx->pks_log, 0, KMAX * 16 * sizeof(double)));   // CFL maxima start at 0
     DPM_CUDA_TRY(ctx, cudaMallocHost(&ctx->pks_log_host, KMAX * 16 * sizeof(double)));
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->resid_ws, (size_t)KMAX * RESID_WS * sizeof(double)));
+    DPM_CUDA_TRY(ctx, cudaMemset(ctx->resid_ws, 0, (size_t)KMAX * RESID_WS * sizeof(double)));   // tickets
+    DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_side) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t gs = ctx->graph_stream;
   // the caller's prior work on `s` (e.g. dpm_pks_init) precedes the steps
@@ -559,6 +585,8 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
         Lg.rebuilt = (i == 0) ? rebuilt : 0;
         Lg.step = done + i;
         Lg.rho_max_mplus = decode_key(L[9]);
+        Lg.clamp_max = prm->coupling == 0 ? decode_key(L[10]) : NAN;
+        Lg.lsq_resid = prm->coupling == 0 ? L[11] : NAN;
       }
     }
     done += accepted;

@@ -107,9 +107,12 @@ struct dpm_ctx {
   };
   std::vector<PksGraph> pks_graphs;
   cudaStream_t graph_stream = nullptr;
-  double* pks_log = nullptr;        // device [PKS_K][16]: red(3), dt_true, stats(5)
+  double* pks_log = nullptr;        // device [PKS_K][16]: red(3), dt_true, stats(6), clamp max (key), lsq residual
   double* pks_log_host = nullptr;   // pinned mirror
   double* pks_backup = nullptr;     // device [PKS_K][2][n^3]: state at the start of each step
+  double* resid_ws = nullptr;       // device [PKS_K][4*64 + 2]: LSQ-residual partials + ticket per step
+  cudaStream_t side_stream = nullptr;   // PKS graphs: the residual runs on a forked branch
+  cudaEvent_t ev_side[2] = {nullptr, nullptr};
 
   // octant DD subdomain (dpm_create_octant)
   int dd = 0;                       // 1 for an octant subdomain
@@ -155,12 +158,16 @@ extern std::atomic<long long> g_dpm_launches;
 // with pdl_prologue(): griddepcontrol.wait (before any global memory access; a no-op when launched
 // without the attribute) then griddepcontrol.launch_dependents, so the next kernel of the stream is
 // launched while this one runs and its CTAs wait on the GPU instead of the launch latency being paid
-// between the two.  DPM_PDL=0 launches them plainly.
+// between the two.  Used only inside the PKS step graphs of small grids (pdl_scope, set by dpm_pks_step
+// for n <= 32): measured +6% steps/s at cfg2 (n = 32) but -23% at cfg3 (n = 64), where the early-launched
+// dependents' waiting CTAs compete with the running grid.  DPM_PDL=0 disables, DPM_PDL=2 forces it for
+// every launch of these kernels.
 __device__ __forceinline__ void pdl_prologue() {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
 }
 bool pdl_enabled();
+extern thread_local int g_pdl_scope;   // > 0 while enqueueing a small-grid PKS step
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -223,7 +230,10 @@ cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int n
 // lsq.cu
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s);
 cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
-                      cudaStream_t s);
+                      cudaStream_t s, double* clampmax = nullptr);
+// ||B C - g|| / ||g|| (max over nrhs <= 2) -> out[0]; ws: 4*64 + 2 doubles, its last 8 bytes a zeroed ticket
+cudaError_t lsq_residual(const double* B, int64_t m, int K, const double* coef, const double* g, int nrhs, double* ws,
+                         double* out, cudaStream_t s);
 
 // lsq.cu building blocks (octant DD)
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s);
@@ -241,7 +251,7 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
                                double* Ri_ws, cudaStream_t s);
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s);
 cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, int nrhs, int clamp, double* ug,
-                       cudaStream_t s);
+                       cudaStream_t s, double* clampmax = nullptr);
 
 // dd.cu (octant DD setup)
 dpm_status dd_setup(dpm_ctx* ctx);

@@ -269,7 +269,7 @@ void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, d
 // u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
 // per block, up to 2 right-hand sides per pass (E read once), coefficients staged in shared memory.
 __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int r0,
-                               int nr, int clamp, double* __restrict__ ug) {
+                               int nr, int clamp, double* __restrict__ ug, double* __restrict__ clampmax) {
   pdl_prologue();
   extern __shared__ double sc[];   // nr * K coefficients + 2 x 8 x 32 partial sums
   for (int i = threadIdx.x; i < nr * K; i += blockDim.x) sc[i] = coef[(size_t)r0 * K + i];
@@ -287,10 +287,77 @@ __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, 
   part[sl * 32 + gl] = s0;
   part[256 + sl * 32 + gl] = s1;
   __syncthreads();
+  double neg = 0.0;   // how far below 0 the reconstructed density went (the clamp magnitude, R17)
   if (sl < nr && g < ng) {
     double t = part[sl * 256 + gl];
     for (int q = 1; q < 8; ++q) t += part[sl * 256 + q * 32 + gl];
     ug[(size_t)(r0 + sl) * ng + g] = clamp ? fmax(t, 0.0) : t;
+    neg = fmax(-t, 0.0);
+  }
+  if (clampmax && sl < 2) {   // warp max, one order-preserving atomicMax per warp (max is order-independent)
+    for (int o = 16; o; o >>= 1) neg = fmax(neg, __shfl_xor_sync(0xffffffffu, neg, o));
+    if (gl == 0) atomicMax((unsigned long long*)clampmax, (unsigned long long)__double_as_longlong(neg) | 0x8000000000000000ull);
+  }
+}
+
+// The BEP least-squares residual of a step: max over the nrhs (<= 2) right-hand sides of
+// ||B C - g||_2 / ||g||_2, B = |gamma_in| x K (column-major), C = K x nrhs, g = |gamma_in| x nrhs.
+// Deterministic: RES_BLOCKS fixed row ranges, per-block partial sums in a fixed reduction order, the
+// last block (ticket) adds the partials in block order and writes out[0].
+constexpr int RES_BLOCKS = 64, RES_T = 256;
+__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ B, int64_t m, int K,
+                                                          const double* __restrict__ coef,
+                                                          const double* __restrict__ g, int nrhs, double* part,
+                                                          unsigned* ticket, double* out) {
+  extern __shared__ double cs[];   // nrhs x K coefficients
+  for (int i = threadIdx.x; i < nrhs * K; i += RES_T) cs[i] = coef[i];
+  __syncthreads();
+  const int64_t r0 = m * blockIdx.x / RES_BLOCKS, r1 = m * (blockIdx.x + 1) / RES_BLOCKS;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};   // (||r||^2, ||g||^2) per right-hand side
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += RES_T) {
+    double b0 = 0.0, b1 = 0.0;
+    for (int c = 0; c < K; ++c) {
+      const double bv = B[(size_t)c * m + i];
+      b0 = fma(bv, cs[c], b0);
+      if (nrhs > 1) b1 = fma(bv, cs[K + c], b1);
+    }
+    const double g0 = g[i], r = b0 - g0;
+    acc[0] = fma(r, r, acc[0]);
+    acc[1] = fma(g0, g0, acc[1]);
+    if (nrhs > 1) {
+      const double g1 = g[m + i], r2 = b1 - g1;
+      acc[2] = fma(r2, r2, acc[2]);
+      acc[3] = fma(g1, g1, acc[3]);
+    }
+  }
+  __shared__ double red[4][RES_T / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int q = 0; q < 4; ++q) {
+    double v = acc[q];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[q][w] = v;
+  }
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 4; ++q) {
+      double s = 0.0;
+      for (int k = 0; k < RES_T / 32; ++k) s += red[q][k];
+      part[blockIdx.x * 4 + q] = s;
+    }
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == RES_BLOCKS - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int b = 0; b < RES_BLOCKS; ++b)
+      for (int q = 0; q < 4; ++q) s[q] += __ldcg(part + b * 4 + q);
+    double res = s[1] > 0 ? sqrt(s[0] / s[1]) : 0.0;
+    if (nrhs > 1 && s[3] > 0) res = fmax(res, sqrt(s[2] / s[3]));
+    out[0] = res;
+    *ticket = 0u;
   }
 }
 
@@ -365,11 +432,11 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
 }
 
 cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
-                      cudaStream_t s) {
+                      cudaStream_t s, double* clampmax) {
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN], ng = ctx->counts[DPM_SET_GAMMA];
   launch_gemv(ctx->Mlsq, m, K, g, nrhs, coef, s);
-  if (u_gamma) return lsq_extend(ctx->E, ng, K, coef, nrhs, clamp, u_gamma, s);
+  if (u_gamma) return lsq_extend(ctx->E, ng, K, coef, nrhs, clamp, u_gamma, s, clampmax);
   return cudaGetLastError();
 }
 
@@ -757,12 +824,26 @@ cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrh
 }
 
 cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, int nrhs, int clamp, double* ug,
-                       cudaStream_t s) {
+                       cudaStream_t s, double* clampmax) {
   for (int r = 0; r < nrhs; r += 2) {
     const int nr = std::min(2, nrhs - r);
     const size_t smem = (size_t)(nr * K + 512) * sizeof(double);
     DPM_COUNT_LAUNCH(1);
-    launch_pdl(extend2_kernel, (unsigned)((ng + 31) / 32), 256, smem, s, E, ng, K, coef, r, nr, clamp, ug);
+    launch_pdl(extend2_kernel, (unsigned)((ng + 31) / 32), 256, smem, s, E, ng, K, coef, r, nr, clamp, ug, clampmax);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t lsq_residual(const double* B, int64_t m, int K, const double* coef, const double* g, int nrhs, double* ws,
+                         double* out, cudaStream_t s) {
+  if (nrhs < 1 || nrhs > 2) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)nrhs * K * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(lsq_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  DPM_COUNT_LAUNCH(1);
+  lsq_resid_kernel<<<RES_BLOCKS, RES_T, smem, s>>>(B, m, K, coef, g, nrhs, ws,
+                                                   reinterpret_cast<unsigned*>(ws + 4 * RES_BLOCKS), out);
   return cudaGetLastError();
 }

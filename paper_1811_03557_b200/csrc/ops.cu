@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
   pdl_prologue();
   const long nn = (long)n * n * n;
   const double ih = 1.0 / h, idt = 1.0 / dt;
-  if (zero6 && blockIdx.x == 0 && threadIdx.x < 6) zero6[threadIdx.x] = 0.0;   // this step's statistics slot
+  if (zero6 && blockIdx.x == 0 && threadIdx.x < 7) zero6[threadIdx.x] = 0.0;   // this step's statistics slot + clamp max
   double cmx[3] = {0.0, 0.0, 0.0};
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     if (backup) {   // the step's rollback copy of the state (speculative PKS graphs), fused with the read

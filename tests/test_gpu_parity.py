@@ -610,3 +610,27 @@ def test_paper_test_a_einf_tables_1_2():
         r = rows[N]
         assert abs(r["Einf_c"] / r["paper_Einf_c"] - 1) <= 2e-4, r            # 5 printed digits
         assert abs(r["Einf_rho"] / r["paper_Einf_rho"] - 1) <= (0.05 if N == 36 else 0.01), r
+
+
+def test_pks_step_log_lsq_residual_and_clamp(api):
+    # dpm_step_log.lsq_resid (||B C - g|| / ||g||, max over ρ and c) and clamp_max (the most
+    # negative reconstructed density before the clamp of R17) against the oracle's same quantities.
+    # A broad IC so that the boundary data are O(1) (for the configured ICs they are ~1e-40 and the
+    # relative residual is round-off noise); cfg3 for a clamp that is active (~3.5e-4).
+    import dataclasses
+    cfg = dataclasses.replace(get_config("cfg2"), ic_rho=(2.0, 3.0), ic_c=(1.0, 1.0), ic_center=(0.6, 0.0, 0.0))
+    for c_, steps in ((cfg, 3), (get_config("cfg3"), 10)):
+        o = pks.PKSOracle(c_, dt_rule=0)
+        _, _, ologs = o.run(nsteps=steps)
+        ctx = api.DPM.from_config(c_)
+        rho = torch.zeros((c_.n,) * 3, dtype=torch.float64, device="cuda")
+        cc = torch.zeros_like(rho)
+        ctx.pks_init(rho, cc, c_.ic_center, *c_.ic_rho, *c_.ic_c)
+        logs = ctx.pks_step(rho, cc, steps, chi=c_.chi, dt_cap=c_.dt)
+        for lg, lo in zip(logs, ologs):
+            if c_ is cfg:
+                assert lo["lsq_resid"] > 1e-4
+                assert abs(lg["lsq_resid"] / lo["lsq_resid"] - 1) <= 1e-8, (lg["lsq_resid"], lo["lsq_resid"])
+            assert abs(lg["clamp_max"] - lo["clamp_max"]) <= 1e-6 * lo["clamp_max"] + 1e-12, (lg, lo)
+        if c_ is not cfg:
+            assert ologs[-1]["clamp_max"] > 1e-5          # the clamp is active at cfg3
