@@ -365,7 +365,8 @@ double decode_key(double slot) {
 
 extern "C" {
 
-constexpr size_t RESID_WS = 4 * 64 + 2;   // lsq_residual workspace per step slot
+// lsq_residual workspace per step slot: partials + ticket + B C (2 x |gamma_in|)
+static size_t resid_ws(const dpm_ctx* ctx) { return 4 * 64 + 2 + 2 * (size_t)ctx->counts[DPM_SET_GAMMA_IN]; }
 
 // Enqueue one PKS step (Steps 4a-7) at a fixed dt on stream s; `slot` receives red(3), dt_true
 // (device dt rule from the state at the start of the step) and the step statistics.
@@ -440,7 +441,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   g_pdl_scope += pdl;
   for (int i = 0; i < K && st == DPM_OK; ++i)
     st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs,
-                          ctx->resid_ws + (size_t)i * RESID_WS);
+                          ctx->resid_ws + (size_t)i * resid_ws(ctx));
   g_pdl_scope -= pdl;
   if (st == DPM_OK) {
     cudaError_t e = cudaMemcpyAsync(ctx->pks_log_host, ctx->pks_log, (size_t)K * 16 * 8, cudaMemcpyDeviceToHost, cs);
@@ -498,8 +499,8 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
     DPM_CUDA_TRY(ctx, cudaMemset(ctx->pks_log, 0, KMAX * 16 * sizeof(double)));   // CFL maxima start at 0
     DPM_CUDA_TRY(ctx, cudaMallocHost(&ctx->pks_log_host, KMAX * 16 * sizeof(double)));
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
-    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->resid_ws, (size_t)KMAX * RESID_WS * sizeof(double)));
-    DPM_CUDA_TRY(ctx, cudaMemset(ctx->resid_ws, 0, (size_t)KMAX * RESID_WS * sizeof(double)));   // tickets
+    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->resid_ws, (size_t)KMAX * resid_ws(ctx) * sizeof(double)));
+    DPM_CUDA_TRY(ctx, cudaMemset(ctx->resid_ws, 0, (size_t)KMAX * resid_ws(ctx) * sizeof(double)));   // tickets
     DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_side) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }

@@ -110,7 +110,7 @@ struct dpm_ctx {
   double* pks_log = nullptr;        // device [PKS_K][16]: red(3), dt_true, stats(6), clamp max (key), lsq residual
   double* pks_log_host = nullptr;   // pinned mirror
   double* pks_backup = nullptr;     // device [PKS_K][2][n^3]: state at the start of each step
-  double* resid_ws = nullptr;       // device [PKS_K][4*64 + 2]: LSQ-residual partials + ticket per step
+  double* resid_ws = nullptr;       // device [PKS_K][4*64 + 2 + 2|gamma_in|]: LSQ-residual workspace per step
   cudaStream_t side_stream = nullptr;   // PKS graphs: the residual runs on a forked branch
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
 
@@ -231,7 +231,7 @@ cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int n
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s);
 cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
                       cudaStream_t s, double* clampmax = nullptr);
-// ||B C - g|| / ||g|| (max over nrhs <= 2) -> out[0]; ws: 4*64 + 2 doubles, its last 8 bytes a zeroed ticket
+// ||B C - g|| / ||g|| (max over nrhs <= 2) -> out[0]; ws: 4*64 + 2 + nrhs*m doubles, ws[256] a zeroed ticket
 cudaError_t lsq_residual(const double* B, int64_t m, int K, const double* coef, const double* g, int nrhs, double* ws,
                          double* out, cudaStream_t s);
 

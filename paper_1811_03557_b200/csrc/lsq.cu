@@ -301,35 +301,21 @@ __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, 
 }
 
 // The BEP least-squares residual of a step: max over the nrhs (<= 2) right-hand sides of
-// ||B C - g||_2 / ||g||_2, B = |gamma_in| x K (column-major), C = K x nrhs, g = |gamma_in| x nrhs.
+// ||B C - g||_2 / ||g||_2 from bc = B C (computed by extend2_kernel with B in place of E).
 // Deterministic: RES_BLOCKS fixed row ranges, per-block partial sums in a fixed reduction order, the
 // last block (ticket) adds the partials in block order and writes out[0].
 constexpr int RES_BLOCKS = 64, RES_T = 256;
-__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ B, int64_t m, int K,
-                                                          const double* __restrict__ coef,
-                                                          const double* __restrict__ g, int nrhs, double* part,
-                                                          unsigned* ticket, double* out) {
-  extern __shared__ double cs[];   // nrhs x K coefficients
-  for (int i = threadIdx.x; i < nrhs * K; i += RES_T) cs[i] = coef[i];
-  __syncthreads();
+__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ bc, const double* __restrict__ g,
+                                                          int64_t m, int nrhs, double* part, unsigned* ticket,
+                                                          double* out) {
   const int64_t r0 = m * blockIdx.x / RES_BLOCKS, r1 = m * (blockIdx.x + 1) / RES_BLOCKS;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};   // (||r||^2, ||g||^2) per right-hand side
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += RES_T) {
-    double b0 = 0.0, b1 = 0.0;
-    for (int c = 0; c < K; ++c) {
-      const double bv = B[(size_t)c * m + i];
-      b0 = fma(bv, cs[c], b0);
-      if (nrhs > 1) b1 = fma(bv, cs[K + c], b1);
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += RES_T)
+    for (int q = 0; q < nrhs; ++q) {
+      const double gv = g[q * m + i], r = bc[q * m + i] - gv;
+      acc[2 * q] = fma(r, r, acc[2 * q]);
+      acc[2 * q + 1] = fma(gv, gv, acc[2 * q + 1]);
     }
-    const double g0 = g[i], r = b0 - g0;
-    acc[0] = fma(r, r, acc[0]);
-    acc[1] = fma(g0, g0, acc[1]);
-    if (nrhs > 1) {
-      const double g1 = g[m + i], r2 = b1 - g1;
-      acc[2] = fma(r2, r2, acc[2]);
-      acc[3] = fma(g1, g1, acc[3]);
-    }
-  }
   __shared__ double red[4][RES_T / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int q = 0; q < 4; ++q) {
@@ -837,13 +823,11 @@ cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, i
 cudaError_t lsq_residual(const double* B, int64_t m, int K, const double* coef, const double* g, int nrhs, double* ws,
                          double* out, cudaStream_t s) {
   if (nrhs < 1 || nrhs > 2) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)nrhs * K * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(lsq_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  DPM_COUNT_LAUNCH(1);
-  lsq_resid_kernel<<<RES_BLOCKS, RES_T, smem, s>>>(B, m, K, coef, g, nrhs, ws,
-                                                   reinterpret_cast<unsigned*>(ws + 4 * RES_BLOCKS), out);
+  double* bc = ws + 4 * RES_BLOCKS + 2;                        // nrhs x m
+  const size_t smem = (size_t)(nrhs * K + 512) * sizeof(double);
+  DPM_COUNT_LAUNCH(2);
+  extend2_kernel<<<(unsigned)((m + 31) / 32), 256, smem, s>>>(B, m, K, coef, 0, nrhs, 0, bc, nullptr);
+  lsq_resid_kernel<<<RES_BLOCKS, RES_T, 0, s>>>(bc, g, m, nrhs, ws, reinterpret_cast<unsigned*>(ws + 4 * RES_BLOCKS),
+                                                out);
   return cudaGetLastError();
 }
