@@ -28,7 +28,7 @@ void free_ctx(dpm_ctx* c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq,
                   c->dd_Eraw, c->dd_assign, c->dd_rows, c->dd_B, c->dd_Q, c->dd_R, c->dd_M, c->dd_D, c->dd_g, c->dd_ug,
-                  c->lsq_ws, c->work, c->scratch, c->red};
+                  c->lsq_ws, c->work, c->scratch, c->red, c->mass_part};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* l : c->lists)
@@ -48,7 +48,6 @@ void free_ctx(dpm_ctx* c) {
   if (c->pks_log) cudaFree(c->pks_log);
   if (c->pks_log_host) cudaFreeHost(c->pks_log_host);
   if (c->pks_backup) cudaFree(c->pks_backup);
-  if (c->resid_ws) cudaFree(c->resid_ws);
   if (c->side_stream) cudaStreamDestroy(c->side_stream);
   for (cudaEvent_t e : c->ev_side)
     if (e) cudaEventDestroy(e);
@@ -113,6 +112,8 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   if (st == DPM_OK && cudaMalloc(&ctx->red, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
   if (st == DPM_OK && cudaMemset(ctx->red, 0, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_CUDA;   // [63]: ticket
   if (st == DPM_OK && cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
+  if (st == DPM_OK && cudaMalloc(&ctx->mass_part, (148 * 4 + 2) * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
+  if (st == DPM_OK && cudaMemset(ctx->mass_part, 0, (148 * 4 + 2) * sizeof(double)) != cudaSuccess) st = DPM_ERR_CUDA;
   if (st != DPM_OK) {
     g_create_err = ctx->err.empty() ? "dpm_create failed" : ctx->err;
     free_ctx(ctx);
@@ -365,13 +366,11 @@ double decode_key(double slot) {
 
 extern "C" {
 
-// lsq_residual workspace per step slot: partials + ticket + B C (2 x |gamma_in|)
-static size_t resid_ws(const dpm_ctx* ctx) { return 4 * 64 + 2 + 2 * (size_t)ctx->counts[DPM_SET_GAMMA_IN]; }
 
 // Enqueue one PKS step (Steps 4a-7) at a fixed dt on stream s; `slot` receives red(3), dt_true
 // (device dt rule from the state at the start of the step) and the step statistics.
 static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_params* prm, double dt,
-                                   double* slot, double* backup, cudaStream_t s, double* rwsp) {
+                                   double* slot, double* backup, cudaStream_t s) {
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
   double* fq = ctx->scratch;              // 2 boxes: f/dt on M+
@@ -405,11 +404,11 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s, slot + 10));
   // the step's BEP least-squares residual ||B C - g|| / ||g|| -> slot[11], on a forked branch
   // of the graph (off the critical path), joined before the step ends (gvec / coef are reused)
-  const bool fork = rwsp && ctx->side_stream;
+  const bool fork = ctx->side_stream != nullptr;
   if (fork) {
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[0], s));
     DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->ev_side[0], 0));
-    DPM_CUDA_TRY(ctx, lsq_residual(ctx->B, ngin, ctx->K, coef, gvec, 2, rwsp, slot + 11, ctx->side_stream));
+    DPM_CUDA_TRY(ctx, lsq_residual(ctx, coef, gvec, 2, slot + 11, ctx->side_stream));
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[1], ctx->side_stream));
   }
   // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
@@ -440,8 +439,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   const int pdl = ctx->n <= 32;   // programmatic dependent launch within the step graph (dpm_internal.h)
   g_pdl_scope += pdl;
   for (int i = 0; i < K && st == DPM_OK; ++i)
-    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs,
-                          ctx->resid_ws + (size_t)i * resid_ws(ctx));
+    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs);
   g_pdl_scope -= pdl;
   if (st == DPM_OK) {
     cudaError_t e = cudaMemcpyAsync(ctx->pks_log_host, ctx->pks_log, (size_t)K * 16 * 8, cudaMemcpyDeviceToHost, cs);
@@ -499,8 +497,6 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
     DPM_CUDA_TRY(ctx, cudaMemset(ctx->pks_log, 0, KMAX * 16 * sizeof(double)));   // CFL maxima start at 0
     DPM_CUDA_TRY(ctx, cudaMallocHost(&ctx->pks_log_host, KMAX * 16 * sizeof(double)));
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
-    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->resid_ws, (size_t)KMAX * resid_ws(ctx) * sizeof(double)));
-    DPM_CUDA_TRY(ctx, cudaMemset(ctx->resid_ws, 0, (size_t)KMAX * resid_ws(ctx) * sizeof(double)));   // tickets
     DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_side) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }

@@ -110,7 +110,6 @@ struct dpm_ctx {
   double* pks_log = nullptr;        // device [PKS_K][16]: red(3), dt_true, stats(6), clamp max (key), lsq residual
   double* pks_log_host = nullptr;   // pinned mirror
   double* pks_backup = nullptr;     // device [PKS_K][2][n^3]: state at the start of each step
-  double* resid_ws = nullptr;       // device [PKS_K][4*64 + 2 + 2|gamma_in|]: LSQ-residual workspace per step
   cudaStream_t side_stream = nullptr;   // PKS graphs: the residual runs on a forked branch
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
 
@@ -145,6 +144,7 @@ struct dpm_ctx {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
   double* red = nullptr;         // device reduction slots
+  double* mass_part = nullptr;   // device [148*4] per-block mass partials + a zeroed ticket (restrict_kernel)
   double* red_host = nullptr;    // pinned
 };
 
@@ -231,9 +231,8 @@ cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int n
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s);
 cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
                       cudaStream_t s, double* clampmax = nullptr);
-// ||B C - g|| / ||g|| (max over nrhs <= 2) -> out[0]; ws: 4*64 + 2 + nrhs*m doubles, ws[256] a zeroed ticket
-cudaError_t lsq_residual(const double* B, int64_t m, int K, const double* coef, const double* g, int nrhs, double* ws,
-                         double* out, cudaStream_t s);
+// ||B C - g|| / ||g|| (max over nrhs <= 2) -> out[0], from the ctx's factorisation (lsq.cu)
+cudaError_t lsq_residual(dpm_ctx* ctx, const double* coef, const double* g, int nrhs, double* out, cudaStream_t s);
 
 // lsq.cu building blocks (octant DD)
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s);

@@ -300,22 +300,30 @@ __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, 
   }
 }
 
-// The BEP least-squares residual of a step: max over the nrhs (<= 2) right-hand sides of
-// ||B C - g||_2 / ||g||_2 from bc = B C (computed by extend2_kernel with B in place of E).
-// Deterministic: RES_BLOCKS fixed row ranges, per-block partial sums in a fixed reduction order, the
-// last block (ticket) adds the partials in block order and writes out[0].
-constexpr int RES_BLOCKS = 64, RES_T = 256;
-__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ bc, const double* __restrict__ g,
-                                                          int64_t m, int nrhs, double* part, unsigned* ticket,
+// The BEP least-squares residual of a step, max over the nrhs (<= 2) right-hand sides of
+// ||B C - g||_2 / ||g||_2.  With the factorisation B D = Q R (column equilibration D, CholeskyQR2) the
+// least-squares solution is C = D R^{-1} Q^T g, so ||B C - g||^2 = ||g||^2 - ||Q^T g||^2 with
+// Q^T g = R D^{-1} C: a K x K triangular product instead of another pass over B (the subtraction loses
+// the digits of the residual's smallness: ~1e-8 relative noise floor).  One block, fixed reduction order
+// (deterministic).
+constexpr int RES_T = 256;
+__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ R, int K,
+                                                          const double* __restrict__ D,
+                                                          const double* __restrict__ coef,
+                                                          const double* __restrict__ g, int64_t m, int nrhs,
                                                           double* out) {
-  const int64_t r0 = m * blockIdx.x / RES_BLOCKS, r1 = m * (blockIdx.x + 1) / RES_BLOCKS;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};   // (||r||^2, ||g||^2) per right-hand side
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += RES_T)
+  extern __shared__ double y[];   // nrhs x K: D^{-1} C
+  for (int i = threadIdx.x; i < nrhs * K; i += RES_T) y[i] = coef[i] / D[i % K];
+  __syncthreads();
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};   // (||Q^T g||^2, ||g||^2) per right-hand side
+  for (int i = threadIdx.x; i < K; i += RES_T)
     for (int q = 0; q < nrhs; ++q) {
-      const double gv = g[q * m + i], r = bc[q * m + i] - gv;
-      acc[2 * q] = fma(r, r, acc[2 * q]);
-      acc[2 * q + 1] = fma(gv, gv, acc[2 * q + 1]);
+      double z = 0.0;
+      for (int jj = i; jj < K; ++jj) z = fma(R[(size_t)jj * K + i], y[q * K + jj], z);
+      acc[2 * q] = fma(z, z, acc[2 * q]);
     }
+  for (int64_t i = threadIdx.x; i < m; i += RES_T)
+    for (int q = 0; q < nrhs; ++q) acc[2 * q + 1] = fma(g[q * m + i], g[q * m + i], acc[2 * q + 1]);
   __shared__ double red[4][RES_T / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int q = 0; q < 4; ++q) {
@@ -324,26 +332,14 @@ __global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restri
     if (lane == 0) red[q][w] = v;
   }
   __syncthreads();
-  __shared__ bool last;
   if (threadIdx.x == 0) {
-    for (int q = 0; q < 4; ++q) {
-      double s = 0.0;
-      for (int k = 0; k < RES_T / 32; ++k) s += red[q][k];
-      part[blockIdx.x * 4 + q] = s;
-    }
-    __threadfence();
-    last = atomicAdd(ticket, 1u) == RES_BLOCKS - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
     double s[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int b = 0; b < RES_BLOCKS; ++b)
-      for (int q = 0; q < 4; ++q) s[q] += __ldcg(part + b * 4 + q);
-    double res = s[1] > 0 ? sqrt(s[0] / s[1]) : 0.0;
-    if (nrhs > 1 && s[3] > 0) res = fmax(res, sqrt(s[2] / s[3]));
+    for (int q = 0; q < 4; ++q)
+      for (int k = 0; k < RES_T / 32; ++k) s[q] += red[q][k];
+    double res = 0.0;
+    for (int q = 0; q < nrhs; ++q)
+      if (s[2 * q + 1] > 0) res = fmax(res, sqrt(fmax(s[2 * q + 1] - s[2 * q], 0.0) / s[2 * q + 1]));
     out[0] = res;
-    *ticket = 0u;
   }
 }
 
@@ -528,7 +524,7 @@ __global__ void __launch_bounds__(256) gram64_kernel(const double* __restrict__ 
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int i = bi + ty + 16 * a, j = bj + tx + 16 * b;
-      if (i < K && j < K && i <= j) atomicAdd(G + (size_t)j * K + i, acc[a][b]);
+      if (i < K && j < K && i <= j) G[(size_t)blockIdx.z * K * K + (size_t)j * K + i] = acc[a][b];   // split slice
     }
 }
 
@@ -645,8 +641,19 @@ __global__ void __launch_bounds__(256) gram_dmma_kernel(const double* __restrict
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int i = bi + wi + 8 * a + (lane >> 2), j = bj + wj + 8 * b + 2 * (lane & 3) + h;
-        if (i < K && j < K && i <= j) atomicAdd(G + (size_t)j * K + i, acc[a][b][h]);
+        if (i < K && j < K && i <= j) G[(size_t)blockIdx.z * K * K + (size_t)j * K + i] = acc[a][b][h];
       }
+}
+
+// G[j][i] (i <= j) = Σ_z P[z][j][i] in slice order; the lower triangle is zero
+__global__ void gram_sum_kernel(const double* __restrict__ P, int nsplit, int K, double* __restrict__ G) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x, KK = (size_t)K * K;
+  if (e >= KK) return;
+  const int j = (int)(e / K), i = (int)(e % K);
+  double s = 0.0;
+  if (i <= j)
+    for (int z = 0; z < nsplit; ++z) s += P[z * KK + e];
+  G[e] = s;
 }
 
 constexpr int DT_RK = 32, DT_P = 72;   // tri-GEMM: k per stage, pitch of the [k][64] stages (72 = 8 mod 16)
@@ -749,23 +756,37 @@ cudaError_t launch_gemm_tri(const double* A, int64_t m, int K, const double* T, 
   return cudaGetLastError();
 }
 
+// G = A^T A (upper triangle).  The row range is split over nsplit slices whose partial Grams are written
+// to a stream-ordered workspace and summed in slice order (deterministic: no atomics).
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(G, 0, (size_t)K * K * sizeof(double), s);
-  if (e != cudaSuccess) return e;
   const int tiles = (K + 63) / 64;
   const int64_t upper = (int64_t)tiles * (tiles + 1) / 2;
   const int64_t target_split = std::max<int64_t>(1, (148 * 4) / upper);
   const int64_t rps = std::max<int64_t>(64, ((m + target_split - 1) / target_split + 15) / 16 * 16);
   const int nsplit = (int)std::max<int64_t>(1, (m + rps - 1) / rps);
+  double* P = G;
+  cudaError_t e;
+  if (nsplit > 1) {
+    if ((e = cudaMallocAsync(&P, (size_t)nsplit * K * K * sizeof(double), s)) != cudaSuccess) return e;
+  } else if ((e = cudaMemsetAsync(G, 0, (size_t)K * K * sizeof(double), s)) != cudaSuccess) {   // lower triangle
+    return e;
+  }
   DPM_COUNT_LAUNCH(1);
   if (lsq_dmma()) {
     const size_t smem = 4 * 64 * DG_PG * sizeof(double);
     if ((e = cudaFuncSetAttribute(gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
       return e;
-    gram_dmma_kernel<<<dim3(tiles, tiles, nsplit), 256, smem, s>>>(A, m, K, G, (rps + DG_RK - 1) / DG_RK * DG_RK);
+    gram_dmma_kernel<<<dim3(tiles, tiles, nsplit), 256, smem, s>>>(A, m, K, P, (rps + DG_RK - 1) / DG_RK * DG_RK);
   } else
-    gram64_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, s>>>(A, m, K, G, rps);
-  return cudaGetLastError();
+    gram64_kernel<<<dim3(tiles, tiles, nsplit), 256, 0, s>>>(A, m, K, P, rps);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (nsplit > 1) {
+    DPM_COUNT_LAUNCH(1);
+    gram_sum_kernel<<<(unsigned)(((size_t)K * K + 255) / 256), 256, 0, s>>>(P, nsplit, K, G);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaFreeAsync(P, s);
+  }
+  return cudaSuccess;
 }
 
 cudaError_t lsq_cholesky(double* G, int K, int* dfail, cudaStream_t s) {
@@ -820,14 +841,15 @@ cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, i
   return cudaGetLastError();
 }
 
-cudaError_t lsq_residual(const double* B, int64_t m, int K, const double* coef, const double* g, int nrhs, double* ws,
-                         double* out, cudaStream_t s) {
+cudaError_t lsq_residual(dpm_ctx* ctx, const double* coef, const double* g, int nrhs, double* out, cudaStream_t s) {
   if (nrhs < 1 || nrhs > 2) return cudaErrorInvalidValue;
-  double* bc = ws + 4 * RES_BLOCKS + 2;                        // nrhs x m
-  const size_t smem = (size_t)(nrhs * K + 512) * sizeof(double);
-  DPM_COUNT_LAUNCH(2);
-  extend2_kernel<<<(unsigned)((m + 31) / 32), 256, smem, s>>>(B, m, K, coef, 0, nrhs, 0, bc, nullptr);
-  lsq_resid_kernel<<<RES_BLOCKS, RES_T, 0, s>>>(bc, g, m, nrhs, ws, reinterpret_cast<unsigned*>(ws + 4 * RES_BLOCKS),
-                                                out);
+  const int K = ctx->K;
+  const size_t smem = (size_t)nrhs * K * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(lsq_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  DPM_COUNT_LAUNCH(1);
+  lsq_resid_kernel<<<1, RES_T, smem, s>>>(ctx->R, K, ctx->colscale, coef, g, ctx->counts[DPM_SET_GAMMA_IN], nrhs, out);
   return cudaGetLastError();
 }

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) diag_kernel(const uint8_t* _
 // restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite,
 // rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max)]
 __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
-                                double* c, double* stats) {
+                                double* c, double* stats, double* mpart) {
   pdl_prologue();
   const long nn = (long)n * n * n;
   double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY, rmaxm = -INFINITY;
@@ -370,7 +370,17 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     for (int q = 0; q < TB / 32; ++q) {
       s += red[0][q]; a = fmax(a, red[1][q]); b = fmin(b, red[2][q]); d = fmin(d, red[3][q]); am = fmax(am, red[4][q]);
     }
-    atomicAdd(stats + 0, s);
+    // the mass: per-block partials summed in block order by the last block (deterministic, R18)
+    mpart[blockIdx.x] = s;
+    __threadfence();
+    unsigned* ticket = reinterpret_cast<unsigned*>(mpart + gridDim.x);
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+      __threadfence();
+      double tot = 0.0;
+      for (unsigned q = 0; q < gridDim.x; ++q) tot += __ldcg(mpart + q);
+      stats[0] = tot;
+      *ticket = 0u;
+    }
     // max via bit patterns on the ordered transform
     auto key = [](double v) {
       unsigned long long x = (unsigned long long)__double_as_longlong(v);
@@ -551,5 +561,6 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
     if (e != cudaSuccess) return e;
   }
   DPM_COUNT_LAUNCH(1);
-  return launch_pdl(restrict_kernel, grid_reduce(nn), TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats);
+  return launch_pdl(restrict_kernel, grid_reduce(nn), TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats,
+                    ctx->mass_part);
 }

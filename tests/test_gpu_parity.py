@@ -630,7 +630,26 @@ def test_pks_step_log_lsq_residual_and_clamp(api):
         for lg, lo in zip(logs, ologs):
             if c_ is cfg:
                 assert lo["lsq_resid"] > 1e-4
-                assert abs(lg["lsq_resid"] / lo["lsq_resid"] - 1) <= 1e-8, (lg["lsq_resid"], lo["lsq_resid"])
+                assert abs(lg["lsq_resid"] / lo["lsq_resid"] - 1) <= 1e-6, (lg["lsq_resid"], lo["lsq_resid"])
             assert abs(lg["clamp_max"] - lo["clamp_max"]) <= 1e-6 * lo["clamp_max"] + 1e-12, (lg, lo)
         if c_ is not cfg:
             assert ologs[-1]["clamp_max"] > 1e-5          # the clamp is active at cfg3
+
+
+def test_runs_are_bitwise_deterministic(api):
+    # no floating-point atomics on the result paths: the Gram matrices of CholeskyQR2 sum their split-K
+    # slices in order, the step mass sums per-block partials in block order
+    cfg = get_config("cfg3")
+    outs = []
+    for _ in range(2):
+        c = api.DPM.from_config(cfg)
+        rho = torch.zeros((cfg.n,) * 3, dtype=torch.float64, device="cuda")
+        cc = torch.zeros_like(rho)
+        c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+        logs = c.pks_step(rho, cc, 12, chi=cfg.chi, dt_cap=cfg.dt)
+        g = torch.from_numpy(np.linspace(-1.0, 1.0, c.info["n_gamma_in"])[None, :].copy()).cuda()
+        coef, _ = c.boundary_lsq(g)
+        outs.append((rho.cpu().numpy(), cc.cpu().numpy(), [lg["mass"] for lg in logs], coef.cpu().numpy()))
+    (r0, c0, m0, k0), (r1, c1, m1, k1) = outs
+    assert np.array_equal(r0, r1) and np.array_equal(c0, c1)
+    assert m0 == m1 and np.array_equal(k0, k1)
