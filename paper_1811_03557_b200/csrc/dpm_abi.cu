@@ -404,7 +404,15 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s, slot + 10));
   // the step's BEP least-squares residual ||B C - g|| / ||g|| -> slot[11], on a forked branch
   // of the graph (off the critical path), joined before the step ends (gvec / coef are reused)
-  const bool fork = ctx->side_stream != nullptr;
+  static const bool resid_on = [] {   // DPM_STEP_RESID=0: no residual (lsq_resid logged as NaN)
+    const char* v = getenv("DPM_STEP_RESID");
+    return !(v && atoi(v) == 0);
+  }();
+  const bool fork = resid_on && ctx->side_stream != nullptr;
+  if (!fork) {
+    const double nan = NAN;
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(slot + 11, &nan, sizeof(double), cudaMemcpyHostToDevice, s));
+  }
   if (fork) {
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[0], s));
     DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->ev_side[0], 0));

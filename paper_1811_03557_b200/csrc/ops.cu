@@ -352,6 +352,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
   }
   __shared__ double red[5][TB / 32];
   __shared__ int sbad;
+  __shared__ bool last_block;
   if (threadIdx.x == 0) sbad = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -370,17 +371,10 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     for (int q = 0; q < TB / 32; ++q) {
       s += red[0][q]; a = fmax(a, red[1][q]); b = fmin(b, red[2][q]); d = fmin(d, red[3][q]); am = fmax(am, red[4][q]);
     }
-    // the mass: per-block partials summed in block order by the last block (deterministic, R18)
+    // the mass: per-block partials, summed by the last block in a fixed order (deterministic, R18)
     mpart[blockIdx.x] = s;
     __threadfence();
-    unsigned* ticket = reinterpret_cast<unsigned*>(mpart + gridDim.x);
-    if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
-      __threadfence();
-      double tot = 0.0;
-      for (unsigned q = 0; q < gridDim.x; ++q) tot += __ldcg(mpart + q);
-      stats[0] = tot;
-      *ticket = 0u;
-    }
+    last_block = atomicAdd(reinterpret_cast<unsigned*>(mpart + 148 * 4), 1u) == gridDim.x - 1;
     // max via bit patterns on the ordered transform
     auto key = [](double v) {
       unsigned long long x = (unsigned long long)__double_as_longlong(v);
@@ -391,6 +385,21 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     atomicMax((unsigned long long*)(stats + 3), key(-d));
     if (sbad) atomicAdd(stats + 4, 1.0);
     atomicMax((unsigned long long*)(stats + 5), key(am));
+  }
+  __syncthreads();
+  if (last_block) {   // thread t sums partials t, t + TB, ... then a fixed shuffle / warp-order tree
+    __threadfence();
+    double v = 0.0;
+    for (unsigned q = threadIdx.x; q < gridDim.x; q += TB) v += __ldcg(mpart + q);
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int q = 0; q < TB / 32; ++q) tot += red[0][q];
+      stats[0] = tot;
+      *reinterpret_cast<unsigned*>(mpart + 148 * 4) = 0u;
+    }
   }
 }
 
