@@ -813,8 +813,8 @@ dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* 
   if (st != DPM_OK) return st;
   if (!wk || !rho || !c) return DPM_ERR_INVALID;
   cudaStream_t s = as_stream(stream);
-  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
-  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 6 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 32, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 32, ctx->red + 32, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
   return DPM_OK;   // dpm_dd_stats() reads the statistics
 }
 
@@ -858,8 +858,8 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
   DPM_CUDA_TRY(ctx, dd_extend_fly(ctx, C, clamp, ug, s));                                   // u_γ = A C (R17)
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));                                // R20
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
-  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 8, s));
-  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 8, ctx->red + 8, 6 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, ctx->red + 32, s));
+  DPM_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->red_host + 32, ctx->red + 32, 9 * sizeof(double), cudaMemcpyDeviceToHost, s));
   if (!stats) return DPM_OK;   // asynchronous form: dpm_dd_stats() later
   return dpm_dd_stats(ctx, stats, stream);
 }
@@ -869,8 +869,8 @@ dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream) {
   if (st != DPM_OK) return st;
   if (!stats) return DPM_ERR_INVALID;
   DPM_CUDA_TRY(ctx, cudaStreamSynchronize(as_stream(stream)));
-  const double* R = ctx->red_host + 8;   // [mass_sum, rho_max, rho_min, c_min, nonfinite, rho_max M+] (R18)
-  stats[0] = R[0] * ctx->h * ctx->h * ctx->h;
+  const double* R = ctx->red_host + 32;   // [mass lo, rho_max, rho_min, c_min, nonfinite, rho_max M+, -, -, mass hi] (R18)
+  stats[0] = mass_fixed_decode(R) * ctx->h * ctx->h * ctx->h;
   stats[1] = decode_key(R[1]);
   stats[2] = -decode_key(R[2]);
   stats[3] = -decode_key(R[3]);

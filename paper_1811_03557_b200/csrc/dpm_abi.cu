@@ -26,9 +26,9 @@ thread_local std::string g_create_err;
 void free_ctx(dpm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq,
+  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq, c->RDinv,
                   c->dd_Eraw, c->dd_assign, c->dd_rows, c->dd_B, c->dd_Q, c->dd_R, c->dd_M, c->dd_D, c->dd_g, c->dd_ug,
-                  c->lsq_ws, c->work, c->scratch, c->red, c->mass_part};
+                  c->lsq_ws, c->work, c->scratch, c->red};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto* l : c->lists)
@@ -112,8 +112,6 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   if (st == DPM_OK && cudaMalloc(&ctx->red, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
   if (st == DPM_OK && cudaMemset(ctx->red, 0, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_CUDA;   // [63]: ticket
   if (st == DPM_OK && cudaMallocHost(&ctx->red_host, 64 * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
-  if (st == DPM_OK && cudaMalloc(&ctx->mass_part, (148 * 4 + 2) * sizeof(double)) != cudaSuccess) st = DPM_ERR_OOM;
-  if (st == DPM_OK && cudaMemset(ctx->mass_part, 0, (148 * 4 + 2) * sizeof(double)) != cudaSuccess) st = DPM_ERR_CUDA;
   if (st != DPM_OK) {
     g_create_err = ctx->err.empty() ? "dpm_create failed" : ctx->err;
     free_ctx(ctx);
@@ -355,6 +353,13 @@ dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c,
 
 }  // extern "C"
 
+double mass_fixed_decode(const double* stats) {
+  unsigned long long lo, hi;
+  std::memcpy(&lo, stats, 8);
+  std::memcpy(&hi, stats + 8, 8);
+  return (double)(long long)hi + (double)lo * 5.42101086242752217004e-20;   // 2^-64
+}
+
 double decode_key(double slot) {
   unsigned long long k;
   std::memcpy(&k, &slot, 8);
@@ -416,7 +421,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   if (fork) {
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[0], s));
     DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->side_stream, ctx->ev_side[0], 0));
-    DPM_CUDA_TRY(ctx, lsq_residual(ctx, coef, gvec, 2, slot + 11, ctx->side_stream));
+    DPM_CUDA_TRY(ctx, lsq_residual(ctx, coef, gvec, 2, coef + 2 * ctx->K, slot + 11, ctx->side_stream));
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[1], ctx->side_stream));
   }
   // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
@@ -491,9 +496,9 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
   cudaStream_t s = as_stream(stream);
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
-  if (!ctx->scratch || ctx->scratch_bytes < (size_t)(4 * field + 2 * ngin + 2 * ng + 2 * ctx->K) * 8) {
+  if (!ctx->scratch || ctx->scratch_bytes < (size_t)(4 * field + 2 * ngin + 2 * ng + 4 * ctx->K) * 8) {
     if (ctx->scratch) cudaFree(ctx->scratch);
-    ctx->scratch_bytes = (size_t)(4 * field + 2 * ngin + 2 * ng + 2 * ctx->K) * 8;
+    ctx->scratch_bytes = (size_t)(4 * field + 2 * ngin + 2 * ng + 4 * ctx->K) * 8;   // + residual z (K x 2)
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->scratch, ctx->scratch_bytes));
     for (auto& g : ctx->pks_graphs) cudaGraphExecDestroy(g.exec);   // captured with the old scratch
     ctx->pks_graphs.clear();
@@ -583,7 +588,7 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
         dpm_step_log& Lg = log[done + i];
         Lg.t = ctx->t;
         Lg.dt = dt;
-        Lg.mass = L[4] * h * h * h;
+        Lg.mass = mass_fixed_decode(L + 4) * h * h * h;
         Lg.rho_max = decode_key(L[5]);
         Lg.rho_min = -decode_key(L[6]);
         Lg.c_min = -decode_key(L[7]);

@@ -82,6 +82,7 @@ struct dpm_ctx {
   double* R = nullptr;           // [K][K] col-major upper triangular
   double* colscale = nullptr;    // [K]
   double* Mlsq = nullptr;        // [K][n_gin] row-major: D R^{-1} Q^T (the LSQ apply operator)
+  double* RDinv = nullptr;       // [K][K] row-major: R D^{-1} (the per-step LSQ residual, lsq_residual)
   double bep_cond = 0;
   double* lsq_ws = nullptr;      // scratch
 
@@ -144,7 +145,6 @@ struct dpm_ctx {
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
   double* red = nullptr;         // device reduction slots
-  double* mass_part = nullptr;   // device [148*4] per-block mass partials + a zeroed ticket (restrict_kernel)
   double* red_host = nullptr;    // pinned
 };
 
@@ -232,7 +232,9 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s);
 cudaError_t lsq_apply(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int nrhs, int clamp,
                       cudaStream_t s, double* clampmax = nullptr);
 // ||B C - g|| / ||g|| (max over nrhs <= 2) -> out[0], from the ctx's factorisation (lsq.cu)
-cudaError_t lsq_residual(dpm_ctx* ctx, const double* coef, const double* g, int nrhs, double* out, cudaStream_t s);
+// zws: K x nrhs scratch
+cudaError_t lsq_residual(dpm_ctx* ctx, const double* coef, const double* g, int nrhs, double* zws, double* out,
+                         cudaStream_t s);
 
 // lsq.cu building blocks (octant DD)
 cudaError_t lsq_gram(const double* A, int64_t m, int K, double* G, cudaStream_t s);
@@ -264,6 +266,7 @@ __host__ __device__ inline int basis_ncomp(int b) { return b == DPM_BASIS_NEUMAN
 dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
                            int32_t device, dpm_ctx** out);
 double decode_key(double slot);   // order-preserving key of the reduction slots -> value
+double mass_fixed_decode(const double* stats);   // 128-bit fixed-point mass (stats[0] low, stats[8] high) -> value
 
 // pks.cu
 cudaError_t launch_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, cudaStream_t s);

@@ -303,27 +303,25 @@ __global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, 
 // The BEP least-squares residual of a step, max over the nrhs (<= 2) right-hand sides of
 // ||B C - g||_2 / ||g||_2.  With the factorisation B D = Q R (column equilibration D, CholeskyQR2) the
 // least-squares solution is C = D R^{-1} Q^T g, so ||B C - g||^2 = ||g||^2 - ||Q^T g||^2 with
-// Q^T g = R D^{-1} C: a K x K triangular product instead of another pass over B (the subtraction loses
-// the digits of the residual's smallness: ~1e-8 relative noise floor).  One block, fixed reduction order
-// (deterministic).
+// Q^T g = (R D^{-1}) C: a K x K GEMV with the operator formed once per factorisation (rdinv_kernel)
+// instead of another pass over B.  The subtraction costs the digits of the residual's own smallness
+// (~1e-8 relative noise floor).  The norms: one block, fixed reduction order (deterministic).
+__global__ void rdinv_kernel(const double* __restrict__ R, const double* __restrict__ D, int K, double* RD) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)K * K) return;
+  const int i = (int)(e / K), j = (int)(e % K);   // row-major (i, j) = R(i, j) / D(j), upper
+  RD[e] = j >= i ? R[(size_t)j * K + i] / D[j] : 0.0;
+}
+
 constexpr int RES_T = 256;
-__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ R, int K,
-                                                          const double* __restrict__ D,
-                                                          const double* __restrict__ coef,
+__global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ z, int K,
                                                           const double* __restrict__ g, int64_t m, int nrhs,
                                                           double* out) {
-  extern __shared__ double y[];   // nrhs x K: D^{-1} C
-  for (int i = threadIdx.x; i < nrhs * K; i += RES_T) y[i] = coef[i] / D[i % K];
-  __syncthreads();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};   // (||Q^T g||^2, ||g||^2) per right-hand side
-  for (int i = threadIdx.x; i < K; i += RES_T)
-    for (int q = 0; q < nrhs; ++q) {
-      double z = 0.0;
-      for (int jj = i; jj < K; ++jj) z = fma(R[(size_t)jj * K + i], y[q * K + jj], z);
-      acc[2 * q] = fma(z, z, acc[2 * q]);
-    }
-  for (int64_t i = threadIdx.x; i < m; i += RES_T)
-    for (int q = 0; q < nrhs; ++q) acc[2 * q + 1] = fma(g[q * m + i], g[q * m + i], acc[2 * q + 1]);
+  for (int q = 0; q < nrhs; ++q) {
+    for (int i = threadIdx.x; i < K; i += RES_T) acc[2 * q] = fma(z[q * K + i], z[q * K + i], acc[2 * q]);
+    for (int64_t i = threadIdx.x; i < m; i += RES_T) acc[2 * q + 1] = fma(g[q * m + i], g[q * m + i], acc[2 * q + 1]);
+  }
   __shared__ double red[4][RES_T / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int q = 0; q < 4; ++q) {
@@ -402,6 +400,11 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   double* Ri = R1;   // R1 is free after the trmm
   DPM_CUDA_TRY(ctx, lsq_rinv(ctx->R, K, Ri, s));
   DPM_CUDA_TRY(ctx, launch_gemm_tri<true>(ctx->Q, m, K, Ri, ctx->colscale, ctx->Mlsq, s));
+  // the residual operator R D^{-1} (row-major K x K) of the per-step LSQ residual (lsq_residual)
+  if (!ctx->RDinv) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->RDinv, (size_t)K * K * sizeof(double)));
+  DPM_COUNT_LAUNCH(1);
+  rdinv_kernel<<<(unsigned)(((size_t)K * K + 255) / 256), 256, 0, s>>>(ctx->R, ctx->colscale, K, ctx->RDinv);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
   int hfail = 0;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->bep_cond, dcond, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -841,15 +844,12 @@ cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, i
   return cudaGetLastError();
 }
 
-cudaError_t lsq_residual(dpm_ctx* ctx, const double* coef, const double* g, int nrhs, double* out, cudaStream_t s) {
-  if (nrhs < 1 || nrhs > 2) return cudaErrorInvalidValue;
+cudaError_t lsq_residual(dpm_ctx* ctx, const double* coef, const double* g, int nrhs, double* zws, double* out,
+                         cudaStream_t s) {
+  if (nrhs < 1 || nrhs > 2 || !ctx->RDinv) return cudaErrorInvalidValue;
   const int K = ctx->K;
-  const size_t smem = (size_t)nrhs * K * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(lsq_resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
+  launch_gemv(ctx->RDinv, K, K, coef, nrhs, zws, s);                      // z = R D^{-1} C = Q^T g
   DPM_COUNT_LAUNCH(1);
-  lsq_resid_kernel<<<1, RES_T, smem, s>>>(ctx->R, K, ctx->colscale, coef, g, ctx->counts[DPM_SET_GAMMA_IN], nrhs, out);
+  lsq_resid_kernel<<<1, RES_T, 0, s>>>(zws, K, g, ctx->counts[DPM_SET_GAMMA_IN], nrhs, out);
   return cudaGetLastError();
 }

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
   pdl_prologue();
   const long nn = (long)n * n * n;
   const double ih = 1.0 / h, idt = 1.0 / dt;
-  if (zero6 && blockIdx.x == 0 && threadIdx.x < 7) zero6[threadIdx.x] = 0.0;   // this step's statistics slot + clamp max
+  if (zero6 && blockIdx.x == 0 && threadIdx.x < 9) zero6[threadIdx.x] = 0.0;   // the step's statistics, clamp max, mass hi
   double cmx[3] = {0.0, 0.0, 0.0};
   for (long p = blockIdx.x * (long)blockDim.x + threadIdx.x; p < nn; p += (long)gridDim.x * blockDim.x) {
     if (backup) {   // the step's rollback copy of the state (speculative PKS graphs), fused with the read
@@ -324,10 +324,10 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) diag_kernel(const uint8_t* _
   }
 }
 
-// restriction to N+ ("on N+") + statistics: [mass_sum, rho_max, -rho_min, -c_min, nonfinite,
-// rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max)]
+// restriction to N+ ("on N+") + statistics: [mass_sum (fixed-point low word), rho_max, -rho_min,
+// -c_min, nonfinite, rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max), -, -, mass high word]
 __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
-                                double* c, double* stats, double* mpart) {
+                                double* c, double* stats) {
   pdl_prologue();
   const long nn = (long)n * n * n;
   double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY, rmaxm = -INFINITY;
@@ -352,7 +352,6 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
   }
   __shared__ double red[5][TB / 32];
   __shared__ int sbad;
-  __shared__ bool last_block;
   if (threadIdx.x == 0) sbad = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -371,10 +370,15 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     for (int q = 0; q < TB / 32; ++q) {
       s += red[0][q]; a = fmax(a, red[1][q]); b = fmin(b, red[2][q]); d = fmin(d, red[3][q]); am = fmax(am, red[4][q]);
     }
-    // the mass: per-block partials, summed by the last block in a fixed order (deterministic, R18)
-    mpart[blockIdx.x] = s;
-    __threadfence();
-    last_block = atomicAdd(reinterpret_cast<unsigned*>(mpart + 148 * 4), 1u) == gridDim.x - 1;
+    // the mass (R18) as an exact 128-bit fixed-point sum (2^-64 resolution): integer additions commute,
+    // so the total does not depend on the order of the blocks (deterministic); stats[0] = low word,
+    // stats[8] = high word (mass_fixed_decode)
+    const double fl = floor(s);
+    const unsigned long long lo = (unsigned long long)((s - fl) * 18446744073709551616.0);
+    const long long hi = (long long)fl;
+    unsigned long long* w = reinterpret_cast<unsigned long long*>(stats);
+    const unsigned long long old = atomicAdd(w, lo);
+    atomicAdd(w + 8, (unsigned long long)hi + (old + lo < old ? 1ull : 0ull));
     // max via bit patterns on the ordered transform
     auto key = [](double v) {
       unsigned long long x = (unsigned long long)__double_as_longlong(v);
@@ -385,21 +389,6 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     atomicMax((unsigned long long*)(stats + 3), key(-d));
     if (sbad) atomicAdd(stats + 4, 1.0);
     atomicMax((unsigned long long*)(stats + 5), key(am));
-  }
-  __syncthreads();
-  if (last_block) {   // thread t sums partials t, t + TB, ... then a fixed shuffle / warp-order tree
-    __threadfence();
-    double v = 0.0;
-    for (unsigned q = threadIdx.x; q < gridDim.x; q += TB) v += __ldcg(mpart + q);
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int q = 0; q < TB / 32; ++q) tot += red[0][q];
-      stats[0] = tot;
-      *reinterpret_cast<unsigned*>(mpart + 148 * 4) = 0u;
-    }
   }
 }
 
@@ -565,11 +554,10 @@ cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c,
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s, bool zeroed) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
-  if (!zeroed) {   // (zeroed: an earlier kernel of the step cleared the 6 slots)
-    cudaError_t e = cudaMemsetAsync(stats, 0, 6 * sizeof(double), s);
+  if (!zeroed) {   // (zeroed: an earlier kernel of the step cleared the 9 slots)
+    cudaError_t e = cudaMemsetAsync(stats, 0, 9 * sizeof(double), s);
     if (e != cudaSuccess) return e;
   }
   DPM_COUNT_LAUNCH(1);
-  return launch_pdl(restrict_kernel, grid_reduce(nn), TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats,
-                    ctx->mass_part);
+  return launch_pdl(restrict_kernel, grid_reduce(nn), TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats);
 }
