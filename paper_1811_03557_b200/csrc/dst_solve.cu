@@ -33,8 +33,6 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include <cooperative_groups.h>
-
 #include "dpm_internal.h"
 
 namespace {
@@ -769,134 +767,7 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
   for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
 }
 
-// The same plane pass split over a cluster of CS CTAs (PKS step): CTA k transforms the
-// z columns [k W, k W + W) (W = 64/CS) along y, the cluster exchanges the plane through distributed
-// shared memory so that CTA k holds the y-mode rows [k W, k W + W) for their exact z tridiagonal solves,
-// exchanges back, and CTA k inverse-transforms its columns.  CS times the CTAs of plane_small_kernel per
-// plane (a PKS step's 2-field solve has only 2n planes for 148 SMs); the same arithmetic per element.
-template <int CS>
-__global__ void __launch_bounds__(PS_THREADS) plane_small_cluster_kernel(double* __restrict__ u, int n,
-                                                                         const double* __restrict__ S_g,
-                                                                         const double* __restrict__ lam_g,
-                                                                         double inv_dt, double h2, double rscale) {
-  namespace cg = cooperative_groups;
-  pdl_prologue();
-  constexpr int W = PSN / CS, WP = W + 1;   // slice width, pitch of the column slice
-  extern __shared__ double psc[];
-  double* S = psc;                         // [64][PSP]
-  double* Pc = S + PSN * PSP;              // [64][WP]: z columns [kW, kW + W) of all y rows
-  double* Pr = Pc + PSN * WP;              // [W][PSP]: y-mode rows [kW, kW + W) of all z
-  double* lam = Pr + W * PSP;              // [64]
-  cg::cluster_group cluster = cg::this_cluster();
-  const int k = (int)cluster.block_rank();
-  const long plane = blockIdx.x / CS;      // field * n + a
-  const int a = (int)(plane % n), t = threadIdx.x;
-  double* g = u + (size_t)plane * n * n;
-  for (int e = t; e < PSN * PSN; e += PS_THREADS) {
-    const int r = e / PSN, c = e % PSN;
-    S[r * PSP + c] = (r < n && c < n) ? __ldg(S_g + r * n + c) : 0.0;
-  }
-  for (int e = t; e < PSN * W; e += PS_THREADS) {
-    const int r = e / W, c = e % W, z = k * W + c;
-    Pc[r * WP + c] = (r < n && z < n) ? g[(size_t)r * n + z] : 0.0;
-  }
-  for (int i = t; i < n; i += PS_THREADS) lam[i] = lam_g[i];
-  __syncthreads();
-  // forward y DST-I of the column slice: thread -> (output rows 4 rb .. 4 rb + 3, column cl)
-  auto ydst = [&]() {
-    constexpr int RB = PS_THREADS / W;     // row blocks over the 256 threads
-    constexpr int RPT = PSN / RB;          // output rows per thread
-    const int cl = t % W, rb = t / W;
-    double acc[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i] = 0.0;
-    if ((n & 1) == 0) {   // folded, as ps_apply: x_y ± x_{n-1-y} over y < n/2
-      for (int y = 0; y < n / 2; ++y) {
-        const double p1 = Pc[y * WP + cl], p2 = Pc[(n - 1 - y) * WP + cl];
-        const double ap = p1 + p2, am = p1 - p2;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) acc[i] = fma(S[y * PSP + RPT * rb + i], (i & 1) ? am : ap, acc[i]);
-      }
-    } else {
-      for (int y = 0; y < n; ++y) {
-        const double pv = Pc[y * WP + cl];
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) acc[i] = fma(S[y * PSP + RPT * rb + i], pv, acc[i]);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) Pc[(RPT * rb + i) * WP + cl] = acc[i];
-  };
-  static_assert(PS_THREADS % W == 0 && PSN % (PS_THREADS / W) == 0 && (PSN / (PS_THREADS / W)) % 2 == 0, "tiling");
-  ydst();
-  cluster.sync();                          // every column slice transformed
-  for (int e = t; e < W * PSN; e += PS_THREADS) {   // gather my rows from the owners of the columns
-    const int rl = e / PSN, z = e % PSN;
-    const double* src = cluster.map_shared_rank(Pc, z / W);
-    Pr[rl * PSP + z] = src[(k * W + rl) * WP + z % W];
-  }
-  cluster.sync();                          // all reads of the column slices done
-  {
-    const int w = t >> 5, lane = t & 31, nw = PS_THREADS >> 5;
-    for (int rl = w; rl < W; rl += nw) {
-      const int b = k * W + rl;
-      if (b >= n) continue;
-      const double hs = h2 * ((inv_dt + lam[a]) + lam[b]);
-      const double mu = 2.0 / ((2.0 + hs) + sqrt(hs * (hs + 4.0)));
-      const double id = 1.0 / (1.0 - ipow(mu, 2 * n + 2));
-      ps_tri_row(Pr + rl * PSP, n, mu, id, rscale);
-    }
-  }
-  __syncthreads();
-  for (int e = t; e < W * PSN; e += PS_THREADS) {   // scatter my rows back into the column slices
-    const int rl = e / PSN, z = e % PSN;
-    double* dst = cluster.map_shared_rank(Pc, z / W);
-    dst[(k * W + rl) * WP + z % W] = Pr[rl * PSP + z];
-  }
-  cluster.sync();
-  ydst();
-  for (int e = t; e < PSN * W; e += PS_THREADS) {
-    const int r = e / W, c = e % W, z = k * W + c;
-    if (r < n && z < n) g[(size_t)r * n + z] = Pc[r * WP + c];
-  }
-}
-
-template <int CS>
-cudaError_t launch_plane_small_cluster(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
-  const int n = p.n;
-  constexpr int W = PSN / CS;
-  const size_t smem = ((size_t)PSN * PSP + (size_t)PSN * (W + 1) + (size_t)W * PSP + PSN) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(plane_small_cluster_kernel<CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((long)nfields * n * CS));
-  cfg.blockDim = dim3(PS_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CS;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  const double sc = 2.0 / (n + 1);
-  DPM_COUNT_LAUNCH(1);
-  return cudaLaunchKernelEx(&cfg, plane_small_cluster_kernel<CS>, u, n, (const double*)p.sinmat,
-                            (const double*)p.lam, 1.0 / p.dt, p.h * p.h, sc * sc * p.h * p.h);
-}
-
 cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
-  static const int cs = [] {   // DPM_PLANE_SMALL_CS = 1 | 2 | 4 CTAs per plane
-    const char* v = getenv("DPM_PLANE_SMALL_CS");
-    return v ? atoi(v) : 4;
-  }();
-  if (cs == 2) return launch_plane_small_cluster<2>(p, u, nfields, s);
-  if (cs == 4) return launch_plane_small_cluster<4>(p, u, nfields, s);
   const int n = p.n;
   const size_t smem = (2 * (size_t)PSN * PSP + PSN) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(plane_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
