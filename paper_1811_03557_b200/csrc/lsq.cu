@@ -266,31 +266,37 @@ void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, d
     launch_pdl(lsq_gemv_kernel<1, 256>, K, 256, 0, s, M, m, K, g, nrhs, coef);
 }
 
-// u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x 8 column slices
-// per block, up to 2 right-hand sides per pass (E read once), coefficients staged in shared memory.
-__global__ void extend2_kernel(const double* __restrict__ E, int64_t ng, int K, const double* __restrict__ coef, int r0,
-                               int nr, int clamp, double* __restrict__ ug, double* __restrict__ clampmax) {
+// u_γ[r][g] = Σ_c E[c][g] coef[r][c] (optionally clamped at 0, R17): 32 γ points x SL column slices
+// per block (SL = 32: 1024 threads, ~K/32 independent coalesced loads per thread in flight — the E stream
+// (|γ| x K, 19 MB at cfg3) is bandwidth-, not FMA-bound), up to 2 right-hand sides per pass (E read
+// once), coefficients staged in shared memory.
+template <int SL>
+__global__ void __launch_bounds__(32 * SL) extend2_kernel(const double* __restrict__ E, int64_t ng, int K,
+                                                         const double* __restrict__ coef, int r0, int nr, int clamp,
+                                                         double* __restrict__ ug, double* __restrict__ clampmax) {
   pdl_prologue();
-  extern __shared__ double sc[];   // nr * K coefficients + 2 x 8 x 32 partial sums
+  extern __shared__ double sc[];   // nr * K coefficients + 2 x SL x 32 partial sums
   for (int i = threadIdx.x; i < nr * K; i += blockDim.x) sc[i] = coef[(size_t)r0 * K + i];
   double* part = sc + nr * K;
   __syncthreads();
   const int gl = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int64_t g = (int64_t)blockIdx.x * 32 + gl;
   double s0 = 0.0, s1 = 0.0;
-  if (g < ng)
-    for (int c = sl; c < K; c += 8) {
-      const double e = E[(size_t)c * ng + g];
+  if (g < ng) {
+#pragma unroll 4
+    for (int c = sl; c < K; c += SL) {
+      const double e = __ldg(E + (size_t)c * ng + g);
       s0 = fma(e, sc[c], s0);
       if (nr > 1) s1 = fma(e, sc[K + c], s1);
     }
+  }
   part[sl * 32 + gl] = s0;
-  part[256 + sl * 32 + gl] = s1;
+  part[SL * 32 + sl * 32 + gl] = s1;
   __syncthreads();
   double neg = 0.0;   // how far below 0 the reconstructed density went (the clamp magnitude, R17)
   if (sl < nr && g < ng) {
-    double t = part[sl * 256 + gl];
-    for (int q = 1; q < 8; ++q) t += part[sl * 256 + q * 32 + gl];
+    double t = part[sl * SL * 32 + gl];
+    for (int q = 1; q < SL; ++q) t += part[sl * SL * 32 + q * 32 + gl];
     ug[(size_t)(r0 + sl) * ng + g] = clamp ? fmax(t, 0.0) : t;
     neg = fmax(-t, 0.0);
   }
@@ -837,9 +843,20 @@ cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, i
                        cudaStream_t s, double* clampmax) {
   for (int r = 0; r < nrhs; r += 2) {
     const int nr = std::min(2, nrhs - r);
-    const size_t smem = (size_t)(nr * K + 512) * sizeof(double);
     DPM_COUNT_LAUNCH(1);
-    launch_pdl(extend2_kernel, (unsigned)((ng + 31) / 32), 256, smem, s, E, ng, K, coef, r, nr, clamp, ug, clampmax);
+    if (K >= 64) {
+      const size_t smem = (size_t)(nr * K + 2 * 32 * 32) * sizeof(double);
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(extend2_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      launch_pdl(extend2_kernel<32>, (unsigned)((ng + 31) / 32), 1024, smem, s, E, ng, K, coef, r, nr, clamp, ug,
+                 clampmax);
+    } else {
+      const size_t smem = (size_t)(nr * K + 2 * 8 * 32) * sizeof(double);
+      launch_pdl(extend2_kernel<8>, (unsigned)((ng + 31) / 32), 256, smem, s, E, ng, K, coef, r, nr, clamp, ug,
+                 clampmax);
+    }
   }
   return cudaGetLastError();
 }
