@@ -350,6 +350,40 @@ def bench_test_b(N=127, harmonics=150):
     return res
 
 
+def bench_rebuild_every_step(api, torch, name="cfg3", steps=20):
+    """NEXT-1: the Step-4b regime forced on every step — each step
+    runs at a new Δt (fixed-dt rule at Δt_i = Δt_0 (1 - 1e-3 i)), so the BEP is rebuilt every step
+    (K = 2 (L+1)^2 AP solves + the CholeskyQR2 factorisation) before the step itself; steps/s of the
+    whole loop, CUDA events."""
+    cfg = get_config(name)
+    ctx = api.DPM.from_config(cfg)
+    n = cfg.n
+    rho = torch.zeros((n, n, n), dtype=torch.float64, device="cuda")
+    c = torch.zeros_like(rho)
+    ctx.pks_init(rho, c, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+    dt0 = ctx.pks_step(rho, c, 1, chi=cfg.chi, dt_cap=cfg.dt)[0]["dt"]
+    ctx.pks_step(rho, c, 2, chi=cfg.chi, dt_cap=dt0 * 0.999, dt_rule=1)   # warm-up (graph capture)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rebuilt = 0
+    e0.record()
+    for i in range(steps):
+        rebuilt += ctx.pks_step(rho, c, 1, chi=cfg.chi, dt_cap=dt0 * (1.0 - 1e-3 * (i + 2)), dt_rule=1)[0]["rebuilt"]
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    return {"config": name, "K": ctx.K, "n": n, "steps": steps, "rebuilds": rebuilt, "ms_per_step": ms,
+            "steps_per_s": 1e3 / ms, "what": "BEP rebuilt on every step (Step 4b), then the step"}
+
+
+def bench_test_a_dd():
+    """NEXT-3: the paper's two-subdomain DD (Case 1) — the DD columns of Tables
+    1-3 on the paper's N1/N2 meshes against the N = 516 SD reference, and Table 6's R_S on B200 (context)."""
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+    import test_a_dd
+    return {"tables": test_a_dd.run_tables(), "rs": test_a_dd.run_rs(sizes=(127,))}
+
+
 def bench_test_a():
     """NEXT-2: the paper's Test A convergence of the max density (Table 3)
     on the paper's meshes N = 36/68/132/260 against its N = 516 reference run, ρ̄0 as cell averages (R36):
@@ -613,8 +647,10 @@ def main():
                        "cfg3": bench_pks(api, torch, "cfg3", hbm_peak=hbm_peak)}
         line["cfg1"] = bench_cfg1(api, torch)
         line["bep_rebuild_cfg4"] = bench_bep(api, torch)
+        line["pks_rebuild_every_step"] = bench_rebuild_every_step(api, torch)
         line["test_b"] = bench_test_b()
         line["test_a"] = bench_test_a()
+        line["test_a_dd"] = bench_test_a_dd()
 
     if world > 1:
         # C1: one BEP build of the cfg4 geometry with its K = 578 columns sharded over the
