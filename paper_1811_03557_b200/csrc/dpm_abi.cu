@@ -91,6 +91,14 @@ dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32
   const bool zonal = basis_zonal(basis);
   if (lmax < 0 || lmax > (zonal ? DPM_MAX_ZONAL_L : 40)) { g_create_err = "lmax out of range"; return DPM_ERR_INVALID; }
   if (cudaSetDevice(device) != cudaSuccess) { g_create_err = "cudaSetDevice failed"; return DPM_ERR_CUDA; }
+  {   // the stream-ordered workspaces (lsq_gram's split-K slices) keep their memory in the device's
+      // default pool between calls instead of returning it to the driver at every synchronisation
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   dpm_ctx* ctx = new (std::nothrow) dpm_ctx();
   if (!ctx) return DPM_ERR_OOM;
   ctx->device = device;
