@@ -103,22 +103,27 @@ cudaError_t bepf_prepare(dpm_ctx* ctx) {
 
 
 // ---- sparse-in forward x pass and γ-out inverse x pass (round 2) ----------------------------------
-// Both work on tiles of 16 consecutive x-lines (a warp per tile; the x-pass tile of dst128f_kernel) and
-// use the exact DST-I sine table T[t] = sin(π t/129) (t = (j k) mod 258) in shared memory.
+// Both work on tiles of consecutive x-lines (a warp per tile) and use the exact DST-I sine table
+// T[t] = sin(π t/129), t = (j k) mod 258, in shared memory.
 constexpr int NX = 128, NXX = NX * NX, TPL = 16, SP_WARPS = 8, OUTP = NX + 1;   // staging [line][k], odd pitch
+constexpr int TPLI = 8, INV_WARPS = 12;                                        // inverse: 8-line tiles, 2 buffers
 
-// X_k = Σ_{j in band(line)} x_j sin(π j k/129) for every line of the tile: only the band values of the
-// line (compact, x-line-major, tab[L] = {128-bit x mask, start}) are read and multiplied, lane = outputs
-// k = lane + 1 + 32 q (q < 4); a tile with no band point is written as zeros without arithmetic.  The
-// outputs are staged in shared memory and stored as coalesced 128-byte row segments (same layout and
-// scale as the dense x pass).
+// X_k = Σ_{j in band(line)} x_j sin(π j k/129) for every line of a 16-line tile: only the band values of
+// the line (compact, x-line-major, tab[L] = {128-bit x mask, start}) are read and multiplied, lane = outputs
+// k = lane + 1 + 32 q (q < 4), the angle index (j k) mod 258 from per-lane shared tables (no integer
+// division); a tile with no band point is written as zeros without arithmetic.  The outputs are staged in
+// shared memory and stored as coalesced 128-byte row segments (same layout and scale as the dense x pass).
 __global__ void __launch_bounds__(32 * SP_WARPS) bep_xfwd_sparse_kernel(double* __restrict__ out, int nfields,
                                                                        const uint32_t* __restrict__ tab,
                                                                        const double* __restrict__ vals, int64_t ldv,
                                                                        const double* __restrict__ sintab) {
   __shared__ double T[258];
-  extern __shared__ double spo[];   // [warp][16 lines][OUTP]
+  __shared__ uint16_t JK[NX + 1][32];   // (j (lane + 1)) mod 258
+  __shared__ uint16_t ST[NX + 1];       // (32 j) mod 258
+  extern __shared__ double spo[];       // [warp][16 lines][OUTP]
   for (int i = threadIdx.x; i < 258; i += blockDim.x) T[i] = sintab[i];
+  for (int i = threadIdx.x; i < (NX + 1) * 32; i += blockDim.x) JK[i >> 5][i & 31] = (uint16_t)(((i >> 5) * ((i & 31) + 1)) % 258);
+  for (int i = threadIdx.x; i <= NX; i += blockDim.x) ST[i] = (uint16_t)((32 * i) % 258);
   __syncthreads();
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   double* O = spo + (size_t)wl * TPL * OUTP;
@@ -139,15 +144,14 @@ __global__ void __launch_bounds__(32 * SP_WARPS) bep_xfwd_sparse_kernel(double* 
     }
     const unsigned busy = __ballot_sync(0xffffffffu, m > 0);
     if (!busy) {   // no band point on the 16 lines: the transform is zero
-      for (int r = lane >> 4; r < NX; r += 2) fo[(size_t)r * NXX + (lane & 15)] = 0.0;
+      for (int r = lane >> 4; r < NX; r += 2) __stcg(fo + (size_t)r * NXX + (lane & 15), 0.0);
       continue;
     }
     const double* fv = vals + (size_t)f * ldv;
     for (int l = 0; l < TPL; ++l) {
-      const int ml = __shfl_sync(0xffffffffu, m, l);
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      if (ml) {
-        const int sl = __shfl_sync(0xffffffffu, start, l);
+      if ((busy >> l) & 1u) {
+        const int ml = __shfl_sync(0xffffffffu, m, l), sl = __shfl_sync(0xffffffffu, start, l);
         uint32_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) w[q] = __shfl_sync(0xffffffffu, mw[q], l);
@@ -166,8 +170,8 @@ __global__ void __launch_bounds__(32 * SP_WARPS) bep_xfwd_sparse_kernel(double* 
           for (int s = 0; s < cnt; ++s) {
             const int jj = __shfl_sync(0xffffffffu, jl, s);
             const double vv = __shfl_sync(0xffffffffu, vl, s);
-            const int st = (32 * jj) % 258;
-            int tt = (jj * (lane + 1)) % 258;
+            const int st = ST[jj];
+            int tt = JK[jj][lane];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               acc[q] = fma(vv, T[tt], acc[q]);
@@ -186,62 +190,83 @@ __global__ void __launch_bounds__(32 * SP_WARPS) bep_xfwd_sparse_kernel(double* 
   }
 }
 
-// γ-out inverse x pass: for the γ points of the tile's 16 lines only, u(x_k) = Σ_j v_j sin(π j k/129)
-// (k = x + 1) over the line's 128 transformed values, staged in shared memory; PgE = u and
-// B = E_in - u are written directly (replaces the dense inverse pass and the γ gather).  Tiles with no
-// γ point are not read.
-__global__ void __launch_bounds__(32 * SP_WARPS) bep_xinv_gamma_kernel(const double* __restrict__ in, int nfields,
-                                                                      const int32_t* __restrict__ gstart,
-                                                                      const int32_t* __restrict__ gent,
-                                                                      const int32_t* __restrict__ ginof,
-                                                                      const double* __restrict__ sintab,
-                                                                      const double* __restrict__ E, int64_t ng,
-                                                                      int64_t ngin, int c0col, double* PgE,
-                                                                      double* B) {
+// γ-out inverse x pass: for the γ points of a tile's 8 lines only, u(x_k) = Σ_j v_j sin(π j k/129)
+// (k = x + 1) over the line's 128 transformed values staged in shared memory (two buffers: the next
+// non-empty tile is fetched with cp.async under this one's sums); PgE = u and B = E_in - u are written
+// directly (replaces the dense inverse pass and the γ gather).  Tiles with no γ point are not read.
+__device__ __forceinline__ int next_busy_tile(int t, int nw, int ntiles, const int32_t* __restrict__ gstart) {
+  constexpr int TPF = NXX / TPLI;
+  for (; t < ntiles; t += nw) {
+    const int c0 = (t % TPF) * TPLI;
+    if (__ldg(gstart + c0) != __ldg(gstart + c0 + TPLI)) return t;
+  }
+  return ntiles;
+}
+
+__device__ __forceinline__ void load_tile8(double* buf, const double* fi, int lane) {
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(buf);
+  const int cc = 2 * (lane & 3);
+#pragma unroll 4
+  for (int r = lane >> 2; r < NX; r += 8)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + 8u * (unsigned)(r * TPLI + cc)),
+                 "l"(fi + (size_t)r * NXX + cc));
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+__global__ void __launch_bounds__(32 * INV_WARPS) bep_xinv_gamma_kernel(const double* __restrict__ in, int nfields,
+                                                                       const int32_t* __restrict__ gstart,
+                                                                       const int32_t* __restrict__ gent,
+                                                                       const int32_t* __restrict__ ginof,
+                                                                       const double* __restrict__ sintab,
+                                                                       const double* __restrict__ E, int64_t ng,
+                                                                       int64_t ngin, int c0col, double* PgE,
+                                                                       double* B) {
   __shared__ double T[258];
-  extern __shared__ double spi[];   // [warp][128][16]
+  extern __shared__ double spi[];   // [warp][2][128][8]
   for (int i = threadIdx.x; i < 258; i += blockDim.x) T[i] = sintab[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  double* R = spi + (size_t)wl * NX * TPL;
-  const unsigned sb = (unsigned)__cvta_generic_to_shared(R);
+  double* R0 = spi + (size_t)wl * 2 * NX * TPLI;
   const size_t field = (size_t)NXX * NX;
-  constexpr int TPF = NXX / TPL;
+  constexpr int TPF = NXX / TPLI;
   const int ntiles = nfields * TPF;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
-  for (int t = gw; t < ntiles; t += nw) {
-    const int f = t / TPF, c0 = (t - f * TPF) * TPL;
-    const int e0 = __ldg(gstart + c0), e1 = __ldg(gstart + c0 + TPL);
-    if (e0 == e1) continue;
-    const double* fi = in + (size_t)f * field + c0;
-    const int cc = 2 * (lane & 7);
-    for (int r = lane >> 3; r < NX; r += 4)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + 8u * (unsigned)(r * TPL + cc)),
-                   "l"(fi + (size_t)r * NXX + cc));
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::);
+  int t = next_busy_tile(gw, nw, ntiles, gstart);
+  if (t < ntiles) load_tile8(R0, in + (size_t)(t / TPF) * field + (t % TPF) * TPLI, lane);
+  for (int buf = 0; t < ntiles; buf ^= 1) {
+    const int f = t / TPF, c0 = (t - f * TPF) * TPLI;
+    const int e0 = __ldg(gstart + c0), e1 = __ldg(gstart + c0 + TPLI);
+    const int tn = next_busy_tile(t + nw, nw, ntiles, gstart);
+    double* R = R0 + buf * NX * TPLI;
+    if (tn < ntiles) {
+      load_tile8(R0 + (buf ^ 1) * NX * TPLI, in + (size_t)(tn / TPF) * field + (tn % TPF) * TPLI, lane);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
     __syncwarp();
     const int c = c0col + f;
     for (int e = e0 + lane; e < e1; e += 32) {
       const int ent = __ldg(gent + e);
-      const int kk = (ent & 127) + 1, l = (ent >> 7) & 15, g = ent >> 11;
+      const int kk = (ent & 127) + 1, l = (ent >> 7) & 7, g = ent >> 11;
       double a0 = 0.0, a1 = 0.0;
       int tt = 0;
 #pragma unroll 8
       for (int j = 0; j < NX; j += 2) {
         tt += kk;
         tt -= tt >= 258 ? 258 : 0;
-        a0 = fma(R[j * TPL + l], T[tt], a0);
+        a0 = fma(R[j * TPLI + l], T[tt], a0);
         tt += kk;
         tt -= tt >= 258 ? 258 : 0;
-        a1 = fma(R[(j + 1) * TPL + l], T[tt], a1);
+        a1 = fma(R[(j + 1) * TPLI + l], T[tt], a1);
       }
       const double u = a0 + a1;
       if (PgE) PgE[(size_t)f * ng + g] = u;
       const int gi = __ldg(ginof + g);
       if (B && gi >= 0) B[(size_t)f * ngin + gi] = __ldg(E + (size_t)c * ng + g) - u;
     }
-    __syncwarp();
+    __syncwarp();   // this buffer is refilled two tiles on
+    t = tn;
   }
 }
 
@@ -307,12 +332,12 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
   // (3) fused plane pass
   if ((e = dst_solve_middle(ctx->plan, ctx->work, nc, s)) != cudaSuccess) return e;
   // (4) inverse x DST-I at the γ points only, writing PgE and B = E_in - Tr_γin u directly
-  const size_t smem_i = (size_t)SP_WARPS * NX * TPL * sizeof(double);
+  const size_t smem_i = (size_t)INV_WARPS * 2 * NX * TPLI * sizeof(double);
   if ((e = cudaFuncSetAttribute(bep_xinv_gamma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_i)) !=
       cudaSuccess)
     return e;
   DPM_COUNT_LAUNCH(1);
-  bep_xinv_gamma_kernel<<<grid, 32 * SP_WARPS, smem_i, s>>>(ctx->work, nc, ctx->bepf_gstart, ctx->bepf_gent,
+  bep_xinv_gamma_kernel<<<sms_count(), 32 * INV_WARPS, smem_i, s>>>(ctx->work, nc, ctx->bepf_gstart, ctx->bepf_gent,
                                                               ctx->bepf_ginof, ctx->bepf_sin, ctx->E, ng,
                                                               ctx->counts[DPM_SET_GAMMA_IN], c0, PgE, B);
   return cudaGetLastError();
