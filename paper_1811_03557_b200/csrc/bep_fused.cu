@@ -105,10 +105,10 @@ cudaError_t bepf_prepare(dpm_ctx* ctx) {
 // ---- sparse-in forward x pass and γ-out inverse x pass (round 2) ----------------------------------
 // Both work on tiles of consecutive x-lines (a warp per tile) and use the exact DST-I sine table
 // T[t] = sin(π t/129), t = (j k) mod 258, in shared memory.
-constexpr int NX = 128, NXX = NX * NX, TPL = 16, SP_WARPS = 8, OUTP = NX + 1;   // staging [line][k], odd pitch
-constexpr int TPLI = 8, INV_WARPS = 12;                                        // inverse: 8-line tiles, 2 buffers
+constexpr int NX = 128, NXX = NX * NX, TPL = 8, SP_WARPS = 12, OUTP = NX + 1;   // staging [line][k], odd pitch
+constexpr int TPLI = 8, INV_WARPS = 24;                                        // inverse: 8-line tiles
 
-// X_k = Σ_{j in band(line)} x_j sin(π j k/129) for every line of a 16-line tile: only the band values of
+// X_k = Σ_{j in band(line)} x_j sin(π j k/129) for every line of an 8-line tile: only the band values of
 // the line (compact, x-line-major, tab[L] = {128-bit x mask, start}) are read and multiplied, lane = outputs
 // k = lane + 1 + 32 q (q < 4), the angle index (j k) mod 258 from per-lane shared tables (no integer
 // division); a tile with no band point is written as zeros without arithmetic.  The outputs are staged in
@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(32 * SP_WARPS) bep_xfwd_sparse_kernel(double* 
       m = __popc(mw[0]) + __popc(mw[1]) + __popc(mw[2]) + __popc(mw[3]);
     }
     const unsigned busy = __ballot_sync(0xffffffffu, m > 0);
-    if (!busy) {   // no band point on the 16 lines: the transform is zero
-      for (int r = lane >> 4; r < NX; r += 2) __stcg(fo + (size_t)r * NXX + (lane & 15), 0.0);
+    if (!busy) {   // no band point on the tile's lines: the transform is zero
+      for (int r = lane >> 3; r < NX; r += 4) __stcg(fo + (size_t)r * NXX + (lane & 7), 0.0);
       continue;
     }
     const double* fv = vals + (size_t)f * ldv;
@@ -185,34 +185,16 @@ __global__ void __launch_bounds__(32 * SP_WARPS) bep_xfwd_sparse_kernel(double* 
       for (int q = 0; q < 4; ++q) O[l * OUTP + lane + 32 * q] = acc[q];
     }
     __syncwarp();
-    for (int r = lane >> 4; r < NX; r += 2) __stcg(fo + (size_t)r * NXX + (lane & 15), O[(lane & 15) * OUTP + r]);
+    for (int r = lane >> 3; r < NX; r += 4) __stcg(fo + (size_t)r * NXX + (lane & 7), O[(lane & 7) * OUTP + r]);
     __syncwarp();
   }
 }
 
 // γ-out inverse x pass: for the γ points of a tile's 8 lines only, u(x_k) = Σ_j v_j sin(π j k/129)
-// (k = x + 1) over the line's 128 transformed values staged in shared memory (two buffers: the next
-// non-empty tile is fetched with cp.async under this one's sums); PgE = u and B = E_in - u are written
-// directly (replaces the dense inverse pass and the γ gather).  Tiles with no γ point are not read.
-__device__ __forceinline__ int next_busy_tile(int t, int nw, int ntiles, const int32_t* __restrict__ gstart) {
-  constexpr int TPF = NXX / TPLI;
-  for (; t < ntiles; t += nw) {
-    const int c0 = (t % TPF) * TPLI;
-    if (__ldg(gstart + c0) != __ldg(gstart + c0 + TPLI)) return t;
-  }
-  return ntiles;
-}
-
-__device__ __forceinline__ void load_tile8(double* buf, const double* fi, int lane) {
-  const unsigned sb = (unsigned)__cvta_generic_to_shared(buf);
-  const int cc = 2 * (lane & 3);
-#pragma unroll 4
-  for (int r = lane >> 2; r < NX; r += 8)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + 8u * (unsigned)(r * TPLI + cc)),
-                 "l"(fi + (size_t)r * NXX + cc));
-  asm volatile("cp.async.commit_group;\n" ::);
-}
-
+// (k = x + 1) over the line's 128 transformed values staged in shared memory; four lanes per γ point
+// (32 terms each, combined by shuffles); PgE = u and B = E_in - u are written directly (replaces the
+// dense inverse pass and the γ gather).  Tiles with no γ point are not read.  24 warps per SM hide the
+// tile loads.
 __global__ void __launch_bounds__(32 * INV_WARPS) bep_xinv_gamma_kernel(const double* __restrict__ in, int nfields,
                                                                        const int32_t* __restrict__ gstart,
                                                                        const int32_t* __restrict__ gent,
@@ -222,51 +204,60 @@ __global__ void __launch_bounds__(32 * INV_WARPS) bep_xinv_gamma_kernel(const do
                                                                        int64_t ngin, int c0col, double* PgE,
                                                                        double* B) {
   __shared__ double T[258];
-  extern __shared__ double spi[];   // [warp][2][128][8]
+  extern __shared__ double spi[];   // [warp][128][8]
   for (int i = threadIdx.x; i < 258; i += blockDim.x) T[i] = sintab[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  double* R0 = spi + (size_t)wl * 2 * NX * TPLI;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, sub = lane & 3;
+  double* R = spi + (size_t)wl * NX * TPLI;
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(R);
   const size_t field = (size_t)NXX * NX;
   constexpr int TPF = NXX / TPLI;
   const int ntiles = nfields * TPF;
   const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), nw = (int)((gridDim.x * blockDim.x) >> 5);
-  int t = next_busy_tile(gw, nw, ntiles, gstart);
-  if (t < ntiles) load_tile8(R0, in + (size_t)(t / TPF) * field + (t % TPF) * TPLI, lane);
-  for (int buf = 0; t < ntiles; buf ^= 1) {
+  for (int t = gw; t < ntiles; t += nw) {
     const int f = t / TPF, c0 = (t - f * TPF) * TPLI;
     const int e0 = __ldg(gstart + c0), e1 = __ldg(gstart + c0 + TPLI);
-    const int tn = next_busy_tile(t + nw, nw, ntiles, gstart);
-    double* R = R0 + buf * NX * TPLI;
-    if (tn < ntiles) {
-      load_tile8(R0 + (buf ^ 1) * NX * TPLI, in + (size_t)(tn / TPF) * field + (tn % TPF) * TPLI, lane);
-      asm volatile("cp.async.wait_group 1;\n" ::);
-    } else {
-      asm volatile("cp.async.wait_group 0;\n" ::);
-    }
+    if (e0 == e1) continue;
+    const double* fi = in + (size_t)f * field + c0;
+    const int cc = 2 * (lane & 3);
+#pragma unroll 4
+    for (int r = lane >> 2; r < NX; r += 8)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb + 8u * (unsigned)(r * TPLI + cc)),
+                   "l"(fi + (size_t)r * NXX + cc));
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncwarp();
     const int c = c0col + f;
-    for (int e = e0 + lane; e < e1; e += 32) {
-      const int ent = __ldg(gent + e);
-      const int kk = (ent & 127) + 1, l = (ent >> 7) & 7, g = ent >> 11;
+    for (int eb = e0; eb < e1; eb += 8) {   // 8 γ points per pass, 4 lanes each
+      const int e = eb + (lane >> 2);
+      const bool ok = e < e1;
+      int ent = ok ? __ldg(gent + e) : 0;
+      const int kk = (ent & 127) + 1, l = (ent >> 7) & 7;
+      // this lane's terms j = 32 sub .. 32 sub + 31 (1-based j + 1), angle index (j k) mod 258
+      unsigned a = (unsigned)((32 * sub + 1) * kk);
+      int tt = (int)(a - 258u * __umulhi(a, 16646912u));   // a mod 258 (a < 2^14)
+      const double* Rl = R + 32 * sub * TPLI + l;
       double a0 = 0.0, a1 = 0.0;
-      int tt = 0;
 #pragma unroll 8
-      for (int j = 0; j < NX; j += 2) {
+      for (int j = 0; j < 32; j += 2) {
+        a0 = fma(Rl[j * TPLI], T[tt], a0);
         tt += kk;
         tt -= tt >= 258 ? 258 : 0;
-        a0 = fma(R[j * TPLI + l], T[tt], a0);
+        a1 = fma(Rl[(j + 1) * TPLI], T[tt], a1);
         tt += kk;
         tt -= tt >= 258 ? 258 : 0;
-        a1 = fma(R[(j + 1) * TPLI + l], T[tt], a1);
       }
-      const double u = a0 + a1;
-      if (PgE) PgE[(size_t)f * ng + g] = u;
-      const int gi = __ldg(ginof + g);
-      if (B && gi >= 0) B[(size_t)f * ngin + gi] = __ldg(E + (size_t)c * ng + g) - u;
+      double u = a0 + a1;
+      u += __shfl_xor_sync(0xffffffffu, u, 1);
+      u += __shfl_xor_sync(0xffffffffu, u, 2);
+      if (ok && sub == 0) {
+        const int g = ent >> 11;
+        if (PgE) PgE[(size_t)f * ng + g] = u;
+        const int gi = __ldg(ginof + g);
+        if (B && gi >= 0) B[(size_t)f * ngin + gi] = __ldg(E + (size_t)c * ng + g) - u;
+      }
     }
-    __syncwarp();   // this buffer is refilled two tiles on
-    t = tn;
+    __syncwarp();
   }
 }
 
@@ -332,7 +323,7 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
   // (3) fused plane pass
   if ((e = dst_solve_middle(ctx->plan, ctx->work, nc, s)) != cudaSuccess) return e;
   // (4) inverse x DST-I at the γ points only, writing PgE and B = E_in - Tr_γin u directly
-  const size_t smem_i = (size_t)INV_WARPS * 2 * NX * TPLI * sizeof(double);
+  const size_t smem_i = (size_t)INV_WARPS * NX * TPLI * sizeof(double);
   if ((e = cudaFuncSetAttribute(bep_xinv_gamma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_i)) !=
       cudaSuccess)
     return e;
