@@ -141,10 +141,6 @@ struct dpm_ctx {
   int32_t* bepf_bpos = nullptr;      // [n_band] line-major position of band point b
   double* bepf_qb = nullptr;         // [cols][n_band] band values of the potential RHS (line-major)
   int bepf_cols = 0;
-  int32_t* bepf_gstart = nullptr;    // [n^2 + 1] γ points per x-line (CSR start), lines in order
-  int32_t* bepf_gent = nullptr;      // [n_gamma] (γ position << 11) | (line mod 16) << 7 | x, by line then x
-  int32_t* bepf_ginof = nullptr;     // [n_gamma] γ_in index of a γ point, -1 for γ_ex
-  double* bepf_sin = nullptr;        // [258] sin(π t / 129), t = 0..257 (exact argument)
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
