@@ -499,6 +499,7 @@ extern "C" {
 
 dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius, int32_t lmax_cap, int32_t deg_if,
                              double dt, int32_t device, dpm_ctx** out) {
+  DPM_NVTX();
   if (out) *out = nullptr;
   if (!grid || !out || octant < 0 || octant > 7 || !(radius > 0) || lmax_cap < 0 || lmax_cap > 40 || deg_if < 0 ||
       deg_if > 30 || !(grid->lo < 0 && grid->hi > radius))
@@ -535,6 +536,7 @@ dpm_status dpm_create_octant(const dpm_grid* grid, int32_t octant, double radius
 
 dpm_status dpm_create_dd1(const dpm_grid* grid, int32_t sub, double r1, double r2, int32_t mz, int32_t mg, double dt,
                           int32_t device, dpm_ctx** out) {
+  DPM_NVTX();
   if (out) *out = nullptr;
   if (!grid || !out || (sub != 0 && sub != 1) || !(r1 > 0) || !(r2 > r1) || mz < 0 || mg < 0 ||
       mz > DPM_MAX_ZONAL_L || mg > DPM_MAX_ZONAL_L)
@@ -579,6 +581,7 @@ dpm_status dpm_create_dd1(const dpm_grid* grid, int32_t sub, double r1, double r
 }
 
 dpm_status dpm_dd_info(const dpm_ctx* ctx, int64_t* n_rows, int32_t* K) {
+  DPM_NVTX();
   if (!ctx || !ctx->dd || !n_rows || !K) return DPM_ERR_INVALID;
   *n_rows = ctx->n_rows;
   *K = ctx->K;
@@ -586,6 +589,7 @@ dpm_status dpm_dd_info(const dpm_ctx* ctx, int64_t* n_rows, int32_t* K) {
 }
 
 dpm_status dpm_dd_copy_assign(const dpm_ctx* ctx, uint8_t* host_bits) {
+  DPM_NVTX();
   if (!ctx || !ctx->dd || !host_bits) return DPM_ERR_INVALID;
   cudaSetDevice(ctx->device);
   dpm_ctx* c = const_cast<dpm_ctx*>(ctx);
@@ -594,6 +598,7 @@ dpm_status dpm_dd_copy_assign(const dpm_ctx* ctx, uint8_t* host_bits) {
 }
 
 dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if ((st = dd_alloc(ctx)) != DPM_OK) return st;
@@ -630,6 +635,7 @@ dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream) {
 }
 
 dpm_status dpm_dd_colnorm2(dpm_ctx* ctx, double* nrm2, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!nrm2 || !ctx->dd_B) return DPM_ERR_STATE;
@@ -640,6 +646,7 @@ dpm_status dpm_dd_colnorm2(dpm_ctx* ctx, double* nrm2, void* stream) {
 }
 
 dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, double* G, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!G || !ctx->dd_B || (pass != 1 && pass != 2) || (pass == 1 && !nrm2_sum)) return DPM_ERR_INVALID;
@@ -659,6 +666,7 @@ dpm_status dpm_dd_gram(dpm_ctx* ctx, int32_t pass, const double* nrm2_sum, doubl
 
 // dd_R layout: R1 | R2 | R = R2 R1 | W = Rp^{-1} of the last pass | W2 = R^{-1} | fail flag
 dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!G_sum || (pass != 1 && pass != 2)) return DPM_ERR_INVALID;
@@ -694,6 +702,7 @@ dpm_status dpm_dd_chol(dpm_ctx* ctx, int32_t pass, const double* G_sum, void* st
 // The same pass from an octant already factored with the same summed Gram on this device: the
 // K x K factors and inverses are copied, only the octant's own GEMMs run.
 dpm_status dpm_dd_chol_copy(dpm_ctx* ctx, int32_t pass, const dpm_ctx* src, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!src || !src->dd || !src->dd_R || src->K != ctx->K || src->device != ctx->device || (pass != 1 && pass != 2))
@@ -724,6 +733,7 @@ dpm_status dpm_dd_chol_copy(dpm_ctx* ctx, int32_t pass, const dpm_ctx* src, void
 }
 
 dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!rho || !c || !ic) return DPM_ERR_INVALID;
@@ -741,6 +751,7 @@ dpm_status dpm_dd_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_i
 }
 
 dpm_status dpm_dd_cfl(dpm_ctx* ctx, const double* c, double chi, double* cfl_dt, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!c || !(chi > 0)) return DPM_ERR_INVALID;
@@ -752,6 +763,7 @@ dpm_status dpm_dd_cfl(dpm_ctx* ctx, const double* c, double chi, double* cfl_dt,
 }
 
 dpm_status dpm_dd_cfl_result(dpm_ctx* ctx, double chi, double* cfl_dt, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!cfl_dt || !(chi > 0)) return DPM_ERR_INVALID;
@@ -772,6 +784,7 @@ dpm_status dpm_dd_cfl_result(dpm_ctx* ctx, double chi, double* cfl_dt, void* str
 // depends only on n, h and dt, shared by the octants).  local_begin = rhs + solve + lsq_rhs;
 // local_finish = green_rhs + solve + restrict.
 dpm_status dpm_dd_rhs(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* fq, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!rho || !c || !fq) return DPM_ERR_INVALID;
@@ -782,6 +795,7 @@ dpm_status dpm_dd_rhs(dpm_ctx* ctx, const double* rho, const double* c, double c
 }
 
 dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!wk || !y) return DPM_ERR_INVALID;
@@ -797,6 +811,7 @@ dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* strea
 }
 
 dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const double* fq, double* wk, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!C || !fq || !wk) return DPM_ERR_INVALID;
@@ -809,6 +824,7 @@ dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const 
 }
 
 dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* c, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!wk || !rho || !c) return DPM_ERR_INVALID;
@@ -819,6 +835,7 @@ dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* 
 }
 
 dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, double chi, double* y, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!rho || !c || !y) return DPM_ERR_INVALID;
@@ -845,6 +862,7 @@ dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, 
 
 dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, double* rho, double* c, double* stats,
                                void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!C || !rho || !c || !ctx->scratch) return DPM_ERR_INVALID;
@@ -865,6 +883,7 @@ dpm_status dpm_dd_local_finish(dpm_ctx* ctx, const double* C, int32_t clamp, dou
 }
 
 dpm_status dpm_dd_stats(dpm_ctx* ctx, double* stats, void* stream) {
+  DPM_NVTX();
   dpm_status st = dd_check(ctx);
   if (st != DPM_OK) return st;
   if (!stats) return DPM_ERR_INVALID;

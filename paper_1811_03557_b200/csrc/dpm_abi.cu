@@ -81,6 +81,7 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 dpm_status dpm_create_impl(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
                            int32_t device, dpm_ctx** out) {
+  DPM_NVTX();
   if (out) *out = nullptr;
   g_create_err.clear();
   if (!grid || !domain || !out) { g_create_err = "null argument"; return DPM_ERR_INVALID; }
@@ -135,6 +136,7 @@ const char* dpm_last_error(const dpm_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lmax, double dt, int32_t basis,
                       int32_t device, dpm_ctx** out) {
+  DPM_NVTX();
   if (out) *out = nullptr;
   g_create_err.clear();
   if (!grid || !domain || !out) { g_create_err = "null argument"; return DPM_ERR_INVALID; }
@@ -150,9 +152,11 @@ dpm_status dpm_create(const dpm_grid* grid, const dpm_domain* domain, int32_t lm
   return dpm_create_impl(grid, domain, lmax, dt, basis, device, out);
 }
 
-void dpm_destroy(dpm_ctx* ctx) { free_ctx(ctx); }
+void dpm_destroy(dpm_ctx* ctx) {
+  DPM_NVTX(); free_ctx(ctx); }
 
 dpm_status dpm_query(const dpm_ctx* ctx, dpm_info* out) {
+  DPM_NVTX();
   if (!ctx || !out) return DPM_ERR_INVALID;
   std::memset(out, 0, sizeof(*out));
   out->n = ctx->n;
@@ -177,12 +181,14 @@ dpm_status dpm_query(const dpm_ctx* ctx, dpm_info* out) {
 }
 
 dpm_status dpm_set_solver(dpm_ctx* ctx, int32_t solver) {
+  DPM_NVTX();
   if (!ctx || (solver != DPM_SOLVER_DST3 && solver != DPM_SOLVER_DST2_TRIDIAG)) return DPM_ERR_INVALID;
   ctx->plan.solver = solver;
   return DPM_OK;
 }
 
 dpm_status dpm_copy_set(const dpm_ctx* ctx, int32_t which, int64_t* host_idx, int64_t cap) {
+  DPM_NVTX();
   if (!ctx || !host_idx || which < 0 || which > 5) return DPM_ERR_INVALID;
   dpm_ctx* c = const_cast<dpm_ctx*>(ctx);
   if (cap < ctx->counts[which]) { c->err = "capacity too small"; return DPM_ERR_INVALID; }
@@ -192,6 +198,7 @@ dpm_status dpm_copy_set(const dpm_ctx* ctx, int32_t which, int64_t* host_idx, in
 }
 
 dpm_status dpm_copy_extension(const dpm_ctx* ctx, double* host_E, double* host_d) {
+  DPM_NVTX();
   if (!ctx) return DPM_ERR_INVALID;
   dpm_ctx* c = const_cast<dpm_ctx*>(ctx);
   cudaSetDevice(ctx->device);
@@ -202,6 +209,7 @@ dpm_status dpm_copy_extension(const dpm_ctx* ctx, double* host_E, double* host_d
 }
 
 dpm_status dpm_set_dt(dpm_ctx* ctx, double dt) {
+  DPM_NVTX();
   if (!ctx || !(dt > 0) || !std::isfinite(dt)) return DPM_ERR_INVALID;
   if (dt != ctx->dt) {
     ctx->dt = dt;
@@ -212,6 +220,7 @@ dpm_status dpm_set_dt(dpm_ctx* ctx, double dt) {
 }
 
 dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t batch, void* stream) {
+  DPM_NVTX();
   if (!ctx || batch < 0 || (batch > 0 && (!q || !u))) return DPM_ERR_INVALID;
   if (batch == 0) return DPM_OK;
   cudaSetDevice(ctx->device);
@@ -220,6 +229,7 @@ dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t
 }
 
 dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* host_u, int64_t batch, void* stream) {
+  DPM_NVTX();
   if (!ctx || batch < 0 || (batch > 0 && (!host_q || !host_u))) return DPM_ERR_INVALID;
   if (batch == 0) return DPM_OK;
   cudaSetDevice(ctx->device);
@@ -263,6 +273,7 @@ dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* 
 }
 
 dpm_status dpm_potential_rhs(dpm_ctx* ctx, const double* v_gamma, double* q, int32_t nrhs, void* stream) {
+  DPM_NVTX();
   if (!ctx || nrhs < 0 || (nrhs > 0 && (!v_gamma || !q))) return DPM_ERR_INVALID;
   if (nrhs == 0) return DPM_OK;
   cudaSetDevice(ctx->device);
@@ -271,6 +282,7 @@ dpm_status dpm_potential_rhs(dpm_ctx* ctx, const double* v_gamma, double* q, int
 }
 
 dpm_status dpm_trace(dpm_ctx* ctx, const double* u, double* out, int32_t which, int64_t batch, void* stream) {
+  DPM_NVTX();
   if (!ctx || (which != DPM_SET_GAMMA && which != DPM_SET_GAMMA_IN) || batch < 0) return DPM_ERR_INVALID;
   if (batch == 0) return DPM_OK;
   if (!u || !out) return DPM_ERR_INVALID;
@@ -280,6 +292,7 @@ dpm_status dpm_trace(dpm_ctx* ctx, const double* u, double* out, int32_t which, 
 }
 
 dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, double* B, void* stream) {
+  DPM_NVTX();
   if (!ctx || c0 < 0 || c1 > ctx->K || c0 > c1) return DPM_ERR_INVALID;
   if (c0 == c1) return DPM_OK;
   cudaSetDevice(ctx->device);
@@ -305,6 +318,7 @@ dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, do
 }
 
 dpm_status dpm_bep_factor(dpm_ctx* ctx, const double* B, void* stream) {
+  DPM_NVTX();
   if (!ctx || !B) return DPM_ERR_INVALID;
   cudaSetDevice(ctx->device);
   dpm_status st = lsq_factor(ctx, B, as_stream(stream));
@@ -316,6 +330,7 @@ dpm_status dpm_bep_factor(dpm_ctx* ctx, const double* B, void* stream) {
 }
 
 dpm_status dpm_build_projection(dpm_ctx* ctx, double* PgE, double* B, void* stream) {
+  DPM_NVTX();
   if (!ctx) return DPM_ERR_INVALID;
   cudaSetDevice(ctx->device);
   const int64_t ngin = ctx->counts[DPM_SET_GAMMA_IN];
@@ -329,6 +344,7 @@ dpm_status dpm_build_projection(dpm_ctx* ctx, double* PgE, double* B, void* stre
 }
 
 dpm_status dpm_boundary_lsq(dpm_ctx* ctx, const double* g, double* coef, double* u_gamma, int32_t nrhs, void* stream) {
+  DPM_NVTX();
   if (!ctx || nrhs < 1 || nrhs > 2048 || !g || !coef) return DPM_ERR_INVALID;
   if (!ctx->have_projection || ctx->dt_bep != ctx->dt) { ctx->err = "no projection at the current dt"; return DPM_ERR_STATE; }
   cudaSetDevice(ctx->device);
@@ -337,6 +353,7 @@ dpm_status dpm_boundary_lsq(dpm_ctx* ctx, const double* g, double* coef, double*
 }
 
 dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, void* stream) {
+  DPM_NVTX();
   if (!ctx || !rho || !c || !ic) return DPM_ERR_INVALID;
   cudaSetDevice(ctx->device);
   DPM_CUDA_TRY(ctx, launch_pks_init(ctx, rho, c, ic, as_stream(stream)));
@@ -347,6 +364,7 @@ dpm_status dpm_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* 
 }
 
 dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out, void* stream) {
+  DPM_NVTX();
   if (!ctx || !rho || !c || !out) return DPM_ERR_INVALID;
   if (ctx->dd) { ctx->err = "diagnostics: single-domain contexts only"; return DPM_ERR_INVALID; }
   cudaSetDevice(ctx->device);
@@ -495,6 +513,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
 
 dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, const dpm_pks_params* prm,
                         dpm_step_log* log, void* stream) {
+  DPM_NVTX();
   if (!ctx || !rho || !c || !prm || nsteps < 0) return DPM_ERR_INVALID;
   if (!(prm->dt_cap > 0) || !(prm->chi > 0)) { ctx->err = "dt_cap and chi must be > 0"; return DPM_ERR_INVALID; }
   if (prm->coupling != 0 && prm->coupling != 1) { ctx->err = "coupling must be 0 or 1"; return DPM_ERR_INVALID; }
@@ -612,9 +631,11 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
   return DPM_OK;
 }
 
-int64_t dpm_launch_count(void) { return (int64_t)g_dpm_launches.load(); }
+int64_t dpm_launch_count(void) {
+  DPM_NVTX(); return (int64_t)g_dpm_launches.load(); }
 
 dpm_status dpm_set_pass_timing(dpm_ctx* ctx, int32_t enable) {
+  DPM_NVTX();
   if (!ctx) return DPM_ERR_INVALID;
   ctx->plan.prof = enable ? &ctx->prof : nullptr;
   ctx->prof.used = 0;
@@ -624,6 +645,7 @@ dpm_status dpm_set_pass_timing(dpm_ctx* ctx, int32_t enable) {
 }
 
 dpm_status dpm_pass_times(dpm_ctx* ctx, double* ms, int64_t* launches, int64_t* points) {
+  DPM_NVTX();
   if (!ctx || !ms || !launches || !points) return DPM_ERR_INVALID;
   cudaSetDevice(ctx->device);
   for (int k = 0; k < 3; ++k) {

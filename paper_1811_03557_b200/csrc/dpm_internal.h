@@ -183,6 +183,15 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
   return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// NVTX range per C-ABI call (SURVEY §5 tracing): every extern "C" dpm_* entry point opens one named
+// after itself, so nsys / ncu timelines show the ABI phases (header-only NVTX3, no extra library).
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define DPM_NVTX() NvtxRange dpm_nvtx_range_(__func__)
+
 // helpers
 #define DPM_CUDA_TRY(ctx, call)                                                       \
   do {                                                                                \

@@ -605,11 +605,16 @@ def test_paper_test_a_einf_tables_1_2():
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
     import test_a
     test_a.IC_CELL = True
+    # E∞(ρ) at N = 36 is NOT asserted against the paper: its +4.4% gap is an open discrepancy that no
+    # reading explains; it is pinned only against our own measurement (a regression
+    # guard, 1e-6) so that a change of the path shows up.
     rows = {r["N"]: r for r in test_a.run_einf()["rows"]}
     for N in (36, 68, 132, 260):
         r = rows[N]
         assert abs(r["Einf_c"] / r["paper_Einf_c"] - 1) <= 2e-4, r            # 5 printed digits
-        assert abs(r["Einf_rho"] / r["paper_Einf_rho"] - 1) <= (0.05 if N == 36 else 0.01), r
+        if N > 36:
+            assert abs(r["Einf_rho"] / r["paper_Einf_rho"] - 1) <= 0.01, r
+    assert abs(rows[36]["Einf_rho"] / 1.4663451025 - 1) <= 1e-6, rows[36]
 
 
 def test_pks_step_log_lsq_residual_and_clamp(api):
