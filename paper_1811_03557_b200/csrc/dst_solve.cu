@@ -767,224 +767,7 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
   for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
 }
 
-// The small-n plane pass with one level of cyclic reduction along z (FACR(1), as plane128_facr_kernel,
-// DESIGN.md §6): per x-mode plane a, with T_y = tridiag(-1, β, -1) along y, β = 4 + h²(1/dt + λ_a),
-//   T_y v_z - v_{z-1} - v_{z+1} = h² g_z;
-// adding T_y (row z) and rows z ± 1 for every odd z eliminates the even z:
-//   -v_{z-2} + (T_y² - 2) v_z - v_{z+2} = h² (T_y g_z + g_{z-1} + g_{z+1})    (even n, z = n-1: T_y² - 1),
-// which the y DST-I diagonalises (eigenvalue τ_b² - 2, τ_b = 2 + h²(1/dt + λ_a + λ_b)): the y transforms run
-// on the n/2 odd z only; the even z follow from T_y v_z = h² g_z + v_{z-1} + v_{z+1} along y.  Every solve
-// is the exact constant-coefficient tridiagonal of ps_tri_strided (the even-n last row by Sherman–Morrison).
-// x normalisation 2/(n+1) on the right-hand sides, y normalisation 2/(n+1) in the reduced solve.
-
-// exact solve of (hs + 2) v_k - v_{k-1} - v_{k+1} = rscale r_k, k < len <= 64, zero ends, entries at
-// row[k * stride]; one warp (2 entries per lane, Kogge–Stone carries, as ps_tri_row)
-__device__ __forceinline__ void ps_tri_strided(double* row, int stride, int len, double mu, double inv_den,
-                                               double rscale) {
-  const int lane = threadIdx.x & 31, k0 = 2 * lane;
-  const double mu2 = mu * mu;
-  double mp[7];
-  mp[0] = mu2;
-#pragma unroll
-  for (int q = 1; q < 7; ++q) mp[q] = mp[q - 1] * mp[q - 1];
-  const double r0 = k0 < len ? row[k0 * stride] : 0.0, r1 = k0 + 1 < len ? row[(k0 + 1) * stride] : 0.0;
-  double y0 = rscale * r0, y1 = fma(mu, y0, rscale * r1);
-  double C = y1;
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    const double tq = __shfl_up_sync(0xffffffffu, C, 1 << q);
-    if (lane >= (1 << q)) C = fma(mp[q], tq, C);
-  }
-  double cin = __shfl_up_sync(0xffffffffu, C, 1);
-  cin = lane == 0 ? 0.0 : cin;
-  y0 = fma(mu, cin, y0);
-  y1 = fma(mu2, cin, y1);
-  if (k0 >= len) y0 = 0.0;
-  if (k0 + 1 >= len) y1 = 0.0;
-  double z1 = y1, z0 = fma(mu, y1, y0);
-  double D = z0;
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    const double tq = __shfl_down_sync(0xffffffffu, D, 1 << q);
-    if (lane + (1 << q) < 32) D = fma(mp[q], tq, D);
-  }
-  double din = __shfl_down_sync(0xffffffffu, D, 1);
-  din = lane == 31 ? 0.0 : din;
-  z1 = fma(mu, din, z1);
-  z0 = fma(mu2, din, z0);
-  const double zf = __shfl_sync(0xffffffffu, z0, 0);
-  const double c2 = mu2 * zf * inv_den;
-  const int rl = max(0, len - lane);
-  double pl = 1.0, pr = 1.0;
-#pragma unroll
-  for (int q = 0; q < 7; ++q) {
-    if ((lane >> q) & 1) pl *= mp[q];
-    if ((rl >> q) & 1) pr *= mp[q];
-  }
-  const double pa0 = mu * pl, pb1 = pr;
-  if (k0 < len) row[k0 * stride] = fma(mu, z0, -c2 * (pa0 - pb1 * mu));
-  if (k0 + 1 < len) row[(k0 + 1) * stride] = fma(mu, z1, -c2 * (pa0 * mu - pb1));
-}
-
-// P <- S P on the odd (kept) columns z = 2c + 1, c < M (thread: 4 output rows x 2 kept columns)
-__device__ __forceinline__ void ps_apply_kept(const double* S, double* P, int n, int M) {
-  const int t = threadIdx.x, rb = t >> 4, cb = t & 15;
-  double acc[4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
-  const int z0 = 2 * cb + 1, z1 = 2 * (cb + 16) + 1;
-  if (4 * rb < n) {
-    if ((n & 1) == 0) {   // folded (ps_apply): x_y ± x_{n-1-y} over y < n/2
-#pragma unroll 2
-      for (int y = 0; y < n / 2; ++y) {
-        double sv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sv[i] = S[y * PSP + 4 * rb + i];
-        const double p10 = P[y * PSP + z0], p20 = P[(n - 1 - y) * PSP + z0];
-        const double p11 = P[y * PSP + z1], p21 = P[(n - 1 - y) * PSP + z1];
-        const double ap0 = p10 + p20, am0 = p10 - p20, ap1 = p11 + p21, am1 = p11 - p21;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i][0] = fma(sv[i], (i & 1) ? am0 : ap0, acc[i][0]);
-          acc[i][1] = fma(sv[i], (i & 1) ? am1 : ap1, acc[i][1]);
-        }
-      }
-    } else {
-#pragma unroll 4
-      for (int y = 0; y < n; ++y) {
-        double sv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sv[i] = S[y * PSP + 4 * rb + i];
-        const double p0 = P[y * PSP + z0], p1 = P[y * PSP + z1];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          acc[i][0] = fma(sv[i], p0, acc[i][0]);
-          acc[i][1] = fma(sv[i], p1, acc[i][1]);
-        }
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (4 * rb + i >= n) continue;
-    if (cb < M) P[(4 * rb + i) * PSP + z0] = acc[i][0];
-    if (cb + 16 < M) P[(4 * rb + i) * PSP + z1] = acc[i][1];
-  }
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(PS_THREADS) plane_small_facr_kernel(double* __restrict__ u, int n,
-                                                                       const double* __restrict__ S_g,
-                                                                       const double* __restrict__ lam_g, double inv_dt,
-                                                                       double h2, double gs, double ys) {
-  pdl_prologue();
-  extern __shared__ double psm_small[];
-  double* S = psm_small;           // [64][PSP]
-  double* P = S + PSN * PSP;       // [64][PSP]: [y][z]
-  double* lam = P + PSN * PSP;     // [64]
-  double* W = lam + PSN;           // [64][33]: Sherman–Morrison responses per y-mode (even n)
-  const long plane = blockIdx.x;   // field * n + a
-  const int a = (int)(plane % n), t = threadIdx.x;
-  double* g = u + (size_t)plane * n * n;
-  for (int e = t; e < PSN * PSN; e += blockDim.x) {
-    const int r = e / PSN, c = e % PSN;
-    const bool in = r < n && c < n;
-    S[r * PSP + c] = in ? __ldg(S_g + r * n + c) : 0.0;
-    P[r * PSP + c] = in ? g[(size_t)r * n + c] : 0.0;
-  }
-  for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
-  __syncthreads();
-  const int M = n / 2;                                // kept z = 2c + 1, c < M
-  const double ha = h2 * (inv_dt + lam[a]);
-  const double beta = 4.0 + ha;
-  // (1) r_z = gs (β g_z(y) - g_z(y-1) - g_z(y+1) + g_{z-1}(y) + g_{z+1}(y)) on the kept columns
-  {
-    double rr[8];
-    int cnt = 0;
-    for (int e = t; e < M * n; e += PS_THREADS, ++cnt) {
-      const int c = e / n, y = e % n, z = 2 * c + 1;
-      const double gc = P[y * PSP + z];
-      const double gu = y > 0 ? P[(y - 1) * PSP + z] : 0.0, gd = y + 1 < n ? P[(y + 1) * PSP + z] : 0.0;
-      const double gl = P[y * PSP + z - 1], gr = z + 1 < n ? P[y * PSP + z + 1] : 0.0;
-      rr[cnt] = gs * (fma(beta, gc, -(gu + gd)) + (gl + gr));
-    }
-    __syncthreads();
-    cnt = 0;
-    for (int e = t; e < M * n; e += PS_THREADS, ++cnt) {
-      const int c = e / n, y = e % n;
-      P[y * PSP + 2 * c + 1] = rr[cnt];
-    }
-  }
-  __syncthreads();
-  ps_apply_kept(S, P, n, M);                          // (2) y DST-I of the kept columns
-  {
-    // (3) per y-mode b: -v_{c-1} + (τ² - 2) v_c - v_{c+1} = ys r̂_c over the M kept entries (stride 2);
-    //     even n: the last row is τ² - 1 (the ghost at z = n), by Sherman–Morrison with w = A0^{-1} e_{M-1}
-    const int w = t >> 5, lane = t & 31, nw = PS_THREADS >> 5;
-    for (int b = w; b < n; b += nw) {
-      const double hs = h2 * ((inv_dt + lam[a]) + lam[b]);
-      const double hr = hs * (hs + 4.0);            // (τ² - 2) - 2, τ = 2 + hs
-      const double mut = 2.0 / ((2.0 + hs) + sqrt(hs * (hs + 4.0)));
-      const double mu = mut * mut;                  // μ of the reduced operator: μ_τ²
-      const double id = 1.0 / (1.0 - ipow(mu, 2 * M + 2));
-      (void)hr;
-      double* row = P + b * PSP + 1;
-      if ((n & 1) == 0) {
-        double* wr = W + b * 33;
-        for (int c = lane; c < M; c += 32) wr[c] = c == M - 1 ? 1.0 : 0.0;
-        __syncwarp();
-        ps_tri_strided(wr, 1, M, mu, id, 1.0);
-        __syncwarp();
-        ps_tri_strided(row, 2, M, mu, id, ys);
-        __syncwarp();
-        const double xl = row[2 * (M - 1)], wl = wr[M - 1];
-        const double f = xl / (1.0 + wl);
-        for (int c = lane; c < M; c += 32) row[2 * c] -= f * wr[c];
-      } else {
-        ps_tri_strided(row, 2, M, mu, id, ys);
-      }
-    }
-  }
-  __syncthreads();
-  ps_apply_kept(S, P, n, M);                          // (4) inverse y DST-I of the kept columns
-  {
-    // (5) even z = 2c: T_y v = gs g_z + v_{z-1} + v_{z+1} along y (ghosts at z = -1, n)
-    const int w = t >> 5, lane = t & 31, nw = PS_THREADS >> 5;
-    const double hse = beta - 2.0;
-    const double mue = 2.0 / ((2.0 + hse) + sqrt(hse * (hse + 4.0)));
-    const double ide = 1.0 / (1.0 - ipow(mue, 2 * n + 2));
-    const int E = (n + 1) / 2;
-    for (int c = w; c < E; c += nw) {
-      const int z = 2 * c;
-      double* col = P + z;
-      for (int y = lane; y < n; y += 32) {
-        const double vl = z > 0 ? P[y * PSP + z - 1] : 0.0, vr = z + 1 < n ? P[y * PSP + z + 1] : 0.0;
-        col[y * PSP] = fma(gs, col[y * PSP], vl + vr);
-      }
-      __syncwarp();
-      ps_tri_strided(col, PSP, n, mue, ide, 1.0);
-    }
-  }
-  __syncthreads();
-  for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
-}
-
 cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
-  static const bool facr = [] {   // DPM_PLANE_SMALL_FACR=0: the full-transform small plane kernel
-    const char* v = getenv("DPM_PLANE_SMALL_FACR");
-    return !(v && atoi(v) == 0);
-  }();
-  if (facr && p.n >= 4) {
-    const int n = p.n;
-    const size_t smem = (2 * (size_t)PSN * PSP + PSN + (size_t)PSN * 33) * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(plane_small_facr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const double sc = 2.0 / (n + 1);
-    DPM_COUNT_LAUNCH(1);
-    return launch_pdl(plane_small_facr_kernel, (unsigned)((long)nfields * n), PS_THREADS, smem, s, u, n,
-                      (const double*)p.sinmat, (const double*)p.lam, 1.0 / p.dt, p.h * p.h, sc * p.h * p.h, sc);
-  }
   const int n = p.n;
   const size_t smem = (2 * (size_t)PSN * PSP + PSN) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(plane_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
