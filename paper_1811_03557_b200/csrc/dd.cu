@@ -376,32 +376,16 @@ __global__ void dd_trmv_t_kernel(const double* __restrict__ A, int K, const doub
     for (int r = 0; r < nout; ++r) out[(size_t)r * K + i] = acc[r];
 }
 
-// y[r][i] = D[i] Σ_{j >= i} W[j K + i] V[r][j] (W upper col-major, nr <= 2): 128 outputs x 8 slices of j
-// per block (loads coalesced over i, 8 independent chains per output), slices summed in a fixed order
-__global__ void __launch_bounds__(1024) dd_trmv_d_kernel(const double* __restrict__ W, int K,
-                                                         const double* __restrict__ V, int nr,
-                                                         const double* __restrict__ D, double* __restrict__ y) {
-  __shared__ double part[8][2][128];
-  const int il = threadIdx.x & 127, js = threadIdx.x >> 7;
-  const int i = blockIdx.x * 128 + il;
-  double s0 = 0.0, s1 = 0.0;
-  if (i < K)
-    for (int j = i + js; j < K; j += 8) {
-      const double w = W[(size_t)j * K + i];
-      s0 = fma(w, V[j], s0);
-      if (nr > 1) s1 = fma(w, V[(size_t)K + j], s1);
-    }
-  part[js][0][il] = s0;
-  part[js][1][il] = s1;
-  __syncthreads();
-  if (js == 0 && i < K)
-    for (int r = 0; r < nr; ++r) {
-      double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s += part[q][r][il];
-      y[(size_t)r * K + i] = D[i] * s;
-    }
-}
+// y[r][i] = D[i] Σ_{j >= i} W[j K + i] V[r][j] (W upper col-major): thread per output, coalesced over i
+__global__ void dd_trmv_d_kernel(const double* __restrict__ W, int K, const double* __restrict__ V, int nr,
+                                 const double* __restrict__ D, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  for (int r = 0; r < nr; ++r) {
+    double s = 0.0;
+    for (int j = i; j < K; ++j) s = fma(W[(size_t)j * K + i], V[(size_t)r * K + j], s);
+    y[(size_t)r * K + i] = D[i] * s;
+  }
 }
 
 // ---- NEXT-3: the paper's two-subdomain DD, Case 1 (concentric, Z ∩ Γ = ∅) ----
@@ -955,7 +939,7 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
   DPM_COUNT_LAUNCH(3);
   dd_trmv_t_kernel<<<(K + 7) / 8, 256, 0, s>>>(R, K, Z, nv, 2, Sg, Tz);                      // Σ_s S_s R^T z_s
   dd_trmv_t_kernel<<<(K + 7) / 8, 256, 0, s>>>(W2, K, Tz, 2, 2, nullptr, Vz);                // R^{-T}
-  dd_trmv_d_kernel<<<(K + 127) / 128, 1024, 0, s>>>(W2, K, Vz, 2, o0->dd_D, y);              // D R^{-1}
+  dd_trmv_d_kernel<<<(K + 127) / 128, 128, 0, s>>>(W2, K, Vz, 2, o0->dd_D, y);               // D R^{-1}
   DPM_CUDA_TRY(o0, cudaGetLastError());
   return DPM_OK;
 }
