@@ -303,8 +303,7 @@ __global__ void __launch_bounds__(256) gemv_multi_kernel(const double* __restric
   }
 }
 
-cudaError_t gemv_multi_launch(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef,
-                              cudaStream_t s) {
+cudaError_t lsq_gemv_multi(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
   if (nrhs > 16) return cudaErrorInvalidValue;
   DPM_COUNT_LAUNCH(1);
   gemv_multi_kernel<2, 16><<<(K + 1) / 2, 256, 0, s>>>(M, m, K, g, nrhs, coef);
@@ -885,10 +884,6 @@ cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int 
   cudaError_t e = lsq_rinv(R, K, Ri_ws, s);
   if (e != cudaSuccess || m == 0) return e;
   return launch_gemm_tri<true>(Q, m, K, Ri_ws, scale, M, s);
-}
-
-cudaError_t lsq_gemv_multi(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
-  return gemv_multi_launch(M, m, K, g, nrhs, coef, s);
 }
 
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
