@@ -931,8 +931,7 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
   DPM_COUNT_LAUNCH(1);
   dd_rows_trace_kernel<<<grid_for(m * nv), TB, 0, s>>>(wk, field, o0->lists[DPM_SET_GAMMA], o0->dd_rows, m, nv, G);
   DPM_CUDA_TRY(o0, cudaGetLastError());
-  for (int v0 = 0; v0 < nv; v0 += 16)                                                        // one pass over Q_0
-    DPM_CUDA_TRY(o0, lsq_gemv_multi(o0->dd_Q, m, K, G + (size_t)v0 * m, std::min(16, nv - v0), Z + (size_t)v0 * K, s));
+  DPM_CUDA_TRY(o0, lsq_gemv(o0->dd_Q, m, K, G, nv, Z, s));                                   // one pass over Q_0
   const size_t KK = (size_t)K * K;
   const double* R = o0->dd_R + 2 * KK;    // R = R2 R1
   const double* W2 = o0->dd_R + 4 * KK;   // R^{-1}

@@ -264,8 +264,6 @@ cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scal
 cudaError_t lsq_build_operator(const double* R, const double* Q, int64_t m, int K, const double* scale, double* M,
                                double* Ri_ws, cudaStream_t s);
 cudaError_t lsq_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s);
-// up to 16 right-hand sides with one pass over M
-cudaError_t lsq_gemv_multi(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s);
 cudaError_t lsq_extend(const double* E, int64_t ng, int K, const double* coef, int nrhs, int clamp, double* ug,
                        cudaStream_t s, double* clampmax = nullptr);
 

@@ -258,58 +258,6 @@ __global__ void __launch_bounds__(GEMV_T) lsq_gemv_kernel(const double* __restri
   }
 }
 
-// Many right-hand sides at once (NR <= 16): each row chunk of M is read once for all of them (the DD
-// shared apply: 16 right-hand sides over octant 0's Q).  Block = ROWS rows of M, 256 threads.
-template <int ROWS, int NR>
-__global__ void __launch_bounds__(256) gemv_multi_kernel(const double* __restrict__ M, int64_t m, int K,
-                                                         const double* __restrict__ g, int nrhs,
-                                                         double* __restrict__ coef) {
-  const int c0 = blockIdx.x * ROWS;
-  const double* a[ROWS];
-#pragma unroll
-  for (int q = 0; q < ROWS; ++q) a[q] = M + (size_t)min(c0 + q, K - 1) * m;
-  double acc[ROWS][NR];
-#pragma unroll
-  for (int q = 0; q < ROWS; ++q)
-#pragma unroll
-    for (int r = 0; r < NR; ++r) acc[q][r] = 0.0;
-  for (int64_t i = threadIdx.x; i < m; i += 256) {
-    double av[ROWS];
-#pragma unroll
-    for (int q = 0; q < ROWS; ++q) av[q] = __ldg(a[q] + i);
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const double x = r < nrhs ? __ldg(g + (size_t)r * m + i) : 0.0;
-#pragma unroll
-      for (int q = 0; q < ROWS; ++q) acc[q][r] = fma(av[q], x, acc[q][r]);
-    }
-  }
-  __shared__ double red[ROWS * NR][8];
-#pragma unroll
-  for (int q = 0; q < ROWS; ++q)
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      double v = acc[q][r];
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if ((threadIdx.x & 31) == 0) red[q * NR + r][threadIdx.x >> 5] = v;
-    }
-  __syncthreads();
-  for (int e = threadIdx.x; e < ROWS * NR; e += 256) {
-    const int q = e / NR, r = e % NR;
-    double v = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) v += red[e][w];
-    if (c0 + q < K && r < nrhs) coef[(size_t)r * K + c0 + q] = v;
-  }
-}
-
-cudaError_t lsq_gemv_multi(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
-  if (nrhs > 16) return cudaErrorInvalidValue;
-  DPM_COUNT_LAUNCH(1);
-  gemv_multi_kernel<2, 16><<<(K + 1) / 2, 256, 0, s>>>(M, m, K, g, nrhs, coef);
-  return cudaGetLastError();
-}
-
 void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, double* coef, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
   if (K >= 4 * 148)
