@@ -320,74 +320,6 @@ __global__ void dd_ic_kernel(const uint8_t* __restrict__ flags, const int32_t* _
 
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
 
-// ---- one operator pass for all octants of a device (dpm_dd_lsq_rhs_shared) ----------------------------
-// S_s: the column signs of octant s's extension relative to octant 0's (E_s = E_0 diag(S_s): the cap SH and
-// plane Legendre bases are even or odd under each reflection, and the recursions evaluate the reflected
-// arguments to exactly ± the same values).  Per column: the γ point of octant 0's largest |E|, and the
-// ratio there, required to be exactly ±1 (*bad set otherwise).
-__global__ void dd_sign_kernel(const double* __restrict__ E0, const double* __restrict__ Es, int64_t ng,
-                               double* sign, int* bad) {
-  const int c = blockIdx.x;
-  const double* a = E0 + (size_t)c * ng;
-  double best = -1.0;
-  int64_t arg = 0;
-  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
-    const double v = fabs(a[g]);
-    if (v > best) { best = v; arg = g; }
-  }
-  __shared__ double sb[TB];
-  __shared__ int64_t sa[TB];
-  sb[threadIdx.x] = best;
-  sa[threadIdx.x] = arg;
-  __syncthreads();
-  for (int o = TB / 2; o; o >>= 1) {
-    if (threadIdx.x < o && (sb[threadIdx.x + o] > sb[threadIdx.x] ||
-                            (sb[threadIdx.x + o] == sb[threadIdx.x] && sa[threadIdx.x + o] < sa[threadIdx.x]))) {
-      sb[threadIdx.x] = sb[threadIdx.x + o];
-      sa[threadIdx.x] = sa[threadIdx.x + o];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double e0 = a[sa[0]], es = Es[(size_t)c * ng + sa[0]];
-    const double r = e0 != 0.0 ? es / e0 : 1.0;
-    if (r != 1.0 && r != -1.0) atomicOr(bad, 1);
-    sign[c] = r < 0 ? -1.0 : 1.0;
-  }
-}
-
-// out[r][i] = Σ_v wts[v][i] (Aᵀ X[v])[i] for the upper-triangular col-major A (element (j, i) at i K + j,
-// j <= i): warp per output i, lanes over j (contiguous), the nv vectors X[v] = X + v K grouped into
-// nout outputs (vector v -> output v % nout), weighted by wts (nullable: 1).  Fixed reduction order.
-__global__ void dd_trmv_t_kernel(const double* __restrict__ A, int K, const double* __restrict__ X, int nv, int nout,
-                                 const double* __restrict__ wts, double* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i >= K) return;
-  const double* row = A + (size_t)i * K;
-  double acc[2] = {0.0, 0.0};
-  for (int v = 0; v < nv; ++v) {
-    double s = 0.0;
-    for (int j = lane; j <= i; j += 32) s = fma(row[j], X[(size_t)v * K + j], s);
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    acc[v % nout] = fma(wts ? wts[(size_t)(v / nout) * K + i] : 1.0, s, acc[v % nout]);
-  }
-  if (lane == 0)
-    for (int r = 0; r < nout; ++r) out[(size_t)r * K + i] = acc[r];
-}
-
-// y[r][i] = D[i] Σ_{j >= i} W[j K + i] V[r][j] (W upper col-major): thread per output, coalesced over i
-__global__ void dd_trmv_d_kernel(const double* __restrict__ W, int K, const double* __restrict__ V, int nr,
-                                 const double* __restrict__ D, double* __restrict__ y) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= K) return;
-  for (int r = 0; r < nr; ++r) {
-    double s = 0.0;
-    for (int j = i; j < K; ++j) s = fma(W[(size_t)j * K + i], V[(size_t)r * K + j], s);
-    y[(size_t)r * K + i] = D[i] * s;
-  }
-}
-
 // ---- NEXT-3: the paper's two-subdomain DD, Case 1 (concentric, Z ∩ Γ = ∅) ----
 // Pieces: Z (the interface |x| = r1, piece 0, bit 1) and Γ (|x| = r2, piece 1, bit 2).  Ω1 (sub 0):
 // every point of ζ1 is on Z; Ω2 (sub 1): a point of γ ∪ ζ2 is on the nearer sphere (reading R38).
@@ -875,71 +807,6 @@ dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* strea
                                                                 ctx->n_rows, 2, ctx->dd_g);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   DPM_CUDA_TRY(ctx, lsq_gemv(ctx->dd_M, ctx->n_rows, ctx->K, ctx->dd_g, 2, y, s));           // y_s = M_s g_s
-  return DPM_OK;
-}
-
-dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* wk, double* y, void* stream) {
-  DPM_NVTX();
-  if (!octs || noct < 1 || !wk || !y) return DPM_ERR_INVALID;
-  dpm_ctx* o0 = octs[0];
-  dpm_status st = dd_check(o0);
-  if (st != DPM_OK) return st;
-  const int K = o0->K;
-  for (int s = 0; s < noct; ++s) {
-    dpm_ctx* o = octs[s];
-    if (!o || o->dd != 1 || o->device != o0->device || o->n != o0->n || o->lo != o0->lo || o->hi != o0->hi ||
-        o->K != K || o->n_rows != o0->n_rows || o->radius != o0->radius) {
-      o0->err = "dd_lsq_rhs_shared: the contexts are not octants of one canonical geometry on one device";
-      return DPM_ERR_INVALID;
-    }
-    if (!o->have_projection || o->dt_bep != o->dt) { o0->err = "dd_lsq_rhs_shared: no factorisation"; return DPM_ERR_STATE; }
-  }
-  cudaStream_t s = as_stream(stream);
-  const size_t field = (size_t)o0->n * o0->n * o0->n;
-  const int64_t ng = o0->counts[DPM_SET_GAMMA], m = o0->n_rows;
-  const int nv = 2 * noct;
-  // signs of every octant relative to octant 0 (geometry only: computed once per pair)
-  for (int q = 0; q < noct; ++q) {
-    dpm_ctx* o = octs[q];
-    if (o->dd_sign && o->dd_sign_ref == o0) continue;
-    if (!o->dd_sign) DPM_CUDA_TRY(o0, cudaMalloc(&o->dd_sign, (size_t)K * sizeof(double) + 16));
-    int* dbad = reinterpret_cast<int*>(o->dd_sign + K);
-    DPM_CUDA_TRY(o0, cudaMemsetAsync(dbad, 0, sizeof(int), s));
-    DPM_COUNT_LAUNCH(1);
-    dd_sign_kernel<<<K, TB, 0, s>>>(o0->dd_Eraw, o->dd_Eraw, ng, o->dd_sign, dbad);
-    int hbad = 0;
-    DPM_CUDA_TRY(o0, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    DPM_CUDA_TRY(o0, cudaStreamSynchronize(s));
-    if (hbad) { o0->err = "dd_lsq_rhs_shared: the octant extensions are not sign-reflections"; return DPM_ERR_INVALID; }
-    o->dd_sign_ref = o0;
-  }
-  const size_t need = ((size_t)nv * m + (size_t)nv * K + 4 * (size_t)K + (size_t)noct * K) * sizeof(double);
-  if (o0->dd_shared_bytes < need) {
-    if (o0->dd_shared) cudaFree(o0->dd_shared);
-    o0->dd_shared = nullptr;
-    o0->dd_shared_bytes = 0;
-    DPM_CUDA_TRY(o0, cudaMalloc(&o0->dd_shared, need));
-    o0->dd_shared_bytes = need;
-  }
-  double* G = o0->dd_shared;              // [nv][m]: BEP right-hand sides of all octants
-  double* Z = G + (size_t)nv * m;         // [nv][K]: Q_0^T g_v
-  double* Tz = Z + (size_t)nv * K;        // [2][K]: Σ_s S_s R^T z_s
-  double* Vz = Tz + 2 * (size_t)K;        // [2][K]: R^{-T} Tz
-  double* Sg = Vz + 2 * (size_t)K;        // [noct][K]: the signs, stacked
-  for (int q = 0; q < noct; ++q)
-    DPM_CUDA_TRY(o0, cudaMemcpyAsync(Sg + (size_t)q * K, octs[q]->dd_sign, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
-  DPM_COUNT_LAUNCH(1);
-  dd_rows_trace_kernel<<<grid_for(m * nv), TB, 0, s>>>(wk, field, o0->lists[DPM_SET_GAMMA], o0->dd_rows, m, nv, G);
-  DPM_CUDA_TRY(o0, cudaGetLastError());
-  DPM_CUDA_TRY(o0, lsq_gemv(o0->dd_Q, m, K, G, nv, Z, s));                                   // one pass over Q_0
-  const size_t KK = (size_t)K * K;
-  const double* R = o0->dd_R + 2 * KK;    // R = R2 R1
-  const double* W2 = o0->dd_R + 4 * KK;   // R^{-1}
-  DPM_COUNT_LAUNCH(3);
-  dd_trmv_t_kernel<<<(K + 7) / 8, 256, 0, s>>>(R, K, Z, nv, 2, Sg, Tz);                      // Σ_s S_s R^T z_s
-  dd_trmv_t_kernel<<<(K + 7) / 8, 256, 0, s>>>(W2, K, Tz, 2, 2, nullptr, Vz);                // R^{-T}
-  dd_trmv_d_kernel<<<(K + 127) / 128, 128, 0, s>>>(W2, K, Vz, 2, o0->dd_D, y);               // D R^{-1}
-  DPM_CUDA_TRY(o0, cudaGetLastError());
   return DPM_OK;
 }
 
