@@ -62,3 +62,20 @@ def test_create_rejects_invalid_without_gpu(lib):
     assert b"inside" in L.lib.dpm_last_error(None)
     d = L.Domain(L.SPHERE, (ctypes.c_double * 3)(0, 0, 0), (ctypes.c_double * 3)(0.5, 0.5, 0.5))
     assert L.lib.dpm_create(ctypes.byref(g), ctypes.byref(d), 2, -1.0, 0, 0, ctypes.byref(h)) == L.DPM_ERR_INVALID
+
+
+def test_dd_creators_reject_invalid_without_gpu(lib):
+    # dpm_create_octant / dpm_create_dd1 validate before any CUDA call (NEXT-3: 0 < r1 < r2, sub in {0, 1},
+    # the subdomain strictly inside its box; octant index 0..7)
+    from paper_1811_03557_b200 import _lib as L
+    h = ctypes.c_void_p()
+    g = L.Grid(20, -0.328125, 0.328125)      # the paper's N1 = 20 mesh for r1 = 0.25
+    bad = [(2, 0.25, 0.5), (0, 0.5, 0.25), (0, 0.0, 0.5), (0, 0.4, 0.5)]   # bad sub, r2 <= r1, r1 = 0, ball > box
+    for sub, r1, r2 in bad:
+        st = L.lib.dpm_create_dd1(ctypes.byref(g), sub, r1, r2, 0, 0, 1e-8, 0, ctypes.byref(h))
+        assert st == L.DPM_ERR_INVALID, (sub, r1, r2)
+    assert L.lib.dpm_create_dd1(ctypes.byref(g), 0, 0.25, 0.5, -1, 0, 1e-8, 0, ctypes.byref(h)) == L.DPM_ERR_INVALID
+    go = L.Grid(16, -0.1, 1.1)
+    assert L.lib.dpm_create_octant(ctypes.byref(go), 8, 1.0, 4, 4, 1e-3, 0, ctypes.byref(h)) == L.DPM_ERR_INVALID
+    assert L.lib.dpm_create_octant(ctypes.byref(go), 0, 2.0, 4, 4, 1e-3, 0, ctypes.byref(h)) == L.DPM_ERR_INVALID
+    assert not h.value
