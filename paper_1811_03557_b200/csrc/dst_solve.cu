@@ -673,6 +673,66 @@ __device__ __forceinline__ void ps_apply(const double* S, double* P, int n) {
   __syncthreads();
 }
 
+// The same y DST-I (P <- S P, even n) on the fp64 tensor pipe (DMMA.8x8x4): the folded products
+// out[b] = Σ_{y < n/2} S[b][y] (P[y] ± P[n-1-y]) (+ for even b, - for odd b) are an (even rows | odd rows) x
+// (y < n/2) x (z) product, m-tiles of 8 even or 8 odd output rows, n-tiles of 8 z, k-steps of 4 y.  Warp w
+// owns n-tile w % NT and every (8 / NT)-th m-tile: its B± fragments are formed once per k-step (one DADD)
+// and reused by all its m-tiles, whose accumulators are independent DMMA chains.  About 5x fewer issued
+// instructions than the DFMA tiles of ps_apply for the same flops (the small-n plane pass is issue- and
+// latency-bound, not fp64-throughput-bound).  Rows / columns >= n are zero in S and P; the A fragments
+// of y >= n/2 are masked to 0.
+__device__ __forceinline__ void ps_apply_dmma(const double* S, double* P, int n) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int half = n >> 1;
+  const int NT = (n + 7) >> 3;                 // n-tiles of 8 z
+  const int MH = (half + 7) >> 3;              // m-tiles per parity (8 output rows of one parity)
+  const int wpn = max(1, (PS_THREADS / 32) / NT);
+  const int nt = w % NT, mg = w / NT;
+  const bool active = w < NT * wpn;
+  const int KS = (half + 3) >> 2;              // k-steps of 4 y
+  double acc[2][4][2];                          // [parity][m-tile slot][2]
+#pragma unroll
+  for (int s = 0; s < 2; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[s][q][0] = acc[s][q][1] = 0.0;
+  const int zb = 8 * nt + (lane >> 2), rl = lane >> 2, kl = lane & 3;
+  if (active) {
+    for (int kk = 0; kk < KS; ++kk) {
+      const int y = 4 * kk + kl;
+      const bool yin = y < half;
+      const double p1 = yin ? P[y * PSP + zb] : 0.0, p2 = yin ? P[(n - 1 - y) * PSP + zb] : 0.0;
+      const double bp = p1 + p2, bm = p1 - p2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = mg + q * wpn;            // m-tile index of this slot
+        if (i >= MH) break;
+        const int be = 2 * (8 * i + rl);       // this lane's A row (even set); the odd set is be + 1
+        const double ae = yin ? S[be * PSP + y] : 0.0, ao = yin ? S[(be + 1) * PSP + y] : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[0][q][0]), "+d"(acc[0][q][1]) : "d"(ae), "d"(bp));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(acc[1][q][0]), "+d"(acc[1][q][1]) : "d"(ao), "d"(bm));
+      }
+    }
+  }
+  __syncthreads();                              // every read of P done
+  if (active) {
+    const int zc = 8 * nt + 2 * (lane & 3);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = mg + q * wpn;
+      if (i >= MH) break;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int b = 2 * (8 * i + rl) + s;
+        P[b * PSP + zc] = acc[s][q][0];
+        P[b * PSP + zc + 1] = acc[s][q][1];
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // exact solve of (hs + 2) v_k - v_{k-1} - v_{k+1} = rscale r_k (k < n <= 64, zero ends) in place, one
 // warp; mu = μ(hs) and inv_den = 1/(1 - μ^{2n+2}) come precomputed (lane-parallel over the warp's rows)
 __device__ __forceinline__ void ps_tri_row(double* row, int n, double mu, double inv_den, double rscale) {
@@ -726,6 +786,9 @@ __device__ __forceinline__ void ps_tri_row(double* row, int n, double mu, double
   if (k0 + 1 < n) row[k0 + 1] = fma(mu, z1, -c2 * (pa0 * mu - pb1));
 }
 
+__device__ int g_ps_dmma = 1;   // DPM_PLANE_SMALL_DMMA=0 -> 0 (set by dst_plan_init)
+__device__ __forceinline__ bool ps_dmma() { return g_ps_dmma != 0; }
+
 __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restrict__ u, int n, const double* __restrict__ S_g,
                                                           const double* __restrict__ lam_g, double inv_dt, double h2,
                                                           double rscale) {
@@ -745,7 +808,8 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
   }
   for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
   __syncthreads();
-  ps_apply(S, P, n);
+  const bool tc = ps_dmma() && (n & 1) == 0;
+  if (tc) ps_apply_dmma(S, P, n); else ps_apply(S, P, n);
   {
     // warp w solves rows b = w + 8 i (i < 8); lane i first computes μ and 1/(1 - μ^{2n+2}) of row i
     const int w = t >> 5, lane = t & 31, nw = blockDim.x >> 5;
@@ -763,7 +827,7 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
     }
   }
   __syncthreads();
-  ps_apply(S, P, n);
+  if (tc) ps_apply_dmma(S, P, n); else ps_apply(S, P, n);
   for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
 }
 
@@ -829,6 +893,9 @@ cudaError_t dst_plan_init(DstPlan& p, int n, double h, double dt) {
     const char* envs = getenv("DPM_PLANE_SMALL");
     if (!(envs && atoi(envs) == 0)) {
       if ((e = cudaMalloc(&p.sinmat, sizeof(double) * n * n)) != cudaSuccess) return e;
+      const char* envd = getenv("DPM_PLANE_SMALL_DMMA");
+      const int dm = (envd && atoi(envd) == 0) ? 0 : 1;
+      if ((e = cudaMemcpyToSymbol(g_ps_dmma, &dm, sizeof(int))) != cudaSuccess) return e;
       DPM_COUNT_LAUNCH(1);
       sinmat_kernel<<<(n * n + 255) / 256, 256>>>(p.sinmat, n);
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
