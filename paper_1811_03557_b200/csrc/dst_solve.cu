@@ -786,6 +786,72 @@ __device__ __forceinline__ void ps_tri_row(double* row, int n, double mu, double
   if (k0 + 1 < n) row[k0 + 1] = fma(mu, z1, -c2 * (pa0 * mu - pb1));
 }
 
+// ps_tri_row on R rows at once (their recurrences and shuffle scans interleaved: R independent chains per
+// warp instead of one); rows with valid[r] == false are skipped (their lanes compute on zeros)
+template <int R>
+__device__ __forceinline__ void ps_tri_rows(double* const (&row)[R], const bool (&valid)[R], int n,
+                                            const double (&mu)[R], const double (&inv_den)[R], double rscale) {
+  const int lane = threadIdx.x & 31, k0 = 2 * lane;
+  double mu2[R], mp[R][7], y0[R], y1[R], C[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    mu2[r] = mu[r] * mu[r];
+    mp[r][0] = mu2[r];
+#pragma unroll
+    for (int q = 1; q < 7; ++q) mp[r][q] = mp[r][q - 1] * mp[r][q - 1];
+    const double r0 = (valid[r] && k0 < n) ? row[r][k0] : 0.0, r1 = (valid[r] && k0 + 1 < n) ? row[r][k0 + 1] : 0.0;
+    y0[r] = rscale * r0;
+    y1[r] = fma(mu[r], y0[r], rscale * r1);
+    C[r] = y1[r];
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double tq = __shfl_up_sync(0xffffffffu, C[r], 1 << q);
+      if (lane >= (1 << q)) C[r] = fma(mp[r][q], tq, C[r]);
+    }
+  double z0[R], z1[R], D[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double cin = __shfl_up_sync(0xffffffffu, C[r], 1);
+    cin = lane == 0 ? 0.0 : cin;
+    y0[r] = fma(mu[r], cin, y0[r]);
+    y1[r] = fma(mu2[r], cin, y1[r]);
+    if (k0 >= n) y0[r] = 0.0;
+    if (k0 + 1 >= n) y1[r] = 0.0;
+    z1[r] = y1[r];
+    z0[r] = fma(mu[r], y1[r], y0[r]);
+    D[r] = z0[r];
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double tq = __shfl_down_sync(0xffffffffu, D[r], 1 << q);
+      if (lane + (1 << q) < 32) D[r] = fma(mp[r][q], tq, D[r]);
+    }
+  const int rl = max(0, n - lane);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double din = __shfl_down_sync(0xffffffffu, D[r], 1);
+    din = lane == 31 ? 0.0 : din;
+    z1[r] = fma(mu[r], din, z1[r]);
+    z0[r] = fma(mu2[r], din, z0[r]);
+    const double zf = __shfl_sync(0xffffffffu, z0[r], 0);
+    const double c2 = mu2[r] * zf * inv_den[r];
+    double pl = 1.0, pr = 1.0;
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      if ((lane >> q) & 1) pl *= mp[r][q];
+      if ((rl >> q) & 1) pr *= mp[r][q];
+    }
+    const double pa0 = mu[r] * pl, pb1 = pr;
+    if (valid[r] && k0 < n) row[r][k0] = fma(mu[r], z0[r], -c2 * (pa0 - pb1 * mu[r]));
+    if (valid[r] && k0 + 1 < n) row[r][k0 + 1] = fma(mu[r], z1[r], -c2 * (pa0 * mu[r] - pb1));
+  }
+}
+
 __device__ int g_ps_dmma = 1;   // DPM_PLANE_SMALL_DMMA=0 -> 0 (set by dst_plan_init)
 __device__ __forceinline__ bool ps_dmma() { return g_ps_dmma != 0; }
 
@@ -820,10 +886,12 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
       mu_l = 2.0 / ((2.0 + hs) + sqrt(hs * (hs + 4.0)));
       id_l = 1.0 / (1.0 - ipow(mu_l, 2 * n + 2));
     }
-    for (int i = 0; i < 8; ++i) {
-      const int b = w + nw * i;
-      const double mu = __shfl_sync(0xffffffffu, mu_l, i), id = __shfl_sync(0xffffffffu, id_l, i);
-      if (b < n) ps_tri_row(P + b * PSP, n, mu, id, rscale);
+    for (int i = 0; i < 8; i += 2) {   // two rows at a time: two interleaved recurrence chains
+      double* rows[2] = {P + (w + nw * i) * PSP, P + (w + nw * (i + 1)) * PSP};
+      const bool valid[2] = {w + nw * i < n, w + nw * (i + 1) < n};
+      const double mu[2] = {__shfl_sync(0xffffffffu, mu_l, i), __shfl_sync(0xffffffffu, mu_l, i + 1)};
+      const double id[2] = {__shfl_sync(0xffffffffu, id_l, i), __shfl_sync(0xffffffffu, id_l, i + 1)};
+      if (valid[0]) ps_tri_rows<2>(rows, valid, n, mu, id, rscale);
     }
   }
   __syncthreads();
