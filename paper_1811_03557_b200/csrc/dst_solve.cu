@@ -852,6 +852,9 @@ __device__ __forceinline__ void ps_tri_rows(double* const (&row)[R], const bool 
   }
 }
 
+#ifndef PS_ROWS
+#define PS_ROWS 4
+#endif
 __device__ int g_ps_dmma = 1;   // DPM_PLANE_SMALL_DMMA=0 -> 0 (set by dst_plan_init)
 __device__ __forceinline__ bool ps_dmma() { return g_ps_dmma != 0; }
 
@@ -886,12 +889,18 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
       mu_l = 2.0 / ((2.0 + hs) + sqrt(hs * (hs + 4.0)));
       id_l = 1.0 / (1.0 - ipow(mu_l, 2 * n + 2));
     }
-    for (int i = 0; i < 8; i += 2) {   // two rows at a time: two interleaved recurrence chains
-      double* rows[2] = {P + (w + nw * i) * PSP, P + (w + nw * (i + 1)) * PSP};
-      const bool valid[2] = {w + nw * i < n, w + nw * (i + 1) < n};
-      const double mu[2] = {__shfl_sync(0xffffffffu, mu_l, i), __shfl_sync(0xffffffffu, mu_l, i + 1)};
-      const double id[2] = {__shfl_sync(0xffffffffu, id_l, i), __shfl_sync(0xffffffffu, id_l, i + 1)};
-      if (valid[0]) ps_tri_rows<2>(rows, valid, n, mu, id, rscale);
+    for (int i = 0; i < 8; i += PS_ROWS) {   // PS_ROWS rows at a time: interleaved recurrence chains
+      double* rows[PS_ROWS];
+      bool valid[PS_ROWS];
+      double mu[PS_ROWS], id[PS_ROWS];
+#pragma unroll
+      for (int r = 0; r < PS_ROWS; ++r) {
+        rows[r] = P + (w + nw * (i + r)) * PSP;
+        valid[r] = w + nw * (i + r) < n;
+        mu[r] = __shfl_sync(0xffffffffu, mu_l, i + r);
+        id[r] = __shfl_sync(0xffffffffu, id_l, i + r);
+      }
+      if (valid[0]) ps_tri_rows<PS_ROWS>(rows, valid, n, mu, id, rscale);
     }
   }
   __syncthreads();
