@@ -853,7 +853,7 @@ __device__ __forceinline__ void ps_tri_rows(double* const (&row)[R], const bool 
 }
 
 #ifndef PS_ROWS
-#define PS_ROWS 4
+#define PS_ROWS 2
 #endif
 __device__ int g_ps_dmma = 1;   // DPM_PLANE_SMALL_DMMA=0 -> 0 (set by dst_plan_init)
 __device__ __forceinline__ bool ps_dmma() { return g_ps_dmma != 0; }
