@@ -487,7 +487,10 @@ def main():
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        try:   # bind the NCCL communicator to this rank's GPU
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        except TypeError:
+            dist.init_process_group("nccl")
     from paper_1811_03557_b200 import api
     from paper_1811_03557_b200._lib import lib as L
 
