@@ -319,19 +319,32 @@ __global__ void rdinv_kernel(const double* __restrict__ R, const double* __restr
   RD[e] = j >= i ? R[(size_t)j * K + i] / D[j] : 0.0;
 }
 
-constexpr int RES_T = 256;
+constexpr int RES_T = 1024;
 __global__ void __launch_bounds__(RES_T) lsq_resid_kernel(const double* __restrict__ z, int K,
                                                           const double* __restrict__ g, int64_t m, int nrhs,
                                                           double* out) {
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};   // (||Q^T g||^2, ||g||^2) per right-hand side
+  // (||Q^T g||^2, ||g||^2) per right-hand side; four independent chains per sum (the g stream is ~|γ_in|
+  // loads per right-hand side in one block: latency, not bandwidth)
+  double acc[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
   for (int q = 0; q < nrhs; ++q) {
-    for (int i = threadIdx.x; i < K; i += RES_T) acc[2 * q] = fma(z[q * K + i], z[q * K + i], acc[2 * q]);
-    for (int64_t i = threadIdx.x; i < m; i += RES_T) acc[2 * q + 1] = fma(g[q * m + i], g[q * m + i], acc[2 * q + 1]);
+    for (int i = threadIdx.x; i < K; i += RES_T) acc[2 * q][0] = fma(z[q * K + i], z[q * K + i], acc[2 * q][0]);
+    const double* gq = g + (size_t)q * m;
+    int64_t i = threadIdx.x;
+    for (; i + 3 * RES_T < m; i += 4 * RES_T) {
+      const double a = gq[i], b = gq[i + RES_T], c = gq[i + 2 * RES_T], d = gq[i + 3 * RES_T];
+      acc[2 * q + 1][0] = fma(a, a, acc[2 * q + 1][0]);
+      acc[2 * q + 1][1] = fma(b, b, acc[2 * q + 1][1]);
+      acc[2 * q + 1][2] = fma(c, c, acc[2 * q + 1][2]);
+      acc[2 * q + 1][3] = fma(d, d, acc[2 * q + 1][3]);
+    }
+    for (; i < m; i += RES_T) acc[2 * q + 1][0] = fma(gq[i], gq[i], acc[2 * q + 1][0]);
   }
   __shared__ double red[4][RES_T / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int q = 0; q < 4; ++q) {
-    double v = acc[q];
+    double v = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) red[q][w] = v;
   }
