@@ -168,3 +168,37 @@ def test_dd_collectives_match_single_process(world):
         np.testing.assert_allclose(n2, octs[0].seen["n2"].numpy(), rtol=1e-14)
         np.testing.assert_allclose(G2, octs[0].seen["G2"].numpy(), rtol=1e-14)
         np.testing.assert_allclose(C, octs[0].seen["C"].numpy(), rtol=1e-14)
+
+
+def _dd1_worker(rank, world, port, q):
+    # NEXT-3 at p = 2: one Case-1 subdomain per rank with its own h (rank 0: h1 = 0.01, rank 1: h2 = 0.1)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1811_03557_b200.dd import DDSolver
+    o = _FakeOctant(rank)
+    o.info = {"h": 0.01 if rank == 0 else 0.1}
+    sol = DDSolver([o], dt_cap=1.0)
+    sol.init((0, 0, 0), (1, 1), (1, 1))
+    log = sol.step()
+    q.put((rank, log["dt"], o.seen["C"].numpy()))
+    dist.destroy_process_group()
+
+
+def test_case1_dd_two_ranks_global_dt_and_coefficients():
+    """The two-subdomain DD with one subdomain per rank and different grids: the global Δt is the minimum
+    over both ranks of min(CFL, 0.5 h_l^2) (R13, R38) and both ranks hold the same summed coefficients."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dd1_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    want_dt = min(1e-3 * 1, 1e-3 * 2, 0.5 * 0.01 ** 2, 0.5 * 0.1 ** 2)
+    yref = _FakeOctant(0).y + _FakeOctant(1).y
+    for rank, dt, C in outs:
+        assert dt == want_dt
+        np.testing.assert_allclose(C, yref.numpy(), rtol=1e-14)
