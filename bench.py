@@ -567,7 +567,9 @@ def main():
     k_gbs = k_bytes / k_avg_s / 1e9 if k_avg_s > 0 else 0.0
     share = k_ms / max(sum(v[0] for v in pt.values()), 1e-30)
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
+    tfile = os.path.join(ROOT, "profiles", "r02", "ncu_traffic.json")
+    if not os.path.exists(tfile):
+        tfile = os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")
     if os.path.exists(tfile):
         tr = json.load(open(tfile)).get(kind)
         if tr and tr.get("points_per_launch"):
