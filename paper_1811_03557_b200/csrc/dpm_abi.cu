@@ -26,7 +26,7 @@ thread_local std::string g_create_err;
 void free_ctx(dpm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq, c->RDinv,
+  void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->mplus_slope, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq, c->RDinv,
                   c->dd_Eraw, c->dd_assign, c->dd_rows, c->dd_B, c->dd_Q, c->dd_R, c->dd_M, c->dd_D, c->dd_g, c->dd_ug,
                   c->lsq_ws, c->work, c->scratch, c->red};
   for (void* p : ptrs)

@@ -66,6 +66,7 @@ struct dpm_ctx {
   int64_t exact_ties = 0;         // nodes within the fp64 tie band, decided exactly on the host (R6)
   int64_t exact_ties_inside = 0;  // of those, the ones in M+
   int32_t* gin_pos = nullptr;    // [n_gamma_in] position of gamma_in points inside gamma
+  uint16_t* mplus_slope = nullptr;  // [n_M+] minmod-slope validity bits per M+ point (flux_rhs_list_kernel)
 
   // gamma geometry + extension matrix (device)
   double* foot = nullptr;        // [n_gamma][3]
@@ -280,6 +281,7 @@ double mass_fixed_decode(const double* stats);   // 128-bit fixed-point mass (st
 // pks.cu
 cudaError_t launch_pks_init(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_ic* ic, cudaStream_t s);
 cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaStream_t s);
+cudaError_t launch_slope_mask(dpm_ctx* ctx, cudaStream_t s);   // ctx->mplus_slope from the flags (setup)
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi,
                             double* fq_rho, double* fq_c, cudaStream_t s,
                             double* backup = nullptr, double* zero6 = nullptr, double* cfl_out3 = nullptr,

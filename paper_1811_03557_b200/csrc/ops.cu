@@ -3,6 +3,8 @@
 //  * trace / BEP gather     PgE = Tr_γ u, B = E_in - Tr_γin u
 //  * PKS: CFL reduction (R19), upwind/minmod flux + IMEX RHS (R15, R16),
 //         combined Green RHS (R20), restriction to N+ with step statistics (R18).
+#include <cstdlib>
+
 #include "dpm_internal.h"
 
 namespace {
@@ -164,6 +166,41 @@ struct CflFuse {
   double* dt_out = nullptr;
 };
 
+// Step 3 on the device, the tail of both flux kernels: block maxima of the face differences -> atomics,
+// the last block (ticket) evaluates the rule into dt_out and re-zeroes the slot.
+__device__ __forceinline__ void cfl_finish(const double (&cmx)[3], double h, const CflFuse& cf) {
+  __shared__ double red[3][TB / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int a = 0; a < 3; ++a) {
+    double v = cmx[a];
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[a][w] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0;
+    for (int q = 0; q < TB / 32; ++q) v = fmax(v, red[threadIdx.x][q]);
+    umax_atomic(cf.out3 + threadIdx.x, v);
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(cf.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    volatile double* r3 = cf.out3;
+    double cfl = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+      const double m = r3[a] / h;
+      if (m > 0) cfl = fmin(cfl, h / (6.0 * cf.chi * m));
+      r3[a] = 0.0;   // ready for the slot's next use
+    }
+    *cf.dt_out = fmin(fmin(cf.dt_prev, cf.cap), fmin(cfl, 0.5 * h * h));
+    *cf.ticket = 0u;
+  }
+}
+
 __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double* __restrict__ rho, const double* __restrict__ c,
                                 const uint8_t* __restrict__ flags, int n, double h, double dt, double chi,
                                 double* __restrict__ fq_rho, double* __restrict__ fq_c, double* __restrict__ backup,
@@ -235,36 +272,110 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_kernel(const double
     fq_c[p] = ((1.0 - dt) * c0 + dt * r0) * idt;
   }
   if (!cf.out3) return;   // (uniform across the grid)
-  __shared__ double red[3][TB / 32];
-  __shared__ bool last;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int a = 0; a < 3; ++a) {
-    double v = cmx[a];
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (lane == 0) red[a][w] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < 3) {
-    double v = 0;
-    for (int q = 0; q < TB / 32; ++q) v = fmax(v, red[threadIdx.x][q]);
-    umax_atomic(cf.out3 + threadIdx.x, v);
-    __threadfence();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(cf.ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    volatile double* r3 = cf.out3;
-    double cfl = INFINITY;
-    for (int a = 0; a < 3; ++a) {
-      const double m = r3[a] / h;
-      if (m > 0) cfl = fmin(cfl, h / (6.0 * cf.chi * m));
-      r3[a] = 0.0;   // ready for the slot's next use
+  cfl_finish(cmx, h, cf);
+}
+
+// The same right-hand sides over the M+ list (R7 order) instead of the whole box: per M+ point the
+// nine slope-validity bits (axis a, offset o = 1..3: the position is in the box and it and both of its
+// neighbours along a are in N+, with the face-ghost rule of flux_rhs_kernel) are precomputed once per
+// context (slope_mask_kernel), so the kernel neither loads the 15 stencil flags nor evaluates the N+
+// logic, and no warp diverges on the M+ test.  The box part (rollback copy, zeros off M+) is a plain
+// streaming loop over all points by the same threads.
+__device__ __forceinline__ unsigned slope_bits(const uint8_t* __restrict__ flags, int n, long p, int i, int j, int k) {
+  unsigned m = 0;
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const int cd = ax == 0 ? i : (ax == 1 ? j : k);
+    const long st = ax == 0 ? (long)n * n : (ax == 1 ? (long)n : 1L);
+    uint8_t Fr[5];
+#pragma unroll
+    for (int o = 0; o < 5; ++o) {
+      const int pos = cd + o - 2;
+      Fr[o] = pos >= 0 && pos < n ? flags[p + (o - 2) * st] : (uint8_t)0;
     }
-    *cf.dt_out = fmin(fmin(cf.dt_prev, cf.cap), fmin(cfl, 0.5 * h * h));
-    *cf.ticket = 0u;
+    bool np[5];
+#pragma unroll
+    for (int o = 0; o < 5; ++o) {
+      const int pos = cd + o - 2;
+      if (pos >= 0 && pos < n) np[o] = Fr[o] & F_NPLUS;
+      else if (pos == -1) np[o] = o + 1 < 5 && (Fr[o + 1 < 5 ? o + 1 : 4] & F_MPLUS);
+      else if (pos == n) np[o] = o >= 1 && (Fr[o >= 1 ? o - 1 : 0] & F_MPLUS);
+      else np[o] = false;
+    }
+#pragma unroll
+    for (int o = 1; o <= 3; ++o) {
+      const int pos = cd + o - 2;
+      if (pos >= 0 && pos < n && np[o] && np[o - 1] && np[o + 1]) m |= 1u << (3 * ax + o - 1);
+    }
   }
+  return m;
+}
+
+__global__ void slope_mask_kernel(const uint8_t* __restrict__ flags, const int64_t* __restrict__ mlist, long nm, int n,
+                                  uint16_t* __restrict__ mask) {
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < nm; q += (long)gridDim.x * blockDim.x) {
+    const long p = mlist[q];
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    mask[q] = (uint16_t)slope_bits(flags, n, p, i, j, k);
+  }
+}
+
+__global__ void __launch_bounds__(TB, STENCIL_MINB) flux_rhs_list_kernel(
+    const double* __restrict__ rho, const double* __restrict__ c, const uint8_t* __restrict__ flags,
+    const int64_t* __restrict__ mlist, const uint16_t* __restrict__ smask, long nm, int n, double h, double dt,
+    double chi, double* __restrict__ fq_rho, double* __restrict__ fq_c, double* __restrict__ backup,
+    double* __restrict__ zero6, CflFuse cf) {
+  pdl_prologue();
+  const long nn = (long)n * n * n;
+  const long tid = blockIdx.x * (long)blockDim.x + threadIdx.x, nth = (long)gridDim.x * blockDim.x;
+  const double ih = 1.0 / h, idt = 1.0 / dt;
+  if (zero6 && blockIdx.x == 0 && threadIdx.x < 9) zero6[threadIdx.x] = 0.0;   // the step's statistics, clamp max, mass hi
+  for (long p = tid; p < nn; p += nth) {
+    if (backup) {   // the step's rollback copy of the state (speculative PKS graphs)
+      backup[p] = rho[p];
+      backup[nn + p] = c[p];
+    }
+    if (!(flags[p] & F_MPLUS)) {
+      fq_rho[p] = 0.0;
+      fq_c[p] = 0.0;
+    }
+  }
+  double cmx[3] = {0.0, 0.0, 0.0};
+  for (long q = tid; q < nm; q += nth) {
+    const long p = mlist[q];
+    const unsigned m = smask[q];
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    const double r0 = rho[p], c0 = c[p];
+    double g = 0.0;
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      const int cd = ax == 0 ? i : (ax == 1 ? j : k);
+      const long st = ax == 0 ? (long)n * n : (ax == 1 ? (long)n : 1L);
+      double R[5];
+#pragma unroll
+      for (int o = 0; o < 5; ++o) {
+        const int pos = cd + o - 2;
+        R[o] = pos >= 0 && pos < n ? rho[p + (o - 2) * st] : 0.0;
+      }
+      const double cE = cd + 1 < n ? c[p + st] : 0.0, cW = cd >= 1 ? c[p - st] : 0.0;   // 0 outside, as valat
+      if (cf.out3) cmx[ax] = fmax(cmx[ax], fmax(fabs(cE - c0), fabs(c0 - cW)));
+      auto sl = [&](int o) -> double {   // h x the slope at offset o - 2 (o = 1, 2, 3), as slope_h
+        if (!((m >> (3 * ax + o - 1)) & 1u)) return 0.0;
+        return minmod3(2.0 * (R[o + 1] - R[o]), 0.5 * (R[o + 1] - R[o - 1]), 2.0 * (R[o] - R[o - 1]));
+      };
+      const double gE = (cE - c0) * ih, gW = (c0 - cW) * ih;   // upwind choice: the sign of the difference
+      const double s0 = sl(2);
+      const double rhoE = gE > 0 ? r0 + 0.5 * s0 : R[3] - 0.5 * sl(3);
+      const double rhoW = gW > 0 ? R[1] + 0.5 * sl(1) : r0 - 0.5 * s0;
+      g += (chi * rhoE * gE - chi * rhoW * gW) * ih;
+    }
+    fq_rho[p] = (r0 - dt * g) * idt;
+    fq_c[p] = ((1.0 - dt) * c0 + dt * r0) * idt;
+  }
+  if (!cf.out3) return;   // (uniform across the grid)
+  cfl_finish(cmx, h, cf);
 }
 
 // combined Green RHS (R20): q_r = fq_r on M+, (I/dt - Δ_h)[u_γ,r] on the band, 0 elsewhere
@@ -283,6 +394,48 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8
       if (f & F_MPLUS) v = fq[t];
       else if (f & F_BAND) v = lop_gamma(gmap, ug + (size_t)r * ng, n, i, j, k, diag, off);
       q[t] = v;
+    }
+  }
+}
+
+// The same combined RHS with the band part over the band list: a streaming pass writes fq on M+ and 0
+// off M+ ∪ band; the band points (never in M+) take (I/dt - Δ_h)[u_γ,r] from one thread each, whose
+// seven gmap lookups are shared by the right-hand sides.
+__global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_list_kernel(
+    const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
+    long nband, int n, const double* __restrict__ fq, const double* __restrict__ ug, int64_t ng, double* q, int nrhs,
+    double diag, double off) {
+  pdl_prologue();
+  const long nn = (long)n * n * n;
+  const long tid = blockIdx.x * (long)blockDim.x + threadIdx.x, nth = (long)gridDim.x * blockDim.x;
+  for (long p = tid; p < nn; p += nth) {
+    const uint8_t f = flags[p];
+    if (f & F_BAND) continue;
+    for (int r = 0; r < nrhs; ++r) {
+      const size_t t = (size_t)r * nn + p;
+      q[t] = (f & F_MPLUS) ? fq[t] : 0.0;
+    }
+  }
+  for (long b = tid; b < nband; b += nth) {
+    const long p = band[b];
+    int i, j, k;
+    ijk(p, n, i, j, k);
+    const int g0 = gmap[p];
+    int gn[6];
+    const int di[6] = {1, -1, 0, 0, 0, 0}, dj[6] = {0, 0, 1, -1, 0, 0}, dk[6] = {0, 0, 0, 0, 1, -1};
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      const int a = i + di[s], bb = j + dj[s], c = k + dk[s];
+      gn[s] = interior(n, a, bb, c) ? gmap[flat(n, a, bb, c)] : -1;
+    }
+    for (int r = 0; r < nrhs; ++r) {   // as lop_gamma: diag v(p) - off Σ_neighbours v, γ entries only
+      const double* v = ug + (size_t)r * ng;
+      const double acc = g0 >= 0 ? diag * v[g0] : 0.0;
+      double nb = 0.0;
+#pragma unroll
+      for (int s = 0; s < 6; ++s)
+        if (gn[s] >= 0) nb += v[gn[s]];
+      q[(size_t)r * nn + p] = acc - off * nb;
     }
   }
 }
@@ -509,9 +662,28 @@ cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, do
     cf.cap = cap;
     cf.dt_out = dt_out;
   }
+  static const bool use_list = [] {   // DPM_FLUX_LIST=0: the whole-box kernel
+    const char* v = getenv("DPM_FLUX_LIST");
+    return !(v && atoi(v) == 0);
+  }();
   DPM_COUNT_LAUNCH(1);
+  if (use_list && ctx->mplus_slope) {
+    const long nm = ctx->counts[DPM_SET_MPLUS];
+    return launch_pdl(flux_rhs_list_kernel, grid_for(nm), TB, 0, s, rho, c, (const uint8_t*)ctx->flags,
+                      (const int64_t*)ctx->lists[DPM_SET_MPLUS], (const uint16_t*)ctx->mplus_slope, nm, ctx->n, ctx->h,
+                      dt, chi, fq_rho, fq_c, backup, zero6, cf);
+  }
   return launch_pdl(flux_rhs_kernel, grid_for(nn), TB, 0, s, rho, c, (const uint8_t*)ctx->flags, ctx->n, ctx->h, dt, chi,
                     fq_rho, fq_c, backup, zero6, cf);
+}
+
+cudaError_t launch_slope_mask(dpm_ctx* ctx, cudaStream_t s) {
+  const long nm = ctx->counts[DPM_SET_MPLUS];
+  cudaError_t e = cudaMalloc(&ctx->mplus_slope, std::max<long>(nm, 1) * sizeof(uint16_t));
+  if (e != cudaSuccess) return e;
+  DPM_COUNT_LAUNCH(1);
+  slope_mask_kernel<<<grid_for(nm), TB, 0, s>>>(ctx->flags, ctx->lists[DPM_SET_MPLUS], nm, ctx->n, ctx->mplus_slope);
+  return cudaGetLastError();
 }
 
 // sequential coupling (dpm_pks_params.coupling = 1): f_c / dt = ((1 - dt) c + dt ρ̄^{i+1}) / dt on M+
@@ -534,7 +706,16 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
                              cudaStream_t s) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
+  static const bool use_list = [] {   // DPM_GREEN_LIST=0: the whole-box kernel
+    const char* v = getenv("DPM_GREEN_LIST");
+    return !(v && atoi(v) == 0);
+  }();
   DPM_COUNT_LAUNCH(1);
+  if (use_list)
+    return launch_pdl(green_rhs_list_kernel, grid_for(nn / 2), TB, 0, s, (const uint8_t*)ctx->flags,
+                      (const int32_t*)ctx->gmap, (const int64_t*)ctx->lists[DPM_SET_BAND],
+                      (long)ctx->counts[DPM_SET_BAND], ctx->n, fq, u_gamma, (int64_t)ctx->counts[DPM_SET_GAMMA], q,
+                      nrhs, diag, off);
   return launch_pdl(green_rhs_kernel, grid_for(nn), TB, 0, s, (const uint8_t*)ctx->flags, (const int32_t*)ctx->gmap,
                     ctx->n, fq, u_gamma, (int64_t)ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
 }

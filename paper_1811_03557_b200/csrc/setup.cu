@@ -505,6 +505,7 @@ dpm_status setup_point_sets(dpm_ctx* ctx) {
   DPM_COUNT_LAUNCH(1);
   ginpos_kernel<<<(ngin + 255) / 256, 256, 0, s>>>(ctx->gin_pos, ctx->gmap, ctx->lists[DPM_SET_GAMMA_IN], ngin);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
+  DPM_CUDA_TRY(ctx, launch_slope_mask(ctx, s));
   DPM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
   return DPM_OK;
 }
