@@ -869,13 +869,19 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
   const long plane = blockIdx.x;   // field * n + a
   const int a = (int)(plane % n), t = threadIdx.x;
   double* g = u + (size_t)plane * n * n;
-  for (int e = t; e < PSN * PSN; e += blockDim.x) {
-    const int r = e / PSN, c = e % PSN;
-    const bool in = r < n && c < n;
-    S[r * PSP + c] = in ? __ldg(S_g + r * n + c) : 0.0;
-    P[r * PSP + c] = in ? g[(size_t)r * n + c] : 0.0;
+  {   // every load in flight at once (cp.async, zero-filled outside the n x n corner)
+    const unsigned sS = (unsigned)__cvta_generic_to_shared(S), sP = (unsigned)__cvta_generic_to_shared(P);
+#pragma unroll 4
+    for (int e = t; e < PSN * PSN; e += PS_THREADS) {
+      const int r = e / PSN, c = e % PSN;
+      const bool in = r < n && c < n;
+      cp_async8(sS + 8u * (unsigned)(r * PSP + c), in ? S_g + r * n + c : S_g, in);
+      cp_async8(sP + 8u * (unsigned)(r * PSP + c), in ? g + (size_t)r * n + c : g, in);
+    }
+    cp_async_commit();
   }
   for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
+  asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   const bool tc = ps_dmma() && (n & 1) == 0;
   if (tc) ps_apply_dmma(S, P, n); else ps_apply(S, P, n);
