@@ -475,7 +475,11 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   const long long l0 = (long long)g_dpm_launches.load();
   DPM_CUDA_TRY(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   dpm_status st = DPM_OK;
-  const int pdl = ctx->n <= 32;   // programmatic dependent launch within the step graph (dpm_internal.h)
+  static const int pdl_nmax = [] {   // programmatic dependent launch within the step graph (dpm_internal.h)
+    const char* v = getenv("DPM_PDL_NMAX");
+    return v ? atoi(v) : 64;
+  }();
+  const int pdl = ctx->n <= pdl_nmax;
   g_pdl_scope += pdl;
   for (int i = 0; i < K && st == DPM_OK; ++i)
     st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs);

@@ -157,15 +157,21 @@ extern std::atomic<long long> g_dpm_launches;
 // Programmatic dependent launch (PDL) for the chain of small kernels of a PKS step (and every other use
 // of these kernels): they are launched with cudaLaunchAttributeProgrammaticStreamSerialization and begin
 // with pdl_prologue(): griddepcontrol.wait (before any global memory access; a no-op when launched
-// without the attribute) then griddepcontrol.launch_dependents, so the next kernel of the stream is
-// launched while this one runs and its CTAs wait on the GPU instead of the launch latency being paid
-// between the two.  Used only inside the PKS step graphs of small grids (pdl_scope, set by dpm_pks_step
-// for n <= 32): measured +6% steps/s at cfg2 (n = 32) but -23% at cfg3 (n = 64), where the early-launched
-// dependents' waiting CTAs compete with the running grid.  DPM_PDL=0 disables, DPM_PDL=2 forces it for
-// every launch of these kernels.
+// without the attribute).  No explicit griddepcontrol.launch_dependents: the next kernel is triggered
+// as this one's blocks exit, so its launch is prepared during this kernel's tail instead of after the
+// kernel boundary, and no dependent CTA waits on an SM while this grid still needs it.  Used inside the
+// PKS step graphs of n <= 64 (pdl_scope, set by dpm_pks_step; DPM_PDL_NMAX overrides the bound).
+// Measured (tools/pdl_ab.sh): cfg2 +6-7% and cfg3 +1.7% steps/s over no PDL; triggering at kernel start
+// (-DDPM_PDL_TRIGGER=1) instead costs 9% at cfg3, where the early dependents' waiting CTAs compete with
+// the running grid.  DPM_PDL=0 disables, DPM_PDL=2 forces it for every launch of these kernels.
+#ifndef DPM_PDL_TRIGGER
+#define DPM_PDL_TRIGGER 0
+#endif
 __device__ __forceinline__ void pdl_prologue() {
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#if DPM_PDL_TRIGGER
   asm volatile("griddepcontrol.launch_dependents;\n" :::);
+#endif
 }
 bool pdl_enabled();
 extern thread_local int g_pdl_scope;   // > 0 while enqueueing a small-grid PKS step
