@@ -842,6 +842,27 @@ __device__ __forceinline__ void st_async(unsigned remote, double v, unsigned rem
 #define FACR_PHASE_TIMING 0
 #endif
 constexpr int FACR_TCTAS = 4096, FACR_TPH = 9;
+// Speed-of-light switches (timing experiments only, tools/plane_sol.sh; results are wrong when any is
+// set): skip the half-plane load, phase 1, the two transforms, the phase-3 recurrences, phase 5 or
+// the store.
+#ifndef PLANE_SOL_NOLOAD
+#define PLANE_SOL_NOLOAD 0
+#endif
+#ifndef PLANE_SOL_NOP1
+#define PLANE_SOL_NOP1 0
+#endif
+#ifndef PLANE_SOL_NOXF
+#define PLANE_SOL_NOXF 0
+#endif
+#ifndef PLANE_SOL_NOP3
+#define PLANE_SOL_NOP3 0
+#endif
+#ifndef PLANE_SOL_NOP5
+#define PLANE_SOL_NOP5 0
+#endif
+#ifndef PLANE_SOL_NOSTORE
+#define PLANE_SOL_NOSTORE 0
+#endif
 #if FACR_PHASE_TIMING
 __device__ unsigned long long g_facr_ph[FACR_TCTAS][FACR_TPH];
 #define FACR_MARK(k)                                                              \
@@ -884,6 +905,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   for (int i = t; i < N; i += PTHR) lam[i] = lam_g[i];
   {
     const unsigned sb = (unsigned)__cvta_generic_to_shared(P);
+#if !PLANE_SOL_NOLOAD
 #pragma unroll 16
     for (int e = t; e < N * PHC; e += PTHR) {
       // a warp covers 32 consecutive z of one row: lanes 0-15 the odd z (kept columns), lanes
@@ -893,6 +915,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (unsigned)(r * PPITCH + c)),
                    "l"(gp + (size_t)r * N + z));
     }
+#endif
     if (rank == 0)   // z = 64 (the partner's first column; an L2 hit, the partner reads it too)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sb + 8u * (unsigned)(t * PPITCH + PHC)),
                    "l"(gp + (size_t)t * N + PHC));
@@ -906,7 +929,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   const double hsa = h2 * (inv_dt + lam[a]);
   const double beta = 4.0 + hsa;
   // (1) r_i = gs (β g_z[y] - g_z[y-1] - g_z[y+1] + g_{z-1}[y] + g_{z+1}[y]),  z = 2i + 1,  i = lane
-  {
+  if (!PLANE_SOL_NOP1) {
     const int y0 = 32 * warp;
     const double* gk = P + lane;             // kept column i
     const double* gl = P + 32 + lane;        // eliminated j = i   (z - 1)
@@ -931,7 +954,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
 #if PLANE_YDST_INLINE
   plane_ydst<true>(P);
 #else
-  plane_ydst_call<true>(P);
+  if (!PLANE_SOL_NOXF) plane_ydst_call<true>(P);
 #endif
   __syncthreads();
   FACR_MARK(3);
@@ -948,10 +971,12 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     double v[M];                                           // the row, in registers until the end
 #pragma unroll
     for (int i = 0; i < M; ++i) v[i] = ys * row[i];
+    if (!PLANE_SOL_NOP3) {
 #pragma unroll
-    for (int i = 1; i < M; ++i) v[i] = fma(mu, v[i - 1], v[i]);
+      for (int i = 1; i < M; ++i) v[i] = fma(mu, v[i - 1], v[i]);
 #pragma unroll
-    for (int i = M - 2; i >= 0; --i) v[i] = fma(mu, v[i + 1], v[i]);
+      for (int i = M - 2; i >= 0; --i) v[i] = fma(mu, v[i + 1], v[i]);
+    }
     double muM = mu;                                       // μ^M, M = 32
 #pragma unroll
     for (int q = 0; q < 5; ++q) muM *= muM;
@@ -978,6 +1003,10 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     const double A = rank == 0 ? -c2 : u31 / den - c2;
     const double B = rank == 0 ? u32 / den : -(a31 + u31 * gL0) * sm / den;
     const double imu = 1.0 / mu;
+    if (PLANE_SOL_NOP3) {
+#pragma unroll
+      for (int i = 0; i < M; ++i) row[i] = v[i] + A + B;
+    } else {
     double pa = mu, pb = mu2M1;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -992,13 +1021,14 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
       ga *= mu;
       gb *= imu;
     }
+    }
   }
   __syncthreads();
   FACR_MARK(4);
 #if PLANE_YDST_INLINE
   plane_ydst<true>(P);
 #else
-  plane_ydst_call<true>(P);
+  if (!PLANE_SOL_NOXF) plane_ydst_call<true>(P);
 #endif
   __syncthreads();
   FACR_MARK(5);
@@ -1015,7 +1045,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   // (5) eliminated column j = 16 (warp/2) + 2 (lane%8) + warp%2, row segment s = lane/8:
   //     [0,33) [33,64) [64,97) [97,128); a half-warp holds 8 columns of one parity x 2 segments
   //     whose start rows are ≡ 0, 1 mod 16: 16 distinct 8-byte bank pairs
-  {
+  if (!PLANE_SOL_NOP5) {
     const int j = 16 * (warp >> 1) + 2 * (lane & 7) + (warp & 1), s = lane >> 3;
     const int kb = (s >> 1) * 64 + (s & 1) * 33, L = (s & 1) ? 31 : 33;
     const double muy = 2.0 / (beta + sqrt((beta - 2.0) * (beta + 2.0)));
@@ -1084,7 +1114,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   }
   __syncthreads();
   FACR_MARK(7);
-  for (int e = t; e < N * PHC; e += PTHR) {   // same lane -> (column, z) map as the load
+  for (int e = t; e < (PLANE_SOL_NOSTORE ? 0 : N * PHC); e += PTHR) {   // same lane -> (column, z) map as the load
     const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
     const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
     __stcg(gp + (size_t)r * N + z, P[r * PPITCH + c]);
