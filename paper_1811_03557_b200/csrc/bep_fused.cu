@@ -91,11 +91,32 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
     if ((e = cudaMalloc(&ctx->bepf_qb, std::max<int64_t>(1, nb) * nc * sizeof(double))) != cudaSuccess) return e;
     ctx->bepf_cols = nc;
   }
+  static const bool zbox = [] {
+    const char* v = getenv("DPM_BEP_ZBOX");
+    return !(v && atoi(v) == 0);
+  }();
+  if (zbox) {
+    // (1') q_c scattered into boxes that stay zero off the band: every chunk writes the same band
+    // positions, so the boxes are zeroed once, when allocated; (2') dense forward x pass box -> work
+    if (ctx->bepf_zcols < nc) {
+      if (ctx->bepf_zbox) cudaFree(ctx->bepf_zbox);
+      ctx->bepf_zbox = nullptr;
+      ctx->bepf_zcols = 0;
+      const size_t bytes = (size_t)nc * ctx->n * ctx->n * ctx->n * sizeof(double);
+      if ((e = cudaMalloc(&ctx->bepf_zbox, bytes)) != cudaSuccess) return e;
+      if ((e = cudaMemsetAsync(ctx->bepf_zbox, 0, bytes, s)) != cudaSuccess) return e;
+      ctx->bepf_zcols = nc;
+    }
+    if ((e = launch_potential_scatter(ctx, ctx->E + (size_t)c0 * ng, ng, ctx->bepf_zbox, nc, s)) != cudaSuccess)
+      return e;
+    if ((e = dst128_pass(0, ctx->bepf_zbox, ctx->work, nc, ctx->plan.atab128, s)) != cudaSuccess) return e;
+  } else {
   // (1) band values of q_c = χ_{M-}(I/dt - Δ_h)[E_c], x-line-major
   if ((e = launch_potential_band(ctx, ctx->E + (size_t)c0 * ng, ng, ctx->bepf_qb, nc, ctx->bepf_bpos, s)) != cudaSuccess)
     return e;
   // (2) forward x DST-I gathered from the band values into the work boxes
   if ((e = dst128_xpass_sparse(ctx->work, nc, ctx->bepf_btab, ctx->bepf_qb, nb, s)) != cudaSuccess) return e;
+  }
   // (3) fused plane pass, (4) inverse x DST-I, (5) γ gather and B = E_in - Tr_γin u
   if ((e = dst_solve_middle(ctx->plan, ctx->work, nc, s)) != cudaSuccess) return e;
   if ((e = dst128_pass(0, ctx->work, ctx->work, nc, ctx->plan.atab128, s)) != cudaSuccess) return e;
@@ -103,7 +124,7 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
 }
 
 void bep_fused_free(dpm_ctx* c) {
-  void* ptrs[] = {c->bepf_btab, c->bepf_bpos, c->bepf_qb};
+  void* ptrs[] = {c->bepf_btab, c->bepf_bpos, c->bepf_qb, c->bepf_zbox};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

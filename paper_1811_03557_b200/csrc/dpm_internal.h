@@ -142,6 +142,8 @@ struct dpm_ctx {
   int32_t* bepf_bpos = nullptr;      // [n_band] line-major position of band point b
   double* bepf_qb = nullptr;         // [cols][n_band] band values of the potential RHS (line-major)
   int bepf_cols = 0;
+  double* bepf_zbox = nullptr;       // [zcols][n^3] boxes that are zero off the band (zero-box mode)
+  int bepf_zcols = 0;
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
@@ -234,6 +236,9 @@ dpm_status setup_point_sets(dpm_ctx* ctx);
 dpm_status setup_geometry(dpm_ctx* ctx);
 
 // ops.cu
+// scatter of the band values only (q must already be zero off the band)
+cudaError_t launch_potential_scatter(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
+                                     cudaStream_t s);
 cudaError_t launch_potential_rhs(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
                                  cudaStream_t s);
 cudaError_t launch_potential_band(const dpm_ctx* ctx, const double* v, int64_t ldv, double* qb, int nrhs,

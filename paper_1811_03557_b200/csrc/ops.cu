@@ -590,11 +590,17 @@ int grid_reduce(long work) { return (int)std::max<long>(1, std::min<long>((work 
 
 cudaError_t launch_potential_rhs(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
                                  cudaStream_t s) {
-  const int n = ctx->n;
-  const size_t field = (size_t)n * n * n;
+  const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   cudaError_t e = cudaMemsetAsync(q, 0, field * nrhs * sizeof(double), s);
   if (e != cudaSuccess) return e;
+  return launch_potential_scatter(ctx, v, ldv, q, nrhs, s);
+}
+
+cudaError_t launch_potential_scatter(const dpm_ctx* ctx, const double* v, int64_t ldv, double* q, int nrhs,
+                                     cudaStream_t s) {
+  const int n = ctx->n;
   const int64_t nb = ctx->counts[DPM_SET_BAND];
+  if (nb * nrhs == 0) return cudaSuccess;
   const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
   DPM_COUNT_LAUNCH(1);
   potential_rhs_kernel<<<grid_for(nb * nrhs), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, q, nrhs, n,

@@ -24,4 +24,4 @@ for _ in range(5):
     e1.synchronize()
     ts.append(e0.elapsed_time(e1))
 ms = statistics.median(ts)
-print(json.dumps({"columns_ms": ms, "columns_per_s": K / ms * 1e3, "env": os.environ.get("DPM_BEP_SPARSE2", "1")}))
+print(json.dumps({"columns_ms": ms, "columns_per_s": K / ms * 1e3, "zbox": os.environ.get("DPM_BEP_ZBOX", "1")}))
