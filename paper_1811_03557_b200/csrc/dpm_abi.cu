@@ -429,10 +429,23 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
     DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
     return DPM_OK;
   }
-  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+  // DPM_STEP_SKIP (timing experiments only, tools/pks_skip.py, results wrong; compiled in only with
+  // -DDPM_TIMING_SKIPS=1): bit 0 the particular solve, 1 the Green solve, 2 trace + least squares +
+  // extension, 3 the Green RHS, 4 the restriction
+#if DPM_TIMING_SKIPS
+  static const int skip = [] {
+    const char* v = getenv("DPM_STEP_SKIP");
+    return v ? atoi(v) : 0;
+  }();
+#else
+  constexpr int skip = 0;
+#endif
+  if (!(skip & 1)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
   // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp (its magnitude -> slot[10])
+  if (!(skip & 4)) {
   DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
   DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec, coef, ug, 2, prm->clamp, s, slot + 10));
+  }
   // the step's BEP least-squares residual ||B C - g|| / ||g|| -> slot[11], on a forked branch
   // of the graph (off the critical path), joined before the step ends (gvec / coef are reused)
   static const bool resid_on = [] {   // DPM_STEP_RESID=0: no residual (lsq_resid logged as NaN)
@@ -451,9 +464,9 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[1], ctx->side_stream));
   }
   // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
-  DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
-  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
-  DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
+  if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
+  if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+  if (!(skip & 16)) DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
   if (fork) DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
   return DPM_OK;
 }

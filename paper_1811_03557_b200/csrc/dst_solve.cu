@@ -621,7 +621,10 @@ __global__ void sinmat_kernel(double* S, int n) {   // S[j][k] = sin(π (j+1)(k+
 
 // P <- S^T P in place (S symmetric); thread (rb, cb) = (t / 16, t % 16) owns rows 4rb..4rb+3 and
 // columns cb + 16j; S and P are zero-padded to 64 x 64.  (512 threads with 2 x 4 tiles: slower.)
-constexpr int PS_THREADS = 256;
+#ifndef PS_THREADS_CFG
+#define PS_THREADS_CFG 256
+#endif
+constexpr int PS_THREADS = PS_THREADS_CFG;
 __device__ __forceinline__ void ps_apply(const double* S, double* P, int n) {
   const int t = threadIdx.x, rb = t >> 4, cb = t & 15;
   double acc[4][4];
@@ -1113,15 +1116,23 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     cudaError_t e;
     const long long pts = (long long)nf * (long long)fe;
     auto pass = [&](int k, const double* in) { return timed(p, k, pts, s, [&] { return run_pass(p, k, in, ui, nf, inv_dt, scale, s); }); };
-    if ((e = pass(0, qi)) != cudaSuccess) return e;
+    // DPM_SKIP_XPASS / DPM_SKIP_PLANE = 1: timing experiments only (tools/pks_skip.py), results wrong;
+    // compiled in only with -DDPM_TIMING_SKIPS=1
+#if DPM_TIMING_SKIPS
+    static const bool skip_x = getenv("DPM_SKIP_XPASS") && atoi(getenv("DPM_SKIP_XPASS")) == 1;
+    static const bool skip_m = getenv("DPM_SKIP_PLANE") && atoi(getenv("DPM_SKIP_PLANE")) == 1;
+#else
+    constexpr bool skip_x = false, skip_m = false;
+#endif
+    if (!skip_x && (e = pass(0, qi)) != cudaSuccess) return e;
     if (p.solver == DPM_SOLVER_DST2_TRIDIAG) {
-      if ((e = middle_passes(p, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
+      if (!skip_m && (e = middle_passes(p, ui, nf, inv_dt, scale, s)) != cudaSuccess) return e;
     } else {
       if ((e = pass(1, ui)) != cudaSuccess) return e;
       if ((e = pass(2, ui)) != cudaSuccess) return e;
       if ((e = pass(1, ui)) != cudaSuccess) return e;
     }
-    if ((e = pass(0, ui)) != cudaSuccess) return e;
+    if (!skip_x && (e = pass(0, ui)) != cudaSuccess) return e;
   }
   if (two) {
     cudaEventRecord(p.ev_join, p.side);
