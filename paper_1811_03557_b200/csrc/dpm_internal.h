@@ -98,7 +98,10 @@ struct dpm_ctx {
   int pks_initialized = 0;
   PassProf prof;
   // PKS step graphs (dpm_pks_step): K speculative steps at a fixed dt captured once and replayed
-  static constexpr int PKS_K = 10;
+#ifndef DPM_PKS_K
+#define DPM_PKS_K 10
+#endif
+  static constexpr int PKS_K = DPM_PKS_K;
   struct PksGraph {
     double dt = 0, chi = 0, cap = 0;
     int k = 0, rule = 0, clamp = 0, coupling = 0, solver = 0;
