@@ -328,6 +328,17 @@ dpm_status dpm_dd_rhs(dpm_ctx* ctx, const double* rho, const double* c, double c
 dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* stream);
 dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const double* fq, double* wk,
                             void* stream);
+/* dpm_dd_lsq_rhs over `noct` config-5 octant contexts of ONE device at once, summed: y = Σ_s M_s g_s (K x 2,
+   DEVICE), the local contribution to C (the caller all-reduces it across ranks as the per-octant y_s).
+   The octants share one canonical geometry, so B_s = B_0 diag(S_s) (their extensions differ only by
+   column signs S_s, read off the extension matrices and required to be exactly ±1), hence
+   Q_s = Q_0 R S_s R^{-1} and  y = D R^{-1} R^{-T} Σ_s S_s R^T (Q_0^T g_s):  one pass over octs[0]'s Q for all
+   2 noct right-hand sides instead of one operator M_s per octant, then K x K products (same result up
+   to rounding, ~κ(R) ε).  wk: DEVICE [noct][2][n^3], the particular solutions in the order of `octs`.
+   DPM_ERR_INVALID if the contexts are not octants of one geometry on one device (same n, box, radius, K,
+   rows) or their extensions are not sign reflections; DPM_ERR_STATE without a factorisation.
+   Asynchronous on stream (the first call per octant pair synchronizes it once to check the signs). */
+dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* wk, double* y, void* stream);
 dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* c, void* stream);
 
 /* Cumulative number of CUDA kernels this library has launched in the process (all

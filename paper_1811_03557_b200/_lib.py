@@ -99,6 +99,7 @@ _sig = {
     "dpm_dd_chol_copy": ([P, C.c_int32, P, P], C.c_int),
     "dpm_dd_rhs": ([P, P, P, C.c_double, P, P], C.c_int),
     "dpm_dd_lsq_rhs": ([P, P, P, P], C.c_int),
+    "dpm_dd_lsq_rhs_shared": ([C.POINTER(P), C.c_int32, P, P, P], C.c_int),
     "dpm_dd_green_rhs": ([P, P, C.c_int32, P, P, P], C.c_int),
     "dpm_dd_restrict": ([P, P, P, P, P], C.c_int),
     "dpm_dd_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),

@@ -269,6 +269,15 @@ class Octant(DPM):
         self._chk(L.lib.dpm_dd_lsq_rhs(self._h, _ptr(_dev_f64(wk, "wk")), _ptr(y), _stream(stream)))
         return y
 
+    def dd_lsq_rhs_shared(self, octs, wk, stream=None):
+        """Σ_s M_s g_s over octant contexts of one device sharing the canonical geometry (this one first):
+        one pass over this octant's Q (dpm_dd_lsq_rhs_shared); wk: [noct][2][n][n][n]."""
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            y = self._t(2, self.K)
+        arr = (C.c_void_p * len(octs))(*[o._h.value for o in octs])
+        self._chk(L.lib.dpm_dd_lsq_rhs_shared(arr, len(octs), _ptr(_dev_f64(wk, "wk")), _ptr(y), _stream(stream)))
+        return y
+
     def dd_green_rhs(self, C, clamp, fq, wk, stream=None):
         self._chk(L.lib.dpm_dd_green_rhs(self._h, _ptr(_dev_f64(C, "C")), clamp, _ptr(_dev_f64(fq, "fq")),
                                          _ptr(_dev_f64(wk, "wk")), _stream(stream)))

@@ -320,6 +320,158 @@ __global__ void dd_ic_kernel(const uint8_t* __restrict__ flags, const int32_t* _
 
 int grid_for(long work) { return (int)std::max<long>(1, std::min<long>((work + TB - 1) / TB, 148L * 16)); }
 
+// ---- one operator pass for all octants of a device (dpm_dd_lsq_rhs_shared) ----------------------------
+// S_s: the column signs of octant s's extension relative to octant 0's (E_s = E_0 diag(S_s): the cap SH and
+// plane Legendre bases are even or odd under each reflection, and the recursions evaluate the reflected
+// arguments to exactly ± the same values).  Per column: the γ point of octant 0's largest |E|, and the
+// ratio there, required to be exactly ±1 (*bad set otherwise).
+__global__ void dd_sign_kernel(const double* __restrict__ E0, const double* __restrict__ Es, int64_t ng,
+                               double* sign, int* bad) {
+  const int c = blockIdx.x;
+  const double* a = E0 + (size_t)c * ng;
+  double best = -1.0;
+  int64_t arg = 0;
+  for (int64_t g = threadIdx.x; g < ng; g += blockDim.x) {
+    const double v = fabs(a[g]);
+    if (v > best) { best = v; arg = g; }
+  }
+  __shared__ double sb[TB];
+  __shared__ int64_t sa[TB];
+  sb[threadIdx.x] = best;
+  sa[threadIdx.x] = arg;
+  __syncthreads();
+  for (int o = TB / 2; o; o >>= 1) {
+    if (threadIdx.x < o && (sb[threadIdx.x + o] > sb[threadIdx.x] ||
+                            (sb[threadIdx.x + o] == sb[threadIdx.x] && sa[threadIdx.x + o] < sa[threadIdx.x]))) {
+      sb[threadIdx.x] = sb[threadIdx.x + o];
+      sa[threadIdx.x] = sa[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double e0 = a[sa[0]], es = Es[(size_t)c * ng + sa[0]];
+    const double r = e0 != 0.0 ? es / e0 : 1.0;
+    if (r != 1.0 && r != -1.0) atomicOr(bad, 1);
+    sign[c] = r < 0 ? -1.0 : 1.0;
+  }
+}
+
+// Tall-skinny products of the shared apply on the fp64 tensor pipe (DMMA.m8n8k4):
+//   part[split][r][c] = Σ_{i in split} A[c lda + i] X[r m + i]     c < M, r < NR <= 16, i < m
+// (A given as M rows of length >= m: the columns of Q_0, or the columns of an upper-triangular K x K
+// factor read as the rows of its transpose, TRI = 1 keeping i <= c).  A CTA = 8 warps on one 32-row tile
+// (4 m-tiles x 2 n-tiles of 8 per warp) and one i-range of ICH; warp w takes its k-groups of 16 i
+// (w, w + 8, ...), lane (g, t) holding i = i0 + 4t + j in k-step j (the same permutation of k for the A
+// and B fragments, so each lane reads 4 consecutive doubles per row).  The 8 warps' partial tiles are
+// summed in shared memory in warp order; the splits by dd_reduce_kernel in split order (deterministic).
+constexpr int TS_ICH = 2048;
+template <int TRI>
+__global__ void __launch_bounds__(256) dd_gemm_ts_kernel(const double* __restrict__ A, int64_t lda, int M,
+                                                         const double* __restrict__ X, int64_t m, int NR,
+                                                         double* __restrict__ part) {
+  __shared__ double red[8][32][17];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int c0 = blockIdx.x * 32;
+  const int64_t ib = (int64_t)blockIdx.y * TS_ICH, ie = m < ib + TS_ICH ? m : ib + TS_ICH;
+  double acc[4][2][2];
+  const double* ar[4];
+  int cc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    cc[q] = c0 + 8 * q + g;
+    ar[q] = A + (size_t)min(cc[q], M - 1) * lda;
+    acc[q][0][0] = acc[q][0][1] = acc[q][1][0] = acc[q][1][1] = 0.0;
+  }
+  const double* xr[2];
+  bool xv[2];
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    xv[nt] = 8 * nt + g < NR;
+    xr[nt] = X + (size_t)min(8 * nt + g, NR - 1) * m;
+  }
+  for (int64_t i0 = ib + 16 * warp; i0 < ie; i0 += 16 * 8) {
+    double a[4][4], b[2][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t i = i0 + 4 * t + j;
+      const bool in = i < ie;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = in && cc[q] < M && (TRI != 1 || i <= cc[q]);
+        a[q][j] = ok ? __ldg(ar[q] + i) : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[nt][j] = (in && xv[nt]) ? __ldg(xr[nt] + i) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                       : "+d"(acc[q][nt][0]), "+d"(acc[q][nt][1])
+                       : "d"(a[q][j]), "d"(b[nt][j]));
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      red[warp][8 * q + g][8 * nt + 2 * t] = acc[q][nt][0];
+      red[warp][8 * q + g][8 * nt + 2 * t + 1] = acc[q][nt][1];
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * 16; e += 256) {
+    const int cl = e & 31, r = e >> 5;
+    if (c0 + cl >= M || r >= NR) continue;
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][cl][r];
+    part[((size_t)blockIdx.y * NR + r) * M + c0 + cl] = v;
+  }
+}
+
+// out[o][c] = Σ_{v ≡ o mod nout} w[v / nout][c] Σ_split part[split][v][c]   (w nullable: 1), fixed order
+__global__ void dd_reduce_kernel(const double* __restrict__ part, int nsplit, int NR, int M,
+                                 const double* __restrict__ w, int nout, double* __restrict__ out) {
+  const long tot = (long)nout * M;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
+    const int o = (int)(e / M), c = (int)(e - (long)o * M);
+    double acc = 0.0;
+    for (int v = o; v < NR; v += nout) {
+      double sv = 0.0;
+      for (int sp = 0; sp < nsplit; ++sp) sv += part[((size_t)sp * NR + v) * M + c];
+      acc = w ? fma(w[(size_t)(v / nout) * M + c], sv, acc) : acc + sv;
+    }
+    out[e] = acc;
+  }
+}
+
+// y[r][c] = D[c] Σ_{i >= c} W[i K + c] V[r][i]  (W upper col-major; nr <= 2): 32 outputs x 8 i-slices per
+// block (coalesced over c), slices summed in order
+__global__ void __launch_bounds__(256) dd_upper_apply_kernel(const double* __restrict__ W, int K,
+                                                             const double* __restrict__ V, int nr,
+                                                             const double* __restrict__ D, double* __restrict__ y) {
+  __shared__ double red[8][2][32];
+  const int cl = threadIdx.x & 31, sl = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
+  double a0 = 0.0, a1 = 0.0;
+  if (c < K)
+    for (int i = c + sl; i < K; i += 8) {
+      const double wv = W[(size_t)i * K + c];
+      a0 = fma(wv, V[i], a0);
+      if (nr > 1) a1 = fma(wv, V[K + i], a1);
+    }
+  red[sl][0][cl] = a0;
+  red[sl][1][cl] = a1;
+  __syncthreads();
+  if (sl < nr && c < K) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += red[q][sl][cl];
+    y[(size_t)sl * K + c] = D[c] * v;
+  }
+}
+
 // ---- NEXT-3: the paper's two-subdomain DD, Case 1 (concentric, Z ∩ Γ = ∅) ----
 // Pieces: Z (the interface |x| = r1, piece 0, bit 1) and Γ (|x| = r2, piece 1, bit 2).  Ω1 (sub 0):
 // every point of ζ1 is on Z; Ω2 (sub 1): a point of γ ∪ ζ2 is on the nearer sphere (reading R38).
@@ -807,6 +959,79 @@ dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* strea
                                                                 ctx->n_rows, 2, ctx->dd_g);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   DPM_CUDA_TRY(ctx, lsq_gemv(ctx->dd_M, ctx->n_rows, ctx->K, ctx->dd_g, 2, y, s));           // y_s = M_s g_s
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* wk, double* y, void* stream) {
+  DPM_NVTX();
+  if (!octs || noct < 1 || !wk || !y) return DPM_ERR_INVALID;
+  dpm_ctx* o0 = octs[0];
+  dpm_status st = dd_check(o0);
+  if (st != DPM_OK) return st;
+  const int K = o0->K;
+  for (int s = 0; s < noct; ++s) {
+    dpm_ctx* o = octs[s];
+    if (!o || o->dd != 1 || o->device != o0->device || o->n != o0->n || o->lo != o0->lo || o->hi != o0->hi ||
+        o->K != K || o->n_rows != o0->n_rows || o->radius != o0->radius) {
+      o0->err = "dd_lsq_rhs_shared: the contexts are not octants of one canonical geometry on one device";
+      return DPM_ERR_INVALID;
+    }
+    if (!o->have_projection || o->dt_bep != o->dt) { o0->err = "dd_lsq_rhs_shared: no factorisation"; return DPM_ERR_STATE; }
+  }
+  cudaStream_t s = as_stream(stream);
+  const size_t field = (size_t)o0->n * o0->n * o0->n;
+  const int64_t ng = o0->counts[DPM_SET_GAMMA], m = o0->n_rows;
+  const int nv = 2 * noct;
+  // signs of every octant relative to octant 0 (geometry only: computed once per pair)
+  for (int q = 0; q < noct; ++q) {
+    dpm_ctx* o = octs[q];
+    if (o->dd_sign && o->dd_sign_ref == o0) continue;
+    if (!o->dd_sign) DPM_CUDA_TRY(o0, cudaMalloc(&o->dd_sign, (size_t)K * sizeof(double) + 16));
+    int* dbad = reinterpret_cast<int*>(o->dd_sign + K);
+    DPM_CUDA_TRY(o0, cudaMemsetAsync(dbad, 0, sizeof(int), s));
+    DPM_COUNT_LAUNCH(1);
+    dd_sign_kernel<<<K, TB, 0, s>>>(o0->dd_Eraw, o->dd_Eraw, ng, o->dd_sign, dbad);
+    int hbad = 0;
+    DPM_CUDA_TRY(o0, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    DPM_CUDA_TRY(o0, cudaStreamSynchronize(s));
+    if (hbad) { o0->err = "dd_lsq_rhs_shared: the octant extensions are not sign-reflections"; return DPM_ERR_INVALID; }
+    o->dd_sign_ref = o0;
+  }
+  const int nsplit = (int)((m + TS_ICH - 1) / TS_ICH), nsk = (K + TS_ICH - 1) / TS_ICH;
+  const int npart = std::max(1, std::max(nsplit, nsk));
+  const size_t need = ((size_t)nv * m + (size_t)npart * nv * K + (size_t)nv * K + 4 * (size_t)K +
+                       (size_t)noct * K) * sizeof(double);
+  if (o0->dd_shared_bytes < need) {
+    if (o0->dd_shared) cudaFree(o0->dd_shared);
+    o0->dd_shared = nullptr;
+    o0->dd_shared_bytes = 0;
+    DPM_CUDA_TRY(o0, cudaMalloc(&o0->dd_shared, need));
+    o0->dd_shared_bytes = need;
+  }
+  double* G = o0->dd_shared;              // [nv][m]: BEP right-hand sides of all octants
+  double* Pt = G + (size_t)nv * m;        // split-K partials
+  double* Z = Pt + (size_t)npart * nv * K;   // [nv][K]: Q_0^T g_v
+  double* Tz = Z + (size_t)nv * K;        // [2][K]: Σ_s S_s R^T z_s
+  double* Vz = Tz + 2 * (size_t)K;        // [2][K]: R^{-T} Tz
+  double* Sg = Vz + 2 * (size_t)K;        // [noct][K]: the signs, stacked
+  for (int q = 0; q < noct; ++q)
+    DPM_CUDA_TRY(o0, cudaMemcpyAsync(Sg + (size_t)q * K, octs[q]->dd_sign, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  DPM_COUNT_LAUNCH(1);
+  dd_rows_trace_kernel<<<grid_for(m * nv), TB, 0, s>>>(wk, field, o0->lists[DPM_SET_GAMMA], o0->dd_rows, m, nv, G);
+  const size_t KK = (size_t)K * K;
+  const double* R = o0->dd_R + 2 * KK;    // R = R2 R1
+  const double* W2 = o0->dd_R + 4 * KK;   // R^{-1}
+  const unsigned ct = (unsigned)((K + 31) / 32);
+  const int rb = (int)std::min<long>(148L * 8, ((long)K * nv + TB - 1) / TB);
+  DPM_COUNT_LAUNCH(7);
+  dd_gemm_ts_kernel<0><<<dim3(ct, nsplit), 256, 0, s>>>(o0->dd_Q, m, K, G, m, nv, Pt);       // one pass over Q_0
+  dd_reduce_kernel<<<rb, TB, 0, s>>>(Pt, nsplit, nv, K, nullptr, nv, Z);
+  dd_gemm_ts_kernel<1><<<dim3(ct, nsk), 256, 0, s>>>(R, K, K, Z, K, nv, Pt);                  // R^T z_v
+  dd_reduce_kernel<<<rb, TB, 0, s>>>(Pt, nsk, nv, K, Sg, 2, Tz);                              // Σ_s S_s (.)
+  dd_gemm_ts_kernel<1><<<dim3(ct, nsk), 256, 0, s>>>(W2, K, K, Tz, K, 2, Pt);                 // R^{-T}
+  dd_reduce_kernel<<<rb, TB, 0, s>>>(Pt, nsk, 2, K, nullptr, 2, Vz);
+  dd_upper_apply_kernel<<<ct, 256, 0, s>>>(W2, K, Vz, 2, o0->dd_D, y);                        // D R^{-1}
+  DPM_CUDA_TRY(o0, cudaGetLastError());
   return DPM_OK;
 }
 

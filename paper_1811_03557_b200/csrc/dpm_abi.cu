@@ -28,6 +28,7 @@ void free_ctx(dpm_ctx* c) {
   cudaSetDevice(c->device);
   void* ptrs[] = {c->flags, c->gmap, c->gin_pos, c->mplus_slope, c->foot, c->dist, c->E, c->B, c->Q, c->R, c->colscale, c->Mlsq, c->RDinv,
                   c->dd_Eraw, c->dd_assign, c->dd_rows, c->dd_B, c->dd_Q, c->dd_R, c->dd_M, c->dd_D, c->dd_g, c->dd_ug,
+                  c->dd_sign, c->dd_shared,
                   c->lsq_ws, c->work, c->scratch, c->red};
   for (void* p : ptrs)
     if (p) cudaFree(p);

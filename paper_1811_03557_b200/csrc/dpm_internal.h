@@ -136,6 +136,10 @@ struct dpm_ctx {
   double* dd_g = nullptr;           // [2][n_rows] per-step BEP right-hand sides
   double* dd_ug = nullptr;          // [2][n_gamma] u_γ = A C
   int dd_blk[6] = {0};              // first column of each piece's block (dd_blk[npieces] = K)
+  double* dd_sign = nullptr;        // [K] (+ flag) column signs relative to octant dd_sign_ref (shared apply)
+  const dpm_ctx* dd_sign_ref = nullptr;
+  double* dd_shared = nullptr;      // workspace of dpm_dd_lsq_rhs_shared (on the first octant)
+  size_t dd_shared_bytes = 0;
   int dd_npieces = 0;
   // Case-1 two-subdomain DD (dd == 2, dpm_create_dd1, NEXT-3): Ω1 = ball r1 (sub 0) or Ω2 = shell (sub 1)
   int dd1_sub = 0, dd1_mz = 0, dd1_mg = 0;

@@ -77,6 +77,13 @@ class DDSolver:
                 and len({str(o.device) for o in self.octs}) == 1 and self.octs[0].device.type == "cuda"
                 and len({(o.n, o.info["h"]) for o in self.octs}) == 1)   # one AP operator for all fields
 
+    def _shared(self):
+        # octants of config 5 (not the Case-1 subdomains): one canonical geometry, extensions that differ
+        # by column signs only; DPM_DD_SHARED=0 applies every octant's own operator
+        import os
+        return (os.environ.get("DPM_DD_SHARED") != "0" and all(hasattr(o, "dd_lsq_rhs_shared") for o in self.octs)
+                and all(getattr(o, "octant", None) is not None and not hasattr(o, "sub") for o in self.octs))
+
     def _step_batched(self, main):
         o0 = self.octs[0]
         nf = 2 * len(self.octs)
@@ -90,13 +97,16 @@ class DDSolver:
         for st in self.streams:
             main.wait_stream(st)
         o0.aux_solve_batch(fq, wk, stream=main)                        # all particular solves at once
-        ys = []
-        for i, o in enumerate(self.octs):
-            self.streams[i].wait_stream(main)
-            ys.append(o.dd_lsq_rhs(wk[2 * i:2 * i + 2], stream=self.streams[i]))
-        for st in self.streams:
-            main.wait_stream(st)
-        Cg = self._sum(ys)                                            # C2: global coefficients
+        if self._shared():   # config 5: B_s = B_0 diag(S_s), one pass over octant 0's Q for all octants
+            Cg = _allreduce(o0.dd_lsq_rhs_shared(self.octs, wk, stream=main), dist.ReduceOp.SUM)
+        else:
+            ys = []
+            for i, o in enumerate(self.octs):
+                self.streams[i].wait_stream(main)
+                ys.append(o.dd_lsq_rhs(wk[2 * i:2 * i + 2], stream=self.streams[i]))
+            for st in self.streams:
+                main.wait_stream(st)
+            Cg = self._sum(ys)                                        # C2: global coefficients
         for i, o in enumerate(self.octs):
             self.streams[i].wait_stream(main)
             o.dd_green_rhs(Cg, self.clamp, fq[2 * i:2 * i + 2], wk[2 * i:2 * i + 2], stream=self.streams[i])

@@ -94,3 +94,19 @@ def test_dd_pks_parity_per_octant_abi_path(api):
     for lg, lo in zip(logs, ologs):
         assert abs(lg["dt"] - lo["dt"]) <= 1e-12 * lo["dt"]
         assert abs(lg["mass"] - lo["mass"]) <= 1e-9 * abs(lo["mass"])
+
+
+def test_dd_lsq_rhs_shared_equals_per_octant(api):
+    # dpm_dd_lsq_rhs_shared (one pass over octant 0's Q, B_s = B_0 diag(S_s)) against the sum of the
+    # per-octant operators M_s g_s on the same particular solutions
+    from paper_1811_03557_b200.dd import DDSolver
+    from dpm_inputs.rng import random_boxes
+    dt = 1e-3
+    octs = [api.Octant(N, *BOX, s, 1.0, LC, LI, dt) for s in range(8)]
+    sol = DDSolver(octs, dt)
+    sol.build(dt)
+    wk = torch.from_numpy(random_boxes(3, 16, N)).cuda()
+    y = octs[0].dd_lsq_rhs_shared(octs, wk)
+    ref = sum(o.dd_lsq_rhs(wk[2 * i:2 * i + 2]) for i, o in enumerate(octs))
+    torch.cuda.synchronize()
+    assert rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-11, rel(y.cpu().numpy(), ref.cpu().numpy())
