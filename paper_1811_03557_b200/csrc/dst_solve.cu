@@ -1086,6 +1086,15 @@ cudaError_t dst_solve_batch(const DstPlan& p, const double* q, double* u, int64_
     return (size_t)(v ? atoi(v) : 1024) << 20;
   }();
   int64_t chunk = std::max<int64_t>(1, (int64_t)(budget / field_bytes));
+  // equal chunks (no small tail launch): ceil(batch / ceil(batch / chunk)) fields each
+  static const bool balanced = [] {
+    const char* v = getenv("DPM_CHUNK_BALANCED");
+    return !(v && atoi(v) == 0);
+  }();
+  if (balanced && batch > chunk) {
+    const int64_t nch = (batch + chunk - 1) / chunk;
+    chunk = (batch + nch - 1) / nch;
+  }
   const double inv_dt = 1.0 / p.dt;
   const double sc = 2.0 / (n + 1);
   const double scale = sc * sc * sc;
