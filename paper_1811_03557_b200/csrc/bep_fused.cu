@@ -95,7 +95,9 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
     const char* v = getenv("DPM_BEP_ZBOX");
     return !(v && atoi(v) == 0);
   }();
-  if (zbox) {
+  // (small-K builds, e.g. the zonal Case-1 subdomains, keep the sparse-in pass: their few columns do not
+  // amortise the boxes' allocation and zeroing in a fresh context)
+  if (zbox && ctx->K >= 128) {
     // (1') q_c scattered into boxes that stay zero off the band: every chunk writes the same band
     // positions, so the boxes are zeroed once, when allocated; (2') dense forward x pass box -> work
     if (ctx->bepf_zcols < nc) {
