@@ -313,15 +313,18 @@ def test_bep_columns_fused_matches_dense_path_cfg4(tmp_path):
         PgE, B = c.bep_columns(0, c.K)
         np.save(sys.argv[1], PgE.cpu().numpy()); np.save(sys.argv[2], B.cpu().numpy())
     ''')
+    # "1": fused with the zero boxes (default), "s": fused with the sparse-in x pass (DPM_BEP_ZBOX=0),
+    # "0": the dense path
     outs = {}
-    for f in ("1", "0"):
+    for f, env in (("1", {}), ("s", {"DPM_BEP_ZBOX": "0"}), ("0", {"DPM_BEP_FUSED": "0"})):
         a, b = str(tmp_path / f"pg{f}.npy"), str(tmp_path / f"b{f}.npy")
-        r = subprocess.run([sys.executable, "-c", code, a, b], cwd=root, env=dict(os.environ, DPM_BEP_FUSED=f),
+        r = subprocess.run([sys.executable, "-c", code, a, b], cwd=root, env=dict(os.environ, **env),
                            capture_output=True, text=True, timeout=900)
         assert r.returncode == 0, r.stderr
         outs[f] = (np.load(a), np.load(b))
-    assert rel(outs["1"][0], outs["0"][0]) <= 1e-12
-    assert rel(outs["1"][1], outs["0"][1]) <= 1e-12
+    for f in ("1", "s"):
+        assert rel(outs[f][0], outs["0"][0]) <= 1e-12, f
+        assert rel(outs[f][1], outs["0"][1]) <= 1e-12, f
 
 
 def test_boundary_lsq_large_K_row_tail(api):
