@@ -110,3 +110,11 @@ def test_dd_lsq_rhs_shared_equals_per_octant(api):
     ref = sum(o.dd_lsq_rhs(wk[2 * i:2 * i + 2]) for i, o in enumerate(octs))
     torch.cuda.synchronize()
     assert rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-11, rel(y.cpu().numpy(), ref.cpu().numpy())
+    # a rank's shard at 4 GPUs / 2 GPUs: the reference octant is not octant 0
+    for sub in ([3, 5], [2, 4, 6, 7]):
+        so = [octs[s] for s in sub]
+        wks = torch.cat([wk[2 * s:2 * s + 2] for s in sub])
+        y = so[0].dd_lsq_rhs_shared(so, wks)
+        ref = sum(o.dd_lsq_rhs(wks[2 * i:2 * i + 2]) for i, o in enumerate(so))
+        torch.cuda.synchronize()
+        assert rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-11, (sub, rel(y.cpu().numpy(), ref.cpu().numpy()))
