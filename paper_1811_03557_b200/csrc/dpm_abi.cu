@@ -465,8 +465,19 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
     DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->ev_side[1], ctx->side_stream));
   }
   // Steps 6-7: Green's formula as one solve of the combined RHS (R20), restricted to N+
-  if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
-  if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+  // (default: the band values written in place into fq, which is zero there, and the solve reads fq;
+  // DPM_GREEN_INPLACE=0: a separate q box written by a streaming pass)
+  static const bool inplace = [] {
+    const char* v = getenv("DPM_GREEN_INPLACE");
+    return !(v && atoi(v) == 0);
+  }();
+  if (inplace) {
+    if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_band_inplace(ctx, fq, ug, 2, s));
+    if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+  } else {
+    if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
+    if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+  }
   if (!(skip & 16)) DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
   if (fork) DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
   return DPM_OK;

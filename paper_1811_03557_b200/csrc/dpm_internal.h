@@ -305,6 +305,7 @@ cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, do
                             double* backup = nullptr, double* zero6 = nullptr, double* cfl_out3 = nullptr,
                             double dt_prev = 0, double cap = 0, double* dt_out = nullptr);
 cudaError_t launch_fc_seq(dpm_ctx* ctx, const double* c, const double* rho_new, double dt, double* fq_c, cudaStream_t s);
+cudaError_t launch_green_band_inplace(dpm_ctx* ctx, double* fq, const double* u_gamma, int nrhs, cudaStream_t s);
 cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
                              cudaStream_t s);
 cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s);

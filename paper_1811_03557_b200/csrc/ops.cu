@@ -404,11 +404,11 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_kernel(const uint8
 __global__ void __launch_bounds__(TB, STENCIL_MINB) green_rhs_list_kernel(
     const uint8_t* __restrict__ flags, const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
     long nband, int n, const double* __restrict__ fq, const double* __restrict__ ug, int64_t ng, double* q, int nrhs,
-    double diag, double off) {
+    double diag, double off, int band_only) {
   pdl_prologue();
   const long nn = (long)n * n * n;
   const long tid = blockIdx.x * (long)blockDim.x + threadIdx.x, nth = (long)gridDim.x * blockDim.x;
-  for (long p = tid; p < nn; p += nth) {
+  for (long p = tid; p < (band_only ? 0 : nn); p += nth) {
     const uint8_t f = flags[p];
     if (f & F_BAND) continue;
     for (int r = 0; r < nrhs; ++r) {
@@ -721,12 +721,23 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
     return launch_pdl(green_rhs_list_kernel, grid_for(nn / 2), TB, 0, s, (const uint8_t*)ctx->flags,
                       (const int32_t*)ctx->gmap, (const int64_t*)ctx->lists[DPM_SET_BAND],
                       (long)ctx->counts[DPM_SET_BAND], ctx->n, fq, u_gamma, (int64_t)ctx->counts[DPM_SET_GAMMA], q,
-                      nrhs, diag, off);
+                      nrhs, diag, off, 0);
   return launch_pdl(green_rhs_kernel, grid_for(nn), TB, 0, s, (const uint8_t*)ctx->flags, (const int32_t*)ctx->gmap,
                     ctx->n, fq, u_gamma, (int64_t)ctx->counts[DPM_SET_GAMMA], q, nrhs, diag, off);
 }
 
 
+
+// The band part of the combined Green RHS written in place into fq (which the flux kernel leaves zero off
+// M+, and the band never meets M+): afterwards fq IS the combined right-hand side q of R20.
+cudaError_t launch_green_band_inplace(dpm_ctx* ctx, double* fq, const double* u_gamma, int nrhs, cudaStream_t s) {
+  const long nb = (long)ctx->counts[DPM_SET_BAND];
+  const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
+  DPM_COUNT_LAUNCH(1);
+  return launch_pdl(green_rhs_list_kernel, grid_for(nb), TB, 0, s, (const uint8_t*)ctx->flags,
+                    (const int32_t*)ctx->gmap, (const int64_t*)ctx->lists[DPM_SET_BAND], nb, ctx->n,
+                    (const double*)fq, u_gamma, (int64_t)ctx->counts[DPM_SET_GAMMA], fq, nrhs, diag, off, 1);
+}
 
 cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(out3, 0, 3 * sizeof(double), s);
