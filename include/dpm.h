@@ -339,6 +339,19 @@ dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const 
    rows) or their extensions are not sign reflections; DPM_ERR_STATE without a factorisation.
    Asynchronous on stream (the first call per octant pair synchronizes it once to check the signs). */
 dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* wk, double* y, void* stream);
+/* dpm_dd_green_rhs for `noct` (<= 8) config-5 octant contexts of ONE device at once: the extension
+   u_γ,s = A_s C (R17, clamped when clamp) of every octant from ONE evaluation of the basis per γ point,
+   then each octant's combined Green RHS (R20).  The octants share one canonical geometry and A_s evaluates
+   the basis at x = σ_s ⊙ p, where every cap SH and plane Legendre function is even or odd in each axis,
+   so A_s = A_0 diag(S_s) with S_s(ν) = (-1)^{popcount(s & π(ν))} (π(ν) the 3-bit parity class, s the
+   octant index): the basis terms are summed per parity class and an 8-point Walsh-Hadamard transform
+   gives every octant (same values as dpm_dd_green_rhs up to the summation order).  C: DEVICE [2][K]
+   (the global coefficients); fq, wk: DEVICE [noct][2][n^3] in the order of `octs`; wk == fq forms the
+   right-hand sides in place (fq is zero off M+ after dpm_dd_rhs and the band never meets M+, so only the
+   band values are written).  DPM_ERR_INVALID if
+   the contexts are not octants of one geometry on one device.  Asynchronous on stream. */
+dpm_status dpm_dd_green_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* C, int32_t clamp,
+                                   const double* fq, double* wk, void* stream);
 dpm_status dpm_dd_restrict(dpm_ctx* ctx, const double* wk, double* rho, double* c, void* stream);
 
 /* Cumulative number of CUDA kernels this library has launched in the process (all

@@ -101,6 +101,7 @@ _sig = {
     "dpm_dd_lsq_rhs": ([P, P, P, P], C.c_int),
     "dpm_dd_lsq_rhs_shared": ([C.POINTER(P), C.c_int32, P, P, P], C.c_int),
     "dpm_dd_green_rhs": ([P, P, C.c_int32, P, P, P], C.c_int),
+    "dpm_dd_green_rhs_shared": ([C.POINTER(P), C.c_int32, P, C.c_int32, P, P, P], C.c_int),
     "dpm_dd_restrict": ([P, P, P, P, P], C.c_int),
     "dpm_dd_pks_init": ([P, P, P, C.POINTER(PksIC), P], C.c_int),
     "dpm_dd_cfl": ([P, P, C.c_double, D, P], C.c_int),

@@ -278,6 +278,13 @@ class Octant(DPM):
         self._chk(L.lib.dpm_dd_lsq_rhs_shared(arr, len(octs), _ptr(_dev_f64(wk, "wk")), _ptr(y), _stream(stream)))
         return y
 
+    def dd_green_rhs_shared(self, octs, coef, clamp, fq, wk, stream=None):
+        """dd_green_rhs for octant contexts of one device sharing the canonical geometry: one basis
+        evaluation per γ point for all of them (dpm_dd_green_rhs_shared); fq, wk: [noct][2][n][n][n]."""
+        arr = (C.c_void_p * len(octs))(*[o._h.value for o in octs])
+        self._chk(L.lib.dpm_dd_green_rhs_shared(arr, len(octs), _ptr(_dev_f64(coef, "C")), clamp, _ptr(_dev_f64(fq, "fq")),
+                                                _ptr(_dev_f64(wk, "wk")), _stream(stream)))
+
     def dd_green_rhs(self, C, clamp, fq, wk, stream=None):
         self._chk(L.lib.dpm_dd_green_rhs(self._h, _ptr(_dev_f64(C, "C")), clamp, _ptr(_dev_f64(fq, "fq")),
                                          _ptr(_dev_f64(wk, "wk")), _stream(stream)))

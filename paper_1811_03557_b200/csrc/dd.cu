@@ -216,6 +216,200 @@ __global__ void __launch_bounds__(128) dd_extend_fly_kernel(const int64_t* __res
   }
 }
 
+// u_γ for several octants of one canonical geometry at once (dpm_dd_green_rhs_shared).  Octant s
+// evaluates the basis at X = σ_s ⊙ P, and every cap SH and plane Legendre function has a definite parity
+// under each axis reflection, so b_ν(σ_s ⊙ P) = (-1)^{popcount(s & π(ν))} b_ν(P) with the parity class
+// π(ν) = 4 p_x + 2 p_y + p_z (s = 4[σx<0] + 2[σy<0] + [σz<0]):
+//   cap  m = 0: (0, 0, l);  Re (x+iy)^m part: (m, 0, l-m);  Im part: (m+1, 1, l-m)   (mod 2)
+//   plane a, φ_jk = P_j(X_o0) P_k(X_o1): j on axis o0, k on axis o1; the d φ part adds axis a.
+// The basis is evaluated once per γ point in the canonical frame, its terms summed per parity class
+// (T_π, in the unrolled loop structure every class index is a compile-time constant), and
+// u_s = Σ_π (-1)^{popcount(s&π)} T_π is an 8-point Walsh-Hadamard transform per field.
+struct ExtOut {
+  double* ug[8];
+  int oct[8];
+  int n;
+};
+__global__ void __launch_bounds__(128) dd_extend_shared_kernel(const int64_t* __restrict__ gamma, int64_t ng, int n,
+                                                               double lo, double h, double radius, int Lc, int Li,
+                                                               int nphi, int K, const uint8_t* __restrict__ assign,
+                                                               const double* __restrict__ C, int clamp, ExtOut out) {
+  extern __shared__ double fly_sm[];
+  double2* cv = reinterpret_cast<double2*>(fly_sm);
+  const int L1 = Lc + 1;
+  double* ta = fly_sm + 2 * K;
+  double* tb = ta + L1 * L1;
+  double* tpm = tb + L1 * L1;
+  double* tz = tpm + L1;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) cv[i] = make_double2(C[i], C[K + i]);
+  for (int e = threadIdx.x; e < L1 * L1; e += blockDim.x) {
+    const int l = e / L1, m = e % L1;
+    ta[e] = (l >= m + 2) ? sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m)) : 0.0;
+    tb[e] = (l >= m + 2) ? sqrt(((l - 1.0) * (l - 1.0) - (double)m * m) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0)) : 0.0;
+  }
+  for (int m = threadIdx.x; m < L1; m += blockDim.x) {
+    tpm[m] = m > 0 ? sqrt((2.0 * m + 1.0) / (2.0 * m)) : 1.0;
+    tz[m] = sqrt(2.0 * m + 3.0);
+  }
+  __syncthreads();
+  const int nc = L1 * L1;
+  constexpr double SQ2 = 1.41421356237309504880;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ng; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pidx = gamma[g];
+    const unsigned up = (unsigned)pidx, un = (unsigned)n, q = up / un;
+    const int k = (int)(up - q * un), i = (int)(q / un), j = (int)(q - (unsigned)i * un);
+    const double X[3] = {lo + (i + 1) * h, lo + (j + 1) * h, lo + (k + 1) * h};
+    const double r = sqrt(X[0] * X[0] + X[1] * X[1] + X[2] * X[2]);
+    const int bits = assign[g];
+    const int cnt = __popc(bits);
+    const double inv = cnt ? 1.0 / cnt : 0.0;
+    double T[8][2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) T[c][0] = T[c][1] = 0.0;
+    if (bits & 1) {   // cap
+      const double x = X[0] / r, y = X[1] / r, z = X[2] / r;
+      const double dcap = r - radius, wc = 0.5 * dcap * dcap;
+      double pmm = 0.28209479177387814347, Cm = 1.0, Sm = 0.0;
+      for (int m = 0; m <= Lc; ++m) {
+        if (m > 0) {
+          pmm *= tpm[m];
+          const double Cn = x * Cm - y * Sm, Sn = x * Sm + y * Cm;
+          Cm = Cn;
+          Sm = Sn;
+        }
+        // (cos | sin part) x (l - m even | odd) x field
+        double cE[2] = {0.0, 0.0}, cO[2] = {0.0, 0.0}, sE[2] = {0.0, 0.0}, sO[2] = {0.0, 0.0};
+        auto term = [&](int l, double pl, double (&cs)[2], double (&sn)[2]) {
+          if (m == 0) {
+            const int nu = l * l + l;
+            const double2 a = cv[nu], d = cv[nc + nu];
+            cs[0] = fma(pl, fma(wc, d.x, a.x), cs[0]);
+            cs[1] = fma(pl, fma(wc, d.y, a.y), cs[1]);
+          } else {
+            const double vc = SQ2 * pl * Cm, vs = SQ2 * pl * Sm;
+            const int nup = l * l + l + m, nun = l * l + l - m;
+            const double2 ap = cv[nup], dp = cv[nc + nup], an = cv[nun], dn = cv[nc + nun];
+            cs[0] = fma(vc, fma(wc, dp.x, ap.x), cs[0]);
+            cs[1] = fma(vc, fma(wc, dp.y, ap.y), cs[1]);
+            sn[0] = fma(vs, fma(wc, dn.x, an.x), sn[0]);
+            sn[1] = fma(vs, fma(wc, dn.y, an.y), sn[1]);
+          }
+        };
+        term(m, pmm, cE, sE);
+        double p2 = pmm, p1 = 0.0;
+        if (m + 1 <= Lc) {
+          p1 = z * tz[m] * pmm;
+          term(m + 1, p1, cO, sO);
+        }
+        for (int l = m + 2; l <= Lc; l += 2) {
+          double pl = ta[l * L1 + m] * (z * p1 - tb[l * L1 + m] * p2);
+          p2 = p1;
+          p1 = pl;
+          term(l, pl, cE, sE);
+          if (l + 1 <= Lc) {
+            pl = ta[(l + 1) * L1 + m] * (z * p1 - tb[(l + 1) * L1 + m] * p2);
+            p2 = p1;
+            p1 = pl;
+            term(l + 1, pl, cO, sO);
+          }
+        }
+        // classes: cos (4(m&1), 0, even|odd) -> 4(m&1) + {0,1}; sin (4((m+1)&1) + 2 + {0,1})
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          if (m & 1) {
+            T[4][f] = fma(inv, cE[f], T[4][f]);
+            T[5][f] = fma(inv, cO[f], T[5][f]);
+            T[2][f] = fma(inv, sE[f], T[2][f]);
+            T[3][f] = fma(inv, sO[f], T[3][f]);
+          } else {
+            T[0][f] = fma(inv, cE[f], T[0][f]);
+            T[1][f] = fma(inv, cO[f], T[1][f]);
+            T[6][f] = fma(inv, sE[f], T[6][f]);
+            T[7][f] = fma(inv, sO[f], T[7][f]);
+          }
+        }
+      }
+    }
+    auto plane = [&](auto ac) {
+      constexpr int a = decltype(ac)::value;
+      constexpr int o0 = a == 0 ? 1 : 0, o1 = a == 2 ? 1 : 2;
+      constexpr int B0 = 4 >> o0, B1 = 4 >> o1, BA = 4 >> a;
+      if (!(bits & (2 << a))) return;
+      double Ps[32], Pt[32];
+      legendre_all(X[o0], Li, Ps);
+      legendre_all(X[o1], Li, Pt);
+      const double d = X[a];
+      const int cb = 2 * nc + 2 * nphi * a;
+      int mi = 0;
+      for (int gd = 0; gd <= Li; ++gd) {
+        // jj ≡ gd (mod 2): parities (gd&1 on o0, 0 on o1); jj ≢ gd: (~gd&1 on o0, 1 on o1)
+        double aS[2] = {0.0, 0.0}, eS[2] = {0.0, 0.0}, aD[2] = {0.0, 0.0}, eD[2] = {0.0, 0.0};
+        for (int jj = gd; jj >= 0; jj -= 2) {
+          {
+            const double phi = Ps[jj] * Pt[gd - jj];
+            const double2 av = cv[cb + mi], ev = cv[cb + nphi + mi];
+            aS[0] = fma(phi, av.x, aS[0]);
+            aS[1] = fma(phi, av.y, aS[1]);
+            eS[0] = fma(phi, ev.x, eS[0]);
+            eS[1] = fma(phi, ev.y, eS[1]);
+            ++mi;
+          }
+          if (jj >= 1) {
+            const double phi = Ps[jj - 1] * Pt[gd - jj + 1];
+            const double2 av = cv[cb + mi], ev = cv[cb + nphi + mi];
+            aD[0] = fma(phi, av.x, aD[0]);
+            aD[1] = fma(phi, av.y, aD[1]);
+            eD[0] = fma(phi, ev.x, eD[0]);
+            eD[1] = fma(phi, ev.y, eD[1]);
+            ++mi;
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          if (gd & 1) {
+            T[B0][f] = fma(inv, aS[f], T[B0][f]);
+            T[B0 + BA][f] = fma(inv * d, eS[f], T[B0 + BA][f]);
+            T[B1][f] = fma(inv, aD[f], T[B1][f]);
+            T[B1 + BA][f] = fma(inv * d, eD[f], T[B1 + BA][f]);
+          } else {
+            T[0][f] = fma(inv, aS[f], T[0][f]);
+            T[BA][f] = fma(inv * d, eS[f], T[BA][f]);
+            T[B0 + B1][f] = fma(inv, aD[f], T[B0 + B1][f]);
+            T[B0 + B1 + BA][f] = fma(inv * d, eD[f], T[B0 + B1 + BA][f]);
+          }
+        }
+      }
+    };
+    plane(std::integral_constant<int, 0>{});
+    plane(std::integral_constant<int, 1>{});
+    plane(std::integral_constant<int, 2>{});
+    // Walsh-Hadamard: T[s] <- Σ_π (-1)^{popcount(s & π)} T[π]
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (!(c & bit))
+#pragma unroll
+          for (int f = 0; f < 2; ++f) {
+            const double u = T[c][f], v = T[c | bit][f];
+            T[c][f] = u + v;
+            T[c | bit][f] = u - v;
+          }
+    for (int o = 0; o < out.n; ++o) {
+      const int so = out.oct[o];
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c == so) {
+          v0 = T[c][0];
+          v1 = T[c][1];
+        }
+      out.ug[o][g] = clamp ? fmax(v0, 0.0) : v0;
+      out.ug[o][ng + g] = clamp ? fmax(v1, 0.0) : v1;
+    }
+  }
+}
+
 // column block of each boundary piece: piece p owns columns [start[p], start[p+1])
 struct PieceBlocks {
   int start[6];
@@ -1045,6 +1239,47 @@ dpm_status dpm_dd_green_rhs(dpm_ctx* ctx, const double* C, int32_t clamp, const 
   if (!ctx->dd_ug) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->dd_ug, (size_t)2 * ng * sizeof(double) + 64));
   DPM_CUDA_TRY(ctx, dd_extend_fly(ctx, C, clamp, ctx->dd_ug, s));
   DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ctx->dd_ug, wk, 2, s));                        // R20
+  return DPM_OK;
+}
+
+dpm_status dpm_dd_green_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* C, int32_t clamp, const double* fq,
+                                   double* wk, void* stream) {
+  DPM_NVTX();
+  if (!octs || noct < 1 || noct > 8 || !C || !fq || !wk) return DPM_ERR_INVALID;
+  dpm_ctx* o0 = octs[0];
+  dpm_status st = dd_check(o0);
+  if (st != DPM_OK) return st;
+  ExtOut eo{};
+  eo.n = noct;
+  const int64_t ng = o0->counts[DPM_SET_GAMMA];
+  for (int q = 0; q < noct; ++q) {
+    dpm_ctx* o = octs[q];
+    if (!o || o->dd != 1 || o->device != o0->device || o->n != o0->n || o->lo != o0->lo || o->hi != o0->hi ||
+        o->K != o0->K || o->radius != o0->radius || o->Lc != o0->Lc || o->Li != o0->Li ||
+        o->counts[DPM_SET_GAMMA] != ng) {
+      o0->err = "dd_green_rhs_shared: the contexts are not octants of one canonical geometry on one device";
+      return DPM_ERR_INVALID;
+    }
+    if (!o->dd_ug) DPM_CUDA_TRY(o0, cudaMalloc(&o->dd_ug, (size_t)2 * ng * sizeof(double) + 64));
+    eo.ug[q] = o->dd_ug;
+    eo.oct[q] = 4 * (o->sigma[0] < 0) + 2 * (o->sigma[1] < 0) + (o->sigma[2] < 0);
+  }
+  cudaStream_t s = as_stream(stream);
+  const int L1 = o0->Lc + 1;
+  const size_t smem = (2 * (size_t)o0->K + 2 * L1 * L1 + 2 * L1) * sizeof(double);
+  DPM_CUDA_TRY(o0, cudaFuncSetAttribute(dd_extend_shared_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  DPM_COUNT_LAUNCH(1);
+  dd_extend_shared_kernel<<<(unsigned)std::min<int64_t>((ng + 127) / 128, 148 * 8), 128, smem, s>>>(
+      o0->lists[DPM_SET_GAMMA], ng, o0->n, o0->lo, o0->h, o0->radius, o0->Lc, o0->Li, o0->nphi, o0->K, o0->dd_assign,
+      C, clamp, eo);
+  DPM_CUDA_TRY(o0, cudaGetLastError());
+  const size_t field = (size_t)o0->n * o0->n * o0->n;
+  for (int q = 0; q < noct; ++q) {
+    if (wk == fq)   // in place: the band values scattered into fq (zero there, as dpm_dd_rhs leaves it)
+      DPM_CUDA_TRY(o0, launch_green_band_inplace(octs[q], wk + 2 * q * field, octs[q]->dd_ug, 2, s));
+    else
+      DPM_CUDA_TRY(o0, launch_green_rhs(octs[q], fq + 2 * q * field, octs[q]->dd_ug, wk + 2 * q * field, 2, s));   // R20
+  }
   return DPM_OK;
 }
 

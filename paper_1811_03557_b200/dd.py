@@ -107,12 +107,16 @@ class DDSolver:
             for st in self.streams:
                 main.wait_stream(st)
             Cg = self._sum(ys)                                        # C2: global coefficients
-        for i, o in enumerate(self.octs):
-            self.streams[i].wait_stream(main)
-            o.dd_green_rhs(Cg, self.clamp, fq[2 * i:2 * i + 2], wk[2 * i:2 * i + 2], stream=self.streams[i])
-        for st in self.streams:
-            main.wait_stream(st)
-        o0.aux_solve_batch(wk, wk, stream=main)                        # all Green solves at once
+        if self._shared():   # config 5: one basis evaluation per γ point for all octants (A_s = A_0 diag(S_s)),
+            o0.dd_green_rhs_shared(self.octs, Cg, self.clamp, fq, fq, stream=main)   # RHS formed in place in fq
+            o0.aux_solve_batch(fq, wk, stream=main)                    # all Green solves at once
+        else:
+            for i, o in enumerate(self.octs):
+                self.streams[i].wait_stream(main)
+                o.dd_green_rhs(Cg, self.clamp, fq[2 * i:2 * i + 2], wk[2 * i:2 * i + 2], stream=self.streams[i])
+            for st in self.streams:
+                main.wait_stream(st)
+            o0.aux_solve_batch(wk, wk, stream=main)                    # all Green solves at once
         for i, (o, (rho, c)) in enumerate(zip(self.octs, self.fields)):
             self.streams[i].wait_stream(main)
             o.dd_restrict(wk[2 * i:2 * i + 2], rho, c, stream=self.streams[i])

@@ -118,3 +118,38 @@ def test_dd_lsq_rhs_shared_equals_per_octant(api):
         ref = sum(o.dd_lsq_rhs(wks[2 * i:2 * i + 2]) for i, o in enumerate(so))
         torch.cuda.synchronize()
         assert rel(y.cpu().numpy(), ref.cpu().numpy()) <= 1e-11, (sub, rel(y.cpu().numpy(), ref.cpu().numpy()))
+
+
+def test_dd_green_rhs_shared_equals_per_octant(api):
+    # dpm_dd_green_rhs_shared (one basis evaluation per γ point, parity classes + Walsh-Hadamard) against
+    # every octant's own extension + Green RHS, on all 8 octants and on a rank-sized subset
+    from paper_1811_03557_b200.dd import DDSolver
+    from dpm_inputs.rng import random_boxes
+    dt = 1e-3
+    octs = [api.Octant(N, *BOX, s, 1.0, LC, LI, dt) for s in range(8)]
+    DDSolver(octs, dt).build(dt)
+    fq = torch.from_numpy(random_boxes(5, 16, N)).cuda()
+    Cg = torch.from_numpy(np.random.default_rng(6).uniform(-1, 1, size=(2, octs[0].K))).cuda()
+    for sub in (list(range(8)), [6, 1, 3]):
+        so = [octs[s] for s in sub]
+        fqs = torch.cat([fq[2 * s:2 * s + 2] for s in sub])
+        for clamp in (0, 1):
+            wk = torch.zeros_like(fqs)
+            so[0].dd_green_rhs_shared(so, Cg, clamp, fqs, wk)
+            ref = torch.zeros_like(fqs)
+            for i, o in enumerate(so):
+                o.dd_green_rhs(Cg, clamp, fqs[2 * i:2 * i + 2], ref[2 * i:2 * i + 2])
+            torch.cuda.synchronize()
+            assert rel(wk.cpu().numpy(), ref.cpu().numpy()) <= 1e-12, (sub, clamp, rel(wk.cpu().numpy(), ref.cpu().numpy()))
+    # in place (wk == fq) on flux-kernel output, which is zero off M+ (where the band lies)
+    rho = [torch.from_numpy(np.abs(random_boxes(7 + s, 1, N)[0])).cuda() for s in range(8)]
+    c = [torch.from_numpy(np.abs(random_boxes(17 + s, 1, N)[0])).cuda() for s in range(8)]
+    fq2 = torch.zeros((16, N, N, N), dtype=torch.float64, device="cuda")
+    for i, o in enumerate(octs):
+        o.dd_rhs(rho[i], c[i], 1.0, fq2[2 * i:2 * i + 2])
+    ref = torch.zeros_like(fq2)
+    for i, o in enumerate(octs):
+        o.dd_green_rhs(Cg, 1, fq2[2 * i:2 * i + 2], ref[2 * i:2 * i + 2])
+    octs[0].dd_green_rhs_shared(octs, Cg, 1, fq2, fq2)
+    torch.cuda.synchronize()
+    assert rel(fq2.cpu().numpy(), ref.cpu().numpy()) <= 1e-12
