@@ -627,7 +627,8 @@ __global__ void __launch_bounds__(256) dd_gemm_ts_kernel(const double* __restric
 
 // out[o][c] = Σ_{v ≡ o mod nout} w[v / nout][c] Σ_split part[split][v][c]   (w nullable: 1), fixed order
 __global__ void dd_reduce_kernel(const double* __restrict__ part, int nsplit, int NR, int M,
-                                 const double* __restrict__ w, int nout, double* __restrict__ out) {
+                                 const double* __restrict__ w, int nout, double* __restrict__ out,
+                                 const double* __restrict__ dscale = nullptr) {
   const long tot = (long)nout * M;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < tot; e += (long)gridDim.x * blockDim.x) {
     const int o = (int)(e / M), c = (int)(e - (long)o * M);
@@ -637,20 +638,24 @@ __global__ void dd_reduce_kernel(const double* __restrict__ part, int nsplit, in
       for (int sp = 0; sp < nsplit; ++sp) sv += part[((size_t)sp * NR + v) * M + c];
       acc = w ? fma(w[(size_t)(v / nout) * M + c], sv, acc) : acc + sv;
     }
-    out[e] = acc;
+    out[e] = dscale ? dscale[c] * acc : acc;
   }
 }
 
-// y[r][c] = D[c] Σ_{i >= c} W[i K + c] V[r][i]  (W upper col-major; nr <= 2): 32 outputs x 8 i-slices per
-// block (coalesced over c), slices summed in order
+// part[chunk][r][c] = Σ_{i >= c, i in chunk} W[i K + c] V[r][i]  (W upper col-major; nr <= 2): 32 outputs x
+// 8 i-slices per block (coalesced over c), blockIdx.y = i-chunk of UA_CH rows; slices summed in order,
+// chunks by dd_reduce_kernel (which applies D)
+constexpr int UA_CH = 64;
 __global__ void __launch_bounds__(256) dd_upper_apply_kernel(const double* __restrict__ W, int K,
                                                              const double* __restrict__ V, int nr,
-                                                             const double* __restrict__ D, double* __restrict__ y) {
+                                                             double* __restrict__ part) {
   __shared__ double red[8][2][32];
   const int cl = threadIdx.x & 31, sl = threadIdx.x >> 5, c = blockIdx.x * 32 + cl;
+  const int ib = blockIdx.y * UA_CH, ie = min(K, ib + UA_CH);
   double a0 = 0.0, a1 = 0.0;
   if (c < K)
-    for (int i = c + sl; i < K; i += 8) {
+#pragma unroll 4
+    for (int i = max(c, ib) + ((sl - max(c, ib) % 8 + 8) % 8); i < ie; i += 8) {
       const double wv = W[(size_t)i * K + c];
       a0 = fma(wv, V[i], a0);
       if (nr > 1) a1 = fma(wv, V[K + i], a1);
@@ -662,8 +667,17 @@ __global__ void __launch_bounds__(256) dd_upper_apply_kernel(const double* __res
     double v = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) v += red[q][sl][cl];
-    y[(size_t)sl * K + c] = D[c] * v;
+    part[((size_t)blockIdx.y * nr + sl) * K + c] = v;
   }
+}
+
+// the stacked column signs of the octants (one launch instead of a copy per octant)
+struct SignPtrs {
+  const double* p[8];
+};
+__global__ void dd_stack_signs_kernel(SignPtrs sp, int noct, int K, double* Sg) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < noct * K; e += gridDim.x * blockDim.x)
+    Sg[e] = sp.p[e / K][e % K];
 }
 
 // ---- NEXT-3: the paper's two-subdomain DD, Case 1 (concentric, Z ∩ Γ = ∅) ----
@@ -1192,7 +1206,8 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
     o->dd_sign_ref = o0;
   }
   const int nsplit = (int)((m + TS_ICH - 1) / TS_ICH), nsk = (K + TS_ICH - 1) / TS_ICH;
-  const int npart = std::max(1, std::max(nsplit, nsk));
+  const int nua = (K + UA_CH - 1) / UA_CH;   // i-chunks of the D R^{-1} apply (2 right-hand sides each)
+  const int npart = std::max(std::max(1, std::max(nsplit, nsk)), (2 * nua + nv - 1) / nv);
   const size_t need = ((size_t)nv * m + (size_t)npart * nv * K + (size_t)nv * K + 4 * (size_t)K +
                        (size_t)noct * K) * sizeof(double);
   if (o0->dd_shared_bytes < need) {
@@ -1208,8 +1223,11 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
   double* Tz = Z + (size_t)nv * K;        // [2][K]: Σ_s S_s R^T z_s
   double* Vz = Tz + 2 * (size_t)K;        // [2][K]: R^{-T} Tz
   double* Sg = Vz + 2 * (size_t)K;        // [noct][K]: the signs, stacked
-  for (int q = 0; q < noct; ++q)
-    DPM_CUDA_TRY(o0, cudaMemcpyAsync(Sg + (size_t)q * K, octs[q]->dd_sign, K * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  if (noct > 8) { o0->err = "dd_lsq_rhs_shared: at most 8 octants"; return DPM_ERR_INVALID; }
+  SignPtrs sp{};
+  for (int q = 0; q < noct; ++q) sp.p[q] = octs[q]->dd_sign;
+  DPM_COUNT_LAUNCH(1);
+  dd_stack_signs_kernel<<<(noct * K + TB - 1) / TB, TB, 0, s>>>(sp, noct, K, Sg);
   DPM_COUNT_LAUNCH(1);
   dd_rows_trace_kernel<<<grid_for(m * nv), TB, 0, s>>>(wk, field, o0->lists[DPM_SET_GAMMA], o0->dd_rows, m, nv, G);
   const size_t KK = (size_t)K * K;
@@ -1224,7 +1242,9 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
   dd_reduce_kernel<<<rb, TB, 0, s>>>(Pt, nsk, nv, K, Sg, 2, Tz);                              // Σ_s S_s (.)
   dd_gemm_ts_kernel<1><<<dim3(ct, nsk), 256, 0, s>>>(W2, K, K, Tz, K, 2, Pt);                 // R^{-T}
   dd_reduce_kernel<<<rb, TB, 0, s>>>(Pt, nsk, 2, K, nullptr, 2, Vz);
-  dd_upper_apply_kernel<<<ct, 256, 0, s>>>(W2, K, Vz, 2, o0->dd_D, y);                        // D R^{-1}
+  DPM_COUNT_LAUNCH(1);
+  dd_upper_apply_kernel<<<dim3(ct, (unsigned)nua), 256, 0, s>>>(W2, K, Vz, 2, Pt);                         // R^{-1} V
+  dd_reduce_kernel<<<rb, TB, 0, s>>>(Pt, nua, 2, K, nullptr, 2, y, o0->dd_D);              // D (.)
   DPM_CUDA_TRY(o0, cudaGetLastError());
   return DPM_OK;
 }
