@@ -69,6 +69,30 @@ cudaError_t bepf_prepare(dpm_ctx* ctx) {
 
 }  // namespace
 
+bool bep_zbox_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("DPM_BEP_ZBOX");
+    return !(v && atoi(v) == 0);
+  }();
+  return on;
+}
+
+// nc boxes that are zero off the band (allocated and zeroed once per context; grown when needed)
+cudaError_t bep_zbox(dpm_ctx* ctx, int nc, double** out, cudaStream_t s) {
+  if (ctx->bepf_zcols < nc) {
+    if (ctx->bepf_zbox) cudaFree(ctx->bepf_zbox);
+    ctx->bepf_zbox = nullptr;
+    ctx->bepf_zcols = 0;
+    const size_t bytes = (size_t)nc * ctx->n * ctx->n * ctx->n * sizeof(double);
+    cudaError_t e = cudaMalloc(&ctx->bepf_zbox, bytes);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ctx->bepf_zbox, 0, bytes, s)) != cudaSuccess) return e;
+    ctx->bepf_zcols = nc;
+  }
+  *out = ctx->bepf_zbox;
+  return cudaSuccess;
+}
+
 bool bep_fused_enabled(const dpm_ctx* ctx) {
   static const bool on = [] {
     const char* v = getenv("DPM_BEP_FUSED");
@@ -91,27 +115,16 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
     if ((e = cudaMalloc(&ctx->bepf_qb, std::max<int64_t>(1, nb) * nc * sizeof(double))) != cudaSuccess) return e;
     ctx->bepf_cols = nc;
   }
-  static const bool zbox = [] {
-    const char* v = getenv("DPM_BEP_ZBOX");
-    return !(v && atoi(v) == 0);
-  }();
   // (small-K builds, e.g. the zonal Case-1 subdomains, keep the sparse-in pass: their few columns do not
   // amortise the boxes' allocation and zeroing in a fresh context)
-  if (zbox && ctx->K >= 128) {
+  if (bep_zbox_enabled() && ctx->K >= 128) {
     // (1') q_c scattered into boxes that stay zero off the band: every chunk writes the same band
     // positions, so the boxes are zeroed once, when allocated; (2') dense forward x pass box -> work
-    if (ctx->bepf_zcols < nc) {
-      if (ctx->bepf_zbox) cudaFree(ctx->bepf_zbox);
-      ctx->bepf_zbox = nullptr;
-      ctx->bepf_zcols = 0;
-      const size_t bytes = (size_t)nc * ctx->n * ctx->n * ctx->n * sizeof(double);
-      if ((e = cudaMalloc(&ctx->bepf_zbox, bytes)) != cudaSuccess) return e;
-      if ((e = cudaMemsetAsync(ctx->bepf_zbox, 0, bytes, s)) != cudaSuccess) return e;
-      ctx->bepf_zcols = nc;
-    }
-    if ((e = launch_potential_scatter(ctx, ctx->E + (size_t)c0 * ng, ng, ctx->bepf_zbox, nc, s)) != cudaSuccess)
+    double* zb = nullptr;
+    if ((e = bep_zbox(ctx, nc, &zb, s)) != cudaSuccess) return e;
+    if ((e = launch_potential_scatter(ctx, ctx->E + (size_t)c0 * ng, ng, zb, nc, s)) != cudaSuccess)
       return e;
-    if ((e = dst128_pass(0, ctx->bepf_zbox, ctx->work, nc, ctx->plan.atab128, s)) != cudaSuccess) return e;
+    if ((e = dst128_pass(0, zb, ctx->work, nc, ctx->plan.atab128, s)) != cudaSuccess) return e;
   } else {
   // (1) band values of q_c = χ_{M-}(I/dt - Δ_h)[E_c], x-line-major
   if ((e = launch_potential_band(ctx, ctx->E + (size_t)c0 * ng, ng, ctx->bepf_qb, nc, ctx->bepf_bpos, s)) != cudaSuccess)

@@ -310,8 +310,18 @@ dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, do
                                           B ? B + (size_t)(a - c0) * ngin : nullptr, s));
       continue;
     }
-    DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, nc, s));
-    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, nc, nullptr, 0, s));
+    // zero boxes (as in the fused n = 128 path): every chunk writes the same band positions, so boxes
+    // zeroed once take the potential RHS by a band scatter and the solve reads them out of place
+    // (DPM_BEP_ZBOX=0: zero-fill + scatter into the work boxes, solved in place)
+    if (bep_zbox_enabled() && ctx->K >= 128 && ctx->plan.solver == DPM_SOLVER_DST2_TRIDIAG) {
+      double* zb = nullptr;
+      DPM_CUDA_TRY(ctx, bep_zbox(ctx, nc, &zb, s));
+      DPM_CUDA_TRY(ctx, launch_potential_scatter(ctx, ctx->E + (size_t)a * ng, ng, zb, nc, s));
+      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, zb, ctx->work, nc, nullptr, 0, s));
+    } else {
+      DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, nc, s));
+      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, nc, nullptr, 0, s));
+    }
     DPM_CUDA_TRY(ctx, launch_bep_gather(ctx, ctx->work, a, nc, PgE ? PgE + (size_t)(a - c0) * ng : nullptr,
                                         B ? B + (size_t)(a - c0) * ngin : nullptr, s));
   }

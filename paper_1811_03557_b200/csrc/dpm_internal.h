@@ -313,6 +313,8 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
                                   cudaStream_t s,
                                   bool zeroed = false);
 // bep_fused.cu (sparse-in / gamma-out BEP columns)
+bool bep_zbox_enabled();
+cudaError_t bep_zbox(dpm_ctx* ctx, int nc, double** out, cudaStream_t s);
 bool bep_fused_enabled(const dpm_ctx* ctx);
 cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double* B, cudaStream_t s);
 void bep_fused_free(dpm_ctx* c);
