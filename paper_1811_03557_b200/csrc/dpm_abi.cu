@@ -46,6 +46,8 @@ void free_ctx(dpm_ctx* c) {
   for (auto& g : c->pks_graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (c->graph_stream) cudaStreamDestroy(c->graph_stream);
+  if (c->fac_exec) cudaGraphExecDestroy(c->fac_exec);
+  if (c->fac_stream) cudaStreamDestroy(c->fac_stream);
   if (c->pks_log) cudaFree(c->pks_log);
   if (c->pks_log_host) cudaFreeHost(c->pks_log_host);
   if (c->pks_backup) cudaFree(c->pks_backup);

@@ -149,6 +149,12 @@ struct dpm_ctx {
   int32_t* bepf_bpos = nullptr;      // [n_band] line-major position of band point b
   double* bepf_qb = nullptr;         // [cols][n_band] band values of the potential RHS (line-major)
   int bepf_cols = 0;
+  cudaGraphExec_t fac_exec = nullptr; // the captured factorisation (lsq_factor) for (fac_B, fac_K, fac_m)
+  cudaStream_t fac_stream = nullptr;
+  const double* fac_B = nullptr;
+  int fac_K = 0;
+  int64_t fac_m = 0;
+  long long fac_launches = 0;
   double* bepf_zbox = nullptr;       // [zcols][n^3] boxes that are zero off the band (zero-box mode)
   int bepf_zcols = 0;
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)

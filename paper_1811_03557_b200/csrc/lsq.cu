@@ -402,28 +402,68 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   int* dfail = (int*)(Riw + (size_t)K * K);
   double* dcond = (double*)(dfail + 4);
   if (!ctx->Mlsq) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->Mlsq, (size_t)m * K * sizeof(double)));
-  DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), s));
-  DPM_COUNT_LAUNCH(1);
-  colnorm_kernel<<<K, TB, 0, s>>>(B, m, ctx->colscale);
-  DPM_COUNT_LAUNCH(1);
-  scale_cols_kernel<<<148 * 8, TB, 0, s>>>(B, m, K, ctx->colscale, ctx->Q);
-  dpm_status st;
-  // CholeskyQR2 ping-pong: Q -> Mlsq (scratch until the operator is formed) -> Q
-  if ((st = chol_qr_pass(ctx, ctx->Q, m, K, R1, Riw, ctx->Mlsq, dfail, s)) != DPM_OK) return st;
-  if ((st = chol_qr_pass(ctx, ctx->Mlsq, m, K, R2, Riw, ctx->Q, dfail, s)) != DPM_OK) return st;
-  DPM_COUNT_LAUNCH(1);
-  trmm_kernel<<<(K * K + 255) / 256, 256, 0, s>>>(R2, R1, ctx->R, K);
-  DPM_COUNT_LAUNCH(1);
-  diag_ratio_kernel<<<1, 1, 0, s>>>(ctx->R, K, dcond);
-  // apply operator M = D R^{-1} Q^T (K x |γ_in|): each LSQ solve is then one GEMV
-  double* Ri = R1;   // R1 is free after the trmm
-  DPM_CUDA_TRY(ctx, lsq_rinv(ctx->R, K, Ri, s));
-  DPM_CUDA_TRY(ctx, launch_gemm_tri<true>(ctx->Q, m, K, Ri, ctx->colscale, ctx->Mlsq, s));
-  // the residual operator R D^{-1} (row-major K x K) of the per-step LSQ residual (lsq_residual)
   if (!ctx->RDinv) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->RDinv, (size_t)K * K * sizeof(double)));
-  DPM_COUNT_LAUNCH(1);
-  rdinv_kernel<<<(unsigned)(((size_t)K * K + 255) / 256), 256, 0, s>>>(ctx->R, ctx->colscale, K, ctx->RDinv);
-  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  // The factorisation is ~80 small dependent kernels at K ~ 250 (blocked Cholesky, blocked R^{-1}): captured
+  // once per (context, B) into a CUDA graph and replayed (Step 4b rebuilds the BEP at every new dt).
+  // DPM_FACTOR_GRAPH=0 launches them directly.
+  static const bool use_graph = [] {
+    const char* v = getenv("DPM_FACTOR_GRAPH");
+    return !(v && atoi(v) == 0);
+  }();
+  auto enqueue = [&](cudaStream_t q) -> dpm_status {
+    DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), q));
+    DPM_COUNT_LAUNCH(1);
+    colnorm_kernel<<<K, TB, 0, q>>>(B, m, ctx->colscale);
+    DPM_COUNT_LAUNCH(1);
+    scale_cols_kernel<<<148 * 8, TB, 0, q>>>(B, m, K, ctx->colscale, ctx->Q);
+    dpm_status st;
+    // CholeskyQR2 ping-pong: Q -> Mlsq (scratch until the operator is formed) -> Q
+    if ((st = chol_qr_pass(ctx, ctx->Q, m, K, R1, Riw, ctx->Mlsq, dfail, q)) != DPM_OK) return st;
+    if ((st = chol_qr_pass(ctx, ctx->Mlsq, m, K, R2, Riw, ctx->Q, dfail, q)) != DPM_OK) return st;
+    DPM_COUNT_LAUNCH(1);
+    trmm_kernel<<<(K * K + 255) / 256, 256, 0, q>>>(R2, R1, ctx->R, K);
+    DPM_COUNT_LAUNCH(1);
+    diag_ratio_kernel<<<1, 1, 0, q>>>(ctx->R, K, dcond);
+    // apply operator M = D R^{-1} Q^T (K x |γ_in|): each LSQ solve is then one GEMV
+    double* Ri = R1;   // R1 is free after the trmm
+    DPM_CUDA_TRY(ctx, lsq_rinv(ctx->R, K, Ri, q));
+    DPM_CUDA_TRY(ctx, launch_gemm_tri<true>(ctx->Q, m, K, Ri, ctx->colscale, ctx->Mlsq, q));
+    // the residual operator R D^{-1} (row-major K x K) of the per-step LSQ residual (lsq_residual)
+    DPM_COUNT_LAUNCH(1);
+    rdinv_kernel<<<(unsigned)(((size_t)K * K + 255) / 256), 256, 0, q>>>(ctx->R, ctx->colscale, K, ctx->RDinv);
+    DPM_CUDA_TRY(ctx, cudaGetLastError());
+    return DPM_OK;
+  };
+  if (!use_graph) {
+    dpm_status st = enqueue(s);
+    if (st != DPM_OK) return st;
+  } else {
+    if (!ctx->fac_exec || ctx->fac_B != B || ctx->fac_K != K || ctx->fac_m != m) {
+      if (ctx->fac_exec) cudaGraphExecDestroy(ctx->fac_exec);
+      ctx->fac_exec = nullptr;
+      if (!ctx->fac_stream) DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->fac_stream, cudaStreamNonBlocking));
+      const long long l0 = (long long)g_dpm_launches.load();
+      DPM_CUDA_TRY(ctx, cudaStreamBeginCapture(ctx->fac_stream, cudaStreamCaptureModeThreadLocal));
+      dpm_status st = enqueue(ctx->fac_stream);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(ctx->fac_stream, &graph);
+      ctx->fac_launches = (long long)g_dpm_launches.load() - l0;
+      g_dpm_launches.fetch_sub(ctx->fac_launches);   // counted on every replay
+      if (st != DPM_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (ec != cudaSuccess) { ctx->err = std::string("factor graph capture: ") + cudaGetErrorString(ec); return DPM_ERR_CUDA; }
+      const cudaError_t ei = cudaGraphInstantiate(&ctx->fac_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) { ctx->err = std::string("factor graph instantiate: ") + cudaGetErrorString(ei); return DPM_ERR_CUDA; }
+      ctx->fac_B = B;
+      ctx->fac_K = K;
+      ctx->fac_m = m;
+    }
+    DPM_CUDA_TRY(ctx, cudaGraphLaunch(ctx->fac_exec, s));
+    g_dpm_launches.fetch_add(ctx->fac_launches);
+  }
   int hfail = 0;
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost, s));
   DPM_CUDA_TRY(ctx, cudaMemcpyAsync(&ctx->bep_cond, dcond, sizeof(double), cudaMemcpyDeviceToHost, s));
