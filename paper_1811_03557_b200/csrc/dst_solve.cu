@@ -861,31 +861,11 @@ __device__ __forceinline__ void ps_tri_rows(double* const (&row)[R], const bool 
 __device__ int g_ps_dmma = 1;   // DPM_PLANE_SMALL_DMMA=0 -> 0 (set by dst_plan_init)
 __device__ __forceinline__ bool ps_dmma() { return g_ps_dmma != 0; }
 
-__global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restrict__ u, int n, const double* __restrict__ S_g,
-                                                          const double* __restrict__ lam_g, double inv_dt, double h2,
-                                                          double rscale) {
-  pdl_prologue();
-  extern __shared__ double psm_small[];
-  double* S = psm_small;           // [64][PSP]
-  double* P = S + PSN * PSP;       // [64][PSP]
-  double* lam = P + PSN * PSP;     // [64]
-  const long plane = blockIdx.x;   // field * n + a
-  const int a = (int)(plane % n), t = threadIdx.x;
-  double* g = u + (size_t)plane * n * n;
-  {   // every load in flight at once (cp.async, zero-filled outside the n x n corner)
-    const unsigned sS = (unsigned)__cvta_generic_to_shared(S), sP = (unsigned)__cvta_generic_to_shared(P);
-#pragma unroll 4
-    for (int e = t; e < PSN * PSN; e += PS_THREADS) {
-      const int r = e / PSN, c = e % PSN;
-      const bool in = r < n && c < n;
-      cp_async8(sS + 8u * (unsigned)(r * PSP + c), in ? S_g + r * n + c : S_g, in);
-      cp_async8(sP + 8u * (unsigned)(r * PSP + c), in ? g + (size_t)r * n + c : g, in);
-    }
-    cp_async_commit();
-  }
-  for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
-  asm volatile("cp.async.wait_group 0;\n" ::);
-  __syncthreads();
+// y DST-I, z tridiagonal of every y-mode row, inverse y DST-I of one plane held in shared memory
+// (S: the sine matrix, P: the plane, both zero-padded to PSN x PSN at pitch PSP; a: the x mode)
+__device__ __forceinline__ void plane_small_body(const double* S, double* P, const double* lam, int n, int a,
+                                                 double inv_dt, double h2, double rscale) {
+  const int t = threadIdx.x;
   const bool tc = ps_dmma() && (n & 1) == 0;
   if (tc) ps_apply_dmma(S, P, n); else ps_apply(S, P, n);
   {
@@ -914,7 +894,86 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
   }
   __syncthreads();
   if (tc) ps_apply_dmma(S, P, n); else ps_apply(S, P, n);
+}
+
+__global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restrict__ u, int n, const double* __restrict__ S_g,
+                                                          const double* __restrict__ lam_g, double inv_dt, double h2,
+                                                          double rscale) {
+  pdl_prologue();
+  extern __shared__ double psm_small[];
+  double* S = psm_small;           // [64][PSP]
+  double* P = S + PSN * PSP;       // [64][PSP]
+  double* lam = P + PSN * PSP;     // [64]
+  const long plane = blockIdx.x;   // field * n + a
+  const int a = (int)(plane % n), t = threadIdx.x;
+  double* g = u + (size_t)plane * n * n;
+  {   // every load in flight at once (cp.async, zero-filled outside the n x n corner)
+    const unsigned sS = (unsigned)__cvta_generic_to_shared(S), sP = (unsigned)__cvta_generic_to_shared(P);
+#pragma unroll 4
+    for (int e = t; e < PSN * PSN; e += PS_THREADS) {
+      const int r = e / PSN, c = e % PSN;
+      const bool in = r < n && c < n;
+      cp_async8(sS + 8u * (unsigned)(r * PSP + c), in ? S_g + r * n + c : S_g, in);
+      cp_async8(sP + 8u * (unsigned)(r * PSP + c), in ? g + (size_t)r * n + c : g, in);
+    }
+    cp_async_commit();
+  }
+  for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  plane_small_body(S, P, lam, n, a, inv_dt, h2, rscale);
   for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
+}
+
+// Batched small-n plane pass (Step-4b rebuilds: K fields at once): persistent CTAs that load the sine
+// matrix once and stream planes through two buffers (the next plane's cp.async in flight under the
+// current plane's transforms); the same per-plane arithmetic as plane_small_kernel.
+__global__ void __launch_bounds__(PS_THREADS) plane_small_batch_kernel(double* __restrict__ u, int n,
+                                                                       const double* __restrict__ S_g,
+                                                                       const double* __restrict__ lam_g, double inv_dt,
+                                                                       double h2, double rscale, long nplanes) {
+  pdl_prologue();
+  extern __shared__ double psm_small[];
+  double* S = psm_small;              // [64][PSP]
+  double* PB = S + PSN * PSP;         // 2 x [64][PSP]
+  double* lam = PB + 2 * PSN * PSP;   // [64]
+  const int t = threadIdx.x;
+  auto load_plane = [&](double* P, long plane) {
+    const double* g = u + (size_t)plane * n * n;
+    const unsigned sP = (unsigned)__cvta_generic_to_shared(P);
+#pragma unroll 4
+    for (int e = t; e < PSN * PSN; e += PS_THREADS) {
+      const int r = e / PSN, c = e % PSN;
+      const bool in = r < n && c < n;
+      cp_async8(sP + 8u * (unsigned)(r * PSP + c), in ? g + (size_t)r * n + c : g, in);
+    }
+  };
+  {
+    const unsigned sS = (unsigned)__cvta_generic_to_shared(S);
+#pragma unroll 4
+    for (int e = t; e < PSN * PSN; e += PS_THREADS) {
+      const int r = e / PSN, c = e % PSN;
+      const bool in = r < n && c < n;
+      cp_async8(sS + 8u * (unsigned)(r * PSP + c), in ? S_g + r * n + c : S_g, in);
+    }
+  }
+  for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
+  if ((long)blockIdx.x < nplanes) load_plane(PB, blockIdx.x);
+  cp_async_commit();
+  int b = 0;
+  for (long plane = blockIdx.x; plane < nplanes; plane += gridDim.x, b ^= 1) {
+    const long nxt = plane + gridDim.x;
+    if (nxt < nplanes) load_plane(PB + (b ^ 1) * PSN * PSP, nxt);
+    cp_async_commit();
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();
+    double* P = PB + b * PSN * PSP;
+    plane_small_body(S, P, lam, n, (int)(plane % n), inv_dt, h2, rscale);
+    double* g = u + (size_t)plane * n * n;
+    for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
+    __syncthreads();   // the buffer is refilled by the prefetch of the next iteration but one
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
 cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
@@ -923,6 +982,22 @@ cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream
   cudaError_t e = cudaFuncSetAttribute(plane_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const double sc = 2.0 / (n + 1);
+  const long planes = (long)nfields * n;
+  static const bool batch_on = [] {   // DPM_PLANE_SMALL_BATCH=0: one CTA per plane at every batch size
+    const char* v = getenv("DPM_PLANE_SMALL_BATCH");
+    return !(v && atoi(v) == 0);
+  }();
+  if (batch_on && planes > 4L * 148) {
+    const size_t bsmem = (3 * (size_t)PSN * PSP + PSN) * sizeof(double);
+    e = cudaFuncSetAttribute(plane_small_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
+    if (e != cudaSuccess) return e;
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, plane_small_batch_kernel, PS_THREADS, bsmem);
+    DPM_COUNT_LAUNCH(1);
+    return launch_pdl(plane_small_batch_kernel, (unsigned)std::min<long>(planes, 148L * std::max(1, occ)), PS_THREADS,
+                      bsmem, s, u, n, (const double*)p.sinmat, (const double*)p.lam, 1.0 / p.dt, p.h * p.h,
+                      sc * sc * p.h * p.h, planes);
+  }
   DPM_COUNT_LAUNCH(1);
   return launch_pdl(plane_small_kernel, (unsigned)((long)nfields * n), PS_THREADS, smem, s, u, n,
                     (const double*)p.sinmat, (const double*)p.lam, 1.0 / p.dt, p.h * p.h, sc * sc * p.h * p.h);
