@@ -590,6 +590,64 @@ __global__ void __launch_bounds__(256) gram64_kernel(const double* __restrict__ 
     }
 }
 
+// R^{-1} by recursive doubling (DPM_RINV_DOUBLING, default): with the diagonal 32 x 32 tiles inverted,
+// level s (= 32, 64, 128, ...) joins each pair of inverted diagonal blocks [P_1 B; 0 P_2] of size s:
+//   inv = [P_1^{-1}, -P_1^{-1} B P_2^{-1}; 0, P_2^{-1}],
+// as two launches of 32 x 32-tile products over all pairs at once (T = B X_22, then X_12 = -X_11 T; the
+// triangular factors' zero tiles skipped).  log2(K/32) levels instead of K/32 dependent block diagonals.
+// mode 0: T[i][j] = Σ_{k in blk2, k <= j} R[i][k] Ri[k][j]      (i in blk1, j in blk2)
+// mode 1: Ri[i][j] = -Σ_{k in blk1, k >= i} Ri[i][k] T[k][j]
+__global__ void __launch_bounds__(256) rinv_pair_kernel(const double* __restrict__ R, int K, int s, int mode,
+                                                        double* __restrict__ Ri, double* __restrict__ T) {
+  __shared__ double sa[RT][RT + 1], sb[RT][RT + 1];
+  const int nt = s / RT;                       // tiles per block side
+  const int pair = blockIdx.x / (nt * nt), tt = blockIdx.x % (nt * nt);
+  const int ti = tt / nt, tj = tt % nt;
+  const int r1 = 2 * pair * s, r2 = r1 + s;    // block 1 rows/cols [r1, r2), block 2 [r2, min(r2 + s, K))
+  if (r2 >= K) return;
+  const int e2 = min(r2 + s, K);
+  const int i0 = r1 + ti * RT, j0 = r2 + tj * RT;
+  if (j0 >= e2) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double acc[4] = {0, 0, 0, 0};
+  const int kb = mode == 0 ? r2 : i0, ke = mode == 0 ? min(j0 + RT, e2) : r2;
+  for (int k0 = kb; k0 < ke; k0 += RT) {
+    for (int q = ty; q < RT; q += 8) {
+      const int ra = i0 + tx, ca = k0 + q;     // left factor (row ra, col ca)
+      const int rb = k0 + tx, cb = j0 + q;     // right factor (row rb, col cb)
+      double av, bv;
+      if (mode == 0) {
+        av = (ra < K && ca < K) ? R[(size_t)ca * K + ra] : 0.0;
+        bv = (rb < e2 && cb < e2 && rb <= cb) ? Ri[(size_t)cb * K + rb] : 0.0;
+      } else {
+        av = (ca < r2 && ra <= ca) ? Ri[(size_t)ca * K + ra] : 0.0;
+        bv = (rb < r2 && cb < e2) ? T[(size_t)cb * K + rb] : 0.0;
+      }
+      sa[tx][q] = av;
+      sb[tx][q] = bv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int l = 0; l < RT; ++l) {
+      const double bv = sb[l][tx];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[u] = fma(sa[ty + 8 * u][l], bv, acc[u]);
+    }
+    __syncthreads();
+  }
+  // stage the tile (row ty + 8u, col tx) and store with lanes over consecutive rows
+#pragma unroll
+  for (int u = 0; u < 4; ++u) sb[ty + 8 * u][tx] = acc[u];
+  __syncthreads();
+  for (int q = ty; q < RT; q += 8) {
+    const int r = i0 + tx, c = j0 + q;
+    if (r < r2 && c < e2) {
+      if (mode == 0) T[(size_t)c * K + r] = sb[tx][q];
+      else Ri[(size_t)c * K + r] = -sb[tx][q];
+    }
+  }
+}
+
 // R^{-1} (upper triangular, col-major; lower triangle of Ri zeroed) by the blocked kernels above
 cudaError_t lsq_rinv(const double* R, int K, double* Ri, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(Ri, 0, (size_t)K * K * sizeof(double), s);
@@ -597,6 +655,24 @@ cudaError_t lsq_rinv(const double* R, int K, double* Ri, cudaStream_t s) {
   const int nb = (K + RT - 1) / RT;
   DPM_COUNT_LAUNCH(1);
   rinv_diag_kernel<<<nb, RT, 0, s>>>(R, K, Ri);
+  static const bool doubling = [] {
+    const char* v = getenv("DPM_RINV_DOUBLING");
+    return !(v && atoi(v) == 0);
+  }();
+  if (doubling) {
+    if (nb == 1) return cudaGetLastError();
+    double* T = nullptr;
+    if ((e = cudaMallocAsync(&T, (size_t)K * K * sizeof(double), s)) != cudaSuccess) return e;
+    for (int sz = RT; sz < K; sz *= 2) {
+      const int pairs = (K + 2 * sz - 1) / (2 * sz), nt = sz / RT;
+      const unsigned grid = (unsigned)(pairs * nt * nt);
+      DPM_COUNT_LAUNCH(2);
+      rinv_pair_kernel<<<grid, 256, 0, s>>>(R, K, sz, 0, Ri, T);
+      rinv_pair_kernel<<<grid, 256, 0, s>>>(R, K, sz, 1, Ri, T);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaFreeAsync(T, s);
+  }
   for (int d = 1; d < nb; ++d) {
     DPM_COUNT_LAUNCH(1);
     rinv_offdiag_kernel<<<nb - d, 256, 0, s>>>(R, K, d, Ri);
