@@ -869,6 +869,84 @@ __global__ void __launch_bounds__(256) gemm_tri_dmma_kernel(const double* __rest
       }
 }
 
+// The same product with 128 x 64 output tiles (DPM_TRI_BM = 128, default): 8 warps of 32 x 32 (4 x 4
+// fragment tiles), so every fragment load feeds 4 DMMAs instead of 2-4 and the T tile is re-read for half
+// as many row tiles.  Stage pitches 132 / 68 (≡ 4 mod 16: each 8-byte bank pair hit twice per load).
+constexpr int DT2_PA = 132, DT2_PT = 68;
+template <bool TRANS>
+__global__ void __launch_bounds__(256) gemm_tri_dmma2_kernel(const double* __restrict__ A, int64_t m, int K,
+                                                             const double* __restrict__ T,
+                                                             const double* __restrict__ scale, double* __restrict__ Cm) {
+  extern __shared__ __align__(16) double tsm[];   // sA[2][DT_RK][DT2_PA] | sT[2][DT_RK][DT2_PT]
+  double* sA = tsm;
+  double* sT = tsm + 2 * DT_RK * DT2_PA;
+  const int64_t r0 = (int64_t)blockIdx.x * 128;
+  const int j0 = blockIdx.y * 64;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wr = 32 * (w >> 1), wj = 32 * (w & 1);
+  const int kbeg = TRANS ? j0 : 0, kend = TRANS ? K : min(K, j0 + 64);
+  auto stage = [&](int buf, int k0) {
+    double* a = sA + buf * DT_RK * DT2_PA;
+    double* tt = sT + buf * DT_RK * DT2_PT;
+    for (int e = t; e < DT_RK * 128; e += 256) {
+      const int kk = e >> 7, c = e & 127;
+      const int k = k0 + kk;
+      const int64_t r = r0 + c;
+      if (r < m && k < K) cpasync8(a + kk * DT2_PA + c, A + (size_t)k * m + r); else a[kk * DT2_PA + c] = 0.0;
+    }
+    for (int e = t; e < DT_RK * 64; e += 256) {
+      const int kk = e >> 6, c = e & 63;
+      const int k = k0 + kk, j = j0 + c;
+      const bool nz = k < K && j < K && (TRANS ? k >= j : k <= j);
+      if (nz) cpasync8(tt + kk * DT2_PT + c, TRANS ? T + (size_t)k * K + j : T + (size_t)j * K + k);
+      else tt[kk * DT2_PT + c] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  int buf = 0;
+  if (kbeg < kend) stage(0, kbeg);
+  for (int k0 = kbeg; k0 < kend; k0 += DT_RK, buf ^= 1) {
+    if (k0 + DT_RK < kend) {
+      stage(buf ^ 1, k0 + DT_RK);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* a = sA + buf * DT_RK * DT2_PA;
+    const double* tt = sT + buf * DT_RK * DT2_PT;
+#pragma unroll
+    for (int ks = 0; ks < DT_RK / 4; ++ks) {
+      const int kk = 4 * ks + (lane & 3);
+      double af[4], bf[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) af[x] = a[kk * DT2_PA + wr + 8 * x + (lane >> 2)];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bf[y] = tt[kk * DT2_PT + wj + 8 * y + (lane >> 2)];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_884(acc[x][y], af[x], bf[y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = r0 + wr + 8 * x + (lane >> 2);
+        const int j = j0 + wj + 8 * y + 2 * (lane & 3) + h;
+        if (r < m && j < K) Cm[(size_t)j * m + r] = scale ? scale[j] * acc[x][y][h] : acc[x][y][h];
+      }
+}
+
 static bool lsq_dmma() {
   static const bool on = [] {
     const char* v = getenv("DPM_LSQ_DMMA");
@@ -882,6 +960,18 @@ cudaError_t launch_gemm_tri(const double* A, int64_t m, int K, const double* T, 
                             cudaStream_t s) {
   const dim3 grid((unsigned)((m + 63) / 64), (K + 63) / 64);
   DPM_COUNT_LAUNCH(1);
+  static const int bm = [] {
+    const char* v = getenv("DPM_TRI_BM");
+    return v && atoi(v) == 64 ? 64 : 128;
+  }();
+  if (lsq_dmma() && bm == 128 && K >= 384) {   // (small K: the 64-row tiles give more CTAs)
+    const size_t smem = 2 * DT_RK * (DT2_PA + DT2_PT) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tri_dmma2_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    gemm_tri_dmma2_kernel<TRANS><<<dim3((unsigned)((m + 127) / 128), (K + 63) / 64), 256, smem, s>>>(A, m, K, T, scale, C);
+    return cudaGetLastError();
+  }
   if (lsq_dmma()) {
     const size_t smem = 4 * DT_RK * DT_P * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(gemm_tri_dmma_kernel<TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
