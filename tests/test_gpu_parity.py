@@ -68,6 +68,19 @@ def test_aux_solve_parity_large_dt(api, n, dt, solver):
     assert rel(u, ap.solve(q, c.info["h"], dt)) <= 1e-11
 
 
+@pytest.mark.parametrize("n,batch", [(33, 20), (48, 14), (64, 10), (17, 40)])
+def test_aux_solve_small_n_large_batch(api, n, batch):
+    # more than 4 x 148 x-mode planes: the persistent batched small-n plane pass (sine matrix loaded once per
+    # CTA, the next plane prefetched) — odd n on the DFMA transform, even n on DMMA; in place
+    dt = 1e-3 if n % 2 else 2e-5
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    assert batch * n > 4 * 148
+    q = random_boxes(300 + n, batch, n)
+    t = torch.from_numpy(q).cuda()
+    c.aux_solve_batch(t, t)
+    assert rel(t.cpu().numpy(), ap.solve(q, c.info["h"], dt)) <= 1e-11
+
+
 def test_aux_solve_128_batch_chunked_inplace(api):
     # n = 128: x pass -> fused plane pass (2-CTA clusters, split z solve) -> x pass, in place,
     # over more than one 1 GiB chunk is too large for the oracle; 3 fields, u aliasing q
