@@ -411,10 +411,24 @@ double decode_key(double slot) {
 extern "C" {
 
 
+// Speculative step graphs without rollback copies (DPM_PKS_ABORT, default): the flux kernel's dt rule sets a
+// device flag when a step asks for a smaller dt, a restriction that sees a non-finite value sets it too,
+// and every later restriction of the graph then leaves (rho, c) alone — so the state after the graph is
+// already the state at the start of the first rejected step (or right after the failing one), and no
+// per-step copy of the state is written.  DPM_PKS_ABORT=0: the per-step rollback copies.
+static bool pks_abort_on() {
+  static const bool on = [] {
+    const char* v = getenv("DPM_PKS_ABORT");
+    return !(v && atoi(v) == 0);
+  }();
+  return on;
+}
+static int* pks_abort_flag(dpm_ctx* ctx) { return reinterpret_cast<int*>(ctx->red + 61); }
+
 // Enqueue one PKS step (Steps 4a-7) at a fixed dt on stream s; `slot` receives red(3), dt_true
 // (device dt rule from the state at the start of the step) and the step statistics.
 static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_params* prm, double dt,
-                                   double* slot, double* backup, cudaStream_t s) {
+                                   double* slot, double* backup, cudaStream_t s, int* abort) {
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
   double* fq = ctx->scratch;              // 2 boxes: f/dt on M+
@@ -426,7 +440,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   // maxima accumulated in slot[0..2]) and Step 4a (flux + IMEX right-hand sides) in one kernel; it also
   // writes the step's rollback copy of rho, c into `backup` when non-null and zeroes the statistics slot
   DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, dt, prm->chi, fq, fq + field, s, backup, slot + 4,
-                                    prm->dt_rule == 0 ? slot : nullptr, dt, prm->dt_cap, slot + 3));
+                                    prm->dt_rule == 0 ? slot : nullptr, dt, prm->dt_cap, slot + 3, abort));
   if (prm->coupling == 1) {   // sequential: the whole ρ step, then the c step from ρ̄^{i+1}
     const int K = ctx->K;
     for (int r = 0; r < 2; ++r) {
@@ -439,7 +453,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
       DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fr, ug + r * ng, wr, 1, s));
       DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wr, wr, 1, nullptr, 0, s));
     }
-    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
+    DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true, abort));
     return DPM_OK;
   }
   // DPM_STEP_SKIP (timing experiments only, tools/pks_skip.py, results wrong; compiled in only with
@@ -490,7 +504,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
     if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
     if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
   }
-  if (!(skip & 16)) DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true));
+  if (!(skip & 16)) DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true, abort));
   if (fork) DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
   return DPM_OK;
 }
@@ -518,8 +532,14 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   }();
   const int pdl = ctx->n <= pdl_nmax;
   g_pdl_scope += pdl;
+  int* abort = pks_abort_on() ? pks_abort_flag(ctx) : nullptr;
+  if (abort) {
+    const cudaError_t em = cudaMemsetAsync(abort, 0, sizeof(int), cs);
+    if (em != cudaSuccess) { ctx->err = "capture memset"; st = DPM_ERR_CUDA; }
+  }
   for (int i = 0; i < K && st == DPM_OK; ++i)
-    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i, ctx->pks_backup + (size_t)i * 2 * field, cs);
+    st = enqueue_pks_step(ctx, rho, c, prm, dt, ctx->pks_log + 16 * i,
+                          abort ? nullptr : ctx->pks_backup + (size_t)i * 2 * field, cs, abort);
   g_pdl_scope -= pdl;
   if (st == DPM_OK) {
     cudaError_t e = cudaMemcpyAsync(ctx->pks_log_host, ctx->pks_log, (size_t)K * 16 * 8, cudaMemcpyDeviceToHost, cs);
@@ -599,7 +619,7 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
     DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_log, KMAX * 16 * sizeof(double)));
     DPM_CUDA_TRY(ctx, cudaMemset(ctx->pks_log, 0, KMAX * 16 * sizeof(double)));   // CFL maxima start at 0
     DPM_CUDA_TRY(ctx, cudaMallocHost(&ctx->pks_log_host, KMAX * 16 * sizeof(double)));
-    DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
+    if (!pks_abort_on()) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->pks_backup, (size_t)KMAX * 2 * field * sizeof(double)));
     DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_side) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -652,11 +672,13 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
     for (int i = 0; i < K; ++i) {
       const double* L = ctx->pks_log_host + 16 * i;
       if (prm->dt_rule == 0 && L[3] < dt) {   // this step needs a smaller dt: roll back to its start
-        DPM_CUDA_TRY(ctx, cudaMemcpyAsync(rho, ctx->pks_backup + (size_t)i * 2 * field, field * 8,
-                                          cudaMemcpyDeviceToDevice, gs));
-        DPM_CUDA_TRY(ctx, cudaMemcpyAsync(c, ctx->pks_backup + (size_t)i * 2 * field + field, field * 8,
-                                          cudaMemcpyDeviceToDevice, gs));
-        DPM_CUDA_TRY(ctx, cudaStreamSynchronize(gs));
+        if (ctx->pks_backup) {   // (abort mode: the graph already left the state at the step's start)
+          DPM_CUDA_TRY(ctx, cudaMemcpyAsync(rho, ctx->pks_backup + (size_t)i * 2 * field, field * 8,
+                                            cudaMemcpyDeviceToDevice, gs));
+          DPM_CUDA_TRY(ctx, cudaMemcpyAsync(c, ctx->pks_backup + (size_t)i * 2 * field + field, field * 8,
+                                            cudaMemcpyDeviceToDevice, gs));
+          DPM_CUDA_TRY(ctx, cudaStreamSynchronize(gs));
+        }
         dt_next = L[3];
         accepted = i;
         break;
@@ -664,7 +686,7 @@ dpm_status dpm_pks_step(dpm_ctx* ctx, double* rho, double* c, int32_t nsteps, co
       ctx->dt_prev = dt;
       ctx->t += dt;
       if (L[8] != 0.0) {
-        if (i + 1 < K) {   // leave the state right after the failing step
+        if (i + 1 < K && ctx->pks_backup) {   // leave the state right after the failing step
           DPM_CUDA_TRY(ctx, cudaMemcpyAsync(rho, ctx->pks_backup + (size_t)(i + 1) * 2 * field, field * 8,
                                             cudaMemcpyDeviceToDevice, gs));
           DPM_CUDA_TRY(ctx, cudaMemcpyAsync(c, ctx->pks_backup + (size_t)(i + 1) * 2 * field + field, field * 8,

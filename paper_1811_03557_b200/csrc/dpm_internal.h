@@ -309,7 +309,7 @@ cudaError_t launch_slope_mask(dpm_ctx* ctx, cudaStream_t s);   // ctx->mplus_slo
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi,
                             double* fq_rho, double* fq_c, cudaStream_t s,
                             double* backup = nullptr, double* zero6 = nullptr, double* cfl_out3 = nullptr,
-                            double dt_prev = 0, double cap = 0, double* dt_out = nullptr);
+                            double dt_prev = 0, double cap = 0, double* dt_out = nullptr, int* abort = nullptr);
 cudaError_t launch_fc_seq(dpm_ctx* ctx, const double* c, const double* rho_new, double dt, double* fq_c, cudaStream_t s);
 cudaError_t launch_green_band_inplace(dpm_ctx* ctx, double* fq, const double* u_gamma, int nrhs, cudaStream_t s);
 cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gamma, double* q, int nrhs,
@@ -317,7 +317,7 @@ cudaError_t launch_green_rhs(dpm_ctx* ctx, const double* fq, const double* u_gam
 cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c, double* out3, cudaStream_t s);
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
                                   cudaStream_t s,
-                                  bool zeroed = false);
+                                  bool zeroed = false, int* abort = nullptr);
 // bep_fused.cu (sparse-in / gamma-out BEP columns)
 bool bep_zbox_enabled();
 cudaError_t bep_zbox(dpm_ctx* ctx, int nc, double** out, cudaStream_t s);

@@ -164,6 +164,7 @@ struct CflFuse {
   unsigned* ticket = nullptr;
   double chi = 0, dt_prev = 0, cap = 0;
   double* dt_out = nullptr;
+  int* abort = nullptr;     // speculative step graphs: set when the rule asks for a dt below dt_prev
 };
 
 // Step 3 on the device, the tail of both flux kernels: block maxima of the face differences -> atomics,
@@ -196,7 +197,9 @@ __device__ __forceinline__ void cfl_finish(const double (&cmx)[3], double h, con
       if (m > 0) cfl = fmin(cfl, h / (6.0 * cf.chi * m));
       r3[a] = 0.0;   // ready for the slot's next use
     }
-    *cf.dt_out = fmin(fmin(cf.dt_prev, cf.cap), fmin(cfl, 0.5 * h * h));
+    const double dtr = fmin(fmin(cf.dt_prev, cf.cap), fmin(cfl, 0.5 * h * h));
+    *cf.dt_out = dtr;
+    if (cf.abort && dtr < cf.dt_prev) *(volatile int*)cf.abort = 1;   // the rest of the graph leaves the state alone
     *cf.ticket = 0u;
   }
 }
@@ -480,8 +483,11 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) diag_kernel(const uint8_t* _
 // restriction to N+ ("on N+") + statistics: [mass_sum (fixed-point low word), rho_max, -rho_min,
 // -c_min, nonfinite, rho_max over M+ (the paper's ||ρ||∞, P:683 eq. sd-norm:max), -, -, mass high word]
 __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_t* __restrict__ flags, int n, const double* __restrict__ u, double* rho,
-                                double* c, double* stats) {
+                                double* c, double* stats, int* abort) {
   pdl_prologue();
+  // speculative step graphs: after a step whose dt rule failed (flux kernel) or whose state went
+  // non-finite (an earlier restriction) the state is left as it is
+  if (abort && *(volatile int*)abort) return;
   const long nn = (long)n * n * n;
   double msum = 0.0, rmax = -INFINITY, rmin = INFINITY, cmin = INFINITY, rmaxm = -INFINITY;
   int bad = 0;
@@ -541,6 +547,7 @@ __global__ void __launch_bounds__(TB, STENCIL_MINB) restrict_kernel(const uint8_
     atomicMax((unsigned long long*)(stats + 2), key(-b));
     atomicMax((unsigned long long*)(stats + 3), key(-d));
     if (sbad) atomicAdd(stats + 4, 1.0);
+    if (sbad && abort) atomicExch(abort, 1);
     atomicMax((unsigned long long*)(stats + 5), key(am));
   }
 }
@@ -657,7 +664,7 @@ cudaError_t launch_cfl_reduce(dpm_ctx* ctx, const double* c, double* out3, cudaS
 
 cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, double dt, double chi, double* fq_rho,
                             double* fq_c, cudaStream_t s, double* backup, double* zero6, double* cfl_out3,
-                            double dt_prev, double cap, double* dt_out) {
+                            double dt_prev, double cap, double* dt_out, int* abort) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   CflFuse cf;
   if (cfl_out3) {
@@ -667,6 +674,7 @@ cudaError_t launch_flux_rhs(dpm_ctx* ctx, const double* rho, const double* c, do
     cf.dt_prev = dt_prev;
     cf.cap = cap;
     cf.dt_out = dt_out;
+    cf.abort = abort;
   }
   static const bool use_list = [] {   // DPM_FLUX_LIST=0: the whole-box kernel
     const char* v = getenv("DPM_FLUX_LIST");
@@ -750,7 +758,7 @@ cudaError_t launch_diagnostics(dpm_ctx* ctx, const double* rho, const double* c,
 }
 
 cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, double* c, double* stats,
-                                  cudaStream_t s, bool zeroed) {
+                                  cudaStream_t s, bool zeroed, int* abort) {
   const long nn = (long)ctx->n * ctx->n * ctx->n;
   if (!zeroed) {   // (zeroed: an earlier kernel of the step cleared the 9 slots)
     cudaError_t e = cudaMemsetAsync(stats, 0, 9 * sizeof(double), s);
@@ -762,5 +770,5 @@ cudaError_t launch_restrict_stats(dpm_ctx* ctx, const double* u, double* rho, do
     return v ? std::max(1, atoi(v)) : 2;
   }();
   const int grid = (int)std::max<long>(1, std::min<long>((nn + TB - 1) / TB, 148L * rb));
-  return launch_pdl(restrict_kernel, grid, TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats);
+  return launch_pdl(restrict_kernel, grid, TB, 0, s, (const uint8_t*)ctx->flags, ctx->n, u, rho, c, stats, abort);
 }
