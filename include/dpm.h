@@ -232,9 +232,9 @@ dpm_status dpm_pks_diagnostics(dpm_ctx* ctx, const double* rho, const double* c,
    RHS (R20) -> 2 AP solves -> restriction to N+.
    Step 3 (R13) runs speculatively: up to 10 consecutive steps at dt_i = dt_{i-1} are replayed as one
    CUDA graph on a ctx-owned stream; every step also evaluates the dt rule on the device from its own
-   input state and saves that state.  The host reads the batch's log once; at the first step whose rule
-   asks for a smaller dt the state is rolled back to that step's saved input, the BEP is rebuilt at the
-   new dt (Step 4b) and stepping resumes.  The accepted dt sequence equals the host rule's.  The
+   input state.  From the first step whose rule asks for a smaller dt (or whose state went non-finite)
+   on, the graph leaves (rho, c) unchanged (a device flag), so the state is that step's input; the host
+   reads the batch's log once, rebuilds the BEP at the new dt (Step 4b) and stepping resumes.  The accepted dt sequence equals the host rule's.  The
    first step of a run evaluates the rule on the host.  The caller's `stream` is synchronized on entry
    and the call returns after the last step (synchronous).  log (HOST, nullable) receives nsteps
    entries.  DPM_ERR_NONFINITE on NaN/Inf (the state is left right after the failing step). */
