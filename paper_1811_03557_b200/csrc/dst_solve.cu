@@ -610,7 +610,20 @@ ztri_warp_kernel(double* __restrict__ u, int nlines, int n_rt, const double* __r
 // shared memory: y DST-I (S^T P, 4 x 4 register tiles), the exact z tridiagonal of every y-mode row
 // (warp per row, 2 entries per lane: the recurrences, Kogge–Stone carries and Sherman–Morrison of
 // ztri_warp_kernel), inverse y DST-I.  One launch instead of three (y, z, y).
-constexpr int PSN = 64, PSP = 65;   // largest n, shared-memory row pitch
+// PS_PP = 72 (≡ 8 mod 16): the DMMA B-fragment loads of the plane hit each 8-byte bank pair twice and its rows
+// are 16-byte aligned (double2 row accesses in the tridiagonal); PS_SP = 66 (≡ 2 mod 8): the A-fragment loads
+// of the sine matrix do the same (cfg3 12.75k -> 13.0k steps/s against 65 / 65)
+#ifndef PS_PP
+#define PS_PP 72
+#endif
+#ifndef PS_SP
+#define PS_SP 66
+#endif
+#ifndef PS_TRI_VEC
+#define PS_TRI_VEC 0   // double2 row pairs in the tridiagonal (needs an even PS_PP; measured slower: 12.8k vs 13.0k cfg3)
+#endif
+// largest n; shared-memory row pitches of the plane (PSP) and of the sine matrix (SSP)
+constexpr int PSN = 64, PSP = PS_PP, SSP = PS_SP;
 
 __global__ void sinmat_kernel(double* S, int n) {   // S[j][k] = sin(π (j+1)(k+1)/(n+1)), exact reduction
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -640,7 +653,7 @@ __device__ __forceinline__ void ps_apply(const double* S, double* P, int n) {
       for (int y = 0; y < n / 2; ++y) {
         double sv[4], ap[4], am[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) sv[i] = S[y * PSP + 4 * rb + i];
+        for (int i = 0; i < 4; ++i) sv[i] = S[y * SSP + 4 * rb + i];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const double p1 = P[y * PSP + cb + 16 * j], p2 = P[(n - 1 - y) * PSP + cb + 16 * j];
@@ -657,7 +670,7 @@ __device__ __forceinline__ void ps_apply(const double* S, double* P, int n) {
       for (int y = 0; y < n; ++y) {
         double sv[4], pv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) sv[i] = S[y * PSP + 4 * rb + i];
+        for (int i = 0; i < 4; ++i) sv[i] = S[y * SSP + 4 * rb + i];
 #pragma unroll
         for (int j = 0; j < 4; ++j) pv[j] = P[y * PSP + cb + 16 * j];
 #pragma unroll
@@ -710,7 +723,7 @@ __device__ __forceinline__ void ps_apply_dmma(const double* S, double* P, int n)
         const int i = mg + q * wpn;            // m-tile index of this slot
         if (i >= MH) break;
         const int be = 2 * (8 * i + rl);       // this lane's A row (even set); the odd set is be + 1
-        const double ae = yin ? S[be * PSP + y] : 0.0, ao = yin ? S[(be + 1) * PSP + y] : 0.0;
+        const double ae = yin ? S[be * SSP + y] : 0.0, ao = yin ? S[(be + 1) * SSP + y] : 0.0;
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(acc[0][q][0]), "+d"(acc[0][q][1]) : "d"(ae), "d"(bp));
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -802,7 +815,15 @@ __device__ __forceinline__ void ps_tri_rows(double* const (&row)[R], const bool 
     mp[r][0] = mu2[r];
 #pragma unroll
     for (int q = 1; q < 7; ++q) mp[r][q] = mp[r][q - 1] * mp[r][q - 1];
-    const double r0 = (valid[r] && k0 < n) ? row[r][k0] : 0.0, r1 = (valid[r] && k0 + 1 < n) ? row[r][k0 + 1] : 0.0;
+    double r0 = 0.0, r1 = 0.0;
+    if (valid[r] && k0 + 1 < n && (PSP % 2) == 0 && PS_TRI_VEC) {   // 16-byte aligned pair
+      const double2 v = *reinterpret_cast<const double2*>(row[r] + k0);
+      r0 = v.x;
+      r1 = v.y;
+    } else {
+      r0 = (valid[r] && k0 < n) ? row[r][k0] : 0.0;
+      r1 = (valid[r] && k0 + 1 < n) ? row[r][k0 + 1] : 0.0;
+    }
     y0[r] = rscale * r0;
     y1[r] = fma(mu[r], y0[r], rscale * r1);
     C[r] = y1[r];
@@ -850,8 +871,14 @@ __device__ __forceinline__ void ps_tri_rows(double* const (&row)[R], const bool 
       if ((rl >> q) & 1) pr *= mp[r][q];
     }
     const double pa0 = mu[r] * pl, pb1 = pr;
-    if (valid[r] && k0 < n) row[r][k0] = fma(mu[r], z0[r], -c2 * (pa0 - pb1 * mu[r]));
-    if (valid[r] && k0 + 1 < n) row[r][k0 + 1] = fma(mu[r], z1[r], -c2 * (pa0 * mu[r] - pb1));
+    const double o0 = fma(mu[r], z0[r], -c2 * (pa0 - pb1 * mu[r]));
+    const double o1 = fma(mu[r], z1[r], -c2 * (pa0 * mu[r] - pb1));
+    if (valid[r] && k0 + 1 < n && (PSP % 2) == 0 && PS_TRI_VEC) {
+      *reinterpret_cast<double2*>(row[r] + k0) = make_double2(o0, o1);
+    } else {
+      if (valid[r] && k0 < n) row[r][k0] = o0;
+      if (valid[r] && k0 + 1 < n) row[r][k0 + 1] = o1;
+    }
   }
 }
 
@@ -901,8 +928,8 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
                                                           double rscale) {
   pdl_prologue();
   extern __shared__ double psm_small[];
-  double* S = psm_small;           // [64][PSP]
-  double* P = S + PSN * PSP;       // [64][PSP]
+  double* S = psm_small;           // [64][SSP]
+  double* P = S + PSN * SSP;       // [64][PSP]
   double* lam = P + PSN * PSP;     // [64]
   const long plane = blockIdx.x;   // field * n + a
   const int a = (int)(plane % n), t = threadIdx.x;
@@ -913,7 +940,7 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
     for (int e = t; e < PSN * PSN; e += PS_THREADS) {
       const int r = e / PSN, c = e % PSN;
       const bool in = r < n && c < n;
-      cp_async8(sS + 8u * (unsigned)(r * PSP + c), in ? S_g + r * n + c : S_g, in);
+      cp_async8(sS + 8u * (unsigned)(r * SSP + c), in ? S_g + r * n + c : S_g, in);
       cp_async8(sP + 8u * (unsigned)(r * PSP + c), in ? g + (size_t)r * n + c : g, in);
     }
     cp_async_commit();
@@ -922,7 +949,8 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_kernel(double* __restr
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
   plane_small_body(S, P, lam, n, a, inv_dt, h2, rscale);
-  for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
+  for (int r = t >> 5; r < n; r += PS_THREADS / 32)   // (no per-element division)
+    for (int c = t & 31; c < n; c += 32) g[r * n + c] = P[r * PSP + c];
 }
 
 // Batched small-n plane pass (Step-4b rebuilds: K fields at once): persistent CTAs that load the sine
@@ -934,8 +962,8 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_batch_kernel(double* _
                                                                        double h2, double rscale, long nplanes) {
   pdl_prologue();
   extern __shared__ double psm_small[];
-  double* S = psm_small;              // [64][PSP]
-  double* PB = S + PSN * PSP;         // 2 x [64][PSP]
+  double* S = psm_small;              // [64][SSP]
+  double* PB = S + PSN * SSP;         // 2 x [64][PSP]
   double* lam = PB + 2 * PSN * PSP;   // [64]
   const int t = threadIdx.x;
   auto load_plane = [&](double* P, long plane) {
@@ -954,7 +982,7 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_batch_kernel(double* _
     for (int e = t; e < PSN * PSN; e += PS_THREADS) {
       const int r = e / PSN, c = e % PSN;
       const bool in = r < n && c < n;
-      cp_async8(sS + 8u * (unsigned)(r * PSP + c), in ? S_g + r * n + c : S_g, in);
+      cp_async8(sS + 8u * (unsigned)(r * SSP + c), in ? S_g + r * n + c : S_g, in);
     }
   }
   for (int i = t; i < n; i += blockDim.x) lam[i] = lam_g[i];
@@ -970,7 +998,8 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_batch_kernel(double* _
     double* P = PB + b * PSN * PSP;
     plane_small_body(S, P, lam, n, (int)(plane % n), inv_dt, h2, rscale);
     double* g = u + (size_t)plane * n * n;
-    for (int e = t; e < n * n; e += blockDim.x) g[e] = P[(e / n) * PSP + e % n];
+    for (int r = t >> 5; r < n; r += PS_THREADS / 32)
+      for (int c = t & 31; c < n; c += 32) g[r * n + c] = P[r * PSP + c];
     __syncthreads();   // the buffer is refilled by the prefetch of the next iteration but one
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
@@ -978,7 +1007,7 @@ __global__ void __launch_bounds__(PS_THREADS) plane_small_batch_kernel(double* _
 
 cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream_t s) {
   const int n = p.n;
-  const size_t smem = (2 * (size_t)PSN * PSP + PSN) * sizeof(double);
+  const size_t smem = ((size_t)PSN * (SSP + PSP) + PSN) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(plane_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const double sc = 2.0 / (n + 1);
@@ -988,7 +1017,7 @@ cudaError_t run_plane_small(const DstPlan& p, double* u, int nfields, cudaStream
     return !(v && atoi(v) == 0);
   }();
   if (batch_on && planes > 4L * 148) {
-    const size_t bsmem = (3 * (size_t)PSN * PSP + PSN) * sizeof(double);
+    const size_t bsmem = ((size_t)PSN * (SSP + 2 * PSP) + PSN) * sizeof(double);
     e = cudaFuncSetAttribute(plane_small_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem);
     if (e != cudaSuccess) return e;
     int occ = 1;
