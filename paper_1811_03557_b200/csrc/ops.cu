@@ -47,18 +47,46 @@ __device__ __forceinline__ double lop_gamma(const int32_t* __restrict__ gmap, co
   return acc - off * nb;
 }
 
+// The band point's seven γ positions (gmap lookups), shared by every right-hand side:
+// (I/dt - Δ_h)[v](p) = diag v(g0) - off Σ v(gn)  over the γ entries only (as lop_gamma)
+struct BandStencil {
+  int g0;
+  int gn[6];
+};
+__device__ __forceinline__ BandStencil band_stencil(const int32_t* __restrict__ gmap, int n, int64_t p) {
+  int i, j, k;
+  ijk(p, n, i, j, k);
+  BandStencil st;
+  st.g0 = gmap[p];
+  const int di[6] = {1, -1, 0, 0, 0, 0}, dj[6] = {0, 0, 1, -1, 0, 0}, dk[6] = {0, 0, 0, 0, 1, -1};
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const int a = i + di[q], b = j + dj[q], c = k + dk[q];
+    st.gn[q] = interior(n, a, b, c) ? gmap[flat(n, a, b, c)] : -1;
+  }
+  return st;
+}
+__device__ __forceinline__ double band_apply(const BandStencil& st, const double* __restrict__ v, double diag, double off) {
+  const double acc = st.g0 >= 0 ? diag * v[st.g0] : 0.0;
+  double nb = 0.0;
+#pragma unroll
+  for (int q = 0; q < 6; ++q)
+    if (st.gn[q] >= 0) nb += v[st.gn[q]];
+  return acc - off * nb;
+}
+
+// thread per (band point, chunk of POT_RC right-hand sides = blockIdx.y): no per-element 64-bit division,
+// the stencil's gmap lookups done once per point and chunk
+constexpr int POT_RC = 8;
 __global__ void potential_rhs_kernel(const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
                                      int64_t nband, const double* __restrict__ v, int64_t ldv, double* q,
                                      int nrhs, int n, double diag, double off) {
   const size_t field = (size_t)n * n * n;
-  const long total = (long)nband * nrhs;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
-    const int r = (int)(t / nband);
-    const long b = t - (long)r * nband;
+  for (long b = blockIdx.x * (long)blockDim.x + threadIdx.x; b < nband; b += (long)gridDim.x * blockDim.x) {
     const long p = band[b];
-    int i, j, k;
-    ijk(p, n, i, j, k);
-    q[r * field + p] = lop_gamma(gmap, v + (size_t)r * ldv, n, i, j, k, diag, off);
+    const BandStencil st = band_stencil(gmap, n, p);
+    const int r1 = min(nrhs, (int)(blockIdx.y + 1) * POT_RC);
+    for (int r = blockIdx.y * POT_RC; r < r1; ++r) q[r * field + p] = band_apply(st, v + (size_t)r * ldv, diag, off);
   }
 }
 
@@ -66,34 +94,30 @@ __global__ void potential_rhs_kernel(const int32_t* __restrict__ gmap, const int
 __global__ void potential_band_kernel(const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
                                       int64_t nband, const double* __restrict__ v, int64_t ldv, double* qb,
                                       int nrhs, int n, double diag, double off, const int32_t* __restrict__ pos) {
-  const long total = (long)nband * nrhs;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
-    const int r = (int)(t / nband);
-    const long b = t - (long)r * nband;
-    int i, j, k;
-    ijk(band[b], n, i, j, k);
-    qb[(size_t)r * nband + (pos ? pos[b] : b)] = lop_gamma(gmap, v + (size_t)r * ldv, n, i, j, k, diag, off);
+  for (long b = blockIdx.x * (long)blockDim.x + threadIdx.x; b < nband; b += (long)gridDim.x * blockDim.x) {
+    const BandStencil st = band_stencil(gmap, n, band[b]);
+    const long o = pos ? pos[b] : b;
+    const int r1 = min(nrhs, (int)(blockIdx.y + 1) * POT_RC);
+    for (int r = blockIdx.y * POT_RC; r < r1; ++r) qb[(size_t)r * nband + o] = band_apply(st, v + (size_t)r * ldv, diag, off);
   }
 }
 
 __global__ void trace_kernel(const double* __restrict__ u, const int64_t* __restrict__ list, int64_t m, double* out,
                              int64_t batch, size_t field) {
   pdl_prologue();
-  const long total = (long)m * batch;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < total; t += (long)gridDim.x * blockDim.x) {
-    const long b = t / m, i = t - b * m;
-    out[t] = u[b * field + list[i]];
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < m; i += (long)gridDim.x * blockDim.x) {
+    const int64_t p = list[i];
+    for (long b = 0; b < batch; ++b) out[b * m + i] = u[b * field + p];
   }
 }
 
 __global__ void bep_gather_kernel(const double* __restrict__ U, int ncols, size_t field, const int64_t* __restrict__ gamma,
                                   int64_t ng, const int64_t* __restrict__ gin, const int32_t* __restrict__ gin_pos,
                                   int64_t ngin, const double* __restrict__ E, int c0, double* PgE, double* B) {
-  const long tot = (long)(ng + ngin) * ncols;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
-    const int c = (int)(t / (ng + ngin));
-    const long r = t - (long)c * (ng + ngin);
-    const double* Uc = U + (size_t)c * field;
+  // column c = blockIdx.y, rows grid-stride over x (no per-element 64-bit division)
+  const int c = blockIdx.y;
+  const double* Uc = U + (size_t)c * field;
+  for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < ng + ngin; r += (long)gridDim.x * blockDim.x) {
     if (r < ng) {
       if (PgE) PgE[(size_t)c * ng + r] = Uc[gamma[r]];
     } else {
@@ -610,7 +634,7 @@ cudaError_t launch_potential_scatter(const dpm_ctx* ctx, const double* v, int64_
   if (nb * nrhs == 0) return cudaSuccess;
   const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
   DPM_COUNT_LAUNCH(1);
-  potential_rhs_kernel<<<grid_for(nb * nrhs), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, q, nrhs, n,
+  potential_rhs_kernel<<<dim3((unsigned)((nb + TB - 1) / TB), (nrhs + POT_RC - 1) / POT_RC), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, q, nrhs, n,
                                                           diag, off);
   return cudaGetLastError();
 }
@@ -621,7 +645,7 @@ cudaError_t launch_potential_band(const dpm_ctx* ctx, const double* v, int64_t l
   if (nb * nrhs == 0) return cudaSuccess;
   const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
   DPM_COUNT_LAUNCH(1);
-  potential_band_kernel<<<grid_for(nb * nrhs), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, qb, nrhs,
+  potential_band_kernel<<<dim3((unsigned)((nb + TB - 1) / TB), (nrhs + POT_RC - 1) / POT_RC), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, qb, nrhs,
                                                            ctx->n, diag, off, pos);
   return cudaGetLastError();
 }
@@ -631,7 +655,7 @@ cudaError_t launch_trace(const dpm_ctx* ctx, const double* u, double* out, int w
   const int64_t m = ctx->counts[which];
   if (m * batch == 0) return cudaSuccess;
   DPM_COUNT_LAUNCH(1);
-  return launch_pdl(trace_kernel, grid_for(m * batch), TB, 0, s, u, (const int64_t*)ctx->lists[which], m, out, batch,
+  return launch_pdl(trace_kernel, grid_for(m), TB, 0, s, u, (const int64_t*)ctx->lists[which], m, out, batch,
                     (size_t)n * n * n);
 }
 
@@ -640,7 +664,8 @@ cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int n
   const int n = ctx->n;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
   DPM_COUNT_LAUNCH(1);
-  bep_gather_kernel<<<grid_for((ng + ngin) * ncols), TB, 0, s>>>(U, ncols, (size_t)n * n * n, ctx->lists[DPM_SET_GAMMA], ng,
+  if (ncols == 0) return cudaSuccess;
+  bep_gather_kernel<<<dim3((unsigned)std::min<int64_t>((ng + ngin + TB - 1) / TB, 148L * 16), ncols), TB, 0, s>>>(U, ncols, (size_t)n * n * n, ctx->lists[DPM_SET_GAMMA], ng,
                                                                  ctx->lists[DPM_SET_GAMMA_IN], ctx->gin_pos, ngin, ctx->E,
                                                                  c0, PgE, B);
   return cudaGetLastError();
