@@ -421,10 +421,8 @@ __global__ void dd_bep_gather_kernel(const double* __restrict__ U, int ncols, si
                                      const int64_t* __restrict__ gamma, int64_t ng, const int32_t* __restrict__ rows,
                                      int64_t nrows, const double* __restrict__ Eraw, int c0, PieceBlocks pb,
                                      double* B) {
-  const long tot = (long)nrows * ncols;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
-    const int cl = (int)(t / nrows);
-    const long ri = t - (long)cl * nrows;
+  const int cl = blockIdx.y;   // column (no per-element 64-bit division)
+  for (long ri = blockIdx.x * (long)blockDim.x + threadIdx.x; ri < nrows; ri += (long)gridDim.x * blockDim.x) {
     const int pos = rows[2 * ri], piece = rows[2 * ri + 1];
     const int c = c0 + cl;
     int blk = 0;
@@ -438,11 +436,9 @@ __global__ void dd_bep_gather_kernel(const double* __restrict__ U, int ncols, si
 // g[r][i] = u_r[gamma[pos_i]]  (BEP right-hand sides replicated over a point's pieces)
 __global__ void dd_rows_trace_kernel(const double* __restrict__ U, size_t field, const int64_t* __restrict__ gamma,
                                      const int32_t* __restrict__ rows, int64_t nrows, int nrhs, double* g) {
-  const long tot = (long)nrows * nrhs;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
-    const int r = (int)(t / nrows);
-    const long i = t - (long)r * nrows;
-    g[t] = U[(size_t)r * field + gamma[rows[2 * i]]];
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nrows; i += (long)gridDim.x * blockDim.x) {
+    const int64_t p = gamma[rows[2 * i]];
+    for (int r = 0; r < nrhs; ++r) g[(size_t)r * nrows + i] = U[(size_t)r * field + p];
   }
 }
 
@@ -976,13 +972,20 @@ dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream) {
   }
   for (int a = 0; a < K; a += ch) {
     const int ncol = std::min(ch, K - a);
-    DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, ncol, s));
-    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, ncol, nullptr, 0, s));
+    if (bep_zbox_enabled() && ctx->K >= 128 && ctx->plan.solver == DPM_SOLVER_DST2_TRIDIAG) {   // (as dpm_bep_columns)
+      double* zb = nullptr;
+      DPM_CUDA_TRY(ctx, bep_zbox(ctx, ncol, &zb, s));
+      DPM_CUDA_TRY(ctx, launch_potential_scatter(ctx, ctx->E + (size_t)a * ng, ng, zb, ncol, s));
+      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, zb, ctx->work, ncol, nullptr, 0, s));
+    } else {
+      DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, ncol, s));
+      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, ncol, nullptr, 0, s));
+    }
     DPM_COUNT_LAUNCH(1);
     PieceBlocks pb{};
     pb.npieces = ctx->dd_npieces;
     for (int p = 0; p <= ctx->dd_npieces && p < 6; ++p) pb.start[p] = ctx->dd_blk[p];
-    dd_bep_gather_kernel<<<grid_for(ctx->n_rows * ncol), TB, 0, s>>>(
+    dd_bep_gather_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ctx->n_rows + TB - 1) / TB, 148L * 16)), ncol), TB, 0, s>>>(
         ctx->work, ncol, field, ctx->lists[DPM_SET_GAMMA], ng, ctx->dd_rows, ctx->n_rows, ctx->dd_Eraw, a, pb,
         ctx->dd_B + (size_t)a * ctx->n_rows);
     DPM_CUDA_TRY(ctx, cudaGetLastError());
@@ -1163,7 +1166,7 @@ dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* strea
   const size_t field = (size_t)ctx->n * ctx->n * ctx->n;
   if (!ctx->dd_g) return DPM_ERR_STATE;
   DPM_COUNT_LAUNCH(1);
-  dd_rows_trace_kernel<<<grid_for(ctx->n_rows * 2), TB, 0, s>>>(wk, field, ctx->lists[DPM_SET_GAMMA], ctx->dd_rows,
+  dd_rows_trace_kernel<<<grid_for(ctx->n_rows), TB, 0, s>>>(wk, field, ctx->lists[DPM_SET_GAMMA], ctx->dd_rows,
                                                                 ctx->n_rows, 2, ctx->dd_g);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   DPM_CUDA_TRY(ctx, lsq_gemv(ctx->dd_M, ctx->n_rows, ctx->K, ctx->dd_g, 2, y, s));           // y_s = M_s g_s
@@ -1229,7 +1232,7 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
   DPM_COUNT_LAUNCH(1);
   dd_stack_signs_kernel<<<(noct * K + TB - 1) / TB, TB, 0, s>>>(sp, noct, K, Sg);
   DPM_COUNT_LAUNCH(1);
-  dd_rows_trace_kernel<<<grid_for(m * nv), TB, 0, s>>>(wk, field, o0->lists[DPM_SET_GAMMA], o0->dd_rows, m, nv, G);
+  dd_rows_trace_kernel<<<grid_for(m), TB, 0, s>>>(wk, field, o0->lists[DPM_SET_GAMMA], o0->dd_rows, m, nv, G);
   const size_t KK = (size_t)K * K;
   const double* R = o0->dd_R + 2 * KK;    // R = R2 R1
   const double* W2 = o0->dd_R + 4 * KK;   // R^{-1}
@@ -1333,7 +1336,7 @@ dpm_status dpm_dd_local_begin(dpm_ctx* ctx, const double* rho, const double* c, 
   DPM_CUDA_TRY(ctx, launch_flux_rhs(ctx, rho, c, ctx->dt, chi, fq, fq + field, s));          // Step 4a
   DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
   DPM_COUNT_LAUNCH(1);
-  dd_rows_trace_kernel<<<grid_for(ctx->n_rows * 2), TB, 0, s>>>(wk, field, ctx->lists[DPM_SET_GAMMA], ctx->dd_rows,
+  dd_rows_trace_kernel<<<grid_for(ctx->n_rows), TB, 0, s>>>(wk, field, ctx->lists[DPM_SET_GAMMA], ctx->dd_rows,
                                                                 ctx->n_rows, 2, ctx->dd_g);
   DPM_CUDA_TRY(ctx, cudaGetLastError());
   DPM_CUDA_TRY(ctx, lsq_gemv(ctx->dd_M, ctx->n_rows, ctx->K, ctx->dd_g, 2, y, s));           // y_s = M_s g_s

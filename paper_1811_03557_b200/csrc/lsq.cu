@@ -32,9 +32,11 @@ __global__ void colnorm_kernel(const double* __restrict__ B, int64_t m, double* 
 }
 
 __global__ void scale_cols_kernel(const double* __restrict__ B, int64_t m, int K, const double* scale, double* A) {
-  const long tot = (long)m * K;
-  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x)
-    A[t] = B[t] * scale[t / m];
+  const int c = blockIdx.y;   // column (no per-element 64-bit division)
+  const double sc = scale[c];
+  const size_t o = (size_t)c * m;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < m; i += (long)gridDim.x * blockDim.x)
+    A[o + i] = B[o + i] * sc;
 }
 
 // Blocked right-looking Cholesky G = R^T R (upper R, column-major K x K, upper triangle used),
@@ -415,7 +417,8 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
     DPM_COUNT_LAUNCH(1);
     colnorm_kernel<<<K, TB, 0, q>>>(B, m, ctx->colscale);
     DPM_COUNT_LAUNCH(1);
-    scale_cols_kernel<<<148 * 8, TB, 0, q>>>(B, m, K, ctx->colscale, ctx->Q);
+    scale_cols_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((m + TB - 1) / TB, 64)), K), TB, 0, q>>>(
+        B, m, K, ctx->colscale, ctx->Q);
     dpm_status st;
     // CholeskyQR2 ping-pong: Q -> Mlsq (scratch until the operator is formed) -> Q
     if ((st = chol_qr_pass(ctx, ctx->Q, m, K, R1, Riw, ctx->Mlsq, dfail, q)) != DPM_OK) return st;
@@ -1041,7 +1044,8 @@ cudaError_t lsq_trmm(const double* A, const double* B, double* C, int K, cudaStr
 
 cudaError_t lsq_scale_cols(const double* B, int64_t m, int K, const double* scale, double* A, cudaStream_t s) {
   DPM_COUNT_LAUNCH(1);
-  scale_cols_kernel<<<148 * 8, TB, 0, s>>>(B, m, K, scale, A);
+  scale_cols_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((m + TB - 1) / TB, 64)), K), TB, 0, s>>>(
+      B, m, K, scale, A);
   return cudaGetLastError();
 }
 

@@ -665,7 +665,7 @@ cudaError_t launch_bep_gather(const dpm_ctx* ctx, const double* U, int c0, int n
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
   DPM_COUNT_LAUNCH(1);
   if (ncols == 0) return cudaSuccess;
-  bep_gather_kernel<<<dim3((unsigned)std::min<int64_t>((ng + ngin + TB - 1) / TB, 148L * 16), ncols), TB, 0, s>>>(U, ncols, (size_t)n * n * n, ctx->lists[DPM_SET_GAMMA], ng,
+  bep_gather_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ng + ngin + TB - 1) / TB, 148L * 16)), ncols), TB, 0, s>>>(U, ncols, (size_t)n * n * n, ctx->lists[DPM_SET_GAMMA], ng,
                                                                  ctx->lists[DPM_SET_GAMMA_IN], ctx->gin_pos, ngin, ctx->E,
                                                                  c0, PgE, B);
   return cudaGetLastError();
