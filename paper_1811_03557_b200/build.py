@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdpm.so")
 OBJDIR = os.path.join(HERE, "build")
-SOURCES = ["dst_solve.cu", "dst128.cu", "bep_fused.cu", "dd.cu", "setup.cu", "ops.cu", "lsq.cu", "dpm_abi.cu"]
+SOURCES = ["dst_solve.cu", "dst128.cu", "bep_fused.cu", "bep_sym.cu", "dd.cu", "setup.cu", "ops.cu", "lsq.cu", "dpm_abi.cu"]
 HEADERS = ["dpm_internal.h", "sh_device.cuh", os.path.join("..", "..", "include", "dpm.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

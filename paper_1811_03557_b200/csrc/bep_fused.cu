@@ -139,6 +139,7 @@ cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double*
 }
 
 void bep_fused_free(dpm_ctx* c) {
+  bep_sym_free(c);
   void* ptrs[] = {c->bepf_btab, c->bepf_bpos, c->bepf_qb, c->bepf_zbox};
   for (void* p : ptrs)
     if (p) cudaFree(p);

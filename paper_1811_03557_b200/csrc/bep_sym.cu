@@ -1,0 +1,422 @@
+// NEXT-1: BEP columns on one octant of the grid, by reflection symmetry.
+//
+// A BEP column is u_c = AP(q_c), q_c = χ_{M-}(I/dt - Δ_h)[E_c] on the band, then
+// Tr_γ u_c and B[:, c] = E_in[:, c] - u_c[γ_in].  When the grid and the point sets are symmetric under the
+// three reflections x_a -> -x_a of the box (n even, centred domain: cfg1-cfg4, the paper's sphere tests)
+// and every column E_c is even or odd under each reflection (the real spherical-harmonic bases are:
+// Y_lm has parity (-1)^m / (-1)^(m+1) in x, ±1 in y, (-1)^(l+m) in z), then q_c and u_c have the same
+// parities (the 7-point operator commutes with the reflections), and u_c is fixed by its values on the
+// octant [0, m)^3, m = n/2 (0-based interior indices; the mirror of i is n-1-i).  On the octant, with
+// s_a = ±1 the parity along axis a, the AP is
+//     (I/dt + T_x,sx + T_y,sy + T_z,sz) u = q,   T_s = tridiag(-1, 2, -1)/h^2 on i = 0..m-1,
+//     u_{-1} = 0 (Dirichlet box wall), u_m = s u_{m-1} (the mirror),
+// and T_s is diagonalised by S_s[j][b] = sin(π k_b (j+1)/(n+1)) with k_b = 2b+1 (s = +1) or 2b+2 (s = -1)
+// (the DST-I modes of that parity; eigenvalues λ_k of R26, Σ_j S_s[j][b]^2 = (n+1)/4).  So:
+//   (1) scatter the octant's band values of q_c into boxes zeroed once (m^3 per column);
+//   (2) forward transform along y and z (per x-plane: Q = S_y^T P S_z, two DMMA GEMMs in shared memory);
+//   (3) per (b, c) spectral pencil, the tridiagonal solve along x with the mirror row (Thomas, in
+//       registers), times the inverse-transform scale (4/(n+1))^2;
+//   (4) inverse transform along y and z (P = S_y U S_z^T);
+//   (5) gather γ / γ_in through the octant map with the parity signs.
+// Per column: m^3 = n^3/8 points, two 2-GEMM plane passes and one tridiagonal pass over 8 n^3/8 bytes each,
+// instead of three full n^3 passes.  Columns that are not parity-definite, asymmetric
+// sets, odd n or n > 128 take the full path (dpm_bep_columns).  DPM_BEP_SYM=0 disables, DPM_BEP_SYM=2 makes a
+// context the octant path does not apply to fail (cudaErrorNotSupported) instead of falling back.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "dpm_internal.h"
+
+namespace {
+
+constexpr int SYM_NW = 4, SYM_NT = SYM_NW * 32;
+constexpr int SYM_MMAX = 64;
+
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int MP>
+struct SymGeo {
+  static constexpr int LD = MP + 8;                 // ≡ 8 mod 16 doubles: conflict-free B fragments
+  static constexpr int RT = MP / 8, CF = MP / 8, KS = MP / 4;
+  static constexpr int RF = (RT + SYM_NW - 1) / SYM_NW;
+};
+
+// Y^T <- A X over MP x MP tiles in shared memory (X[k][col] at k*LD + col; the result D[row][col] is
+// written to Y[col*LD + row]); A[r][k] = S[k][r] (TRANS) or S[r][k], S the zero-padded MP x MP table.
+template <int MP>
+__device__ __forceinline__ void sym_gemm(const double* __restrict__ S, bool trans, const double* X, double* Y) {
+  using G = SymGeo<MP>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[G::RF][G::CF][2];
+#pragma unroll
+  for (int f = 0; f < G::RF; ++f)
+#pragma unroll
+    for (int c = 0; c < G::CF; ++c) acc[f][c][0] = acc[f][c][1] = 0.0;
+#pragma unroll 4
+  for (int ks = 0; ks < G::KS; ++ks) {
+    const int kr = ks * 4 + (lane & 3);
+    double a[G::RF];
+#pragma unroll
+    for (int f = 0; f < G::RF; ++f) {
+      const int rt = warp * G::RF + f, row = rt * 8 + (lane >> 2);
+      a[f] = rt < G::RT ? __ldg(trans ? S + kr * MP + row : S + row * MP + kr) : 0.0;
+    }
+    double b[G::CF];
+#pragma unroll
+    for (int c = 0; c < G::CF; ++c) b[c] = X[kr * G::LD + c * 8 + (lane >> 2)];
+#pragma unroll
+    for (int f = 0; f < G::RF; ++f)
+#pragma unroll
+      for (int c = 0; c < G::CF; ++c)
+        if (warp * G::RF + f < G::RT) dmma884(acc[f][c], a[f], b[c]);
+  }
+#pragma unroll
+  for (int f = 0; f < G::RF; ++f) {
+    const int rt = warp * G::RF + f;
+    if (rt >= G::RT) continue;
+    const int row = rt * 8 + (lane >> 2);
+#pragma unroll
+    for (int c = 0; c < G::CF; ++c) {
+      const int col = c * 8 + 2 * (lane & 3);
+      Y[col * G::LD + row] = acc[f][c][0];
+      Y[(col + 1) * G::LD + row] = acc[f][c][1];
+    }
+  }
+}
+
+// (2) / (4): per x-plane (column cc, plane i) of the m^3 octant boxes: forward Q = S_y^T P S_z, inverse
+// P = S_y Q S_z^T (S_y, S_z the tables of the column's y / z parities, par bits 1 / 2).
+template <int MP, bool FWD>
+__global__ void __launch_bounds__(SYM_NT) sym_yz_kernel(const double* in, double* out, int ncols, int m,
+                                                        const uint8_t* __restrict__ par,
+                                                        const double* __restrict__ S) {
+  using G = SymGeo<MP>;
+  extern __shared__ __align__(16) double sh[];
+  double* X = sh;
+  double* Y = sh + MP * G::LD;
+  for (int e = threadIdx.x; e < MP * G::LD; e += SYM_NT) X[e] = 0.0;   // padding stays zero (see below)
+  __syncthreads();
+  const long m2 = (long)m * m, nplanes = (long)ncols * m;
+  for (long p = blockIdx.x; p < nplanes; p += gridDim.x) {
+    const int cc = (int)(p / m);
+    const int pr = par[cc];
+    const double* src = in + p * m2;
+    for (int e = threadIdx.x; e < m * MP; e += SYM_NT) {
+      const int j = e / MP, k = e % MP;
+      if (k < m) X[j * G::LD + k] = src[j * m + k];
+    }
+    __syncthreads();
+    // rows / columns >= m: the padded table rows and columns are zero, so the padding of X stays zero
+    sym_gemm<MP>(S + ((pr >> 1) & 1) * MP * MP, FWD, X, Y);
+    __syncthreads();
+    sym_gemm<MP>(S + ((pr >> 2) & 1) * MP * MP, FWD, Y, X);
+    __syncthreads();
+    double* dst = out + p * m2;
+    for (int e = threadIdx.x; e < m * MP; e += SYM_NT) {
+      const int j = e / MP, k = e % MP;
+      if (k < m) dst[j * m + k] = X[j * G::LD + k];
+    }
+    __syncthreads();
+  }
+}
+
+// (3): per spectral pencil (column cc, w = b*m + c): (1/dt + λ_b + λ_c + T_x,sx) v = q along x, then
+// v *= scale.  Thomas with the elimination factors in shared memory and the right-hand side in registers.
+template <int MP>
+__global__ void __launch_bounds__(SYM_NT) sym_x_kernel(double* u, int ncols, int m, const uint8_t* __restrict__ par,
+                                                       const double* __restrict__ lamr, double inv_dt, double h2i,
+                                                       double scale) {
+  extern __shared__ __align__(16) double ef[];   // [MP][SYM_NT]
+  const long m2 = (long)m * m, total = (long)ncols * m2;
+  const long id = (long)blockIdx.x * SYM_NT + threadIdx.x;
+  if (id >= total) return;
+  const int cc = (int)(id / m2);
+  const int w = (int)(id - (long)cc * m2);
+  const int b = w / m, c = w - b * m;
+  const int pr = par[cc];
+  const double d = ((inv_dt + lamr[((pr >> 1) & 1) * MP + b]) + lamr[((pr >> 2) & 1) * MP + c]) + 2.0 * h2i;
+  const double dlast = (pr & 1) ? d + h2i : d - h2i;   // u_m = -u_{m-1} (odd) / +u_{m-1} (even)
+  double* col = u + (long)cc * m2 * m + w;
+  double g[MP];
+#pragma unroll
+  for (int i = 0; i < MP; ++i) g[i] = i < m ? col[(long)i * m2] : 0.0;
+  double eprev = 0.0, gprev = 0.0;
+#pragma unroll
+  for (int i = 0; i < MP; ++i) {
+    if (i < m) {
+      const double den = (i == m - 1 ? dlast : d) - h2i * eprev;
+      const double r = 1.0 / den;
+      eprev = h2i * r;
+      gprev = (g[i] + h2i * gprev) * r;
+      g[i] = gprev;
+      ef[i * SYM_NT + threadIdx.x] = eprev;
+    }
+  }
+  double next = 0.0;
+#pragma unroll
+  for (int i = MP - 1; i >= 0; --i) {
+    if (i < m) {
+      next = (i == m - 1) ? g[i] : g[i] + ef[i * SYM_NT + threadIdx.x] * next;
+      col[(long)i * m2] = next * scale;
+    }
+  }
+}
+
+// (5): PgE = Tr_γ u, B = E_in - Tr_γin u through the octant map: gidx[r] = octant index | reflection bits << 24
+__global__ void sym_gather_kernel(const double* __restrict__ U, long m3, const int32_t* __restrict__ gidx, long ng,
+                                  long ngin, const int32_t* __restrict__ gin_pos, const double* __restrict__ E,
+                                  int c0, int cout0, const uint8_t* __restrict__ par, double* PgE, double* B) {
+  const int cc = blockIdx.y;
+  const double* Uc = U + (long)cc * m3;
+  const int pr = par[cc];
+  const int col = c0 + cc - cout0;
+  for (long r = blockIdx.x * (long)blockDim.x + threadIdx.x; r < ng + ngin; r += (long)gridDim.x * blockDim.x) {
+    const int e = gidx[r];
+    double v = Uc[e & 0xFFFFFF];
+    if (__popc((e >> 24) & pr) & 1) v = -v;
+    if (r < ng) {
+      if (PgE) PgE[(long)col * ng + r] = v;
+    } else if (B) {
+      const long i = r - ng;
+      B[(long)col * ngin + i] = E[(long)(c0 + cc) * ng + gin_pos[i]] - v;
+    }
+  }
+}
+
+// parity sums of every column of E: out[c] = {Σ E^2, Σ (E - E∘mirror_a)^2 (a = x, y, z), Σ (E + E∘mirror_a)^2}
+__global__ void sym_parity_kernel(const double* __restrict__ E, long ng, const int32_t* __restrict__ mir, int K,
+                                  double* out) {
+  __shared__ double red[7][256];
+  const int c = blockIdx.x;
+  const double* Ec = E + (long)c * ng;
+  double s[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (long r = threadIdx.x; r < ng; r += blockDim.x) {
+    const double v = Ec[r];
+    s[0] += v * v;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double w = Ec[mir[a * ng + r]];
+      s[1 + a] += (v - w) * (v - w);
+      s[4 + a] += (v + w) * (v + w);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 7; ++q) red[q][threadIdx.x] = s[q];
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+#pragma unroll
+      for (int q = 0; q < 7; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x < 7) out[(long)c * 7 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+template <typename T>
+cudaError_t upload(T** dst, const std::vector<T>& v) {
+  cudaError_t e = cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T));
+  if (e != cudaSuccess) return e;
+  return v.empty() ? cudaSuccess : cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+int sym_mp(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : m <= 32 ? 32 : 64; }
+
+// Decide once per context whether the octant path applies and build its tables (host sync: first call only).
+cudaError_t sym_prepare(dpm_ctx* ctx) {
+  ctx->sym = -1;
+  const char* env = getenv("DPM_BEP_SYM");
+  if (env && atoi(env) == 0) return cudaSuccess;
+  const int n = ctx->n;
+  if (n % 2 || n / 2 > SYM_MMAX || !ctx->E || ctx->dd == 1 || ctx->K == 0) return cudaSuccess;
+  const int m = n / 2;
+  const long nn = (long)n * n, n3 = nn * n;
+  // the sets the potential RHS and the traces read: γ (gmap), the band, M+, γ_in
+  const int sets[4] = {DPM_SET_GAMMA, DPM_SET_BAND, DPM_SET_MPLUS, DPM_SET_GAMMA_IN};
+  std::vector<int64_t> L[4];
+  cudaError_t e;
+  for (int q = 0; q < 4; ++q) {
+    L[q].resize(ctx->counts[sets[q]]);
+    if (!L[q].empty() &&
+        (e = cudaMemcpy(L[q].data(), ctx->lists[sets[q]], L[q].size() * 8, cudaMemcpyDeviceToHost)) != cudaSuccess)
+      return e;
+  }
+  auto mirror = [&](int64_t p, int a) -> int64_t {
+    const int i = (int)(p / nn), j = (int)((p / n) % n), k = (int)(p % n);
+    if (a == 0) return ((int64_t)(n - 1 - i) * n + j) * n + k;
+    if (a == 1) return ((int64_t)i * n + (n - 1 - j)) * n + k;
+    return ((int64_t)i * n + j) * n + (n - 1 - k);
+  };
+  std::vector<uint8_t> in(n3);
+  for (int q = 0; q < 4; ++q) {
+    std::fill(in.begin(), in.end(), 0);
+    for (int64_t p : L[q]) in[p] = 1;
+    for (int64_t p : L[q])
+      for (int a = 0; a < 3; ++a)
+        if (!in[mirror(p, a)]) return cudaSuccess;   // not reflection-symmetric: full path
+  }
+  const std::vector<int64_t>& gam = L[0];
+  const long ng = (long)gam.size(), ngin = (long)L[3].size();
+  std::vector<int32_t> gpos(n3, -1);
+  for (long r = 0; r < ng; ++r) gpos[gam[r]] = (int32_t)r;
+  std::vector<int32_t> mir(3 * ng);
+  for (int a = 0; a < 3; ++a)
+    for (long r = 0; r < ng; ++r) mir[a * ng + r] = gpos[mirror(gam[r], a)];
+  // parity of every column of E
+  int32_t* dmir = nullptr;
+  double* dsum = nullptr;
+  const int K = ctx->K;
+  if ((e = upload(&dmir, mir)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&dsum, (size_t)K * 7 * sizeof(double))) != cudaSuccess) { cudaFree(dmir); return e; }
+  DPM_COUNT_LAUNCH(1);
+  sym_parity_kernel<<<K, 256>>>(ctx->E, ng, dmir, K, dsum);
+  std::vector<double> sums((size_t)K * 7);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(sums.data(), dsum, sums.size() * 8, cudaMemcpyDeviceToHost);
+  cudaFree(dmir);
+  cudaFree(dsum);
+  if (e != cudaSuccess) return e;
+  std::vector<uint8_t> par(K);
+  constexpr double tol = 1e-20;   // squared relative: a column within 1e-10 of even / odd
+  for (int c = 0; c < K; ++c) {
+    const double* s = &sums[(size_t)c * 7];
+    uint8_t p = 0;
+    for (int a = 0; a < 3; ++a) {
+      if (s[1 + a] <= tol * s[0]) continue;          // even
+      if (s[4 + a] <= tol * s[0]) { p |= 1 << a; continue; }   // odd
+      return cudaSuccess;                             // not parity-definite: full path
+    }
+    par[c] = p;
+  }
+  // octant band list, γ / γ_in octant map, sine tables, reduced eigenvalues
+  std::vector<int64_t> olist;
+  std::vector<int32_t> odst;
+  for (int64_t p : L[1]) {
+    const int i = (int)(p / nn), j = (int)((p / n) % n), k = (int)(p % n);
+    if (i < m && j < m && k < m) {
+      olist.push_back(p);
+      odst.push_back((int32_t)(((long)i * m + j) * m + k));
+    }
+  }
+  auto octant = [&](int64_t p) -> int32_t {
+    int i = (int)(p / nn), j = (int)((p / n) % n), k = (int)(p % n), bits = 0;
+    if (i >= m) { i = n - 1 - i; bits |= 1; }
+    if (j >= m) { j = n - 1 - j; bits |= 2; }
+    if (k >= m) { k = n - 1 - k; bits |= 4; }
+    return (int32_t)((((long)i * m + j) * m + k) | ((long)bits << 24));
+  };
+  std::vector<int32_t> gidx(ng + ngin);
+  for (long r = 0; r < ng; ++r) gidx[r] = octant(gam[r]);
+  for (long r = 0; r < ngin; ++r) gidx[ng + r] = octant(L[3][r]);
+  const int MP = sym_mp(m);
+  std::vector<double> S(2 * (size_t)MP * MP, 0.0), lam(2 * MP, 0.0);
+  const long per = 2L * (n + 1);
+  for (int s = 0; s < 2; ++s)
+    for (int b = 0; b < m; ++b) {
+      const long k = 2L * b + 1 + s;
+      for (int j = 0; j < m; ++j) S[((size_t)s * MP + j) * MP + b] = std::sin(M_PI * (double)((k * (j + 1)) % per) / (n + 1));
+      const double sk = std::sin((double)k * M_PI / (2.0 * (n + 1)));
+      lam[s * MP + b] = (4.0 / (ctx->h * ctx->h)) * sk * sk;
+    }
+  if ((e = upload(&ctx->sym_list, olist)) != cudaSuccess) return e;
+  if ((e = upload(&ctx->sym_dst, odst)) != cudaSuccess) return e;
+  if ((e = upload(&ctx->sym_gidx, gidx)) != cudaSuccess) return e;
+  if ((e = upload(&ctx->sym_par, par)) != cudaSuccess) return e;
+  if ((e = upload(&ctx->sym_S, S)) != cudaSuccess) return e;
+  if ((e = upload(&ctx->sym_lam, lam)) != cudaSuccess) return e;
+  ctx->sym_nlist = (int64_t)olist.size();
+  ctx->sym_m = m;
+  ctx->sym = 1;
+  return cudaSuccess;
+}
+
+template <int MP>
+cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const uint8_t* par, cudaStream_t s) {
+  const int m = ctx->sym_m, n = ctx->n;
+  constexpr size_t smem_yz = 2 * (size_t)MP * SymGeo<MP>::LD * sizeof(double);
+  constexpr size_t smem_x = (size_t)MP * SYM_NT * sizeof(double);
+  cudaFuncSetAttribute(sym_yz_kernel<MP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
+  cudaFuncSetAttribute(sym_yz_kernel<MP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
+  cudaFuncSetAttribute(sym_x_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x);
+  const long planes = (long)nc * m;
+  const int grid_yz = (int)std::min<long>(planes, 148L * 3);
+  const long pencils = (long)nc * m * m;
+  const double h2i = 1.0 / (ctx->h * ctx->h), scale = (4.0 / (n + 1)) * (4.0 / (n + 1));
+  DPM_COUNT_LAUNCH(3);
+  sym_yz_kernel<MP, true><<<grid_yz, SYM_NT, smem_yz, s>>>(q, u, nc, m, par, ctx->sym_S);
+  sym_x_kernel<MP><<<(unsigned)((pencils + SYM_NT - 1) / SYM_NT), SYM_NT, smem_x, s>>>(u, nc, m, par, ctx->sym_lam,
+                                                                                    1.0 / ctx->dt, h2i, scale);
+  sym_yz_kernel<MP, false><<<grid_yz, SYM_NT, smem_yz, s>>>(u, u, nc, m, par, ctx->sym_S);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Columns [c0, c1) by the octant path when it applies (*done = true), else *done = false and nothing runs.
+cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B, cudaStream_t s, bool* done) {
+  *done = false;
+  if (ctx->sym == 0) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return cudaSuccess;
+    cudaError_t e = cudaStreamSynchronize(s);   // E and the sets are ready
+    if (e != cudaSuccess) return e;
+    if ((e = sym_prepare(ctx)) != cudaSuccess) return e;
+  }
+  if (ctx->sym != 1) {   // DPM_BEP_SYM=2: the octant path is required (tests), its absence an error
+    const char* env = getenv("DPM_BEP_SYM");
+    return env && atoi(env) == 2 ? cudaErrorNotSupported : cudaSuccess;
+  }
+  const int m = ctx->sym_m, MP = sym_mp(m);
+  const long m3 = (long)m * m * m;
+  const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  const int cap = (int)std::max<long>(1, std::min<long>(ctx->K, (1L << 31) / (m3 * 8)));
+  const int want = std::min(cap, c1 - c0);
+  cudaError_t e;
+  if (ctx->sym_cols < want) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;   // no allocation inside a graph capture
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return cudaSuccess;
+    if (ctx->sym_zbox) cudaFree(ctx->sym_zbox);
+    if (ctx->sym_work) cudaFree(ctx->sym_work);
+    ctx->sym_zbox = ctx->sym_work = nullptr;
+    ctx->sym_cols = 0;
+    if ((e = cudaMalloc(&ctx->sym_zbox, (size_t)want * m3 * 8)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&ctx->sym_work, (size_t)want * m3 * 8)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(ctx->sym_zbox, 0, (size_t)want * m3 * 8, s)) != cudaSuccess) return e;
+    ctx->sym_cols = want;
+  }
+  for (int a = c0; a < c1; a += cap) {
+    const int nc = std::min(cap, c1 - a);
+    const uint8_t* par = ctx->sym_par + a;
+    // (1) the octant's band values of q_c into the zero boxes (the same positions for every chunk)
+    if ((e = launch_potential_list(ctx, ctx->E + (size_t)a * ng, ng, ctx->sym_list, ctx->sym_dst, ctx->sym_nlist,
+                                   ctx->sym_zbox, m3, nc, s)) != cudaSuccess)
+      return e;
+    // (2)-(4)
+    switch (MP) {
+      case 8: e = sym_solve<8>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
+      case 16: e = sym_solve<16>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
+      case 32: e = sym_solve<32>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
+      default: e = sym_solve<64>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
+    }
+    if (e != cudaSuccess) return e;
+    // (5)
+    DPM_COUNT_LAUNCH(1);
+    sym_gather_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ng + ngin + 255) / 256, 148L * 16)), nc),
+                        256, 0, s>>>(ctx->sym_work, m3, ctx->sym_gidx, ng, ngin, ctx->gin_pos, ctx->E, a, c0, par, PgE,
+                                     B);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  *done = true;
+  return cudaSuccess;
+}
+
+void bep_sym_free(dpm_ctx* c) {
+  void* ptrs[] = {c->sym_list, c->sym_dst, c->sym_gidx, c->sym_par, c->sym_S, c->sym_lam, c->sym_zbox, c->sym_work};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}

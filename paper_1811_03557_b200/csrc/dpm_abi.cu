@@ -304,6 +304,11 @@ dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, do
   dpm_status st = ensure_work(ctx, std::min(ch, c1 - c0));
   if (st != DPM_OK) return st;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
+  {   // reflection-symmetric geometry with parity-definite columns: solved on the octant (bep_sym.cu)
+    bool done = false;
+    DPM_CUDA_TRY(ctx, bep_sym_columns(ctx, c0, c1, PgE, B, s, &done));
+    if (done) return DPM_OK;
+  }
   const bool fused = bep_fused_enabled(ctx);
   for (int a = c0; a < c1; a += ch) {
     const int nc = std::min(ch, c1 - a);

@@ -157,6 +157,17 @@ struct dpm_ctx {
   long long fac_launches = 0;
   double* bepf_zbox = nullptr;       // [zcols][n^3] boxes that are zero off the band (zero-box mode)
   int bepf_zcols = 0;
+  // BEP columns on the octant by reflection symmetry (bep_sym.cu): 0 undecided, 1 on, -1 full path
+  int sym = 0, sym_m = 0, sym_cols = 0;
+  int64_t sym_nlist = 0;
+  int64_t* sym_list = nullptr;       // [sym_nlist] band points inside the octant (flat n^3 index)
+  int32_t* sym_dst = nullptr;        // [sym_nlist] their octant (m^3) index
+  int32_t* sym_gidx = nullptr;       // [n_gamma + n_gamma_in] octant index | reflection bits << 24
+  uint8_t* sym_par = nullptr;        // [K] column parities (bit a: odd under x_a -> -x_a)
+  double* sym_S = nullptr;           // [2][MP][MP] octant sine matrices (even / odd parity)
+  double* sym_lam = nullptr;         // [2][MP] their eigenvalues
+  double* sym_zbox = nullptr;        // [sym_cols][m^3] octant boxes, zero off the band
+  double* sym_work = nullptr;        // [sym_cols][m^3]
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
@@ -324,3 +335,8 @@ cudaError_t bep_zbox(dpm_ctx* ctx, int nc, double** out, cudaStream_t s);
 bool bep_fused_enabled(const dpm_ctx* ctx);
 cudaError_t bep_columns_fused(dpm_ctx* ctx, int c0, int nc, double* PgE, double* B, cudaStream_t s);
 void bep_fused_free(dpm_ctx* c);
+cudaError_t launch_potential_list(const dpm_ctx* ctx, const double* v, int64_t ldv, const int64_t* list,
+                                  const int32_t* dst, int64_t nlist, double* q, int64_t qstride, int nrhs,
+                                  cudaStream_t s);
+cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B, cudaStream_t s, bool* done);
+void bep_sym_free(dpm_ctx* c);

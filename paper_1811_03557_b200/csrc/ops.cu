@@ -90,6 +90,19 @@ __global__ void potential_rhs_kernel(const int32_t* __restrict__ gmap, const int
   }
 }
 
+// the potential RHS at a list of band points written to q[r * qstride + dst[b]] (the octant boxes of
+// bep_sym.cu: the band points of the octant, at their octant positions)
+__global__ void potential_list_kernel(const int32_t* __restrict__ gmap, const int64_t* __restrict__ list,
+                                      const int32_t* __restrict__ dst, int64_t nlist, const double* __restrict__ v,
+                                      int64_t ldv, double* q, int64_t qstride, int nrhs, int n, double diag, double off) {
+  for (long b = blockIdx.x * (long)blockDim.x + threadIdx.x; b < nlist; b += (long)gridDim.x * blockDim.x) {
+    const BandStencil st = band_stencil(gmap, n, list[b]);
+    const long o = dst[b];
+    const int r1 = min(nrhs, (int)(blockIdx.y + 1) * POT_RC);
+    for (int r = blockIdx.y * POT_RC; r < r1; ++r) q[r * qstride + o] = band_apply(st, v + (size_t)r * ldv, diag, off);
+  }
+}
+
 // the same values compacted to the band: qb[r][b] = q_r(band[b])  (fused BEP build, bep_fused.cu)
 __global__ void potential_band_kernel(const int32_t* __restrict__ gmap, const int64_t* __restrict__ band,
                                       int64_t nband, const double* __restrict__ v, int64_t ldv, double* qb,
@@ -636,6 +649,17 @@ cudaError_t launch_potential_scatter(const dpm_ctx* ctx, const double* v, int64_
   DPM_COUNT_LAUNCH(1);
   potential_rhs_kernel<<<dim3((unsigned)((nb + TB - 1) / TB), (nrhs + POT_RC - 1) / POT_RC), TB, 0, s>>>(ctx->gmap, ctx->lists[DPM_SET_BAND], nb, v, ldv, q, nrhs, n,
                                                           diag, off);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_potential_list(const dpm_ctx* ctx, const double* v, int64_t ldv, const int64_t* list,
+                                  const int32_t* dst, int64_t nlist, double* q, int64_t qstride, int nrhs,
+                                  cudaStream_t s) {
+  if (nlist * nrhs == 0) return cudaSuccess;
+  const double diag = 1.0 / ctx->dt + 6.0 / (ctx->h * ctx->h), off = 1.0 / (ctx->h * ctx->h);
+  DPM_COUNT_LAUNCH(1);
+  potential_list_kernel<<<dim3((unsigned)((nlist + TB - 1) / TB), (nrhs + POT_RC - 1) / POT_RC), TB, 0, s>>>(
+      ctx->gmap, list, dst, nlist, v, ldv, q, qstride, nrhs, ctx->n, diag, off);
   return cudaGetLastError();
 }
 

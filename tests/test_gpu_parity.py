@@ -301,7 +301,8 @@ def _bep_oracle_columns(cfg, cols):
 @pytest.mark.parametrize("name,cols", [("cfg1", (0, 7, 49)), ("cfg2", (0, 5, 40, 97)), ("cfg3", (0, 33, 161)),
                                        ("cfg4", (0, 1, 17, 300, 577))])
 def test_bep_columns_fused_vs_oracle(api, name, cols):
-    # sparse-in / γ-out BEP columns (bep_fused.cu, the default dpm_bep_columns path): potential RHS
+    # the default dpm_bep_columns path (cfg1-cfg4: the octant path of bep_sym.cu, symmetric sets and
+    # parity-definite columns), against the oracle.  Before it: sparse-in / γ-out columns (bep_fused.cu): potential RHS
     # from the band values, x DST-I straight from them, middle passes, inverse x DST-I at γ only;
     # against the oracle's potential RHS -> AP solve -> trace, column by column, at full size for cfg4
     cfg = get_config(name)
@@ -338,6 +339,59 @@ def test_bep_columns_fused_matches_dense_path_cfg4(tmp_path):
     for f in ("1", "s"):
         assert rel(outs[f][0], outs["0"][0]) <= 1e-12, f
         assert rel(outs[f][1], outs["0"][1]) <= 1e-12, f
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_bep_columns_octant_matches_full_path(tmp_path, name):
+    # the octant path (bep_sym.cu: reflection-symmetric sets, parity-definite columns, m = n/2) required
+    # (DPM_BEP_SYM=2: an error if it does not apply) against the full-grid path (DPM_BEP_SYM=0), all K
+    # columns; separate processes (the selector is decided once per context)
+    import os, subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent('''
+        import sys, numpy as np, torch
+        from dpm_inputs import get_config
+        from paper_1811_03557_b200 import api
+        c = api.DPM.from_config(get_config(sys.argv[3]))
+        PgE, B = c.bep_columns(0, c.K)
+        np.save(sys.argv[1], PgE.cpu().numpy()); np.save(sys.argv[2], B.cpu().numpy())
+    ''')
+    outs = {}
+    for f in ("2", "0"):
+        a, b = str(tmp_path / f"pg{f}.npy"), str(tmp_path / f"b{f}.npy")
+        r = subprocess.run([sys.executable, "-c", code, a, b, name], cwd=root,
+                           env=dict(os.environ, DPM_BEP_SYM=f), capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr
+        outs[f] = (np.load(a), np.load(b))
+    assert rel(outs["2"][0], outs["0"][0]) <= 1e-12
+    assert rel(outs["2"][1], outs["0"][1]) <= 1e-12
+
+
+def test_bep_columns_asymmetric_domain_takes_full_path(tmp_path):
+    # a sphere off the box centre: the sets are not reflection-symmetric, so the octant path must not
+    # apply (DPM_BEP_SYM=2 fails) and the default path still matches the oracle
+    import dataclasses, os, subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent('''
+        import dataclasses
+        from dpm_inputs import get_config
+        from paper_1811_03557_b200 import api
+        cfg = dataclasses.replace(get_config("cfg1"), center=(0.05, 0.0, 0.0))
+        c = api.DPM.from_config(cfg)
+        c.bep_columns(0, c.K)
+    ''')
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, DPM_BEP_SYM="2"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    cfg = dataclasses.replace(get_config("cfg1"), center=(0.05, 0.0, 0.0))
+    from paper_1811_03557_b200 import api as A
+    c = A.DPM.from_config(cfg)
+    cols = (0, 7, 49)
+    ref = _bep_oracle_columns(cfg, cols)
+    for col, (pg_o, b_o) in zip(cols, ref):
+        PgE, B = c.bep_columns(col, col + 1)
+        assert rel(PgE.cpu().numpy()[0], pg_o) <= 1e-11, col
+        assert rel(B.cpu().numpy()[0], b_o) <= 1e-11, col
 
 
 def test_boundary_lsq_large_K_row_tail(api):
