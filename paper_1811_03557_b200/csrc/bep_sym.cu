@@ -42,45 +42,62 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 
 template <int MP>
 struct SymGeo {
-  static constexpr int LD = MP + 8;                 // ≡ 8 mod 16 doubles: conflict-free B fragments
+  static constexpr int LD = MP + 4;                 // ≡ 4 mod 16 doubles: conflict-free B fragments
   static constexpr int RT = MP / 8, CF = MP / 8, KS = MP / 4;
   static constexpr int RF = (RT + SYM_NW - 1) / SYM_NW;
 };
 
-// Y^T <- A X over MP x MP tiles in shared memory (X[k][col] at k*LD + col; the result D[row][col] is
-// written to Y[col*LD + row]); A[r][k] = S[k][r] (TRANS) or S[r][k], S the zero-padded MP x MP table.
+__device__ __forceinline__ void cp_async16(unsigned saddr, const double* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(unsigned saddr, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(g));
+}
+
+// A fragments of A[r][k] = S[k][r] (TRANS) or S[r][k] for this warp's row tiles, S the zero-padded
+// MP x MP table
 template <int MP>
-__device__ __forceinline__ void sym_gemm(const double* __restrict__ S, bool trans, const double* X, double* Y) {
+__device__ __forceinline__ void sym_afrag(const double* __restrict__ S, bool trans,
+                                          double (&A)[SymGeo<MP>::RF][SymGeo<MP>::KS]) {
   using G = SymGeo<MP>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int f = 0; f < G::RF; ++f) {
+    const int rt = warp * G::RF + f, row = rt * 8 + (lane >> 2);
+#pragma unroll
+    for (int ks = 0; ks < G::KS; ++ks) {
+      const int kr = ks * 4 + (lane & 3);
+      A[f][ks] = rt < G::RT ? __ldg(trans ? S + kr * MP + row : S + row * MP + kr) : 0.0;
+    }
+  }
+}
+
+// Y^T <- A X over MP x MP tiles in shared memory (X[k][col] at k*LD + col; the result D[row][col] is
+// written to Y[col*LD + row]), A in registers (sym_afrag)
+template <int MP>
+__device__ __forceinline__ void sym_gemm(const double (&A)[SymGeo<MP>::RF][SymGeo<MP>::KS], const double* X, double* Y) {
+  using G = SymGeo<MP>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp * G::RF >= G::RT) return;
   double acc[G::RF][G::CF][2];
 #pragma unroll
   for (int f = 0; f < G::RF; ++f)
 #pragma unroll
     for (int c = 0; c < G::CF; ++c) acc[f][c][0] = acc[f][c][1] = 0.0;
-#pragma unroll 4
+#pragma unroll
   for (int ks = 0; ks < G::KS; ++ks) {
     const int kr = ks * 4 + (lane & 3);
-    double a[G::RF];
-#pragma unroll
-    for (int f = 0; f < G::RF; ++f) {
-      const int rt = warp * G::RF + f, row = rt * 8 + (lane >> 2);
-      a[f] = rt < G::RT ? __ldg(trans ? S + kr * MP + row : S + row * MP + kr) : 0.0;
-    }
     double b[G::CF];
 #pragma unroll
     for (int c = 0; c < G::CF; ++c) b[c] = X[kr * G::LD + c * 8 + (lane >> 2)];
 #pragma unroll
     for (int f = 0; f < G::RF; ++f)
 #pragma unroll
-      for (int c = 0; c < G::CF; ++c)
-        if (warp * G::RF + f < G::RT) dmma884(acc[f][c], a[f], b[c]);
+      for (int c = 0; c < G::CF; ++c) dmma884(acc[f][c], A[f][ks], b[c]);
   }
 #pragma unroll
   for (int f = 0; f < G::RF; ++f) {
-    const int rt = warp * G::RF + f;
-    if (rt >= G::RT) continue;
-    const int row = rt * 8 + (lane >> 2);
+    const int row = (warp * G::RF + f) * 8 + (lane >> 2);
 #pragma unroll
     for (int c = 0; c < G::CF; ++c) {
       const int col = c * 8 + 2 * (lane & 3);
@@ -91,31 +108,60 @@ __device__ __forceinline__ void sym_gemm(const double* __restrict__ S, bool tran
 }
 
 // (2) / (4): per x-plane (column cc, plane i) of the m^3 octant boxes: forward Q = S_y^T P S_z, inverse
-// P = S_y Q S_z^T (S_y, S_z the tables of the column's y / z parities, par bits 1 / 2).
+// P = S_y Q S_z^T (S_y, S_z the tables of the column's y / z parities, par bits 1 / 2).  Persistent CTAs over
+// contiguous ranges of planes (a column's 64 planes share their tables: the A fragments stay in registers
+// and are reloaded when the parity class changes); the next plane streams in by cp.async under the GEMMs.
 template <int MP, bool FWD>
-__global__ void __launch_bounds__(SYM_NT) sym_yz_kernel(const double* in, double* out, int ncols, int m,
-                                                        const uint8_t* __restrict__ par,
-                                                        const double* __restrict__ S) {
+__global__ void __launch_bounds__(SYM_NT, 2) sym_yz_kernel(const double* in, double* out, int ncols, int m,
+                                                           const uint8_t* __restrict__ par,
+                                                           const double* __restrict__ S) {
   using G = SymGeo<MP>;
   extern __shared__ __align__(16) double sh[];
-  double* X = sh;
-  double* Y = sh + MP * G::LD;
-  for (int e = threadIdx.x; e < MP * G::LD; e += SYM_NT) X[e] = 0.0;   // padding stays zero (see below)
+  double* Y = sh + 2 * MP * G::LD;
+  for (int e = threadIdx.x; e < 3 * MP * G::LD; e += SYM_NT) sh[e] = 0.0;   // padding stays zero
   __syncthreads();
   const long m2 = (long)m * m, nplanes = (long)ncols * m;
-  for (long p = blockIdx.x; p < nplanes; p += gridDim.x) {
-    const int cc = (int)(p / m);
-    const int pr = par[cc];
+  const long per = (nplanes + gridDim.x - 1) / gridDim.x;
+  const long p0 = blockIdx.x * per, p1 = min(nplanes, p0 + per);
+  if (p0 >= p1) return;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(sh);
+  const bool v2 = (m & 1) == 0;
+  auto issue = [&](long p, int buf) {
     const double* src = in + p * m2;
-    for (int e = threadIdx.x; e < m * MP; e += SYM_NT) {
-      const int j = e / MP, k = e % MP;
-      if (k < m) X[j * G::LD + k] = src[j * m + k];
+    const unsigned sb = sbase + 8u * (unsigned)(buf * MP * G::LD);
+    if (v2) {
+      const int h = m / 2;
+      for (int e = threadIdx.x; e < m * h; e += SYM_NT) {
+        const int j = e / h, k = 2 * (e - j * h);
+        cp_async16(sb + 8u * (unsigned)(j * G::LD + k), src + j * m + k);
+      }
+    } else {
+      for (int e = threadIdx.x; e < m * m; e += SYM_NT) {
+        const int j = e / m, k = e - j * m;
+        cp_async8(sb + 8u * (unsigned)(j * G::LD + k), src + e);
+      }
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  issue(p0, 0);
+  double A1[G::RF][G::KS], A2[G::RF][G::KS];
+  int cls = -1;
+  for (long p = p0; p < p1; ++p) {
+    const int buf = (int)((p - p0) & 1);
+    double* X = sh + buf * MP * G::LD;
+    if (p + 1 < p1) issue(p + 1, buf ^ 1);
+    else asm volatile("cp.async.commit_group;\n" ::);
+    const int pr = par[p / m] & 6;
+    if (pr != cls) {
+      sym_afrag<MP>(S + ((pr >> 1) & 1) * MP * MP, FWD, A1);
+      sym_afrag<MP>(S + ((pr >> 2) & 1) * MP * MP, FWD, A2);
+      cls = pr;
+    }
+    asm volatile("cp.async.wait_group 1;\n" ::);
     __syncthreads();
-    // rows / columns >= m: the padded table rows and columns are zero, so the padding of X stays zero
-    sym_gemm<MP>(S + ((pr >> 1) & 1) * MP * MP, FWD, X, Y);
+    sym_gemm<MP>(A1, X, Y);
     __syncthreads();
-    sym_gemm<MP>(S + ((pr >> 2) & 1) * MP * MP, FWD, Y, X);
+    sym_gemm<MP>(A2, Y, X);
     __syncthreads();
     double* dst = out + p * m2;
     for (int e = threadIdx.x; e < m * MP; e += SYM_NT) {
@@ -338,13 +384,13 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
 template <int MP>
 cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const uint8_t* par, cudaStream_t s) {
   const int m = ctx->sym_m, n = ctx->n;
-  constexpr size_t smem_yz = 2 * (size_t)MP * SymGeo<MP>::LD * sizeof(double);
+  constexpr size_t smem_yz = 3 * (size_t)MP * SymGeo<MP>::LD * sizeof(double);
   constexpr size_t smem_x = (size_t)MP * SYM_NT * sizeof(double);
   cudaFuncSetAttribute(sym_yz_kernel<MP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
   cudaFuncSetAttribute(sym_yz_kernel<MP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
   cudaFuncSetAttribute(sym_x_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x);
   const long planes = (long)nc * m;
-  const int grid_yz = (int)std::min<long>(planes, 148L * 3);
+  const int grid_yz = (int)std::min<long>(planes, 148L * 2);
   const long pencils = (long)nc * m * m;
   const double h2i = 1.0 / (ctx->h * ctx->h), scale = (4.0 / (n + 1)) * (4.0 / (n + 1));
   DPM_COUNT_LAUNCH(3);

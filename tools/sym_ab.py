@@ -14,7 +14,7 @@ from paper_1811_03557_b200 import api  # noqa: E402
 
 out = sys.argv[1] if len(sys.argv) > 1 else None
 res = {}
-for name in ("cfg1", "cfg2", "cfg3", "cfg4"):
+for name in os.environ.get("SYM_CFGS", "cfg1,cfg2,cfg3,cfg4").split(","):
     ctx = api.DPM.from_config(get_config(name))
     K = ctx.K
     PgE, B = ctx.bep_columns(0, K)
