@@ -172,43 +172,63 @@ __global__ void __launch_bounds__(SYM_NT, 2) sym_yz_kernel(const double* in, dou
   }
 }
 
-// (3): per spectral pencil (column cc, w = b*m + c): (1/dt + λ_b + λ_c + T_x,sx) v = q along x, then
-// v *= scale.  Thomas with the elimination factors in shared memory and the right-hand side in registers.
-template <int MP>
-__global__ void __launch_bounds__(SYM_NT) sym_x_kernel(double* u, int ncols, int m, const uint8_t* __restrict__ par,
-                                                       const double* __restrict__ lamr, double inv_dt, double h2i,
-                                                       double scale) {
-  extern __shared__ __align__(16) double ef[];   // [MP][SYM_NT]
+// (3a): LU factors of the x tridiagonal of every spectral pencil (w = b*m + c) of every y/z parity class q:
+// den_i = d - h2i e_{i-1}, r_i = 1/den_i, e_i = h2i r_i (i < m-1), and the last row's r for both x parities
+// (u_m = +u_{m-1}: d - h2i; u_m = -u_{m-1}: d + h2i).  They depend on Δt and the geometry only, not on the
+// column: built once per Δt, read by every column of the class.
+__global__ void sym_lu_kernel(int m, int MP, const double* __restrict__ lamr, double inv_dt, double h2i, double* R,
+                              double* Ef, double* Rl) {
+  const long m2 = (long)m * m;
+  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= 4 * m2) return;
+  const int q = (int)(id / m2), w = (int)(id - q * m2), b = w / m, c = w - b * m;
+  const double d = ((inv_dt + lamr[(q & 1) * MP + b]) + lamr[((q >> 1) & 1) * MP + c]) + 2.0 * h2i;
+  double e = 0.0;
+  for (int i = 0; i < m - 1; ++i) {
+    const double r = 1.0 / (d - h2i * e);
+    e = h2i * r;
+    R[((long)q * m + i) * m2 + w] = r;
+    Ef[((long)q * m + i) * m2 + w] = e;
+  }
+  Rl[((long)q * 2 + 0) * m2 + w] = 1.0 / ((d - h2i) - h2i * e);
+  Rl[((long)q * 2 + 1) * m2 + w] = 1.0 / ((d + h2i) - h2i * e);
+}
+
+// (3b): per spectral pencil (column cc, w = b*m + c): (1/dt + λ_b + λ_c + T_x,sx) v = q along x with the
+// factors of (3a), then v *= scale.  The right-hand side in registers, the factors streamed (L2-resident).
+template <int MP, bool EXACT>
+__global__ void __launch_bounds__(SYM_NT) sym_x_kernel(double* u, int ncols, int m_rt, const uint8_t* __restrict__ par,
+                                                       const double* __restrict__ R, const double* __restrict__ Ef,
+                                                       const double* __restrict__ Rl, double h2i, double scale) {
+  const int m = EXACT ? MP : m_rt;
   const long m2 = (long)m * m, total = (long)ncols * m2;
   const long id = (long)blockIdx.x * SYM_NT + threadIdx.x;
   if (id >= total) return;
   const int cc = (int)(id / m2);
   const int w = (int)(id - (long)cc * m2);
-  const int b = w / m, c = w - b * m;
-  const int pr = par[cc];
-  const double d = ((inv_dt + lamr[((pr >> 1) & 1) * MP + b]) + lamr[((pr >> 2) & 1) * MP + c]) + 2.0 * h2i;
-  const double dlast = (pr & 1) ? d + h2i : d - h2i;   // u_m = -u_{m-1} (odd) / +u_{m-1} (even)
+  const int pr = par[cc], q = (pr >> 1) & 3;
   double* col = u + (long)cc * m2 * m + w;
+  const double* Rq = R + (long)q * m * m2 + w;
+  const double* Eq = Ef + (long)q * m * m2 + w;
   double g[MP];
 #pragma unroll
   for (int i = 0; i < MP; ++i) g[i] = i < m ? col[(long)i * m2] : 0.0;
-  double eprev = 0.0, gprev = 0.0;
+  const double rl = __ldg(Rl + ((long)q * 2 + (pr & 1)) * m2 + w);
+  double gprev = 0.0, next = 0.0;
 #pragma unroll
   for (int i = 0; i < MP; ++i) {
-    if (i < m) {
-      const double den = (i == m - 1 ? dlast : d) - h2i * eprev;
-      const double r = 1.0 / den;
-      eprev = h2i * r;
-      gprev = (g[i] + h2i * gprev) * r;
+    if (i < m - 1) {
+      gprev = (g[i] + h2i * gprev) * __ldg(Rq + (long)i * m2);
       g[i] = gprev;
-      ef[i * SYM_NT + threadIdx.x] = eprev;
+    } else if (i == m - 1) {
+      next = (g[i] + h2i * gprev) * rl;
+      col[(long)i * m2] = next * scale;
     }
   }
-  double next = 0.0;
 #pragma unroll
-  for (int i = MP - 1; i >= 0; --i) {
-    if (i < m) {
-      next = (i == m - 1) ? g[i] : g[i] + ef[i * SYM_NT + threadIdx.x] * next;
+  for (int i = MP - 2; i >= 0; --i) {
+    if (i < m - 1) {
+      next = g[i] + __ldg(Eq + (long)i * m2) * next;
       col[(long)i * m2] = next * scale;
     }
   }
@@ -375,6 +395,11 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
   if ((e = upload(&ctx->sym_par, par)) != cudaSuccess) return e;
   if ((e = upload(&ctx->sym_S, S)) != cudaSuccess) return e;
   if ((e = upload(&ctx->sym_lam, lam)) != cudaSuccess) return e;
+  {   // LU factors of the x tridiagonals (sym_lu_kernel): R, E [4][m][m^2] and the last rows [4][2][m^2]
+    const size_t m2 = (size_t)m * m;
+    if ((e = cudaMalloc(&ctx->sym_R, (8 * m2 * m + 8 * m2) * sizeof(double))) != cudaSuccess) return e;
+    ctx->sym_lu_dt = 0.0;
+  }
   ctx->sym_nlist = (int64_t)olist.size();
   ctx->sym_m = m;
   ctx->sym = 1;
@@ -384,19 +409,28 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
 template <int MP>
 cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const uint8_t* par, cudaStream_t s) {
   const int m = ctx->sym_m, n = ctx->n;
+  const long m2 = (long)m * m;
   constexpr size_t smem_yz = 3 * (size_t)MP * SymGeo<MP>::LD * sizeof(double);
-  constexpr size_t smem_x = (size_t)MP * SYM_NT * sizeof(double);
   cudaFuncSetAttribute(sym_yz_kernel<MP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
   cudaFuncSetAttribute(sym_yz_kernel<MP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
-  cudaFuncSetAttribute(sym_x_kernel<MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x);
   const long planes = (long)nc * m;
   const int grid_yz = (int)std::min<long>(planes, 148L * 2);
-  const long pencils = (long)nc * m * m;
+  const long pencils = (long)nc * m2;
   const double h2i = 1.0 / (ctx->h * ctx->h), scale = (4.0 / (n + 1)) * (4.0 / (n + 1));
+  if (ctx->sym_lu_dt != ctx->dt) {   // (3a) once per Δt
+    DPM_COUNT_LAUNCH(1);
+    sym_lu_kernel<<<(unsigned)((4 * m2 + 127) / 128), 128, 0, s>>>(m, MP, ctx->sym_lam, 1.0 / ctx->dt, h2i, ctx->sym_R,
+                                                                   ctx->sym_R + 4 * m2 * m, ctx->sym_R + 8 * m2 * m);
+    ctx->sym_lu_dt = ctx->dt;
+  }
+  const double* R = ctx->sym_R;
   DPM_COUNT_LAUNCH(3);
   sym_yz_kernel<MP, true><<<grid_yz, SYM_NT, smem_yz, s>>>(q, u, nc, m, par, ctx->sym_S);
-  sym_x_kernel<MP><<<(unsigned)((pencils + SYM_NT - 1) / SYM_NT), SYM_NT, smem_x, s>>>(u, nc, m, par, ctx->sym_lam,
-                                                                                    1.0 / ctx->dt, h2i, scale);
+  const unsigned gx = (unsigned)((pencils + SYM_NT - 1) / SYM_NT);
+  if (m == MP)
+    sym_x_kernel<MP, true><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale);
+  else
+    sym_x_kernel<MP, false><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale);
   sym_yz_kernel<MP, false><<<grid_yz, SYM_NT, smem_yz, s>>>(u, u, nc, m, par, ctx->sym_S);
   return cudaGetLastError();
 }
@@ -462,7 +496,7 @@ cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B
 }
 
 void bep_sym_free(dpm_ctx* c) {
-  void* ptrs[] = {c->sym_list, c->sym_dst, c->sym_gidx, c->sym_par, c->sym_S, c->sym_lam, c->sym_zbox, c->sym_work};
+  void* ptrs[] = {c->sym_list, c->sym_dst, c->sym_gidx, c->sym_par, c->sym_S, c->sym_lam, c->sym_zbox, c->sym_work, c->sym_R};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }

@@ -168,6 +168,8 @@ struct dpm_ctx {
   double* sym_lam = nullptr;         // [2][MP] their eigenvalues
   double* sym_zbox = nullptr;        // [sym_cols][m^3] octant boxes, zero off the band
   double* sym_work = nullptr;        // [sym_cols][m^3]
+  double* sym_R = nullptr;           // x-tridiagonal LU factors (sym_lu_kernel), built at Δt = sym_lu_dt
+  double sym_lu_dt = 0.0;
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
