@@ -284,6 +284,37 @@ __global__ void sym_parity_kernel(const double* __restrict__ E, long ng, const i
   if (threadIdx.x < 7) out[(long)c * 7 + threadIdx.x] = red[threadIdx.x][0];
 }
 
+// does every column of a BEP matrix B (|γ_in| x K, column-major) have the parity recorded for it?  flag = 1
+// if some column is off by more than 1e-10 (relative, 2-norm) from it under some reflection
+__global__ void sym_check_kernel(const double* __restrict__ B, long m, const int32_t* __restrict__ mir,
+                                 const uint8_t* __restrict__ par, int* flag) {
+  __shared__ double red[4][256];
+  const int c = blockIdx.x, pr = par[c];
+  const double* Bc = B + (long)c * m;
+  double s[4] = {0, 0, 0, 0};
+  for (long r = threadIdx.x; r < m; r += blockDim.x) {
+    const double v = Bc[r];
+    s[0] += v * v;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double w = Bc[mir[a * m + r]], d = ((pr >> a) & 1) ? v + w : v - w;
+      s[1 + a] += d * d;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = s[q];
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int a = 0; a < 3; ++a)
+      if (!(red[1 + a][0] <= 1e-20 * red[0][0])) atomicExch(flag, 1);
+}
+
 template <typename T>
 cudaError_t upload(T** dst, const std::vector<T>& v) {
   cudaError_t e = cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T));
@@ -400,6 +431,21 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
     if ((e = cudaMalloc(&ctx->sym_R, (8 * m2 * m + 8 * m2) * sizeof(double))) != cudaSuccess) return e;
     ctx->sym_lu_dt = 0.0;
   }
+  {   // columns grouped by parity class (stable): the block-diagonal BEP factorisation (lsq_factor)
+    std::vector<int32_t> perm;
+    for (int cl = 0; cl < 8; ++cl) {
+      ctx->sym_off[cl] = (int)perm.size();
+      for (int c = 0; c < K; ++c)
+        if (par[c] == cl) perm.push_back(c);
+    }
+    ctx->sym_off[8] = K;
+    std::vector<int32_t> ginpos(n3, -1), mirin(3 * ngin);
+    for (long r = 0; r < ngin; ++r) ginpos[L[3][r]] = (int32_t)r;
+    for (int a = 0; a < 3; ++a)
+      for (long r = 0; r < ngin; ++r) mirin[a * ngin + r] = ginpos[mirror(L[3][r], a)];
+    if ((e = upload(&ctx->sym_perm, perm)) != cudaSuccess) return e;
+    if ((e = upload(&ctx->sym_mirin, mirin)) != cudaSuccess) return e;
+  }
   ctx->sym_nlist = (int64_t)olist.size();
   ctx->sym_m = m;
   ctx->sym = 1;
@@ -496,7 +542,30 @@ cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B
 }
 
 void bep_sym_free(dpm_ctx* c) {
-  void* ptrs[] = {c->sym_list, c->sym_dst, c->sym_gidx, c->sym_par, c->sym_S, c->sym_lam, c->sym_zbox, c->sym_work, c->sym_R};
+  void* ptrs[] = {c->sym_list, c->sym_dst, c->sym_gidx, c->sym_par, c->sym_S, c->sym_lam, c->sym_zbox, c->sym_work, c->sym_R, c->sym_perm, c->sym_mirin, c->sym_Bp, c->sym_tmp, c->sym_dg, c->sym_flag};
+  for (cudaStream_t st : c->sym_streams)
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : c->sym_ev)
+    if (ev) cudaEventDestroy(ev);
   for (void* p : ptrs)
     if (p) cudaFree(p);
+}
+
+// The block-diagonal factorisation of B applies: octant path on, and every column of B has its class parity
+// (one check kernel and a host sync; DPM_BEP_SYM_FACTOR=0 disables).
+bool bep_sym_blocks(dpm_ctx* ctx, const double* B, cudaStream_t s) {
+  static const bool on = [] {
+    const char* v = getenv("DPM_BEP_SYM_FACTOR");
+    return !(v && atoi(v) == 0);
+  }();
+  if (!on || ctx->sym != 1 || !ctx->sym_perm) return false;
+  if (!ctx->sym_flag && cudaMalloc(&ctx->sym_flag, sizeof(int)) != cudaSuccess) return false;
+  const long m = ctx->counts[DPM_SET_GAMMA_IN];
+  int h = 1;
+  if (cudaMemsetAsync(ctx->sym_flag, 0, sizeof(int), s) != cudaSuccess) return false;
+  DPM_COUNT_LAUNCH(1);
+  sym_check_kernel<<<ctx->K, 256, 0, s>>>(B, m, ctx->sym_mirin, ctx->sym_par, ctx->sym_flag);
+  if (cudaMemcpyAsync(&h, ctx->sym_flag, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess) return false;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+  return h == 0;
 }

@@ -154,6 +154,7 @@ struct dpm_ctx {
   const double* fac_B = nullptr;
   int fac_K = 0;
   int64_t fac_m = 0;
+  int fac_blocks = 0;                 // the captured factorisation is the block-diagonal one (bep_sym.cu)
   long long fac_launches = 0;
   double* bepf_zbox = nullptr;       // [zcols][n^3] boxes that are zero off the band (zero-box mode)
   int bepf_zcols = 0;
@@ -170,6 +171,15 @@ struct dpm_ctx {
   double* sym_work = nullptr;        // [sym_cols][m^3]
   double* sym_R = nullptr;           // x-tridiagonal LU factors (sym_lu_kernel), built at Δt = sym_lu_dt
   double sym_lu_dt = 0.0;
+  int sym_off[9] = {0};              // parity-class column ranges in the class order sym_perm
+  int32_t* sym_perm = nullptr;       // [K] class-ordered position -> column
+  int32_t* sym_mirin = nullptr;      // [3][n_gamma_in] γ_in position of the mirror point
+  double* sym_Bp = nullptr;          // [K][n_gamma_in] class-ordered B, then the operator blocks
+  double* sym_tmp = nullptr;         // [K][n_gamma_in] CholeskyQR2 ping-pong
+  double* sym_dg = nullptr;          // [K] |diag R| (class order)
+  int* sym_flag = nullptr;
+  cudaStream_t sym_streams[8] = {};  // one capture branch per parity class
+  cudaEvent_t sym_ev[9] = {};
   // host-buffer solve pipeline (dpm_aux_solve_batch_host)
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   cudaEvent_t pipe_ev[9] = {};   // host pipeline: up / solved / down per ring buffer (3)
@@ -342,3 +352,4 @@ cudaError_t launch_potential_list(const dpm_ctx* ctx, const double* v, int64_t l
                                   cudaStream_t s);
 cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B, cudaStream_t s, bool* done);
 void bep_sym_free(dpm_ctx* c);
+bool bep_sym_blocks(dpm_ctx* ctx, const double* B, cudaStream_t s);

@@ -387,6 +387,49 @@ template <bool TRANS>
 cudaError_t launch_gemm_tri(const double* A, int64_t m, int K, const double* T, const double* scale, double* C,
                             cudaStream_t s);
 
+// ---- block-diagonal factorisation (octant path, bep_sym.cu): columns of different reflection parities are
+// exactly orthogonal over the symmetric γ_in, so AᵀA is block-diagonal by parity class and CholeskyQR2,
+// R^{-1}, M = D R^{-1} Q^T and R D^{-1} factor class by class (the 8 blocks ~1/8 of the Gram flops, ~1/64 of
+// the Cholesky / R^{-1} work).  The classes run as parallel branches of the captured factorisation graph; M,
+// R D^{-1} and the column scales are scattered back to the original column order, so lsq_apply /
+// lsq_residual / dpm_boundary_lsq are unchanged.
+__global__ void permute_cols_kernel(const double* __restrict__ B, int64_t m, const int32_t* __restrict__ perm,
+                                    double* __restrict__ Bp) {
+  const int j = blockIdx.y;
+  const double* src = B + (size_t)perm[j] * m;
+  double* dst = Bp + (size_t)j * m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void scatter_rows_kernel(const double* __restrict__ Mp, int64_t m, const int32_t* __restrict__ perm,
+                                    double* __restrict__ M) {
+  const int j = blockIdx.y;
+  const double* src = Mp + (size_t)j * m;
+  double* dst = M + (size_t)perm[j] * m;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void scatter_block_kernel(const double* __restrict__ RDp, const double* __restrict__ Rp,
+                                     const double* __restrict__ cs, const int32_t* __restrict__ perm, int Kp, int K,
+                                     double* RD, double* colscale, double* dg) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= Kp * Kp) return;
+  const int a = e / Kp, b = e - a * Kp;
+  RD[(size_t)perm[a] * K + perm[b]] = RDp[e];
+  if (a == b) {
+    colscale[perm[a]] = cs[a];
+    dg[a] = fabs(Rp[(size_t)a * Kp + a]);
+  }
+}
+__global__ void vec_ratio_kernel(const double* d, int K, double* out) {
+  double mx = 0, mn = INFINITY;
+  for (int i = 0; i < K; ++i) {
+    mx = fmax(mx, d[i]);
+    mn = fmin(mn, d[i]);
+  }
+  *out = mx / mn;
+}
+
 dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
   const int K = ctx->K;
   const int64_t m = ctx->counts[DPM_SET_GAMMA_IN];
@@ -412,7 +455,61 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
     const char* v = getenv("DPM_FACTOR_GRAPH");
     return !(v && atoi(v) == 0);
   }();
+  const bool blocks = bep_sym_blocks(ctx, B, s);
+  if (blocks) {
+    if (!ctx->sym_Bp) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->sym_Bp, (size_t)m * K * sizeof(double)));
+    if (!ctx->sym_tmp) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->sym_tmp, (size_t)m * K * sizeof(double)));
+    if (!ctx->sym_dg) DPM_CUDA_TRY(ctx, cudaMalloc(&ctx->sym_dg, (size_t)2 * K * sizeof(double)));
+    for (int p = 0; p < 8; ++p)
+      if (!ctx->sym_streams[p]) DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->sym_streams[p], cudaStreamNonBlocking));
+    for (int p = 0; p < 9; ++p)
+      if (!ctx->sym_ev[p]) DPM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->sym_ev[p], cudaEventDisableTiming));
+  }
+  auto enqueue_blocks = [&](cudaStream_t q) -> dpm_status {
+    double* cs = ctx->sym_dg;      // column scales, class order
+    double* dg = ctx->sym_dg + K;  // |diag R|, class order
+    DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), q));
+    DPM_CUDA_TRY(ctx, cudaMemsetAsync(ctx->RDinv, 0, (size_t)K * K * sizeof(double), q));
+    const unsigned gm = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + TB - 1) / TB, 64));
+    DPM_COUNT_LAUNCH(1);
+    permute_cols_kernel<<<dim3(gm, K), TB, 0, q>>>(B, m, ctx->sym_perm, ctx->sym_Bp);
+    DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->sym_ev[8], q));
+    size_t roff = 0;
+    for (int p = 0; p < 8; ++p) {
+      const int o = ctx->sym_off[p], Kp = ctx->sym_off[p + 1] - o;
+      if (Kp == 0) continue;
+      cudaStream_t st = ctx->sym_streams[p];
+      DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(st, ctx->sym_ev[8], 0));
+      double* Bpp = ctx->sym_Bp + (size_t)o * m;
+      double* Qp = ctx->Q + (size_t)o * m;
+      double* Tp = ctx->sym_tmp + (size_t)o * m;
+      double *R1p = R1 + roff, *R2p = R2 + roff, *Riwp = Riw + roff, *Rp = ctx->R + roff;
+      roff += (size_t)Kp * Kp;
+      DPM_COUNT_LAUNCH(2);
+      colnorm_kernel<<<Kp, TB, 0, st>>>(Bpp, m, cs + o);
+      scale_cols_kernel<<<dim3(gm, Kp), TB, 0, st>>>(Bpp, m, Kp, cs + o, Qp);
+      dpm_status r;
+      if ((r = chol_qr_pass(ctx, Qp, m, Kp, R1p, Riwp, Tp, dfail, st)) != DPM_OK) return r;
+      if ((r = chol_qr_pass(ctx, Tp, m, Kp, R2p, Riwp, Qp, dfail, st)) != DPM_OK) return r;
+      DPM_COUNT_LAUNCH(1);
+      trmm_kernel<<<(Kp * Kp + 255) / 256, 256, 0, st>>>(R2p, R1p, Rp, Kp);
+      DPM_CUDA_TRY(ctx, lsq_rinv(Rp, Kp, R1p, st));
+      DPM_CUDA_TRY(ctx, launch_gemm_tri<true>(Qp, m, Kp, R1p, cs + o, Bpp, st));   // M_p rows into Bpp
+      DPM_COUNT_LAUNCH(3);
+      rdinv_kernel<<<(unsigned)(((size_t)Kp * Kp + 255) / 256), 256, 0, st>>>(Rp, cs + o, Kp, R2p);
+      scatter_rows_kernel<<<dim3(gm, Kp), TB, 0, st>>>(Bpp, m, ctx->sym_perm + o, ctx->Mlsq);
+      scatter_block_kernel<<<(Kp * Kp + 255) / 256, 256, 0, st>>>(R2p, Rp, cs + o, ctx->sym_perm + o, Kp, K,
+                                                                  ctx->RDinv, ctx->colscale, dg + o);
+      DPM_CUDA_TRY(ctx, cudaEventRecord(ctx->sym_ev[p], st));
+      DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(q, ctx->sym_ev[p], 0));
+    }
+    DPM_COUNT_LAUNCH(1);
+    vec_ratio_kernel<<<1, 1, 0, q>>>(dg, K, dcond);
+    DPM_CUDA_TRY(ctx, cudaGetLastError());
+    return DPM_OK;
+  };
   auto enqueue = [&](cudaStream_t q) -> dpm_status {
+    if (blocks) return enqueue_blocks(q);
     DPM_CUDA_TRY(ctx, cudaMemsetAsync(dfail, 0, sizeof(int), q));
     DPM_COUNT_LAUNCH(1);
     colnorm_kernel<<<K, TB, 0, q>>>(B, m, ctx->colscale);
@@ -441,7 +538,7 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
     dpm_status st = enqueue(s);
     if (st != DPM_OK) return st;
   } else {
-    if (!ctx->fac_exec || ctx->fac_B != B || ctx->fac_K != K || ctx->fac_m != m) {
+    if (!ctx->fac_exec || ctx->fac_B != B || ctx->fac_K != K || ctx->fac_m != m || ctx->fac_blocks != (int)blocks) {
       if (ctx->fac_exec) cudaGraphExecDestroy(ctx->fac_exec);
       ctx->fac_exec = nullptr;
       if (!ctx->fac_stream) DPM_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->fac_stream, cudaStreamNonBlocking));
@@ -463,6 +560,7 @@ dpm_status lsq_factor(dpm_ctx* ctx, const double* B, cudaStream_t s) {
       ctx->fac_B = B;
       ctx->fac_K = K;
       ctx->fac_m = m;
+      ctx->fac_blocks = (int)blocks;
     }
     DPM_CUDA_TRY(ctx, cudaGraphLaunch(ctx->fac_exec, s));
     g_dpm_launches.fetch_add(ctx->fac_launches);

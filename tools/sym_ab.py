@@ -27,7 +27,22 @@ for name in os.environ.get("SYM_CFGS", "cfg1,cfg2,cfg3,cfg4").split(","):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = statistics.median(ts)
-    res[name] = {"K": K, "columns_ms": ms, "columns_per_s": K / ms * 1e3}
+    ctx.build_projection(want_outputs=False)
+    tb = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.build_projection(want_outputs=False)
+        e1.record()
+        e1.synchronize()
+        tb.append(e0.elapsed_time(e1))
+    # one boundary LSQ on a fixed random right-hand side (coefficients compared across modes)
+    g = torch.from_numpy(np.random.default_rng(7).uniform(-1, 1, (1, ctx.info["n_gamma_in"]))).cuda()
+    coef, ug = ctx.boundary_lsq(g)
+    res[name] = {"K": K, "columns_ms": ms, "columns_per_s": K / ms * 1e3, "build_ms": statistics.median(tb)}
+    if out:
+        np.save(f"{out}_{name}_coef.npy", coef.cpu().numpy())
+        np.save(f"{out}_{name}_ug.npy", ug.cpu().numpy())
     if out:
         np.save(f"{out}_{name}_pg.npy", PgE.cpu().numpy())
         np.save(f"{out}_{name}_b.npy", B.cpu().numpy())
