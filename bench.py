@@ -296,12 +296,15 @@ def bench_cfg1(api, torch, reps=20):
 
 def bench_bep(api, torch, reps=3):
     """NEXT-1: the Step-4b rebuild at the cfg4 geometry (K = 578 BEP columns, N=128):
-    dpm_bep_columns over all K (sparse-in / gamma-out fused path unless DPM_BEP_FUSED=0) and the
-    whole dpm_build_projection (columns + CholeskyQR2 factorisation); median of reps, CUDA events."""
+    dpm_bep_columns over all K (the octant path of bep_sym.cu: reflection-symmetric sets, parity-definite
+    columns, DPM_BEP_SYM=0 for the full-grid path) and the whole dpm_build_projection (columns + CholeskyQR2
+    factorisation, block-diagonal by parity class on the octant path); median of reps, CUDA events."""
     cfg = get_config("cfg4")
     ctx = api.DPM.from_config(cfg)
     K = ctx.K
-    res = {"K": K, "fused": os.environ.get("DPM_BEP_FUSED") != "0"}
+    res = {"K": K, "path": "full grid" if os.environ.get("DPM_BEP_SYM") == "0" else
+           "octant (reflection symmetry, 8 parity classes)",
+           "fused": os.environ.get("DPM_BEP_FUSED") != "0"}
     for name, fn in (("columns_ms", lambda: ctx.bep_columns(0, K)),
                      ("rebuild_ms", lambda: ctx.build_projection(False))):
         fn()
