@@ -436,6 +436,9 @@ def bench_dd(api, torch, world, rank, steps=None, reps=5):
     out = {"octants": 8, "octants_per_rank": per, "n": cfg.n, "K": octs[0].K, "rows_per_octant": octs[0].n_rows,
            "steps": steps, "reps": reps, "total_s": med("total_s"), "builds": runs[-1]["builds"],
            "build_s_incl_their_steps": med("build_s"), "steps_per_s_excl_builds": med("steps_per_s"),
+           "steps_per_s_incl_builds": steps / med("total_s"),
+           "builds_shared": "octant 0's block by K AP solves, the others by column signs (dpm_dd_bep_block_from)"
+           if os.environ.get("DPM_DD_SHARED") != "0" and per > 1 else "every octant by K AP solves",
            "dt_first": logs[0]["dt"], "dt_last": logs[-1]["dt"], "t_end": logs[-1]["t"],
            "mass_after_step1": logs[0]["mass"], "mass_end": logs[-1]["mass"], "rho_max_end": logs[-1]["rho_max"],
            "note": "non-physical config (SURVEY §0 item 6: IC spike at the 8-octant corner); matches probe P12"}

@@ -283,6 +283,14 @@ dpm_status dpm_dd_copy_assign(const dpm_ctx* ctx, uint8_t* host_bits);
 /* K AP solves of the potentials of the effective density columns at the ctx's dt, then the
    BEP block B_s (n_rows x K column-major, kept in ctx; copied to B_out if non-NULL). */
 dpm_status dpm_dd_bep_block(dpm_ctx* ctx, double* B_out, void* stream);
+/* Config 5 (R24): the BEP block of octant ctx from the already built block of another octant `ref` of the
+   same canonical geometry on the same device, B_s = B_ref diag(S) with S the column signs of ctx's extension
+   relative to ref's (E_s = E_ref diag(S): every cap SH and plane Legendre function is even or odd under each
+   reflection, and the K AP solves of P:241-253 are linear in their right-hand sides), instead of K AP solves.
+   ref must hold its block at ctx's dt (dpm_dd_bep_block).  DPM_ERR_INVALID if the contexts are not octants of
+   one geometry on one device or the extensions are not sign reflections; DPM_ERR_STATE if ref has no block at
+   this dt.  Asynchronous on stream (the first call per pair synchronizes it once to check the signs). */
+dpm_status dpm_dd_bep_block_from(dpm_ctx* ctx, dpm_ctx* ref, double* B_out, void* stream);
 /* nrm2[c] = Σ_rows B_s[:, c]^2 (K). */
 dpm_status dpm_dd_colnorm2(dpm_ctx* ctx, double* nrm2, void* stream);
 /* pass 1: D = 1/sqrt(nrm2_sum) (synchronizes), Q1 = B_s D, G = Q1^T Q1;  pass 2: G = Q1^T Q1

@@ -93,6 +93,7 @@ _sig = {
     "dpm_dd_info": ([P, C.POINTER(C.c_int64), C.POINTER(C.c_int32)], C.c_int),
     "dpm_dd_copy_assign": ([P, C.POINTER(C.c_uint8)], C.c_int),
     "dpm_dd_bep_block": ([P, P, P], C.c_int),
+    "dpm_dd_bep_block_from": ([P, P, P, P], C.c_int),
     "dpm_dd_colnorm2": ([P, P, P], C.c_int),
     "dpm_dd_gram": ([P, C.c_int32, P, P, P], C.c_int),
     "dpm_dd_chol": ([P, C.c_int32, P, P], C.c_int),

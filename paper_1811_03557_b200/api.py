@@ -245,6 +245,12 @@ class Octant(DPM):
         self._chk(L.lib.dpm_dd_bep_block(self._h, _ptr(B), _stream(stream)))
         return B
 
+    def bep_block_from(self, ref, want=False, stream=None):
+        """B_s = B_ref diag(S_s) from another octant of the same geometry (dpm_dd_bep_block_from)."""
+        B = self._t(self.K, self.n_rows) if want else None
+        self._chk(L.lib.dpm_dd_bep_block_from(self._h, ref._h, _ptr(B), _stream(stream)))
+        return B
+
     def colnorm2(self, stream=None):
         out = self._t(self.K)
         self._chk(L.lib.dpm_dd_colnorm2(self._h, _ptr(out), _stream(stream)))

@@ -1173,6 +1173,64 @@ dpm_status dpm_dd_lsq_rhs(dpm_ctx* ctx, const double* wk, double* y, void* strea
   return DPM_OK;
 }
 
+// o->dd_sign: the column signs S of octant o's extension relative to o0's (E_o = E_0 diag(S)); computed once
+// per pair (one host sync), DPM_ERR_INVALID (error on o0) if the extensions are not sign reflections
+dpm_status dd_signs(dpm_ctx* o0, dpm_ctx* o, cudaStream_t s) {
+  if (o->dd_sign && o->dd_sign_ref == o0) return DPM_OK;
+  const int K = o0->K;
+  const int64_t ng = o0->counts[DPM_SET_GAMMA];
+  if (!o->dd_sign) DPM_CUDA_TRY(o0, cudaMalloc(&o->dd_sign, (size_t)K * sizeof(double) + 16));
+  int* dbad = reinterpret_cast<int*>(o->dd_sign + K);
+  DPM_CUDA_TRY(o0, cudaMemsetAsync(dbad, 0, sizeof(int), s));
+  DPM_COUNT_LAUNCH(1);
+  dd_sign_kernel<<<K, TB, 0, s>>>(o0->dd_Eraw, o->dd_Eraw, ng, o->dd_sign, dbad);
+  int hbad = 0;
+  DPM_CUDA_TRY(o0, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  DPM_CUDA_TRY(o0, cudaStreamSynchronize(s));
+  if (hbad) { o0->err = "the octant extensions are not sign-reflections"; return DPM_ERR_INVALID; }
+  o->dd_sign_ref = o0;
+  return DPM_OK;
+}
+
+__global__ void dd_signed_copy_kernel(const double* __restrict__ B0, int64_t m, const double* __restrict__ sign,
+                                      double* __restrict__ B) {
+  const int c = blockIdx.y;
+  const double sg = sign[c];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    B[(size_t)c * m + i] = sg * B0[(size_t)c * m + i];
+}
+
+dpm_status dpm_dd_bep_block_from(dpm_ctx* ctx, dpm_ctx* ref, double* B_out, void* stream) {
+  DPM_NVTX();
+  dpm_status st = dd_check(ctx);
+  if (st != DPM_OK) return st;
+  if (!ref || ref->dd != 1 || ctx->dd != 1 || ref->device != ctx->device || ref->n != ctx->n || ref->lo != ctx->lo ||
+      ref->hi != ctx->hi || ref->K != ctx->K || ref->n_rows != ctx->n_rows || ref->radius != ctx->radius) {
+    ctx->err = "dd_bep_block_from: the contexts are not octants of one canonical geometry on one device";
+    return DPM_ERR_INVALID;
+  }
+  if (!ref->dd_B || ref->dt_bep != ctx->dt || ref->dt != ctx->dt) {
+    ctx->err = "dd_bep_block_from: the reference block is not built at this dt";
+    return DPM_ERR_STATE;
+  }
+  if ((st = dd_alloc(ctx)) != DPM_OK) return st;
+  cudaStream_t s = as_stream(stream);
+  if ((st = dd_signs(ref, ctx, s)) != DPM_OK) {
+    ctx->err = ref->err;
+    return st;
+  }
+  const int64_t m = ctx->n_rows;
+  DPM_COUNT_LAUNCH(1);
+  dd_signed_copy_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((m + TB - 1) / TB, 64)), ctx->K), TB, 0,
+                          s>>>(ref->dd_B, m, ctx->dd_sign, ctx->dd_B);
+  DPM_CUDA_TRY(ctx, cudaGetLastError());
+  if (B_out)
+    DPM_CUDA_TRY(ctx, cudaMemcpyAsync(B_out, ctx->dd_B, (size_t)ctx->K * m * 8, cudaMemcpyDeviceToDevice, s));
+  ctx->have_projection = 0;
+  ctx->dt_bep = ctx->dt;
+  return DPM_OK;
+}
+
 dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const double* wk, double* y, void* stream) {
   DPM_NVTX();
   if (!octs || noct < 1 || !wk || !y) return DPM_ERR_INVALID;
@@ -1194,20 +1252,8 @@ dpm_status dpm_dd_lsq_rhs_shared(dpm_ctx* const* octs, int32_t noct, const doubl
   const int64_t ng = o0->counts[DPM_SET_GAMMA], m = o0->n_rows;
   const int nv = 2 * noct;
   // signs of every octant relative to octant 0 (geometry only: computed once per pair)
-  for (int q = 0; q < noct; ++q) {
-    dpm_ctx* o = octs[q];
-    if (o->dd_sign && o->dd_sign_ref == o0) continue;
-    if (!o->dd_sign) DPM_CUDA_TRY(o0, cudaMalloc(&o->dd_sign, (size_t)K * sizeof(double) + 16));
-    int* dbad = reinterpret_cast<int*>(o->dd_sign + K);
-    DPM_CUDA_TRY(o0, cudaMemsetAsync(dbad, 0, sizeof(int), s));
-    DPM_COUNT_LAUNCH(1);
-    dd_sign_kernel<<<K, TB, 0, s>>>(o0->dd_Eraw, o->dd_Eraw, ng, o->dd_sign, dbad);
-    int hbad = 0;
-    DPM_CUDA_TRY(o0, cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    DPM_CUDA_TRY(o0, cudaStreamSynchronize(s));
-    if (hbad) { o0->err = "dd_lsq_rhs_shared: the octant extensions are not sign-reflections"; return DPM_ERR_INVALID; }
-    o->dd_sign_ref = o0;
-  }
+  for (int q = 0; q < noct; ++q)
+    if ((st = dd_signs(o0, octs[q], s)) != DPM_OK) return st;
   const int nsplit = (int)((m + TS_ICH - 1) / TS_ICH), nsk = (K + TS_ICH - 1) / TS_ICH;
   const int nua = (K + UA_CH - 1) / UA_CH;   // i-chunks of the D R^{-1} apply (2 right-hand sides each)
   const int npart = std::max(std::max(1, std::max(nsplit, nsk)), (2 * nua + nv - 1) / nv);

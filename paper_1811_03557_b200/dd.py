@@ -13,6 +13,7 @@ the collectives of the distributed CholeskyQR2 / step:
   * C2 (per step): all-reduce(sum) of y_s = M_s g_s (K x 2) -> the global coefficients C.
 Local contributions are summed in octant order before the cross-rank all-reduce.
 """
+import os
 from typing import Callable, List, Optional, Sequence
 
 import torch
@@ -48,9 +49,17 @@ class DDSolver:
         return _allreduce(acc, dist.ReduceOp.SUM)
 
     def build(self, dt: float):
+        # octants of one canonical geometry on one device: the first builds its block by K AP solves, the
+        # others take it by column signs (B_s = B_0 diag(S_s), dpm_dd_bep_block_from); DPM_DD_SHARED=0 off
+        ref = {}
         for o in self.octs:
             o.set_dt(dt)
-            o.bep_block()
+            r = ref.get(str(o.device))
+            if r is not None and self._shared_build():
+                o.bep_block_from(r)
+            else:
+                o.bep_block()
+                ref[str(o.device)] = o
         n2 = self._sum([o.colnorm2() for o in self.octs])
         G1 = self._sum([o.gram(1, n2) for o in self.octs])
         self._chol(1, G1)
@@ -76,6 +85,11 @@ class DDSolver:
         return (len(self.octs) > 1 and all(hasattr(o, "dd_rhs") for o in self.octs)
                 and len({str(o.device) for o in self.octs}) == 1 and self.octs[0].device.type == "cuda"
                 and len({(o.n, o.info["h"]) for o in self.octs}) == 1)   # one AP operator for all fields
+
+    def _shared_build(self):
+        # config-5 octants only (the Case-1 subdomains have different geometries)
+        return (os.environ.get("DPM_DD_SHARED") != "0" and all(hasattr(o, "bep_block_from") for o in self.octs)
+                and all(getattr(o, "octant", None) is not None and not hasattr(o, "sub") for o in self.octs))
 
     def _shared(self):
         # octants of config 5 (not the Case-1 subdomains): one canonical geometry, extensions that differ

@@ -53,6 +53,24 @@ def test_bep_block(api, setup, s):
     assert rel(B, Bo) <= 1e-11, rel(B, Bo)
 
 
+def test_bep_block_from_reference_octant(api, setup):
+    # dpm_dd_bep_block_from: octant s's block from octant 0's by the column signs of the extensions
+    # (B_s = B_0 diag(S_s)) against the oracle's block of octant s and the GPU's own K AP solves
+    dt = 1e-3
+    g0 = api.Octant(N, *BOX, 0, 1.0, LC, LI, dt)
+    g0.bep_block()
+    for s in (1, 5, 7):
+        g = api.Octant(N, *BOX, s, 1.0, LC, LI, dt)
+        Bf = g.bep_block_from(g0, want=True).cpu().numpy().T
+        Bo, _ = odd.bep_block(setup, setup.octants[s], dt)
+        assert rel(Bf, Bo) <= 1e-11, (s, rel(Bf, Bo))
+        Bd = g.bep_block(want=True).cpu().numpy().T
+        assert rel(Bf, Bd) <= 1e-13, (s, rel(Bf, Bd))
+    g1 = api.Octant(N, *BOX, 1, 1.0, LC, LI, 2e-3)   # reference block at another dt: refused
+    with pytest.raises(Exception):
+        g1.bep_block_from(g0)
+
+
 def test_dd_pks_parity(api):
     from paper_1811_03557_b200.dd import DDSolver
     steps, cap = 3, 1e-3
