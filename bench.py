@@ -340,7 +340,7 @@ def bench_bep_distributed(ctx, torch, dist, world, rank, reps=3):
         ts.append(float(t.item()))
     c0, c1 = parallel.shard_range(ctx.K, world, rank)
     return {"K": ctx.K, "ranks": world, "columns_per_rank": c1 - c0, "build_ms": statistics.median(ts),
-            "collective": "all_gather of the |gamma_in| x K reduced BEP (NCCL)"}
+            "collective": "all_gather of the |gamma_in| x K reduced BEP (%s)" % dist.get_backend()}
 
 
 def bench_test_b(N=127, harmonics=150):
@@ -491,12 +491,23 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # Functional check of the N > 1 path on a box with ONE GPU (tests/test_gpu_multirank.py): every rank on
+    # cuda:0 (DPM_BENCH_ONE_GPU=1) and the collectives over gloo (DPM_BENCH_BACKEND=gloo; NCCL refuses two
+    # ranks on one device).  The kernels of different ranks never wait on one another (host-side
+    # collectives only); such a run measures nothing about scaling and says so in the line.
+    backend = os.environ.get("DPM_BENCH_BACKEND", "nccl")
+    one_gpu = os.environ.get("DPM_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        try:   # bind the NCCL communicator to this rank's GPU
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        except TypeError:
-            dist.init_process_group("nccl")
+        if backend != "nccl":
+            dist.init_process_group(backend)
+        else:
+            try:   # bind the NCCL communicator to this rank's GPU
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            except TypeError:
+                dist.init_process_group("nccl")
     from paper_1811_03557_b200 import api
     from paper_1811_03557_b200._lib import lib as L
 
@@ -608,6 +619,9 @@ def main():
                                   "frac": flops_per_solve * value / world / 1e12 / FP64_PEAK_TFLOPS,
                                   "flops_per_solve": flops_per_solve}},
             "gpu_launches": int(launches), "clocks": clocks}
+    if world > 1 and (one_gpu or backend != "nccl"):
+        line["functional_only"] = ("%d ranks, backend %s%s: a check of the multi-rank path, not a scaling number"
+                                   % (world, backend, ", all on cuda:0" if one_gpu else ""))
 
     if not args.no_e2e and nb:
         # e2e through the C-ABI host-buffer call: pinned host q/u, H2D + solve + D2H inside the timed region
@@ -671,7 +685,10 @@ def main():
         except NameError:
             pass
         torch.cuda.empty_cache()
-        line["bep_build_distributed_cfg4"] = bench_bep_distributed(ctx, torch, dist, world, rank)
+        try:
+            line["bep_build_distributed_cfg4"] = bench_bep_distributed(ctx, torch, dist, world, rank)
+        except Exception as e:   # the headline above stands; the error is reported in its place
+            line["bep_build_distributed_cfg4"] = {"error": repr(e)}
 
     if not args.no_dd and 8 % world == 0:
         try:
@@ -679,7 +696,12 @@ def main():
         except NameError:
             pass
         torch.cuda.empty_cache()
-        dd = bench_dd(api, torch, world, rank)
+        try:
+            dd = bench_dd(api, torch, world, rank)
+        except Exception as e:
+            if world == 1:
+                raise
+            dd = {"error": repr(e)}
         if rank == 0:
             line["dd"] = {"cfg5": dd}
 
