@@ -19,8 +19,14 @@
 //   (4) inverse transform along y and z (P = S_y U S_z^T);
 //   (5) gather γ / γ_in through the octant map with the parity signs.
 // Per column: m^3 = n^3/8 points, two 2-GEMM plane passes and one tridiagonal pass over 8 n^3/8 bytes each,
-// instead of three full n^3 passes.  Columns that are not parity-definite, asymmetric
-// sets, odd n or n > 128 take the full path (dpm_bep_columns).  DPM_BEP_SYM=0 disables, DPM_BEP_SYM=2 makes a
+// instead of three full n^3 passes.
+// Odd n (the paper's N = 127 Test B mesh): the octant is [0, m)^3 with m = (n+1)/2 and its last index the
+// centre node, which is its own mirror.  Along an axis of even parity the unknowns are i = 0..m-1 with
+// u_m = u_{m-2} (centre row d u_c - 2 u_{c-1}/h^2), the modes k = 2b+1, and the forward sum over the full line
+// counts the centre once: weight 1/2 on the centre entry (a separate forward table, S[2..3]); along an axis of
+// odd parity the centre value is 0, the unknowns i = 0..m-2 (plain Dirichlet), the modes k = 2b+2, b < m-1 (the
+// centre row and the mode b = m-1 of that table are zero).
+// Columns that are not parity-definite, asymmetric sets or (n+1)/2 > 64 take the full path (dpm_bep_columns).  DPM_BEP_SYM=0 disables, DPM_BEP_SYM=2 makes a
 // context the octant path does not apply to fail (cudaErrorNotSupported) instead of falling back.
 #include <algorithm>
 #include <cmath>
@@ -153,8 +159,8 @@ __global__ void __launch_bounds__(SYM_NT, 2) sym_yz_kernel(const double* in, dou
     else asm volatile("cp.async.commit_group;\n" ::);
     const int pr = par[p / m] & 6;
     if (pr != cls) {
-      sym_afrag<MP>(S + ((pr >> 1) & 1) * MP * MP, FWD, A1);
-      sym_afrag<MP>(S + ((pr >> 2) & 1) * MP * MP, FWD, A2);
+      sym_afrag<MP>(S + ((FWD ? 2 : 0) + ((pr >> 1) & 1)) * MP * MP, FWD, A1);   // [0,1] inverse, [2,3] forward
+      sym_afrag<MP>(S + ((FWD ? 2 : 0) + ((pr >> 2) & 1)) * MP * MP, FWD, A2);
       cls = pr;
     }
     asm volatile("cp.async.wait_group 1;\n" ::);
@@ -174,10 +180,11 @@ __global__ void __launch_bounds__(SYM_NT, 2) sym_yz_kernel(const double* in, dou
 
 // (3a): LU factors of the x tridiagonal of every spectral pencil (w = b*m + c) of every y/z parity class q:
 // den_i = d - h2i e_{i-1}, r_i = 1/den_i, e_i = h2i r_i (i < m-1), and the last row's r for both x parities
-// (u_m = +u_{m-1}: d - h2i; u_m = -u_{m-1}: d + h2i).  They depend on Δt and the geometry only, not on the
-// column: built once per Δt, read by every column of the class.
-__global__ void sym_lu_kernel(int m, int MP, const double* __restrict__ lamr, double inv_dt, double h2i, double* R,
-                              double* Ef, double* Rl) {
+// (u_m = +u_{m-1}: d - h2i; u_m = -u_{m-1}: d + h2i; odd n: the centre row d with -2 h2i below the diagonal
+// for the even parity, and 0 for the odd parity, whose centre value is 0).  They depend on Δt and the geometry
+// only, not on the column: built once per Δt, read by every column of the class.
+__global__ void sym_lu_kernel(int m, int MP, int odd, const double* __restrict__ lamr, double inv_dt, double h2i,
+                              double* R, double* Ef, double* Rl) {
   const long m2 = (long)m * m;
   const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= 4 * m2) return;
@@ -190,8 +197,8 @@ __global__ void sym_lu_kernel(int m, int MP, const double* __restrict__ lamr, do
     R[((long)q * m + i) * m2 + w] = r;
     Ef[((long)q * m + i) * m2 + w] = e;
   }
-  Rl[((long)q * 2 + 0) * m2 + w] = 1.0 / ((d - h2i) - h2i * e);
-  Rl[((long)q * 2 + 1) * m2 + w] = 1.0 / ((d + h2i) - h2i * e);
+  Rl[((long)q * 2 + 0) * m2 + w] = odd ? 1.0 / (d - 2.0 * h2i * e) : 1.0 / ((d - h2i) - h2i * e);
+  Rl[((long)q * 2 + 1) * m2 + w] = odd ? 0.0 : 1.0 / ((d + h2i) - h2i * e);
 }
 
 // (3b): per spectral pencil (column cc, w = b*m + c): (1/dt + λ_b + λ_c + T_x,sx) v = q along x with the
@@ -199,7 +206,8 @@ __global__ void sym_lu_kernel(int m, int MP, const double* __restrict__ lamr, do
 template <int MP, bool EXACT>
 __global__ void __launch_bounds__(SYM_NT) sym_x_kernel(double* u, int ncols, int m_rt, const uint8_t* __restrict__ par,
                                                        const double* __restrict__ R, const double* __restrict__ Ef,
-                                                       const double* __restrict__ Rl, double h2i, double scale) {
+                                                       const double* __restrict__ Rl, double h2i, double scale,
+                                                       double lm_even) {
   const int m = EXACT ? MP : m_rt;
   const long m2 = (long)m * m, total = (long)ncols * m2;
   const long id = (long)blockIdx.x * SYM_NT + threadIdx.x;
@@ -214,6 +222,7 @@ __global__ void __launch_bounds__(SYM_NT) sym_x_kernel(double* u, int ncols, int
 #pragma unroll
   for (int i = 0; i < MP; ++i) g[i] = i < m ? col[(long)i * m2] : 0.0;
   const double rl = __ldg(Rl + ((long)q * 2 + (pr & 1)) * m2 + w);
+  const double hl = (pr & 1) ? h2i : lm_even * h2i;   // last row's subdiagonal (odd n, even parity: 2/h^2)
   double gprev = 0.0, next = 0.0;
 #pragma unroll
   for (int i = 0; i < MP; ++i) {
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(SYM_NT) sym_x_kernel(double* u, int ncols, int
       gprev = (g[i] + h2i * gprev) * __ldg(Rq + (long)i * m2);
       g[i] = gprev;
     } else if (i == m - 1) {
-      next = (g[i] + h2i * gprev) * rl;
+      next = (g[i] + hl * gprev) * rl;
       col[(long)i * m2] = next * scale;
     }
   }
@@ -330,8 +339,9 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
   const char* env = getenv("DPM_BEP_SYM");
   if (env && atoi(env) == 0) return cudaSuccess;
   const int n = ctx->n;
-  if (n % 2 || n / 2 > SYM_MMAX || !ctx->E || ctx->dd == 1 || ctx->K == 0) return cudaSuccess;
-  const int m = n / 2;
+  const int m = (n + 1) / 2;   // odd n: the last octant index is the centre node (its own mirror)
+  const bool odd = n & 1;
+  if (m > SYM_MMAX || m < 2 || !ctx->E || ctx->dd == 1 || ctx->K == 0) return cudaSuccess;
   const long nn = (long)n * n, n3 = nn * n;
   // the sets the potential RHS and the traces read: γ (gmap), the band, M+, γ_in
   const int sets[4] = {DPM_SET_GAMMA, DPM_SET_BAND, DPM_SET_MPLUS, DPM_SET_GAMMA_IN};
@@ -411,12 +421,17 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
   for (long r = 0; r < ng; ++r) gidx[r] = octant(gam[r]);
   for (long r = 0; r < ngin; ++r) gidx[ng + r] = octant(L[3][r]);
   const int MP = sym_mp(m);
-  std::vector<double> S(2 * (size_t)MP * MP, 0.0), lam(2 * MP, 0.0);
+  std::vector<double> S(4 * (size_t)MP * MP, 0.0), lam(2 * MP, 0.0);   // S[0,1]: inverse, S[2,3]: forward
   const long per = 2L * (n + 1);
   for (int s = 0; s < 2; ++s)
     for (int b = 0; b < m; ++b) {
       const long k = 2L * b + 1 + s;
-      for (int j = 0; j < m; ++j) S[((size_t)s * MP + j) * MP + b] = std::sin(M_PI * (double)((k * (j + 1)) % per) / (n + 1));
+      for (int j = 0; j < m; ++j) {
+        double v = std::sin(M_PI * (double)((k * (j + 1)) % per) / (n + 1));
+        if (odd && s == 1 && (j == m - 1 || b == m - 1)) v = 0.0;   // sin(k π/2), k even / the mode k = n+1
+        S[((size_t)s * MP + j) * MP + b] = v;
+        S[((size_t)(2 + s) * MP + j) * MP + b] = odd && j == m - 1 ? 0.5 * v : v;
+      }
       const double sk = std::sin((double)k * M_PI / (2.0 * (n + 1)));
       lam[s * MP + b] = (4.0 / (ctx->h * ctx->h)) * sk * sk;
     }
@@ -463,10 +478,12 @@ cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const ui
   const int grid_yz = (int)std::min<long>(planes, 148L * 2);
   const long pencils = (long)nc * m2;
   const double h2i = 1.0 / (ctx->h * ctx->h), scale = (4.0 / (n + 1)) * (4.0 / (n + 1));
+  const double lm = (n & 1) ? 2.0 : 1.0;
   if (ctx->sym_lu_dt != ctx->dt) {   // (3a) once per Δt
     DPM_COUNT_LAUNCH(1);
-    sym_lu_kernel<<<(unsigned)((4 * m2 + 127) / 128), 128, 0, s>>>(m, MP, ctx->sym_lam, 1.0 / ctx->dt, h2i, ctx->sym_R,
-                                                                   ctx->sym_R + 4 * m2 * m, ctx->sym_R + 8 * m2 * m);
+    sym_lu_kernel<<<(unsigned)((4 * m2 + 127) / 128), 128, 0, s>>>(m, MP, n & 1, ctx->sym_lam, 1.0 / ctx->dt, h2i,
+                                                                   ctx->sym_R, ctx->sym_R + 4 * m2 * m,
+                                                                   ctx->sym_R + 8 * m2 * m);
     ctx->sym_lu_dt = ctx->dt;
   }
   const double* R = ctx->sym_R;
@@ -474,9 +491,9 @@ cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const ui
   sym_yz_kernel<MP, true><<<grid_yz, SYM_NT, smem_yz, s>>>(q, u, nc, m, par, ctx->sym_S);
   const unsigned gx = (unsigned)((pencils + SYM_NT - 1) / SYM_NT);
   if (m == MP)
-    sym_x_kernel<MP, true><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale);
+    sym_x_kernel<MP, true><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale, lm);
   else
-    sym_x_kernel<MP, false><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale);
+    sym_x_kernel<MP, false><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale, lm);
   sym_yz_kernel<MP, false><<<grid_yz, SYM_NT, smem_yz, s>>>(u, u, nc, m, par, ctx->sym_S);
   return cudaGetLastError();
 }

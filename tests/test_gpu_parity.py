@@ -341,9 +341,32 @@ def test_bep_columns_fused_matches_dense_path_cfg4(tmp_path):
         assert rel(outs[f][1], outs["0"][1]) <= 1e-12, f
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+@pytest.mark.parametrize("name", ["testB25", "testB31", "cfg1n15", "cfg2n31"])
+def test_bep_columns_octant_odd_n_vs_oracle(api, monkeypatch, name):
+    # odd n (the paper's Test B meshes, n = N): the octant is [0, (n+1)/2)^3 with the centre node its own
+    # mirror (m = 13: odd m, padded tables; m = 16: exact; the zonal Test B basis has the z parities only,
+    # the full real-SH bases of cfg1 / cfg2 at odd n all eight classes); the octant path required
+    # (DPM_BEP_SYM=2), against the oracle's potential RHS -> AP solve -> trace
+    import dataclasses
+    from dpm_inputs.configs import test_b_config
+    monkeypatch.setenv("DPM_BEP_SYM", "2")
+    if name.startswith("testB"):
+        cfg = test_b_config(int(name[5:]), 9)
+    else:
+        cfg = dataclasses.replace(get_config(name[:4]), n=int(name[5:]))
+    c = api.DPM.from_config(cfg)
+    cols = sorted({0, 1, 2, 3, c.K // 2, c.K // 2 + 1, c.K - 2, c.K - 1})
+    ref = _bep_oracle_columns(cfg, cols)
+    for col, (pg_o, b_o) in zip(cols, ref):
+        PgE, B = c.bep_columns(col, col + 1)
+        assert rel(PgE.cpu().numpy()[0], pg_o) <= 1e-11, (name, col)
+        assert rel(B.cpu().numpy()[0], b_o) <= 1e-11, (name, col)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "testB27", "testB127"])
 def test_bep_columns_octant_matches_full_path(tmp_path, name):
-    # the octant path (bep_sym.cu: reflection-symmetric sets, parity-definite columns, m = n/2) required
+    # the octant path (bep_sym.cu: reflection-symmetric sets, parity-definite columns, m = n/2, or (n+1)/2
+    # with the centre node for odd n: Test B's N = 127 mesh with its 150 zonal harmonics) required
     # (DPM_BEP_SYM=2: an error if it does not apply) against the full-grid path (DPM_BEP_SYM=0), all K
     # columns; separate processes (the selector is decided once per context)
     import os, subprocess, sys, textwrap
@@ -352,7 +375,10 @@ def test_bep_columns_octant_matches_full_path(tmp_path, name):
         import sys, numpy as np, torch
         from dpm_inputs import get_config
         from paper_1811_03557_b200 import api
-        c = api.DPM.from_config(get_config(sys.argv[3]))
+        from dpm_inputs.configs import test_b_config
+        nm = sys.argv[3]
+        cfg = get_config(nm) if nm.startswith("cfg") else test_b_config(int(nm[5:]), 150 if nm == "testB127" else 9)
+        c = api.DPM.from_config(cfg)
         PgE, B = c.bep_columns(0, c.K)
         np.save(sys.argv[1], PgE.cpu().numpy()); np.save(sys.argv[2], B.cpu().numpy())
     ''')
