@@ -841,6 +841,15 @@ __device__ __forceinline__ void st_async(unsigned remote, double v, unsigned rem
 #ifndef FACR_PHASE_TIMING
 #define FACR_PHASE_TIMING 0
 #endif
+// Phase 5 with the four running powers of its correction merged into two and the powers of μ from shared
+// squarings (0: the first form, four walks and five ipow128 calls)
+// unroll depth of the final store loop (shared-memory loads in flight ahead of the global stores)
+#ifndef PLANE_STORE_UNROLL
+#define PLANE_STORE_UNROLL 4
+#endif
+#ifndef PLANE_P5_MERGED
+#define PLANE_P5_MERGED 1
+#endif
 constexpr int FACR_TCTAS = 4096, FACR_TPH = 9;
 // Speed-of-light switches (timing experiments only, tools/plane_sol.sh; results are wrong when any is
 // set): skip the half-plane load, phase 1, the two transforms, the phase-3 recurrences, phase 5 or
@@ -1063,7 +1072,15 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     for (int q = 1; q < 33; ++q) x[q] = fma(muy, x[q - 1], x[q]);
     const double yv = (s & 1) ? x[30] : x[32];
     const int base = lane & 7;
+#if PLANE_P5_MERGED
+    // the powers of μ this phase needs, from 5 squarings and a few products (all of them shrink with the
+    // exponent: an underflow to 0 only drops terms that are themselves negligible, as with ipow128)
+    const double m4 = mu2 * mu2, m8 = m4 * m4, m16 = m8 * m8, m32 = m16 * m16;
+    const double mu31 = ((m16 * m8) * (m4 * mu2)) * muy, mu33 = m32 * muy;
+    const double m64 = m32 * m32, m128 = m64 * m64, m256 = m128 * m128;
+#else
     const double mu33 = ipow128(muy, 33), mu31 = ipow128(muy, 31);
+#endif
     const double Y0 = __shfl_sync(0xffffffffu, yv, base), Y1 = __shfl_sync(0xffffffffu, yv, base + 8),
                  Y2 = __shfl_sync(0xffffffffu, yv, base + 16);
     // incoming true y_{kb-1}: segment lengths 33, 31, 33
@@ -1084,6 +1101,26 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
     const double Z3 = T3, Z2 = fma(mu33, Z3, T2), Z1 = fma(mu31, Z2, T1), Z0 = fma(mu33, Z1, T0);
     const double Zr = s == 0 ? Z1 : s == 1 ? Z2 : s == 2 ? Z3 : 0.0;   // true z at ke
     // S3 (ascending): w_k = μ (ẑ_k + cin ζ_k) - c2 (μ^{k+1} - μ^{2n+1-k}),  c2 = μ² z_0 / (1 - μ^{2n+2})
+#if PLANE_P5_MERGED
+    // the four running powers of the unmerged form pair up: μ^{q+1} and μ^{kb+1+q} are both ∝ μ^q, μ^{2L+1-q}
+    // and μ^{2n+1-kb-q} both ∝ μ^{-q}, so  w_q = μ x_q + a_q + b_q  with
+    //   a_q = (ci μ² - c2 μ^{kb+1}) μ^q,   b_q = (c2 μ^{2n+1-kb} - ci μ^{2L+2}) μ^{-q}
+    // (same walking directions as before: a shrinks, b grows from a start that is negligible when tiny)
+    const double c2 = mu2 * Z0 / (1.0 - m256 * mu2);
+    const double ci = cin * i1m;
+    const double mu34 = mu33 * muy;
+    const double pkb = s == 0 ? muy : s == 1 ? mu34 : s == 2 ? m64 * muy : m64 * mu34;          // μ^{kb+1}
+    const double pnk = s == 0 ? m256 * muy : s == 1 ? (m128 * m64) * m32 : s == 2 ? (m128 * m64) * muy
+                                                                                   : m128 * m32;   // μ^{2n+1-kb}
+    const double p2l = (s & 1) ? m64 : m64 * m4;                                                   // μ^{2L+2}
+    double aq = fma(ci, mu2, -c2 * pkb), bq = fma(c2, pnk, -ci * p2l);
+#pragma unroll
+    for (int q = 0; q < 33; ++q) {
+      x[q] = fma(muy, x[q], aq + bq);
+      aq *= muy;
+      bq *= imu;
+    }
+#else
     const double c2 = mu2 * Z0 / (1.0 - ipow128(muy, 2 * N + 2));
     const double ci = cin * i1m;
     double p1 = muy, p2 = ipow128(muy, 2 * L + 1);                // μ^{k-kb+1}, μ^{2ke-kb+1-k}
@@ -1096,6 +1133,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
       pa *= muy;
       pb *= imu;
     }
+#endif
     // S4 (descending): + μ^{ke-k+1} Zr, then the single store of the segment
     double pr = mu2 * Zr;                                          // Zr = 0 for the last segment
     if (s & 1) {
@@ -1114,6 +1152,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   }
   __syncthreads();
   FACR_MARK(7);
+#pragma unroll PLANE_STORE_UNROLL
   for (int e = t; e < (PLANE_SOL_NOSTORE ? 0 : N * PHC); e += PTHR) {   // same lane -> (column, z) map as the load
     const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
     const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
