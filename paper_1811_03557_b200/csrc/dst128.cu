@@ -847,6 +847,8 @@ __device__ __forceinline__ void st_async(unsigned remote, double v, unsigned rem
 #ifndef PLANE_STORE_UNROLL
 #define PLANE_STORE_UNROLL 4
 #endif
+#define PLANE_PRAGMA(x) _Pragma(#x)
+#define PLANE_UNROLL(n) PLANE_PRAGMA(unroll n)
 #ifndef PLANE_P5_MERGED
 #define PLANE_P5_MERGED 1
 #endif
@@ -1152,7 +1154,7 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   }
   __syncthreads();
   FACR_MARK(7);
-#pragma unroll PLANE_STORE_UNROLL
+  PLANE_UNROLL(PLANE_STORE_UNROLL)
   for (int e = t; e < (PLANE_SOL_NOSTORE ? 0 : N * PHC); e += PTHR) {   // same lane -> (column, z) map as the load
     const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
     const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
