@@ -795,7 +795,7 @@ plane128_kernel(double* __restrict__ u, const double* __restrict__ lam_g, double
 // plane128_kernel; 30% fewer instructions, DFMA count -40%.
 // Running powers of μ are only walked in the direction in which they shrink when their term is
 // not negligible (see plane128_kernel).
-__device__ __forceinline__ double ipow128(double b, int e) {   // b^e, 0 <= e < 512
+[[maybe_unused]] __device__ __forceinline__ double ipow128(double b, int e) {   // b^e, 0 <= e < 512
   double r = 1.0;
 #pragma unroll
   for (int q = 0; q < 9; ++q) {
@@ -846,6 +846,9 @@ __device__ __forceinline__ void st_async(unsigned remote, double v, unsigned rem
 // unroll depth of the final store loop (shared-memory loads in flight ahead of the global stores)
 #ifndef PLANE_STORE_UNROLL
 #define PLANE_STORE_UNROLL 4
+#endif
+#ifndef PLANE_STORE_CS
+#define PLANE_STORE_CS 0   // 1: st.global.cs (evict-first) for the plane's output
 #endif
 #define PLANE_PRAGMA(x) _Pragma(#x)
 #define PLANE_UNROLL(n) PLANE_PRAGMA(unroll n)
@@ -1158,7 +1161,11 @@ plane128_facr_kernel(double* __restrict__ u, const double* __restrict__ lam_g, d
   for (int e = t; e < (PLANE_SOL_NOSTORE ? 0 : N * PHC); e += PTHR) {   // same lane -> (column, z) map as the load
     const int r = e >> 6, c = ((e >> 5) & 1) * 16 + (e & 15) + ((e & 16) ? 32 : 0);
     const int z = 2 * (c & 31) + ((e & 16) ? 0 : 1);
+#if PLANE_STORE_CS
+    __stcs(gp + (size_t)r * N + z, P[r * PPITCH + c]);
+#else
     __stcg(gp + (size_t)r * N + z, P[r * PPITCH + c]);
+#endif
   }
   FACR_MARK(8);
   // no exit barrier: each CTA has consumed every remote store aimed at it (its mbarrier waits), and
