@@ -333,6 +333,28 @@ cudaError_t upload(T** dst, const std::vector<T>& v) {
 
 int sym_mp(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : m <= 32 ? 32 : 64; }
 
+// octant sine tables S[0,1] (inverse) / S[2,3] (forward, half weight on the centre entry for odd n) of the
+// even / odd parity, zero-padded to MP x MP, and their eigenvalues lam[2][MP]
+void sym_tables(int n, double h, std::vector<double>& S, std::vector<double>& lam) {
+  const int m = (n + 1) / 2, MP = sym_mp(m);
+  const bool odd = n & 1;
+  S.assign(4 * (size_t)MP * MP, 0.0);
+  lam.assign(2 * MP, 0.0);
+  const long per = 2L * (n + 1);
+  for (int s = 0; s < 2; ++s)
+    for (int b = 0; b < m; ++b) {
+      const long k = 2L * b + 1 + s;
+      for (int j = 0; j < m; ++j) {
+        double v = std::sin(M_PI * (double)((k * (j + 1)) % per) / (n + 1));
+        if (odd && s == 1 && (j == m - 1 || b == m - 1)) v = 0.0;   // sin(k π/2), k even / the mode k = n+1
+        S[((size_t)s * MP + j) * MP + b] = v;
+        S[((size_t)(2 + s) * MP + j) * MP + b] = odd && j == m - 1 ? 0.5 * v : v;
+      }
+      const double sk = std::sin((double)k * M_PI / (2.0 * (n + 1)));
+      lam[s * MP + b] = (4.0 / (h * h)) * sk * sk;
+    }
+}
+
 // Decide once per context whether the octant path applies and build its tables (host sync: first call only).
 cudaError_t sym_prepare(dpm_ctx* ctx) {
   ctx->sym = -1;
@@ -421,20 +443,8 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
   for (long r = 0; r < ng; ++r) gidx[r] = octant(gam[r]);
   for (long r = 0; r < ngin; ++r) gidx[ng + r] = octant(L[3][r]);
   const int MP = sym_mp(m);
-  std::vector<double> S(4 * (size_t)MP * MP, 0.0), lam(2 * MP, 0.0);   // S[0,1]: inverse, S[2,3]: forward
-  const long per = 2L * (n + 1);
-  for (int s = 0; s < 2; ++s)
-    for (int b = 0; b < m; ++b) {
-      const long k = 2L * b + 1 + s;
-      for (int j = 0; j < m; ++j) {
-        double v = std::sin(M_PI * (double)((k * (j + 1)) % per) / (n + 1));
-        if (odd && s == 1 && (j == m - 1 || b == m - 1)) v = 0.0;   // sin(k π/2), k even / the mode k = n+1
-        S[((size_t)s * MP + j) * MP + b] = v;
-        S[((size_t)(2 + s) * MP + j) * MP + b] = odd && j == m - 1 ? 0.5 * v : v;
-      }
-      const double sk = std::sin((double)k * M_PI / (2.0 * (n + 1)));
-      lam[s * MP + b] = (4.0 / (ctx->h * ctx->h)) * sk * sk;
-    }
+  std::vector<double> S, lam;
+  sym_tables(n, ctx->h, S, lam);
   if ((e = upload(&ctx->sym_list, olist)) != cudaSuccess) return e;
   if ((e = upload(&ctx->sym_dst, odst)) != cudaSuccess) return e;
   if ((e = upload(&ctx->sym_gidx, gidx)) != cudaSuccess) return e;
@@ -467,9 +477,19 @@ cudaError_t sym_prepare(dpm_ctx* ctx) {
   return cudaSuccess;
 }
 
+// the octant operator a solve runs on: tables, LU factor storage, and when to (re)build the factors
+struct SymOp {
+  int n, m;
+  double h, dt;
+  const double* S;
+  const double* lam;
+  double* R;
+  bool build_lu;   // launch sym_lu_kernel before the solve
+};
+
 template <int MP>
-cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const uint8_t* par, cudaStream_t s) {
-  const int m = ctx->sym_m, n = ctx->n;
+cudaError_t sym_solve(const SymOp& op, const double* q, double* u, int nc, const uint8_t* par, cudaStream_t s) {
+  const int m = op.m, n = op.n;
   const long m2 = (long)m * m;
   constexpr size_t smem_yz = 3 * (size_t)MP * SymGeo<MP>::LD * sizeof(double);
   cudaFuncSetAttribute(sym_yz_kernel<MP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_yz);
@@ -477,25 +497,89 @@ cudaError_t sym_solve(dpm_ctx* ctx, const double* q, double* u, int nc, const ui
   const long planes = (long)nc * m;
   const int grid_yz = (int)std::min<long>(planes, 148L * 2);
   const long pencils = (long)nc * m2;
-  const double h2i = 1.0 / (ctx->h * ctx->h), scale = (4.0 / (n + 1)) * (4.0 / (n + 1));
+  const double h2i = 1.0 / (op.h * op.h), scale = (4.0 / (n + 1)) * (4.0 / (n + 1));
   const double lm = (n & 1) ? 2.0 : 1.0;
-  if (ctx->sym_lu_dt != ctx->dt) {   // (3a) once per Δt
+  if (op.build_lu) {   // (3a) once per Δt
     DPM_COUNT_LAUNCH(1);
-    sym_lu_kernel<<<(unsigned)((4 * m2 + 127) / 128), 128, 0, s>>>(m, MP, n & 1, ctx->sym_lam, 1.0 / ctx->dt, h2i,
-                                                                   ctx->sym_R, ctx->sym_R + 4 * m2 * m,
-                                                                   ctx->sym_R + 8 * m2 * m);
-    ctx->sym_lu_dt = ctx->dt;
+    sym_lu_kernel<<<(unsigned)((4 * m2 + 127) / 128), 128, 0, s>>>(m, MP, n & 1, op.lam, 1.0 / op.dt, h2i, op.R,
+                                                                   op.R + 4 * m2 * m, op.R + 8 * m2 * m);
   }
-  const double* R = ctx->sym_R;
+  const double* R = op.R;
   DPM_COUNT_LAUNCH(3);
-  sym_yz_kernel<MP, true><<<grid_yz, SYM_NT, smem_yz, s>>>(q, u, nc, m, par, ctx->sym_S);
+  sym_yz_kernel<MP, true><<<grid_yz, SYM_NT, smem_yz, s>>>(q, u, nc, m, par, op.S);
   const unsigned gx = (unsigned)((pencils + SYM_NT - 1) / SYM_NT);
   if (m == MP)
     sym_x_kernel<MP, true><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale, lm);
   else
     sym_x_kernel<MP, false><<<gx, SYM_NT, 0, s>>>(u, nc, m, par, R, R + 4 * m2 * m, R + 8 * m2 * m, h2i, scale, lm);
-  sym_yz_kernel<MP, false><<<grid_yz, SYM_NT, smem_yz, s>>>(u, u, nc, m, par, ctx->sym_S);
+  sym_yz_kernel<MP, false><<<grid_yz, SYM_NT, smem_yz, s>>>(u, u, nc, m, par, op.S);
   return cudaGetLastError();
+}
+
+cudaError_t sym_solve_mp(const SymOp& op, const double* q, double* u, int nc, const uint8_t* par, cudaStream_t s) {
+  switch (sym_mp(op.m)) {
+    case 8: return sym_solve<8>(op, q, u, nc, par, s);
+    case 16: return sym_solve<16>(op, q, u, nc, par, s);
+    case 32: return sym_solve<32>(op, q, u, nc, par, s);
+    default: return sym_solve<64>(op, q, u, nc, par, s);
+  }
+}
+
+// ---- parity-split AP solve of dense boxes (octsplit_solve) ---------------------------------------------------
+// fold: the 8 parity components of every field on the octant, Q[(f*8 + p)][i][j][k] =
+// (1/8) Σ_σ (-1)^{popcount(p & σ)} q_f(σ(i, j, k)), σ the 8 reflections (bit a: axis a mirrored, i -> n-1-i; at
+// the centre node of an odd n the mirror is the node itself and the odd components come out exactly 0)
+__global__ void osp_fold_kernel(const double* __restrict__ q, double* __restrict__ Q, int nf, int n, int m) {
+  const long m3 = (long)m * m * m, n2 = (long)n * n, n3 = n2 * n;
+  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nf * m3) return;
+  const int f = (int)(id / m3);
+  const long o = id - (long)f * m3;
+  const int i = (int)(o / ((long)m * m)), j = (int)((o / m) % m), k = (int)(o % m);
+  const double* qf = q + (long)f * n3;
+  double v[8];
+#pragma unroll
+  for (int sg = 0; sg < 8; ++sg) {
+    const int ii = (sg & 1) ? n - 1 - i : i, jj = (sg & 2) ? n - 1 - j : j, kk = (sg & 4) ? n - 1 - k : k;
+    v[sg] = qf[ii * n2 + (long)jj * n + kk];
+  }
+#pragma unroll
+  for (int st = 1; st < 8; st <<= 1)   // 8-point Walsh-Hadamard transform
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+      if (!(a & st)) {
+        const double x = v[a], y = v[a | st];
+        v[a] = x + y;
+        v[a | st] = x - y;
+      }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) Q[((long)f * 8 + p) * m3 + o] = 0.125 * v[p];
+}
+
+// unfold: u_f(x) = Σ_p (-1)^{popcount(p & bits(x))} U[(f*8 + p)][octant point of x]
+__global__ void osp_unfold_kernel(const double* __restrict__ U, double* __restrict__ u, int nf, int n, int m) {
+  const long m3 = (long)m * m * m, n2 = (long)n * n, n3 = n2 * n;
+  const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= nf * n3) return;
+  const int f = (int)(id / n3);
+  const long x = id - (long)f * n3;
+  int i = (int)(x / n2), j = (int)((x / n) % n), k = (int)(x % n), bits = 0;
+  if (i >= m) { i = n - 1 - i; bits |= 1; }
+  if (j >= m) { j = n - 1 - j; bits |= 2; }
+  if (k >= m) { k = n - 1 - k; bits |= 4; }
+  const double* Uf = U + (long)f * 8 * m3 + ((long)i * m + j) * m + k;
+  double acc = 0.0;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const double v = Uf[p * m3];
+    acc += (__popc(p & bits) & 1) ? -v : v;
+  }
+  u[id] = acc;
+}
+
+__global__ void osp_par_kernel(uint8_t* par, int ncols) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < ncols) par[c] = (uint8_t)(c & 7);
 }
 
 }  // namespace
@@ -514,7 +598,7 @@ cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B
     const char* env = getenv("DPM_BEP_SYM");
     return env && atoi(env) == 2 ? cudaErrorNotSupported : cudaSuccess;
   }
-  const int m = ctx->sym_m, MP = sym_mp(m);
+  const int m = ctx->sym_m;
   const long m3 = (long)m * m * m;
   const int64_t ng = ctx->counts[DPM_SET_GAMMA], ngin = ctx->counts[DPM_SET_GAMMA_IN];
   const int cap = (int)std::max<long>(1, std::min<long>(ctx->K, (1L << 31) / (m3 * 8)));
@@ -540,11 +624,10 @@ cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B
                                    ctx->sym_zbox, m3, nc, s)) != cudaSuccess)
       return e;
     // (2)-(4)
-    switch (MP) {
-      case 8: e = sym_solve<8>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
-      case 16: e = sym_solve<16>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
-      case 32: e = sym_solve<32>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
-      default: e = sym_solve<64>(ctx, ctx->sym_zbox, ctx->sym_work, nc, par, s); break;
+    {
+      const SymOp op{ctx->n, m, ctx->h, ctx->dt, ctx->sym_S, ctx->sym_lam, ctx->sym_R, ctx->sym_lu_dt != ctx->dt};
+      ctx->sym_lu_dt = ctx->dt;
+      e = sym_solve_mp(op, ctx->sym_zbox, ctx->sym_work, nc, par, s);
     }
     if (e != cudaSuccess) return e;
     // (5)
@@ -558,7 +641,103 @@ cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B
   return cudaSuccess;
 }
 
+// ---- parity-split AP solve: host side -------------------------------------------------------------------------
+// 0 when s is not capturing, else the id of its capture sequence (never 0)
+static unsigned long long osp_capture_id(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(s, &cs, &id) != cudaSuccess) return ~0ull;
+  return cs == cudaStreamCaptureStatusNone ? 0ull : (id ? id : ~0ull);
+}
+
+cudaError_t octsplit_prepare(dpm_ctx* ctx, int64_t batch) {
+  if (ctx->osp == 0) {
+    const char* env = getenv("DPM_OCTSPLIT");
+    const int n = ctx->n;
+    ctx->osp = (env && atoi(env) == 0) || n <= 64 || n >= 128 ? -1 : 1;   // n <= 64, n = 128: their own plane passes
+  }
+  if (ctx->osp != 1 || batch <= 0) return cudaSuccess;
+  const int n = ctx->n, m = (n + 1) / 2;
+  const size_t m3 = (size_t)m * m * m, m2 = (size_t)m * m;
+  cudaError_t e;
+  if (!ctx->osp_S) {
+    std::vector<double> S, lam;
+    sym_tables(n, ctx->h, S, lam);
+    if ((e = upload(&ctx->osp_S, S)) != cudaSuccess) return e;
+    if ((e = upload(&ctx->osp_lam, lam)) != cudaSuccess) return e;
+    for (int k = 0; k < 2; ++k)
+      if ((e = cudaMalloc(&ctx->osp_R[k], (8 * m2 * m + 8 * m2) * sizeof(double))) != cudaSuccess) return e;
+    ctx->osp_lu_dt = 0.0;
+  }
+  const int want = (int)std::min<int64_t>(batch, 32);
+  if (ctx->osp_cap < want) {
+    if (ctx->osp_Q) cudaFree(ctx->osp_Q);
+    if (ctx->osp_U) cudaFree(ctx->osp_U);
+    if (ctx->osp_par) cudaFree(ctx->osp_par);
+    ctx->osp_Q = ctx->osp_U = nullptr;
+    ctx->osp_par = nullptr;
+    ctx->osp_cap = 0;
+    if ((e = cudaMalloc(&ctx->osp_Q, (size_t)want * 8 * m3 * 8)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&ctx->osp_U, (size_t)want * 8 * m3 * 8)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&ctx->osp_par, (size_t)want * 8)) != cudaSuccess) return e;
+    DPM_COUNT_LAUNCH(1);
+    osp_par_kernel<<<(want * 8 + 255) / 256, 256>>>(ctx->osp_par, want * 8);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+    ctx->osp_cap = want;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t octsplit_solve(dpm_ctx* ctx, const double* q, double* u, int64_t batch, cudaStream_t s, bool* done) {
+  *done = false;
+  if (ctx->osp == -1 || ctx->plan.solver != DPM_SOLVER_DST2_TRIDIAG || ctx->plan.prof || batch <= 0) return cudaSuccess;
+  const unsigned long long cap_id = osp_capture_id(s);
+  const bool cap = cap_id != 0;
+  if (!cap) {
+    cudaError_t e = octsplit_prepare(ctx, batch);
+    if (e != cudaSuccess) return e;
+  }
+  if (ctx->osp != 1 || ctx->osp_cap == 0) return cudaSuccess;   // off, or a capture before any prepare: dst path
+  const int n = ctx->n, m = (n + 1) / 2;
+  const size_t m3 = (size_t)m * m * m, n3 = (size_t)n * n * n;
+  const double dt = ctx->plan.dt;
+  for (int64_t b0 = 0; b0 < batch; b0 += ctx->osp_cap) {
+    const int nf = (int)std::min<int64_t>(ctx->osp_cap, batch - b0);
+    bool build;
+    int slot;
+    if (cap) {   // inside a graph: slot 1, rebuilt by the first solve of every captured graph (one Δt per graph)
+      slot = 1;
+      build = ctx->osp_cap_id != cap_id || cap_id == ~0ull || ctx->osp_cap_dt != dt;
+      ctx->osp_cap_id = cap_id;
+      ctx->osp_cap_dt = dt;
+    } else {
+      slot = 0;
+      build = ctx->osp_lu_dt != dt;
+      ctx->osp_lu_dt = dt;
+    }
+    DPM_COUNT_LAUNCH(2);
+    osp_fold_kernel<<<(unsigned)((nf * m3 + 255) / 256), 256, 0, s>>>(q + b0 * n3, ctx->osp_Q, nf, n, m);
+    const SymOp op{n, m, ctx->h, dt, ctx->osp_S, ctx->osp_lam, ctx->osp_R[slot], build};
+    cudaError_t e = sym_solve_mp(op, ctx->osp_Q, ctx->osp_U, nf * 8, ctx->osp_par, s);
+    if (e != cudaSuccess) return e;
+    osp_unfold_kernel<<<(unsigned)((nf * n3 + 255) / 256), 256, 0, s>>>(ctx->osp_U, u + b0 * n3, nf, n, m);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  *done = true;
+  return cudaSuccess;
+}
+
+cudaError_t ctx_solve(dpm_ctx* ctx, const double* q, double* u, int64_t batch, cudaStream_t s) {
+  bool done = false;
+  cudaError_t e = octsplit_solve(ctx, q, u, batch, s, &done);
+  if (e != cudaSuccess || done) return e;
+  return dst_solve_batch(ctx->plan, q, u, batch, nullptr, 0, s);
+}
+
 void bep_sym_free(dpm_ctx* c) {
+  for (void* p : {(void*)c->osp_S, (void*)c->osp_lam, (void*)c->osp_R[0], (void*)c->osp_R[1], (void*)c->osp_Q,
+                  (void*)c->osp_U, (void*)c->osp_par})
+    if (p) cudaFree(p);
   void* ptrs[] = {c->sym_list, c->sym_dst, c->sym_gidx, c->sym_par, c->sym_S, c->sym_lam, c->sym_zbox, c->sym_work, c->sym_R, c->sym_perm, c->sym_mirin, c->sym_Bp, c->sym_tmp, c->sym_dg, c->sym_flag};
   for (cudaStream_t st : c->sym_streams)
     if (st) cudaStreamDestroy(st);

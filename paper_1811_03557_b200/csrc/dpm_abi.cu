@@ -227,7 +227,7 @@ dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t
   if (!ctx || batch < 0 || (batch > 0 && (!q || !u))) return DPM_ERR_INVALID;
   if (batch == 0) return DPM_OK;
   cudaSetDevice(ctx->device);
-  DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, q, u, batch, nullptr, 0, as_stream(stream)));
+  DPM_CUDA_TRY(ctx, ctx_solve(ctx, q, u, batch, as_stream(stream)));
   return DPM_OK;
 }
 
@@ -264,7 +264,7 @@ dpm_status dpm_aux_solve_batch_host(dpm_ctx* ctx, const double* host_q, double* 
     DPM_CUDA_TRY(ctx, cudaMemcpyAsync(buf, host_q + b0 * field, nb * field * 8, cudaMemcpyHostToDevice, ctx->h2d_stream));
     DPM_CUDA_TRY(ctx, cudaEventRecord(up[bi], ctx->h2d_stream));
     DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, up[bi], 0));
-    DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, buf, buf, nb, nullptr, 0, s));
+    DPM_CUDA_TRY(ctx, ctx_solve(ctx, buf, buf, nb, s));
     DPM_CUDA_TRY(ctx, cudaEventRecord(solved[bi], s));
     DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->d2h_stream, solved[bi], 0));
     DPM_CUDA_TRY(ctx, cudaMemcpyAsync(host_u + b0 * field, buf, nb * field * 8, cudaMemcpyDeviceToHost, ctx->d2h_stream));
@@ -324,10 +324,10 @@ dpm_status dpm_bep_columns(dpm_ctx* ctx, int32_t c0, int32_t c1, double* PgE, do
       double* zb = nullptr;
       DPM_CUDA_TRY(ctx, bep_zbox(ctx, nc, &zb, s));
       DPM_CUDA_TRY(ctx, launch_potential_scatter(ctx, ctx->E + (size_t)a * ng, ng, zb, nc, s));
-      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, zb, ctx->work, nc, nullptr, 0, s));
+      DPM_CUDA_TRY(ctx, ctx_solve(ctx, zb, ctx->work, nc, s));
     } else {
       DPM_CUDA_TRY(ctx, launch_potential_rhs(ctx, ctx->E + (size_t)a * ng, ng, ctx->work, nc, s));
-      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, ctx->work, ctx->work, nc, nullptr, 0, s));
+      DPM_CUDA_TRY(ctx, ctx_solve(ctx, ctx->work, ctx->work, nc, s));
     }
     DPM_CUDA_TRY(ctx, launch_bep_gather(ctx, ctx->work, a, nc, PgE ? PgE + (size_t)(a - c0) * ng : nullptr,
                                         B ? B + (size_t)(a - c0) * ngin : nullptr, s));
@@ -452,11 +452,11 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
       double* fr = fq + r * field;
       double* wr = wk + r * field;
       if (r == 1) DPM_CUDA_TRY(ctx, launch_fc_seq(ctx, c, wk, dt, fr, s));
-      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fr, wr, 1, nullptr, 0, s));
+      DPM_CUDA_TRY(ctx, ctx_solve(ctx, fr, wr, 1, s));
       DPM_CUDA_TRY(ctx, launch_trace(ctx, wr, gvec + r * ngin, DPM_SET_GAMMA_IN, 1, s));
       DPM_CUDA_TRY(ctx, lsq_apply(ctx, gvec + r * ngin, coef + (size_t)r * K, ug + r * ng, 1, prm->clamp, s));
       DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fr, ug + r * ng, wr, 1, s));
-      DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wr, wr, 1, nullptr, 0, s));
+      DPM_CUDA_TRY(ctx, ctx_solve(ctx, wr, wr, 1, s));
     }
     DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true, abort));
     return DPM_OK;
@@ -472,7 +472,7 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
 #else
   constexpr int skip = 0;
 #endif
-  if (!(skip & 1)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+  if (!(skip & 1)) DPM_CUDA_TRY(ctx, ctx_solve(ctx, fq, wk, 2, s));
   // Step 5: BEP right-hand side on gamma_in, least squares, extension, clamp (its magnitude -> slot[10])
   if (!(skip & 4)) {
   DPM_CUDA_TRY(ctx, launch_trace(ctx, wk, gvec, DPM_SET_GAMMA_IN, 2, s));
@@ -504,10 +504,10 @@ static dpm_status enqueue_pks_step(dpm_ctx* ctx, double* rho, double* c, const d
   }();
   if (inplace) {
     if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_band_inplace(ctx, fq, ug, 2, s));
-    if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, fq, wk, 2, nullptr, 0, s));
+    if (!(skip & 2)) DPM_CUDA_TRY(ctx, ctx_solve(ctx, fq, wk, 2, s));
   } else {
     if (!(skip & 8)) DPM_CUDA_TRY(ctx, launch_green_rhs(ctx, fq, ug, wk, 2, s));
-    if (!(skip & 2)) DPM_CUDA_TRY(ctx, dst_solve_batch(ctx->plan, wk, wk, 2, nullptr, 0, s));
+    if (!(skip & 2)) DPM_CUDA_TRY(ctx, ctx_solve(ctx, wk, wk, 2, s));
   }
   if (!(skip & 16)) DPM_CUDA_TRY(ctx, launch_restrict_stats(ctx, wk, rho, c, slot + 4, s, true, abort));
   if (fork) DPM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
@@ -529,6 +529,7 @@ static dpm_status pks_graph(dpm_ctx* ctx, double* rho, double* c, const dpm_pks_
   PassProf* prof = ctx->plan.prof;
   ctx->plan.prof = nullptr;   // no timing events inside graphs
   const long long l0 = (long long)g_dpm_launches.load();
+  DPM_CUDA_TRY(ctx, octsplit_prepare(ctx, 2));   // the parity-split solver's tables and boxes (no allocation in a capture)
   DPM_CUDA_TRY(ctx, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   dpm_status st = DPM_OK;
   static const int pdl_nmax = [] {   // programmatic dependent launch within the step graph (dpm_internal.h)
