@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(SYM_NT, 2) sym_yz_kernel(const double* in, dou
   using G = SymGeo<MP>;
   extern __shared__ __align__(16) double sh[];
   double* Y = sh + 2 * MP * G::LD;
-  for (int e = threadIdx.x; e < 3 * MP * G::LD; e += SYM_NT) sh[e] = 0.0;   // padding stays zero
-  __syncthreads();
+  if (m < MP) {   // rows / columns >= m stay zero (m = MP: every entry read is loaded or written first)
+    for (int e = threadIdx.x; e < 3 * MP * G::LD; e += SYM_NT) sh[e] = 0.0;
+    __syncthreads();
+  }
   const long m2 = (long)m * m, nplanes = (long)ncols * m;
   const long per = (nplanes + gridDim.x - 1) / gridDim.x;
   const long p0 = blockIdx.x * per, p1 = min(nplanes, p0 + per);
@@ -556,25 +558,35 @@ __global__ void osp_fold_kernel(const double* __restrict__ q, double* __restrict
   for (int p = 0; p < 8; ++p) Q[((long)f * 8 + p) * m3 + o] = 0.125 * v[p];
 }
 
-// unfold: u_f(x) = Σ_p (-1)^{popcount(p & bits(x))} U[(f*8 + p)][octant point of x]
+// unfold: u_f(σ(i, j, k)) = Σ_p (-1)^{popcount(p & σ)} U[(f*8 + p)][i][j][k] for the 8 reflections σ of every octant
+// point (the same Walsh-Hadamard transform; one thread per octant point reads its 8 components once and writes
+// the 8 images; at the centre node of an odd n the images coincide and, the odd components being exactly 0
+// there, so do the values written)
 __global__ void osp_unfold_kernel(const double* __restrict__ U, double* __restrict__ u, int nf, int n, int m) {
   const long m3 = (long)m * m * m, n2 = (long)n * n, n3 = n2 * n;
   const long id = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= nf * n3) return;
-  const int f = (int)(id / n3);
-  const long x = id - (long)f * n3;
-  int i = (int)(x / n2), j = (int)((x / n) % n), k = (int)(x % n), bits = 0;
-  if (i >= m) { i = n - 1 - i; bits |= 1; }
-  if (j >= m) { j = n - 1 - j; bits |= 2; }
-  if (k >= m) { k = n - 1 - k; bits |= 4; }
-  const double* Uf = U + (long)f * 8 * m3 + ((long)i * m + j) * m + k;
-  double acc = 0.0;
+  if (id >= nf * m3) return;
+  const int f = (int)(id / m3);
+  const long o = id - (long)f * m3;
+  const int i = (int)(o / ((long)m * m)), j = (int)((o / m) % m), k = (int)(o % m);
+  double v[8];
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    const double v = Uf[p * m3];
-    acc += (__popc(p & bits) & 1) ? -v : v;
+  for (int p = 0; p < 8; ++p) v[p] = U[((long)f * 8 + p) * m3 + o];
+#pragma unroll
+  for (int st = 1; st < 8; st <<= 1)
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+      if (!(a & st)) {
+        const double x = v[a], y = v[a | st];
+        v[a] = x + y;
+        v[a | st] = x - y;
+      }
+  double* uf = u + (long)f * n3;
+#pragma unroll
+  for (int sg = 0; sg < 8; ++sg) {
+    const int ii = (sg & 1) ? n - 1 - i : i, jj = (sg & 2) ? n - 1 - j : j, kk = (sg & 4) ? n - 1 - k : k;
+    uf[ii * n2 + (long)jj * n + kk] = v[sg];
   }
-  u[id] = acc;
 }
 
 __global__ void osp_par_kernel(uint8_t* par, int ncols) {
@@ -654,7 +666,9 @@ cudaError_t octsplit_prepare(dpm_ctx* ctx, int64_t batch) {
   if (ctx->osp == 0) {
     const char* env = getenv("DPM_OCTSPLIT");
     const int n = ctx->n;
-    ctx->osp = (env && atoi(env) == 0) || n <= 64 || n >= 128 ? -1 : 1;   // n <= 64, n = 128: their own plane passes
+    const char* nm = getenv("DPM_OCTSPLIT_NMIN");   // n <= 64 and n = 128 have their own fused plane passes
+    const int nmin = nm ? atoi(nm) : 65;
+    ctx->osp = (env && atoi(env) == 0) || n < nmin || n < 4 || n >= 128 ? -1 : 1;
   }
   if (ctx->osp != 1 || batch <= 0) return cudaSuccess;
   const int n = ctx->n, m = (n + 1) / 2;
@@ -720,7 +734,7 @@ cudaError_t octsplit_solve(dpm_ctx* ctx, const double* q, double* u, int64_t bat
     const SymOp op{n, m, ctx->h, dt, ctx->osp_S, ctx->osp_lam, ctx->osp_R[slot], build};
     cudaError_t e = sym_solve_mp(op, ctx->osp_Q, ctx->osp_U, nf * 8, ctx->osp_par, s);
     if (e != cudaSuccess) return e;
-    osp_unfold_kernel<<<(unsigned)((nf * n3 + 255) / 256), 256, 0, s>>>(ctx->osp_U, u + b0 * n3, nf, n, m);
+    osp_unfold_kernel<<<(unsigned)((nf * m3 + 255) / 256), 256, 0, s>>>(ctx->osp_U, u + b0 * n3, nf, n, m);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   *done = true;
