@@ -124,7 +124,10 @@ dpm_status dpm_set_dt(dpm_ctx* ctx, double dt);
  *   u_b = (I/dt - Δ_h)^{-1} q_b  on the n^3 interior, zero Dirichlet ghosts,
  * by 3D DST-I, eigenvalue divide (λ_m = (4/h^2) sin^2(m pi/(2(n+1))), R26), inverse
  * 3D DST-I.  q, u: DEVICE [batch][n][n][n]; u may equal q (in place).  batch >= 0.
- * Asynchronous on `stream`.
+ * Asynchronous on `stream`.  The same solution by any of the library's exact factorisations of that
+ * transform: DST-I along x and y with a tridiagonal solve along z (default), the literal 3D DST-I
+ * (dpm_set_solver), and for 64 < n < 128 the 8 reflection-parity components solved on the octant
+ * (DESIGN.md §6).  The first call at a new n may allocate work space on the device (it synchronises).
  * ------------------------------------------------------------------------------- */
 dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t batch, void* stream);
 
