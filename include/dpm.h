@@ -126,7 +126,7 @@ dpm_status dpm_set_dt(dpm_ctx* ctx, double dt);
  * 3D DST-I.  q, u: DEVICE [batch][n][n][n]; u may equal q (in place).  batch >= 0.
  * Asynchronous on `stream`.  The same solution by any of the library's exact factorisations of that
  * transform: DST-I along x and y with a tridiagonal solve along z (default), the literal 3D DST-I
- * (dpm_set_solver), and for 64 < n < 128 the 8 reflection-parity components solved on the octant
+ * (dpm_set_solver), and at n = 127 the 8 reflection-parity components solved on the octant
  * (DESIGN.md §6).  The first call at a new n may allocate work space on the device (it synchronises).
  * ------------------------------------------------------------------------------- */
 dpm_status dpm_aux_solve_batch(dpm_ctx* ctx, const double* q, double* u, int64_t batch, void* stream);

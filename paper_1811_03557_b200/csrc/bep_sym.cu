@@ -666,9 +666,11 @@ cudaError_t octsplit_prepare(dpm_ctx* ctx, int64_t batch) {
   if (ctx->osp == 0) {
     const char* env = getenv("DPM_OCTSPLIT");
     const int n = ctx->n;
-    const char* nm = getenv("DPM_OCTSPLIT_NMIN");   // n <= 64 and n = 128 have their own fused plane passes
-    const int nmin = nm ? atoi(nm) : 65;
-    ctx->osp = (env && atoi(env) == 0) || n < nmin || n < 4 || n >= 128 ? -1 : 1;
+    // default: only where it measures faster than the generic passes, i.e. the exact 64^3 octant of n = 127 (the
+    // paper's Test B mesh); other n pad the GEMMs or take 8-byte copies and lose (tools/octsplit_sweep.py), n <= 64
+    // and n = 128 have their own fused plane passes.  DPM_OCTSPLIT=2: every 4 <= n < 128 (tests, A/B); 0: off.
+    const int mode = env ? atoi(env) : 1;
+    ctx->osp = mode == 2 ? (n >= 4 && n < 128 ? 1 : -1) : mode == 1 && n == 127 ? 1 : -1;
   }
   if (ctx->osp != 1 || batch <= 0) return cudaSuccess;
   const int n = ctx->n, m = (n + 1) / 2;

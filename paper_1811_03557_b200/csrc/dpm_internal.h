@@ -178,7 +178,7 @@ struct dpm_ctx {
   double* sym_tmp = nullptr;         // [K][n_gamma_in] CholeskyQR2 ping-pong
   double* sym_dg = nullptr;          // [K] |diag R| (class order)
   int* sym_flag = nullptr;
-  // parity-split AP solve for 64 < n < 128 (bep_sym.cu, octsplit_solve): operator tables of its own (the BEP
+  // parity-split AP solve (bep_sym.cu, octsplit_solve; n = 127 by default): operator tables of its own (the BEP
   // octant path needs symmetric sets, the solver does not), LU factors in two slots (0: eager calls, cached
   // by Δt; 1: inside graph captures, rebuilt at the start of every captured graph), fold / solve boxes
   int osp = 0;                       // 0: undecided, 1: on, -1: off
@@ -365,8 +365,8 @@ cudaError_t launch_potential_list(const dpm_ctx* ctx, const double* v, int64_t l
                                   const int32_t* dst, int64_t nlist, double* q, int64_t qstride, int nrhs,
                                   cudaStream_t s);
 cudaError_t bep_sym_columns(dpm_ctx* ctx, int c0, int c1, double* PgE, double* B, cudaStream_t s, bool* done);
-// AP solve of `batch` dense boxes by the 8 reflection-parity components on the octant (64 < n < 128, default
-// solver); *done = false and nothing runs when it does not apply.  ctx_solve: that, else dst_solve_batch.
+// AP solve of `batch` dense boxes by the 8 reflection-parity components on the octant (n = 127 by default,
+// every 4 <= n < 128 with DPM_OCTSPLIT=2; default solver only); *done = false and nothing runs when it does not apply.  ctx_solve: that, else dst_solve_batch.
 cudaError_t octsplit_prepare(dpm_ctx* ctx, int64_t batch);   // tables and boxes (allocates: not inside a capture)
 cudaError_t octsplit_solve(dpm_ctx* ctx, const double* q, double* u, int64_t batch, cudaStream_t s, bool* done);
 cudaError_t ctx_solve(dpm_ctx* ctx, const double* q, double* u, int64_t batch, cudaStream_t s);

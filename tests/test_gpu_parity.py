@@ -68,6 +68,58 @@ def test_aux_solve_parity_large_dt(api, n, dt, solver):
     assert rel(u, ap.solve(q, c.info["h"], dt)) <= 1e-11
 
 
+@pytest.mark.parametrize("n,dt,batch", [(127, 1e-3, 3), (127, 1e-12, 1), (127, 10.0, 35), (126, 1e-4, 2), (100, 1e-5, 2),
+                                        (65, 1e-3, 2), (31, 1e-3, 3), (16, 1e-2, 2), (7, 1e-3, 2)])
+def test_aux_solve_parity_split(api, monkeypatch, n, dt, batch):
+    # the parity-split solver (octsplit_solve: the 8 reflection-parity components on the octant) on every
+    # n it is written for (DPM_OCTSPLIT=2; by default only n = 127 takes it): odd and even n, exact and padded
+    # octants, odd m, tiny and large dt, more fields than one chunk (32), in place
+    monkeypatch.setenv("DPM_OCTSPLIT", "2")
+    c = api.DPM(n, -1.1, 1.1, "sphere", (0, 0, 0), (1, 1, 1), 2, dt, "cauchy")
+    q = random_boxes(900 + n, batch, n)
+    t = torch.from_numpy(q).cuda()
+    c.aux_solve_batch(t, t)
+    sel = [0, batch // 2, batch - 1] if batch > 3 else list(range(batch))   # the oracle on a sample of the chunked batch
+    assert rel(t.cpu().numpy()[sel], ap.solve(q[sel], c.info["h"], dt)) <= 1e-11
+
+
+def test_aux_solve_parity_split_in_step_graphs(api):
+    # n = 127 (default on): PKS steps replayed from graphs captured at two dt values, interleaved with an
+    # eager solve at a third dt: every path must see the x-pass LU factors of its own dt (capture slot
+    # rebuilt per graph, eager slot cached by dt); against the same sequence on the generic passes
+    import os, subprocess, sys, textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent('''
+        import sys, numpy as np, torch
+        from dpm_inputs.configs import test_b_config
+        from dpm_inputs.rng import random_boxes
+        from paper_1811_03557_b200 import api
+        cfg = test_b_config(127, 12)
+        c = api.DPM.from_config(cfg)
+        n = cfg.n
+        rho = torch.zeros((n,) * 3, dtype=torch.float64, device="cuda"); cc = torch.zeros_like(rho)
+        c.pks_init(rho, cc, cfg.ic_center, *cfg.ic_rho, *cfg.ic_c)
+        q = torch.from_numpy(random_boxes(5, 1, n)).cuda()
+        outs = []
+        for cap in (cfg.dt, 0.5 * cfg.dt, cfg.dt, 0.5 * cfg.dt):
+            c.pks_step(rho, cc, 3, chi=cfg.chi, dt_cap=cap, dt_rule=1)
+            c.set_dt(0.3 * cfg.dt)
+            outs.append(c.aux_solve_batch(q).cpu().numpy())
+        np.save(sys.argv[1], np.stack([rho.cpu().numpy(), cc.cpu().numpy()])); np.save(sys.argv[2], np.stack(outs))
+    ''')
+    res = {}
+    for f in ("1", "0"):
+        import tempfile
+        d = tempfile.mkdtemp()
+        a, b = os.path.join(d, "s.npy"), os.path.join(d, "u.npy")
+        r = subprocess.run([sys.executable, "-c", code, a, b], cwd=root, env=dict(os.environ, DPM_OCTSPLIT=f),
+                           capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[f] = (np.load(a), np.load(b))
+    assert rel(res["1"][0][0], res["0"][0][0]) <= 1e-9 and rel(res["1"][0][1], res["0"][0][1]) <= 1e-9
+    assert rel(res["1"][1], res["0"][1]) <= 1e-11
+
+
 @pytest.mark.parametrize("n,batch", [(33, 20), (48, 14), (64, 10), (17, 40)])
 def test_aux_solve_small_n_large_batch(api, n, batch):
     # more than 4 x 148 x-mode planes: the persistent batched small-n plane pass (sine matrix loaded once per
