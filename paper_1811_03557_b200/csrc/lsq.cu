@@ -264,6 +264,8 @@ void launch_gemv(const double* M, int64_t m, int K, const double* g, int nrhs, d
   DPM_COUNT_LAUNCH(1);
   if (K >= 4 * 148)
     launch_pdl(lsq_gemv_kernel<4, 512>, (K + 3) / 4, 512, 0, s, M, m, K, g, nrhs, coef);
+  else if (K <= 2 * 148 && m >= 32768)   // few long rows (Test B: K = 150, |γ_in| ~ 6e4): 4x the loads in flight per row
+    launch_pdl(lsq_gemv_kernel<1, 1024>, K, 1024, 0, s, M, m, K, g, nrhs, coef);
   else
     launch_pdl(lsq_gemv_kernel<1, 256>, K, 256, 0, s, M, m, K, g, nrhs, coef);
 }
